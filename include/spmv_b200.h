@@ -1,0 +1,217 @@
+/*
+ * spmv_b200.h — C ABI of the B200-native SpMV engine (libspmv_b200.so).
+ *
+ * Every entry point replaces one function of the reference package
+ * `spmvkit` (pure Python/numpy, /root/reference/pkg/src/spmvkit); the
+ * replaced interface is cited as file:line next to each declaration.
+ *
+ * Conventions
+ *   - Plain C types only: device pointers, 64-bit sizes, an opaque
+ *     `void* stream` (a cudaStream_t; NULL = legacy default stream).
+ *   - Indices are the reference's uint32 (formats.py:24), DIA offsets its
+ *     int32 (formats.py:25).  Values are f32 or f64 (formats.py:27).
+ *   - DIA values are the reference's row-major (padded_rows, ndiags) block
+ *     (formats.py:166-207), padded_rows a multiple of ROW_PAD = 8.
+ *   - Every call returns an spmv_status; spmv_last_error() gives the
+ *     thread-local message of the last failing call.  The codes map 1:1 to
+ *     the reference's exception classes (errors.py:4-37).
+ *   - SpMV calls never allocate and never write caller memory other than y
+ *     (kernels.py:59,72,94: the kernel owns a fresh y).  Workspace lives in
+ *     the plan objects.  All calls are reentrant (bench.py:167-172 calls
+ *     kernels from several threads).
+ *   - Calls that return a host-visible count (plan creation, conversion
+ *     analyze steps) synchronise `stream`; SpMV calls are asynchronous.
+ */
+#ifndef SPMV_B200_H
+#define SPMV_B200_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define SPMV_B200_ABI_VERSION 1
+
+typedef enum {
+    SPMV_F32 = 0,
+    SPMV_F64 = 1
+} spmv_dtype;
+
+typedef enum {
+    SPMV_OK = 0,
+    SPMV_DIMENSION_MISMATCH = 1,   /* errors.py:8  DimensionMismatch      */
+    SPMV_UNSORTED_INPUT = 2,       /* errors.py:12 UnsortedInput          */
+    SPMV_FILL_RATIO_EXCEEDED = 3,  /* errors.py:16 FillRatioExceeded      */
+    SPMV_UNSUPPORTED = 4,          /* errors.py:20 UnsupportedCombination */
+    SPMV_CUDA_ERROR = 5,
+    SPMV_INVALID_ARG = 6,
+    SPMV_INDEX_OVERFLOW = 7        /* errors.py:36 IndexOverflow          */
+} spmv_status;
+
+/* ---- library ----------------------------------------------------------- */
+int spmv_abi_version(void);
+const char* spmv_last_error(void);
+/* Number of SMs of the current device (grid sizing; 148 on B200). */
+int spmv_device_sm_count(int* out);
+
+/* ---- CSR (kernels.py:69-82 spmv_csr_plain, :143-171 spmv_csr_vla) ------ */
+typedef struct spmv_csr_plan spmv_csr_plan;
+
+/* Analyse the row-length histogram once (CSR-Adaptive style binning):
+ * rows of length <= exact_len go to the CSR-stream kernel (one thread sums
+ * the row left to right => bit-exact with spmv_csr_plain); longer rows are
+ * split into warp chunks (bit-exact with spmv_csr_vla(lanes=32) for rows of
+ * at most one chunk, deterministic and within 1e-12 otherwise).
+ * exact_len <= 0 selects the default (32). */
+int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
+                         const uint32_t* row_pointers, int exact_len,
+                         void* stream, spmv_csr_plan** out);
+int spmv_csr_plan_destroy(spmv_csr_plan* plan);
+/* n_long_rows: rows handled by the chunk kernel; n_items: warp work items;
+ * launches: kernels one spmv_csr call launches. */
+int spmv_csr_plan_info(const spmv_csr_plan* plan, int64_t* n_long_rows,
+                       int64_t* n_items, int64_t* launches);
+
+/* y[r] = sum_j av[j] * x[aj[j] - col_base] over row r.  x holds the window
+ * of global columns [col_base, col_base + x_len).  For a single-device
+ * product col_base = 0 and x_len = ncols. */
+int spmv_csr(const spmv_csr_plan* plan, const uint32_t* row_pointers,
+             const uint32_t* col_indices, const void* values, const void* x,
+             int64_t col_base, int64_t x_len, void* y, void* stream);
+
+/* Sub-warp vector kernel, lane l accumulates entries s+l, s+l+L, ... then a
+ * pairwise-halving tree over next_pow2(L) lanes: bit-exact with
+ * spmv_csr_vla(LaneConfig(L)) (lanes.py:101-128).  1 <= lanes <= 1024. */
+int spmv_csr_vla(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
+                 const uint32_t* row_pointers, const uint32_t* col_indices,
+                 const void* values, const void* x, int64_t col_base,
+                 int64_t x_len, void* y, int lanes, void* stream);
+
+/* ---- COO (kernels.py:56-66 spmv_coo_plain, :104-140 spmv_coo_vla) ------ */
+typedef struct spmv_coo_plan spmv_coo_plan;
+
+/* Checks the row order once.  If rows are not non-decreasing, the plan
+ * keeps a stable row-sorted copy of the triples (np.add.at accumulates in
+ * storage order per row, kernels.py:65, and a stable sort keeps that
+ * order).  Also run-length-encodes the rows for the long-row chunks. */
+int spmv_coo_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
+                         const uint32_t* row_indices,
+                         const uint32_t* col_indices, const void* values,
+                         void* stream, spmv_coo_plan** out);
+int spmv_coo_plan_destroy(spmv_coo_plan* plan);
+/* row_sorted: 1 when the input rows were already non-decreasing. */
+int spmv_coo_plan_info(const spmv_coo_plan* plan, int64_t* n_runs,
+                       int64_t* n_long_runs, int64_t* n_items,
+                       int* row_sorted, int64_t* launches);
+
+/* Fixed 2048-entry tiles, segmented reduction without atomics: rows of at
+ * most 32 entries are summed left to right by one thread starting from
+ * +0.0 (bit-exact with np.add.at), longer runs go to the warp chunks. */
+int spmv_coo(const spmv_coo_plan* plan, const uint32_t* row_indices,
+             const uint32_t* col_indices, const void* values, const void* x,
+             int64_t col_base, int64_t x_len, void* y, void* stream);
+
+/* Requires the reference's `sorted` flag (kernels.py:119-120; checked by
+ * the caller).  Per row: chunks of L entries, each tree-reduced, added once
+ * into y: bit-exact with spmv_coo_vla.  outer_steps (may be NULL) receives
+ * the reference's step count (kernels.py:138-140); non-NULL synchronises. */
+int spmv_coo_vla(const spmv_coo_plan* plan, const uint32_t* row_indices,
+                 const uint32_t* col_indices, const void* values,
+                 const void* x, int64_t col_base, int64_t x_len, void* y,
+                 int lanes, int64_t* outer_steps, void* stream);
+
+/* ---- DIA (kernels.py:85-101 spmv_dia_plain, :174-210 spmv_dia_vla) ----- */
+/* Rows [0, nrows) of the block `values` (row stride ndiags) are the global
+ * rows [row_base, row_base + nrows); avail_rows >= nrows rows of the block
+ * are readable (padding included).  Column bound checks use the global
+ * ncols; x is the window starting at global column col_base.  Each row sums
+ * its in-bounds diagonals in ascending offset order from +0.0, so the
+ * result is bit-exact with spmv_dia_plain and spmv_dia_vla (any lanes). */
+int spmv_dia(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags,
+             int64_t avail_rows, const int32_t* offsets, const void* values,
+             const void* x, int64_t row_base, int64_t col_base, int64_t x_len,
+             void* y, void* stream);
+
+/* ---- conversions (convert.py) ------------------------------------------ */
+/* convert.py:87-94: IRP from a sorted COO (copies AJ/AV too). */
+int spmv_coo_to_csr(int dtype, int64_t nrows, int64_t nnz,
+                    const uint32_t* row_indices, const uint32_t* col_indices,
+                    const void* values, uint32_t* row_pointers_out,
+                    uint32_t* col_indices_out, void* values_out, void* stream);
+
+/* convert.py:97-110: row expansion; *sorted_out = 1 iff columns strictly
+ * increase inside every row.  Synchronises. */
+int spmv_csr_to_coo(int dtype, int64_t nrows, int64_t nnz,
+                    const uint32_t* row_pointers, const uint32_t* col_indices,
+                    const void* values, uint32_t* row_indices_out,
+                    uint32_t* col_indices_out, void* values_out,
+                    int* sorted_out, void* stream);
+
+/* convert.py:113-144: two phases so the host can apply the DiaFillPolicy
+ * before the block is allocated (convert.py:128-139). */
+typedef struct spmv_dia_builder spmv_dia_builder;
+int spmv_coo_to_dia_analyze(int64_t nrows, int64_t ncols, int64_t nnz,
+                            const uint32_t* row_indices,
+                            const uint32_t* col_indices, void* stream,
+                            spmv_dia_builder** out, int64_t* ndiags_out);
+int spmv_coo_to_dia_offsets(const spmv_dia_builder* b, int32_t* offsets_out,
+                            void* stream);
+/* values_out: (padded_rows, ndiags) row-major, fully written (zeros +
+ * scatter). */
+int spmv_coo_to_dia_fill(const spmv_dia_builder* b, int dtype,
+                         int64_t padded_rows, const uint32_t* row_indices,
+                         const uint32_t* col_indices, const void* values,
+                         void* values_out, void* stream);
+int spmv_dia_builder_destroy(spmv_dia_builder* b);
+
+/* convert.py:147-177: in-bounds cells != 0 (NaN kept, -0.0 dropped), in
+ * (row, col) order.  count synchronises; fill writes nnz_out triples. */
+typedef struct spmv_dia_collect spmv_dia_collect;
+int spmv_dia_to_coo_count(int dtype, int64_t nrows, int64_t ncols,
+                          int64_t ndiags, const int32_t* offsets,
+                          const void* values, void* stream,
+                          spmv_dia_collect** out, int64_t* nnz_out);
+int spmv_dia_to_coo_fill(const spmv_dia_collect* c, int dtype,
+                         const int32_t* offsets, const void* values,
+                         uint32_t* row_indices_out, uint32_t* col_indices_out,
+                         void* values_out, void* stream);
+int spmv_dia_collect_destroy(spmv_dia_collect* c);
+
+/* convert.py:60-84: stable (row, col) sort; duplicate coordinates summed in
+ * numpy's np.add.reduceat order (first element + pairwise sum of the rest,
+ * numpy 2.3 pairwise_sum), zero sums kept.  Two phases: sort + count, then
+ * emit. */
+typedef struct spmv_coo_sorter spmv_coo_sorter;
+int spmv_sort_coo_analyze(int dtype, int64_t nnz, const uint32_t* row_indices,
+                          const uint32_t* col_indices, void* stream,
+                          spmv_coo_sorter** out, int64_t* nnz_out);
+int spmv_sort_coo_emit(const spmv_coo_sorter* s, int dtype,
+                       const void* values, uint32_t* row_indices_out,
+                       uint32_t* col_indices_out, void* values_out,
+                       void* stream);
+int spmv_coo_sorter_destroy(spmv_coo_sorter* s);
+
+/* ---- generators (matrixio.py:170-210 gen_stencil27) -------------------- */
+/* nnz = prod(3*n_d - 2) (1 for n_d = 1).  IndexOverflow when 27*n > 2^32-1
+ * (matrixio.py:182-183). */
+int spmv_stencil27_nnz(int64_t nx, int64_t ny, int64_t nz, int64_t* nnz_out);
+/* Rows [row_begin, row_end) of the global stencil operator; row_pointers_out
+ * gets (row_end - row_begin + 1) entries rebased to start at 0. */
+int spmv_stencil27_fill(int dtype, int64_t nx, int64_t ny, int64_t nz,
+                        int64_t row_begin, int64_t row_end,
+                        uint32_t* row_pointers_out, uint32_t* col_indices_out,
+                        void* values_out, void* stream);
+
+/* ---- row-partition helpers (hpcg.py:95-189) ---------------------------- */
+/* Min and max column referenced by rows [0, nrows) of a CSR block
+ * (min = UINT32_MAX, max = 0 when empty).  Synchronises. */
+int spmv_csr_col_bounds(int64_t nrows, const uint32_t* row_pointers,
+                        const uint32_t* col_indices, void* stream,
+                        uint32_t* min_out, uint32_t* max_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* SPMV_B200_H */

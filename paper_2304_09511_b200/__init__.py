@@ -1,0 +1,56 @@
+"""B200-native SpMV engine (COO / CSR / DIA) — drop-in for spmvkit's hot path.
+
+Public surface mirrors the reference package (/root/reference/pkg/src/
+spmvkit/__init__.py:11-93) for the hot-path modules: containers, errors,
+conversions, kernels + registry + dispatch, lanes, the stencil generator and
+the row-partitioned multi-GPU path.  All products run in hand-written
+sm_100a kernels (libspmv_b200.so, built in-tree by `_build.build()`); there
+is no CPU fallback.
+"""
+
+from .convert import (
+    DiaFillPolicy,
+    coo_to_csr,
+    coo_to_dia,
+    csr_to_coo,
+    dense_to_coo,
+    dia_to_coo,
+    sort_coo,
+    switch_format,
+    to_format,
+)
+from .errors import (
+    DeviceError,
+    DimensionMismatch,
+    FillRatioExceeded,
+    IndexOverflow,
+    SparseError,
+    UnsortedInput,
+    UnsupportedCombination,
+)
+from .formats import (
+    CooMatrix,
+    CsrMatrix,
+    DiaMatrix,
+    DynamicMatrix,
+    Format,
+    MatrixShape,
+    as_device,
+    validate,
+)
+from .kernels import (
+    KernelRegistry,
+    KernelVersion,
+    default_registry,
+    dispatch,
+    spmv_coo_plain,
+    spmv_coo_vla,
+    spmv_csr_plain,
+    spmv_csr_vla,
+    spmv_dia_plain,
+    spmv_dia_vla,
+)
+from .lanes import LaneConfig
+from .matrixio import gen_stencil27, gen_stencil27_rows
+
+__version__ = "0.1.0"

@@ -1,0 +1,92 @@
+// Library-level C ABI: error reporting, device queries, partition helpers.
+#include <cub/cub.cuh>
+
+#include <mutex>
+
+#include "common.cuh"
+
+namespace spmv {
+
+static thread_local std::string g_last_error;
+
+void set_error(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  (void)code;
+  g_last_error = buf;
+}
+
+int fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof(buf), fmt, ap);
+  va_end(ap);
+  g_last_error = buf;
+  return code;
+}
+
+int sm_count() {
+  static std::mutex mu;
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return 148;
+  std::lock_guard<std::mutex> lock(mu);
+  if (!cache[dev]) {
+    int n = 0;
+    if (cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || n <= 0) n = 148;
+    cache[dev] = n;
+  }
+  return cache[dev];
+}
+
+}  // namespace spmv
+
+using namespace spmv;
+
+extern "C" {
+
+int spmv_abi_version(void) { return SPMV_B200_ABI_VERSION; }
+
+const char* spmv_last_error(void) { return g_last_error.c_str(); }
+
+int spmv_device_sm_count(int* out) {
+  if (!out) return fail(SPMV_INVALID_ARG, "out is NULL");
+  *out = sm_count();
+  return SPMV_OK;
+}
+
+int spmv_csr_col_bounds(int64_t nrows, const uint32_t* irp, const uint32_t* aj, void* stream, uint32_t* min_out,
+                        uint32_t* max_out) {
+  if (!min_out || !max_out) return fail(SPMV_INVALID_ARG, "NULL output");
+  *min_out = UINT32_MAX;
+  *max_out = 0;
+  if (nrows <= 0) return SPMV_OK;
+  cudaStream_t st = as_stream(stream);
+  uint32_t b[2] = {0, 0};
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&b[0], irp, 4, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&b[1], irp + nrows, 4, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t n = int64_t(b[1]) - int64_t(b[0]);
+  if (n <= 0) return SPMV_OK;
+  DevBuf out, tmp;
+  int rc = out.alloc(8);
+  if (rc) return rc;
+  size_t t1 = 0, t2 = 0;
+  SPMV_CUDA_TRY(cub::DeviceReduce::Min(nullptr, t1, aj + b[0], out.as<uint32_t>(), n, st));
+  SPMV_CUDA_TRY(cub::DeviceReduce::Max(nullptr, t2, aj + b[0], out.as<uint32_t>() + 1, n, st));
+  if ((rc = tmp.alloc(t1 > t2 ? t1 : t2))) return rc;
+  SPMV_CUDA_TRY(cub::DeviceReduce::Min(tmp.ptr, t1, aj + b[0], out.as<uint32_t>(), n, st));
+  SPMV_CUDA_TRY(cub::DeviceReduce::Max(tmp.ptr, t2, aj + b[0], out.as<uint32_t>() + 1, n, st));
+  uint32_t h[2];
+  SPMV_CUDA_TRY(cudaMemcpyAsync(h, out.ptr, 8, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  *min_out = h[0];
+  *max_out = h[1];
+  return SPMV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,123 @@
+// Shared helpers for the sm_100a SpMV kernels and their C ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+
+#include "../../include/spmv_b200.h"
+
+namespace spmv {
+
+// ---------------------------------------------------------------- errors --
+void set_error(int code, const char* fmt, ...);
+int fail(int code, const char* fmt, ...);
+
+#define SPMV_CUDA_TRY(expr)                                                   \
+  do {                                                                        \
+    cudaError_t _e = (expr);                                                  \
+    if (_e != cudaSuccess)                                                    \
+      return ::spmv::fail(SPMV_CUDA_ERROR, "%s failed: %s (%s:%d)", #expr,    \
+                          cudaGetErrorString(_e), __FILE__, __LINE__);        \
+  } while (0)
+
+#define SPMV_LAUNCH_CHECK()                                                   \
+  do {                                                                        \
+    cudaError_t _e = cudaGetLastError();                                      \
+    if (_e != cudaSuccess)                                                    \
+      return ::spmv::fail(SPMV_CUDA_ERROR, "kernel launch failed: %s (%s:%d)",\
+                          cudaGetErrorString(_e), __FILE__, __LINE__);        \
+  } while (0)
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+int sm_count();
+
+// Device scratch owned by plans and builders.
+struct DevBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  int alloc(size_t n) {
+    release();
+    if (n == 0) return SPMV_OK;
+    cudaError_t e = cudaMalloc(&ptr, n);
+    if (e != cudaSuccess) {
+      ptr = nullptr;
+      return fail(SPMV_CUDA_ERROR, "cudaMalloc(%zu) failed: %s", n, cudaGetErrorString(e));
+    }
+    bytes = n;
+    return SPMV_OK;
+  }
+  void release() {
+    if (ptr) cudaFree(ptr);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  template <typename T> T* as() const { return reinterpret_cast<T*>(ptr); }
+  ~DevBuf() { release(); }
+  DevBuf() = default;
+  DevBuf(const DevBuf&) = delete;
+  DevBuf& operator=(const DevBuf&) = delete;
+};
+
+inline size_t value_size(int dtype) { return dtype == SPMV_F64 ? 8 : 4; }
+inline bool valid_dtype(int dtype) { return dtype == SPMV_F32 || dtype == SPMV_F64; }
+
+// ------------------------------------------------------------ arithmetic --
+// The reference never fuses multiply-add (kernels.py:65,75,81,100 and
+// lanes.py:104 round the product, then add).  Explicit _rn intrinsics keep
+// nvcc from contracting to FMA, so every product/sum rounds like numpy.
+template <typename T> __device__ __forceinline__ T mul_rn(T a, T b);
+template <typename T> __device__ __forceinline__ T add_rn(T a, T b);
+template <> __device__ __forceinline__ double mul_rn<double>(double a, double b) { return __dmul_rn(a, b); }
+template <> __device__ __forceinline__ double add_rn<double>(double a, double b) { return __dadd_rn(a, b); }
+template <> __device__ __forceinline__ float mul_rn<float>(float a, float b) { return __fmul_rn(a, b); }
+template <> __device__ __forceinline__ float add_rn<float>(float a, float b) { return __fadd_rn(a, b); }
+
+// Streaming (read-once) loads: bypass L1 allocation so the x window keeps L1.
+template <typename T> __device__ __forceinline__ T ld_stream(const T* p);
+template <> __device__ __forceinline__ double ld_stream<double>(const double* p) {
+  double v;
+  asm("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+template <> __device__ __forceinline__ float ld_stream<float>(const float* p) {
+  float v;
+  asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+template <> __device__ __forceinline__ uint32_t ld_stream<uint32_t>(const uint32_t* p) {
+  uint32_t v;
+  asm("ld.global.nc.L1::no_allocate.u32 %0, [%1];" : "=r"(v) : "l"(p));
+  return v;
+}
+
+// Warp tree of lanes.py:107-128: vals[:w] + vals[w:2w] for w = W/2 .. 1.
+// shfl_down by w hands lane i the value of lane i+w, i.e. the same pairs in
+// the same operand order.
+template <typename T>
+__device__ __forceinline__ T tree_reduce_warp(T v, int width) {
+  for (int w = width >> 1; w >= 1; w >>= 1)
+    v = add_rn(v, __shfl_down_sync(0xffffffffu, v, w, width));
+  return v;
+}
+
+// Long-row work item shared by the CSR and COO plans: entries [begin, end)
+// of one row; rows with nchunks > 1 combine partials[first .. first+nchunks)
+// in chunk order.
+struct LongItem {
+  uint32_t row;
+  uint32_t begin;
+  uint32_t end;
+  uint32_t first;
+  uint32_t nchunks;
+  uint32_t pad0, pad1, pad2;
+};
+
+constexpr int kExactLen = 32;        // rows up to this length are summed by one thread
+constexpr int kChunk = 2048;         // entries per long-row warp item
+
+}  // namespace spmv

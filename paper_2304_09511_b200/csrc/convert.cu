@@ -1,0 +1,489 @@
+// On-device format conversions, bit-exact with convert.py.
+//
+//   coo_to_csr  (convert.py:87-94)   boundary scatter of a sorted row array
+//   csr_to_coo  (convert.py:97-110)  row expansion + strictly-increasing check
+//   coo_to_dia  (convert.py:113-144) diagonal-id bitmap, scan, scatter
+//   dia_to_coo  (convert.py:147-177) per-row compaction of nonzero cells
+//   sort_coo    (convert.py:60-84)   stable 64-bit key radix sort, duplicate
+//                                    runs summed in np.add.reduceat order
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "common.cuh"
+
+namespace spmv {
+
+static int64_t grid_for(int64_t n, int tb = 256) {
+  int64_t g = (n + tb - 1) / tb;
+  const int64_t cap = int64_t(sm_count()) * 32;
+  if (g > cap) g = cap;
+  if (g < 1) g = 1;
+  return g;
+}
+
+#define GRID_STRIDE(k, n) \
+  for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < (n); k += int64_t(gridDim.x) * blockDim.x)
+
+// ---- coo -> csr: irp[r] = first entry with row >= r -----------------------
+__global__ void coo_irp_kernel(const uint32_t* __restrict__ ai, int64_t nnz, int64_t nrows, uint32_t* __restrict__ irp) {
+  GRID_STRIDE(k, nnz) {
+    const int64_t rk = ai[k];
+    const int64_t rp = k == 0 ? -1 : int64_t(ai[k - 1]);
+    for (int64_t r = rp + 1; r <= rk; ++r) irp[r] = uint32_t(k);
+    if (k == nnz - 1)
+      for (int64_t r = rk + 1; r <= nrows; ++r) irp[r] = uint32_t(nnz);
+  }
+}
+
+// ---- csr -> coo ------------------------------------------------------------
+// Thread per row for rows of <= 64 entries, warp per row for longer ones.
+__global__ void csr_expand_short_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj,
+                                        int64_t nrows, uint32_t* __restrict__ ai, int* __restrict__ unsorted) {
+  GRID_STRIDE(r, nrows) {
+    const uint32_t s = irp[r], e = irp[r + 1];
+    if (e - s > 64) continue;
+    bool bad = false;
+    for (uint32_t j = s; j < e; ++j) {
+      ai[j] = uint32_t(r);
+      if (j > s && aj[j] <= aj[j - 1]) bad = true;
+    }
+    if (bad) *unsorted = 1;
+  }
+}
+
+__global__ void csr_expand_long_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj,
+                                       int64_t nrows, uint32_t* __restrict__ ai, int* __restrict__ unsorted) {
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t r = warp; r < nrows; r += nwarps) {
+    const uint32_t s = irp[r], e = irp[r + 1];
+    if (e - s <= 64) continue;
+    bool bad = false;
+    for (uint32_t j = s + lane; j < e; j += 32) {
+      ai[j] = uint32_t(r);
+      if (j > s && aj[j] <= aj[j - 1]) bad = true;
+    }
+    if (__any_sync(0xffffffffu, bad) && lane == 0) *unsorted = 1;
+  }
+}
+
+// ---- coo -> dia --------------------------------------------------------------
+__global__ void diag_mark_kernel(const uint32_t* __restrict__ ai, const uint32_t* __restrict__ aj, int64_t nnz,
+                                 int64_t nrows, uint32_t* __restrict__ flags) {
+  GRID_STRIDE(k, nnz) flags[int64_t(aj[k]) - int64_t(ai[k]) + nrows - 1] = 1u;
+}
+
+__global__ void diag_offsets_kernel(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos, int64_t nd_all,
+                                    int64_t nrows, int32_t* __restrict__ offsets) {
+  GRID_STRIDE(d, nd_all) if (flags[d]) offsets[pos[d]] = int32_t(d - (nrows - 1));
+}
+
+template <typename T>
+__global__ void diag_scatter_kernel(const uint32_t* __restrict__ ai, const uint32_t* __restrict__ aj,
+                                    const T* __restrict__ av, int64_t nnz, int64_t nrows, int64_t ndiags,
+                                    const uint32_t* __restrict__ pos, T* __restrict__ out) {
+  GRID_STRIDE(k, nnz) {
+    const int64_t r = ai[k];
+    const int64_t d = pos[int64_t(aj[k]) - r + nrows - 1];
+    out[r * ndiags + d] = av[k];
+  }
+}
+
+// ---- dia -> coo --------------------------------------------------------------
+template <typename T>
+__global__ void dia_count_kernel(const int32_t* __restrict__ offs, const T* __restrict__ vals, int64_t nrows,
+                                 int64_t ncols, int64_t nd, unsigned long long* __restrict__ counts) {
+  GRID_STRIDE(i, nrows) {
+    unsigned long long c = 0;
+    for (int64_t d = 0; d < nd; ++d) {
+      const int64_t col = i + offs[d];
+      if (col >= 0 && col < ncols && vals[i * nd + d] != T(0)) ++c;
+    }
+    counts[i] = c;
+  }
+}
+
+template <typename T>
+__global__ void dia_emit_kernel(const int32_t* __restrict__ offs, const T* __restrict__ vals, int64_t nrows,
+                                int64_t ncols, int64_t nd, const unsigned long long* __restrict__ starts,
+                                uint32_t* __restrict__ ai, uint32_t* __restrict__ aj, T* __restrict__ av) {
+  GRID_STRIDE(i, nrows) {
+    unsigned long long o = starts[i];
+    for (int64_t d = 0; d < nd; ++d) {
+      const int64_t col = i + offs[d];
+      const T v = vals[i * nd + d];
+      if (col >= 0 && col < ncols && v != T(0)) {
+        ai[o] = uint32_t(i);
+        aj[o] = uint32_t(col);
+        av[o] = v;
+        ++o;
+      }
+    }
+  }
+}
+
+// ---- sort_coo ------------------------------------------------------------------
+__global__ void make_keys_kernel(const uint32_t* __restrict__ ai, const uint32_t* __restrict__ aj, int64_t nnz,
+                                 unsigned long long* __restrict__ keys, uint32_t* __restrict__ idx) {
+  GRID_STRIDE(k, nnz) {
+    keys[k] = (static_cast<unsigned long long>(ai[k]) << 32) | aj[k];
+    idx[k] = uint32_t(k);
+  }
+}
+
+__global__ void key_heads_kernel(const unsigned long long* __restrict__ keys, int64_t n, uint32_t* __restrict__ head) {
+  GRID_STRIDE(k, n) head[k] = (k == 0 || keys[k] != keys[k - 1]) ? 1u : 0u;
+}
+
+__global__ void key_runs_kernel(const uint32_t* __restrict__ head, const uint32_t* __restrict__ pos, int64_t n,
+                                uint32_t* __restrict__ run_start) {
+  GRID_STRIDE(k, n) if (head[k]) run_start[pos[k]] = uint32_t(k);
+}
+
+// numpy 2.3 pairwise_sum (loops_utils.h): < 8 terms sequential from -0.0,
+// <= 128 terms eight interleaved accumulators, else split at n/2 rounded
+// down to a multiple of 8.  Verified bit-for-bit against np.add.reduceat
+// (tests/golden/make_golden.py pins it).
+template <typename T>
+__device__ T np_pairwise(const T* __restrict__ av, const uint32_t* __restrict__ perm, uint32_t lo, uint32_t n) {
+  if (n < 8) {
+    T res = T(-0.0);
+    for (uint32_t i = 0; i < n; ++i) res = add_rn(res, av[perm[lo + i]]);
+    return res;
+  }
+  if (n <= 128) {
+    T r[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) r[j] = av[perm[lo + j]];
+    uint32_t i = 8;
+    for (; i < n - (n % 8); i += 8)
+#pragma unroll
+      for (int j = 0; j < 8; ++j) r[j] = add_rn(r[j], av[perm[lo + i + j]]);
+    T res = add_rn(add_rn(add_rn(r[0], r[1]), add_rn(r[2], r[3])), add_rn(add_rn(r[4], r[5]), add_rn(r[6], r[7])));
+    for (; i < n; ++i) res = add_rn(res, av[perm[lo + i]]);
+    return res;
+  }
+  uint32_t n2 = n / 2;
+  n2 -= n2 % 8;
+  return add_rn(np_pairwise(av, perm, lo, n2), np_pairwise(av, perm, lo + n2, n - n2));
+}
+
+template <typename T>
+__global__ void sort_emit_kernel(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ perm,
+                                 const uint32_t* __restrict__ run_start, int64_t n_runs, int64_t nnz,
+                                 const T* __restrict__ av, uint32_t* __restrict__ ai, uint32_t* __restrict__ aj,
+                                 T* __restrict__ out) {
+  GRID_STRIDE(i, n_runs) {
+    const uint32_t a = run_start[i];
+    const uint32_t b = (i + 1 < n_runs) ? run_start[i + 1] : uint32_t(nnz);
+    const unsigned long long key = keys[a];
+    ai[i] = uint32_t(key >> 32);
+    aj[i] = uint32_t(key & 0xffffffffull);
+    T v = av[perm[a]];
+    if (b - a > 1) v = add_rn(v, np_pairwise(av, perm, a + 1, b - a - 1));
+    out[i] = v;
+  }
+}
+
+}  // namespace spmv
+
+using namespace spmv;
+
+struct spmv_dia_builder {
+  int64_t nrows = 0, ncols = 0, nnz = 0, nd_all = 0, ndiags = 0;
+  DevBuf flags, pos;
+};
+
+struct spmv_dia_collect {
+  int64_t nrows = 0, ncols = 0, ndiags = 0, nnz = 0;
+  DevBuf counts, starts;
+};
+
+struct spmv_coo_sorter {
+  int64_t nnz = 0, n_runs = 0;
+  DevBuf keys, perm, run_start;
+};
+
+template <typename V>
+static int excl_scan(const V* in, V* out, int64_t n, cudaStream_t st) {
+  size_t tmp_bytes = 0;
+  SPMV_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, in, out, n, st));
+  DevBuf tmp;
+  int rc = tmp.alloc(tmp_bytes);
+  if (rc) return rc;
+  SPMV_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.ptr, tmp_bytes, in, out, n, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  return SPMV_OK;
+}
+
+template <typename V>
+static int scan_total(const V* flags, const V* pos, int64_t n, cudaStream_t st, int64_t* total) {
+  V a = 0, b = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&a, flags + n - 1, sizeof(V), cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&b, pos + n - 1, sizeof(V), cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  *total = int64_t(a) + int64_t(b);
+  return SPMV_OK;
+}
+
+extern "C" {
+
+int spmv_coo_to_csr(int dtype, int64_t nrows, int64_t nnz, const uint32_t* ai, const uint32_t* aj, const void* av,
+                    uint32_t* irp, uint32_t* aj_out, void* av_out, void* stream) {
+  if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
+  if (nrows < 0 || nnz < 0 || nnz > int64_t(UINT32_MAX)) return fail(SPMV_INVALID_ARG, "bad sizes");
+  if (!irp) return fail(SPMV_INVALID_ARG, "row_pointers_out is NULL");
+  cudaStream_t st = as_stream(stream);
+  if (nnz == 0) {
+    SPMV_CUDA_TRY(cudaMemsetAsync(irp, 0, sizeof(uint32_t) * (nrows + 1), st));
+    return SPMV_OK;
+  }
+  coo_irp_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, nnz, nrows, irp);
+  SPMV_LAUNCH_CHECK();
+  SPMV_CUDA_TRY(cudaMemcpyAsync(aj_out, aj, 4 * nnz, cudaMemcpyDeviceToDevice, st));
+  SPMV_CUDA_TRY(cudaMemcpyAsync(av_out, av, value_size(dtype) * nnz, cudaMemcpyDeviceToDevice, st));
+  return SPMV_OK;
+}
+
+int spmv_csr_to_coo(int dtype, int64_t nrows, int64_t nnz, const uint32_t* irp, const uint32_t* aj, const void* av,
+                    uint32_t* ai_out, uint32_t* aj_out, void* av_out, int* sorted_out, void* stream) {
+  if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
+  if (nrows < 0 || nnz < 0 || nnz > int64_t(UINT32_MAX)) return fail(SPMV_INVALID_ARG, "bad sizes");
+  cudaStream_t st = as_stream(stream);
+  if (sorted_out) *sorted_out = 1;
+  if (nnz == 0 || nrows == 0) return SPMV_OK;
+  DevBuf flag;
+  int rc = flag.alloc(sizeof(int));
+  if (rc) return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(flag.ptr, 0, sizeof(int), st));
+  csr_expand_short_kernel<<<unsigned(grid_for(nrows)), 256, 0, st>>>(irp, aj, nrows, ai_out, flag.as<int>());
+  SPMV_LAUNCH_CHECK();
+  csr_expand_long_kernel<<<unsigned(grid_for(nrows * 32)), 256, 0, st>>>(irp, aj, nrows, ai_out, flag.as<int>());
+  SPMV_LAUNCH_CHECK();
+  SPMV_CUDA_TRY(cudaMemcpyAsync(aj_out, aj, 4 * nnz, cudaMemcpyDeviceToDevice, st));
+  SPMV_CUDA_TRY(cudaMemcpyAsync(av_out, av, value_size(dtype) * nnz, cudaMemcpyDeviceToDevice, st));
+  int h = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&h, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  if (sorted_out) *sorted_out = h ? 0 : 1;
+  return SPMV_OK;
+}
+
+int spmv_coo_to_dia_analyze(int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* ai, const uint32_t* aj,
+                            void* stream, spmv_dia_builder** out, int64_t* ndiags_out) {
+  if (!out || !ndiags_out) return fail(SPMV_INVALID_ARG, "NULL output");
+  *out = nullptr;
+  if (nrows < 0 || ncols < 0 || nnz < 0) return fail(SPMV_INVALID_ARG, "bad sizes");
+  cudaStream_t st = as_stream(stream);
+  auto* b = new spmv_dia_builder();
+  b->nrows = nrows;
+  b->ncols = ncols;
+  b->nnz = nnz;
+  int rc = SPMV_OK;
+  if (nnz > 0) {
+    b->nd_all = nrows + ncols - 1;
+    if (!(rc = b->flags.alloc(4 * b->nd_all)) && !(rc = b->pos.alloc(4 * b->nd_all))) {
+      cudaError_t e = cudaMemsetAsync(b->flags.ptr, 0, 4 * b->nd_all, st);
+      if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "memset: %s", cudaGetErrorString(e));
+      if (!rc) {
+        diag_mark_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, aj, nnz, nrows, b->flags.as<uint32_t>());
+        e = cudaGetLastError();
+        if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "diag_mark: %s", cudaGetErrorString(e));
+      }
+      if (!rc) rc = excl_scan<uint32_t>(b->flags.as<uint32_t>(), b->pos.as<uint32_t>(), b->nd_all, st);
+      if (!rc) rc = scan_total<uint32_t>(b->flags.as<uint32_t>(), b->pos.as<uint32_t>(), b->nd_all, st, &b->ndiags);
+    }
+  }
+  if (rc) {
+    delete b;
+    return rc;
+  }
+  *ndiags_out = b->ndiags;
+  *out = b;
+  return SPMV_OK;
+}
+
+int spmv_coo_to_dia_offsets(const spmv_dia_builder* b, int32_t* offsets_out, void* stream) {
+  if (!b) return fail(SPMV_INVALID_ARG, "builder is NULL");
+  if (b->ndiags == 0) return SPMV_OK;
+  cudaStream_t st = as_stream(stream);
+  diag_offsets_kernel<<<unsigned(grid_for(b->nd_all)), 256, 0, st>>>(b->flags.as<uint32_t>(), b->pos.as<uint32_t>(),
+                                                                     b->nd_all, b->nrows, offsets_out);
+  SPMV_LAUNCH_CHECK();
+  return SPMV_OK;
+}
+
+int spmv_coo_to_dia_fill(const spmv_dia_builder* b, int dtype, int64_t padded_rows, const uint32_t* ai,
+                         const uint32_t* aj, const void* av, void* values_out, void* stream) {
+  if (!b) return fail(SPMV_INVALID_ARG, "builder is NULL");
+  if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
+  if (padded_rows < b->nrows) return fail(SPMV_INVALID_ARG, "padded_rows < nrows");
+  cudaStream_t st = as_stream(stream);
+  const size_t bytes = value_size(dtype) * size_t(padded_rows) * size_t(b->ndiags);
+  if (bytes) SPMV_CUDA_TRY(cudaMemsetAsync(values_out, 0, bytes, st));
+  if (b->nnz == 0 || b->ndiags == 0) return SPMV_OK;
+  if (dtype == SPMV_F64)
+    diag_scatter_kernel<double><<<unsigned(grid_for(b->nnz)), 256, 0, st>>>(
+        ai, aj, static_cast<const double*>(av), b->nnz, b->nrows, b->ndiags, b->pos.as<uint32_t>(),
+        static_cast<double*>(values_out));
+  else
+    diag_scatter_kernel<float><<<unsigned(grid_for(b->nnz)), 256, 0, st>>>(
+        ai, aj, static_cast<const float*>(av), b->nnz, b->nrows, b->ndiags, b->pos.as<uint32_t>(),
+        static_cast<float*>(values_out));
+  SPMV_LAUNCH_CHECK();
+  return SPMV_OK;
+}
+
+int spmv_dia_builder_destroy(spmv_dia_builder* b) {
+  delete b;
+  return SPMV_OK;
+}
+
+int spmv_dia_to_coo_count(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags, const int32_t* offsets,
+                          const void* values, void* stream, spmv_dia_collect** out, int64_t* nnz_out) {
+  if (!out || !nnz_out) return fail(SPMV_INVALID_ARG, "NULL output");
+  *out = nullptr;
+  if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
+  if (nrows < 0 || ncols < 0 || ndiags < 0) return fail(SPMV_INVALID_ARG, "bad sizes");
+  cudaStream_t st = as_stream(stream);
+  auto* c = new spmv_dia_collect();
+  c->nrows = nrows;
+  c->ncols = ncols;
+  c->ndiags = ndiags;
+  int rc = SPMV_OK;
+  if (nrows > 0 && ndiags > 0) {
+    rc = c->counts.alloc(8 * nrows);
+    if (!rc) rc = c->starts.alloc(8 * nrows);
+    if (!rc) {
+      if (dtype == SPMV_F64)
+        dia_count_kernel<double><<<unsigned(grid_for(nrows)), 256, 0, st>>>(
+            offsets, static_cast<const double*>(values), nrows, ncols, ndiags, c->counts.as<unsigned long long>());
+      else
+        dia_count_kernel<float><<<unsigned(grid_for(nrows)), 256, 0, st>>>(
+            offsets, static_cast<const float*>(values), nrows, ncols, ndiags, c->counts.as<unsigned long long>());
+      cudaError_t e = cudaGetLastError();
+      if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "dia_count: %s", cudaGetErrorString(e));
+    }
+    if (!rc)
+      rc = excl_scan<unsigned long long>(c->counts.as<unsigned long long>(), c->starts.as<unsigned long long>(),
+                                         nrows, st);
+    if (!rc)
+      rc = scan_total<unsigned long long>(c->counts.as<unsigned long long>(), c->starts.as<unsigned long long>(),
+                                          nrows, st, &c->nnz);
+    if (!rc && c->nnz > int64_t(UINT32_MAX))
+      rc = fail(SPMV_INDEX_OVERFLOW, "DIA holds %lld nonzeros, over the 32-bit index range", (long long)c->nnz);
+  }
+  if (rc) {
+    delete c;
+    return rc;
+  }
+  *nnz_out = c->nnz;
+  *out = c;
+  return SPMV_OK;
+}
+
+int spmv_dia_to_coo_fill(const spmv_dia_collect* c, int dtype, const int32_t* offsets, const void* values,
+                         uint32_t* ai, uint32_t* aj, void* av, void* stream) {
+  if (!c) return fail(SPMV_INVALID_ARG, "collector is NULL");
+  if (c->nnz == 0) return SPMV_OK;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == SPMV_F64)
+    dia_emit_kernel<double><<<unsigned(grid_for(c->nrows)), 256, 0, st>>>(
+        offsets, static_cast<const double*>(values), c->nrows, c->ncols, c->ndiags,
+        c->starts.as<unsigned long long>(), ai, aj, static_cast<double*>(av));
+  else
+    dia_emit_kernel<float><<<unsigned(grid_for(c->nrows)), 256, 0, st>>>(
+        offsets, static_cast<const float*>(values), c->nrows, c->ncols, c->ndiags,
+        c->starts.as<unsigned long long>(), ai, aj, static_cast<float*>(av));
+  SPMV_LAUNCH_CHECK();
+  return SPMV_OK;
+}
+
+int spmv_dia_collect_destroy(spmv_dia_collect* c) {
+  delete c;
+  return SPMV_OK;
+}
+
+int spmv_sort_coo_analyze(int dtype, int64_t nnz, const uint32_t* ai, const uint32_t* aj, void* stream,
+                          spmv_coo_sorter** out, int64_t* nnz_out) {
+  if (!out || !nnz_out) return fail(SPMV_INVALID_ARG, "NULL output");
+  *out = nullptr;
+  if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
+  if (nnz < 0 || nnz > int64_t(UINT32_MAX)) return fail(SPMV_INVALID_ARG, "bad nnz");
+  cudaStream_t st = as_stream(stream);
+  auto* s = new spmv_coo_sorter();
+  s->nnz = nnz;
+  int rc = SPMV_OK;
+  if (nnz > 0) {
+    DevBuf keys_in, idx_in, head, pos, tmp;
+    rc = keys_in.alloc(8 * nnz);
+    if (!rc) rc = idx_in.alloc(4 * nnz);
+    if (!rc) rc = s->keys.alloc(8 * nnz);
+    if (!rc) rc = s->perm.alloc(4 * nnz);
+    if (!rc) rc = head.alloc(4 * nnz);
+    if (!rc) rc = pos.alloc(4 * nnz);
+    if (!rc) {
+      make_keys_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, aj, nnz, keys_in.as<unsigned long long>(),
+                                                                idx_in.as<uint32_t>());
+      size_t tmp_bytes = 0;
+      cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in.as<unsigned long long>(),
+                                                      s->keys.as<unsigned long long>(), idx_in.as<uint32_t>(),
+                                                      s->perm.as<uint32_t>(), nnz, 0, 64, st);
+      if (e == cudaSuccess) {
+        rc = tmp.alloc(tmp_bytes);
+        if (!rc)
+          e = cub::DeviceRadixSort::SortPairs(tmp.ptr, tmp_bytes, keys_in.as<unsigned long long>(),
+                                              s->keys.as<unsigned long long>(), idx_in.as<uint32_t>(),
+                                              s->perm.as<uint32_t>(), nnz, 0, 64, st);
+      }
+      if (!rc && e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "radix sort: %s", cudaGetErrorString(e));
+    }
+    if (!rc) {
+      key_heads_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(s->keys.as<unsigned long long>(), nnz,
+                                                                head.as<uint32_t>());
+      rc = excl_scan<uint32_t>(head.as<uint32_t>(), pos.as<uint32_t>(), nnz, st);
+    }
+    if (!rc) rc = scan_total<uint32_t>(head.as<uint32_t>(), pos.as<uint32_t>(), nnz, st, &s->n_runs);
+    if (!rc) rc = s->run_start.alloc(4 * s->n_runs);
+    if (!rc) {
+      key_runs_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(head.as<uint32_t>(), pos.as<uint32_t>(), nnz,
+                                                               s->run_start.as<uint32_t>());
+      cudaError_t e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "sort_coo analyze: %s", cudaGetErrorString(e));
+    }
+  }
+  if (rc) {
+    delete s;
+    return rc;
+  }
+  *nnz_out = s->n_runs;
+  *out = s;
+  return SPMV_OK;
+}
+
+int spmv_sort_coo_emit(const spmv_coo_sorter* s, int dtype, const void* av, uint32_t* ai_out, uint32_t* aj_out,
+                       void* av_out, void* stream) {
+  if (!s) return fail(SPMV_INVALID_ARG, "sorter is NULL");
+  if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
+  if (s->n_runs == 0) return SPMV_OK;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == SPMV_F64)
+    sort_emit_kernel<double><<<unsigned(grid_for(s->n_runs)), 256, 0, st>>>(
+        s->keys.as<unsigned long long>(), s->perm.as<uint32_t>(), s->run_start.as<uint32_t>(), s->n_runs, s->nnz,
+        static_cast<const double*>(av), ai_out, aj_out, static_cast<double*>(av_out));
+  else
+    sort_emit_kernel<float><<<unsigned(grid_for(s->n_runs)), 256, 0, st>>>(
+        s->keys.as<unsigned long long>(), s->perm.as<uint32_t>(), s->run_start.as<uint32_t>(), s->n_runs, s->nnz,
+        static_cast<const float*>(av), ai_out, aj_out, static_cast<float*>(av_out));
+  SPMV_LAUNCH_CHECK();
+  return SPMV_OK;
+}
+
+int spmv_coo_sorter_destroy(spmv_coo_sorter* s) {
+  delete s;
+  return SPMV_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,219 @@
+// DIA SpMV for sm_100a.
+//
+// Reference: spmv_dia_plain (kernels.py:85-101) adds, for each diagonal in
+// ascending offset order, values[i, d] * x[i + off] into y[i] for the rows
+// whose column lies inside the matrix; spmv_dia_vla (kernels.py:174-210)
+// visits each row's diagonals in the same order.  One thread per row that
+// starts from +0.0 and adds its in-bounds products in diagonal order is
+// therefore bit-exact with both.
+//
+// Data layout: the reference's row-major (padded_rows, ndiags) block
+// (formats.py:166-207).  A tile of R consecutive rows is one contiguous
+// R*ndiags*sizeof(T) byte range, so a single cp.async.bulk (TMA 1-D bulk
+// copy, completion on an mbarrier) stages it into shared memory; a
+// persistent CTA keeps STAGES tiles in flight while it computes on the
+// oldest one.  Each thread then reads its row from shared memory (stride
+// ndiags, odd strides are bank-conflict free for 8-byte words) and gathers
+// x through L1: the x window of a tile is re-read by every diagonal with
+// the same (dz, dy), so it stays L1/L2 resident.
+#include "common.cuh"
+
+namespace spmv {
+
+constexpr int kDiaThreads = 256;
+constexpr int kMaxSmemOffsets = 2048;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
+               : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n"
+      ".reg .pred P1;\n"
+      "WAIT_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
+      "@!P1 bra WAIT_%=;\n"
+      "}\n" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+          smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+template <typename T>
+__device__ __forceinline__ T dia_row(const T* __restrict__ v, const int32_t* __restrict__ offs, int nd, int64_t grow,
+                                     int64_t ncols, const T* __restrict__ xb) {
+  T acc = T(0);
+#pragma unroll 9
+  for (int d = 0; d < nd; ++d) {
+    const int64_t col = grow + offs[d];
+    if (col >= 0 && col < ncols) acc = add_rn(acc, mul_rn(v[d], __ldg(xb + col)));
+  }
+  return acc;
+}
+
+// Persistent TMA-pipelined kernel.  Tile t covers local rows
+// [t*R, t*R + R) (the last tile is clipped to avail_rows).
+template <typename T, int STAGES>
+__global__ void __launch_bounds__(kDiaThreads)
+dia_bulk_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offsets, int nd, const T* __restrict__ x,
+                T* __restrict__ y, int64_t nrows, int64_t avail_rows, int64_t ncols, int64_t row_base,
+                int64_t col_base, int rows_per_tile, int64_t ntiles, uint32_t stage_bytes) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  int32_t* s_off = reinterpret_cast<int32_t*>(smem + 128);
+  const size_t off_bytes = (size_t(nd) * 4 + 127) & ~size_t(127);
+  unsigned char* bufs = smem + 128 + off_bytes;
+  const int tid = threadIdx.x;
+  const T* xb = x - col_base;
+
+  for (int d = tid; d < nd; d += blockDim.x) s_off[d] = offsets[d];
+  if (tid == 0) {
+    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  const int64_t first = blockIdx.x;
+  const int64_t stride = gridDim.x;
+  const int64_t my_tiles = first < ntiles ? (ntiles - 1 - first) / stride + 1 : 0;
+  const size_t row_bytes = size_t(nd) * sizeof(T);
+
+  auto issue = [&](int64_t i) {
+    const int64_t t = first + i * stride;
+    const int64_t lr0 = t * rows_per_tile;
+    int64_t rows = avail_rows - lr0;
+    if (rows > rows_per_tile) rows = rows_per_tile;
+    const uint32_t bytes = uint32_t(rows * row_bytes);
+    const int s = int(i % STAGES);
+    mbar_arrive_expect_tx(&bars[s], bytes);
+    bulk_g2s(bufs + size_t(s) * stage_bytes, reinterpret_cast<const unsigned char*>(vals) + lr0 * row_bytes, bytes,
+             &bars[s]);
+  };
+
+  if (tid == 0)
+    for (int64_t i = 0; i < STAGES && i < my_tiles; ++i) issue(i);
+
+  for (int64_t i = 0; i < my_tiles; ++i) {
+    const int s = int(i % STAGES);
+    mbar_wait(&bars[s], uint32_t((i / STAGES) & 1));
+    const int64_t t = first + i * stride;
+    const int64_t lr0 = t * rows_per_tile;
+    const T* tile = reinterpret_cast<const T*>(bufs + size_t(s) * stage_bytes);
+    int64_t rows = nrows - lr0;
+    if (rows > rows_per_tile) rows = rows_per_tile;
+    for (int lr = tid; lr < rows; lr += blockDim.x)
+      y[lr0 + lr] = dia_row<T>(tile + size_t(lr) * nd, s_off, nd, row_base + lr0 + lr, ncols, xb);
+    __syncthreads();  // every thread is done with stage s
+    if (tid == 0 && i + STAGES < my_tiles) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(i + STAGES);
+    }
+  }
+}
+
+// Fallback for blocks the bulk engine cannot address (misaligned base or a
+// row count that does not give 16-byte multiples): thread per row, values
+// read straight from global memory.
+template <typename T>
+__global__ void __launch_bounds__(kDiaThreads)
+dia_direct_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offsets, int nd, const T* __restrict__ x,
+                  T* __restrict__ y, int64_t nrows, int64_t ncols, int64_t row_base, int64_t col_base) {
+  const T* xb = x - col_base;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nrows; i += int64_t(gridDim.x) * blockDim.x) {
+    T acc = T(0);
+    const T* v = vals + size_t(i) * nd;
+    for (int d = 0; d < nd; ++d) {
+      const int64_t col = row_base + i + __ldg(offsets + d);
+      if (col >= 0 && col < ncols) acc = add_rn(acc, mul_rn(__ldg(v + d), __ldg(xb + col)));
+    }
+    y[i] = acc;
+  }
+}
+
+template <typename T>
+static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_rows, const int32_t* offsets,
+                      const T* vals, const T* x, int64_t row_base, int64_t col_base, T* y, cudaStream_t st) {
+  if (nrows == 0) return SPMV_OK;
+  const int sms = sm_count();
+  const size_t row_bytes = size_t(nd) * sizeof(T);
+  // Tile size: ~56 KB per stage, R a multiple of 8 rows, at most 512 rows.
+  int64_t R = int64_t(57344 / (row_bytes ? row_bytes : 1)) / 8 * 8;
+  if (R > 512) R = 512;
+  if (R >= kDiaThreads) R = R / kDiaThreads * kDiaThreads;  // whole rows per thread
+  const bool aligned = (reinterpret_cast<uintptr_t>(vals) % 16 == 0) && ((R * row_bytes) % 16 == 0) &&
+                       ((avail_rows * row_bytes) % 16 == 0);
+  const bool use_bulk = nd > 0 && nd <= kMaxSmemOffsets && R >= 8 && aligned;
+  if (!use_bulk) {
+    int64_t grid = (nrows + kDiaThreads - 1) / kDiaThreads;
+    if (grid > int64_t(sms) * 32) grid = int64_t(sms) * 32;
+    dia_direct_kernel<T><<<unsigned(grid), kDiaThreads, 0, st>>>(vals, offsets, int(nd), x, y, nrows, ncols,
+                                                                   row_base, col_base);
+    SPMV_LAUNCH_CHECK();
+    return SPMV_OK;
+  }
+  const int64_t ntiles = (nrows + R - 1) / R;
+  const uint32_t stage_bytes = uint32_t(((R * row_bytes) + 127) & ~size_t(127));
+  const int stages = stage_bytes > 40960 ? 2 : 3;
+  const size_t off_bytes = (size_t(nd) * 4 + 127) & ~size_t(127);
+  const size_t smem = 128 + off_bytes + size_t(stages) * stage_bytes;
+  int ctas_per_sm = int((227 * 1024) / (smem + 1024));
+  if (ctas_per_sm < 1) ctas_per_sm = 1;
+  if (ctas_per_sm > 4) ctas_per_sm = 4;
+  int64_t grid = int64_t(sms) * ctas_per_sm;
+  if (grid > ntiles) grid = ntiles;
+  if (stages == 2) {
+    SPMV_CUDA_TRY(cudaFuncSetAttribute(dia_bulk_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    dia_bulk_kernel<T, 2><<<unsigned(grid), kDiaThreads, smem, st>>>(vals, offsets, int(nd), x, y, nrows, avail_rows,
+                                                                     ncols, row_base, col_base, int(R), ntiles,
+                                                                     stage_bytes);
+  } else {
+    SPMV_CUDA_TRY(cudaFuncSetAttribute(dia_bulk_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    dia_bulk_kernel<T, 3><<<unsigned(grid), kDiaThreads, smem, st>>>(vals, offsets, int(nd), x, y, nrows, avail_rows,
+                                                                     ncols, row_base, col_base, int(R), ntiles,
+                                                                     stage_bytes);
+  }
+  SPMV_LAUNCH_CHECK();
+  return SPMV_OK;
+}
+
+}  // namespace spmv
+
+using namespace spmv;
+
+extern "C" int spmv_dia(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags, int64_t avail_rows,
+                        const int32_t* offsets, const void* values, const void* x, int64_t row_base,
+                        int64_t col_base, int64_t x_len, void* y, void* stream) {
+  if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
+  if (nrows < 0 || ncols < 0 || ndiags < 0 || avail_rows < nrows || row_base < 0 || col_base < 0 || x_len < 0)
+    return fail(SPMV_INVALID_ARG, "bad DIA sizes");
+  if (nrows == 0) return SPMV_OK;
+  if (!y) return fail(SPMV_INVALID_ARG, "y is NULL");
+  cudaStream_t st = as_stream(stream);
+  if (ndiags == 0) {
+    SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, size_t(nrows) * value_size(dtype), st));
+    return SPMV_OK;
+  }
+  if (!offsets || !values || !x) return fail(SPMV_INVALID_ARG, "NULL pointer");
+  if (dtype == SPMV_F64)
+    return dia_launch<double>(nrows, ncols, ndiags, avail_rows, offsets, static_cast<const double*>(values),
+                              static_cast<const double*>(x), row_base, col_base, static_cast<double*>(y), st);
+  return dia_launch<float>(nrows, ncols, ndiags, avail_rows, offsets, static_cast<const float*>(values),
+                           static_cast<const float*>(x), row_base, col_base, static_cast<float*>(y), st);
+}

@@ -1,0 +1,292 @@
+"""SpMV entry points, kernel registry and dispatch — the drop-in boundary.
+
+Same names, argument meaning and error behaviour as the reference's
+kernels.py (kernels.py:39-297), with every product computed by the sm_100a
+kernels of libspmv_b200.so:
+
+  spmv_csr_plain  kernels.py:69-82    CSR-stream + long-row warp chunks
+  spmv_coo_plain  kernels.py:56-66    fixed-tile segmented reduction
+  spmv_dia_plain  kernels.py:85-101   TMA-staged row tiles
+  spmv_*_vla      kernels.py:104-210  sub-warp / CTA lane kernels
+
+Host/device behaviour: a numpy (or list) `x` gets the reference contract —
+x is cast to the value dtype on the host (kernels.py:51-52), copied to the
+device, and a fresh numpy y is returned.  A CUDA tensor `x` stays on the
+device and a fresh CUDA tensor y is returned (pass `out=` to reuse one).
+Matrices may be our device containers or reference host containers (these
+are uploaded once and cached, formats.as_device).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from enum import Enum
+
+import numpy as np
+import torch
+
+from . import _lib
+from .errors import DimensionMismatch, UnsortedInput, UnsupportedCombination
+from .formats import CooMatrix, CsrMatrix, DiaMatrix, Format, as_container, as_device
+from .lanes import LaneConfig
+
+
+class KernelVersion(str, Enum):
+    """Identifier for the two kernel families (kernels.py:39-43)."""
+
+    PLAIN = "plain"
+    VLA = "vla"
+
+
+def _stream(device: torch.device) -> int:
+    return torch.cuda.current_stream(device).cuda_stream
+
+
+def _ptr(t: torch.Tensor) -> int:
+    return t.data_ptr() if t.numel() else 0
+
+
+def _checked_x(m, x):
+    """kernels.py:46-53: 1-D of length ncols, cast to the value dtype.
+
+    Returns (device x, was_host)."""
+    if isinstance(x, torch.Tensor):
+        if x.dim() != 1 or x.shape[0] != m.shape.ncols:
+            raise DimensionMismatch(f"x has shape {tuple(x.shape)}, expected ({m.shape.ncols},)")
+        xv = x
+        if xv.dtype != m.values.dtype:
+            xv = xv.to(m.values.dtype)
+        if xv.device != m.values.device:
+            xv = xv.to(m.values.device)
+        return xv.contiguous(), False
+    xh = np.asarray(x)
+    if xh.ndim != 1 or xh.shape[0] != m.shape.ncols:
+        raise DimensionMismatch(f"x has shape {xh.shape}, expected ({m.shape.ncols},)")
+    if xh.dtype != m.dtype:
+        xh = xh.astype(m.dtype)
+    xv = torch.from_numpy(np.ascontiguousarray(xh)).to(m.values.device, non_blocking=False)
+    return xv, True
+
+
+def _new_y(m, out):
+    if out is not None:
+        if out.shape != (m.shape.nrows,) or out.dtype != m.values.dtype or out.device != m.values.device:
+            raise DimensionMismatch("out must be a 1-D tensor of length nrows with the value dtype")
+        return out
+    return torch.empty(m.shape.nrows, dtype=m.values.dtype, device=m.values.device)
+
+
+def _finish(y: torch.Tensor, host: bool):
+    return y.cpu().numpy() if host else y
+
+
+# -------------------------------------------------------------------- plans --
+class _Plan:
+    """Owns a C plan handle; destroyed with the container's plan cache."""
+
+    def __init__(self, kind: str, handle: ctypes.c_void_p):
+        self.kind = kind
+        self.handle = handle
+
+    def __del__(self):
+        try:
+            if self.handle:
+                getattr(_lib.load(), f"spmv_{self.kind}_plan_destroy")(self.handle)
+                self.handle = None
+        except Exception:
+            pass
+
+    def info(self) -> dict:
+        if self.kind == "csr":
+            a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+            _lib.call("spmv_csr_plan_info", self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
+            return {"long_rows": a.value, "items": b.value, "launches": c.value}
+        a, b, c, d, e = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_int64()
+        _lib.call("spmv_coo_plan_info", self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
+                  ctypes.byref(d), ctypes.byref(e))
+        return {"runs": a.value, "long_runs": b.value, "items": c.value, "row_sorted": bool(d.value),
+                "launches": e.value}
+
+
+def csr_plan(A: CsrMatrix, exact_len: int = 0) -> _Plan:
+    """CSR plan: long-row work list from the row-length histogram (cached)."""
+
+    def make():
+        h = ctypes.c_void_p()
+        _lib.call("spmv_csr_plan_create", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.nnz,
+                  _ptr(A.row_pointers), int(exact_len), _stream(A.device), ctypes.byref(h))
+        return _Plan("csr", h)
+
+    return A.plan(("csr", exact_len), make)
+
+
+def coo_plan(A: CooMatrix) -> _Plan:
+    """COO plan: row-order check, optional stable row sort, run table (cached)."""
+
+    def make():
+        h = ctypes.c_void_p()
+        _lib.call("spmv_coo_plan_create", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.nnz,
+                  _ptr(A.row_indices), _ptr(A.col_indices), _ptr(A.values), _stream(A.device), ctypes.byref(h))
+        return _Plan("coo", h)
+
+    return A.plan("coo", make)
+
+
+# ------------------------------------------------------------------ kernels --
+def spmv_coo_plain(A, x, out=None):
+    """``y = A @ x`` with np.add.at semantics (kernels.py:56-66)."""
+    A = as_device(A)
+    xv, host = _checked_x(A, x)
+    y = _new_y(A, out)
+    if A.nrows:
+        p = coo_plan(A)
+        _lib.call("spmv_coo", p.handle, _ptr(A.row_indices), _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0,
+                  A.ncols, _ptr(y), _stream(A.device))
+    return _finish(y, host)
+
+
+def spmv_csr_plain(A, x, out=None):
+    """``y = A @ x`` with one left-to-right sum per row (kernels.py:69-82)."""
+    A = as_device(A)
+    xv, host = _checked_x(A, x)
+    y = _new_y(A, out)
+    if A.nrows:
+        p = csr_plan(A)
+        _lib.call("spmv_csr", p.handle, _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0,
+                  A.ncols, _ptr(y), _stream(A.device))
+    return _finish(y, host)
+
+
+def spmv_dia_plain(A, x, out=None):
+    """``y = A @ x`` over stored diagonals (kernels.py:85-101)."""
+    A = as_device(A)
+    xv, host = _checked_x(A, x)
+    y = _new_y(A, out)
+    if A.nrows:
+        _lib.call("spmv_dia", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.ndiags, A.padded_rows,
+                  _ptr(A.offsets), _ptr(A.values), _ptr(xv), 0, 0, A.ncols, _ptr(y), _stream(A.device))
+    return _finish(y, host)
+
+
+def spmv_coo_vla(A, x, config: LaneConfig | None = None, stats: dict | None = None, out=None):
+    """Vector-style COO product (kernels.py:104-140); requires `sorted`.
+
+    When ``stats`` is given the reference's outer step count is recorded
+    under ``"outer_steps"``."""
+    cfg = config or LaneConfig()
+    A = as_device(A)
+    if not A.sorted:
+        raise UnsortedInput("vla COO kernel requires a sorted, duplicate-free COO")
+    xv, host = _checked_x(A, x)
+    y = _new_y(A, out)
+    steps = ctypes.c_int64(0)
+    if A.nrows:
+        p = coo_plan(A)
+        _lib.call("spmv_coo_vla", p.handle, _ptr(A.row_indices), _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0,
+                  A.ncols, _ptr(y), int(cfg.lanes), ctypes.byref(steps) if stats is not None else None,
+                  _stream(A.device))
+    if stats is not None:
+        stats["outer_steps"] = int(steps.value)
+    return _finish(y, host)
+
+
+def spmv_csr_vla(A, x, config: LaneConfig | None = None, out=None):
+    """Vector-style CSR product (kernels.py:143-171)."""
+    cfg = config or LaneConfig()
+    A = as_device(A)
+    xv, host = _checked_x(A, x)
+    y = _new_y(A, out)
+    if A.nrows:
+        _lib.call("spmv_csr_vla", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.nnz, _ptr(A.row_pointers),
+                  _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0, A.ncols, _ptr(y), int(cfg.lanes),
+                  _stream(A.device))
+    return _finish(y, host)
+
+
+def spmv_dia_vla(A, x, config: LaneConfig | None = None, out=None):
+    """Vector-style DIA product (kernels.py:174-210).  Each row visits its
+    diagonals in the same order for every lane count, so the GPU row kernel
+    is bit-exact with it for all L."""
+    _ = config or LaneConfig()
+    return spmv_dia_plain(A, x, out=out)
+
+
+# ----------------------------------------------------------------- registry --
+class KernelRegistry:
+    """Dispatch table mapping ``(format, version)`` to a kernel callable
+    (kernels.py:213-244).  Callables take ``(matrix, x, config)``."""
+
+    def __init__(self, table=None) -> None:
+        self._table = dict(table or {})
+
+    def register(self, fmt, version, fn) -> None:
+        self._table[(Format(fmt), KernelVersion(version))] = fn
+
+    def unregister(self, fmt, version) -> None:
+        self._table.pop((Format(fmt), KernelVersion(version)), None)
+
+    def supports(self, fmt, version) -> bool:
+        return (Format(fmt), KernelVersion(version)) in self._table
+
+    def lookup(self, fmt, version):
+        key = (Format(fmt), KernelVersion(version))
+        try:
+            return self._table[key]
+        except KeyError:
+            raise UnsupportedCombination(
+                f"no kernel registered for ({key[0].value}, {key[1].value})") from None
+
+    def pairs(self) -> list:
+        return sorted(self._table)
+
+    def copy(self) -> "KernelRegistry":
+        return KernelRegistry(self._table)
+
+
+def _plain_coo(A, x, config):
+    return spmv_coo_plain(A, x)
+
+
+def _plain_csr(A, x, config):
+    return spmv_csr_plain(A, x)
+
+
+def _plain_dia(A, x, config):
+    return spmv_dia_plain(A, x)
+
+
+def _vla_coo(A, x, config):
+    return spmv_coo_vla(A, x, config)
+
+
+def _vla_csr(A, x, config):
+    return spmv_csr_vla(A, x, config)
+
+
+def _vla_dia(A, x, config):
+    return spmv_dia_vla(A, x, config)
+
+
+def default_registry() -> KernelRegistry:
+    """Fresh registry holding both versions for all three formats (GPU)."""
+    reg = KernelRegistry()
+    reg.register(Format.COO, KernelVersion.PLAIN, _plain_coo)
+    reg.register(Format.CSR, KernelVersion.PLAIN, _plain_csr)
+    reg.register(Format.DIA, KernelVersion.PLAIN, _plain_dia)
+    reg.register(Format.COO, KernelVersion.VLA, _vla_coo)
+    reg.register(Format.CSR, KernelVersion.VLA, _vla_csr)
+    reg.register(Format.DIA, KernelVersion.VLA, _vla_dia)
+    return reg
+
+
+_DEFAULT_REGISTRY = default_registry()
+
+
+def dispatch(matrix, x, version=KernelVersion.PLAIN, config: LaneConfig | None = None,
+             registry: KernelRegistry | None = None):
+    """Run ``y = A @ x`` with the kernel registered for the matrix's format
+    (kernels.py:286-297).  Accepts a container or a DynamicMatrix."""
+    m = as_container(matrix)
+    reg = registry if registry is not None else _DEFAULT_REGISTRY
+    fn = reg.lookup(m.format, KernelVersion(version))
+    return fn(m, x, config)

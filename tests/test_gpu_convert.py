@@ -1,0 +1,148 @@
+"""On-device conversions: bit-exact with the reference (convert.py), mirroring
+test_convert.py and acceptance criterion 04 (test_acceptance.py:128-155)."""
+
+import numpy as np
+import pytest
+
+from _util import bit_equal, corpus_names, load_golden, matrix_arrays
+from test_gpu_kernels import dev_matrix
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def sp(lib_built):
+    import paper_2304_09511_b200 as sp
+    return sp
+
+
+def host(m):
+    return m.to_host()
+
+
+def assert_coo_equal(got, ref_arrs):
+    h = got.to_host()
+    assert h["shape"].nnz == int(ref_arrs["shape"][2])
+    assert np.array_equal(h["row_indices"], ref_arrs["row_indices"])
+    assert np.array_equal(h["col_indices"], ref_arrs["col_indices"])
+    assert bit_equal(h["values"], ref_arrs["values"])
+
+
+@pytest.mark.parametrize("name", corpus_names())
+def test_corpus_conversions_bit_exact(sp, name):
+    d = load_golden("corpus")
+    coo_a = matrix_arrays(d, f"{name}/coo")
+    csr_a = matrix_arrays(d, f"{name}/csr")
+    dia_a = matrix_arrays(d, f"{name}/dia")
+    orig_a = matrix_arrays(d, f"{name}/orig")
+    loose = sp.DiaFillPolicy(max_fill_ratio=float("inf"))
+    # the as-given container through the hub, to every format
+    fmt0 = "csr" if "row_pointers" in orig_a else ("dia" if "offsets" in orig_a else "coo")
+    orig = dev_matrix(sp, orig_a, fmt0)
+    assert_coo_equal(sp.to_format(orig, "coo"), coo_a)
+    csr = sp.to_format(orig, "csr")
+    h = csr.to_host()
+    assert np.array_equal(h["row_pointers"], csr_a["row_pointers"])
+    assert np.array_equal(h["col_indices"], csr_a["col_indices"]) and bit_equal(h["values"], csr_a["values"])
+    dia = sp.to_format(orig, "dia", loose)
+    h = dia.to_host()
+    assert np.array_equal(h["offsets"], dia_a["offsets"]) and bit_equal(h["values"], dia_a["values"])
+    # round trips (criterion 04)
+    coo = dev_matrix(sp, coo_a, "coo")
+    assert_coo_equal(sp.csr_to_coo(sp.coo_to_csr(coo)), coo_a)
+    try:
+        dd = sp.coo_to_dia(coo)
+    except sp.FillRatioExceeded:
+        return
+    back = sp.dia_to_coo(dd)
+    keep = coo_a["values"] != 0
+    ref = dict(coo_a)
+    ref.update(row_indices=coo_a["row_indices"][keep], col_indices=coo_a["col_indices"][keep],
+               values=coo_a["values"][keep], shape=np.array([coo_a["shape"][0], coo_a["shape"][1], keep.sum()]))
+    assert_coo_equal(back, ref)
+
+
+def test_sort_coo_duplicates_pairwise(sp):
+    d = load_golden("convert")
+    for dt in ("float64", "float32"):
+        src = matrix_arrays(d, f"dups_{dt}/in")
+        got = sp.sort_coo(dev_matrix(sp, src, "coo"))
+        assert got.sorted
+        assert_coo_equal(got, matrix_arrays(d, f"dups_{dt}/sorted"))
+
+
+def test_csr_to_coo_unsorted_and_dia_specials(sp):
+    d = load_golden("convert")
+    coo = sp.csr_to_coo(dev_matrix(sp, matrix_arrays(d, "csr_unsorted/in"), "csr"))
+    assert not coo.sorted
+    assert np.array_equal(coo.to_host()["row_indices"], matrix_arrays(d, "csr_unsorted/coo")["row_indices"])
+    fixed = sp.sort_coo(coo)
+    assert fixed.to_host()["col_indices"].tolist()[:2] == [1, 3]
+    got = sp.dia_to_coo(dev_matrix(sp, matrix_arrays(d, "dia_special/in"), "dia"))
+    assert_coo_equal(got, matrix_arrays(d, "dia_special/coo"))
+    rand = dev_matrix(sp, matrix_arrays(d, "rand/coo"), "coo")
+    h = sp.coo_to_csr(rand).to_host()
+    assert np.array_equal(h["row_pointers"], matrix_arrays(d, "rand/csr")["row_pointers"])
+    h = sp.coo_to_dia(rand, sp.DiaFillPolicy(float("inf"))).to_host()
+    assert np.array_equal(h["offsets"], matrix_arrays(d, "rand/dia")["offsets"])
+    assert bit_equal(h["values"], matrix_arrays(d, "rand/dia")["values"])
+
+
+def test_canonical_conversion_kats(sp):
+    d = load_golden("canonical")
+    can = dev_matrix(sp, matrix_arrays(d, "coo"), "coo")
+    assert sp.coo_to_csr(can).to_host()["row_pointers"].tolist() == [0, 2, 4, 6, 9, 11]
+    dia = sp.coo_to_dia(can)
+    h = dia.to_host()
+    assert h["offsets"].tolist() == [-3, -1, 0, 1, 2] and dia.padded_rows == 8
+    assert h["values"][3].tolist() == [6.0, 0.0, 7.0, 8.0, 0.0] and dia.nnz == 11
+    assert not h["values"][5:].any()
+    assert sp.sort_coo(can) is can
+    assert sp.to_format(sp.to_format(can, "csr"), "csr").format == sp.Format.CSR
+
+
+def test_fill_policy(sp):
+    corner = sp.CooMatrix.from_arrays(1000, 1000, [0, 999], [999, 0], [1.0, 2.0], sorted=True)
+    with pytest.raises(sp.FillRatioExceeded) as exc:
+        sp.coo_to_dia(corner)
+    assert "fill ratio" in str(exc.value)
+    n = 64
+    rows = np.arange(n)
+    anti = sp.CooMatrix.from_arrays(n, n, rows, n - 1 - rows, np.ones(n))
+    with pytest.raises(sp.FillRatioExceeded):
+        sp.coo_to_dia(sp.sort_coo(anti))
+    with pytest.raises(sp.FillRatioExceeded) as exc:
+        sp.coo_to_dia(sp.CooMatrix.from_arrays(3, 3, [0, 1], [1, 0], [1.0, 2.0], sorted=True),
+                      sp.DiaFillPolicy(max_fill_ratio=1e9, max_ndiags=1))
+    assert "cap" in str(exc.value)
+    pair = sp.CooMatrix.from_arrays(16, 16, [0, 15], [15, 0], [1.0, 2.0], sorted=True)
+    with pytest.raises(sp.FillRatioExceeded):
+        sp.coo_to_dia(pair)
+    dia = sp.coo_to_dia(pair, sp.DiaFillPolicy(max_fill_ratio=16.0))
+    assert dia.to_host()["offsets"].tolist() == [-15, 15] and tuple(dia.values.shape) == (16, 2)
+    with pytest.raises(sp.UnsortedInput):
+        sp.coo_to_csr(sp.CooMatrix.from_arrays(2, 2, [1, 0], [0, 0], [1.0, 2.0]))
+    with pytest.raises(sp.UnsortedInput):
+        sp.coo_to_dia(sp.CooMatrix.from_arrays(2, 2, [1, 0], [0, 1], [1.0, 2.0]))
+
+
+def test_stencil_generator_bit_exact(sp):
+    d = load_golden("stencil")
+    for dims in d["dims"]:
+        key = "x".join(str(int(v)) for v in dims)
+        ref = matrix_arrays(d, key)
+        m = sp.gen_stencil27(*map(int, dims))
+        h = m.to_host()
+        assert np.array_equal(h["row_pointers"], ref["row_pointers"])
+        assert np.array_equal(h["col_indices"], ref["col_indices"]) and bit_equal(h["values"], ref["values"])
+        assert bit_equal(sp.spmv_csr_plain(m, d[f"{key}/x"]), d[f"{key}/y"])
+    with pytest.raises(sp.IndexOverflow):
+        sp.gen_stencil27(2048, 2048, 1024)
+
+
+def test_validate_device(sp):
+    d = load_golden("canonical")
+    for fmt in ("coo", "csr", "dia"):
+        assert sp.validate(dev_matrix(sp, matrix_arrays(d, fmt), fmt)) == []
+    bad = sp.CooMatrix.from_arrays(2, 2, [1, 0], [0, 1], [1.0, 2.0], sorted=True)
+    assert any("sorted flag" in v for v in sp.validate(bad))
