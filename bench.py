@@ -1,0 +1,424 @@
+#!/usr/bin/env python
+"""bench.py — SpMV GFLOP/s and achieved HBM GB/s vs the byte roofline.
+
+Default workload (BASELINE.json configs[4], the one the metric's 1/2/4/8-GPU
+scaling is quoted on, and the largest single-GPU config): the 27-point
+stencil on a 256^3 grid, 16,777,216 rows, 449,455,096 entries, fp64, CSR
+(headline) with DIA and COO reported under "per_format".  One step = one
+SpMV y = A x.  Inputs (5.7 GB CSR) are far larger than L2 (126 MB), so no
+flush is needed between steps.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config c5|c1|c3|c4]
+  python bench.py --impl reference ...   # the reference's CPU path (oracle port)
+
+N>1 is launched by torchrun: each rank owns a contiguous z-slab of rows
+(hpcg.py:95-154 with procs (1,1,P)) and exchanges one x plane with each
+neighbour over NCCL every step; time is the max over ranks.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "SpMV GFLOP/s and achieved HBM GB/s vs byte roofline per format, 1/2/4/8 B200"
+UNIT = "GFLOP/s"
+L2_BYTES = 126 * 1024 * 1024
+
+CONFIGS = {
+    "c5": {"workload": "27-point stencil 256^3, f64, CSR headline (+DIA, COO)", "grid": (256, 256, 256),
+           "formats": ("csr", "dia", "coo")},
+    "c1": {"workload": "27-point stencil 64^3, f64, CSR headline (+DIA, COO); L2 flushed between steps",
+           "grid": (64, 64, 64), "formats": ("csr", "dia", "coo")},
+    "c3": {"workload": "Zipf(1.8) 2M x 2M, rows 1..50000, f64, CSR headline (+COO, f32)", "formats": ("csr", "coo")},
+    "c4": {"workload": "banded 2^23 rows, 11 diagonals, N(0,1), f64, DIA headline (+CSR)", "formats": ("dia", "csr")},
+}
+
+
+def peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured"}
+    return {"hbm_gbs": 6650.0, "source": "fallback"}
+
+
+def algo_bytes(fmt: str, nrows: int, ncols: int, nnz: int, sv: int, ndiags: int = 0) -> int:
+    """Minimum-byte model: values + indices + x once + y once."""
+    if fmt == "csr":
+        return nnz * (sv + 4) + (nrows + 1) * 4 + ncols * sv + nrows * sv
+    if fmt == "coo":
+        return nnz * (sv + 8) + ncols * sv + nrows * sv
+    return nrows * ndiags * sv + ndiags * 4 + ncols * sv + nrows * sv
+
+
+# ------------------------------------------------------------------ clocks --
+class ClockSampler:
+    """NVML sampling of SM clock + clock-event reasons during a region."""
+
+    REASONS = {0x1: "gpu_idle", 0x2: "applications_clocks_setting", 0x4: "sw_power_cap", 0x8: "hw_slowdown",
+               0x20: "sw_thermal_slowdown", 0x40: "hw_thermal_slowdown", 0x80: "hw_power_brake_slowdown",
+               0x100: "display_clock_setting"}
+
+    def __init__(self, index: int, period_s: float = 0.005):
+        self.index, self.period = index, period_s
+        self.samples, self.reasons = [], set()
+        self._stop = threading.Event()
+        self._thread = None
+        self.max_mhz = None
+        try:
+            import pynvml
+            pynvml.nvmlInit()
+            self._nvml = pynvml
+            self._h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.max_mhz = pynvml.nvmlDeviceGetMaxClockInfo(self._h, pynvml.NVML_CLOCK_SM)
+        except Exception:
+            self._nvml = None
+
+    def _run(self):
+        nv = self._nvml
+        while not self._stop.is_set():
+            try:
+                self.samples.append(nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM))
+                fn = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or \
+                    nv.nvmlDeviceGetCurrentClocksThrottleReasons
+                bits = fn(self._h)
+                for b, name in self.REASONS.items():
+                    if bits & b and name != "gpu_idle":
+                        self.reasons.add(name)
+            except Exception:
+                pass
+            time.sleep(self.period)
+
+    def __enter__(self):
+        if self._nvml is not None:
+            self._thread = threading.Thread(target=self._run, daemon=True)
+            self._thread.start()
+        return self
+
+    def __exit__(self, *exc):
+        self._stop.set()
+        if self._thread:
+            self._thread.join()
+
+    def summary(self) -> dict:
+        return {"sm_mhz": statistics.median(self.samples) if self.samples else None, "sm_max_mhz": self.max_mhz,
+                "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------ timing --
+def time_steps(torch, fn, steps: int, warmup: int, flush=None, dist=None):
+    """W untimed steps, barrier + sync, then K steps between CUDA events on
+    the launching stream.  With `flush`, an L2-flush write runs between
+    steps outside per-step event pairs.  Returns seconds per step (max over
+    ranks when distributed)."""
+    for _ in range(warmup):
+        fn()
+    stream = torch.cuda.current_stream()
+    if dist is not None:
+        dist.barrier()
+    torch.cuda.synchronize()
+    if flush is None:
+        start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        start.record(stream)
+        for _ in range(steps):
+            fn()
+        end.record(stream)
+        torch.cuda.synchronize()
+        t = start.elapsed_time(end) / 1e3 / steps
+    else:
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(steps)]
+        for a, b in evs:
+            flush()
+            a.record(stream)
+            fn()
+            b.record(stream)
+        torch.cuda.synchronize()
+        t = sum(a.elapsed_time(b) for a, b in evs) / 1e3 / steps
+    if dist is not None:
+        tt = torch.tensor([t], dtype=torch.float64, device="cuda")
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t = float(tt.item())
+    return t
+
+
+def roofline(bytes_per_launch: int, t_launch: float, pk: dict, traffic=None) -> dict:
+    achieved = bytes_per_launch / t_launch / 1e9
+    return {"bound": "hbm", "achieved": round(achieved, 1), "peak": pk["hbm_gbs"], "unit": "GB/s",
+            "frac": round(achieved / pk["hbm_gbs"], 4), "peak_source": pk["source"], "traffic": traffic}
+
+
+def traffic_for(key: str):
+    """DRAM bytes per launch from the committed ncu capture, if present."""
+    p = ROOT / "profiles" / "traffic.json"
+    if not p.exists():
+        return None
+    try:
+        return json.loads(p.read_text()).get(key)
+    except Exception:
+        return None
+
+
+# ------------------------------------------------------------ workloads --
+def build_workload(torch, sp, cfg_name: str, device):
+    """Device containers + x for a config.  Returns dict fmt -> container."""
+    from paper_2304_09511_b200 import synthetic
+    cfg = CONFIGS[cfg_name]
+    mats = {}
+    if cfg_name in ("c5", "c1"):
+        csr = sp.gen_stencil27(*cfg["grid"])
+        mats["csr"] = csr
+        if "coo" in cfg["formats"] or "dia" in cfg["formats"]:
+            coo = sp.csr_to_coo(csr)
+            if "dia" in cfg["formats"]:
+                mats["dia"] = sp.coo_to_dia(coo)
+            if "coo" in cfg["formats"]:
+                mats["coo"] = coo
+            else:
+                del coo
+    elif cfg_name == "c3":
+        irp, cols, vals = synthetic.zipf_csr(2_000_000, 2_000_000, synthetic.ZIPF_SEED)
+        csr = sp.CsrMatrix.from_arrays(2_000_000, 2_000_000, irp, cols, vals)
+        mats["csr"] = csr
+        mats["coo"] = sp.csr_to_coo(csr)
+        mats["csr_f32"] = sp.CsrMatrix.from_arrays(2_000_000, 2_000_000, irp, cols, vals.astype(np.float32))
+    elif cfg_name == "c4":
+        n = 1 << 23
+        offs, vals, nnz = synthetic.banded_dia(n, synthetic.BANDED_OFFSETS, synthetic.BANDED_SEED)
+        dia = sp.DiaMatrix(sp.MatrixShape(n, n, nnz), offs, vals)
+        mats["dia"] = dia
+        mats["csr"] = sp.to_format(dia, "csr")
+    n = next(iter(mats.values())).ncols
+    x = torch.from_numpy(synthetic.probe_x(n, synthetic.X_SEED)).to(device)
+    return mats, x
+
+
+def spmv_fn(sp, fmt: str):
+    return {"csr": sp.spmv_csr_plain, "coo": sp.spmv_coo_plain, "dia": sp.spmv_dia_plain}[fmt.split("_")[0]]
+
+
+def launches_per_spmv(sp, m) -> int:
+    from paper_2304_09511_b200 import kernels as K
+    if m.format == sp.Format.CSR:
+        return K.csr_plan(m).info()["launches"]
+    if m.format == sp.Format.COO:
+        return K.coo_plan(m).info()["launches"]
+    return 1
+
+
+def bytes_of(m, fmt) -> int:
+    sv = m.values.element_size()
+    nd = m.ndiags if fmt.startswith("dia") else 0
+    rows = m.nrows
+    return algo_bytes(fmt.split("_")[0], rows, m.ncols, m.nnz, sv, nd)
+
+
+# ------------------------------------------------------------ cpu baseline --
+def cpu_baseline_csr(irp, cols, vals, x, budget_s: float = 10.0, y_check=None) -> dict:
+    """C restatement of spmv_csr_plain (oracle/spmv_oracle.c), all host threads,
+    repeated until the time budget is spent.  Optionally checks the GPU y."""
+    from oracle import c_oracle
+    nrows = irp.shape[0] - 1
+    threads = c_oracle.max_threads()
+    t0 = time.perf_counter()
+    y = c_oracle.csr_plain(nrows, irp, cols, vals, x)
+    first = time.perf_counter() - t0
+    reps = max(1, min(20, int(budget_s / max(first, 1e-3))))
+    t0 = time.perf_counter()
+    for _ in range(reps):
+        c_oracle.csr_plain(nrows, irp, cols, vals, x)
+    t = (time.perf_counter() - t0) / reps
+    out = {"value": round(2.0 * vals.shape[0] / t / 1e9, 3), "unit": UNIT, "cores": threads, "kind": "port",
+           "sample": f"full matrix ({vals.shape[0]} entries), {reps} SpMVs, oracle/spmv_oracle.c csr_plain "
+                     f"(OpenMP rows, same summation order as kernels.py:69-82)",
+           "s_per_spmv": round(t, 4)}
+    if y_check is not None:
+        out["gpu_y_bit_exact_vs_oracle"] = bool(np.array_equal(y.view(np.uint64), y_check.view(np.uint64)))
+    return out
+
+
+# ------------------------------------------------------------------- ours --
+def run_ours(args, torch, dist, rank, world, local_rank):
+    import paper_2304_09511_b200 as sp
+    device = torch.device("cuda", local_rank)
+    torch.cuda.set_device(device)
+    pk = peaks()
+    cfg = CONFIGS[args.config]
+    if world > 1:
+        from paper_2304_09511_b200 import dist as D
+        return D.bench_multi(args, torch, dist, rank, world, device, pk, CONFIGS, algo_bytes, time_steps,
+                             ClockSampler, roofline, METRIC, UNIT)
+    mats, x = build_workload(torch, sp, args.config, device)
+    flush_buf = None
+    flush = None
+    if args.config == "c1":
+        flush_buf = torch.empty(2 * L2_BYTES // 4, dtype=torch.float32, device=device)
+        flush = lambda: flush_buf.zero_()  # noqa: E731
+    results = {}
+    head = args.format or cfg["formats"][0]
+    clocks = None
+    order = [head] + [f for f in mats if f != head]
+    for fmt in ([head] if args.no_extras else order):
+        m = mats[fmt]
+        y = torch.empty(m.nrows, dtype=m.values.dtype, device=device)
+        fn_ = spmv_fn(sp, fmt)
+        xx = x if m.values.dtype == torch.float64 else x.float()
+        fn = lambda: fn_(m, xx, out=y)  # noqa: E731
+        fn()  # plan creation (untimed, like measure()'s conversion + warm-up)
+        torch.cuda.synchronize()
+        if fmt == head:
+            sampler = ClockSampler(local_rank)
+            with sampler:
+                t = time_steps(torch, fn, args.steps, args.warmup, flush)
+            clocks = sampler.summary()
+        else:
+            t = time_steps(torch, fn, max(10, args.steps // 4), args.warmup, flush)
+        b = bytes_of(m, fmt)
+        results[fmt] = {"gflops": round(2.0 * m.nnz / t / 1e9, 2), "ms_per_spmv": round(t * 1e3, 4),
+                        "gbs": round(b / t / 1e9, 1), "bytes_per_spmv": b, "launches": launches_per_spmv(sp, m),
+                        "roofline_frac": round(b / t / 1e9 / pk["hbm_gbs"], 4), "nnz": m.nnz}
+    m = mats[head]
+    t = results[head]["ms_per_spmv"] / 1e3
+    line = {
+        "metric": METRIC, "value": results[head]["gflops"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": results[head]["ms_per_spmv"], "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
+        "config": {"workload": cfg["workload"], "config": args.config, "format": head, "nrows": m.nrows,
+                   "nnz": m.nnz, "l2": "inputs larger than L2 (126 MB), no flush" if args.config != "c1"
+                   else "L2 flushed (252 MB write) between steps, outside the timed events",
+                   "parallelism": "row-partition" if world > 1 else "single GPU"},
+        "roofline": roofline(results[head]["bytes_per_spmv"], t, pk, traffic_for(f"{args.config}/{head}")),
+        "gpu_launches": args.steps * results[head]["launches"],
+        "clocks": clocks,
+        "per_format": results,
+    }
+    if not args.no_extras:
+        line["e2e"] = e2e_measure(args, torch, sp, m, x, head)
+        if args.config in ("c5", "c1", "c3"):
+            csr = mats["csr"]
+            h = csr.to_host()
+            y_gpu = sp.spmv_csr_plain(csr, x).cpu().numpy()
+            line["cpu_baseline"] = cpu_baseline_csr(h["row_pointers"], h["col_indices"], h["values"],
+                                                    x.cpu().numpy(), args.cpu_budget, y_check=y_gpu)
+    print(json.dumps(line), flush=True)
+
+
+def e2e_measure(args, torch, sp, m, x, fmt) -> dict:
+    """Public API with host buffers: pinned x -> device, SpMV, y -> pinned
+    host, synchronised every step (kernels.py contract: y is returned)."""
+    fn_ = spmv_fn(sp, fmt)
+    xh = x.to(m.values.dtype).cpu().pin_memory()
+    yh = torch.empty(m.nrows, dtype=m.values.dtype).pin_memory()
+    steps = max(5, min(args.steps, 30))
+    for _ in range(3):
+        fn_(m, xh, out=yh)
+    torch.cuda.synchronize()
+    stream = torch.cuda.current_stream()
+    a, b = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    t0 = time.perf_counter()
+    a.record(stream)
+    for _ in range(steps):
+        fn_(m, xh, out=yh)
+    b.record(stream)
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / steps
+    t = a.elapsed_time(b) / 1e3 / steps
+    sv = m.values.element_size()
+    return {"value": round(2.0 * m.nnz / t / 1e9, 2), "unit": UNIT, "h2d_bytes_per_step": m.ncols * sv,
+            "d2h_bytes_per_step": m.nrows * sv, "ms_per_step": round(t * 1e3, 3),
+            "wall_ms_per_step": round(wall * 1e3, 3), "steps": steps,
+            "path": f"{fn_.__module__}.{fn_.__name__}(A, pinned CPU x, out=pinned CPU y)"}
+
+
+# -------------------------------------------------------------- reference --
+def run_reference(args, rank, world):
+    """The reference's CPU SpMV (C restatement of kernels.py:69-82, all host
+    threads) on a bounded sample of the same workload; no GPU touched."""
+    if rank != 0:
+        return
+    from oracle import c_oracle
+    from paper_2304_09511_b200 import synthetic
+    cfg = CONFIGS[args.config]
+    if args.config not in ("c5", "c1"):
+        print(json.dumps({"impl": "reference", "unavailable": f"reference arm implemented for c1/c5, not {args.config}"}))
+        return
+    nx, ny, nz = cfg["grid"]
+    n = nx * ny * nz
+    x = synthetic.probe_x(n, synthetic.X_SEED)
+    # calibrate the sample: a z-slab sized so one step takes <= ~0.25 s
+    plane = nx * ny
+    slab = max(1, min(nz, 16))
+    irp, cols, vals = c_oracle.stencil27_rows(nx, ny, nz, 0, slab * plane)
+    t0 = time.perf_counter()
+    c_oracle.csr_plain(slab * plane, irp, cols, vals, x)
+    t1 = time.perf_counter() - t0
+    per_plane = t1 / slab
+    planes = int(max(1, min(nz, 0.25 / max(per_plane, 1e-6))))
+    r0 = (nz // 2 - planes // 2) * plane if planes < nz else 0
+    r1 = r0 + planes * plane
+    irp, cols, vals = c_oracle.stencil27_rows(nx, ny, nz, r0, r1)
+    fn = lambda: c_oracle.csr_plain(r1 - r0, irp, cols, vals, x)  # noqa: E731
+    for _ in range(args.warmup):
+        fn()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        fn()
+    t = (time.perf_counter() - t0) / args.steps
+    v = round(2.0 * vals.shape[0] / t / 1e9, 3)
+    sample = (f"z-planes {r0 // plane}..{r1 // plane - 1} of the {nx}x{ny}x{nz} stencil "
+              f"({r1 - r0} rows, {vals.shape[0]} entries) per step")
+    line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
+            "config": {"workload": cfg["workload"], "config": args.config, "format": "csr"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "kind": "port", "cores": c_oracle.max_threads(),
+                             "sample": sample + "; oracle/spmv_oracle.c csr_plain (restates kernels.py:69-82)"},
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=200)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=("ours", "reference"), default="ours")
+    ap.add_argument("--config", choices=tuple(CONFIGS), default="c5")
+    ap.add_argument("--format", default=None, help="headline format (default: the config's first)")
+    ap.add_argument("--no-extras", action="store_true", help="headline format only (profiling runs)")
+    ap.add_argument("--cpu-budget", type=float, default=10.0)
+    args = ap.parse_args()
+    if args.warmup < 3:
+        args.warmup = 3
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, rank, world)
+        return
+    import torch
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_ours(args, torch, dist, rank, world, local_rank)
+    finally:
+        if dist is not None:
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -91,3 +91,16 @@ def csr_vla(nrows, irp, aj, av, x, lanes):
     getattr(lib(), "oracle_csr_vla_" + _suffix(av.dtype))(
         ctypes.c_int64(nrows), _p(irp), _p(aj), _p(av), _p(x), _p(y), ctypes.c_int(lanes))
     return y
+
+
+def stencil27_rows(nx, ny, nz, r0, r1):
+    """Rows [r0, r1) of the f64 27-point operator (matrixio.py:170-210)."""
+    irp = np.empty(r1 - r0 + 1, dtype=np.uint32)
+    lib().oracle_stencil27_irp(ctypes.c_int64(nx), ctypes.c_int64(ny), ctypes.c_int64(nz), ctypes.c_int64(r0),
+                               ctypes.c_int64(r1), _p(irp))
+    nnz = int(irp[-1])
+    cols = np.empty(nnz, dtype=np.uint32)
+    vals = np.empty(nnz, dtype=np.float64)
+    lib().oracle_stencil27_fill_f64(ctypes.c_int64(nx), ctypes.c_int64(ny), ctypes.c_int64(nz), ctypes.c_int64(r0),
+                                    ctypes.c_int64(r1), _p(irp), _p(cols), _p(vals))
+    return irp, cols, vals

@@ -123,3 +123,35 @@ void oracle_set_threads(int n) { (void)n; }
 
 DEFINE_KERNELS(double, f64)
 DEFINE_KERNELS(float, f32)
+
+/* matrixio.py:170-210 restricted to rows [r0, r1): row p = (z*ny+y)*nx+x,
+ * neighbours in (dz, dy, dx) order (ascending columns), 26 / -1.  Two-pass:
+ * irp (rebased) first, then columns and values.  Used by bench.py's
+ * reference arm, which must not touch the GPU. */
+static int64_t axis_cnt(int64_t n, int64_t i) { return n == 1 ? 1 : ((i == 0 || i == n - 1) ? 2 : 3); }
+
+void oracle_stencil27_irp(int64_t nx, int64_t ny, int64_t nz, int64_t r0, int64_t r1, uint32_t* irp) {
+  irp[0] = 0;
+  for (int64_t p = r0; p < r1; ++p) {
+    int64_t x = p % nx, y = (p / nx) % ny, z = p / (nx * ny);
+    irp[p - r0 + 1] = irp[p - r0] + (uint32_t)(axis_cnt(nx, x) * axis_cnt(ny, y) * axis_cnt(nz, z));
+  }
+}
+
+void oracle_stencil27_fill_f64(int64_t nx, int64_t ny, int64_t nz, int64_t r0, int64_t r1, const uint32_t* irp,
+                               uint32_t* cols, double* vals) {
+  _Pragma("omp parallel for schedule(static, 4096)")
+  for (int64_t p = r0; p < r1; ++p) {
+    int64_t x = p % nx, y = (p / nx) % ny, z = p / (nx * ny);
+    int64_t k = irp[p - r0];
+    for (int dz = -1; dz <= 1; ++dz)
+      for (int dy = -1; dy <= 1; ++dy)
+        for (int dx = -1; dx <= 1; ++dx) {
+          int64_t qx = x + dx, qy = y + dy, qz = z + dz;
+          if (qx < 0 || qx >= nx || qy < 0 || qy >= ny || qz < 0 || qz >= nz) continue;
+          cols[k] = (uint32_t)((qz * ny + qy) * nx + qx);
+          vals[k] = (dx == 0 && dy == 0 && dz == 0) ? 26.0 : -1.0;
+          ++k;
+        }
+  }
+}

@@ -11,8 +11,10 @@ kernels of libspmv_b200.so:
 
 Host/device behaviour: a numpy (or list) `x` gets the reference contract —
 x is cast to the value dtype on the host (kernels.py:51-52), copied to the
-device, and a fresh numpy y is returned.  A CUDA tensor `x` stays on the
-device and a fresh CUDA tensor y is returned (pass `out=` to reuse one).
+device, and a fresh numpy y is returned.  A CPU torch tensor (pinned for
+asynchronous copies) gives a CPU tensor back.  A CUDA tensor `x` stays on
+the device and a fresh CUDA tensor y is returned.  `out=` may be a CUDA
+tensor (reused, no allocation) or a (pinned) CPU tensor that receives y.
 Matrices may be our device containers or reference host containers (these
 are uploaded once and cached, formats.as_device).
 """
@@ -49,35 +51,49 @@ def _ptr(t: torch.Tensor) -> int:
 def _checked_x(m, x):
     """kernels.py:46-53: 1-D of length ncols, cast to the value dtype.
 
-    Returns (device x, was_host)."""
+    Returns (device x, origin) with origin "device", "torch_host" (a CPU
+    tensor, ideally pinned: copied with non_blocking) or "numpy"."""
     if isinstance(x, torch.Tensor):
         if x.dim() != 1 or x.shape[0] != m.shape.ncols:
             raise DimensionMismatch(f"x has shape {tuple(x.shape)}, expected ({m.shape.ncols},)")
         xv = x
         if xv.dtype != m.values.dtype:
-            xv = xv.to(m.values.dtype)
+            xv = xv.to(m.values.dtype)  # cast where x lives, like the reference's astype
+        if not xv.is_cuda:
+            return xv.contiguous().to(m.values.device, non_blocking=xv.is_pinned()), "torch_host"
         if xv.device != m.values.device:
             xv = xv.to(m.values.device)
-        return xv.contiguous(), False
+        return xv.contiguous(), "device"
     xh = np.asarray(x)
     if xh.ndim != 1 or xh.shape[0] != m.shape.ncols:
         raise DimensionMismatch(f"x has shape {xh.shape}, expected ({m.shape.ncols},)")
     if xh.dtype != m.dtype:
         xh = xh.astype(m.dtype)
-    xv = torch.from_numpy(np.ascontiguousarray(xh)).to(m.values.device, non_blocking=False)
-    return xv, True
+    xv = torch.from_numpy(np.ascontiguousarray(xh)).to(m.values.device)
+    return xv, "numpy"
 
 
 def _new_y(m, out):
-    if out is not None:
+    if out is not None and out.is_cuda:
         if out.shape != (m.shape.nrows,) or out.dtype != m.values.dtype or out.device != m.values.device:
             raise DimensionMismatch("out must be a 1-D tensor of length nrows with the value dtype")
         return out
+    if out is not None and (out.shape != (m.shape.nrows,) or out.dtype != m.values.dtype):
+        raise DimensionMismatch("out must be a 1-D tensor of length nrows with the value dtype")
     return torch.empty(m.shape.nrows, dtype=m.values.dtype, device=m.values.device)
 
 
-def _finish(y: torch.Tensor, host: bool):
-    return y.cpu().numpy() if host else y
+def _finish(y: torch.Tensor, origin: str, out=None):
+    """Deliver y where the caller's x came from (or into a host `out`)."""
+    if out is not None and not out.is_cuda:
+        out.copy_(y, non_blocking=out.is_pinned())
+        torch.cuda.current_stream(y.device).synchronize()
+        return out
+    if origin == "numpy":
+        return y.cpu().numpy()
+    if origin == "torch_host":
+        return y.cpu()
+    return y
 
 
 # -------------------------------------------------------------------- plans --
@@ -136,36 +152,36 @@ def coo_plan(A: CooMatrix) -> _Plan:
 def spmv_coo_plain(A, x, out=None):
     """``y = A @ x`` with np.add.at semantics (kernels.py:56-66)."""
     A = as_device(A)
-    xv, host = _checked_x(A, x)
+    xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
         p = coo_plan(A)
         _lib.call("spmv_coo", p.handle, _ptr(A.row_indices), _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0,
                   A.ncols, _ptr(y), _stream(A.device))
-    return _finish(y, host)
+    return _finish(y, origin, out)
 
 
 def spmv_csr_plain(A, x, out=None):
     """``y = A @ x`` with one left-to-right sum per row (kernels.py:69-82)."""
     A = as_device(A)
-    xv, host = _checked_x(A, x)
+    xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
         p = csr_plan(A)
         _lib.call("spmv_csr", p.handle, _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0,
                   A.ncols, _ptr(y), _stream(A.device))
-    return _finish(y, host)
+    return _finish(y, origin, out)
 
 
 def spmv_dia_plain(A, x, out=None):
     """``y = A @ x`` over stored diagonals (kernels.py:85-101)."""
     A = as_device(A)
-    xv, host = _checked_x(A, x)
+    xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
         _lib.call("spmv_dia", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.ndiags, A.padded_rows,
                   _ptr(A.offsets), _ptr(A.values), _ptr(xv), 0, 0, A.ncols, _ptr(y), _stream(A.device))
-    return _finish(y, host)
+    return _finish(y, origin, out)
 
 
 def spmv_coo_vla(A, x, config: LaneConfig | None = None, stats: dict | None = None, out=None):
@@ -177,7 +193,7 @@ def spmv_coo_vla(A, x, config: LaneConfig | None = None, stats: dict | None = No
     A = as_device(A)
     if not A.sorted:
         raise UnsortedInput("vla COO kernel requires a sorted, duplicate-free COO")
-    xv, host = _checked_x(A, x)
+    xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     steps = ctypes.c_int64(0)
     if A.nrows:
@@ -187,20 +203,20 @@ def spmv_coo_vla(A, x, config: LaneConfig | None = None, stats: dict | None = No
                   _stream(A.device))
     if stats is not None:
         stats["outer_steps"] = int(steps.value)
-    return _finish(y, host)
+    return _finish(y, origin, out)
 
 
 def spmv_csr_vla(A, x, config: LaneConfig | None = None, out=None):
     """Vector-style CSR product (kernels.py:143-171)."""
     cfg = config or LaneConfig()
     A = as_device(A)
-    xv, host = _checked_x(A, x)
+    xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
         _lib.call("spmv_csr_vla", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.nnz, _ptr(A.row_pointers),
                   _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0, A.ncols, _ptr(y), int(cfg.lanes),
                   _stream(A.device))
-    return _finish(y, host)
+    return _finish(y, origin, out)
 
 
 def spmv_dia_vla(A, x, config: LaneConfig | None = None, out=None):
