@@ -6,145 +6,275 @@
 // walks each row in L-entry steps, tree-reduces every step and adds it once
 // into y[row].
 //
-// Plain path: fixed 2048-entry tiles (256 threads x 8 entries), so work per
-// CTA does not depend on row lengths (Zipf rows up to 50k entries).  Inside
-// a tile the row indices are segmented with a block scan; no atomics touch y.
-//   * a row of <= 32 entries is "owned" by the tile holding its first entry;
-//     one thread sums it left to right from +0.0 (shared-memory products,
-//     plus at most 31 entries past the tile end) => bit-exact with np.add.at.
-//     Whether a boundary row is short is decided from the 32 row indices on
-//     either side of the tile, so both neighbouring tiles agree.
-//   * rows of > 32 entries come from the plan's run table and go through
-//     the shared long-row warp chunks (longrow.cuh).
-//   * each tile zero-fills the empty rows between consecutive row starts,
-//     so y needs no separate memset pass.
-#include "longrow.cuh"
+// Plain path — coo_tile_kernel, persistent, TMA-fed (tile.cuh): fixed
+// 2048-entry tiles, so work per CTA does not depend on row lengths.  The
+// row indices (plus 32 on each side), column indices and values of a tile
+// are bulk-copied into a shared-memory ring; segments are found with a block
+// scan; no atomics touch y.
+//   * a row of <= 32 entries is owned by the tile holding its first entry;
+//     one thread sums it left to right from +0.0 out of shared memory (the
+//     32-entry extension covers rows crossing the tile end) => bit-exact
+//     with np.add.at.  Both neighbouring tiles decide "short" from the same
+//     32-entry windows, so they agree on the owner.
+//   * longer rows: one warp per in-tile segment (vla-32 order); segments of
+//     rows crossing tile boundaries leave carries that coo_fixup_kernel adds
+//     in tile order (deterministic, within 1e-12).
+//   * each tile zero-fills the empty rows before its row starts, so y needs
+//     no separate memset pass.
+// Rows must be non-decreasing; the plan makes a stable row-sorted copy when
+// they are not (np.add.at order inside a row = storage order, kept).
+#include <cub/cub.cuh>
+
+#include <algorithm>
+
+#include "tile.cuh"
 
 namespace spmv {
 
-constexpr int kCooThreads = 256;
-constexpr int kCooItems = 8;
-constexpr int kCooTile = kCooThreads * kCooItems;
-constexpr uint32_t kNoRow = 0xffffffffu;
+constexpr int kCooItems = kTile / kTileThreads;
 
 template <typename T>
-__global__ void __launch_bounds__(kCooThreads)
-coo_tile_kernel(const uint32_t* __restrict__ ai, const uint32_t* __restrict__ aj, const T* __restrict__ av,
-                const T* __restrict__ x, int64_t col_base, T* __restrict__ y, int64_t nnz, int64_t nrows) {
-  using BlockScan = cub::BlockScan<int, kCooThreads>;
-  __shared__ typename BlockScan::TempStorage scan_tmp;
-  __shared__ uint32_t s_row[kCooTile];
-  __shared__ T s_prod[kCooTile];
-  __shared__ uint16_t s_seg[kCooTile];
-  __shared__ uint16_t s_start[kCooTile + 1];
-  __shared__ uint8_t s_owned[kCooTile];
-  __shared__ uint32_t s_prev[32], s_next[32];
-  __shared__ int s_nseg;
+struct CooParams {
+  const uint32_t* ai;
+  const uint32_t* aj;
+  const T* av;
+  const T* x;
+  T* y;
+  uint32_t* head_row;
+  uint32_t* tail_row;
+  uint32_t* pass;
+  T* head_val;
+  T* tail_val;
+  int64_t nrows, nnz, col_base, ntiles, n_bulk;
+};
 
-  const T* xb = x - col_base;
-  const int tid = threadIdx.x;
-  const int64_t base = int64_t(blockIdx.x) * kCooTile;
-  const int cnt = int(min(int64_t(kCooTile), nnz - base));
+template <typename T>
+struct CooSmem {
+  static constexpr size_t rows_bytes = align_up(sizeof(uint32_t) * (kTile + 2 * kExt), 128);
+  static constexpr size_t cols_bytes = align_up(sizeof(uint32_t) * (kTile + kExt), 128);
+  static constexpr size_t vals_bytes = align_up(sizeof(T) * (kTile + kExt), 128);
+  static constexpr size_t stage_bytes = rows_bytes + cols_bytes + vals_bytes;
+  static constexpr size_t starts_bytes = align_up(sizeof(uint16_t) * (kTile + 1), 128);
+  static constexpr size_t long_bytes = align_up(sizeof(LongSeg) * kMaxLongSegs, 128);
+  static constexpr size_t header = 128 + starts_bytes + long_bytes;
+  static constexpr size_t total = header + kTileStages * stage_bytes;
+};
 
-  // 1. row indices of the tile (striped, coalesced) and the 32 on each side
-  for (int k = tid; k < kCooTile; k += kCooThreads) s_row[k] = k < cnt ? ld_stream(ai + base + k) : kNoRow;
-  if (tid < 32) {
-    const int64_t g = base - 32 + tid;
-    s_prev[tid] = g >= 0 ? ai[g] : kNoRow;
-  } else if (tid < 64) {
-    const int64_t g = base + cnt + (tid - 32);
-    s_next[tid - 32] = g < nnz ? ai[g] : kNoRow;
+// rows: tile-relative view, valid for k in [-kExt, kTile + kExt).
+template <typename T>
+__device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_t* __restrict__ rows,
+                                 const uint32_t* __restrict__ cols, T* __restrict__ vals, uint16_t* s_start,
+                                 LongSeg* s_long, int* s_nseg, int* s_nlong, void* scan_tmp_raw) {
+  using BlockScan = cub::BlockScan<int, kTileThreads>;
+  auto& scan_tmp = *reinterpret_cast<typename BlockScan::TempStorage*>(scan_tmp_raw);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t E0 = t * kTile;
+  const int cnt_in = int(min(int64_t(kTile), P.nnz - E0));
+  const int cnt_ext = int(min(int64_t(kTile + kExt), P.nnz - E0));
+  const T* xb = P.x - P.col_base;
+
+  // 1. products in place (4 gathers in flight per thread)
+  {
+    int k = tid;
+    for (; k + 3 * kTileThreads < cnt_ext; k += 4 * kTileThreads) {
+      const uint32_t c0 = cols[k], c1 = cols[k + kTileThreads], c2 = cols[k + 2 * kTileThreads],
+                     c3 = cols[k + 3 * kTileThreads];
+      const T x0 = __ldg(xb + c0), x1 = __ldg(xb + c1), x2 = __ldg(xb + c2), x3 = __ldg(xb + c3);
+      vals[k] = mul_rn(vals[k], x0);
+      vals[k + kTileThreads] = mul_rn(vals[k + kTileThreads], x1);
+      vals[k + 2 * kTileThreads] = mul_rn(vals[k + 2 * kTileThreads], x2);
+      vals[k + 3 * kTileThreads] = mul_rn(vals[k + 3 * kTileThreads], x3);
+    }
+    for (; k < cnt_ext; k += kTileThreads) vals[k] = mul_rn(vals[k], __ldg(xb + cols[k]));
   }
-  __syncthreads();
 
-  // 2. segment heads (blocked: thread owns entries tid*8 .. tid*8+7)
+  // 2. segment heads over the tile's own entries (blocked, 8 per thread)
   bool head[kCooItems];
   int nh = 0;
 #pragma unroll
   for (int i = 0; i < kCooItems; ++i) {
     const int k = tid * kCooItems + i;
-    head[i] = k < cnt && (k == 0 || s_row[k] != s_row[k - 1]);
+    head[i] = k < cnt_in && (k == 0 || rows[k] != rows[k - 1]);
     nh += head[i];
   }
   int off = 0, total = 0;
   BlockScan(scan_tmp).ExclusiveSum(nh, off, total);
   {
-    int cur = off - 1;
+    int cur = off;
 #pragma unroll
-    for (int i = 0; i < kCooItems; ++i) {
-      const int k = tid * kCooItems + i;
-      if (head[i]) {
-        ++cur;
-        s_start[cur] = uint16_t(k);
-      }
-      if (k < cnt) s_seg[k] = uint16_t(cur);
-    }
+    for (int i = 0; i < kCooItems; ++i)
+      if (head[i]) s_start[cur++] = uint16_t(tid * kCooItems + i);
   }
   if (tid == 0) {
-    s_nseg = total;
-    s_start[total] = uint16_t(cnt);  // cnt <= 2048 fits
+    *s_nseg = total;
+    *s_nlong = 0;
+    s_start[total] = uint16_t(cnt_in);
+    P.head_row[t] = kNoRow;
+    P.tail_row[t] = kNoRow;
+    P.pass[t] = 0;
   }
   __syncthreads();
-  const int nseg = s_nseg;
+  const int nseg = *s_nseg;
 
-  // 3. classify segments; zero-fill empty rows before each row start
-  for (int s = tid; s < nseg; s += kCooThreads) {
+  // 3. one thread per segment: short owned rows summed left to right from
+  //    +0.0 (np.add.at order); long ones queued; empty rows zero-filled.
+  for (int s = tid; s < nseg; s += kTileThreads) {
     const int k0 = s_start[s], k1 = s_start[s + 1];
-    const uint32_t r = s_row[k0];
-    const bool cont_before = (k0 == 0) && base > 0 && s_prev[31] == r;
+    const uint32_t r = rows[k0];
+    const bool cont_before = (k0 == 0) && rows[-1] == r;
     int before = 0, after = 0;
     if (cont_before)
-      while (before < 32 && s_prev[31 - before] == r) ++before;
-    if (k1 == cnt && base + cnt < nnz)
-      while (after < 32 && s_next[after] == r) ++after;
+      while (before < kExt && rows[-1 - before] == r) ++before;
+    if (k1 == cnt_in)
+      while (after < kExt && rows[cnt_in + after] == r) ++after;
     const int n = before + (k1 - k0) + after;
-    const bool is_long = before == 32 || after == 32 || n > kExactLen;
-    s_owned[s] = (!is_long && !cont_before) ? 1 : 0;
+    const bool is_long = before == kExt || after == kExt || n > kExactLen;
     if (!cont_before) {
-      const int64_t prev = k0 > 0 ? int64_t(s_row[k0 - 1]) : (base > 0 ? int64_t(s_prev[31]) : int64_t(-1));
-      for (int64_t q = prev + 1; q < int64_t(r); ++q) y[q] = T(0);
+      const int64_t prev = k0 > 0 ? int64_t(rows[k0 - 1]) : (E0 > 0 ? int64_t(rows[-1]) : int64_t(-1));
+      for (int64_t q = prev + 1; q < int64_t(r); ++q) P.y[q] = T(0);
     }
-    if (k1 == cnt && base + cnt == nnz)
-      for (int64_t q = int64_t(r) + 1; q < nrows; ++q) y[q] = T(0);
+    if (k1 == cnt_in && E0 + cnt_in == P.nnz)
+      for (int64_t q = int64_t(r) + 1; q < P.nrows; ++q) P.y[q] = T(0);
+    if (is_long) {
+      const int idx = atomicAdd(s_nlong, 1);
+      LongSeg L;
+      L.row = r;
+      L.lo = uint32_t(k0);
+      L.hi = uint32_t(k1);
+      L.flags = (cont_before ? 1u : 0u) | ((after > 0) ? 2u : 0u);
+      L.s = L.e = 0;
+      s_long[idx] = L;
+    } else if (!cont_before) {
+      T acc = T(0);
+      const int kend = k1 + after;
+      for (int k = k0; k < kend; ++k) acc = add_rn(acc, vals[k]);
+      P.y[r] = acc;
+    }
   }
   __syncthreads();
 
-  // 4. products of owned entries (striped, coalesced, 4 in flight)
-  {
-    int k = tid;
-    for (; k + 3 * kCooThreads < cnt; k += 4 * kCooThreads) {
-      const bool o0 = s_owned[s_seg[k]], o1 = s_owned[s_seg[k + kCooThreads]];
-      const bool o2 = s_owned[s_seg[k + 2 * kCooThreads]], o3 = s_owned[s_seg[k + 3 * kCooThreads]];
-      T v0 = T(0), v1 = T(0), v2 = T(0), v3 = T(0);
-      uint32_t c0 = 0, c1 = 0, c2 = 0, c3 = 0;
-      if (o0) { c0 = ld_stream(aj + base + k); v0 = ld_stream(av + base + k); }
-      if (o1) { c1 = ld_stream(aj + base + k + kCooThreads); v1 = ld_stream(av + base + k + kCooThreads); }
-      if (o2) { c2 = ld_stream(aj + base + k + 2 * kCooThreads); v2 = ld_stream(av + base + k + 2 * kCooThreads); }
-      if (o3) { c3 = ld_stream(aj + base + k + 3 * kCooThreads); v3 = ld_stream(av + base + k + 3 * kCooThreads); }
-      if (o0) s_prod[k] = mul_rn(v0, __ldg(xb + c0));
-      if (o1) s_prod[k + kCooThreads] = mul_rn(v1, __ldg(xb + c1));
-      if (o2) s_prod[k + 2 * kCooThreads] = mul_rn(v2, __ldg(xb + c2));
-      if (o3) s_prod[k + 3 * kCooThreads] = mul_rn(v3, __ldg(xb + c3));
-    }
-    for (; k < cnt; k += kCooThreads)
-      if (s_owned[s_seg[k]]) s_prod[k] = mul_rn(ld_stream(av + base + k), __ldg(xb + ld_stream(aj + base + k)));
-  }
-  __syncthreads();
-
-  // 5. one thread per owned row: left-to-right sum from +0.0
-  for (int s = tid; s < nseg; s += kCooThreads) {
-    if (!s_owned[s]) continue;
-    const int k0 = s_start[s], k1 = s_start[s + 1];
-    const uint32_t r = s_row[k0];
-    T acc = T(0);
-    for (int k = k0; k < k1; ++k) acc = add_rn(acc, s_prod[k]);
-    if (k1 == cnt) {
-      for (int j = 0; j < 32 && s_next[j] == r; ++j) {
-        const int64_t g = base + cnt + j;
-        acc = add_rn(acc, mul_rn(av[g], __ldg(xb + aj[g])));
+  // 4. long segments: one warp each (vla-32 order); cross-tile parts go to
+  //    the carry slots for coo_fixup_kernel.
+  const int nl = *s_nlong;
+  for (int i = warp; i < nl; i += kTileThreads / 32) {
+    const LongSeg L = s_long[i];
+    const T part = warp_segment_sum(vals, L.lo, L.hi, lane);
+    if (lane == 0) {
+      const bool cb = L.flags & 1u, ca = L.flags & 2u;
+      if (!cb && !ca) {
+        P.y[L.row] = part;
+      } else if (cb) {
+        P.head_row[t] = L.row;
+        P.head_val[t] = part;
+        P.pass[t] = ca ? 1u : 0u;
+      } else {
+        P.tail_row[t] = L.row;
+        P.tail_val[t] = part;
       }
     }
-    y[r] = acc;
+  }
+}
+
+template <typename T, bool BULK>
+__global__ void __launch_bounds__(kTileThreads)
+coo_tile_kernel(const CooParams<T> P) {
+  using BlockScan = cub::BlockScan<int, kTileThreads>;
+  __shared__ typename BlockScan::TempStorage scan_tmp;
+  extern __shared__ __align__(128) unsigned char smem[];
+  using S = CooSmem<T>;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  int* s_nseg = reinterpret_cast<int*>(smem + 32);
+  int* s_nlong = reinterpret_cast<int*>(smem + 36);
+  uint16_t* s_start = reinterpret_cast<uint16_t*>(smem + 128);
+  LongSeg* s_long = reinterpret_cast<LongSeg*>(smem + 128 + S::starts_bytes);
+  unsigned char* stages = smem + S::header;
+  const int tid = threadIdx.x;
+  auto rows_of = [&](int s) { return reinterpret_cast<uint32_t*>(stages + s * S::stage_bytes); };
+  auto cols_of = [&](int s) { return reinterpret_cast<uint32_t*>(stages + s * S::stage_bytes + S::rows_bytes); };
+  auto vals_of = [&](int s) {
+    return reinterpret_cast<T*>(stages + s * S::stage_bytes + S::rows_bytes + S::cols_bytes);
+  };
+  // Row slots the copy did not fill: the window before tile 0 and past nnz.
+  auto pad_rows = [&](uint32_t* rb, int64_t t) {
+    const int64_t E0 = t * kTile;
+    const int cnt_ext = int(min(int64_t(kTile + kExt), P.nnz - E0));
+    if (t == 0)
+      for (int k = tid; k < kExt; k += kTileThreads) rb[k] = kNoRow;
+    for (int k = cnt_ext + tid; k < kTile + kExt; k += kTileThreads) rb[kExt + k] = kNoRow;
+  };
+
+  int64_t n_bulk = BULK ? P.n_bulk : 0;
+  if (BULK) {
+    if (tid == 0) {
+      for (int s = 0; s < kTileStages; ++s) mbar_init(&bars[s], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t first = blockIdx.x, stride = gridDim.x;
+    const int64_t mine = first < n_bulk ? (n_bulk - 1 - first) / stride + 1 : 0;
+    auto issue = [&](int64_t i) {
+      const int64_t t = first + i * stride;
+      const int64_t E0 = t * kTile;
+      const uint32_t cnt = uint32_t(min(int64_t(kTile + kExt), P.nnz - E0));
+      const uint32_t pre = t > 0 ? uint32_t(kExt) : 0u;
+      const int s = int(i % kTileStages);
+      mbar_arrive_expect_tx(&bars[s], (cnt + pre) * 4u + cnt * (4u + uint32_t(sizeof(T))));
+      bulk_g2s(rows_of(s) + (kExt - pre), P.ai + E0 - pre, (cnt + pre) * 4u, &bars[s]);
+      bulk_g2s(cols_of(s), P.aj + E0, cnt * 4u, &bars[s]);
+      bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s]);
+    };
+    if (tid == 0)
+      for (int64_t i = 0; i < kTileStages && i < mine; ++i) issue(i);
+    for (int64_t i = 0; i < mine; ++i) {
+      const int s = int(i % kTileStages);
+      const int64_t t = first + i * stride;
+      mbar_wait(&bars[s], uint32_t((i / kTileStages) & 1));
+      pad_rows(rows_of(s), t);
+      __syncthreads();
+      coo_process_tile<T>(P, t, rows_of(s) + kExt, cols_of(s), vals_of(s), s_start, s_long, s_nseg, s_nlong,
+                          &scan_tmp);
+      __syncthreads();
+      if (tid == 0 && i + kTileStages < mine) {
+        fence_proxy_async();
+        issue(i + kTileStages);
+      }
+    }
+  }
+  for (int64_t t = n_bulk + blockIdx.x; t < P.ntiles; t += gridDim.x) {
+    const int64_t E0 = t * kTile;
+    const int cnt = int(min(int64_t(kTile + kExt), P.nnz - E0));
+    uint32_t* rb = rows_of(0);
+    uint32_t* c = cols_of(0);
+    T* v = vals_of(0);
+    for (int k = tid - kExt; k < cnt; k += kTileThreads) {
+      const int64_t g = E0 + k;
+      if (g >= 0) rb[kExt + k] = P.ai[g];
+      if (k >= 0) {
+        c[k] = P.aj[g];
+        v[k] = P.av[g];
+      }
+    }
+    pad_rows(rb, t);
+    __syncthreads();
+    coo_process_tile<T>(P, t, rb + kExt, c, v, s_start, s_long, s_nseg, s_nlong, &scan_tmp);
+    __syncthreads();
+  }
+}
+
+// Cross-tile long rows: walk from the tile where the row starts (its tail
+// slot) through the following tiles' head slots, adding in tile order.
+template <typename T>
+__global__ void coo_fixup_kernel(const CooParams<T> P) {
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t < P.ntiles;
+       t += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t r = P.tail_row[t];
+    if (r == kNoRow) continue;
+    T acc = P.tail_val[t];
+    for (int64_t u = t + 1; u < P.ntiles && P.head_row[u] == r; ++u) {
+      acc = add_rn(acc, P.head_val[u]);
+      if (!P.pass[u]) break;
+    }
+    P.y[r] = acc;
   }
 }
 
@@ -281,10 +411,36 @@ struct spmv_coo_plan {
   bool row_sorted = true;
   DevBuf sorted_ai, sorted_aj, sorted_av;  // only when the input rows were unsorted
   DevBuf run_start, run_row;
-  int64_t n_runs = 0;
-  LongRows longrows;
+  int64_t n_runs = 0, n_long = 0, ntiles = 0;
+  DevBuf head_row, tail_row, pass, head_val, tail_val;
   DevBuf steps;
+  int grid = 0;
 };
+
+__global__ void count_long_runs_kernel(const uint32_t* __restrict__ run_start, int64_t n_runs,
+                                       unsigned long long* __restrict__ n_long) {
+  unsigned long long c = 0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_runs; i += int64_t(gridDim.x) * blockDim.x)
+    c += (run_start[i + 1] - run_start[i]) > uint32_t(kExactLen);
+  for (int o = 16; o >= 1; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(n_long, c);
+}
+
+template <typename T>
+static int coo_launch_config(spmv_coo_plan* p) {
+  using S = CooSmem<T>;
+  SPMV_CUDA_TRY(cudaFuncSetAttribute(coo_tile_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(S::total)));
+  SPMV_CUDA_TRY(cudaFuncSetAttribute(coo_tile_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(S::total)));
+  int per_sm = 0;
+  SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coo_tile_kernel<T, true>, kTileThreads,
+                                                              S::total));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = int64_t(sm_count()) * per_sm;
+  p->grid = int(p->ntiles < cap ? p->ntiles : cap);
+  return SPMV_OK;
+}
 
 static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const void* av,
                           cudaStream_t st) {
@@ -356,8 +512,23 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
   const uint32_t nnz32 = uint32_t(nnz);
   SPMV_CUDA_TRY(cudaMemcpyAsync(p->run_start.as<uint32_t>() + p->n_runs, &nnz32, 4, cudaMemcpyHostToDevice, st));
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
-  return p->longrows.build(p->run_start.as<uint32_t>(), p->run_row.as<uint32_t>(), p->n_runs, kExactLen,
-                           value_size(p->dtype), st);
+  DevBuf nl;
+  if ((rc = nl.alloc(8))) return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(nl.ptr, 0, 8, st));
+  count_long_runs_kernel<<<unsigned(std::min<int64_t>((p->n_runs + 255) / 256, int64_t(sm_count()) * 16)), 256, 0,
+                           st>>>(p->run_start.as<uint32_t>(), p->n_runs, nl.as<unsigned long long>());
+  SPMV_LAUNCH_CHECK();
+  unsigned long long h = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&h, nl.ptr, 8, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  p->n_long = int64_t(h);
+  p->ntiles = (nnz + kTile - 1) / kTile;
+  const size_t vs = value_size(p->dtype);
+  if ((rc = p->head_row.alloc(4 * p->ntiles)) || (rc = p->tail_row.alloc(4 * p->ntiles)) ||
+      (rc = p->pass.alloc(4 * p->ntiles)) || (rc = p->head_val.alloc(vs * p->ntiles)) ||
+      (rc = p->tail_val.alloc(vs * p->ntiles)))
+    return rc;
+  return p->dtype == SPMV_F64 ? coo_launch_config<double>(p) : coo_launch_config<float>(p);
 }
 
 template <typename T>
@@ -373,10 +544,36 @@ static int coo_run(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* a
     aj = p->sorted_aj.as<uint32_t>();
     av = p->sorted_av.as<T>();
   }
-  const int64_t tiles = (p->nnz + kCooTile - 1) / kCooTile;
-  coo_tile_kernel<T><<<unsigned(tiles), kCooThreads, 0, st>>>(ai, aj, av, x, col_base, y, p->nnz, p->nrows);
+  CooParams<T> P;
+  P.ai = ai;
+  P.aj = aj;
+  P.av = av;
+  P.x = x;
+  P.y = y;
+  P.head_row = p->head_row.as<uint32_t>();
+  P.tail_row = p->tail_row.as<uint32_t>();
+  P.pass = p->pass.as<uint32_t>();
+  P.head_val = p->head_val.as<T>();
+  P.tail_val = p->tail_val.as<T>();
+  P.nrows = p->nrows;
+  P.nnz = p->nnz;
+  P.col_base = col_base;
+  P.ntiles = p->ntiles;
+  const bool aligned = (reinterpret_cast<uintptr_t>(ai) % 16 == 0) && (reinterpret_cast<uintptr_t>(aj) % 16 == 0) &&
+                       (reinterpret_cast<uintptr_t>(av) % 16 == 0);
+  P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles) : 0;
+  const size_t smem = CooSmem<T>::total;
+  if (aligned)
+    coo_tile_kernel<T, true><<<unsigned(p->grid), kTileThreads, smem, st>>>(P);
+  else
+    coo_tile_kernel<T, false><<<unsigned(p->grid), kTileThreads, smem, st>>>(P);
   SPMV_LAUNCH_CHECK();
-  return p->longrows.launch<T>(aj, av, x, col_base, y, st);
+  if (p->n_long > 0) {
+    const int64_t g = std::min<int64_t>((p->ntiles + 255) / 256, int64_t(sm_count()) * 8);
+    coo_fixup_kernel<T><<<unsigned(g), 256, 0, st>>>(P);
+    SPMV_LAUNCH_CHECK();
+  }
+  return SPMV_OK;
 }
 
 extern "C" {
@@ -414,10 +611,10 @@ int spmv_coo_plan_info(const spmv_coo_plan* p, int64_t* n_runs, int64_t* n_long_
                        int* row_sorted, int64_t* launches) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (n_runs) *n_runs = p->n_runs;
-  if (n_long_runs) *n_long_runs = p->longrows.n_long;
-  if (n_items) *n_items = p->longrows.n_items;
+  if (n_long_runs) *n_long_runs = p->n_long;
+  if (n_items) *n_items = p->ntiles;
   if (row_sorted) *row_sorted = p->row_sorted ? 1 : 0;
-  if (launches) *launches = (p->nrows > 0 ? 1 : 0) + (p->longrows.n_items > 0 ? 1 : 0);
+  if (launches) *launches = (p->nrows > 0 ? 1 : 0) + (p->n_long > 0 ? 1 : 0);
   return SPMV_OK;
 }
 

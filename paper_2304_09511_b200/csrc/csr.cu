@@ -4,77 +4,237 @@
 // to right after rounding every product; spmv_csr_vla (kernels.py:143-171)
 // uses L strided lane accumulators and a pairwise tree (lanes.py:107-128).
 //
-// Plain path = CSR-Adaptive style binning decided once in the plan:
-//   * csr_stream_kernel: 128 consecutive rows per CTA.  When every row of
-//     the group has <= exact_len entries (the stencil case) the group's
-//     contiguous nnz range is streamed with coalesced loads, products are
-//     formed in parallel into shared memory, and each thread then sums its
-//     row from shared memory left to right — the reference order, so the
-//     result is bit-exact.  Groups that contain long rows sum their short
-//     rows per thread straight from global memory (still left to right) and
-//     skip the long rows.
-//   * long_rows_kernel (longrow.cuh): warp chunks for rows > exact_len.
-#include "longrow.cuh"
+// Plain path — csr_tile_kernel, persistent, TMA-fed (tile.cuh):
+//   1. a producer thread bulk-copies the tile's column indices and values
+//      (kTile + kExt entries) into a STAGES-deep shared-memory ring;
+//   2. all threads form the rounded products in place (x gathered through
+//      L1/L2; x is the only irregular stream);
+//   3. rows that start in the tile with <= exact_len entries (all stencil
+//      rows) are summed left to right by one thread from shared memory —
+//      the reference order, so bit-exact; empty rows get +0.0;
+//   4. longer rows: one warp per in-tile segment (vla-32 order, so a long
+//      row inside one tile is bit-exact with spmv_csr_vla(32)); a row that
+//      spans tiles leaves one partial per tile and the last tile to finish
+//      (atomic ticket, no spinning) adds them in tile order — deterministic,
+//      within 1e-12 of the reference.
+// Every stored entry is read from HBM exactly once (+kExt/kTile = 1.6%
+// overlap that hits L2), the row pointers once, x through L2, y written
+// once: the minimum-byte model of SURVEY.md §8(d).
+#include <algorithm>
+
+#include "tile.cuh"
 
 namespace spmv {
 
-constexpr int kGroupRows = 128;        // rows per CTA = threads per CTA
-constexpr int kStreamCap = kGroupRows * kExactLen;  // staged products per CTA
+template <typename T>
+struct CsrParams {
+  const uint32_t* irp;
+  const uint32_t* aj;
+  const T* av;
+  const T* x;
+  T* y;
+  const uint32_t* row_lo;  // ntiles + 1: first row of each tile's row range
+  T* head;
+  T* tail;
+  uint32_t* cnt;
+  int64_t nrows, nnz, col_base, ntiles, n_bulk;
+  int exact_len;
+};
 
 template <typename T>
-__global__ void __launch_bounds__(kGroupRows)
-csr_stream_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj,
-                  const T* __restrict__ av, const T* __restrict__ x, int64_t col_base,
-                  T* __restrict__ y, int64_t nrows, int exact_len) {
-  __shared__ T prod[kStreamCap];
-  const T* xb = x - col_base;
-  const int tid = threadIdx.x;
-  const int64_t r0 = int64_t(blockIdx.x) * kGroupRows;
-  const int64_t r = r0 + tid;
-  const int64_t rend = min(r0 + kGroupRows, nrows);
+struct CsrSmem {
+  static constexpr size_t cols_bytes = align_up(sizeof(uint32_t) * (kTile + kExt), 128);
+  static constexpr size_t vals_bytes = align_up(sizeof(T) * (kTile + kExt), 128);
+  static constexpr size_t stage_bytes = cols_bytes + vals_bytes;
+  static constexpr size_t header = align_up(64 + sizeof(LongSeg) * kMaxLongSegs, 128);
+  static constexpr size_t total = header + kTileStages * stage_bytes;
+};
+
+template <typename T>
+__device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_t* __restrict__ cols,
+                                 T* __restrict__ vals, LongSeg* s_long, int* s_nlong) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int64_t E0 = t * kTile;
+  const int cnt_ext = int(min(int64_t(kTile + kExt), P.nnz - E0));
+  const int64_t E1 = E0 + kTile;
+  const T* xb = P.x - P.col_base;
+
+  // Row range of the tile; prefetch the first row's pointers before the
+  // product phase so their latency overlaps it.
+  const int64_t R0 = t == 0 ? 0 : int64_t(P.row_lo[t]);
+  const int64_t R1 = P.row_lo[t + 1];
+  const int64_t rend = R1 < P.nrows ? R1 + 1 : P.nrows;
+  int64_t r = R0 + tid;
   uint32_t s = 0, e = 0;
-  if (r < nrows) {
-    s = irp[r];
-    e = irp[r + 1];
+  if (r < rend) {
+    s = __ldg(P.irp + r);
+    e = __ldg(P.irp + r + 1);
   }
-  const uint32_t len = e - s;
-  const bool is_short = len <= uint32_t(exact_len);
-  const uint32_t j0 = irp[r0];
-  const uint32_t j1 = irp[rend];
-  const uint32_t total = j1 - j0;
-  const bool pure = __syncthreads_and(is_short) && total <= uint32_t(kStreamCap);
-  if (pure) {
-    // Coalesced stream of the group's [j0, j1): 4 products in flight/thread.
-    uint32_t k = tid;
-    for (; k + 3 * kGroupRows < total; k += 4 * kGroupRows) {
-      const uint32_t c0 = ld_stream(aj + j0 + k), c1 = ld_stream(aj + j0 + k + kGroupRows);
-      const uint32_t c2 = ld_stream(aj + j0 + k + 2 * kGroupRows), c3 = ld_stream(aj + j0 + k + 3 * kGroupRows);
-      const T v0 = ld_stream(av + j0 + k), v1 = ld_stream(av + j0 + k + kGroupRows);
-      const T v2 = ld_stream(av + j0 + k + 2 * kGroupRows), v3 = ld_stream(av + j0 + k + 3 * kGroupRows);
-      prod[k] = mul_rn(v0, __ldg(xb + c0));
-      prod[k + kGroupRows] = mul_rn(v1, __ldg(xb + c1));
-      prod[k + 2 * kGroupRows] = mul_rn(v2, __ldg(xb + c2));
-      prod[k + 3 * kGroupRows] = mul_rn(v3, __ldg(xb + c3));
+
+  // Products in place, 4 independent gathers in flight per thread.
+  {
+    int k = tid;
+    for (; k + 3 * kTileThreads < cnt_ext; k += 4 * kTileThreads) {
+      const uint32_t c0 = cols[k], c1 = cols[k + kTileThreads], c2 = cols[k + 2 * kTileThreads],
+                     c3 = cols[k + 3 * kTileThreads];
+      const T x0 = __ldg(xb + c0), x1 = __ldg(xb + c1), x2 = __ldg(xb + c2), x3 = __ldg(xb + c3);
+      vals[k] = mul_rn(vals[k], x0);
+      vals[k + kTileThreads] = mul_rn(vals[k + kTileThreads], x1);
+      vals[k + 2 * kTileThreads] = mul_rn(vals[k + 2 * kTileThreads], x2);
+      vals[k + 3 * kTileThreads] = mul_rn(vals[k + 3 * kTileThreads], x3);
     }
-    for (; k < total; k += kGroupRows) prod[k] = mul_rn(ld_stream(av + j0 + k), __ldg(xb + ld_stream(aj + j0 + k)));
-    __syncthreads();
-    if (r < nrows) {
-      T acc = T(0);
-      if (len) {
-        const T* p = prod + (s - j0);
-        acc = p[0];  // cumsum starts from the first product (keeps -0.0)
+    for (; k < cnt_ext; k += kTileThreads) vals[k] = mul_rn(vals[k], __ldg(xb + cols[k]));
+  }
+  if (tid == 0) *s_nlong = 0;
+  __syncthreads();
+
+  // Rows: short ones summed here, long segments queued for the warps.
+  while (r < rend) {
+    const uint32_t len = e - s;
+    if (len == 0) {
+      if (r < R1) P.y[r] = T(0);
+    } else if (len <= uint32_t(P.exact_len)) {
+      if (int64_t(s) >= E0 && int64_t(s) < E1) {
+        const T* p = vals + (s - E0);
+        T acc = p[0];  // cumsum starts from the first product (keeps -0.0)
         for (uint32_t i = 1; i < len; ++i) acc = add_rn(acc, p[i]);
+        P.y[r] = acc;
       }
-      y[r] = acc;
+    } else {
+      const int64_t lo = max(int64_t(s), E0), hi = min(int64_t(e), E1);
+      if (lo < hi) {
+        const int idx = atomicAdd(s_nlong, 1);
+        LongSeg L;
+        L.row = uint32_t(r);
+        L.lo = uint32_t(lo - E0);
+        L.hi = uint32_t(hi - E0);
+        L.flags = 0;
+        L.s = s;
+        L.e = e;
+        s_long[idx] = L;
+      }
     }
-  } else if (r < nrows && is_short) {
-    T acc = T(0);
-    if (len) {
-      acc = mul_rn(ld_stream(av + s), __ldg(xb + ld_stream(aj + s)));
-      for (uint32_t j = s + 1; j < e; ++j) acc = add_rn(acc, mul_rn(ld_stream(av + j), __ldg(xb + ld_stream(aj + j))));
+    r += kTileThreads;
+    if (r < rend) {
+      s = __ldg(P.irp + r);
+      e = __ldg(P.irp + r + 1);
     }
-    y[r] = acc;
   }
+  __syncthreads();
+
+  const int nl = *s_nlong;
+  for (int i = warp; i < nl; i += kTileThreads / 32) {
+    const LongSeg L = s_long[i];
+    const T part = warp_segment_sum(vals, L.lo, L.hi, lane);
+    if (lane == 0) {
+      if (int64_t(L.s) >= E0 && int64_t(L.e) <= E1) {
+        P.y[L.row] = part;
+      } else {
+        const int64_t t0 = L.s / kTile, t1 = (int64_t(L.e) - 1) / kTile;
+        if (t == t0)
+          P.tail[t] = part;
+        else
+          P.head[t] = part;
+        __threadfence();
+        const uint32_t ticket = atomicAdd(P.cnt + t0, 1u);
+        if (ticket == uint32_t(t1 - t0)) {
+          __threadfence();
+          T sum = __ldcg(P.tail + t0);
+          for (int64_t u = t0 + 1; u <= t1; ++u) sum = add_rn(sum, __ldcg(P.head + u));
+          P.y[L.row] = sum;
+          P.cnt[t0] = 0;  // ready for the next product
+        }
+      }
+    }
+  }
+}
+
+template <typename T, bool BULK>
+__global__ void __launch_bounds__(kTileThreads)
+csr_tile_kernel(const CsrParams<T> P) {
+  extern __shared__ __align__(128) unsigned char smem[];
+  using S = CsrSmem<T>;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  int* s_nlong = reinterpret_cast<int*>(smem + 32);
+  LongSeg* s_long = reinterpret_cast<LongSeg*>(smem + 64);
+  unsigned char* stages = smem + S::header;
+  const int tid = threadIdx.x;
+  auto cols_of = [&](int s) { return reinterpret_cast<uint32_t*>(stages + s * S::stage_bytes); };
+  auto vals_of = [&](int s) { return reinterpret_cast<T*>(stages + s * S::stage_bytes + S::cols_bytes); };
+
+  int64_t n_bulk = BULK ? P.n_bulk : 0;
+  if (BULK) {
+    if (tid == 0) {
+      for (int s = 0; s < kTileStages; ++s) mbar_init(&bars[s], 1);
+      mbar_fence_init();
+    }
+    __syncthreads();
+    const int64_t first = blockIdx.x, stride = gridDim.x;
+    const int64_t mine = first < n_bulk ? (n_bulk - 1 - first) / stride + 1 : 0;
+    auto issue = [&](int64_t i) {
+      const int64_t t = first + i * stride;
+      const int64_t E0 = t * kTile;
+      const uint32_t cnt = uint32_t(min(int64_t(kTile + kExt), P.nnz - E0));
+      const int s = int(i % kTileStages);
+      mbar_arrive_expect_tx(&bars[s], cnt * uint32_t(sizeof(uint32_t) + sizeof(T)));
+      bulk_g2s(cols_of(s), P.aj + E0, cnt * uint32_t(sizeof(uint32_t)), &bars[s]);
+      bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s]);
+    };
+    if (tid == 0)
+      for (int64_t i = 0; i < kTileStages && i < mine; ++i) issue(i);
+    for (int64_t i = 0; i < mine; ++i) {
+      const int s = int(i % kTileStages);
+      mbar_wait(&bars[s], uint32_t((i / kTileStages) & 1));
+      csr_process_tile<T>(P, first + i * stride, cols_of(s), vals_of(s), s_long, s_nlong);
+      __syncthreads();
+      if (tid == 0 && i + kTileStages < mine) {
+        fence_proxy_async();
+        issue(i + kTileStages);
+      }
+    }
+  }
+  // Tiles the bulk engine cannot address: cooperative loads into stage 0.
+  for (int64_t t = n_bulk + blockIdx.x; t < P.ntiles; t += gridDim.x) {
+    const int64_t E0 = t * kTile;
+    const int cnt = int(min(int64_t(kTile + kExt), P.nnz - E0));
+    uint32_t* c = cols_of(0);
+    T* v = vals_of(0);
+    for (int k = tid; k < cnt; k += kTileThreads) {
+      c[k] = P.aj[E0 + k];
+      v[k] = P.av[E0 + k];
+    }
+    __syncthreads();
+    csr_process_tile<T>(P, t, c, v, s_long, s_nlong);
+    __syncthreads();
+  }
+}
+
+// row_lo[t] = row containing entry t*kTile (last r with irp[r] <= t*kTile);
+// row_lo[ntiles] = nrows.
+__global__ void csr_row_lo_kernel(const uint32_t* __restrict__ irp, int64_t nrows, int64_t ntiles,
+                                  uint32_t* __restrict__ row_lo) {
+  for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t <= ntiles; t += int64_t(gridDim.x) * blockDim.x) {
+    if (t == ntiles) {
+      row_lo[t] = uint32_t(nrows);
+      continue;
+    }
+    const uint64_t key = uint64_t(t) * kTile;
+    int64_t lo = 0, hi = nrows;  // find last r in [0, nrows) with irp[r] <= key
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (uint64_t(irp[mid]) <= key) lo = mid; else hi = mid - 1;
+    }
+    row_lo[t] = uint32_t(lo);
+  }
+}
+
+__global__ void count_long_rows_kernel(const uint32_t* __restrict__ irp, int64_t nrows, int exact_len,
+                                       unsigned long long* __restrict__ n_long) {
+  unsigned long long c = 0;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += int64_t(gridDim.x) * blockDim.x)
+    c += (irp[r + 1] - irp[r]) > uint32_t(exact_len);
+  for (int o = 16; o >= 1; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(n_long, c);
 }
 
 // ---- vla: sub-warp (L <= 32) or CTA (32 < L <= 1024) per row ------------
@@ -141,19 +301,62 @@ using namespace spmv;
 
 struct spmv_csr_plan {
   int dtype = SPMV_F64;
-  int64_t nrows = 0, ncols = 0, nnz = 0;
+  int64_t nrows = 0, ncols = 0, nnz = 0, ntiles = 0;
   int exact_len = kExactLen;
-  LongRows longrows;
+  int64_t n_long = 0;
+  DevBuf row_lo, head, tail, cnt;
+  int grid_bulk = 0, grid_direct = 0;
 };
+
+template <typename T>
+static int csr_launch_config(spmv_csr_plan* p) {
+  using S = CsrSmem<T>;
+  SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_tile_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(S::total)));
+  SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_tile_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                     int(S::total)));
+  int per_sm = 0;
+  SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_tile_kernel<T, true>, kTileThreads,
+                                                              S::total));
+  if (per_sm < 1) per_sm = 1;
+  const int64_t cap = int64_t(sm_count()) * per_sm;
+  p->grid_bulk = int(p->ntiles < cap ? p->ntiles : cap);
+  p->grid_direct = p->grid_bulk;
+  return SPMV_OK;
+}
 
 template <typename T>
 static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st) {
   if (p->nrows == 0) return SPMV_OK;
-  const int64_t groups = (p->nrows + kGroupRows - 1) / kGroupRows;
-  csr_stream_kernel<T><<<unsigned(groups), kGroupRows, 0, st>>>(irp, aj, av, x, col_base, y, p->nrows, p->exact_len);
+  if (p->nnz == 0) {
+    SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
+    return SPMV_OK;
+  }
+  CsrParams<T> P;
+  P.irp = irp;
+  P.aj = aj;
+  P.av = av;
+  P.x = x;
+  P.y = y;
+  P.row_lo = p->row_lo.as<uint32_t>();
+  P.head = p->head.as<T>();
+  P.tail = p->tail.as<T>();
+  P.cnt = p->cnt.as<uint32_t>();
+  P.nrows = p->nrows;
+  P.nnz = p->nnz;
+  P.col_base = col_base;
+  P.ntiles = p->ntiles;
+  P.exact_len = p->exact_len;
+  const bool aligned = (reinterpret_cast<uintptr_t>(aj) % 16 == 0) && (reinterpret_cast<uintptr_t>(av) % 16 == 0);
+  P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles) : 0;
+  const size_t smem = CsrSmem<T>::total;
+  if (aligned)
+    csr_tile_kernel<T, true><<<unsigned(p->grid_bulk), kTileThreads, smem, st>>>(P);
+  else
+    csr_tile_kernel<T, false><<<unsigned(p->grid_direct), kTileThreads, smem, st>>>(P);
   SPMV_LAUNCH_CHECK();
-  return p->longrows.launch<T>(aj, av, x, col_base, y, st);
+  return SPMV_OK;
 }
 
 extern "C" {
@@ -167,15 +370,46 @@ int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, c
     return fail(SPMV_INVALID_ARG, "bad CSR sizes nrows=%lld ncols=%lld nnz=%lld", (long long)nrows,
                 (long long)ncols, (long long)nnz);
   if (!row_pointers) return fail(SPMV_INVALID_ARG, "row_pointers is NULL");
-  if (exact_len <= 0) exact_len = kExactLen;
-  if (exact_len > kExactLen) exact_len = kExactLen;  // stream capacity is sized for 32
+  if (exact_len <= 0 || exact_len > kExactLen) exact_len = kExactLen;  // tile extension covers 32
+  cudaStream_t st = as_stream(stream);
   auto* p = new spmv_csr_plan();
   p->dtype = dtype;
   p->nrows = nrows;
   p->ncols = ncols;
   p->nnz = nnz;
   p->exact_len = exact_len;
-  int rc = p->longrows.build(row_pointers, nullptr, nrows, exact_len, value_size(dtype), as_stream(stream));
+  p->ntiles = (nnz + kTile - 1) / kTile;
+  int rc = SPMV_OK;
+  const size_t vs = value_size(dtype);
+  if (nrows > 0 && nnz > 0) {
+    if (!rc) rc = p->row_lo.alloc(4 * (p->ntiles + 1));
+    if (!rc) rc = p->head.alloc(vs * p->ntiles);
+    if (!rc) rc = p->tail.alloc(vs * p->ntiles);
+    if (!rc) rc = p->cnt.alloc(4 * p->ntiles);
+    DevBuf nl;
+    if (!rc) rc = nl.alloc(8);
+    if (!rc) {
+      cudaError_t e = cudaMemsetAsync(p->cnt.ptr, 0, 4 * p->ntiles, st);
+      if (e == cudaSuccess) e = cudaMemsetAsync(nl.ptr, 0, 8, st);
+      const int64_t g1 = std::min<int64_t>((p->ntiles + 256) / 256, int64_t(sm_count()) * 16);
+      if (e == cudaSuccess) {
+        csr_row_lo_kernel<<<unsigned(g1), 256, 0, st>>>(row_pointers, nrows, p->ntiles, p->row_lo.as<uint32_t>());
+        e = cudaGetLastError();
+      }
+      const int64_t g2 = std::min<int64_t>((nrows + 255) / 256, int64_t(sm_count()) * 16);
+      if (e == cudaSuccess) {
+        count_long_rows_kernel<<<unsigned(g2), 256, 0, st>>>(row_pointers, nrows, exact_len,
+                                                             nl.as<unsigned long long>());
+        e = cudaGetLastError();
+      }
+      unsigned long long h = 0;
+      if (e == cudaSuccess) e = cudaMemcpyAsync(&h, nl.ptr, 8, cudaMemcpyDeviceToHost, st);
+      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
+      if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "CSR plan: %s", cudaGetErrorString(e));
+      p->n_long = int64_t(h);
+    }
+    if (!rc) rc = dtype == SPMV_F64 ? csr_launch_config<double>(p) : csr_launch_config<float>(p);
+  }
   if (rc) {
     delete p;
     return rc;
@@ -191,9 +425,9 @@ int spmv_csr_plan_destroy(spmv_csr_plan* plan) {
 
 int spmv_csr_plan_info(const spmv_csr_plan* p, int64_t* n_long_rows, int64_t* n_items, int64_t* launches) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
-  if (n_long_rows) *n_long_rows = p->longrows.n_long;
-  if (n_items) *n_items = p->longrows.n_items;
-  if (launches) *launches = (p->nrows > 0 ? 1 : 0) + (p->longrows.n_items > 0 ? 1 : 0);
+  if (n_long_rows) *n_long_rows = p->n_long;
+  if (n_items) *n_items = p->ntiles;
+  if (launches) *launches = p->nrows > 0 ? 1 : 0;
   return SPMV_OK;
 }
 

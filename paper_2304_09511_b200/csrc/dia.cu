@@ -16,61 +16,45 @@
 // ndiags, odd strides are bank-conflict free for 8-byte words) and gathers
 // x through L1: the x window of a tile is re-read by every diagonal with
 // the same (dz, dy), so it stays L1/L2 resident.
-#include "common.cuh"
+#include "tma.cuh"
 
 namespace spmv {
 
 constexpr int kDiaThreads = 256;
 constexpr int kMaxSmemOffsets = 2048;
 
-__device__ __forceinline__ uint32_t smem_u32(const void* p) {
-  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
-}
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
-}
-
-__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t* bar, uint32_t bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes)
-               : "memory");
-}
-
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
-  asm volatile(
-      "{\n"
-      ".reg .pred P1;\n"
-      "WAIT_%=:\n"
-      "mbarrier.try_wait.parity.shared::cta.b64 P1, [%0], %1;\n"
-      "@!P1 bra WAIT_%=;\n"
-      "}\n" ::"r"(smem_u32(bar)),
-      "r"(parity)
-      : "memory");
-}
-
-__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
-  asm volatile(
-      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
-          smem_u32(dst)),
-      "l"(src), "r"(bytes), "r"(smem_u32(bar))
-      : "memory");
-}
-
-template <typename T>
+// One row: ascending diagonals, in-bounds cells only, from +0.0.  With ND
+// known at compile time all ND x-gathers are issued before the first add
+// (one L2 round trip per row instead of ND).
+template <typename T, int ND>
 __device__ __forceinline__ T dia_row(const T* __restrict__ v, const int32_t* __restrict__ offs, int nd, int64_t grow,
                                      int64_t ncols, const T* __restrict__ xb) {
   T acc = T(0);
+  if constexpr (ND > 0) {
+    T xv[ND];
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      const int64_t col = grow + offs[d];
+      xv[d] = (col >= 0 && col < ncols) ? __ldg(xb + col) : T(0);
+    }
+#pragma unroll
+    for (int d = 0; d < ND; ++d) {
+      const int64_t col = grow + offs[d];
+      if (col >= 0 && col < ncols) acc = add_rn(acc, mul_rn(v[d], xv[d]));
+    }
+  } else {
 #pragma unroll 9
-  for (int d = 0; d < nd; ++d) {
-    const int64_t col = grow + offs[d];
-    if (col >= 0 && col < ncols) acc = add_rn(acc, mul_rn(v[d], __ldg(xb + col)));
+    for (int d = 0; d < nd; ++d) {
+      const int64_t col = grow + offs[d];
+      if (col >= 0 && col < ncols) acc = add_rn(acc, mul_rn(v[d], __ldg(xb + col)));
+    }
   }
   return acc;
 }
 
 // Persistent TMA-pipelined kernel.  Tile t covers local rows
 // [t*R, t*R + R) (the last tile is clipped to avail_rows).
-template <typename T, int STAGES>
+template <typename T, int STAGES, int ND>
 __global__ void __launch_bounds__(kDiaThreads)
 dia_bulk_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offsets, int nd, const T* __restrict__ x,
                 T* __restrict__ y, int64_t nrows, int64_t avail_rows, int64_t ncols, int64_t row_base,
@@ -119,7 +103,7 @@ dia_bulk_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offsets,
     int64_t rows = nrows - lr0;
     if (rows > rows_per_tile) rows = rows_per_tile;
     for (int lr = tid; lr < rows; lr += blockDim.x)
-      y[lr0 + lr] = dia_row<T>(tile + size_t(lr) * nd, s_off, nd, row_base + lr0 + lr, ncols, xb);
+      y[lr0 + lr] = dia_row<T, ND>(tile + size_t(lr) * nd, s_off, nd, row_base + lr0 + lr, ncols, xb);
     __syncthreads();  // every thread is done with stage s
     if (tid == 0 && i + STAGES < my_tiles) {
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -178,17 +162,33 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
   if (ctas_per_sm > 4) ctas_per_sm = 4;
   int64_t grid = int64_t(sms) * ctas_per_sm;
   if (grid > ntiles) grid = ntiles;
+  auto launch = [&](auto kernel) -> int {
+    SPMV_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    kernel<<<unsigned(grid), kDiaThreads, smem, st>>>(vals, offsets, int(nd), x, y, nrows, avail_rows, ncols,
+                                                       row_base, col_base, int(R), ntiles, stage_bytes);
+    return SPMV_OK;
+  };
+  int rc;
   if (stages == 2) {
-    SPMV_CUDA_TRY(cudaFuncSetAttribute(dia_bulk_kernel<T, 2>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    dia_bulk_kernel<T, 2><<<unsigned(grid), kDiaThreads, smem, st>>>(vals, offsets, int(nd), x, y, nrows, avail_rows,
-                                                                     ncols, row_base, col_base, int(R), ntiles,
-                                                                     stage_bytes);
+    switch (nd) {
+      case 27: rc = launch(dia_bulk_kernel<T, 2, 27>); break;
+      case 11: rc = launch(dia_bulk_kernel<T, 2, 11>); break;
+      case 7: rc = launch(dia_bulk_kernel<T, 2, 7>); break;
+      case 5: rc = launch(dia_bulk_kernel<T, 2, 5>); break;
+      case 3: rc = launch(dia_bulk_kernel<T, 2, 3>); break;
+      default: rc = launch(dia_bulk_kernel<T, 2, 0>); break;
+    }
   } else {
-    SPMV_CUDA_TRY(cudaFuncSetAttribute(dia_bulk_kernel<T, 3>, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    dia_bulk_kernel<T, 3><<<unsigned(grid), kDiaThreads, smem, st>>>(vals, offsets, int(nd), x, y, nrows, avail_rows,
-                                                                     ncols, row_base, col_base, int(R), ntiles,
-                                                                     stage_bytes);
+    switch (nd) {
+      case 27: rc = launch(dia_bulk_kernel<T, 3, 27>); break;
+      case 11: rc = launch(dia_bulk_kernel<T, 3, 11>); break;
+      case 7: rc = launch(dia_bulk_kernel<T, 3, 7>); break;
+      case 5: rc = launch(dia_bulk_kernel<T, 3, 5>); break;
+      case 3: rc = launch(dia_bulk_kernel<T, 3, 3>); break;
+      default: rc = launch(dia_bulk_kernel<T, 3, 0>); break;
+    }
   }
+  if (rc) return rc;
   SPMV_LAUNCH_CHECK();
   return SPMV_OK;
 }

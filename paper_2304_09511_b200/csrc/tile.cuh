@@ -1,0 +1,49 @@
+// Fixed-size entry tiles shared by the CSR and COO plain kernels.
+//
+// A tile is kTile consecutive stored entries plus a kExt-entry extension
+// (the tail of a short row that starts in the tile), staged into shared
+// memory by TMA bulk copies in a persistent, STAGES-deep pipeline.  Work per
+// tile is independent of the row-length distribution (Zipf rows up to 50k
+// entries), and every entry is read from HBM once.
+#pragma once
+
+#include "tma.cuh"
+
+namespace spmv {
+
+constexpr int kTile = 2048;
+constexpr int kExt = 32;  // == kExactLen: a short row never reaches further
+constexpr int kTileThreads = 256;
+constexpr int kTileStages = 2;
+constexpr int kMaxLongSegs = 160;  // >= kTile/(kExactLen+1) + 2
+constexpr uint32_t kNoRow = 0xffffffffu;
+
+static_assert(kExt == kExactLen, "extension must cover a whole short row");
+
+struct LongSeg {
+  uint32_t row;
+  uint32_t lo, hi;  // entry range inside this tile [lo, hi), tile-relative
+  uint32_t flags;   // CSR: unused; COO: bit0 cont_before, bit1 cont_after
+  uint32_t s, e;    // CSR: the row's global entry range
+};
+
+// Number of tiles whose [E0, E0 + kTile + kExt) window (clamped to nnz) can be
+// bulk-copied without reading past the arrays: all of them when nnz % 4 == 0,
+// otherwise those with E0 + kTile + kExt <= nnz.
+inline int64_t bulk_tiles(int64_t nnz, int64_t ntiles) {
+  if (nnz % 4 == 0) return ntiles;
+  const int64_t full = (nnz - kTile - kExt) >= 0 ? (nnz - kTile - kExt) / kTile + 1 : 0;
+  return full < ntiles ? full : ntiles;
+}
+
+// Warp-level vla-32 reduction of smem products [lo, hi): lane l sums lo+l,
+// lo+l+32, ... then the lanes.py:107-128 tree.  Equals spmv_csr_vla(32) when
+// [lo, hi) is a whole row.
+template <typename T>
+__device__ __forceinline__ T warp_segment_sum(const T* __restrict__ p, uint32_t lo, uint32_t hi, int lane) {
+  T acc = T(0);
+  for (uint32_t j = lo + lane; j < hi; j += 32) acc = add_rn(acc, p[j]);
+  return tree_reduce_warp(acc, 32);
+}
+
+}  // namespace spmv
