@@ -210,6 +210,16 @@ int spmv_csr_col_bounds(int64_t nrows, const uint32_t* row_pointers,
                         const uint32_t* col_indices, void* stream,
                         uint32_t* min_out, uint32_t* max_out);
 
+/* Rows of a CSR slab that need no halo: every row in [*i_lo, *i_hi) reads
+ * only columns in [col_lo, col_hi).  *i_lo = 1 + last row reading a column
+ * below col_lo (0 if none); *i_hi = first row reading a column >= col_hi
+ * (nrows if none).  Lets the interior rows run while the halo exchange is in
+ * flight (hpcg.py:157-180 split into overlap-able parts).  Synchronises. */
+int spmv_csr_halo_split(int64_t nrows, const uint32_t* row_pointers,
+                        const uint32_t* col_indices, int64_t col_lo,
+                        int64_t col_hi, void* stream, int64_t* i_lo,
+                        int64_t* i_hi);
+
 #ifdef __cplusplus
 }
 #endif

@@ -1,6 +1,7 @@
 // Library-level C ABI: error reporting, device queries, partition helpers.
 #include <cub/cub.cuh>
 
+#include <cstdlib>
 #include <mutex>
 
 #include "common.cuh"
@@ -90,3 +91,69 @@ int spmv_csr_col_bounds(int64_t nrows, const uint32_t* irp, const uint32_t* aj, 
 }
 
 }  // extern "C"
+
+// ---- interior / boundary split of a row slab (hpcg.py:95-154 semantics) ----
+namespace spmv {
+__global__ void halo_split_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj, int64_t nrows,
+                                  int64_t col_lo, int64_t col_hi, unsigned long long* __restrict__ out) {
+  // out[0] = max row + 1 touching a column < col_lo; out[1] = min row touching a column >= col_hi
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += int64_t(gridDim.x) * blockDim.x) {
+    bool lo = false, hi = false;
+    for (uint32_t j = irp[r]; j < irp[r + 1]; ++j) {
+      const int64_t c = aj[j];
+      lo |= c < col_lo;
+      hi |= c >= col_hi;
+    }
+    if (lo) atomicMax(out, (unsigned long long)(r + 1));
+    if (hi) atomicMin(out + 1, (unsigned long long)r);
+  }
+}
+}  // namespace spmv
+
+extern "C" int spmv_csr_halo_split(int64_t nrows, const uint32_t* irp, const uint32_t* aj, int64_t col_lo,
+                                   int64_t col_hi, void* stream, int64_t* i_lo, int64_t* i_hi) {
+  if (!i_lo || !i_hi) return fail(SPMV_INVALID_ARG, "NULL output");
+  *i_lo = 0;
+  *i_hi = nrows;
+  if (nrows <= 0) return SPMV_OK;
+  cudaStream_t st = as_stream(stream);
+  DevBuf out;
+  int rc = out.alloc(16);
+  if (rc) return rc;
+  unsigned long long init[2] = {0ull, (unsigned long long)nrows};
+  SPMV_CUDA_TRY(cudaMemcpyAsync(out.ptr, init, 16, cudaMemcpyHostToDevice, st));
+  int64_t grid = (nrows + 255) / 256;
+  if (grid > int64_t(sm_count()) * 16) grid = int64_t(sm_count()) * 16;
+  halo_split_kernel<<<unsigned(grid), 256, 0, st>>>(irp, aj, nrows, col_lo, col_hi, out.as<unsigned long long>());
+  SPMV_LAUNCH_CHECK();
+  unsigned long long h[2];
+  SPMV_CUDA_TRY(cudaMemcpyAsync(h, out.ptr, 16, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  *i_lo = int64_t(h[0]);
+  *i_hi = int64_t(h[1]);
+  return SPMV_OK;
+}
+
+// ---- tuning knobs (experiments only; defaults are the measured best) ----
+namespace spmv {
+static int env_int(const char* name, int dflt) {
+  const char* v = getenv(name);
+  if (!v || !*v) return dflt;
+  return atoi(v);
+}
+int tile_entries() {
+  static const int t = [] {
+    const int v = env_int("SPMV_TILE", 2048);
+    return (v == 1024) ? 1024 : 2048;
+  }();
+  return t;
+}
+int dia_rows_per_tile() {
+  static const int r = env_int("SPMV_DIA_ROWS", 0);
+  return r;
+}
+int dia_stages() {
+  static const int s = env_int("SPMV_DIA_STAGES", 0);
+  return s;
+}
+}  // namespace spmv

@@ -31,8 +31,6 @@
 
 namespace spmv {
 
-constexpr int kCooItems = kTile / kTileThreads;
-
 template <typename T>
 struct CooParams {
   const uint32_t* ai;
@@ -48,29 +46,32 @@ struct CooParams {
   int64_t nrows, nnz, col_base, ntiles, n_bulk;
 };
 
-template <typename T>
+template <typename T, int TILE>
 struct CooSmem {
-  static constexpr size_t rows_bytes = align_up(sizeof(uint32_t) * (kTile + 2 * kExt), 128);
-  static constexpr size_t cols_bytes = align_up(sizeof(uint32_t) * (kTile + kExt), 128);
-  static constexpr size_t vals_bytes = align_up(sizeof(T) * (kTile + kExt), 128);
+  static constexpr int rounds = TILE / kTileThreads;
+  static constexpr size_t rows_bytes = align_up(sizeof(uint32_t) * (TILE + 2 * kExt), 128);
+  static constexpr size_t cols_bytes = align_up(sizeof(uint32_t) * (TILE + kExt), 128);
+  static constexpr size_t vals_bytes = align_up(sizeof(T) * (TILE + kExt), 128);
   static constexpr size_t stage_bytes = rows_bytes + cols_bytes + vals_bytes;
-  static constexpr size_t starts_bytes = align_up(sizeof(uint16_t) * (kTile + 1), 128);
-  static constexpr size_t long_bytes = align_up(sizeof(LongSeg) * kMaxLongSegs, 128);
-  static constexpr size_t header = 128 + starts_bytes + long_bytes;
+  static constexpr size_t starts_bytes = align_up(sizeof(uint16_t) * (TILE + 1), 128);
+  static constexpr size_t long_bytes = align_up(sizeof(LongSeg) * max_long_segs<TILE>(), 128);
+  static constexpr size_t counts_bytes = align_up(sizeof(int) * 2 * 64, 128);
+  static constexpr size_t header = 128 + starts_bytes + long_bytes + counts_bytes;
   static constexpr size_t total = header + kTileStages * stage_bytes;
+  static_assert(rounds * (kTileThreads / 32) <= 64, "segment scan covers at most 64 warp counts");
 };
 
-// rows: tile-relative view, valid for k in [-kExt, kTile + kExt).
-template <typename T>
+// rows: tile-relative view, valid for k in [-kExt, TILE + kExt).
+template <typename T, int TILE>
 __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_t* __restrict__ rows,
                                  const uint32_t* __restrict__ cols, T* __restrict__ vals, uint16_t* s_start,
-                                 LongSeg* s_long, int* s_nseg, int* s_nlong, void* scan_tmp_raw) {
-  using BlockScan = cub::BlockScan<int, kTileThreads>;
-  auto& scan_tmp = *reinterpret_cast<typename BlockScan::TempStorage*>(scan_tmp_raw);
+                                 LongSeg* s_long, int* s_nseg, int* s_nlong, int* s_wcnt) {
+  constexpr int R = TILE / kTileThreads;
+  constexpr int W = kTileThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t E0 = t * kTile;
-  const int cnt_in = int(min(int64_t(kTile), P.nnz - E0));
-  const int cnt_ext = int(min(int64_t(kTile + kExt), P.nnz - E0));
+  const int64_t E0 = t * TILE;
+  const int cnt_in = int(min(int64_t(TILE), P.nnz - E0));
+  const int cnt_ext = int(min(int64_t(TILE + kExt), P.nnz - E0));
   const T* xb = P.x - P.col_base;
 
   // 1. products in place (4 gathers in flight per thread)
@@ -88,30 +89,45 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
     for (; k < cnt_ext; k += kTileThreads) vals[k] = mul_rn(vals[k], __ldg(xb + cols[k]));
   }
 
-  // 2. segment heads over the tile's own entries (blocked, 8 per thread)
-  bool head[kCooItems];
-  int nh = 0;
+  // 2. segment heads, striped (round i, warp w covers entries
+  //    [256 i + 32 w, +32)): ballots + a 64-entry warp scan give every head
+  //    its position in entry order without shared-memory bank conflicts.
+  unsigned bal[R];
 #pragma unroll
-  for (int i = 0; i < kCooItems; ++i) {
-    const int k = tid * kCooItems + i;
-    head[i] = k < cnt_in && (k == 0 || rows[k] != rows[k - 1]);
-    nh += head[i];
+  for (int i = 0; i < R; ++i) {
+    const int k = i * kTileThreads + tid;
+    const bool h = k < cnt_in && (k == 0 || rows[k] != rows[k - 1]);
+    bal[i] = __ballot_sync(0xffffffffu, h);
+    if (lane == 0) s_wcnt[i * W + warp] = __popc(bal[i]);
   }
-  int off = 0, total = 0;
-  BlockScan(scan_tmp).ExclusiveSum(nh, off, total);
+  __syncthreads();
+  if (warp == 0) {
+    const int v0 = (2 * lane < R * W) ? s_wcnt[2 * lane] : 0;
+    const int v1 = (2 * lane + 1 < R * W) ? s_wcnt[2 * lane + 1] : 0;
+    int incl = v0 + v1;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int u = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += u;
+    }
+    const int excl = incl - v0 - v1;
+    s_wcnt[64 + 2 * lane] = excl;
+    s_wcnt[64 + 2 * lane + 1] = excl + v0;
+    if (lane == 31) {
+      *s_nseg = incl;
+      *s_nlong = 0;
+      s_start[incl] = uint16_t(cnt_in);
+      P.head_row[t] = kNoRow;
+      P.tail_row[t] = kNoRow;
+      P.pass[t] = 0;
+    }
+  }
+  __syncthreads();
   {
-    int cur = off;
+    const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
-    for (int i = 0; i < kCooItems; ++i)
-      if (head[i]) s_start[cur++] = uint16_t(tid * kCooItems + i);
-  }
-  if (tid == 0) {
-    *s_nseg = total;
-    *s_nlong = 0;
-    s_start[total] = uint16_t(cnt_in);
-    P.head_row[t] = kNoRow;
-    P.tail_row[t] = kNoRow;
-    P.pass[t] = 0;
+    for (int i = 0; i < R; ++i)
+      if ((bal[i] >> lane) & 1u)
+        s_start[s_wcnt[64 + i * W + warp] + __popc(bal[i] & lt)] = uint16_t(i * kTileThreads + tid);
   }
   __syncthreads();
   const int nseg = *s_nseg;
@@ -175,18 +191,17 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
   }
 }
 
-template <typename T, bool BULK>
+template <typename T, bool BULK, int TILE>
 __global__ void __launch_bounds__(kTileThreads)
 coo_tile_kernel(const CooParams<T> P) {
-  using BlockScan = cub::BlockScan<int, kTileThreads>;
-  __shared__ typename BlockScan::TempStorage scan_tmp;
   extern __shared__ __align__(128) unsigned char smem[];
-  using S = CooSmem<T>;
+  using S = CooSmem<T, TILE>;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   int* s_nseg = reinterpret_cast<int*>(smem + 32);
   int* s_nlong = reinterpret_cast<int*>(smem + 36);
   uint16_t* s_start = reinterpret_cast<uint16_t*>(smem + 128);
   LongSeg* s_long = reinterpret_cast<LongSeg*>(smem + 128 + S::starts_bytes);
+  int* s_wcnt = reinterpret_cast<int*>(smem + 128 + S::starts_bytes + S::long_bytes);
   unsigned char* stages = smem + S::header;
   const int tid = threadIdx.x;
   auto rows_of = [&](int s) { return reinterpret_cast<uint32_t*>(stages + s * S::stage_bytes); };
@@ -196,11 +211,11 @@ coo_tile_kernel(const CooParams<T> P) {
   };
   // Row slots the copy did not fill: the window before tile 0 and past nnz.
   auto pad_rows = [&](uint32_t* rb, int64_t t) {
-    const int64_t E0 = t * kTile;
-    const int cnt_ext = int(min(int64_t(kTile + kExt), P.nnz - E0));
+    const int64_t E0 = t * TILE;
+    const int cnt_ext = int(min(int64_t(TILE + kExt), P.nnz - E0));
     if (t == 0)
       for (int k = tid; k < kExt; k += kTileThreads) rb[k] = kNoRow;
-    for (int k = cnt_ext + tid; k < kTile + kExt; k += kTileThreads) rb[kExt + k] = kNoRow;
+    for (int k = cnt_ext + tid; k < TILE + kExt; k += kTileThreads) rb[kExt + k] = kNoRow;
   };
 
   int64_t n_bulk = BULK ? P.n_bulk : 0;
@@ -214,8 +229,8 @@ coo_tile_kernel(const CooParams<T> P) {
     const int64_t mine = first < n_bulk ? (n_bulk - 1 - first) / stride + 1 : 0;
     auto issue = [&](int64_t i) {
       const int64_t t = first + i * stride;
-      const int64_t E0 = t * kTile;
-      const uint32_t cnt = uint32_t(min(int64_t(kTile + kExt), P.nnz - E0));
+      const int64_t E0 = t * TILE;
+      const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
       const uint32_t pre = t > 0 ? uint32_t(kExt) : 0u;
       const int s = int(i % kTileStages);
       mbar_arrive_expect_tx(&bars[s], (cnt + pre) * 4u + cnt * (4u + uint32_t(sizeof(T))));
@@ -231,8 +246,8 @@ coo_tile_kernel(const CooParams<T> P) {
       mbar_wait(&bars[s], uint32_t((i / kTileStages) & 1));
       pad_rows(rows_of(s), t);
       __syncthreads();
-      coo_process_tile<T>(P, t, rows_of(s) + kExt, cols_of(s), vals_of(s), s_start, s_long, s_nseg, s_nlong,
-                          &scan_tmp);
+      coo_process_tile<T, TILE>(P, t, rows_of(s) + kExt, cols_of(s), vals_of(s), s_start, s_long, s_nseg, s_nlong,
+                                s_wcnt);
       __syncthreads();
       if (tid == 0 && i + kTileStages < mine) {
         fence_proxy_async();
@@ -241,8 +256,8 @@ coo_tile_kernel(const CooParams<T> P) {
     }
   }
   for (int64_t t = n_bulk + blockIdx.x; t < P.ntiles; t += gridDim.x) {
-    const int64_t E0 = t * kTile;
-    const int cnt = int(min(int64_t(kTile + kExt), P.nnz - E0));
+    const int64_t E0 = t * TILE;
+    const int cnt = int(min(int64_t(TILE + kExt), P.nnz - E0));
     uint32_t* rb = rows_of(0);
     uint32_t* c = cols_of(0);
     T* v = vals_of(0);
@@ -256,7 +271,7 @@ coo_tile_kernel(const CooParams<T> P) {
     }
     pad_rows(rb, t);
     __syncthreads();
-    coo_process_tile<T>(P, t, rb + kExt, c, v, s_start, s_long, s_nseg, s_nlong, &scan_tmp);
+    coo_process_tile<T, TILE>(P, t, rb + kExt, c, v, s_start, s_long, s_nseg, s_nlong, s_wcnt);
     __syncthreads();
   }
 }
@@ -411,7 +426,7 @@ struct spmv_coo_plan {
   bool row_sorted = true;
   DevBuf sorted_ai, sorted_aj, sorted_av;  // only when the input rows were unsorted
   DevBuf run_start, run_row;
-  int64_t n_runs = 0, n_long = 0, ntiles = 0;
+  int64_t n_runs = 0, n_long = 0, ntiles = 0, tile = 2048;
   DevBuf head_row, tail_row, pass, head_val, tail_val;
   DevBuf steps;
   int grid = 0;
@@ -426,16 +441,16 @@ __global__ void count_long_runs_kernel(const uint32_t* __restrict__ run_start, i
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(n_long, c);
 }
 
-template <typename T>
+template <typename T, int TILE>
 static int coo_launch_config(spmv_coo_plan* p) {
-  using S = CooSmem<T>;
-  SPMV_CUDA_TRY(cudaFuncSetAttribute(coo_tile_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  using S = CooSmem<T, TILE>;
+  SPMV_CUDA_TRY(cudaFuncSetAttribute(coo_tile_kernel<T, true, TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(S::total)));
-  SPMV_CUDA_TRY(cudaFuncSetAttribute(coo_tile_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  SPMV_CUDA_TRY(cudaFuncSetAttribute(coo_tile_kernel<T, false, TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(S::total)));
   int per_sm = 0;
-  SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coo_tile_kernel<T, true>, kTileThreads,
-                                                              S::total));
+  SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coo_tile_kernel<T, true, TILE>,
+                                                              kTileThreads, S::total));
   if (per_sm < 1) per_sm = 1;
   const int64_t cap = int64_t(sm_count()) * per_sm;
   p->grid = int(p->ntiles < cap ? p->ntiles : cap);
@@ -522,17 +537,20 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
   SPMV_CUDA_TRY(cudaMemcpyAsync(&h, nl.ptr, 8, cudaMemcpyDeviceToHost, st));
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
   p->n_long = int64_t(h);
-  p->ntiles = (nnz + kTile - 1) / kTile;
+  p->tile = tile_entries();
+  p->ntiles = (nnz + p->tile - 1) / p->tile;
   const size_t vs = value_size(p->dtype);
   if ((rc = p->head_row.alloc(4 * p->ntiles)) || (rc = p->tail_row.alloc(4 * p->ntiles)) ||
       (rc = p->pass.alloc(4 * p->ntiles)) || (rc = p->head_val.alloc(vs * p->ntiles)) ||
       (rc = p->tail_val.alloc(vs * p->ntiles)))
     return rc;
-  return p->dtype == SPMV_F64 ? coo_launch_config<double>(p) : coo_launch_config<float>(p);
+  if (p->tile == 1024)
+    return p->dtype == SPMV_F64 ? coo_launch_config<double, 1024>(p) : coo_launch_config<float, 1024>(p);
+  return p->dtype == SPMV_F64 ? coo_launch_config<double, 2048>(p) : coo_launch_config<float, 2048>(p);
 }
 
-template <typename T>
-static int coo_run(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const T* av, const T* x,
+template <typename T, int TILE>
+static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st) {
   if (p->nrows == 0) return SPMV_OK;
   if (p->nnz == 0) {
@@ -561,12 +579,12 @@ static int coo_run(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* a
   P.ntiles = p->ntiles;
   const bool aligned = (reinterpret_cast<uintptr_t>(ai) % 16 == 0) && (reinterpret_cast<uintptr_t>(aj) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(av) % 16 == 0);
-  P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles) : 0;
-  const size_t smem = CooSmem<T>::total;
+  P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
+  const size_t smem = CooSmem<T, TILE>::total;
   if (aligned)
-    coo_tile_kernel<T, true><<<unsigned(p->grid), kTileThreads, smem, st>>>(P);
+    coo_tile_kernel<T, true, TILE><<<unsigned(p->grid), kTileThreads, smem, st>>>(P);
   else
-    coo_tile_kernel<T, false><<<unsigned(p->grid), kTileThreads, smem, st>>>(P);
+    coo_tile_kernel<T, false, TILE><<<unsigned(p->grid), kTileThreads, smem, st>>>(P);
   SPMV_LAUNCH_CHECK();
   if (p->n_long > 0) {
     const int64_t g = std::min<int64_t>((p->ntiles + 255) / 256, int64_t(sm_count()) * 8);
@@ -574,6 +592,13 @@ static int coo_run(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* a
     SPMV_LAUNCH_CHECK();
   }
   return SPMV_OK;
+}
+
+template <typename T>
+static int coo_run(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const T* av, const T* x,
+                   int64_t col_base, T* y, cudaStream_t st) {
+  if (p->tile == 1024) return coo_run_tiled<T, 1024>(p, ai, aj, av, x, col_base, y, st);
+  return coo_run_tiled<T, 2048>(p, ai, aj, av, x, col_base, y, st);
 }
 
 extern "C" {
@@ -612,7 +637,7 @@ int spmv_coo_plan_info(const spmv_coo_plan* p, int64_t* n_runs, int64_t* n_long_
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (n_runs) *n_runs = p->n_runs;
   if (n_long_runs) *n_long_runs = p->n_long;
-  if (n_items) *n_items = p->ntiles;
+  if (n_items) *n_items = p->tile;
   if (row_sorted) *row_sorted = p->row_sorted ? 1 : 0;
   if (launches) *launches = (p->nrows > 0 ? 1 : 0) + (p->n_long > 0 ? 1 : 0);
   return SPMV_OK;

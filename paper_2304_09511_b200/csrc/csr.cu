@@ -6,7 +6,7 @@
 //
 // Plain path — csr_tile_kernel, persistent, TMA-fed (tile.cuh):
 //   1. a producer thread bulk-copies the tile's column indices and values
-//      (kTile + kExt entries) into a STAGES-deep shared-memory ring;
+//      (TILE + kExt entries) into a STAGES-deep shared-memory ring;
 //   2. all threads form the rounded products in place (x gathered through
 //      L1/L2; x is the only irregular stream);
 //   3. rows that start in the tile with <= exact_len entries (all stencil
@@ -17,7 +17,7 @@
 //      spans tiles leaves one partial per tile and the last tile to finish
 //      (atomic ticket, no spinning) adds them in tile order — deterministic,
 //      within 1e-12 of the reference.
-// Every stored entry is read from HBM exactly once (+kExt/kTile = 1.6%
+// Every stored entry is read from HBM exactly once (+kExt/TILE = 1.6%
 // overlap that hits L2), the row pointers once, x through L2, y written
 // once: the minimum-byte model of SURVEY.md §8(d).
 #include <algorithm>
@@ -41,22 +41,22 @@ struct CsrParams {
   int exact_len;
 };
 
-template <typename T>
+template <typename T, int TILE>
 struct CsrSmem {
-  static constexpr size_t cols_bytes = align_up(sizeof(uint32_t) * (kTile + kExt), 128);
-  static constexpr size_t vals_bytes = align_up(sizeof(T) * (kTile + kExt), 128);
+  static constexpr size_t cols_bytes = align_up(sizeof(uint32_t) * (TILE + kExt), 128);
+  static constexpr size_t vals_bytes = align_up(sizeof(T) * (TILE + kExt), 128);
   static constexpr size_t stage_bytes = cols_bytes + vals_bytes;
-  static constexpr size_t header = align_up(64 + sizeof(LongSeg) * kMaxLongSegs, 128);
+  static constexpr size_t header = align_up(64 + sizeof(LongSeg) * max_long_segs<TILE>(), 128);
   static constexpr size_t total = header + kTileStages * stage_bytes;
 };
 
-template <typename T>
+template <typename T, int TILE>
 __device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_t* __restrict__ cols,
                                  T* __restrict__ vals, LongSeg* s_long, int* s_nlong) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int64_t E0 = t * kTile;
-  const int cnt_ext = int(min(int64_t(kTile + kExt), P.nnz - E0));
-  const int64_t E1 = E0 + kTile;
+  const int64_t E0 = t * TILE;
+  const int cnt_ext = int(min(int64_t(TILE + kExt), P.nnz - E0));
+  const int64_t E1 = E0 + TILE;
   const T* xb = P.x - P.col_base;
 
   // Row range of the tile; prefetch the first row's pointers before the
@@ -130,7 +130,7 @@ __device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_
       if (int64_t(L.s) >= E0 && int64_t(L.e) <= E1) {
         P.y[L.row] = part;
       } else {
-        const int64_t t0 = L.s / kTile, t1 = (int64_t(L.e) - 1) / kTile;
+        const int64_t t0 = L.s / TILE, t1 = (int64_t(L.e) - 1) / TILE;
         if (t == t0)
           P.tail[t] = part;
         else
@@ -149,11 +149,11 @@ __device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_
   }
 }
 
-template <typename T, bool BULK>
+template <typename T, bool BULK, int TILE>
 __global__ void __launch_bounds__(kTileThreads)
 csr_tile_kernel(const CsrParams<T> P) {
   extern __shared__ __align__(128) unsigned char smem[];
-  using S = CsrSmem<T>;
+  using S = CsrSmem<T, TILE>;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   int* s_nlong = reinterpret_cast<int*>(smem + 32);
   LongSeg* s_long = reinterpret_cast<LongSeg*>(smem + 64);
@@ -173,8 +173,8 @@ csr_tile_kernel(const CsrParams<T> P) {
     const int64_t mine = first < n_bulk ? (n_bulk - 1 - first) / stride + 1 : 0;
     auto issue = [&](int64_t i) {
       const int64_t t = first + i * stride;
-      const int64_t E0 = t * kTile;
-      const uint32_t cnt = uint32_t(min(int64_t(kTile + kExt), P.nnz - E0));
+      const int64_t E0 = t * TILE;
+      const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
       const int s = int(i % kTileStages);
       mbar_arrive_expect_tx(&bars[s], cnt * uint32_t(sizeof(uint32_t) + sizeof(T)));
       bulk_g2s(cols_of(s), P.aj + E0, cnt * uint32_t(sizeof(uint32_t)), &bars[s]);
@@ -185,7 +185,7 @@ csr_tile_kernel(const CsrParams<T> P) {
     for (int64_t i = 0; i < mine; ++i) {
       const int s = int(i % kTileStages);
       mbar_wait(&bars[s], uint32_t((i / kTileStages) & 1));
-      csr_process_tile<T>(P, first + i * stride, cols_of(s), vals_of(s), s_long, s_nlong);
+      csr_process_tile<T, TILE>(P, first + i * stride, cols_of(s), vals_of(s), s_long, s_nlong);
       __syncthreads();
       if (tid == 0 && i + kTileStages < mine) {
         fence_proxy_async();
@@ -195,8 +195,8 @@ csr_tile_kernel(const CsrParams<T> P) {
   }
   // Tiles the bulk engine cannot address: cooperative loads into stage 0.
   for (int64_t t = n_bulk + blockIdx.x; t < P.ntiles; t += gridDim.x) {
-    const int64_t E0 = t * kTile;
-    const int cnt = int(min(int64_t(kTile + kExt), P.nnz - E0));
+    const int64_t E0 = t * TILE;
+    const int cnt = int(min(int64_t(TILE + kExt), P.nnz - E0));
     uint32_t* c = cols_of(0);
     T* v = vals_of(0);
     for (int k = tid; k < cnt; k += kTileThreads) {
@@ -204,21 +204,21 @@ csr_tile_kernel(const CsrParams<T> P) {
       v[k] = P.av[E0 + k];
     }
     __syncthreads();
-    csr_process_tile<T>(P, t, c, v, s_long, s_nlong);
+    csr_process_tile<T, TILE>(P, t, c, v, s_long, s_nlong);
     __syncthreads();
   }
 }
 
 // row_lo[t] = row containing entry t*kTile (last r with irp[r] <= t*kTile);
 // row_lo[ntiles] = nrows.
-__global__ void csr_row_lo_kernel(const uint32_t* __restrict__ irp, int64_t nrows, int64_t ntiles,
+__global__ void csr_row_lo_kernel(const uint32_t* __restrict__ irp, int64_t nrows, int64_t ntiles, int64_t tile,
                                   uint32_t* __restrict__ row_lo) {
   for (int64_t t = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; t <= ntiles; t += int64_t(gridDim.x) * blockDim.x) {
     if (t == ntiles) {
       row_lo[t] = uint32_t(nrows);
       continue;
     }
-    const uint64_t key = uint64_t(t) * kTile;
+    const uint64_t key = uint64_t(t) * uint64_t(tile);
     int64_t lo = 0, hi = nrows;  // find last r in [0, nrows) with irp[r] <= key
     while (lo < hi) {
       const int64_t mid = (lo + hi + 1) >> 1;
@@ -301,23 +301,23 @@ using namespace spmv;
 
 struct spmv_csr_plan {
   int dtype = SPMV_F64;
-  int64_t nrows = 0, ncols = 0, nnz = 0, ntiles = 0;
+  int64_t nrows = 0, ncols = 0, nnz = 0, ntiles = 0, tile = 2048;
   int exact_len = kExactLen;
   int64_t n_long = 0;
   DevBuf row_lo, head, tail, cnt;
   int grid_bulk = 0, grid_direct = 0;
 };
 
-template <typename T>
+template <typename T, int TILE>
 static int csr_launch_config(spmv_csr_plan* p) {
-  using S = CsrSmem<T>;
-  SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_tile_kernel<T, true>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  using S = CsrSmem<T, TILE>;
+  SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_tile_kernel<T, true, TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(S::total)));
-  SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_tile_kernel<T, false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_tile_kernel<T, false, TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                      int(S::total)));
   int per_sm = 0;
-  SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_tile_kernel<T, true>, kTileThreads,
-                                                              S::total));
+  SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_tile_kernel<T, true, TILE>,
+                                                              kTileThreads, S::total));
   if (per_sm < 1) per_sm = 1;
   const int64_t cap = int64_t(sm_count()) * per_sm;
   p->grid_bulk = int(p->ntiles < cap ? p->ntiles : cap);
@@ -325,8 +325,8 @@ static int csr_launch_config(spmv_csr_plan* p) {
   return SPMV_OK;
 }
 
-template <typename T>
-static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
+template <typename T, int TILE>
+static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st) {
   if (p->nrows == 0) return SPMV_OK;
   if (p->nnz == 0) {
@@ -349,14 +349,21 @@ static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* 
   P.ntiles = p->ntiles;
   P.exact_len = p->exact_len;
   const bool aligned = (reinterpret_cast<uintptr_t>(aj) % 16 == 0) && (reinterpret_cast<uintptr_t>(av) % 16 == 0);
-  P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles) : 0;
-  const size_t smem = CsrSmem<T>::total;
+  P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
+  const size_t smem = CsrSmem<T, TILE>::total;
   if (aligned)
-    csr_tile_kernel<T, true><<<unsigned(p->grid_bulk), kTileThreads, smem, st>>>(P);
+    csr_tile_kernel<T, true, TILE><<<unsigned(p->grid_bulk), kTileThreads, smem, st>>>(P);
   else
-    csr_tile_kernel<T, false><<<unsigned(p->grid_direct), kTileThreads, smem, st>>>(P);
+    csr_tile_kernel<T, false, TILE><<<unsigned(p->grid_direct), kTileThreads, smem, st>>>(P);
   SPMV_LAUNCH_CHECK();
   return SPMV_OK;
+}
+
+template <typename T>
+static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
+                   int64_t col_base, T* y, cudaStream_t st) {
+  if (p->tile == 1024) return csr_run_tiled<T, 1024>(p, irp, aj, av, x, col_base, y, st);
+  return csr_run_tiled<T, 2048>(p, irp, aj, av, x, col_base, y, st);
 }
 
 extern "C" {
@@ -378,7 +385,8 @@ int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, c
   p->ncols = ncols;
   p->nnz = nnz;
   p->exact_len = exact_len;
-  p->ntiles = (nnz + kTile - 1) / kTile;
+  p->tile = tile_entries();
+  p->ntiles = (nnz + p->tile - 1) / p->tile;
   int rc = SPMV_OK;
   const size_t vs = value_size(dtype);
   if (nrows > 0 && nnz > 0) {
@@ -393,7 +401,8 @@ int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, c
       if (e == cudaSuccess) e = cudaMemsetAsync(nl.ptr, 0, 8, st);
       const int64_t g1 = std::min<int64_t>((p->ntiles + 256) / 256, int64_t(sm_count()) * 16);
       if (e == cudaSuccess) {
-        csr_row_lo_kernel<<<unsigned(g1), 256, 0, st>>>(row_pointers, nrows, p->ntiles, p->row_lo.as<uint32_t>());
+        csr_row_lo_kernel<<<unsigned(g1), 256, 0, st>>>(row_pointers, nrows, p->ntiles, p->tile,
+                                                         p->row_lo.as<uint32_t>());
         e = cudaGetLastError();
       }
       const int64_t g2 = std::min<int64_t>((nrows + 255) / 256, int64_t(sm_count()) * 16);
@@ -408,7 +417,12 @@ int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, c
       if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "CSR plan: %s", cudaGetErrorString(e));
       p->n_long = int64_t(h);
     }
-    if (!rc) rc = dtype == SPMV_F64 ? csr_launch_config<double>(p) : csr_launch_config<float>(p);
+    if (!rc) {
+      if (p->tile == 1024)
+        rc = dtype == SPMV_F64 ? csr_launch_config<double, 1024>(p) : csr_launch_config<float, 1024>(p);
+      else
+        rc = dtype == SPMV_F64 ? csr_launch_config<double, 2048>(p) : csr_launch_config<float, 2048>(p);
+    }
   }
   if (rc) {
     delete p;
@@ -426,7 +440,7 @@ int spmv_csr_plan_destroy(spmv_csr_plan* plan) {
 int spmv_csr_plan_info(const spmv_csr_plan* p, int64_t* n_long_rows, int64_t* n_items, int64_t* launches) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (n_long_rows) *n_long_rows = p->n_long;
-  if (n_items) *n_items = p->ntiles;
+  if (n_items) *n_items = p->tile;
   if (launches) *launches = p->nrows > 0 ? 1 : 0;
   return SPMV_OK;
 }

@@ -20,6 +20,9 @@
 
 namespace spmv {
 
+int dia_rows_per_tile();
+int dia_stages();
+
 constexpr int kDiaThreads = 256;
 constexpr int kMaxSmemOffsets = 2048;
 
@@ -141,6 +144,7 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
   int64_t R = int64_t(57344 / (row_bytes ? row_bytes : 1)) / 8 * 8;
   if (R > 512) R = 512;
   if (R >= kDiaThreads) R = R / kDiaThreads * kDiaThreads;  // whole rows per thread
+  if (dia_rows_per_tile() >= 8) R = dia_rows_per_tile() / 8 * 8;
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) % 16 == 0) && ((R * row_bytes) % 16 == 0) &&
                        ((avail_rows * row_bytes) % 16 == 0);
   const bool use_bulk = nd > 0 && nd <= kMaxSmemOffsets && R >= 8 && aligned;
@@ -154,7 +158,8 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
   }
   const int64_t ntiles = (nrows + R - 1) / R;
   const uint32_t stage_bytes = uint32_t(((R * row_bytes) + 127) & ~size_t(127));
-  const int stages = stage_bytes > 40960 ? 2 : 3;
+  int stages = stage_bytes > 40960 ? 2 : 3;
+  if (dia_stages() == 2 || dia_stages() == 3) stages = dia_stages();
   const size_t off_bytes = (size_t(nd) * 4 + 127) & ~size_t(127);
   const size_t smem = 128 + off_bytes + size_t(stages) * stage_bytes;
   int ctas_per_sm = int((227 * 1024) / (smem + 1024));

@@ -11,12 +11,18 @@
 
 namespace spmv {
 
-constexpr int kTile = 2048;
 constexpr int kExt = 32;  // == kExactLen: a short row never reaches further
 constexpr int kTileThreads = 256;
 constexpr int kTileStages = 2;
-constexpr int kMaxLongSegs = 160;  // >= kTile/(kExactLen+1) + 2
 constexpr uint32_t kNoRow = 0xffffffffu;
+
+// Long segments per tile: at most TILE/(kExactLen+1) inner ones + 2 boundary.
+template <int TILE>
+constexpr int max_long_segs() { return TILE / (kExactLen + 1) + 4; }
+
+// Tile size used by the plans (entries).  1024 keeps more CTAs resident per
+// SM (smaller shared-memory ring); 2048 halves the per-tile overhead.
+int tile_entries();
 
 static_assert(kExt == kExactLen, "extension must cover a whole short row");
 
@@ -30,9 +36,9 @@ struct LongSeg {
 // Number of tiles whose [E0, E0 + kTile + kExt) window (clamped to nnz) can be
 // bulk-copied without reading past the arrays: all of them when nnz % 4 == 0,
 // otherwise those with E0 + kTile + kExt <= nnz.
-inline int64_t bulk_tiles(int64_t nnz, int64_t ntiles) {
+inline int64_t bulk_tiles(int64_t nnz, int64_t ntiles, int64_t tile) {
   if (nnz % 4 == 0) return ntiles;
-  const int64_t full = (nnz - kTile - kExt) >= 0 ? (nnz - kTile - kExt) / kTile + 1 : 0;
+  const int64_t full = (nnz - tile - kExt) >= 0 ? (nnz - tile - kExt) / tile + 1 : 0;
   return full < ntiles ? full : ntiles;
 }
 

@@ -116,11 +116,11 @@ class _Plan:
         if self.kind == "csr":
             a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
             _lib.call("spmv_csr_plan_info", self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
-            return {"long_rows": a.value, "items": b.value, "launches": c.value}
+            return {"long_rows": a.value, "tile": b.value, "launches": c.value}
         a, b, c, d, e = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_int64()
         _lib.call("spmv_coo_plan_info", self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                   ctypes.byref(d), ctypes.byref(e))
-        return {"runs": a.value, "long_runs": b.value, "items": c.value, "row_sorted": bool(d.value),
+        return {"runs": a.value, "long_runs": b.value, "tile": c.value, "row_sorted": bool(d.value),
                 "launches": e.value}
 
 

@@ -6,8 +6,8 @@ Exactness contract checked here:
   * DIA plain/vla                     bit-exact, every row
   * CSR plain, rows <= 32 entries     bit-exact with spmv_csr_plain
   * COO plain, rows <= 32 entries     bit-exact with spmv_coo_plain
-  * longer rows inside one 2048-entry
-    tile (entries [2048t, 2048t+2048)) bit-exact with spmv_csr_vla(lanes=32)
+  * longer rows inside one tile       bit-exact with spmv_csr_vla(lanes=32)
+    (entries [T t, T t + T), T = the plan's tile, 1024 or 2048)
   * longer rows spanning tiles        rel_err <= 1e-12 (f64) / 1e-5 (f32)
   * CSR/COO vla, any lane count       bit-exact with the reference vla
 """
@@ -43,12 +43,16 @@ def row_lengths(arrs: dict) -> np.ndarray:
     return np.diff(arrs["row_pointers"].astype(np.int64))
 
 
-TILE = 2048
+def plan_tile(m) -> int:
+    from paper_2304_09511_b200 import kernels as K
+    return K.csr_plan(m).info()["tile"] if m.format.value == "csr" else K.coo_plan(m).info()["tile"]
 
 
-def check_rowwise(y, y_plain, y_vla32, lens, tol):
-    """Apply the exactness contract row by row."""
+def check_rowwise(y, y_plain, y_vla32, lens, tol, tile):
+    """Apply the exactness contract row by row (tile = the plan's entries
+    per tile)."""
     y = np.asarray(y)
+    TILE = tile
     short = lens <= 32
     assert bit_equal(y[short], y_plain[short]), first_diff(y[short], y_plain[short])
     ends = np.cumsum(lens)
@@ -73,7 +77,7 @@ def test_corpus_all_kernels(sp, name):
         if fmt == "dia":
             assert bit_equal(y, ref), (fmt, first_diff(y, ref))
         else:
-            check_rowwise(y, ref, d[f"{name}/csr/y_vla32"], lens, 1e-12)
+            check_rowwise(y, ref, d[f"{name}/csr/y_vla32"], lens, 1e-12, plan_tile(m))
         for lanes in LANES:
             stats = {}
             if fmt == "coo":
@@ -128,7 +132,7 @@ def test_long_rows(sp, name):
         y = sp.dispatch(m, x)
         ref = d[f"{name}/{fmt}/y_plain"]
         if tol == 1e-12:
-            check_rowwise(y, ref, d[f"{name}/csr/y_vla32"], lens, tol)
+            check_rowwise(y, ref, d[f"{name}/csr/y_vla32"], lens, tol, plan_tile(m))
         else:
             # fp32: against the reference evaluated in f64 on the f32 inputs
             from oracle import spmv_oracle as O
