@@ -148,6 +148,10 @@ int tile_entries() {
   }();
   return t;
 }
+int ctas_per_sm_cap() {
+  static const int c = env_int("SPMV_CTAS_PER_SM", 0);
+  return c;
+}
 int dia_rows_per_tile() {
   static const int r = env_int("SPMV_DIA_ROWS", 0);
   return r;

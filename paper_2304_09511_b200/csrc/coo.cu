@@ -64,7 +64,7 @@ struct CooSmem {
 // rows: tile-relative view, valid for k in [-kExt, TILE + kExt).
 template <typename T, int TILE>
 __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_t* __restrict__ rows,
-                                 const uint32_t* __restrict__ cols, T* __restrict__ vals, uint16_t* s_start,
+                                 const uint32_t* __restrict__ cols, const T* __restrict__ vals, uint16_t* s_start,
                                  LongSeg* s_long, int* s_nseg, int* s_nlong, int* s_wcnt) {
   constexpr int R = TILE / kTileThreads;
   constexpr int W = kTileThreads / 32;
@@ -73,21 +73,6 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
   const int cnt_in = int(min(int64_t(TILE), P.nnz - E0));
   const int cnt_ext = int(min(int64_t(TILE + kExt), P.nnz - E0));
   const T* xb = P.x - P.col_base;
-
-  // 1. products in place (4 gathers in flight per thread)
-  {
-    int k = tid;
-    for (; k + 3 * kTileThreads < cnt_ext; k += 4 * kTileThreads) {
-      const uint32_t c0 = cols[k], c1 = cols[k + kTileThreads], c2 = cols[k + 2 * kTileThreads],
-                     c3 = cols[k + 3 * kTileThreads];
-      const T x0 = __ldg(xb + c0), x1 = __ldg(xb + c1), x2 = __ldg(xb + c2), x3 = __ldg(xb + c3);
-      vals[k] = mul_rn(vals[k], x0);
-      vals[k + kTileThreads] = mul_rn(vals[k + kTileThreads], x1);
-      vals[k + 2 * kTileThreads] = mul_rn(vals[k + 2 * kTileThreads], x2);
-      vals[k + 3 * kTileThreads] = mul_rn(vals[k + 3 * kTileThreads], x3);
-    }
-    for (; k < cnt_ext; k += kTileThreads) vals[k] = mul_rn(vals[k], __ldg(xb + cols[k]));
-  }
 
   // 2. segment heads, striped (round i, warp w covers entries
   //    [256 i + 32 w, +32)): ballots + a 64-entry warp scan give every head
@@ -161,10 +146,8 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
       L.s = L.e = 0;
       s_long[idx] = L;
     } else if (!cont_before) {
-      T acc = T(0);
-      const int kend = k1 + after;
-      for (int k = k0; k < kend; ++k) acc = add_rn(acc, vals[k]);
-      P.y[r] = acc;
+      // +0.0 seed: np.add.at accumulates into a zeroed y
+      P.y[r] = row_dot(cols + k0, vals + k0, k1 + after - k0, xb, T(0));
     }
   }
   __syncthreads();
@@ -174,7 +157,7 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
   const int nl = *s_nlong;
   for (int i = warp; i < nl; i += kTileThreads / 32) {
     const LongSeg L = s_long[i];
-    const T part = warp_segment_sum(vals, L.lo, L.hi, lane);
+    const T part = warp_segment_dot(cols, vals, L.lo, L.hi, lane, xb);
     if (lane == 0) {
       const bool cb = L.flags & 1u, ca = L.flags & 2u;
       if (!cb && !ca) {
@@ -451,6 +434,7 @@ static int coo_launch_config(spmv_coo_plan* p) {
   int per_sm = 0;
   SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coo_tile_kernel<T, true, TILE>,
                                                               kTileThreads, S::total));
+  if (ctas_per_sm_cap() > 0 && per_sm > ctas_per_sm_cap()) per_sm = ctas_per_sm_cap();
   if (per_sm < 1) per_sm = 1;
   const int64_t cap = int64_t(sm_count()) * per_sm;
   p->grid = int(p->ntiles < cap ? p->ntiles : cap);

@@ -7,12 +7,14 @@
 // Plain path — csr_tile_kernel, persistent, TMA-fed (tile.cuh):
 //   1. a producer thread bulk-copies the tile's column indices and values
 //      (TILE + kExt entries) into a STAGES-deep shared-memory ring;
-//   2. all threads form the rounded products in place (x gathered through
-//      L1/L2; x is the only irregular stream);
-//   3. rows that start in the tile with <= exact_len entries (all stencil
-//      rows) are summed left to right by one thread from shared memory —
-//      the reference order, so bit-exact; empty rows get +0.0;
-//   4. longer rows: one warp per in-tile segment (vla-32 order, so a long
+//   2. rows that start in the tile with <= exact_len entries (all stencil
+//      rows) are computed by one thread each: rounded products of the
+//      staged values and gathered x, summed left to right — the reference
+//      order, so bit-exact; empty rows get +0.0.  Row-per-lane mapping puts
+//      32 consecutive rows in a warp, so each gather instruction touches a
+//      few consecutive x lines (entry-per-lane would touch ~10 and saturate
+//      the L1 wavefront pipe);
+//   3. longer rows: one warp per in-tile segment (vla-32 order, so a long
 //      row inside one tile is bit-exact with spmv_csr_vla(32)); a row that
 //      spans tiles leaves one partial per tile and the last tile to finish
 //      (atomic ticket, no spinning) adds them in tile order — deterministic,
@@ -52,15 +54,14 @@ struct CsrSmem {
 
 template <typename T, int TILE>
 __device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_t* __restrict__ cols,
-                                 T* __restrict__ vals, LongSeg* s_long, int* s_nlong) {
+                                 const T* __restrict__ vals, LongSeg* s_long, int* s_nlong) {
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int64_t E0 = t * TILE;
   const int cnt_ext = int(min(int64_t(TILE + kExt), P.nnz - E0));
   const int64_t E1 = E0 + TILE;
   const T* xb = P.x - P.col_base;
 
-  // Row range of the tile; prefetch the first row's pointers before the
-  // product phase so their latency overlaps it.
+  // Row range of the tile (the first row's pointers are loaded up front).
   const int64_t R0 = t == 0 ? 0 : int64_t(P.row_lo[t]);
   const int64_t R1 = P.row_lo[t + 1];
   const int64_t rend = R1 < P.nrows ? R1 + 1 : P.nrows;
@@ -71,20 +72,6 @@ __device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_
     e = __ldg(P.irp + r + 1);
   }
 
-  // Products in place, 4 independent gathers in flight per thread.
-  {
-    int k = tid;
-    for (; k + 3 * kTileThreads < cnt_ext; k += 4 * kTileThreads) {
-      const uint32_t c0 = cols[k], c1 = cols[k + kTileThreads], c2 = cols[k + 2 * kTileThreads],
-                     c3 = cols[k + 3 * kTileThreads];
-      const T x0 = __ldg(xb + c0), x1 = __ldg(xb + c1), x2 = __ldg(xb + c2), x3 = __ldg(xb + c3);
-      vals[k] = mul_rn(vals[k], x0);
-      vals[k + kTileThreads] = mul_rn(vals[k + kTileThreads], x1);
-      vals[k + 2 * kTileThreads] = mul_rn(vals[k + 2 * kTileThreads], x2);
-      vals[k + 3 * kTileThreads] = mul_rn(vals[k + 3 * kTileThreads], x3);
-    }
-    for (; k < cnt_ext; k += kTileThreads) vals[k] = mul_rn(vals[k], __ldg(xb + cols[k]));
-  }
   if (tid == 0) *s_nlong = 0;
   __syncthreads();
 
@@ -95,10 +82,8 @@ __device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_
       if (r < R1) P.y[r] = T(0);
     } else if (len <= uint32_t(P.exact_len)) {
       if (int64_t(s) >= E0 && int64_t(s) < E1) {
-        const T* p = vals + (s - E0);
-        T acc = p[0];  // cumsum starts from the first product (keeps -0.0)
-        for (uint32_t i = 1; i < len; ++i) acc = add_rn(acc, p[i]);
-        P.y[r] = acc;
+        // -0.0 seed: the sum starts from the first product, like cumsum
+        P.y[r] = row_dot(cols + (s - E0), vals + (s - E0), int(len), xb, T(-0.0));
       }
     } else {
       const int64_t lo = max(int64_t(s), E0), hi = min(int64_t(e), E1);
@@ -125,7 +110,7 @@ __device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_
   const int nl = *s_nlong;
   for (int i = warp; i < nl; i += kTileThreads / 32) {
     const LongSeg L = s_long[i];
-    const T part = warp_segment_sum(vals, L.lo, L.hi, lane);
+    const T part = warp_segment_dot(cols, vals, L.lo, L.hi, lane, xb);
     if (lane == 0) {
       if (int64_t(L.s) >= E0 && int64_t(L.e) <= E1) {
         P.y[L.row] = part;
@@ -318,6 +303,7 @@ static int csr_launch_config(spmv_csr_plan* p) {
   int per_sm = 0;
   SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_tile_kernel<T, true, TILE>,
                                                               kTileThreads, S::total));
+  if (ctas_per_sm_cap() > 0 && per_sm > ctas_per_sm_cap()) per_sm = ctas_per_sm_cap();
   if (per_sm < 1) per_sm = 1;
   const int64_t cap = int64_t(sm_count()) * per_sm;
   p->grid_bulk = int(p->ntiles < cap ? p->ntiles : cap);

@@ -23,6 +23,7 @@ constexpr int max_long_segs() { return TILE / (kExactLen + 1) + 4; }
 // Tile size used by the plans (entries).  1024 keeps more CTAs resident per
 // SM (smaller shared-memory ring); 2048 halves the per-tile overhead.
 int tile_entries();
+int ctas_per_sm_cap();  // 0 = occupancy limit
 
 static_assert(kExt == kExactLen, "extension must cover a whole short row");
 
@@ -42,13 +43,34 @@ inline int64_t bulk_tiles(int64_t nnz, int64_t ntiles, int64_t tile) {
   return full < ntiles ? full : ntiles;
 }
 
-// Warp-level vla-32 reduction of smem products [lo, hi): lane l sums lo+l,
-// lo+l+32, ... then the lanes.py:107-128 tree.  Equals spmv_csr_vla(32) when
-// [lo, hi) is a whole row.
+// Left-to-right dot product of a staged row: acc = ((acc0 + p0) + p1) + ...
+// with p_j = vals[j] * x[cols[j]] rounded first.  Eight gathers are issued
+// before their adds (the add order is unchanged).  acc0 = -0.0 reproduces
+// cumsum (the first product itself, kernels.py:81); acc0 = +0.0 reproduces
+// np.add.at on a zeroed y (kernels.py:65).
 template <typename T>
-__device__ __forceinline__ T warp_segment_sum(const T* __restrict__ p, uint32_t lo, uint32_t hi, int lane) {
+__device__ __forceinline__ T row_dot(const uint32_t* __restrict__ c, const T* __restrict__ v, int len,
+                                     const T* __restrict__ xb, T acc) {
+  int i = 0;
+  for (; i + 8 <= len; i += 8) {
+    T p[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) p[j] = mul_rn(v[i + j], __ldg(xb + c[i + j]));
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc = add_rn(acc, p[j]);
+  }
+  for (; i < len; ++i) acc = add_rn(acc, mul_rn(v[i], __ldg(xb + c[i])));
+  return acc;
+}
+
+// Warp-level vla-32 dot product of staged entries [lo, hi): lane l sums
+// lo+l, lo+l+32, ... then the lanes.py:107-128 tree.  Equals
+// spmv_csr_vla(32) when [lo, hi) is a whole row.
+template <typename T>
+__device__ __forceinline__ T warp_segment_dot(const uint32_t* __restrict__ c, const T* __restrict__ v, uint32_t lo,
+                                              uint32_t hi, int lane, const T* __restrict__ xb) {
   T acc = T(0);
-  for (uint32_t j = lo + lane; j < hi; j += 32) acc = add_rn(acc, p[j]);
+  for (uint32_t j = lo + lane; j < hi; j += 32) acc = add_rn(acc, mul_rn(v[j], __ldg(xb + c[j])));
   return tree_reduce_warp(acc, 32);
 }
 
