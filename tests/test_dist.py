@@ -163,4 +163,8 @@ def test_emulated_ranks_random_matrix_allgather(lib_built):
         for p in s.parts:
             s.run_part(p, y)
         ys.append(y)
-    assert torch.cat(ys).cpu().numpy().tobytes() == ref.tobytes()
+    got = torch.cat(ys).cpu().numpy()
+    short = lens <= 32  # bit-exact rows; longer rows are reduced per tile (1e-12)
+    assert got[short].tobytes() == ref[short].tobytes()
+    assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1.0)) <= 1e-12
+    assert all(p.allgather or p.recv_entries == n - (p.rows[1] - p.rows[0]) for p in plans)
