@@ -21,7 +21,10 @@ from .errors import (
     UnsupportedCombination,
 )
 
-LIB_PATH = Path(__file__).resolve().parent / "libspmv_b200.so"
+import os
+
+# SPMV_B200_LIB overrides the library path (A/B experiments of two builds).
+LIB_PATH = Path(os.environ.get("SPMV_B200_LIB") or (Path(__file__).resolve().parent / "libspmv_b200.so"))
 
 F32, F64 = 0, 1
 

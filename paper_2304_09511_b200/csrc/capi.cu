@@ -141,12 +141,20 @@ static int env_int(const char* name, int dflt) {
   if (!v || !*v) return dflt;
   return atoi(v);
 }
+// 0 = let the plan choose (CSR: 1024 when the matrix has long rows, more
+// CTAs per SM hide the long-row gathers; 2048 otherwise; COO: 2048).
 int tile_entries() {
   static const int t = [] {
-    const int v = env_int("SPMV_TILE", 2048);
-    return (v == 1024) ? 1024 : 2048;
+    const int v = env_int("SPMV_TILE", 0);
+    return (v == 1024 || v == 2048) ? v : 0;
   }();
   return t;
+}
+// Experiments: bit0 = products mode allowed (off by default: measured slower
+// on Zipf), bit1 = one warp per long segment instead of 256-entry units.
+int tile_mode_flags() {
+  static const int f = env_int("SPMV_TILE_MODE", 0);
+  return f;
 }
 int ctas_per_sm_cap() {
   static const int c = env_int("SPMV_CTAS_PER_SM", 0);

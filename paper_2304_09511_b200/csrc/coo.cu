@@ -44,6 +44,7 @@ struct CooParams {
   T* head_val;
   T* tail_val;
   int64_t nrows, nnz, col_base, ntiles, n_bulk;
+  int mode;
 };
 
 template <typename T, int TILE>
@@ -56,7 +57,11 @@ struct CooSmem {
   static constexpr size_t starts_bytes = align_up(sizeof(uint16_t) * (TILE + 1), 128);
   static constexpr size_t long_bytes = align_up(sizeof(LongSeg) * max_long_segs<TILE>(), 128);
   static constexpr size_t counts_bytes = align_up(sizeof(int) * 2 * 64, 128);
-  static constexpr size_t header = 128 + starts_bytes + long_bytes + counts_bytes;
+  static constexpr size_t units_bytes = align_up(sizeof(LongUnit) * max_units<TILE>(), 128);
+  static constexpr size_t upart_bytes = align_up(sizeof(T) * max_units<TILE>(), 128);
+  static constexpr size_t spart_bytes = align_up(sizeof(T) * max_long_segs<TILE>(), 128);
+  static constexpr size_t header = 128 + starts_bytes + long_bytes + counts_bytes + units_bytes + upart_bytes +
+                                   spart_bytes;
   static constexpr size_t total = header + kTileStages * stage_bytes;
   static_assert(rounds * (kTileThreads / 32) <= 64, "segment scan covers at most 64 warp counts");
 };
@@ -64,7 +69,7 @@ struct CooSmem {
 // rows: tile-relative view, valid for k in [-kExt, TILE + kExt).
 template <typename T, int TILE>
 __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_t* __restrict__ rows,
-                                 const uint32_t* __restrict__ cols, const T* __restrict__ vals, uint16_t* s_start,
+                                 const uint32_t* __restrict__ cols, T* __restrict__ vals, uint16_t* s_start,
                                  LongSeg* s_long, int* s_nseg, int* s_nlong, int* s_wcnt) {
   constexpr int R = TILE / kTileThreads;
   constexpr int W = kTileThreads / 32;
@@ -116,6 +121,13 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
   }
   __syncthreads();
   const int nseg = *s_nseg;
+  // Many short rows (more segments than threads): issue the whole tile's
+  // gathers entry-per-lane first (see tile.cuh form_products).
+  const bool products = (P.mode & 1) && nseg > kTileThreads;
+  if (products) {
+    form_products(cols, vals, cnt_ext, xb);
+    __syncthreads();
+  }
 
   // 3. one thread per segment: short owned rows summed left to right from
   //    +0.0 (np.add.at order); long ones queued; empty rows zero-filled.
@@ -142,41 +154,55 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
       L.row = r;
       L.lo = uint32_t(k0);
       L.hi = uint32_t(k1);
-      L.flags = (cont_before ? 1u : 0u) | ((after > 0) ? 2u : 0u);
+      L.flags = (cont_before ? 1u : 0u) | ((after > 0) ? 2u : 0u) | (products ? 4u : 0u);
       L.s = L.e = 0;
       s_long[idx] = L;
     } else if (!cont_before) {
       // +0.0 seed: np.add.at accumulates into a zeroed y
-      P.y[r] = row_dot(cols + k0, vals + k0, k1 + after - k0, xb, T(0));
+      P.y[r] = products ? row_sum(vals + k0, k1 + after - k0, T(0))
+                        : row_dot(cols + k0, vals + k0, k1 + after - k0, xb, T(0));
     }
   }
   __syncthreads();
 
-  // 4. long segments: one warp each (vla-32 order); cross-tile parts go to
-  //    the carry slots for coo_fixup_kernel.
-  const int nl = *s_nlong;
-  for (int i = warp; i < nl; i += kTileThreads / 32) {
+  __syncthreads();
+}
+
+// 4. long segments (out of line): units over all warps (vla-32 order inside
+//    a unit); cross-tile parts go to the carry slots for coo_fixup_kernel.
+template <typename T, int TILE>
+__device__ __forceinline__ void coo_tile_long(int64_t t, const uint32_t* __restrict__ cols, const T* __restrict__ vals,
+                                           const LongSeg* __restrict__ s_long, int nl, unsigned char* scratch,
+                                           int* s_nunits, const T* __restrict__ xb, T* __restrict__ y,
+                                           uint32_t* head_row, T* head_val, uint32_t* pass, uint32_t* tail_row,
+                                           T* tail_val, bool warp_per_seg) {
+  using S = CooSmem<T, TILE>;
+  LongUnit* units = reinterpret_cast<LongUnit*>(scratch);
+  T* unit_part = reinterpret_cast<T*>(scratch + S::units_bytes);
+  T* seg_part = reinterpret_cast<T*>(scratch + S::units_bytes + S::upart_bytes);
+  const bool products = s_long[0].flags & 4u;
+  reduce_long_segments<T, TILE>(cols, vals, s_long, nl, units, unit_part, s_nunits, seg_part, xb, products,
+                                warp_per_seg);
+  for (int i = threadIdx.x; i < nl; i += kTileThreads) {
     const LongSeg L = s_long[i];
-    const T part = warp_segment_dot(cols, vals, L.lo, L.hi, lane, xb);
-    if (lane == 0) {
-      const bool cb = L.flags & 1u, ca = L.flags & 2u;
-      if (!cb && !ca) {
-        P.y[L.row] = part;
-      } else if (cb) {
-        P.head_row[t] = L.row;
-        P.head_val[t] = part;
-        P.pass[t] = ca ? 1u : 0u;
-      } else {
-        P.tail_row[t] = L.row;
-        P.tail_val[t] = part;
-      }
+    const T part = seg_part[i];
+    const bool cb = L.flags & 1u, ca = L.flags & 2u;
+    if (!cb && !ca) {
+      y[L.row] = part;
+    } else if (cb) {
+      head_row[t] = L.row;
+      head_val[t] = part;
+      pass[t] = ca ? 1u : 0u;
+    } else {
+      tail_row[t] = L.row;
+      tail_val[t] = part;
     }
   }
 }
 
 template <typename T, bool BULK, int TILE>
-__global__ void __launch_bounds__(kTileThreads)
-coo_tile_kernel(const CooParams<T> P) {
+__global__ void __launch_bounds__(kTileThreads, 3)
+coo_tile_kernel(const __grid_constant__ CooParams<T> P) {
   extern __shared__ __align__(128) unsigned char smem[];
   using S = CooSmem<T, TILE>;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
@@ -185,6 +211,7 @@ coo_tile_kernel(const CooParams<T> P) {
   uint16_t* s_start = reinterpret_cast<uint16_t*>(smem + 128);
   LongSeg* s_long = reinterpret_cast<LongSeg*>(smem + 128 + S::starts_bytes);
   int* s_wcnt = reinterpret_cast<int*>(smem + 128 + S::starts_bytes + S::long_bytes);
+  unsigned char* scratch = reinterpret_cast<unsigned char*>(s_wcnt) + S::counts_bytes;
   unsigned char* stages = smem + S::header;
   const int tid = threadIdx.x;
   auto rows_of = [&](int s) { return reinterpret_cast<uint32_t*>(stages + s * S::stage_bytes); };
@@ -192,70 +219,73 @@ coo_tile_kernel(const CooParams<T> P) {
   auto vals_of = [&](int s) {
     return reinterpret_cast<T*>(stages + s * S::stage_bytes + S::rows_bytes + S::cols_bytes);
   };
-  // Row slots the copy did not fill: the window before tile 0 and past nnz.
-  auto pad_rows = [&](uint32_t* rb, int64_t t) {
-    const int64_t E0 = t * TILE;
-    const int cnt_ext = int(min(int64_t(TILE + kExt), P.nnz - E0));
-    if (t == 0)
-      for (int k = tid; k < kExt; k += kTileThreads) rb[k] = kNoRow;
-    for (int k = cnt_ext + tid; k < TILE + kExt; k += kTileThreads) rb[kExt + k] = kNoRow;
-  };
 
-  int64_t n_bulk = BULK ? P.n_bulk : 0;
+  const int64_t n_bulk = BULK ? P.n_bulk : 0;
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t mine_bulk = first < n_bulk ? (n_bulk - 1 - first) / stride + 1 : 0;
+  const int64_t tail0 = n_bulk + first;
+  const int64_t mine_tail = tail0 < P.ntiles ? (P.ntiles - 1 - tail0) / stride + 1 : 0;
+  auto issue = [&](int64_t i) {
+    const int64_t t = first + i * stride;
+    const int64_t E0 = t * TILE;
+    const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
+    const uint32_t pre = t > 0 ? uint32_t(kExt) : 0u;
+    const int s = int(i % kTileStages);
+    mbar_arrive_expect_tx(&bars[s], (cnt + pre) * 4u + cnt * (4u + uint32_t(sizeof(T))));
+    bulk_g2s(rows_of(s) + (kExt - pre), P.ai + E0 - pre, (cnt + pre) * 4u, &bars[s]);
+    bulk_g2s(cols_of(s), P.aj + E0, cnt * 4u, &bars[s]);
+    bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s]);
+  };
   if (BULK) {
     if (tid == 0) {
       for (int s = 0; s < kTileStages; ++s) mbar_init(&bars[s], 1);
       mbar_fence_init();
     }
     __syncthreads();
-    const int64_t first = blockIdx.x, stride = gridDim.x;
-    const int64_t mine = first < n_bulk ? (n_bulk - 1 - first) / stride + 1 : 0;
-    auto issue = [&](int64_t i) {
-      const int64_t t = first + i * stride;
-      const int64_t E0 = t * TILE;
-      const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
-      const uint32_t pre = t > 0 ? uint32_t(kExt) : 0u;
-      const int s = int(i % kTileStages);
-      mbar_arrive_expect_tx(&bars[s], (cnt + pre) * 4u + cnt * (4u + uint32_t(sizeof(T))));
-      bulk_g2s(rows_of(s) + (kExt - pre), P.ai + E0 - pre, (cnt + pre) * 4u, &bars[s]);
-      bulk_g2s(cols_of(s), P.aj + E0, cnt * 4u, &bars[s]);
-      bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s]);
-    };
     if (tid == 0)
-      for (int64_t i = 0; i < kTileStages && i < mine; ++i) issue(i);
-    for (int64_t i = 0; i < mine; ++i) {
-      const int s = int(i % kTileStages);
-      const int64_t t = first + i * stride;
-      mbar_wait(&bars[s], uint32_t((i / kTileStages) & 1));
-      pad_rows(rows_of(s), t);
-      __syncthreads();
-      coo_process_tile<T, TILE>(P, t, rows_of(s) + kExt, cols_of(s), vals_of(s), s_start, s_long, s_nseg, s_nlong,
-                                s_wcnt);
-      __syncthreads();
-      if (tid == 0 && i + kTileStages < mine) {
-        fence_proxy_async();
-        issue(i + kTileStages);
-      }
-    }
+      for (int64_t i = 0; i < kTileStages && i < mine_bulk; ++i) issue(i);
   }
-  for (int64_t t = n_bulk + blockIdx.x; t < P.ntiles; t += gridDim.x) {
-    const int64_t E0 = t * TILE;
-    const int cnt = int(min(int64_t(TILE + kExt), P.nnz - E0));
-    uint32_t* rb = rows_of(0);
-    uint32_t* c = cols_of(0);
-    T* v = vals_of(0);
-    for (int k = tid - kExt; k < cnt; k += kTileThreads) {
-      const int64_t g = E0 + k;
-      if (g >= 0) rb[kExt + k] = P.ai[g];
-      if (k >= 0) {
-        c[k] = P.aj[g];
-        v[k] = P.av[g];
+  for (int64_t i = 0; i < mine_bulk + mine_tail; ++i) {
+    int s = 0;
+    int64_t t;
+    if (i < mine_bulk) {
+      s = int(i % kTileStages);
+      t = first + i * stride;
+      mbar_wait(&bars[s], uint32_t((i / kTileStages) & 1));
+    } else {
+      t = tail0 + (i - mine_bulk) * stride;
+      const int64_t E0 = t * TILE;
+      const int cnt = int(min(int64_t(TILE + kExt), P.nnz - E0));
+      for (int k = tid - kExt; k < cnt; k += kTileThreads) {
+        const int64_t g = E0 + k;
+        if (g >= 0) rows_of(0)[kExt + k] = P.ai[g];
+        if (k >= 0) {
+          cols_of(0)[k] = P.aj[g];
+          vals_of(0)[k] = P.av[g];
+        }
       }
     }
-    pad_rows(rb, t);
+    // Row slots the copy did not fill: the window before tile 0, past nnz.
+    {
+      const int64_t E0 = t * TILE;
+      const int cnt_ext = int(min(int64_t(TILE + kExt), P.nnz - E0));
+      uint32_t* rb = rows_of(s);
+      if (t == 0)
+        for (int k = tid; k < kExt; k += kTileThreads) rb[k] = kNoRow;
+      for (int k = cnt_ext + tid; k < TILE + kExt; k += kTileThreads) rb[kExt + k] = kNoRow;
+    }
     __syncthreads();
-    coo_process_tile<T, TILE>(P, t, rb + kExt, c, v, s_start, s_long, s_nseg, s_nlong, s_wcnt);
-    __syncthreads();
+    coo_process_tile<T, TILE>(P, t, rows_of(s) + kExt, cols_of(s), vals_of(s), s_start, s_long, s_nseg, s_nlong,
+                              s_wcnt);
+    const int nl = *s_nlong;
+    if (nl > 0)
+      coo_tile_long<T, TILE>(t, cols_of(s), vals_of(s), s_long, nl, scratch, s_nlong + 1, P.x - P.col_base, P.y,
+                             P.head_row, P.head_val, P.pass, P.tail_row, P.tail_val, (P.mode & 2) != 0);
+    __syncthreads();  // stage s free
+    if (BULK && tid == 0 && i + kTileStages < mine_bulk) {
+      fence_proxy_async();
+      issue(i + kTileStages);
+    }
   }
 }
 
@@ -521,7 +551,7 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
   SPMV_CUDA_TRY(cudaMemcpyAsync(&h, nl.ptr, 8, cudaMemcpyDeviceToHost, st));
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
   p->n_long = int64_t(h);
-  p->tile = tile_entries();
+  p->tile = tile_entries() ? tile_entries() : 2048;
   p->ntiles = (nnz + p->tile - 1) / p->tile;
   const size_t vs = value_size(p->dtype);
   if ((rc = p->head_row.alloc(4 * p->ntiles)) || (rc = p->tail_row.alloc(4 * p->ntiles)) ||
@@ -561,6 +591,7 @@ static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint3
   P.nnz = p->nnz;
   P.col_base = col_base;
   P.ntiles = p->ntiles;
+  P.mode = tile_mode_flags();
   const bool aligned = (reinterpret_cast<uintptr_t>(ai) % 16 == 0) && (reinterpret_cast<uintptr_t>(aj) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;

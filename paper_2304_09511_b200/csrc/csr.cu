@@ -38,9 +38,9 @@ struct CsrParams {
   const uint32_t* row_lo;  // ntiles + 1: first row of each tile's row range
   T* head;
   T* tail;
-  uint32_t* cnt;
   int64_t nrows, nnz, col_base, ntiles, n_bulk;
   int exact_len;
+  int mode;
 };
 
 template <typename T, int TILE>
@@ -48,20 +48,27 @@ struct CsrSmem {
   static constexpr size_t cols_bytes = align_up(sizeof(uint32_t) * (TILE + kExt), 128);
   static constexpr size_t vals_bytes = align_up(sizeof(T) * (TILE + kExt), 128);
   static constexpr size_t stage_bytes = cols_bytes + vals_bytes;
-  static constexpr size_t header = align_up(64 + sizeof(LongSeg) * max_long_segs<TILE>(), 128);
+  static constexpr size_t segs_off = 64;
+  static constexpr size_t units_off = segs_off + align_up(sizeof(LongSeg) * max_long_segs<TILE>(), 16);
+  static constexpr size_t upart_off = units_off + align_up(sizeof(LongUnit) * max_units<TILE>(), 16);
+  static constexpr size_t spart_off = upart_off + align_up(sizeof(T) * max_units<TILE>(), 16);
+  static constexpr size_t header = align_up(spart_off + sizeof(T) * max_long_segs<TILE>(), 128);
   static constexpr size_t total = header + kTileStages * stage_bytes;
 };
 
+// Rows of one tile.  Row-per-lane mode (few rows per tile, e.g. the
+// stencil's ~77): each thread forms its row's products from the staged
+// entries, so a warp's gathers hit consecutive x.  Products mode (more rows
+// than threads, e.g. Zipf's short rows): all gathers of the tile are issued
+// entry-per-lane first, then rows are summed from shared memory.  Long
+// segments are only queued here.
 template <typename T, int TILE>
-__device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_t* __restrict__ cols,
-                                 const T* __restrict__ vals, LongSeg* s_long, int* s_nlong) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+__device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, const uint32_t* __restrict__ cols,
+                                              T* __restrict__ vals, LongSeg* s_long, int* s_nlong) {
+  const int tid = threadIdx.x;
   const int64_t E0 = t * TILE;
-  const int cnt_ext = int(min(int64_t(TILE + kExt), P.nnz - E0));
   const int64_t E1 = E0 + TILE;
   const T* xb = P.x - P.col_base;
-
-  // Row range of the tile (the first row's pointers are loaded up front).
   const int64_t R0 = t == 0 ? 0 : int64_t(P.row_lo[t]);
   const int64_t R1 = P.row_lo[t + 1];
   const int64_t rend = R1 < P.nrows ? R1 + 1 : P.nrows;
@@ -71,20 +78,19 @@ __device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_
     s = __ldg(P.irp + r);
     e = __ldg(P.irp + r + 1);
   }
-
+  const bool products = (P.mode & 1) && (rend - R0) > kTileThreads;
+  if (products) form_products(cols, vals, int(min(int64_t(TILE + kExt), P.nnz - E0)), xb);
   if (tid == 0) *s_nlong = 0;
   __syncthreads();
-
-  // Rows: short ones summed here, long segments queued for the warps.
   while (r < rend) {
     const uint32_t len = e - s;
     if (len == 0) {
       if (r < R1) P.y[r] = T(0);
     } else if (len <= uint32_t(P.exact_len)) {
-      if (int64_t(s) >= E0 && int64_t(s) < E1) {
+      if (int64_t(s) >= E0 && int64_t(s) < E1)
         // -0.0 seed: the sum starts from the first product, like cumsum
-        P.y[r] = row_dot(cols + (s - E0), vals + (s - E0), int(len), xb, T(-0.0));
-      }
+        P.y[r] = products ? row_sum(vals + (s - E0), int(len), T(-0.0))
+                          : row_dot(cols + (s - E0), vals + (s - E0), int(len), xb, T(-0.0));
     } else {
       const int64_t lo = max(int64_t(s), E0), hi = min(int64_t(e), E1);
       if (lo < hi) {
@@ -93,7 +99,7 @@ __device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_
         L.row = uint32_t(r);
         L.lo = uint32_t(lo - E0);
         L.hi = uint32_t(hi - E0);
-        L.flags = 0;
+        L.flags = products ? 1u : 0u;
         L.s = s;
         L.e = e;
         s_long[idx] = L;
@@ -106,91 +112,131 @@ __device__ void csr_process_tile(const CsrParams<T>& P, int64_t t, const uint32_
     }
   }
   __syncthreads();
+}
 
-  const int nl = *s_nlong;
-  for (int i = warp; i < nl; i += kTileThreads / 32) {
+// Long segments of one tile.  A row inside the tile is written directly; a
+// row spanning tiles leaves its partial in tail[t] (the tile holding its
+// first entry) or head[t] (later tiles); csr_span_fixup_kernel adds them in
+// tile order after the tile kernel (no fences or atomics in the hot kernel).
+template <typename T, int TILE>
+__device__ __forceinline__ void csr_tile_long(int64_t t, const uint32_t* __restrict__ cols, const T* __restrict__ vals,
+                                           const LongSeg* __restrict__ s_long, int nl, unsigned char* scratch,
+                                           int* s_nunits, const T* __restrict__ xb, T* __restrict__ y,
+                                           T* __restrict__ head, T* __restrict__ tail, bool warp_per_seg) {
+  using S = CsrSmem<T, TILE>;
+  LongUnit* units = reinterpret_cast<LongUnit*>(scratch + S::units_off);
+  T* unit_part = reinterpret_cast<T*>(scratch + S::upart_off);
+  T* seg_part = reinterpret_cast<T*>(scratch + S::spart_off);
+  const bool products = s_long[0].flags & 1u;
+  reduce_long_segments<T, TILE>(cols, vals, s_long, nl, units, unit_part, s_nunits, seg_part, xb, products,
+                                warp_per_seg);
+  const int64_t E0 = t * TILE, E1 = E0 + TILE;
+  for (int i = threadIdx.x; i < nl; i += kTileThreads) {
     const LongSeg L = s_long[i];
-    const T part = warp_segment_dot(cols, vals, L.lo, L.hi, lane, xb);
-    if (lane == 0) {
-      if (int64_t(L.s) >= E0 && int64_t(L.e) <= E1) {
-        P.y[L.row] = part;
-      } else {
-        const int64_t t0 = L.s / TILE, t1 = (int64_t(L.e) - 1) / TILE;
-        if (t == t0)
-          P.tail[t] = part;
-        else
-          P.head[t] = part;
-        __threadfence();
-        const uint32_t ticket = atomicAdd(P.cnt + t0, 1u);
-        if (ticket == uint32_t(t1 - t0)) {
-          __threadfence();
-          T sum = __ldcg(P.tail + t0);
-          for (int64_t u = t0 + 1; u <= t1; ++u) sum = add_rn(sum, __ldcg(P.head + u));
-          P.y[L.row] = sum;
-          P.cnt[t0] = 0;  // ready for the next product
-        }
-      }
-    }
+    const T part = seg_part[i];
+    if (int64_t(L.s) >= E0 && int64_t(L.e) <= E1)
+      y[L.row] = part;
+    else if (int64_t(L.s) >= E0)
+      tail[t] = part;  // the row starts here and continues: csr_span_fixup_kernel adds the rest
+    else
+      head[t] = part;
   }
 }
 
 template <typename T, bool BULK, int TILE>
-__global__ void __launch_bounds__(kTileThreads)
-csr_tile_kernel(const CsrParams<T> P) {
+__global__ void __launch_bounds__(kTileThreads, 4)
+csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
   extern __shared__ __align__(128) unsigned char smem[];
   using S = CsrSmem<T, TILE>;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   int* s_nlong = reinterpret_cast<int*>(smem + 32);
-  LongSeg* s_long = reinterpret_cast<LongSeg*>(smem + 64);
+  LongSeg* s_long = reinterpret_cast<LongSeg*>(smem + S::segs_off);
   unsigned char* stages = smem + S::header;
   const int tid = threadIdx.x;
   auto cols_of = [&](int s) { return reinterpret_cast<uint32_t*>(stages + s * S::stage_bytes); };
   auto vals_of = [&](int s) { return reinterpret_cast<T*>(stages + s * S::stage_bytes + S::cols_bytes); };
 
-  int64_t n_bulk = BULK ? P.n_bulk : 0;
+  // This CTA's tiles: bulk-copyable ones first (TMA pipeline), then the
+  // tail tiles the bulk engine cannot address (cooperative loads).
+  const int64_t n_bulk = BULK ? P.n_bulk : 0;
+  const int64_t first = blockIdx.x, stride = gridDim.x;
+  const int64_t mine_bulk = first < n_bulk ? (n_bulk - 1 - first) / stride + 1 : 0;
+  const int64_t tail0 = n_bulk + first;
+  const int64_t mine_tail = tail0 < P.ntiles ? (P.ntiles - 1 - tail0) / stride + 1 : 0;
+  auto issue = [&](int64_t i) {
+    const int64_t E0 = (first + i * stride) * TILE;
+    const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
+    const int s = int(i % kTileStages);
+    mbar_arrive_expect_tx(&bars[s], cnt * uint32_t(sizeof(uint32_t) + sizeof(T)));
+    bulk_g2s(cols_of(s), P.aj + E0, cnt * uint32_t(sizeof(uint32_t)), &bars[s]);
+    bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s]);
+  };
   if (BULK) {
     if (tid == 0) {
       for (int s = 0; s < kTileStages; ++s) mbar_init(&bars[s], 1);
       mbar_fence_init();
     }
     __syncthreads();
-    const int64_t first = blockIdx.x, stride = gridDim.x;
-    const int64_t mine = first < n_bulk ? (n_bulk - 1 - first) / stride + 1 : 0;
-    auto issue = [&](int64_t i) {
-      const int64_t t = first + i * stride;
-      const int64_t E0 = t * TILE;
-      const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
-      const int s = int(i % kTileStages);
-      mbar_arrive_expect_tx(&bars[s], cnt * uint32_t(sizeof(uint32_t) + sizeof(T)));
-      bulk_g2s(cols_of(s), P.aj + E0, cnt * uint32_t(sizeof(uint32_t)), &bars[s]);
-      bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s]);
-    };
     if (tid == 0)
-      for (int64_t i = 0; i < kTileStages && i < mine; ++i) issue(i);
-    for (int64_t i = 0; i < mine; ++i) {
-      const int s = int(i % kTileStages);
+      for (int64_t i = 0; i < kTileStages && i < mine_bulk; ++i) issue(i);
+  }
+  for (int64_t i = 0; i < mine_bulk + mine_tail; ++i) {
+    int s = 0;
+    int64_t t;
+    if (i < mine_bulk) {
+      s = int(i % kTileStages);
+      t = first + i * stride;
       mbar_wait(&bars[s], uint32_t((i / kTileStages) & 1));
-      csr_process_tile<T, TILE>(P, first + i * stride, cols_of(s), vals_of(s), s_long, s_nlong);
-      __syncthreads();
-      if (tid == 0 && i + kTileStages < mine) {
-        fence_proxy_async();
-        issue(i + kTileStages);
+    } else {
+      t = tail0 + (i - mine_bulk) * stride;
+      const int64_t E0 = t * TILE;
+      const int cnt = int(min(int64_t(TILE + kExt), P.nnz - E0));
+      for (int k = tid; k < cnt; k += kTileThreads) {
+        cols_of(0)[k] = P.aj[E0 + k];
+        vals_of(0)[k] = P.av[E0 + k];
       }
+      __syncthreads();
+    }
+    csr_tile_rows<T, TILE>(P, t, cols_of(s), vals_of(s), s_long, s_nlong);
+    const int nl = *s_nlong;
+    if (nl > 0)
+      csr_tile_long<T, TILE>(t, cols_of(s), vals_of(s), s_long, nl, smem, s_nlong + 1, P.x - P.col_base, P.y,
+                             P.head, P.tail, (P.mode & 2) != 0);
+    __syncthreads();  // stage s free
+    if (BULK && tid == 0 && i + kTileStages < mine_bulk) {
+      fence_proxy_async();
+      issue(i + kTileStages);
     }
   }
-  // Tiles the bulk engine cannot address: cooperative loads into stage 0.
-  for (int64_t t = n_bulk + blockIdx.x; t < P.ntiles; t += gridDim.x) {
-    const int64_t E0 = t * TILE;
-    const int cnt = int(min(int64_t(TILE + kExt), P.nnz - E0));
-    uint32_t* c = cols_of(0);
-    T* v = vals_of(0);
-    for (int k = tid; k < cnt; k += kTileThreads) {
-      c[k] = P.aj[E0 + k];
-      v[k] = P.av[E0 + k];
+}
+
+// Rows spanning tiles: y = tail[t0] + head[t0+1] + ... + head[t1].
+template <typename T>
+__global__ void csr_span_fixup_kernel(const uint32_t* __restrict__ span_row, const uint32_t* __restrict__ span_t0,
+                                      const uint32_t* __restrict__ span_t1, int64_t n_span, const T* __restrict__ head,
+                                      const T* __restrict__ tail, T* __restrict__ y) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_span; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t t0 = span_t0[i], t1 = span_t1[i];
+    T sum = tail[t0];
+    for (uint32_t u = t0 + 1; u <= t1; ++u) sum = add_rn(sum, head[u]);
+    y[span_row[i]] = sum;
+  }
+}
+
+__global__ void csr_span_list_kernel(const uint32_t* __restrict__ irp, int64_t nrows, int exact_len, int64_t tile,
+                                     uint32_t* __restrict__ span_row, uint32_t* __restrict__ span_t0,
+                                     uint32_t* __restrict__ span_t1, unsigned long long* __restrict__ n_span) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t s = irp[r], e = irp[r + 1];
+    if (e - s <= uint32_t(exact_len)) continue;
+    const uint64_t t0 = s / uint64_t(tile), t1 = (uint64_t(e) - 1) / uint64_t(tile);
+    if (t0 == t1) continue;
+    const unsigned long long k = atomicAdd(n_span, 1ull);
+    if (span_row) {
+      span_row[k] = uint32_t(r);
+      span_t0[k] = uint32_t(t0);
+      span_t1[k] = uint32_t(t1);
     }
-    __syncthreads();
-    csr_process_tile<T, TILE>(P, t, c, v, s_long, s_nlong);
-    __syncthreads();
   }
 }
 
@@ -290,6 +336,8 @@ struct spmv_csr_plan {
   int exact_len = kExactLen;
   int64_t n_long = 0;
   DevBuf row_lo, head, tail, cnt;
+  DevBuf span_row, span_t0, span_t1;
+  int64_t n_span = 0;
   int grid_bulk = 0, grid_direct = 0;
 };
 
@@ -328,12 +376,12 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
   P.row_lo = p->row_lo.as<uint32_t>();
   P.head = p->head.as<T>();
   P.tail = p->tail.as<T>();
-  P.cnt = p->cnt.as<uint32_t>();
   P.nrows = p->nrows;
   P.nnz = p->nnz;
   P.col_base = col_base;
   P.ntiles = p->ntiles;
   P.exact_len = p->exact_len;
+  P.mode = tile_mode_flags();
   const bool aligned = (reinterpret_cast<uintptr_t>(aj) % 16 == 0) && (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
   const size_t smem = CsrSmem<T, TILE>::total;
@@ -342,6 +390,12 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
   else
     csr_tile_kernel<T, false, TILE><<<unsigned(p->grid_direct), kTileThreads, smem, st>>>(P);
   SPMV_LAUNCH_CHECK();
+  if (p->n_span > 0) {
+    const int64_t g = std::min<int64_t>((p->n_span + 255) / 256, int64_t(sm_count()) * 8);
+    csr_span_fixup_kernel<T><<<unsigned(g), 256, 0, st>>>(p->span_row.as<uint32_t>(), p->span_t0.as<uint32_t>(),
+                                                          p->span_t1.as<uint32_t>(), p->n_span, P.head, P.tail, y);
+    SPMV_LAUNCH_CHECK();
+  }
   return SPMV_OK;
 }
 
@@ -350,6 +404,60 @@ static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* 
                    int64_t col_base, T* y, cudaStream_t st) {
   if (p->tile == 1024) return csr_run_tiled<T, 1024>(p, irp, aj, av, x, col_base, y, st);
   return csr_run_tiled<T, 2048>(p, irp, aj, av, x, col_base, y, st);
+}
+
+static int count_async(unsigned long long* dev, unsigned long long* host, cudaStream_t st) {
+  SPMV_CUDA_TRY(cudaMemcpyAsync(host, dev, 8, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  return SPMV_OK;
+}
+
+// Plan analysis (once per matrix): long-row census, tile size, per-tile row
+// ranges and the list of long rows spanning tiles.
+static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st) {
+  const int64_t nrows = p->nrows;
+  unsigned long long* ctr = p->cnt.as<unsigned long long>();
+  unsigned long long h = 0;
+  int rc;
+  const int64_t g_rows = std::min<int64_t>((nrows + 255) / 256, int64_t(sm_count()) * 16);
+  SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
+  count_long_rows_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, p->exact_len, ctr);
+  SPMV_LAUNCH_CHECK();
+  if ((rc = count_async(ctr, &h, st))) return rc;
+  p->n_long = int64_t(h);
+  // Long rows leave gathers to the warps: smaller tiles keep more CTAs per SM.
+  p->tile = tile_entries() ? tile_entries() : (p->n_long > 0 ? 1024 : 2048);
+  p->ntiles = (p->nnz + p->tile - 1) / p->tile;
+  const size_t vs = value_size(p->dtype);
+  if ((rc = p->row_lo.alloc(4 * (p->ntiles + 1))) || (rc = p->head.alloc(vs * p->ntiles)) ||
+      (rc = p->tail.alloc(vs * p->ntiles)))
+    return rc;
+  const int64_t g_tiles = std::min<int64_t>((p->ntiles + 256) / 256, int64_t(sm_count()) * 16);
+  csr_row_lo_kernel<<<unsigned(g_tiles), 256, 0, st>>>(irp, nrows, p->ntiles, p->tile, p->row_lo.as<uint32_t>());
+  SPMV_LAUNCH_CHECK();
+  if (p->n_long > 0) {
+    // two passes: count, then fill (order is irrelevant: rows are independent)
+    SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
+    csr_span_list_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, p->exact_len, p->tile, nullptr, nullptr,
+                                                             nullptr, ctr);
+    SPMV_LAUNCH_CHECK();
+    if ((rc = count_async(ctr, &h, st))) return rc;
+    p->n_span = int64_t(h);
+    if (p->n_span > 0) {
+      if ((rc = p->span_row.alloc(4 * p->n_span)) || (rc = p->span_t0.alloc(4 * p->n_span)) ||
+          (rc = p->span_t1.alloc(4 * p->n_span)))
+        return rc;
+      SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
+      csr_span_list_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, p->exact_len, p->tile,
+                                                               p->span_row.as<uint32_t>(), p->span_t0.as<uint32_t>(),
+                                                               p->span_t1.as<uint32_t>(), ctr);
+      SPMV_LAUNCH_CHECK();
+    }
+  }
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  if (p->tile == 1024)
+    return p->dtype == SPMV_F64 ? csr_launch_config<double, 1024>(p) : csr_launch_config<float, 1024>(p);
+  return p->dtype == SPMV_F64 ? csr_launch_config<double, 2048>(p) : csr_launch_config<float, 2048>(p);
 }
 
 extern "C" {
@@ -371,45 +479,8 @@ int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, c
   p->ncols = ncols;
   p->nnz = nnz;
   p->exact_len = exact_len;
-  p->tile = tile_entries();
-  p->ntiles = (nnz + p->tile - 1) / p->tile;
-  int rc = SPMV_OK;
-  const size_t vs = value_size(dtype);
-  if (nrows > 0 && nnz > 0) {
-    if (!rc) rc = p->row_lo.alloc(4 * (p->ntiles + 1));
-    if (!rc) rc = p->head.alloc(vs * p->ntiles);
-    if (!rc) rc = p->tail.alloc(vs * p->ntiles);
-    if (!rc) rc = p->cnt.alloc(4 * p->ntiles);
-    DevBuf nl;
-    if (!rc) rc = nl.alloc(8);
-    if (!rc) {
-      cudaError_t e = cudaMemsetAsync(p->cnt.ptr, 0, 4 * p->ntiles, st);
-      if (e == cudaSuccess) e = cudaMemsetAsync(nl.ptr, 0, 8, st);
-      const int64_t g1 = std::min<int64_t>((p->ntiles + 256) / 256, int64_t(sm_count()) * 16);
-      if (e == cudaSuccess) {
-        csr_row_lo_kernel<<<unsigned(g1), 256, 0, st>>>(row_pointers, nrows, p->ntiles, p->tile,
-                                                         p->row_lo.as<uint32_t>());
-        e = cudaGetLastError();
-      }
-      const int64_t g2 = std::min<int64_t>((nrows + 255) / 256, int64_t(sm_count()) * 16);
-      if (e == cudaSuccess) {
-        count_long_rows_kernel<<<unsigned(g2), 256, 0, st>>>(row_pointers, nrows, exact_len,
-                                                             nl.as<unsigned long long>());
-        e = cudaGetLastError();
-      }
-      unsigned long long h = 0;
-      if (e == cudaSuccess) e = cudaMemcpyAsync(&h, nl.ptr, 8, cudaMemcpyDeviceToHost, st);
-      if (e == cudaSuccess) e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "CSR plan: %s", cudaGetErrorString(e));
-      p->n_long = int64_t(h);
-    }
-    if (!rc) {
-      if (p->tile == 1024)
-        rc = dtype == SPMV_F64 ? csr_launch_config<double, 1024>(p) : csr_launch_config<float, 1024>(p);
-      else
-        rc = dtype == SPMV_F64 ? csr_launch_config<double, 2048>(p) : csr_launch_config<float, 2048>(p);
-    }
-  }
+  int rc = p->cnt.alloc(8);  // scratch counter
+  if (!rc && nrows > 0 && nnz > 0) rc = csr_plan_build(p, row_pointers, st);
   if (rc) {
     delete p;
     return rc;
@@ -427,7 +498,7 @@ int spmv_csr_plan_info(const spmv_csr_plan* p, int64_t* n_long_rows, int64_t* n_
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (n_long_rows) *n_long_rows = p->n_long;
   if (n_items) *n_items = p->tile;
-  if (launches) *launches = p->nrows > 0 ? 1 : 0;
+  if (launches) *launches = (p->nrows > 0 ? 1 : 0) + (p->n_span > 0 ? 1 : 0);
   return SPMV_OK;
 }
 

@@ -24,6 +24,7 @@ constexpr int max_long_segs() { return TILE / (kExactLen + 1) + 4; }
 // SM (smaller shared-memory ring); 2048 halves the per-tile overhead.
 int tile_entries();
 int ctas_per_sm_cap();  // 0 = occupancy limit
+int tile_mode_flags();  // experiments: bit0 no products mode, bit1 warp-per-segment long rows
 
 static_assert(kExt == kExactLen, "extension must cover a whole short row");
 
@@ -61,6 +62,129 @@ __device__ __forceinline__ T row_dot(const uint32_t* __restrict__ c, const T* __
   }
   for (; i < len; ++i) acc = add_rn(acc, mul_rn(v[i], __ldg(xb + c[i])));
   return acc;
+}
+
+// Left-to-right sum of already-formed products (the "products" tile mode).
+template <typename T>
+__device__ __forceinline__ T row_sum(const T* __restrict__ p, int len, T acc) {
+  for (int i = 0; i < len; ++i) acc = add_rn(acc, p[i]);
+  return acc;
+}
+
+// Products mode: every thread forms the rounded products of entries
+// tid, tid+256, ... in place (4 gathers in flight).  Used for tiles holding
+// many short rows, where a row per lane would serialise ~1 L2 round trip
+// per row; entry-per-lane issues the whole tile's gathers in parallel.
+template <typename T>
+__device__ __forceinline__ void form_products(const uint32_t* __restrict__ cols, T* __restrict__ vals, int cnt,
+                                              const T* __restrict__ xb) {
+  int k = threadIdx.x;
+  for (; k + 3 * kTileThreads < cnt; k += 4 * kTileThreads) {
+    const uint32_t c0 = cols[k], c1 = cols[k + kTileThreads], c2 = cols[k + 2 * kTileThreads],
+                   c3 = cols[k + 3 * kTileThreads];
+    const T x0 = __ldg(xb + c0), x1 = __ldg(xb + c1), x2 = __ldg(xb + c2), x3 = __ldg(xb + c3);
+    vals[k] = mul_rn(vals[k], x0);
+    vals[k + kTileThreads] = mul_rn(vals[k + kTileThreads], x1);
+    vals[k + 2 * kTileThreads] = mul_rn(vals[k + 2 * kTileThreads], x2);
+    vals[k + 3 * kTileThreads] = mul_rn(vals[k + 3 * kTileThreads], x3);
+  }
+  for (; k < cnt; k += kTileThreads) vals[k] = mul_rn(vals[k], __ldg(xb + cols[k]));
+}
+
+// Long segments of one tile, reduced by all warps of the CTA: every segment
+// is cut into kUnit-entry units (lane-strided vla-32 reduction each); the
+// partials of a segment are then added in unit order by one thread.  A
+// segment of <= kUnit entries is a single unit, so a whole row of 33..kUnit
+// entries inside one tile is bit-exact with spmv_csr_vla(32); longer ones
+// are deterministic and within 1e-12.
+constexpr int kUnit = 256;
+template <int TILE>
+constexpr int max_units() { return TILE / kUnit + max_long_segs<TILE>(); }
+
+struct LongUnit {  // scratch slot; reduce_long_segments stores unit offsets here
+  uint32_t a, b;
+};
+
+// seg_part[i] <- reduction of segment i (i < nl).  Ends with __syncthreads().
+template <typename T, int TILE>
+__device__ __forceinline__ void reduce_long_segments(const uint32_t* __restrict__ cols, const T* __restrict__ vals,
+                                     const LongSeg* __restrict__ segs, int nl, LongUnit* units, T* unit_part,
+                                     int* s_nunits, T* seg_part, const T* __restrict__ xb, bool products,
+                                     bool warp_per_seg = false) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  if (warp_per_seg) {
+    for (int i = warp; i < nl; i += kTileThreads / 32) {
+      T acc = T(0);
+      for (uint32_t j = segs[i].lo + lane; j < segs[i].hi; j += 32)
+        acc = add_rn(acc, products ? vals[j] : mul_rn(vals[j], __ldg(xb + cols[j])));
+      acc = tree_reduce_warp(acc, 32);
+      if (lane == 0) seg_part[i] = acc;
+    }
+    __syncthreads();
+    return;
+  }
+  // unit offsets of the segments: warp 0 scans ceil(len / kUnit), up to
+  // 4 segments per lane (nl <= max_long_segs < 128)
+  int* first = reinterpret_cast<int*>(units);  // first[i] = first unit of segment i, first[nl] = total
+  if (warp == 0) {
+    int cnt[4], sum = 0;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = lane * 4 + q;
+      cnt[q] = i < nl ? int((segs[i].hi - segs[i].lo + kUnit - 1) / kUnit) : 0;
+      sum += cnt[q];
+    }
+    int incl = sum;
+    for (int o = 1; o < 32; o <<= 1) {
+      const int v = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += v;
+    }
+    int run = incl - sum;
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int i = lane * 4 + q;
+      if (i < nl) first[i] = run;
+      run += cnt[q];
+    }
+    if (lane == 31) {
+      first[nl] = incl;
+      *s_nunits = incl;
+    }
+  }
+  __syncthreads();
+  const int nu = *s_nunits;
+  for (int u = warp; u < nu; u += kTileThreads / 32) {
+    int lo_i = 0, hi_i = nl - 1;  // segment of unit u: last i with first[i] <= u
+    while (lo_i < hi_i) {
+      const int mid = (lo_i + hi_i + 1) >> 1;
+      if (first[mid] <= u) lo_i = mid; else hi_i = mid - 1;
+    }
+    const uint32_t ulo = segs[lo_i].lo + uint32_t(u - first[lo_i]) * kUnit;
+    const uint32_t uhi = min(segs[lo_i].hi, ulo + uint32_t(kUnit));
+    T acc = T(0);
+    uint32_t j = ulo + lane;
+    if (products) {
+      for (; j < uhi; j += 32) acc = add_rn(acc, vals[j]);
+    } else {
+      for (; j + 96 < uhi; j += 128) {  // 4 gathers in flight per lane, adds in order
+        const T p0 = mul_rn(vals[j], __ldg(xb + cols[j]));
+        const T p1 = mul_rn(vals[j + 32], __ldg(xb + cols[j + 32]));
+        const T p2 = mul_rn(vals[j + 64], __ldg(xb + cols[j + 64]));
+        const T p3 = mul_rn(vals[j + 96], __ldg(xb + cols[j + 96]));
+        acc = add_rn(add_rn(add_rn(add_rn(acc, p0), p1), p2), p3);
+      }
+      for (; j < uhi; j += 32) acc = add_rn(acc, mul_rn(vals[j], __ldg(xb + cols[j])));
+    }
+    acc = tree_reduce_warp(acc, 32);
+    if (lane == 0) unit_part[u] = acc;
+  }
+  __syncthreads();
+  for (int i = tid; i < nl; i += kTileThreads) {
+    T s = unit_part[first[i]];
+    for (int u = first[i] + 1; u < first[i + 1]; ++u) s = add_rn(s, unit_part[u]);
+    seg_part[i] = s;
+  }
+  __syncthreads();
 }
 
 // Warp-level vla-32 dot product of staged entries [lo, hi): lane l sums

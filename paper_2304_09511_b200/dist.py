@@ -264,8 +264,9 @@ def build_local_slab(csr_rows: CsrMatrix, r0: int, r1: int, fmt: str = "csr") ->
             lo_col, hi_col = r0, r1
         win = (min(r0, lo_col), max(r1, hi_col))
         if offs:
-            i_lo = min(nloc, max(0, r0 - min(offs)))
-            i_hi = min(nloc, max(0, r1 - max(offs)))
+            # rows reading below r0 / at or above r1 (none at the matrix edges)
+            i_lo = min(nloc, max(0, r0 - min(offs))) if win[0] < r0 else 0
+            i_hi = min(nloc, max(0, r1 - max(offs))) if win[1] > r1 else nloc
         else:
             i_lo, i_hi = 0, nloc
         i_lo = min(nloc, round_up(i_lo, ROW_PAD))
