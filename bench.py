@@ -306,7 +306,7 @@ def run_ours(args, torch, dist, rank, world, local_rank):
     }
     if not args.no_extras:
         line["e2e"] = e2e_measure(args, torch, sp, m, x, head)
-        if args.config in ("c5", "c1", "c3"):
+        if args.config in ("c5", "c1", "c3", "c4"):
             csr = mats["csr"]
             h = csr.to_host()
             y_gpu = sp.spmv_csr_plain(csr, x).cpu().numpy()

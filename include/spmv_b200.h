@@ -58,18 +58,21 @@ int spmv_device_sm_count(int* out);
 /* ---- CSR (kernels.py:69-82 spmv_csr_plain, :143-171 spmv_csr_vla) ------ */
 typedef struct spmv_csr_plan spmv_csr_plan;
 
-/* Analyse the row-length histogram once (CSR-Adaptive style binning):
- * rows of length <= exact_len go to the CSR-stream kernel (one thread sums
- * the row left to right => bit-exact with spmv_csr_plain); longer rows are
- * split into warp chunks (bit-exact with spmv_csr_vla(lanes=32) for rows of
- * at most one chunk, deterministic and within 1e-12 otherwise).
- * exact_len <= 0 selects the default (32). */
+/* Analyse the matrix once: long-row census (rows > exact_len entries), tile
+ * size (2048 entries, 1024 when long rows exist), the row range of every
+ * tile and the list of long rows spanning tiles.  The SpMV kernel streams
+ * fixed entry tiles with TMA bulk copies; rows of <= exact_len entries are
+ * summed left to right by one thread (bit-exact with spmv_csr_plain); longer
+ * rows are reduced in 256-entry vla-32 units (bit-exact with
+ * spmv_csr_vla(32) for rows of <= 256 entries inside one tile, deterministic
+ * and within 1e-12 otherwise).  exact_len <= 0 selects the default (32). */
 int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
                          const uint32_t* row_pointers, int exact_len,
                          void* stream, spmv_csr_plan** out);
 int spmv_csr_plan_destroy(spmv_csr_plan* plan);
-/* n_long_rows: rows handled by the chunk kernel; n_items: warp work items;
- * launches: kernels one spmv_csr call launches. */
+/* n_long_rows: rows longer than exact_len; n_items: entries per tile;
+ * launches: kernels one spmv_csr call launches (1, or 2 with the span
+ * fix-up). */
 int spmv_csr_plan_info(const spmv_csr_plan* plan, int64_t* n_long_rows,
                        int64_t* n_items, int64_t* launches);
 
@@ -94,20 +97,22 @@ typedef struct spmv_coo_plan spmv_coo_plan;
 /* Checks the row order once.  If rows are not non-decreasing, the plan
  * keeps a stable row-sorted copy of the triples (np.add.at accumulates in
  * storage order per row, kernels.py:65, and a stable sort keeps that
- * order).  Also run-length-encodes the rows for the long-row chunks. */
+ * order).  Also run-length-encodes the rows (vla kernel, long-run census). */
 int spmv_coo_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
                          const uint32_t* row_indices,
                          const uint32_t* col_indices, const void* values,
                          void* stream, spmv_coo_plan** out);
 int spmv_coo_plan_destroy(spmv_coo_plan* plan);
-/* row_sorted: 1 when the input rows were already non-decreasing. */
+/* row_sorted: 1 when the input rows were already non-decreasing;
+ * n_items: entries per tile. */
 int spmv_coo_plan_info(const spmv_coo_plan* plan, int64_t* n_runs,
                        int64_t* n_long_runs, int64_t* n_items,
                        int* row_sorted, int64_t* launches);
 
-/* Fixed 2048-entry tiles, segmented reduction without atomics: rows of at
- * most 32 entries are summed left to right by one thread starting from
- * +0.0 (bit-exact with np.add.at), longer runs go to the warp chunks. */
+/* Fixed 2048-entry tiles (TMA bulk copies), segmented without atomics: rows
+ * of at most 32 entries are summed left to right by one thread starting
+ * from +0.0 (bit-exact with np.add.at); longer runs are reduced in 256-entry
+ * vla-32 units, cross-tile parts combined in tile order by a fix-up kernel. */
 int spmv_coo(const spmv_coo_plan* plan, const uint32_t* row_indices,
              const uint32_t* col_indices, const void* values, const void* x,
              int64_t col_base, int64_t x_len, void* y, void* stream);
