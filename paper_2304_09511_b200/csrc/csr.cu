@@ -403,6 +403,7 @@ template <typename T>
 static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st) {
   if (p->tile == 1024) return csr_run_tiled<T, 1024>(p, irp, aj, av, x, col_base, y, st);
+  if (p->tile == 4096) return csr_run_tiled<T, 4096>(p, irp, aj, av, x, col_base, y, st);
   return csr_run_tiled<T, 2048>(p, irp, aj, av, x, col_base, y, st);
 }
 
@@ -457,6 +458,8 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
   if (p->tile == 1024)
     return p->dtype == SPMV_F64 ? csr_launch_config<double, 1024>(p) : csr_launch_config<float, 1024>(p);
+  if (p->tile == 4096)
+    return p->dtype == SPMV_F64 ? csr_launch_config<double, 4096>(p) : csr_launch_config<float, 4096>(p);
   return p->dtype == SPMV_F64 ? csr_launch_config<double, 2048>(p) : csr_launch_config<float, 2048>(p);
 }
 
