@@ -225,6 +225,21 @@ int spmv_csr_halo_split(int64_t nrows, const uint32_t* row_pointers,
                         int64_t col_hi, void* stream, int64_t* i_lo,
                         int64_t* i_hi);
 
+/* ---- CG vector kernels (hpcg.py:211-258) ------------------------------- */
+/* Deterministic dot product: ws holds spmv_dot_workspace_entries() values;
+ * the result lands in ws[entries-1] (device).  Fixed reduction tree, run to
+ * run identical and independent of the SM count. */
+int spmv_dot_workspace_entries(void);
+int spmv_dot(int dtype, int64_t n, const void* a, const void* b, void* ws,
+             void* stream);
+/* x += alpha p; r -= alpha Ap (rounded products, no FMA, hpcg.py:243-246);
+ * the new r.r lands in ws[entries-1] like spmv_dot. */
+int spmv_cg_update(int dtype, int64_t n, double alpha, const void* p,
+                   const void* ap, void* x, void* r, void* ws, void* stream);
+/* p = r + beta p (hpcg.py:253). */
+int spmv_cg_direction(int dtype, int64_t n, double beta, const void* r,
+                      void* p, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

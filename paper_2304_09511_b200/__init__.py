@@ -22,6 +22,7 @@ from .convert import (
 from .errors import (
     DeviceError,
     DimensionMismatch,
+    Diverged,
     FillRatioExceeded,
     IndexOverflow,
     SparseError,
@@ -52,5 +53,6 @@ from .kernels import (
 )
 from .lanes import LaneConfig
 from .matrixio import gen_stencil27, gen_stencil27_rows
+from .cg import CgState, cg_solve
 
 __version__ = "0.1.0"

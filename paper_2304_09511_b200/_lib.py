@@ -78,6 +78,10 @@ SIGNATURES = {
     "spmv_stencil27_fill": [_c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp],
     "spmv_csr_col_bounds": [_c_i64, _vp, _vp, _vp, _pu32, _pu32],
     "spmv_csr_halo_split": [_c_i64, _vp, _vp, _c_i64, _c_i64, _vp, _pi64, _pi64],
+    "spmv_dot_workspace_entries": [],
+    "spmv_dot": [_c_int, _c_i64, _vp, _vp, _vp, _vp],
+    "spmv_cg_update": [_c_int, _c_i64, ctypes.c_double, _vp, _vp, _vp, _vp, _vp, _vp],
+    "spmv_cg_direction": [_c_int, _c_i64, ctypes.c_double, _vp, _vp, _vp],
 }
 _RESTYPE = {"spmv_last_error": ctypes.c_char_p}
 

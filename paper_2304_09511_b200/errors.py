@@ -31,3 +31,7 @@ class IndexOverflow(SparseError):
 
 class DeviceError(SparseError):
     """A CUDA call inside the engine failed (no reference counterpart)."""
+
+
+class Diverged(SparseError):
+    """Iterative solve produced a non-finite quantity (errors.py:40)."""

@@ -18,6 +18,7 @@ Files written:
                   edge cases (duplicates, signed zeros, NaN, unsorted cols)
   reduceat.npz    np.add.reduceat segments (pins the pairwise-sum model)
   stencil.npz     gen_stencil27 on small grids
+  cg.npz          hpcg.cg_solve: iterations, residual histories, solutions
 """
 
 from __future__ import annotations
@@ -247,8 +248,28 @@ def make_stencil() -> None:
     np.savez_compressed(OUT / "stencil.npz", **d)
 
 
+def make_cg() -> None:
+    """hpcg.cg_solve runs (acceptance criterion 06, test_hpcg.py:108-158)."""
+    from spmvkit.hpcg import ProblemSpec, build_problem, cg_solve, gather_global
+    d: dict = {}
+    for key, spec, tol, iters in (("p16", ProblemSpec(16, 16, 16), 1e-9, 200),
+                                  ("p16_split", ProblemSpec(8, 16, 16, 2, 1, 1), 1e-9, 200),
+                                  ("p8", ProblemSpec(8, 8, 8), 1e-9, 200),
+                                  ("p2", ProblemSpec(2, 2, 2), 1e-10, 20)):
+        ranks = build_problem(spec)
+        st = cg_solve(ranks, tol=tol, max_iters=iters)
+        d[f"{key}/dims"] = np.array(spec.global_dims, dtype=np.int64)
+        d[f"{key}/iterations"] = np.array(st.iterations)
+        d[f"{key}/norms"] = np.asarray(st.residual_norms, dtype=np.float64)
+        d[f"{key}/converged"] = np.array(st.converged)
+        d[f"{key}/x"] = gather_global(ranks, st.x_parts)
+        d[f"{key}/b"] = gather_global(ranks, [rs.b_local for rs in ranks])
+    np.savez_compressed(OUT / "cg.npz", **d)
+
+
 if __name__ == "__main__":
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    make_cg()
     make_canonical()
     make_convert()
     make_reduceat()
