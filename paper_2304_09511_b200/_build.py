@@ -27,7 +27,7 @@ NVCC_FLAGS = ARCH + [
     "-Xcompiler", "-fPIC",
     "-Xptxas", "-warn-spills",
     f"-I{INCLUDE}",
-]
+] + os.environ.get("SPMV_NVCC_EXTRA", "").split()
 
 
 def _sources():

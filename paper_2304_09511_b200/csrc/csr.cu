@@ -144,7 +144,10 @@ __device__ __forceinline__ void csr_tile_long(int64_t t, const uint32_t* __restr
 }
 
 template <typename T, bool BULK, int TILE>
-__global__ void __launch_bounds__(kTileThreads, 4)
+#ifndef SPMV_CSR_MINB
+#define SPMV_CSR_MINB 4
+#endif
+__global__ void __launch_bounds__(kTileThreads, SPMV_CSR_MINB)
 csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
   extern __shared__ __align__(128) unsigned char smem[];
   using S = CsrSmem<T, TILE>;

@@ -49,17 +49,29 @@ inline int64_t bulk_tiles(int64_t nnz, int64_t ntiles, int64_t tile) {
 // before their adds (the add order is unchanged).  acc0 = -0.0 reproduces
 // cumsum (the first product itself, kernels.py:81); acc0 = +0.0 reproduces
 // np.add.at on a zeroed y (kernels.py:65).
+#ifndef SPMV_ROW_BATCH
+#define SPMV_ROW_BATCH 8
+#endif
 template <typename T>
 __device__ __forceinline__ T row_dot(const uint32_t* __restrict__ c, const T* __restrict__ v, int len,
                                      const T* __restrict__ xb, T acc) {
+  constexpr int B = SPMV_ROW_BATCH;
   int i = 0;
-  for (; i + 8 <= len; i += 8) {
-    T p[8];
+  for (; i + B <= len; i += B) {
+    T p[B];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) p[j] = mul_rn(v[i + j], __ldg(xb + c[i + j]));
+    for (int j = 0; j < B; ++j) p[j] = mul_rn(v[i + j], __ldg(xb + c[i + j]));
 #pragma unroll
-    for (int j = 0; j < 8; ++j) acc = add_rn(acc, p[j]);
+    for (int j = 0; j < B; ++j) acc = add_rn(acc, p[j]);
   }
+  if (B > 8)
+    for (; i + 8 <= len; i += 8) {
+      T p[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) p[j] = mul_rn(v[i + j], __ldg(xb + c[i + j]));
+#pragma unroll
+      for (int j = 0; j < 8; ++j) acc = add_rn(acc, p[j]);
+    }
   for (; i < len; ++i) acc = add_rn(acc, mul_rn(v[i], __ldg(xb + c[i])));
   return acc;
 }
