@@ -24,8 +24,12 @@ from .errors import (
     DimensionMismatch,
     Diverged,
     FillRatioExceeded,
+    AllCandidatesFailed,
+    EmptyInput,
     IndexOverflow,
+    ParseError,
     SparseError,
+    UnsupportedField,
     UnsortedInput,
     UnsupportedCombination,
 )
@@ -52,7 +56,8 @@ from .kernels import (
     spmv_dia_vla,
 )
 from .lanes import LaneConfig
-from .matrixio import gen_stencil27, gen_stencil27_rows
+from .matrixio import gen_stencil27, gen_stencil27_rows, read_matrix_market, write_matrix_market
 from .cg import CgState, cg_solve
+from .autotune import Measurement, TuneChoice, distribution_report, measure, tune
 
 __version__ = "0.1.0"

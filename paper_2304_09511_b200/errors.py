@@ -35,3 +35,19 @@ class DeviceError(SparseError):
 
 class Diverged(SparseError):
     """Iterative solve produced a non-finite quantity (errors.py:40)."""
+
+
+class AllCandidatesFailed(SparseError):
+    """Every tuning candidate failed, so no choice can be made (errors.py:24)."""
+
+
+class EmptyInput(SparseError):
+    """Operation requires at least one input element (errors.py:52)."""
+
+
+class ParseError(SparseError):
+    """Malformed Matrix Market content (errors.py:28)."""
+
+
+class UnsupportedField(SparseError):
+    """Matrix Market field or symmetry this reader does not support (errors.py:32)."""

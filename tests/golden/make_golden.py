@@ -19,6 +19,7 @@ Files written:
   reduceat.npz    np.add.reduceat segments (pins the pairwise-sum model)
   stencil.npz     gen_stencil27 on small grids
   cg.npz          hpcg.cg_solve: iterations, residual histories, solutions
+  mm.npz          read_matrix_market on small hand-written files
 """
 
 from __future__ import annotations
@@ -248,6 +249,30 @@ def make_stencil() -> None:
     np.savez_compressed(OUT / "stencil.npz", **d)
 
 
+MM_TEXTS = {
+    "general_dups": "%%MatrixMarket matrix coordinate real general\n% comment\n4 5 7\n1 1 1.5\n3 2 -2.25\n"
+                    "1 1 0.125\n4 5 1e-3\n2 3 7\n3 2 2.25\n1 4 -0.0\n",
+    "symmetric": "%%MatrixMarket matrix coordinate real symmetric\n5 5 6\n1 1 4\n2 1 -1\n3 2 -1.5\n"
+                 "5 3 0.5\n4 4 3.25\n5 5 2\n",
+    "skew": "%%MatrixMarket matrix coordinate real skew-symmetric\n4 4 3\n2 1 1.5\n3 1 -2\n4 3 0.75\n",
+    "pattern": "%%MatrixMarket matrix coordinate pattern general\n3 6 4\n1 6\n3 1\n2 2\n1 1\n",
+    "integer_sym": "%%MatrixMarket matrix coordinate integer symmetric\n% x\n\n3 3 4\n1 1 2\n2 1 -3\n"
+                   "3 1 5\n3 3 -7\n",
+    "empty": "%%MatrixMarket matrix coordinate real general\n3 4 0\n",
+}
+
+
+def make_mm() -> None:
+    """matrixio.read_matrix_market on small hand-written files."""
+    from spmvkit.matrixio import read_matrix_market
+    d: dict = {}
+    for name, text in MM_TEXTS.items():
+        d[f"{name}/text"] = np.array(text)
+        put_matrix(d, f"{name}/coo", read_matrix_market(text.encode()))
+    d["names"] = np.array(list(MM_TEXTS))
+    np.savez_compressed(OUT / "mm.npz", **d)
+
+
 def make_cg() -> None:
     """hpcg.cg_solve runs (acceptance criterion 06, test_hpcg.py:108-158)."""
     from spmvkit.hpcg import ProblemSpec, build_problem, cg_solve, gather_global
@@ -269,6 +294,7 @@ def make_cg() -> None:
 
 if __name__ == "__main__":
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    make_mm()
     make_cg()
     make_canonical()
     make_convert()
