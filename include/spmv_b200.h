@@ -70,6 +70,9 @@ int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
                          const uint32_t* row_pointers, int exact_len,
                          void* stream, spmv_csr_plan** out);
 int spmv_csr_plan_destroy(spmv_csr_plan* plan);
+/* Profiling builds only (-DSPMV_PHASE_TIMING): per-phase cycle counters of
+ * the CSR tile kernel, read and reset (8 entries); else SPMV_UNSUPPORTED. */
+int spmv_debug_csr_phases(unsigned long long* out8);
 /* n_long_rows: rows longer than exact_len; n_items: entries per tile;
  * launches: kernels one spmv_csr call launches (1, or 2 with the span
  * fix-up). */

@@ -28,6 +28,17 @@
 
 namespace spmv {
 
+#ifdef SPMV_PHASE_TIMING
+// [0] wait  [1] rows (thread 0, incl. barrier)  [2] long+end barrier  [3] issue
+// [4] sum of row-thread loop cycles  [5] row-thread count  [6] tiles
+__device__ unsigned long long g_phase[8];
+#define PHASE_T(v) const unsigned long long v = clock64()
+#define PHASE_ADD(i, v) atomicAdd(&g_phase[i], (unsigned long long)(v))
+#else
+#define PHASE_T(v)
+#define PHASE_ADD(i, v)
+#endif
+
 template <typename T>
 struct CsrParams {
   const uint32_t* irp;
@@ -82,6 +93,8 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
   if (products) form_products(cols, vals, int(min(int64_t(TILE + kExt), P.nnz - E0)), xb);
   if (tid == 0) *s_nlong = 0;
   __syncthreads();
+  PHASE_T(rt0);
+  const bool had_row = r < rend;
   while (r < rend) {
     const uint32_t len = e - s;
     if (len == 0) {
@@ -111,6 +124,13 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
       e = __ldg(P.irp + r + 1);
     }
   }
+#ifdef SPMV_PHASE_TIMING
+  if (had_row) {
+    PHASE_T(rt1);
+    PHASE_ADD(4, rt1 - rt0);
+    PHASE_ADD(5, 1);
+  }
+#endif
   __syncthreads();
 }
 
@@ -186,6 +206,7 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
   for (int64_t i = 0; i < mine_bulk + mine_tail; ++i) {
     int s = 0;
     int64_t t;
+    PHASE_T(p0);
     if (i < mine_bulk) {
       s = int(i % kTileStages);
       t = first + i * stride;
@@ -200,16 +221,29 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
       }
       __syncthreads();
     }
+    PHASE_T(p1);
     csr_tile_rows<T, TILE>(P, t, cols_of(s), vals_of(s), s_long, s_nlong);
+    PHASE_T(p2);
     const int nl = *s_nlong;
     if (nl > 0)
       csr_tile_long<T, TILE>(t, cols_of(s), vals_of(s), s_long, nl, smem, s_nlong + 1, P.x - P.col_base, P.y,
                              P.head, P.tail, (P.mode & 2) != 0);
     __syncthreads();  // stage s free
+    PHASE_T(p3);
     if (BULK && tid == 0 && i + kTileStages < mine_bulk) {
       fence_proxy_async();
       issue(i + kTileStages);
     }
+#ifdef SPMV_PHASE_TIMING
+    if (tid == 0) {
+      PHASE_T(p4);
+      PHASE_ADD(0, p1 - p0);
+      PHASE_ADD(1, p2 - p1);
+      PHASE_ADD(2, p3 - p2);
+      PHASE_ADD(3, p4 - p3);
+      PHASE_ADD(6, 1);
+    }
+#endif
   }
 }
 
@@ -493,6 +527,20 @@ int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, c
   }
   *out = p;
   return SPMV_OK;
+}
+
+// Debug builds only (-DSPMV_PHASE_TIMING): read and reset the phase counters.
+int spmv_debug_csr_phases(unsigned long long* out8) {
+#ifdef SPMV_PHASE_TIMING
+  SPMV_CUDA_TRY(cudaDeviceSynchronize());
+  SPMV_CUDA_TRY(cudaMemcpyFromSymbol(out8, g_phase, sizeof(unsigned long long) * 8));
+  unsigned long long z[8] = {0};
+  SPMV_CUDA_TRY(cudaMemcpyToSymbol(g_phase, z, sizeof(z)));
+  return SPMV_OK;
+#else
+  (void)out8;
+  return fail(SPMV_UNSUPPORTED, "library built without SPMV_PHASE_TIMING");
+#endif
 }
 
 int spmv_csr_plan_destroy(spmv_csr_plan* plan) {
