@@ -125,7 +125,7 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
     }
   }
 #ifdef SPMV_PHASE_TIMING
-  if (had_row) {
+  if (had_row && tid == 0) {  // thread 0 only: no atomic contention
     PHASE_T(rt1);
     PHASE_ADD(4, rt1 - rt0);
     PHASE_ADD(5, 1);
