@@ -33,10 +33,17 @@ namespace spmv {
 // [4] sum of row-thread loop cycles  [5] row-thread count  [6] tiles
 __device__ unsigned long long g_phase[8];
 #define PHASE_T(v) const unsigned long long v = clock64()
-#define PHASE_ADD(i, v) atomicAdd(&g_phase[i], (unsigned long long)(v))
+#define PHASE_ADD(i, v) (s_phase_acc[i] += (unsigned long long)(v))
 #else
 #define PHASE_T(v)
 #define PHASE_ADD(i, v)
+#endif
+
+#ifdef SPMV_PHASE_TIMING
+// per-CTA accumulators in shared memory (thread 0 writes), flushed once
+#define PHASE_DECL __shared__ unsigned long long s_phase_acc[8];
+#else
+#define PHASE_DECL
 #endif
 
 template <typename T>
@@ -75,7 +82,11 @@ struct CsrSmem {
 // segments are only queued here.
 template <typename T, int TILE>
 __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, const uint32_t* __restrict__ cols,
-                                              T* __restrict__ vals, LongSeg* s_long, int* s_nlong) {
+                                              T* __restrict__ vals, LongSeg* s_long, int* s_nlong
+#ifdef SPMV_PHASE_TIMING
+                                              , unsigned long long* s_phase_acc
+#endif
+) {
   const int tid = threadIdx.x;
   const int64_t E0 = t * TILE;
   const int64_t E1 = E0 + TILE;
@@ -170,6 +181,11 @@ template <typename T, bool BULK, int TILE>
 __global__ void __launch_bounds__(kTileThreads, SPMV_CSR_MINB)
 csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
   extern __shared__ __align__(128) unsigned char smem[];
+  PHASE_DECL
+#ifdef SPMV_PHASE_TIMING
+  if (threadIdx.x < 8) s_phase_acc[threadIdx.x] = 0;
+  __syncthreads();
+#endif
   using S = CsrSmem<T, TILE>;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
   int* s_nlong = reinterpret_cast<int*>(smem + 32);
@@ -222,7 +238,11 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
       __syncthreads();
     }
     PHASE_T(p1);
-    csr_tile_rows<T, TILE>(P, t, cols_of(s), vals_of(s), s_long, s_nlong);
+    csr_tile_rows<T, TILE>(P, t, cols_of(s), vals_of(s), s_long, s_nlong
+#ifdef SPMV_PHASE_TIMING
+                           , s_phase_acc
+#endif
+    );
     PHASE_T(p2);
     const int nl = *s_nlong;
     if (nl > 0)
@@ -245,6 +265,9 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
     }
 #endif
   }
+#ifdef SPMV_PHASE_TIMING
+  if (threadIdx.x < 8) atomicAdd(&g_phase[threadIdx.x], s_phase_acc[threadIdx.x]);
+#endif
 }
 
 // Rows spanning tiles: y = tail[t0] + head[t0+1] + ... + head[t1].
