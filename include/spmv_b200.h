@@ -86,6 +86,24 @@ int spmv_csr(const spmv_csr_plan* plan, const uint32_t* row_pointers,
              const uint32_t* col_indices, const void* values, const void* x,
              int64_t col_base, int64_t x_len, void* y, void* stream);
 
+/* Tile-range launches (pipelined host transfers): the plan's tiles are
+ * independent except for long rows spanning tiles, which the fix-up adds
+ * (fixup = 1 on the last range).  After tiles [0, k) ran, rows
+ * [0, row_lo[k]) of y are final; tiles [a, b) read x only below
+ * max(maxcol[a..b)) + 1.  spmv_csr_plan_tile_info copies row_lo (ntiles+1)
+ * and maxcol (ntiles) to host arrays (maxcol is computed on first use). */
+int spmv_csr_plan_tiles(const spmv_csr_plan* plan, int64_t* ntiles,
+                        int64_t* tile);
+int spmv_csr_plan_tile_info(spmv_csr_plan* plan,
+                            const uint32_t* col_indices,
+                            uint32_t* row_lo_host, uint32_t* maxcol_host,
+                            void* stream);
+int spmv_csr_range(const spmv_csr_plan* plan, const uint32_t* row_pointers,
+                   const uint32_t* col_indices, const void* values,
+                   const void* x, int64_t col_base, int64_t x_len, void* y,
+                   int64_t tile_begin, int64_t tile_end, int fixup,
+                   void* stream);
+
 /* Sub-warp vector kernel, lane l accumulates entries s+l, s+l+L, ... then a
  * pairwise-halving tree over next_pow2(L) lanes: bit-exact with
  * spmv_csr_vla(LaneConfig(L)) (lanes.py:101-128).  1 <= lanes <= 1024. */

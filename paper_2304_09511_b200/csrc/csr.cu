@@ -57,6 +57,7 @@ struct CsrParams {
   T* head;
   T* tail;
   int64_t nrows, nnz, col_base, ntiles, n_bulk;
+  int64_t tile_begin, tile_end;  // tiles [tile_begin, tile_end) of this launch
   int exact_len;
   int mode;
 };
@@ -195,13 +196,15 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
   auto cols_of = [&](int s) { return reinterpret_cast<uint32_t*>(stages + s * S::stage_bytes); };
   auto vals_of = [&](int s) { return reinterpret_cast<T*>(stages + s * S::stage_bytes + S::cols_bytes); };
 
-  // This CTA's tiles: bulk-copyable ones first (TMA pipeline), then the
-  // tail tiles the bulk engine cannot address (cooperative loads).
-  const int64_t n_bulk = BULK ? P.n_bulk : 0;
-  const int64_t first = blockIdx.x, stride = gridDim.x;
+  // This CTA's tiles (grid-strided over [tile_begin, tile_end), so all SMs
+  // sweep neighbouring rows together and share x lines in L2): bulk-copyable
+  // ones first (TMA pipeline), then the tail tiles the bulk engine cannot
+  // address (cooperative loads).
+  const int64_t n_bulk = BULK ? min(P.n_bulk, P.tile_end) : P.tile_begin;
+  const int64_t first = P.tile_begin + blockIdx.x, stride = gridDim.x;
   const int64_t mine_bulk = first < n_bulk ? (n_bulk - 1 - first) / stride + 1 : 0;
-  const int64_t tail0 = n_bulk + first;
-  const int64_t mine_tail = tail0 < P.ntiles ? (P.ntiles - 1 - tail0) / stride + 1 : 0;
+  const int64_t tail0 = max(n_bulk, P.tile_begin) + blockIdx.x;
+  const int64_t mine_tail = tail0 < P.tile_end ? (P.tile_end - 1 - tail0) / stride + 1 : 0;
   auto issue = [&](int64_t i) {
     const int64_t E0 = (first + i * stride) * TILE;
     const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
@@ -297,6 +300,26 @@ __global__ void csr_span_list_kernel(const uint32_t* __restrict__ irp, int64_t n
       span_t0[k] = uint32_t(t0);
       span_t1[k] = uint32_t(t1);
     }
+  }
+}
+
+// maxcol[t] = largest column read by tile t (its entries + the kExt
+// extension): the x prefix a tile-range launch needs (pipelined uploads).
+__global__ void tile_maxcol_kernel(const uint32_t* __restrict__ aj, int64_t nnz, int64_t ntiles, int64_t tile,
+                                   uint32_t* __restrict__ maxcol) {
+  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
+    const int64_t e0 = t * tile, e1 = min(nnz, e0 + tile + kExt);
+    uint32_t m = 0;
+    for (int64_t j = e0 + threadIdx.x; j < e1; j += blockDim.x) m = max(m, aj[j]);
+    for (int o = 16; o >= 1; o >>= 1) m = max(m, __shfl_down_sync(0xffffffffu, m, o));
+    __shared__ uint32_t w[8];
+    if ((threadIdx.x & 31) == 0) w[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int i = 1; i < int(blockDim.x >> 5); ++i) m = max(m, w[i]);
+      maxcol[t] = max(m, w[0]);
+    }
+    __syncthreads();
   }
 }
 
@@ -398,6 +421,7 @@ struct spmv_csr_plan {
   DevBuf row_lo, head, tail, cnt;
   DevBuf span_row, span_t0, span_t1;
   int64_t n_span = 0;
+  DevBuf maxcol;
   int grid_bulk = 0, grid_direct = 0;
 };
 
@@ -421,7 +445,7 @@ static int csr_launch_config(spmv_csr_plan* p) {
 
 template <typename T, int TILE>
 static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
-                   int64_t col_base, T* y, cudaStream_t st) {
+                   int64_t col_base, T* y, cudaStream_t st, int64_t tb, int64_t te, bool fixup) {
   if (p->nrows == 0) return SPMV_OK;
   if (p->nnz == 0) {
     SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
@@ -440,17 +464,22 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
   P.nnz = p->nnz;
   P.col_base = col_base;
   P.ntiles = p->ntiles;
+  P.tile_begin = tb;
+  P.tile_end = te;
   P.exact_len = p->exact_len;
   P.mode = tile_mode_flags();
   const bool aligned = (reinterpret_cast<uintptr_t>(aj) % 16 == 0) && (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
   const size_t smem = CsrSmem<T, TILE>::total;
-  if (aligned)
-    csr_tile_kernel<T, true, TILE><<<unsigned(p->grid_bulk), kTileThreads, smem, st>>>(P);
-  else
-    csr_tile_kernel<T, false, TILE><<<unsigned(p->grid_direct), kTileThreads, smem, st>>>(P);
-  SPMV_LAUNCH_CHECK();
-  if (p->n_span > 0) {
+  const int64_t grid = std::min<int64_t>(aligned ? p->grid_bulk : p->grid_direct, te - tb);
+  if (grid > 0) {
+    if (aligned)
+      csr_tile_kernel<T, true, TILE><<<unsigned(grid), kTileThreads, smem, st>>>(P);
+    else
+      csr_tile_kernel<T, false, TILE><<<unsigned(grid), kTileThreads, smem, st>>>(P);
+    SPMV_LAUNCH_CHECK();
+  }
+  if (fixup && p->n_span > 0) {
     const int64_t g = std::min<int64_t>((p->n_span + 255) / 256, int64_t(sm_count()) * 8);
     csr_span_fixup_kernel<T><<<unsigned(g), 256, 0, st>>>(p->span_row.as<uint32_t>(), p->span_t0.as<uint32_t>(),
                                                           p->span_t1.as<uint32_t>(), p->n_span, P.head, P.tail, y);
@@ -461,10 +490,11 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
 
 template <typename T>
 static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
-                   int64_t col_base, T* y, cudaStream_t st) {
-  if (p->tile == 1024) return csr_run_tiled<T, 1024>(p, irp, aj, av, x, col_base, y, st);
-  if (p->tile == 4096) return csr_run_tiled<T, 4096>(p, irp, aj, av, x, col_base, y, st);
-  return csr_run_tiled<T, 2048>(p, irp, aj, av, x, col_base, y, st);
+                   int64_t col_base, T* y, cudaStream_t st, int64_t tb = 0, int64_t te = -1, bool fixup = true) {
+  if (te < 0) te = p->ntiles;
+  if (p->tile == 1024) return csr_run_tiled<T, 1024>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
+  if (p->tile == 4096) return csr_run_tiled<T, 4096>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
+  return csr_run_tiled<T, 2048>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
 }
 
 static int count_async(unsigned long long* dev, unsigned long long* host, cudaStream_t st) {
@@ -577,6 +607,48 @@ int spmv_csr_plan_info(const spmv_csr_plan* p, int64_t* n_long_rows, int64_t* n_
   if (n_items) *n_items = p->tile;
   if (launches) *launches = (p->nrows > 0 ? 1 : 0) + (p->n_span > 0 ? 1 : 0);
   return SPMV_OK;
+}
+
+int spmv_csr_plan_tiles(const spmv_csr_plan* p, int64_t* ntiles, int64_t* tile) {
+  if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
+  if (ntiles) *ntiles = p->ntiles;
+  if (tile) *tile = p->tile;
+  return SPMV_OK;
+}
+
+int spmv_csr_plan_tile_info(spmv_csr_plan* p, const uint32_t* aj, uint32_t* row_lo_host, uint32_t* maxcol_host,
+                            void* stream) {
+  if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
+  if (p->ntiles == 0) return SPMV_OK;
+  cudaStream_t st = as_stream(stream);
+  if (!p->maxcol.ptr) {
+    int rc = p->maxcol.alloc(4 * p->ntiles);
+    if (rc) return rc;
+    const int64_t g = std::min<int64_t>(p->ntiles, int64_t(sm_count()) * 8);
+    tile_maxcol_kernel<<<unsigned(g), 256, 0, st>>>(aj, p->nnz, p->ntiles, p->tile, p->maxcol.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+  }
+  if (row_lo_host)
+    SPMV_CUDA_TRY(cudaMemcpyAsync(row_lo_host, p->row_lo.ptr, 4 * (p->ntiles + 1), cudaMemcpyDeviceToHost, st));
+  if (maxcol_host)
+    SPMV_CUDA_TRY(cudaMemcpyAsync(maxcol_host, p->maxcol.ptr, 4 * p->ntiles, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  return SPMV_OK;
+}
+
+int spmv_csr_range(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av, const void* x,
+                   int64_t col_base, int64_t x_len, void* y, int64_t tile_begin, int64_t tile_end, int fixup,
+                   void* stream) {
+  if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
+  if (tile_begin < 0 || tile_end > p->ntiles || tile_begin > tile_end) return fail(SPMV_INVALID_ARG, "bad tile range");
+  if (p->nrows == 0 || p->nnz == 0) return fail(SPMV_INVALID_ARG, "tile ranges need a non-empty matrix");
+  if (x_len < 0 || col_base < 0) return fail(SPMV_DIMENSION_MISMATCH, "bad x window");
+  cudaStream_t st = as_stream(stream);
+  if (p->dtype == SPMV_F64)
+    return csr_run<double>(p, irp, aj, static_cast<const double*>(av), static_cast<const double*>(x), col_base,
+                           static_cast<double*>(y), st, tile_begin, tile_end, fixup != 0);
+  return csr_run<float>(p, irp, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
+                        static_cast<float*>(y), st, tile_begin, tile_end, fixup != 0);
 }
 
 int spmv_csr(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av, const void* x,

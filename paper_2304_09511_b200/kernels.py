@@ -148,6 +148,134 @@ def coo_plan(A: CooMatrix) -> _Plan:
     return A.plan("coo", make)
 
 
+# --------------------------------------------------------- host pipelining --
+# A product whose x and y both live in host memory is PCIe-bound (x in, y
+# out).  CSR and DIA products are split into row ranges so the upload of x
+# (column chunks, copy stream 1), the kernels (compute stream) and the
+# download of finished rows of y (copy stream 2) overlap; PCIe is full
+# duplex, so the step approaches max(H2D, D2H) instead of H2D + compute + D2H.
+_SIDE_STREAMS: dict = {}
+PIPELINE_CHUNKS = 16
+
+
+def _side_streams(dev):
+    key = str(dev)
+    if key not in _SIDE_STREAMS:
+        _SIDE_STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
+    return _SIDE_STREAMS[key]
+
+
+def _csr_tile_info(A: CsrMatrix, p: "_Plan"):
+    def make():
+        nt, tile = ctypes.c_int64(), ctypes.c_int64()
+        _lib.call("spmv_csr_plan_tiles", p.handle, ctypes.byref(nt), ctypes.byref(tile))
+        n = int(nt.value)
+        row_lo = np.empty(n + 1, dtype=np.uint32)
+        maxcol = np.empty(max(n, 1), dtype=np.uint32)
+        _lib.call("spmv_csr_plan_tile_info", p.handle, _ptr(A.col_indices), row_lo.ctypes.data, maxcol.ctypes.data,
+                  _stream(A.device))
+        return n, row_lo.astype(np.int64), np.maximum.accumulate(maxcol[:n].astype(np.int64))
+    return A.plan("csr_tiles", make)
+
+
+def _upload_x_chunks(xh: torch.Tensor, xd: torch.Tensor, h2d, chunks: int):
+    """Column chunks of x, in order on `h2d`; returns (bounds, events)."""
+    n = xh.shape[0]
+    bounds = [n * j // chunks for j in range(chunks + 1)]
+    events = []
+    with torch.cuda.stream(h2d):
+        for j in range(chunks):
+            a, b = bounds[j], bounds[j + 1]
+            if b > a:
+                xd[a:b].copy_(xh[a:b], non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(h2d)
+            events.append(ev)
+    return bounds, events
+
+
+def _wait_x(cur, bounds, events, col_hi: int) -> None:
+    """Make `cur` wait until x[0 .. col_hi] is on the device."""
+    j = 0
+    while j + 1 < len(bounds) - 1 and bounds[j + 1] <= col_hi:
+        j += 1
+    cur.wait_event(events[j])
+
+
+def _pipelined(A, xh: torch.Tensor, yh: torch.Tensor, launch_range, ranges, chunks: int, y_final_at_end: bool):
+    """Generic H2D / compute / D2H overlap.  `ranges`: list of
+    (col_hi, rows_done) per compute step; `launch_range(k, xd, yd, stream)`."""
+    dev = A.values.device
+    cur = torch.cuda.current_stream(dev)
+    h2d, d2h = _side_streams(dev)
+    xd = torch.empty(A.ncols, dtype=A.values.dtype, device=dev)
+    yd = torch.empty(A.nrows, dtype=A.values.dtype, device=dev)
+    h2d.wait_stream(cur)
+    d2h.wait_stream(cur)
+    bounds, events = _upload_x_chunks(xh, xd, h2d, chunks)
+    done = 0
+    for k, (col_hi, rows_done) in enumerate(ranges):
+        _wait_x(cur, bounds, events, col_hi)
+        launch_range(k, xd, yd, cur)
+        if not y_final_at_end and rows_done > done:
+            ev = torch.cuda.Event()
+            ev.record(cur)
+            d2h.wait_event(ev)
+            with torch.cuda.stream(d2h):
+                yh[done:rows_done].copy_(yd[done:rows_done], non_blocking=True)
+            done = rows_done
+    if done < A.nrows:
+        ev = torch.cuda.Event()
+        ev.record(cur)
+        d2h.wait_event(ev)
+        with torch.cuda.stream(d2h):
+            yh[done:].copy_(yd[done:], non_blocking=True)
+    xd.record_stream(h2d)
+    yd.record_stream(d2h)
+    d2h.synchronize()
+    return yh
+
+
+def _csr_pipelined(A: CsrMatrix, xh, yh, chunks: int = PIPELINE_CHUNKS):
+    p = csr_plan(A)
+    nt, row_lo, maxcol_prefix = _csr_tile_info(A, p)
+    tb = [nt * k // chunks for k in range(chunks + 1)]
+    steps = [(k, tb[k], tb[k + 1]) for k in range(chunks) if tb[k + 1] > tb[k]]
+    ranges = [(int(maxcol_prefix[te - 1]), int(row_lo[te]) if te < nt else A.nrows) for _, _, te in steps]
+    spans = p.info()["launches"] > 1  # long rows spanning tiles: y final only after the fix-up
+
+    def launch(k, xd, yd, stream):
+        _, a, b = steps[k]
+        _lib.call("spmv_csr_range", p.handle, _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values), _ptr(xd), 0,
+                  A.ncols, _ptr(yd), a, b, 1 if k == len(steps) - 1 else 0, stream.cuda_stream)
+
+    return _pipelined(A, xh, yh, launch, ranges, chunks, spans)
+
+
+def _dia_pipelined(A: DiaMatrix, xh, yh, chunks: int = PIPELINE_CHUNKS):
+    offs = A.plan("dia_offsets", lambda: A.offsets.cpu().numpy().astype(np.int64))
+    max_off = int(offs.max()) if offs.size else 0
+    rb = [(A.nrows * k // chunks) // 8 * 8 for k in range(chunks)] + [A.nrows]
+    steps = [(rb[k], rb[k + 1]) for k in range(chunks) if rb[k + 1] > rb[k]]
+    ranges = [(min(A.ncols - 1, b - 1 + max_off), b) for a, b in steps]
+    esz = A.values.element_size()
+
+    def launch(k, xd, yd, stream):
+        a, b = steps[k]
+        _lib.call("spmv_dia", _lib.dtype_code(A.values.dtype), b - a, A.ncols, A.ndiags, A.padded_rows - a,
+                  _ptr(A.offsets), A.values.data_ptr() + a * A.ndiags * esz, _ptr(xd), a, 0, A.ncols,
+                  yd.data_ptr() + a * esz, stream.cuda_stream)
+
+    return _pipelined(A, xh, yh, launch, ranges, chunks, False)
+
+
+def _host_pipeline_ok(A, x, out) -> bool:
+    return (isinstance(x, torch.Tensor) and not x.is_cuda and out is not None and not out.is_cuda
+            and x.dtype == A.values.dtype and x.dim() == 1 and x.shape[0] == A.ncols
+            and out.shape == (A.nrows,) and out.dtype == A.values.dtype and A.nnz > 0 and A.nrows > 0
+            and x.is_contiguous() and out.is_contiguous())
+
+
 # ------------------------------------------------------------------ kernels --
 def spmv_coo_plain(A, x, out=None):
     """``y = A @ x`` with np.add.at semantics (kernels.py:56-66)."""
@@ -164,6 +292,8 @@ def spmv_coo_plain(A, x, out=None):
 def spmv_csr_plain(A, x, out=None):
     """``y = A @ x`` with one left-to-right sum per row (kernels.py:69-82)."""
     A = as_device(A)
+    if _host_pipeline_ok(A, x, out):
+        return _csr_pipelined(A, x, out)
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
@@ -176,6 +306,8 @@ def spmv_csr_plain(A, x, out=None):
 def spmv_dia_plain(A, x, out=None):
     """``y = A @ x`` over stored diagonals (kernels.py:85-101)."""
     A = as_device(A)
+    if _host_pipeline_ok(A, x, out) and A.ndiags > 0:
+        return _dia_pipelined(A, x, out)
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:

@@ -237,3 +237,26 @@ def test_linearity(sp):
             lhs = sp.dispatch(m, 0.6 * x1 - 1.2 * x2, version)
             rhs = 0.6 * sp.dispatch(m, x1, version) - 1.2 * sp.dispatch(m, x2, version)
             assert rel_err(lhs, rhs) <= 1e-10
+
+
+def test_host_pipelined_products_match(sp):
+    """Host x -> host y products are pipelined (x uploaded in column chunks,
+    tile ranges launched as their x arrives, finished rows downloaded while
+    later tiles run); the result must equal the device product bit for bit,
+    also with long rows spanning tiles (y downloaded after the fix-up)."""
+    from paper_2304_09511_b200 import kernels as K
+    A = sp.gen_stencil27(48, 40, 36)
+    xh = torch.rand(A.ncols, dtype=torch.float64).pin_memory()
+    yh = torch.empty(A.nrows, dtype=torch.float64).pin_memory()
+    ref = sp.spmv_csr_plain(A, xh.cuda()).cpu()
+    assert K._host_pipeline_ok(A, xh, yh)
+    assert torch.equal(sp.spmv_csr_plain(A, xh, out=yh), ref)
+    dia = sp.to_format(A, "dia")
+    yh2 = torch.empty_like(yh)
+    assert torch.equal(sp.spmv_dia_plain(dia, xh, out=yh2), sp.spmv_dia_plain(dia, xh.cuda()).cpu())
+    d = load_golden("long_rows")
+    csr = dev_matrix(sp, matrix_arrays(d, "edges/csr"), "csr")
+    x = torch.from_numpy(d["edges/x"])
+    y_dev = sp.spmv_csr_plain(csr, x.cuda()).cpu()
+    y3 = torch.empty(csr.nrows, dtype=torch.float64)
+    assert torch.equal(sp.spmv_csr_plain(csr, x, out=y3), y_dev)
