@@ -104,6 +104,17 @@ int spmv_csr_range(const spmv_csr_plan* plan, const uint32_t* row_pointers,
                    int64_t tile_begin, int64_t tile_end, int fixup,
                    void* stream);
 
+/* Host x -> host y (both pinned for overlap): x is uploaded in `chunks`
+ * column pieces on a plan-owned copy stream, tile ranges run on `stream`
+ * as soon as the x prefix they read has arrived, and finished rows of y are
+ * downloaded on a second copy stream while later tiles run (PCIe is full
+ * duplex).  Device staging lives in the plan (not reentrant per plan).
+ * Asynchronous: y_host is valid once `stream` is synchronised.
+ * chunks <= 0 selects the default (48). */
+int spmv_csr_host(spmv_csr_plan* plan, const uint32_t* row_pointers,
+                  const uint32_t* col_indices, const void* values,
+                  const void* x_host, void* y_host, int chunks, void* stream);
+
 /* Sub-warp vector kernel, lane l accumulates entries s+l, s+l+L, ... then a
  * pairwise-halving tree over next_pow2(L) lanes: bit-exact with
  * spmv_csr_vla(LaneConfig(L)) (lanes.py:101-128).  1 <= lanes <= 1024. */

@@ -23,6 +23,7 @@
 // overlap that hits L2), the row pointers once, x through L2, y written
 // once: the minimum-byte model of SURVEY.md §8(d).
 #include <algorithm>
+#include <vector>
 
 #include "tile.cuh"
 
@@ -422,6 +423,17 @@ struct spmv_csr_plan {
   DevBuf span_row, span_t0, span_t1;
   int64_t n_span = 0;
   DevBuf maxcol;
+  // host-buffer pipeline (spmv_csr_host): created on first use
+  std::vector<uint32_t> h_row_lo;
+  std::vector<int64_t> h_maxcol_prefix;
+  DevBuf xd, yd;
+  cudaStream_t h2d = nullptr, d2h = nullptr;
+  std::vector<cudaEvent_t> events;
+  ~spmv_csr_plan() {
+    if (h2d) cudaStreamDestroy(h2d);
+    if (d2h) cudaStreamDestroy(d2h);
+    for (auto e : events) cudaEventDestroy(e);
+  }
   int grid_bulk = 0, grid_direct = 0;
 };
 
@@ -495,6 +507,87 @@ static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* 
   if (p->tile == 1024) return csr_run_tiled<T, 1024>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
   if (p->tile == 4096) return csr_run_tiled<T, 4096>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
   return csr_run_tiled<T, 2048>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
+}
+
+// Host x -> host y product with H2D / compute / D2H overlap (see
+// spmv_csr_host in the header).
+static int csr_host_prepare(spmv_csr_plan* p, const uint32_t* aj, int chunks, cudaStream_t st) {
+  if (p->h_row_lo.empty()) {
+    int rc;
+    if (!p->maxcol.ptr) {
+      if ((rc = p->maxcol.alloc(4 * p->ntiles))) return rc;
+      const int64_t g = std::min<int64_t>(p->ntiles, int64_t(sm_count()) * 8);
+      tile_maxcol_kernel<<<unsigned(g), 256, 0, st>>>(aj, p->nnz, p->ntiles, p->tile, p->maxcol.as<uint32_t>());
+      SPMV_LAUNCH_CHECK();
+    }
+    p->h_row_lo.resize(p->ntiles + 1);
+    std::vector<uint32_t> mc(p->ntiles);
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->h_row_lo.data(), p->row_lo.ptr, 4 * (p->ntiles + 1), cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(mc.data(), p->maxcol.ptr, 4 * p->ntiles, cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    p->h_maxcol_prefix.resize(p->ntiles);
+    int64_t m = 0;
+    for (int64_t t = 0; t < p->ntiles; ++t) p->h_maxcol_prefix[t] = m = std::max<int64_t>(m, mc[t]);
+    const size_t vs = value_size(p->dtype);
+    if ((rc = p->xd.alloc(vs * std::max<int64_t>(p->ncols, 1))) || (rc = p->yd.alloc(vs * p->nrows))) return rc;
+    SPMV_CUDA_TRY(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
+    SPMV_CUDA_TRY(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
+  }
+  while (int(p->events.size()) < 2 * chunks + 2) {
+    cudaEvent_t e;
+    SPMV_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->events.push_back(e);
+  }
+  return SPMV_OK;
+}
+
+template <typename T>
+static int csr_host_run(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* xh, T* yh,
+                        int chunks, cudaStream_t st) {
+  int rc = csr_host_prepare(p, aj, chunks, st);
+  if (rc) return rc;
+  T* xd = p->xd.as<T>();
+  T* yd = p->yd.as<T>();
+  cudaEvent_t* ev = p->events.data();  // [0..chunks): x chunks, [chunks..2chunks): tiles, 2chunks: start, +1: end
+  SPMV_CUDA_TRY(cudaEventRecord(ev[2 * chunks], st));
+  SPMV_CUDA_TRY(cudaStreamWaitEvent(p->h2d, ev[2 * chunks], 0));
+  SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[2 * chunks], 0));
+  std::vector<int64_t> xb(chunks + 1);
+  for (int j = 0; j <= chunks; ++j) xb[j] = p->ncols * j / chunks;
+  for (int j = 0; j < chunks; ++j) {
+    if (xb[j + 1] > xb[j])
+      SPMV_CUDA_TRY(cudaMemcpyAsync(xd + xb[j], xh + xb[j], sizeof(T) * (xb[j + 1] - xb[j]), cudaMemcpyHostToDevice,
+                                    p->h2d));
+    SPMV_CUDA_TRY(cudaEventRecord(ev[j], p->h2d));
+  }
+  const bool spans = p->n_span > 0;  // y final only after the fix-up
+  int64_t done = 0;
+  int xj = 0;
+  for (int k = 0; k < chunks; ++k) {
+    const int64_t tb = p->ntiles * k / chunks, te = p->ntiles * (k + 1) / chunks;
+    if (te <= tb) continue;
+    const int64_t col_hi = p->h_maxcol_prefix[te - 1];
+    while (xj + 1 < chunks && xb[xj + 1] <= col_hi) ++xj;
+    SPMV_CUDA_TRY(cudaStreamWaitEvent(st, ev[xj], 0));
+    if ((rc = csr_run<T>(p, irp, aj, av, xd, 0, yd, st, tb, te, k == chunks - 1))) return rc;
+    const int64_t rows_done = te < p->ntiles ? int64_t(p->h_row_lo[te]) : p->nrows;
+    if (!spans && rows_done > done) {
+      SPMV_CUDA_TRY(cudaEventRecord(ev[chunks + k], st));
+      SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[chunks + k], 0));
+      SPMV_CUDA_TRY(cudaMemcpyAsync(yh + done, yd + done, sizeof(T) * (rows_done - done), cudaMemcpyDeviceToHost,
+                                    p->d2h));
+      done = rows_done;
+    }
+  }
+  if (done < p->nrows) {
+    SPMV_CUDA_TRY(cudaEventRecord(ev[2 * chunks - 1], st));
+    SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[2 * chunks - 1], 0));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(yh + done, yd + done, sizeof(T) * (p->nrows - done), cudaMemcpyDeviceToHost,
+                                  p->d2h));
+  }
+  SPMV_CUDA_TRY(cudaEventRecord(ev[2 * chunks + 1], p->d2h));
+  SPMV_CUDA_TRY(cudaStreamWaitEvent(st, ev[2 * chunks + 1], 0));
+  return SPMV_OK;
 }
 
 static int count_async(unsigned long long* dev, unsigned long long* host, cudaStream_t st) {
@@ -649,6 +742,22 @@ int spmv_csr_range(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* 
                            static_cast<double*>(y), st, tile_begin, tile_end, fixup != 0);
   return csr_run<float>(p, irp, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
                         static_cast<float*>(y), st, tile_begin, tile_end, fixup != 0);
+}
+
+int spmv_csr_host(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av, const void* x_host,
+                  void* y_host, int chunks, void* stream) {
+  if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
+  if (!x_host || !y_host) return fail(SPMV_INVALID_ARG, "NULL host buffer");
+  if (p->nrows == 0 || p->nnz == 0) return fail(SPMV_INVALID_ARG, "host pipeline needs a non-empty matrix");
+  if (chunks <= 0) chunks = 48;
+  if (chunks > 1024) chunks = 1024;
+  if (chunks > p->ntiles) chunks = int(p->ntiles);
+  cudaStream_t st = as_stream(stream);
+  if (p->dtype == SPMV_F64)
+    return csr_host_run<double>(p, irp, aj, static_cast<const double*>(av), static_cast<const double*>(x_host),
+                                static_cast<double*>(y_host), chunks, st);
+  return csr_host_run<float>(p, irp, aj, static_cast<const float*>(av), static_cast<const float*>(x_host),
+                             static_cast<float*>(y_host), chunks, st);
 }
 
 int spmv_csr(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av, const void* x,

@@ -155,7 +155,8 @@ def coo_plan(A: CooMatrix) -> _Plan:
 # download of finished rows of y (copy stream 2) overlap; PCIe is full
 # duplex, so the step approaches max(H2D, D2H) instead of H2D + compute + D2H.
 _SIDE_STREAMS: dict = {}
-PIPELINE_CHUNKS = 16
+PIPELINE_CHUNKS = int(__import__("os").environ.get("SPMV_PIPELINE_CHUNKS", "32"))
+HOST_CHUNKS = int(__import__("os").environ.get("SPMV_HOST_CHUNKS", "0"))  # 0: library default
 
 
 def _side_streams(dev):
@@ -293,7 +294,12 @@ def spmv_csr_plain(A, x, out=None):
     """``y = A @ x`` with one left-to-right sum per row (kernels.py:69-82)."""
     A = as_device(A)
     if _host_pipeline_ok(A, x, out):
-        return _csr_pipelined(A, x, out)
+        # host x -> host y: the C ABI pipelines upload / tiles / download
+        p = csr_plan(A)
+        _lib.call("spmv_csr_host", p.handle, _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values),
+                  x.data_ptr(), out.data_ptr(), HOST_CHUNKS, _stream(A.device))
+        torch.cuda.current_stream(A.device).synchronize()
+        return out
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
