@@ -156,6 +156,12 @@ int tile_mode_flags() {
   static const int f = env_int("SPMV_TILE_MODE", 0);
   return f;
 }
+// L2 evict_first hint on the TMA matrix stream: -1 = per-plan choice (COO
+// always; CSR when the plan has long rows), 0 = never, 1 = always.
+int tma_hint_mode() {
+  static const int m = env_int("SPMV_TMA_HINT", -1);
+  return m;
+}
 int ctas_per_sm_cap() {
   static const int c = env_int("SPMV_CTAS_PER_SM", 0);
   return c;

@@ -95,6 +95,10 @@ template <> __device__ __forceinline__ uint32_t ld_stream<uint32_t>(const uint32
   return v;
 }
 
+// x gathers go through the read-only path.  (An L2 evict_last policy on
+// them cost DIA a third of its throughput; see profiles/r1_notes.md.)
+template <typename T> __device__ __forceinline__ T ldx(const T* p) { return __ldg(p); }
+
 // Warp tree of lanes.py:107-128: vals[:w] + vals[w:2w] for w = W/2 .. 1.
 // shfl_down by w hands lane i the value of lane i+w, i.e. the same pairs in
 // the same operand order.

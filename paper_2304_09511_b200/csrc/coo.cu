@@ -232,9 +232,9 @@ coo_tile_kernel(const __grid_constant__ CooParams<T> P) {
     const uint32_t pre = t > 0 ? uint32_t(kExt) : 0u;
     const int s = int(i % kTileStages);
     mbar_arrive_expect_tx(&bars[s], (cnt + pre) * 4u + cnt * (4u + uint32_t(sizeof(T))));
-    bulk_g2s(rows_of(s) + (kExt - pre), P.ai + E0 - pre, (cnt + pre) * 4u, &bars[s]);
-    bulk_g2s(cols_of(s), P.aj + E0, cnt * 4u, &bars[s]);
-    bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s]);
+    bulk_g2s(rows_of(s) + (kExt - pre), P.ai + E0 - pre, (cnt + pre) * 4u, &bars[s], (P.mode & 4) != 0);
+    bulk_g2s(cols_of(s), P.aj + E0, cnt * 4u, &bars[s], (P.mode & 4) != 0);
+    bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s], (P.mode & 4) != 0);
   };
   if (BULK) {
     if (tid == 0) {
@@ -375,7 +375,7 @@ coo_vla_warp_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __re
       T p = T(0);
       if (st < nsteps && lane < lanes && c0 + lane < b) {
         const uint32_t j = c0 + lane;
-        p = mul_rn(ld_stream(av + j), __ldg(xb + ld_stream(aj + j)));
+        p = mul_rn(ld_stream(av + j), ldx(xb + ld_stream(aj + j)));
       }
       p = tree_reduce_warp(p, width);
       if (st < nsteps) yv = add_rn(yv, p);
@@ -408,7 +408,7 @@ __global__ void coo_vla_block_kernel(const uint32_t* __restrict__ run_start, con
     uint32_t nsteps = 0;
     for (uint32_t c0 = a; c0 < b; c0 += uint32_t(lanes), ++nsteps) {
       T p = T(0);
-      if (t < lanes && c0 + t < b) p = mul_rn(ld_stream(av + c0 + t), __ldg(xb + ld_stream(aj + c0 + t)));
+      if (t < lanes && c0 + t < b) p = mul_rn(ld_stream(av + c0 + t), ldx(xb + ld_stream(aj + c0 + t)));
       red[t] = p;
       __syncthreads();
       for (int w = width >> 1; w >= 32; w >>= 1) {
@@ -591,7 +591,7 @@ static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint3
   P.nnz = p->nnz;
   P.col_base = col_base;
   P.ntiles = p->ntiles;
-  P.mode = tile_mode_flags();
+  P.mode = tile_mode_flags() | (tma_hint_mode() != 0 ? 4 : 0);
   const bool aligned = (reinterpret_cast<uintptr_t>(ai) % 16 == 0) && (reinterpret_cast<uintptr_t>(aj) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;

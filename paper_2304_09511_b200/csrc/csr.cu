@@ -107,7 +107,9 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
   if (tid == 0) *s_nlong = 0;
   __syncthreads();
   PHASE_T(rt0);
+#ifdef SPMV_PHASE_TIMING
   const bool had_row = r < rend;
+#endif
   while (r < rend) {
     const uint32_t len = e - s;
     if (len == 0) {
@@ -211,8 +213,8 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
     const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
     const int s = int(i % kTileStages);
     mbar_arrive_expect_tx(&bars[s], cnt * uint32_t(sizeof(uint32_t) + sizeof(T)));
-    bulk_g2s(cols_of(s), P.aj + E0, cnt * uint32_t(sizeof(uint32_t)), &bars[s]);
-    bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s]);
+    bulk_g2s(cols_of(s), P.aj + E0, cnt * uint32_t(sizeof(uint32_t)), &bars[s], (P.mode & 4) != 0);
+    bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s], (P.mode & 4) != 0);
   };
   if (BULK) {
     if (tid == 0) {
@@ -374,7 +376,7 @@ csr_vla_warp_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict
     T acc = T(0);
     if (lane < lanes)
       for (uint32_t j = s + lane; j < e; j += uint32_t(lanes))
-        acc = add_rn(acc, mul_rn(ld_stream(av + j), __ldg(xb + ld_stream(aj + j))));
+        acc = add_rn(acc, mul_rn(ld_stream(av + j), ldx(xb + ld_stream(aj + j))));
     acc = tree_reduce_warp(acc, width);
     if (lane == 0 && r < nrows) y[r] = (s == e) ? T(0) : acc;
   }
@@ -394,7 +396,7 @@ __global__ void csr_vla_block_kernel(const uint32_t* __restrict__ irp, const uin
     T acc = T(0);
     if (t < lanes)
       for (uint32_t j = s + t; j < e; j += uint32_t(lanes))
-        acc = add_rn(acc, mul_rn(ld_stream(av + j), __ldg(xb + ld_stream(aj + j))));
+        acc = add_rn(acc, mul_rn(ld_stream(av + j), ldx(xb + ld_stream(aj + j))));
     red[t] = acc;
     __syncthreads();
     for (int w = width >> 1; w >= 32; w >>= 1) {
@@ -479,7 +481,7 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
   P.tile_begin = tb;
   P.tile_end = te;
   P.exact_len = p->exact_len;
-  P.mode = tile_mode_flags();
+  P.mode = tile_mode_flags() | ((tma_hint_mode() < 0 ? p->n_long > 0 : tma_hint_mode() > 0) ? 4 : 0);
   const bool aligned = (reinterpret_cast<uintptr_t>(aj) % 16 == 0) && (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
   const size_t smem = CsrSmem<T, TILE>::total;

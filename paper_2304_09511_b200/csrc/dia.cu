@@ -38,7 +38,7 @@ __device__ __forceinline__ T dia_row(const T* __restrict__ v, const int32_t* __r
 #pragma unroll
     for (int d = 0; d < ND; ++d) {
       const int64_t col = grow + offs[d];
-      xv[d] = (col >= 0 && col < ncols) ? __ldg(xb + col) : T(0);
+      xv[d] = (col >= 0 && col < ncols) ? ldx(xb + col) : T(0);
     }
 #pragma unroll
     for (int d = 0; d < ND; ++d) {
@@ -49,7 +49,7 @@ __device__ __forceinline__ T dia_row(const T* __restrict__ v, const int32_t* __r
 #pragma unroll 9
     for (int d = 0; d < nd; ++d) {
       const int64_t col = grow + offs[d];
-      if (col >= 0 && col < ncols) acc = add_rn(acc, mul_rn(v[d], __ldg(xb + col)));
+      if (col >= 0 && col < ncols) acc = add_rn(acc, mul_rn(v[d], ldx(xb + col)));
     }
   }
   return acc;
@@ -128,7 +128,7 @@ dia_direct_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offset
     const T* v = vals + size_t(i) * nd;
     for (int d = 0; d < nd; ++d) {
       const int64_t col = row_base + i + __ldg(offsets + d);
-      if (col >= 0 && col < ncols) acc = add_rn(acc, mul_rn(__ldg(v + d), __ldg(xb + col)));
+      if (col >= 0 && col < ncols) acc = add_rn(acc, mul_rn(__ldg(v + d), ldx(xb + col)));
     }
     y[i] = acc;
   }

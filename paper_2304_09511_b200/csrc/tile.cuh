@@ -24,6 +24,7 @@ constexpr int max_long_segs() { return TILE / (kExactLen + 1) + 4; }
 // SM (smaller shared-memory ring); 2048 halves the per-tile overhead.
 int tile_entries();
 int ctas_per_sm_cap();  // 0 = occupancy limit
+int tma_hint_mode();    // SPMV_TMA_HINT: -1 auto, 0 off, 1 on
 int tile_mode_flags();  // experiments: bit0 no products mode, bit1 warp-per-segment long rows
 
 static_assert(kExt == kExactLen, "extension must cover a whole short row");
@@ -60,7 +61,7 @@ __device__ __forceinline__ T row_dot(const uint32_t* __restrict__ c, const T* __
   for (; i + B <= len; i += B) {
     T p[B];
 #pragma unroll
-    for (int j = 0; j < B; ++j) p[j] = mul_rn(v[i + j], __ldg(xb + c[i + j]));
+    for (int j = 0; j < B; ++j) p[j] = mul_rn(v[i + j], ldx(xb + c[i + j]));
 #pragma unroll
     for (int j = 0; j < B; ++j) acc = add_rn(acc, p[j]);
   }
@@ -68,11 +69,11 @@ __device__ __forceinline__ T row_dot(const uint32_t* __restrict__ c, const T* __
     for (; i + 8 <= len; i += 8) {
       T p[8];
 #pragma unroll
-      for (int j = 0; j < 8; ++j) p[j] = mul_rn(v[i + j], __ldg(xb + c[i + j]));
+      for (int j = 0; j < 8; ++j) p[j] = mul_rn(v[i + j], ldx(xb + c[i + j]));
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc = add_rn(acc, p[j]);
     }
-  for (; i < len; ++i) acc = add_rn(acc, mul_rn(v[i], __ldg(xb + c[i])));
+  for (; i < len; ++i) acc = add_rn(acc, mul_rn(v[i], ldx(xb + c[i])));
   return acc;
 }
 
@@ -94,13 +95,13 @@ __device__ __forceinline__ void form_products(const uint32_t* __restrict__ cols,
   for (; k + 3 * kTileThreads < cnt; k += 4 * kTileThreads) {
     const uint32_t c0 = cols[k], c1 = cols[k + kTileThreads], c2 = cols[k + 2 * kTileThreads],
                    c3 = cols[k + 3 * kTileThreads];
-    const T x0 = __ldg(xb + c0), x1 = __ldg(xb + c1), x2 = __ldg(xb + c2), x3 = __ldg(xb + c3);
+    const T x0 = ldx(xb + c0), x1 = ldx(xb + c1), x2 = ldx(xb + c2), x3 = ldx(xb + c3);
     vals[k] = mul_rn(vals[k], x0);
     vals[k + kTileThreads] = mul_rn(vals[k + kTileThreads], x1);
     vals[k + 2 * kTileThreads] = mul_rn(vals[k + 2 * kTileThreads], x2);
     vals[k + 3 * kTileThreads] = mul_rn(vals[k + 3 * kTileThreads], x3);
   }
-  for (; k < cnt; k += kTileThreads) vals[k] = mul_rn(vals[k], __ldg(xb + cols[k]));
+  for (; k < cnt; k += kTileThreads) vals[k] = mul_rn(vals[k], ldx(xb + cols[k]));
 }
 
 // Long segments of one tile, reduced by all warps of the CTA: every segment
@@ -128,7 +129,7 @@ __device__ __forceinline__ void reduce_long_segments(const uint32_t* __restrict_
     for (int i = warp; i < nl; i += kTileThreads / 32) {
       T acc = T(0);
       for (uint32_t j = segs[i].lo + lane; j < segs[i].hi; j += 32)
-        acc = add_rn(acc, products ? vals[j] : mul_rn(vals[j], __ldg(xb + cols[j])));
+        acc = add_rn(acc, products ? vals[j] : mul_rn(vals[j], ldx(xb + cols[j])));
       acc = tree_reduce_warp(acc, 32);
       if (lane == 0) seg_part[i] = acc;
     }
@@ -179,13 +180,13 @@ __device__ __forceinline__ void reduce_long_segments(const uint32_t* __restrict_
       for (; j < uhi; j += 32) acc = add_rn(acc, vals[j]);
     } else {
       for (; j + 96 < uhi; j += 128) {  // 4 gathers in flight per lane, adds in order
-        const T p0 = mul_rn(vals[j], __ldg(xb + cols[j]));
-        const T p1 = mul_rn(vals[j + 32], __ldg(xb + cols[j + 32]));
-        const T p2 = mul_rn(vals[j + 64], __ldg(xb + cols[j + 64]));
-        const T p3 = mul_rn(vals[j + 96], __ldg(xb + cols[j + 96]));
+        const T p0 = mul_rn(vals[j], ldx(xb + cols[j]));
+        const T p1 = mul_rn(vals[j + 32], ldx(xb + cols[j + 32]));
+        const T p2 = mul_rn(vals[j + 64], ldx(xb + cols[j + 64]));
+        const T p3 = mul_rn(vals[j + 96], ldx(xb + cols[j + 96]));
         acc = add_rn(add_rn(add_rn(add_rn(acc, p0), p1), p2), p3);
       }
-      for (; j < uhi; j += 32) acc = add_rn(acc, mul_rn(vals[j], __ldg(xb + cols[j])));
+      for (; j < uhi; j += 32) acc = add_rn(acc, mul_rn(vals[j], ldx(xb + cols[j])));
     }
     acc = tree_reduce_warp(acc, 32);
     if (lane == 0) unit_part[u] = acc;
@@ -206,7 +207,7 @@ template <typename T>
 __device__ __forceinline__ T warp_segment_dot(const uint32_t* __restrict__ c, const T* __restrict__ v, uint32_t lo,
                                               uint32_t hi, int lane, const T* __restrict__ xb) {
   T acc = T(0);
-  for (uint32_t j = lo + lane; j < hi; j += 32) acc = add_rn(acc, mul_rn(v[j], __ldg(xb + c[j])));
+  for (uint32_t j = lo + lane; j < hi; j += 32) acc = add_rn(acc, mul_rn(v[j], ldx(xb + c[j])));
   return tree_reduce_warp(acc, 32);
 }
 
