@@ -217,6 +217,17 @@ def launches_per_spmv(sp, m) -> int:
     return 1
 
 
+def plan_of(sp, m) -> dict:
+    """Kernel configuration the plan chose (tile entries, consumer groups)."""
+    from paper_2304_09511_b200 import kernels as K
+    if m.format == sp.Format.CSR:
+        i = K.csr_plan(m).info()
+        return {"tile": i["tile"], "groups": i["groups"]}
+    if m.format == sp.Format.COO:
+        return {"tile": K.coo_plan(m).info()["tile"]}
+    return {}
+
+
 def bytes_of(m, fmt) -> int:
     sv = m.values.element_size()
     nd = m.ndiags if fmt.startswith("dia") else 0
@@ -288,7 +299,7 @@ def run_ours(args, torch, dist, rank, world, local_rank):
         b = bytes_of(m, fmt)
         results[fmt] = {"gflops": round(2.0 * m.nnz / t / 1e9, 2), "ms_per_spmv": round(t * 1e3, 4),
                         "gbs": round(b / t / 1e9, 1), "bytes_per_spmv": b, "launches": launches_per_spmv(sp, m),
-                        "roofline_frac": round(b / t / 1e9 / pk["hbm_gbs"], 4), "nnz": m.nnz}
+                        "plan": plan_of(sp, m), "roofline_frac": round(b / t / 1e9 / pk["hbm_gbs"], 4), "nnz": m.nnz}
     m = mats[head]
     t = results[head]["ms_per_spmv"] / 1e3
     line = {

@@ -59,8 +59,10 @@ int spmv_device_sm_count(int* out);
 typedef struct spmv_csr_plan spmv_csr_plan;
 
 /* Analyse the matrix once: long-row census (rows > exact_len entries), tile
- * size (2048 entries, 1024 when long rows exist), the row range of every
- * tile and the list of long rows spanning tiles.  The SpMV kernel streams
+ * size (2048 entries, 1024 when long rows exist), consumer groups per CTA
+ * (G groups share a G+1 stage ring: 3, or 7 for rows averaging < 16
+ * entries, 1 with long rows), the row range of every tile and the list of
+ * long rows spanning tiles.  The SpMV kernel streams
  * fixed entry tiles with TMA bulk copies; rows of <= exact_len entries are
  * summed left to right by one thread (bit-exact with spmv_csr_plain); longer
  * rows are reduced in 256-entry vla-32 units (bit-exact with
@@ -74,10 +76,12 @@ int spmv_csr_plan_destroy(spmv_csr_plan* plan);
  * the CSR tile kernel, read and reset (8 entries); else SPMV_UNSUPPORTED. */
 int spmv_debug_csr_phases(unsigned long long* out8);
 /* n_long_rows: rows longer than exact_len; n_items: entries per tile;
- * launches: kernels one spmv_csr call launches (1, or 2 with the span
- * fix-up). */
+ * launches: kernels one spmv_csr call launches (1; +1 for tail tiles the
+ * bulk engine cannot address when groups > 1; +1 for the span fix-up). */
 int spmv_csr_plan_info(const spmv_csr_plan* plan, int64_t* n_long_rows,
                        int64_t* n_items, int64_t* launches);
+/* Consumer groups per tile CTA the plan chose (SPMV_CSR_GROUPS overrides). */
+int spmv_csr_plan_groups(const spmv_csr_plan* plan, int* groups);
 
 /* y[r] = sum_j av[j] * x[aj[j] - col_base] over row r.  x holds the window
  * of global columns [col_base, col_base + x_len).  For a single-device

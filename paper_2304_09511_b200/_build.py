@@ -64,11 +64,16 @@ def build(verbose: bool = False, force: bool = False) -> Path:
     """Compile every csrc/*.cu for sm_100a and link libspmv_b200.so."""
     OBJ_DIR.mkdir(exist_ok=True)
     srcs = _sources()
+    stamp = OBJ_DIR / "flags.txt"  # objects built with other flags are stale
+    flags = " ".join(NVCC_FLAGS)
+    if not stamp.exists() or stamp.read_text() != flags:
+        force = True
     if force:
         for o in OBJ_DIR.glob("*.o"):
             o.unlink()
     with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
         objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
+    stamp.write_text(flags)
     if force or _stale(LIB_PATH, objs):
         # Export only the C ABI (spmv_*); static cudart and C++ internals stay local.
         cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB_PATH), *map(str, objs),

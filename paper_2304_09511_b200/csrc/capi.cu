@@ -146,7 +146,7 @@ static int env_int(const char* name, int dflt) {
 int tile_entries() {
   static const int t = [] {
     const int v = env_int("SPMV_TILE", 0);
-    return (v == 1024 || v == 2048 || v == 4096) ? v : 0;
+    return (v == 1024 || v == 1920 || v == 2048 || v == 4096) ? v : 0;
   }();
   return t;
 }
@@ -161,6 +161,11 @@ int tile_mode_flags() {
 int tma_hint_mode() {
   static const int m = env_int("SPMV_TMA_HINT", -1);
   return m;
+}
+// CSR consumer groups per tile CTA (0 = plan's choice).
+int csr_groups() {
+  static const int g = env_int("SPMV_CSR_GROUPS", 0);
+  return g;
 }
 int ctas_per_sm_cap() {
   static const int c = env_int("SPMV_CTAS_PER_SM", 0);

@@ -97,7 +97,14 @@ template <> __device__ __forceinline__ uint32_t ld_stream<uint32_t>(const uint32
 
 // x gathers go through the read-only path.  (An L2 evict_last policy on
 // them cost DIA a third of its throughput; see profiles/r1_notes.md.)
-template <typename T> __device__ __forceinline__ T ldx(const T* p) { return __ldg(p); }
+template <typename T> __device__ __forceinline__ T ldx(const T* p) {
+#ifdef SPMV_NO_X  // experiment: gathers replaced by a constant (results wrong)
+  (void)p;
+  return T(1);
+#else
+  return __ldg(p);
+#endif
+}
 
 // Warp tree of lanes.py:107-128: vals[:w] + vals[w:2w] for w = W/2 .. 1.
 // shfl_down by w hands lane i the value of lane i+w, i.e. the same pairs in

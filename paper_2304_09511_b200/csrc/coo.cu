@@ -125,7 +125,7 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
   // gathers entry-per-lane first (see tile.cuh form_products).
   const bool products = (P.mode & 1) && nseg > kTileThreads;
   if (products) {
-    form_products(cols, vals, cnt_ext, xb);
+    form_products(cols, vals, cnt_ext, xb, int(threadIdx.x));
     __syncthreads();
   }
 
@@ -182,7 +182,7 @@ __device__ __forceinline__ void coo_tile_long(int64_t t, const uint32_t* __restr
   T* seg_part = reinterpret_cast<T*>(scratch + S::units_bytes + S::upart_bytes);
   const bool products = s_long[0].flags & 4u;
   reduce_long_segments<T, TILE>(cols, vals, s_long, nl, units, unit_part, s_nunits, seg_part, xb, products,
-                                warp_per_seg);
+                                warp_per_seg, TileGroup<kTileThreads>{int(threadIdx.x), 0});
   for (int i = threadIdx.x; i < nl; i += kTileThreads) {
     const LongSeg L = s_long[i];
     const T part = seg_part[i];
@@ -551,7 +551,7 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
   SPMV_CUDA_TRY(cudaMemcpyAsync(&h, nl.ptr, 8, cudaMemcpyDeviceToHost, st));
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
   p->n_long = int64_t(h);
-  p->tile = tile_entries() ? tile_entries() : 2048;
+  p->tile = tile_entries() == 1024 ? 1024 : 2048;  // the COO kernels exist for these two
   p->ntiles = (nnz + p->tile - 1) / p->tile;
   const size_t vs = value_size(p->dtype);
   if ((rc = p->head_row.alloc(4 * p->ntiles)) || (rc = p->tail_row.alloc(4 * p->ntiles)) ||

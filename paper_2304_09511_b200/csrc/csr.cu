@@ -63,18 +63,32 @@ struct CsrParams {
   int mode;
 };
 
-template <typename T, int TILE>
+// Shared memory of a CSR tile CTA with G consumer groups and G + 1 stages:
+// [0, 64) stage mbarriers, [64, 96) stage tickets, [96, 160) two counters
+// per group, then one long-row scratch block per group, then the stage ring.
+template <typename T, int TILE, int G = 1>
 struct CsrSmem {
+  static constexpr int stages = G + 1;
   static constexpr size_t cols_bytes = align_up(sizeof(uint32_t) * (TILE + kExt), 128);
   static constexpr size_t vals_bytes = align_up(sizeof(T) * (TILE + kExt), 128);
   static constexpr size_t stage_bytes = cols_bytes + vals_bytes;
-  static constexpr size_t segs_off = 64;
-  static constexpr size_t units_off = segs_off + align_up(sizeof(LongSeg) * max_long_segs<TILE>(), 16);
+  static constexpr size_t units_off = align_up(sizeof(LongSeg) * max_long_segs<TILE>(), 16);  // in a group block
   static constexpr size_t upart_off = units_off + align_up(sizeof(LongUnit) * max_units<TILE>(), 16);
   static constexpr size_t spart_off = upart_off + align_up(sizeof(T) * max_units<TILE>(), 16);
-  static constexpr size_t header = align_up(spart_off + sizeof(T) * max_long_segs<TILE>(), 128);
-  static constexpr size_t total = header + kTileStages * stage_bytes;
+  static constexpr size_t group_bytes = align_up(spart_off + sizeof(T) * max_long_segs<TILE>(), 16);
+  static constexpr size_t tickets_off = 64, counters_off = 96, groups_off = 160;
+  static constexpr size_t header = align_up(groups_off + G * group_bytes, 128);
+  static constexpr size_t total = header + stages * stage_bytes;
+  static_assert(stages <= 8, "mbarrier / ticket / counter slots");
 };
+
+// Threads per CTA and resident CTAs per SM the CSR tile kernel is built for.
+template <int G> constexpr int csr_group_threads() { return G == 1 ? kTileThreads : 128; }
+template <int G> constexpr int csr_cta_threads() { return G * csr_group_threads<G>(); }
+#ifndef SPMV_CSR_MINB
+#define SPMV_CSR_MINB 4
+#endif
+template <int G> constexpr int csr_min_blocks() { return G == 1 ? SPMV_CSR_MINB : (G == 2 ? 3 : (G == 3 ? 2 : 1)); }
 
 // Rows of one tile.  Row-per-lane mode (few rows per tile, e.g. the
 // stencil's ~77): each thread forms its row's products from the staged
@@ -82,14 +96,15 @@ struct CsrSmem {
 // than threads, e.g. Zipf's short rows): all gathers of the tile are issued
 // entry-per-lane first, then rows are summed from shared memory.  Long
 // segments are only queued here.
-template <typename T, int TILE>
+template <typename T, int TILE, int NT>
 __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, const uint32_t* __restrict__ cols,
-                                              T* __restrict__ vals, LongSeg* s_long, int* s_nlong
+                                              T* __restrict__ vals, LongSeg* s_long, int* s_nlong,
+                                              const TileGroup<NT>& grp
 #ifdef SPMV_PHASE_TIMING
                                               , unsigned long long* s_phase_acc
 #endif
 ) {
-  const int tid = threadIdx.x;
+  const int tid = grp.tid;
   const int64_t E0 = t * TILE;
   const int64_t E1 = E0 + TILE;
   const T* xb = P.x - P.col_base;
@@ -102,10 +117,10 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
     s = __ldg(P.irp + r);
     e = __ldg(P.irp + r + 1);
   }
-  const bool products = (P.mode & 1) && (rend - R0) > kTileThreads;
-  if (products) form_products(cols, vals, int(min(int64_t(TILE + kExt), P.nnz - E0)), xb);
+  const bool products = (P.mode & 1) && (rend - R0) > NT;
+  if (products) form_products<T, NT>(cols, vals, int(min(int64_t(TILE + kExt), P.nnz - E0)), xb, tid);
   if (tid == 0) *s_nlong = 0;
-  __syncthreads();
+  grp.sync();
   PHASE_T(rt0);
 #ifdef SPMV_PHASE_TIMING
   const bool had_row = r < rend;
@@ -133,40 +148,41 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
         s_long[idx] = L;
       }
     }
-    r += kTileThreads;
+    r += NT;
     if (r < rend) {
       s = __ldg(P.irp + r);
       e = __ldg(P.irp + r + 1);
     }
   }
 #ifdef SPMV_PHASE_TIMING
-  if (had_row && tid == 0) {  // thread 0 only: no atomic contention
+  if (had_row && threadIdx.x == 0) {  // thread 0 only: no atomic contention
     PHASE_T(rt1);
     PHASE_ADD(4, rt1 - rt0);
     PHASE_ADD(5, 1);
   }
 #endif
-  __syncthreads();
+  grp.sync();
 }
 
 // Long segments of one tile.  A row inside the tile is written directly; a
 // row spanning tiles leaves its partial in tail[t] (the tile holding its
 // first entry) or head[t] (later tiles); csr_span_fixup_kernel adds them in
 // tile order after the tile kernel (no fences or atomics in the hot kernel).
-template <typename T, int TILE>
+template <typename T, int TILE, int NT>
 __device__ __forceinline__ void csr_tile_long(int64_t t, const uint32_t* __restrict__ cols, const T* __restrict__ vals,
                                            const LongSeg* __restrict__ s_long, int nl, unsigned char* scratch,
                                            int* s_nunits, const T* __restrict__ xb, T* __restrict__ y,
-                                           T* __restrict__ head, T* __restrict__ tail, bool warp_per_seg) {
-  using S = CsrSmem<T, TILE>;
+                                           T* __restrict__ head, T* __restrict__ tail, bool warp_per_seg,
+                                           const TileGroup<NT>& grp) {
+  using S = CsrSmem<T, TILE>;  // group-block offsets do not depend on G
   LongUnit* units = reinterpret_cast<LongUnit*>(scratch + S::units_off);
   T* unit_part = reinterpret_cast<T*>(scratch + S::upart_off);
   T* seg_part = reinterpret_cast<T*>(scratch + S::spart_off);
   const bool products = s_long[0].flags & 1u;
-  reduce_long_segments<T, TILE>(cols, vals, s_long, nl, units, unit_part, s_nunits, seg_part, xb, products,
-                                warp_per_seg);
+  reduce_long_segments<T, TILE, NT>(cols, vals, s_long, nl, units, unit_part, s_nunits, seg_part, xb, products,
+                                    warp_per_seg, grp);
   const int64_t E0 = t * TILE, E1 = E0 + TILE;
-  for (int i = threadIdx.x; i < nl; i += kTileThreads) {
+  for (int i = grp.tid; i < nl; i += NT) {
     const LongSeg L = s_long[i];
     const T part = seg_part[i];
     if (int64_t(L.s) >= E0 && int64_t(L.e) <= E1)
@@ -178,90 +194,111 @@ __device__ __forceinline__ void csr_tile_long(int64_t t, const uint32_t* __restr
   }
 }
 
-template <typename T, bool BULK, int TILE>
-#ifndef SPMV_CSR_MINB
-#define SPMV_CSR_MINB 4
-#endif
-__global__ void __launch_bounds__(kTileThreads, SPMV_CSR_MINB)
+// G == 1: one 256-thread group, 2 stages (a tile computes while the next
+// loads).  G > 1: G groups of 128 threads over G + 1 stages, tile i of the
+// CTA going to group i % G and stage i % (G + 1): G tiles compute while one
+// loads, so more rows are in flight per byte of shared memory (the stencil's
+// limiter).  Multi-group CTAs take bulk tiles only; the host runs the tail
+// tiles with G == 1.
+template <typename T, bool BULK, int TILE, int G>
+__global__ void __launch_bounds__(csr_cta_threads<G>(), csr_min_blocks<G>())
 csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
+  static_assert(G == 1 || BULK, "multi-group CTAs are TMA-fed");
+  constexpr int NT = csr_group_threads<G>();
   extern __shared__ __align__(128) unsigned char smem[];
   PHASE_DECL
 #ifdef SPMV_PHASE_TIMING
   if (threadIdx.x < 8) s_phase_acc[threadIdx.x] = 0;
   __syncthreads();
 #endif
-  using S = CsrSmem<T, TILE>;
+  using S = CsrSmem<T, TILE, G>;
+  constexpr int STAGES = S::stages;
+  const int g = int(threadIdx.x) / NT;
+  const TileGroup<NT> grp{int(threadIdx.x) % NT, G == 1 ? 0 : 1 + g};
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-  int* s_nlong = reinterpret_cast<int*>(smem + 32);
-  LongSeg* s_long = reinterpret_cast<LongSeg*>(smem + S::segs_off);
+  volatile int* tickets = reinterpret_cast<volatile int*>(smem + S::tickets_off);  // CTA-local tile of each stage
+  int* s_nlong = reinterpret_cast<int*>(smem + S::counters_off) + 2 * g;           // [0] segments, [1] units
+  unsigned char* gscratch = smem + S::groups_off + size_t(g) * S::group_bytes;
+  LongSeg* s_long = reinterpret_cast<LongSeg*>(gscratch);
   unsigned char* stages = smem + S::header;
-  const int tid = threadIdx.x;
   auto cols_of = [&](int s) { return reinterpret_cast<uint32_t*>(stages + s * S::stage_bytes); };
   auto vals_of = [&](int s) { return reinterpret_cast<T*>(stages + s * S::stage_bytes + S::cols_bytes); };
 
   // This CTA's tiles (grid-strided over [tile_begin, tile_end), so all SMs
   // sweep neighbouring rows together and share x lines in L2): bulk-copyable
   // ones first (TMA pipeline), then the tail tiles the bulk engine cannot
-  // address (cooperative loads).
+  // address (cooperative loads, G == 1 only).
   const int64_t n_bulk = BULK ? min(P.n_bulk, P.tile_end) : P.tile_begin;
   const int64_t first = P.tile_begin + blockIdx.x, stride = gridDim.x;
   const int64_t mine_bulk = first < n_bulk ? (n_bulk - 1 - first) / stride + 1 : 0;
   const int64_t tail0 = max(n_bulk, P.tile_begin) + blockIdx.x;
-  const int64_t mine_tail = tail0 < P.tile_end ? (P.tile_end - 1 - tail0) / stride + 1 : 0;
+  const int64_t mine_tail = G == 1 && tail0 < P.tile_end ? (P.tile_end - 1 - tail0) / stride + 1 : 0;
   auto issue = [&](int64_t i) {
     const int64_t E0 = (first + i * stride) * TILE;
     const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
-    const int s = int(i % kTileStages);
+    const int s = int(i % STAGES);
+    if (G > 1) tickets[s] = int(i);
     mbar_arrive_expect_tx(&bars[s], cnt * uint32_t(sizeof(uint32_t) + sizeof(T)));
     bulk_g2s(cols_of(s), P.aj + E0, cnt * uint32_t(sizeof(uint32_t)), &bars[s], (P.mode & 4) != 0);
     bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s], (P.mode & 4) != 0);
   };
   if (BULK) {
-    if (tid == 0) {
-      for (int s = 0; s < kTileStages; ++s) mbar_init(&bars[s], 1);
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&bars[s], 1);
+        tickets[s] = -1;
+      }
       mbar_fence_init();
     }
     __syncthreads();
-    if (tid == 0)
-      for (int64_t i = 0; i < kTileStages && i < mine_bulk; ++i) issue(i);
+    if (threadIdx.x == 0)
+      for (int64_t i = 0; i < STAGES && i < mine_bulk; ++i) issue(i);
   }
-  for (int64_t i = 0; i < mine_bulk + mine_tail; ++i) {
+  for (int64_t i = g; i < mine_bulk + mine_tail; i += G) {
     int s = 0;
     int64_t t;
     PHASE_T(p0);
     if (i < mine_bulk) {
-      s = int(i % kTileStages);
+      s = int(i % STAGES);
       t = first + i * stride;
-      mbar_wait(&bars[s], uint32_t((i / kTileStages) & 1));
+      // A parity wait only tells the current phase from the previous one.
+      // With G > 1 the previous tile of this stage belongs to another group
+      // and may still be in flight, so first wait until tile i is the one
+      // issued into the stage (its predecessor's phase has then completed).
+      if (G > 1)
+        while (tickets[s] != int(i)) __nanosleep(32);
+      mbar_wait(&bars[s], uint32_t((i / STAGES) & 1));
     } else {
       t = tail0 + (i - mine_bulk) * stride;
       const int64_t E0 = t * TILE;
       const int cnt = int(min(int64_t(TILE + kExt), P.nnz - E0));
-      for (int k = tid; k < cnt; k += kTileThreads) {
+      for (int k = grp.tid; k < cnt; k += NT) {
         cols_of(0)[k] = P.aj[E0 + k];
         vals_of(0)[k] = P.av[E0 + k];
       }
-      __syncthreads();
+      grp.sync();
     }
     PHASE_T(p1);
-    csr_tile_rows<T, TILE>(P, t, cols_of(s), vals_of(s), s_long, s_nlong
+#ifndef SPMV_STREAM_ONLY  // experiment: TMA stream alone (y is not written)
+    csr_tile_rows<T, TILE, NT>(P, t, cols_of(s), vals_of(s), s_long, s_nlong, grp
 #ifdef SPMV_PHASE_TIMING
-                           , s_phase_acc
+                               , s_phase_acc
 #endif
     );
     PHASE_T(p2);
     const int nl = *s_nlong;
     if (nl > 0)
-      csr_tile_long<T, TILE>(t, cols_of(s), vals_of(s), s_long, nl, smem, s_nlong + 1, P.x - P.col_base, P.y,
-                             P.head, P.tail, (P.mode & 2) != 0);
-    __syncthreads();  // stage s free
+      csr_tile_long<T, TILE, NT>(t, cols_of(s), vals_of(s), s_long, nl, gscratch, s_nlong + 1, P.x - P.col_base,
+                                 P.y, P.head, P.tail, (P.mode & 2) != 0, grp);
+#endif
+    grp.sync();  // stage s free
     PHASE_T(p3);
-    if (BULK && tid == 0 && i + kTileStages < mine_bulk) {
+    if (BULK && grp.tid == 0 && i + STAGES < mine_bulk) {
       fence_proxy_async();
-      issue(i + kTileStages);
+      issue(i + STAGES);
     }
 #ifdef SPMV_PHASE_TIMING
-    if (tid == 0) {
+    if (threadIdx.x == 0) {
       PHASE_T(p4);
       PHASE_ADD(0, p1 - p0);
       PHASE_ADD(1, p2 - p1);
@@ -272,6 +309,7 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
 #endif
   }
 #ifdef SPMV_PHASE_TIMING
+  __syncthreads();
   if (threadIdx.x < 8) atomicAdd(&g_phase[threadIdx.x], s_phase_acc[threadIdx.x]);
 #endif
 }
@@ -436,28 +474,45 @@ struct spmv_csr_plan {
     if (d2h) cudaStreamDestroy(d2h);
     for (auto e : events) cudaEventDestroy(e);
   }
-  int grid_bulk = 0, grid_direct = 0;
+  int groups = 1;                    // consumer groups per tile CTA (csr_tile_kernel G)
+  int grid_bulk = 0, grid_direct = 0;  // G-group TMA kernel / single-group kernel
 };
 
-template <typename T, int TILE>
-static int csr_launch_config(spmv_csr_plan* p) {
-  using S = CsrSmem<T, TILE>;
-  SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_tile_kernel<T, true, TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(S::total)));
-  SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_tile_kernel<T, false, TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(S::total)));
-  int per_sm = 0;
-  SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_tile_kernel<T, true, TILE>,
-                                                              kTileThreads, S::total));
-  if (ctas_per_sm_cap() > 0 && per_sm > ctas_per_sm_cap()) per_sm = ctas_per_sm_cap();
-  if (per_sm < 1) per_sm = 1;
-  const int64_t cap = int64_t(sm_count()) * per_sm;
-  p->grid_bulk = int(p->ntiles < cap ? p->ntiles : cap);
-  p->grid_direct = p->grid_bulk;
+// (tile, groups) pairs with compiled kernels.
+#define SPMV_CSR_CONFIGS(X) \
+  X(1024, 1) X(2048, 1) X(4096, 1) X(1920, 1) X(1920, 2) X(2048, 3) X(2048, 7) X(1792, 7)
+static bool csr_config_known(int64_t tile, int groups) {
+#define X(TL, GR) if (tile == TL && groups == GR) return true;
+  SPMV_CSR_CONFIGS(X)
+#undef X
+  return false;
+}
+
+template <typename K>
+static int csr_ctas_per_sm(K kernel, int threads, size_t smem, int* per_sm) {
+  SPMV_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kernel, threads, smem));
+  if (ctas_per_sm_cap() > 0 && *per_sm > ctas_per_sm_cap()) *per_sm = ctas_per_sm_cap();
+  if (*per_sm < 1) *per_sm = 1;
   return SPMV_OK;
 }
 
-template <typename T, int TILE>
+template <typename T, int TILE, int G>
+static int csr_launch_config(spmv_csr_plan* p) {
+  int per_sm = 0, per_sm1 = 0, rc;
+  using S1 = CsrSmem<T, TILE, 1>;
+  if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, true, TILE, G>, csr_cta_threads<G>(), CsrSmem<T, TILE, G>::total,
+                            &per_sm)))
+    return rc;
+  if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, true, TILE, 1>, kTileThreads, S1::total, &per_sm1))) return rc;
+  if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, false, TILE, 1>, kTileThreads, S1::total, &per_sm1))) return rc;
+  const int64_t cap = int64_t(sm_count()) * per_sm, cap1 = int64_t(sm_count()) * per_sm1;
+  p->grid_bulk = int(p->ntiles < cap ? p->ntiles : cap);
+  p->grid_direct = int(p->ntiles < cap1 ? p->ntiles : cap1);
+  return SPMV_OK;
+}
+
+template <typename T, int TILE, int G>
 static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st, int64_t tb, int64_t te, bool fixup) {
   if (p->nrows == 0) return SPMV_OK;
@@ -484,15 +539,29 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
   P.mode = tile_mode_flags() | ((tma_hint_mode() < 0 ? p->n_long > 0 : tma_hint_mode() > 0) ? 4 : 0);
   const bool aligned = (reinterpret_cast<uintptr_t>(aj) % 16 == 0) && (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
-  const size_t smem = CsrSmem<T, TILE>::total;
-  const int64_t grid = std::min<int64_t>(aligned ? p->grid_bulk : p->grid_direct, te - tb);
-  if (grid > 0) {
-    if (aligned)
-      csr_tile_kernel<T, true, TILE><<<unsigned(grid), kTileThreads, smem, st>>>(P);
-    else
-      csr_tile_kernel<T, false, TILE><<<unsigned(grid), kTileThreads, smem, st>>>(P);
-    SPMV_LAUNCH_CHECK();
+  const size_t smem1 = CsrSmem<T, TILE, 1>::total;
+  if (!aligned) {
+    const int64_t grid = std::min<int64_t>(p->grid_direct, te - tb);
+    if (grid > 0) csr_tile_kernel<T, false, TILE, 1><<<unsigned(grid), kTileThreads, smem1, st>>>(P);
+  } else if (G == 1) {
+    const int64_t grid = std::min<int64_t>(p->grid_bulk, te - tb);
+    if (grid > 0) csr_tile_kernel<T, true, TILE, 1><<<unsigned(grid), kTileThreads, smem1, st>>>(P);
+  } else {
+    // bulk tiles on the multi-group kernel, the (rare) tail tiles past
+    // n_bulk on the single-group one
+    const int64_t bulk_end = std::min<int64_t>(te, P.n_bulk);
+    const int64_t grid = std::min<int64_t>(p->grid_bulk, bulk_end - tb);
+    if (grid > 0)
+      csr_tile_kernel<T, true, TILE, G>
+          <<<unsigned(grid), csr_cta_threads<G>(), CsrSmem<T, TILE, G>::total, st>>>(P);
+    if (te > bulk_end) {
+      CsrParams<T> Q = P;
+      Q.tile_begin = std::max<int64_t>(tb, bulk_end);
+      const int64_t g1 = std::min<int64_t>(p->grid_direct, te - Q.tile_begin);
+      csr_tile_kernel<T, true, TILE, 1><<<unsigned(g1), kTileThreads, smem1, st>>>(Q);
+    }
   }
+  SPMV_LAUNCH_CHECK();
   if (fixup && p->n_span > 0) {
     const int64_t g = std::min<int64_t>((p->n_span + 255) / 256, int64_t(sm_count()) * 8);
     csr_span_fixup_kernel<T><<<unsigned(g), 256, 0, st>>>(p->span_row.as<uint32_t>(), p->span_t0.as<uint32_t>(),
@@ -506,9 +575,11 @@ template <typename T>
 static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st, int64_t tb = 0, int64_t te = -1, bool fixup = true) {
   if (te < 0) te = p->ntiles;
-  if (p->tile == 1024) return csr_run_tiled<T, 1024>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
-  if (p->tile == 4096) return csr_run_tiled<T, 4096>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
-  return csr_run_tiled<T, 2048>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
+#define X(TL, GR) \
+  if (p->tile == TL && p->groups == GR) return csr_run_tiled<T, TL, GR>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
+  SPMV_CSR_CONFIGS(X)
+#undef X
+  return fail(SPMV_INVALID_ARG, "no CSR kernel for tile %lld x %d groups", (long long)p->tile, p->groups);
 }
 
 // Host x -> host y product with H2D / compute / D2H overlap (see
@@ -612,7 +683,24 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
   if ((rc = count_async(ctr, &h, st))) return rc;
   p->n_long = int64_t(h);
   // Long rows leave gathers to the warps: smaller tiles keep more CTAs per SM.
-  p->tile = tile_entries() ? tile_entries() : (p->n_long > 0 ? 1024 : 2048);
+  // Long rows: 1024-entry tiles, one group (more CTAs hide the long-row
+  // gathers).  Otherwise 2048-entry tiles with G consumer groups sharing a
+  // G + 1 stage ring: 3 groups (2 CTAs/SM) for stencil-like rows, 7 groups
+  // (1 CTA/SM) for short rows (average < 16 entries), measured best on the
+  // 27-point stencil and the 11-diagonal banded matrix respectively.
+  if (p->n_long > 0) {
+    p->tile = 1024;
+    p->groups = 1;
+  } else {
+    p->tile = 2048;
+    p->groups = p->nnz < 16 * p->nrows ? 7 : 3;
+  }
+  if (tile_entries()) {
+    p->tile = tile_entries();
+    p->groups = 1;
+  }
+  if (csr_groups() > 0) p->groups = csr_groups();
+  if (!csr_config_known(p->tile, p->groups)) p->groups = 1;
   p->ntiles = (p->nnz + p->tile - 1) / p->tile;
   const size_t vs = value_size(p->dtype);
   if ((rc = p->row_lo.alloc(4 * (p->ntiles + 1))) || (rc = p->head.alloc(vs * p->ntiles)) ||
@@ -641,11 +729,12 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
     }
   }
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
-  if (p->tile == 1024)
-    return p->dtype == SPMV_F64 ? csr_launch_config<double, 1024>(p) : csr_launch_config<float, 1024>(p);
-  if (p->tile == 4096)
-    return p->dtype == SPMV_F64 ? csr_launch_config<double, 4096>(p) : csr_launch_config<float, 4096>(p);
-  return p->dtype == SPMV_F64 ? csr_launch_config<double, 2048>(p) : csr_launch_config<float, 2048>(p);
+#define X(TL, GR)                                                                                    \
+  if (p->tile == TL && p->groups == GR)                                                             \
+    return p->dtype == SPMV_F64 ? csr_launch_config<double, TL, GR>(p) : csr_launch_config<float, TL, GR>(p);
+  SPMV_CSR_CONFIGS(X)
+#undef X
+  return fail(SPMV_INVALID_ARG, "no CSR kernel for tile %lld x %d groups", (long long)p->tile, p->groups);
 }
 
 extern "C" {
@@ -700,7 +789,15 @@ int spmv_csr_plan_info(const spmv_csr_plan* p, int64_t* n_long_rows, int64_t* n_
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (n_long_rows) *n_long_rows = p->n_long;
   if (n_items) *n_items = p->tile;
-  if (launches) *launches = (p->nrows > 0 ? 1 : 0) + (p->n_span > 0 ? 1 : 0);
+  if (launches)
+    *launches = (p->nrows > 0 ? 1 : 0) + (p->n_span > 0 ? 1 : 0) +
+                (p->groups > 1 && p->nnz > 0 && bulk_tiles(p->nnz, p->ntiles, p->tile) < p->ntiles ? 1 : 0);
+  return SPMV_OK;
+}
+
+int spmv_csr_plan_groups(const spmv_csr_plan* p, int* groups) {
+  if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
+  if (groups) *groups = p->groups;
   return SPMV_OK;
 }
 

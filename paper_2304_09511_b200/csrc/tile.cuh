@@ -24,10 +24,24 @@ constexpr int max_long_segs() { return TILE / (kExactLen + 1) + 4; }
 // SM (smaller shared-memory ring); 2048 halves the per-tile overhead.
 int tile_entries();
 int ctas_per_sm_cap();  // 0 = occupancy limit
+int csr_groups();       // SPMV_CSR_GROUPS: 0 = plan choice
 int tma_hint_mode();    // SPMV_TMA_HINT: -1 auto, 0 off, 1 on
 int tile_mode_flags();  // experiments: bit0 no products mode, bit1 warp-per-segment long rows
 
 static_assert(kExt == kExactLen, "extension must cover a whole short row");
+
+// A consumer group of NT threads inside a tile CTA.  The single-group
+// kernels use the whole CTA (barrier 0 == __syncthreads); the multi-group
+// CSR kernel runs G groups of 128 threads, each on its own named barrier, so
+// G tiles are computed at once while one more stage is loading.
+template <int NT>
+struct TileGroup {
+  int tid;  // thread index inside the group
+  int bar;  // named barrier id
+  __device__ __forceinline__ void sync() const {
+    asm volatile("bar.sync %0, %1;" ::"r"(bar), "n"(NT) : "memory");
+  }
+};
 
 struct LongSeg {
   uint32_t row;
@@ -88,20 +102,19 @@ __device__ __forceinline__ T row_sum(const T* __restrict__ p, int len, T acc) {
 // tid, tid+256, ... in place (4 gathers in flight).  Used for tiles holding
 // many short rows, where a row per lane would serialise ~1 L2 round trip
 // per row; entry-per-lane issues the whole tile's gathers in parallel.
-template <typename T>
+template <typename T, int NT = kTileThreads>
 __device__ __forceinline__ void form_products(const uint32_t* __restrict__ cols, T* __restrict__ vals, int cnt,
-                                              const T* __restrict__ xb) {
-  int k = threadIdx.x;
-  for (; k + 3 * kTileThreads < cnt; k += 4 * kTileThreads) {
-    const uint32_t c0 = cols[k], c1 = cols[k + kTileThreads], c2 = cols[k + 2 * kTileThreads],
-                   c3 = cols[k + 3 * kTileThreads];
+                                              const T* __restrict__ xb, int gtid) {
+  int k = gtid;
+  for (; k + 3 * NT < cnt; k += 4 * NT) {
+    const uint32_t c0 = cols[k], c1 = cols[k + NT], c2 = cols[k + 2 * NT], c3 = cols[k + 3 * NT];
     const T x0 = ldx(xb + c0), x1 = ldx(xb + c1), x2 = ldx(xb + c2), x3 = ldx(xb + c3);
     vals[k] = mul_rn(vals[k], x0);
-    vals[k + kTileThreads] = mul_rn(vals[k + kTileThreads], x1);
-    vals[k + 2 * kTileThreads] = mul_rn(vals[k + 2 * kTileThreads], x2);
-    vals[k + 3 * kTileThreads] = mul_rn(vals[k + 3 * kTileThreads], x3);
+    vals[k + NT] = mul_rn(vals[k + NT], x1);
+    vals[k + 2 * NT] = mul_rn(vals[k + 2 * NT], x2);
+    vals[k + 3 * NT] = mul_rn(vals[k + 3 * NT], x3);
   }
-  for (; k < cnt; k += kTileThreads) vals[k] = mul_rn(vals[k], ldx(xb + cols[k]));
+  for (; k < cnt; k += NT) vals[k] = mul_rn(vals[k], ldx(xb + cols[k]));
 }
 
 // Long segments of one tile, reduced by all warps of the CTA: every segment
@@ -118,22 +131,22 @@ struct LongUnit {  // scratch slot; reduce_long_segments stores unit offsets her
   uint32_t a, b;
 };
 
-// seg_part[i] <- reduction of segment i (i < nl).  Ends with __syncthreads().
-template <typename T, int TILE>
+// seg_part[i] <- reduction of segment i (i < nl).  Ends with a group barrier.
+template <typename T, int TILE, int NT = kTileThreads>
 __device__ __forceinline__ void reduce_long_segments(const uint32_t* __restrict__ cols, const T* __restrict__ vals,
                                      const LongSeg* __restrict__ segs, int nl, LongUnit* units, T* unit_part,
                                      int* s_nunits, T* seg_part, const T* __restrict__ xb, bool products,
-                                     bool warp_per_seg = false) {
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+                                     bool warp_per_seg, const TileGroup<NT>& grp) {
+  const int tid = grp.tid, lane = tid & 31, warp = tid >> 5;
   if (warp_per_seg) {
-    for (int i = warp; i < nl; i += kTileThreads / 32) {
+    for (int i = warp; i < nl; i += NT / 32) {
       T acc = T(0);
       for (uint32_t j = segs[i].lo + lane; j < segs[i].hi; j += 32)
         acc = add_rn(acc, products ? vals[j] : mul_rn(vals[j], ldx(xb + cols[j])));
       acc = tree_reduce_warp(acc, 32);
       if (lane == 0) seg_part[i] = acc;
     }
-    __syncthreads();
+    grp.sync();
     return;
   }
   // unit offsets of the segments: warp 0 scans ceil(len / kUnit), up to
@@ -164,9 +177,9 @@ __device__ __forceinline__ void reduce_long_segments(const uint32_t* __restrict_
       *s_nunits = incl;
     }
   }
-  __syncthreads();
+  grp.sync();
   const int nu = *s_nunits;
-  for (int u = warp; u < nu; u += kTileThreads / 32) {
+  for (int u = warp; u < nu; u += NT / 32) {
     int lo_i = 0, hi_i = nl - 1;  // segment of unit u: last i with first[i] <= u
     while (lo_i < hi_i) {
       const int mid = (lo_i + hi_i + 1) >> 1;
@@ -191,13 +204,13 @@ __device__ __forceinline__ void reduce_long_segments(const uint32_t* __restrict_
     acc = tree_reduce_warp(acc, 32);
     if (lane == 0) unit_part[u] = acc;
   }
-  __syncthreads();
-  for (int i = tid; i < nl; i += kTileThreads) {
+  grp.sync();
+  for (int i = tid; i < nl; i += NT) {
     T s = unit_part[first[i]];
     for (int u = first[i] + 1; u < first[i + 1]; ++u) s = add_rn(s, unit_part[u]);
     seg_part[i] = s;
   }
-  __syncthreads();
+  grp.sync();
 }
 
 // Warp-level vla-32 dot product of staged entries [lo, hi): lane l sums

@@ -115,8 +115,10 @@ class _Plan:
     def info(self) -> dict:
         if self.kind == "csr":
             a, b, c = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64()
+            g = ctypes.c_int()
             _lib.call("spmv_csr_plan_info", self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
-            return {"long_rows": a.value, "tile": b.value, "launches": c.value}
+            _lib.call("spmv_csr_plan_groups", self.handle, ctypes.byref(g))
+            return {"long_rows": a.value, "tile": b.value, "launches": c.value, "groups": g.value}
         a, b, c, d, e = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_int64()
         _lib.call("spmv_coo_plan_info", self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                   ctypes.byref(d), ctypes.byref(e))
