@@ -175,8 +175,8 @@ int dia_rows_per_tile() {
   static const int r = env_int("SPMV_DIA_ROWS", 0);
   return r;
 }
-int dia_stages() {
-  static const int s = env_int("SPMV_DIA_STAGES", 0);
-  return s;
+int dia_config() {  // SPMV_DIA_CFG: -1 auto; 0..4 see dia.cu
+  static const int c = env_int("SPMV_DIA_CFG", -1);
+  return c;
 }
 }  // namespace spmv

@@ -21,7 +21,12 @@
 namespace spmv {
 
 int dia_rows_per_tile();
-int dia_stages();
+int dia_config();
+
+template <int G_, int S_, int NT_>
+struct DiaCfg {
+  static constexpr int G = G_, S = S_, NT = NT_;
+};
 
 constexpr int kDiaThreads = 256;
 constexpr int kMaxSmemOffsets = 2048;
@@ -56,24 +61,33 @@ __device__ __forceinline__ T dia_row(const T* __restrict__ v, const int32_t* __r
 }
 
 // Persistent TMA-pipelined kernel.  Tile t covers local rows
-// [t*R, t*R + R) (the last tile is clipped to avail_rows).
-template <typename T, int STAGES, int ND>
-__global__ void __launch_bounds__(kDiaThreads)
+// [t*R, t*R + R) (the last tile is clipped to avail_rows).  G consumer
+// groups of NT threads share an S-stage ring: tile i of the CTA goes to
+// group i % G and stage i % S, so G tiles compute while S - G load (more
+// rows in flight per byte of shared memory than one group with a
+// double buffer).
+template <typename T, int G, int S, int NT, int ND>
+__global__ void __launch_bounds__(G * NT)
 dia_bulk_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offsets, int nd, const T* __restrict__ x,
                 T* __restrict__ y, int64_t nrows, int64_t avail_rows, int64_t ncols, int64_t row_base,
                 int64_t col_base, int rows_per_tile, int64_t ntiles, uint32_t stage_bytes) {
+  static_assert(S > G && S <= 8, "stages");
   extern __shared__ __align__(128) unsigned char smem[];
-  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                 // [0, 64)
+  volatile int* tickets = reinterpret_cast<volatile int*>(smem + 64);  // [64, 96): CTA-local tile of each stage
   int32_t* s_off = reinterpret_cast<int32_t*>(smem + 128);
   const size_t off_bytes = (size_t(nd) * 4 + 127) & ~size_t(127);
   unsigned char* bufs = smem + 128 + off_bytes;
-  const int tid = threadIdx.x;
+  const int g = int(threadIdx.x) / NT, tid = int(threadIdx.x) % NT;
   const T* xb = x - col_base;
 
-  for (int d = tid; d < nd; d += blockDim.x) s_off[d] = offsets[d];
-  if (tid == 0) {
-    for (int s = 0; s < STAGES; ++s) mbar_init(&bars[s], 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  for (int d = threadIdx.x; d < nd; d += blockDim.x) s_off[d] = offsets[d];
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&bars[s], 1);
+      tickets[s] = -1;
+    }
+    mbar_fence_init();
   }
   __syncthreads();
 
@@ -88,29 +102,40 @@ dia_bulk_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offsets,
     int64_t rows = avail_rows - lr0;
     if (rows > rows_per_tile) rows = rows_per_tile;
     const uint32_t bytes = uint32_t(rows * row_bytes);
-    const int s = int(i % STAGES);
+    const int s = int(i % S);
+    if (G > 1) tickets[s] = int(i);
     mbar_arrive_expect_tx(&bars[s], bytes);
     bulk_g2s(bufs + size_t(s) * stage_bytes, reinterpret_cast<const unsigned char*>(vals) + lr0 * row_bytes, bytes,
              &bars[s]);
   };
+  auto group_sync = [&]() {
+    if (G == 1)
+      __syncthreads();
+    else
+      asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(NT) : "memory");
+  };
 
-  if (tid == 0)
-    for (int64_t i = 0; i < STAGES && i < my_tiles; ++i) issue(i);
+  if (threadIdx.x == 0)
+    for (int64_t i = 0; i < S && i < my_tiles; ++i) issue(i);
 
-  for (int64_t i = 0; i < my_tiles; ++i) {
-    const int s = int(i % STAGES);
-    mbar_wait(&bars[s], uint32_t((i / STAGES) & 1));
+  for (int64_t i = g; i < my_tiles; i += G) {
+    const int s = int(i % S);
+    // parity waits only tell the current phase from the previous one: with
+    // G > 1 wait until tile i is the one issued into the stage
+    if (G > 1)
+      while (tickets[s] != int(i)) __nanosleep(32);
+    mbar_wait(&bars[s], uint32_t((i / S) & 1));
     const int64_t t = first + i * stride;
     const int64_t lr0 = t * rows_per_tile;
     const T* tile = reinterpret_cast<const T*>(bufs + size_t(s) * stage_bytes);
     int64_t rows = nrows - lr0;
     if (rows > rows_per_tile) rows = rows_per_tile;
-    for (int lr = tid; lr < rows; lr += blockDim.x)
+    for (int lr = tid; lr < rows; lr += NT)
       y[lr0 + lr] = dia_row<T, ND>(tile + size_t(lr) * nd, s_off, nd, row_base + lr0 + lr, ncols, xb);
-    __syncthreads();  // every thread is done with stage s
-    if (tid == 0 && i + STAGES < my_tiles) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(i + STAGES);
+    group_sync();  // every thread of the group is done with stage s
+    if (tid == 0 && i + S < my_tiles) {
+      fence_proxy_async();
+      issue(i + S);
     }
   }
 }
@@ -143,9 +168,22 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
   // Tile size: one row per thread (R = 256) when a stage fits ~56 KB, else
   // fewer rows (a multiple of 8).  Measured: 256-row tiles beat 512-row
   // tiles by 43% on 11 diagonals (more CTAs per SM, one row per thread).
-  int64_t R = int64_t(57344 / (row_bytes ? row_bytes : 1)) / 8 * 8;
-  if (R > kDiaThreads) R = kDiaThreads;
-  if (dia_rows_per_tile() >= 8) R = dia_rows_per_tile() / 8 * 8;
+  // Kernel configuration (groups G, stages S, threads per group NT; one row
+  // per thread): SPMV_DIA_CFG, else 3 groups over 4 stages — 256-row
+  // stages when a stage holds more than 40 KB (e.g. 27 diagonals: one CTA
+  // per SM, 768 rows computing), else 128-row stages (several CTAs per SM).
+  // Measured on B200: 27-pt stencil 1287 -> 1610 GFLOP/s, 11-diagonal
+  // banded 1225 -> 1398 against one group with a double buffer.
+  static constexpr int kCfgStages[5] = {2, 3, 4, 4, 8};
+  static constexpr int kCfgThreads[5] = {256, 256, 128, 256, 128};
+  int cfg = dia_config();
+  if (cfg < 0 || cfg > 4) cfg = row_bytes * 256 > 40960 ? 3 : 2;
+  const int nt = kCfgThreads[cfg], nstage = kCfgStages[cfg];
+  // rows per stage: NT, or fewer (a multiple of 8) so that S stages fit
+  const size_t budget = (size_t(227) * 1024 - 1024 - 128 - ((size_t(nd) * 4 + 127) & ~size_t(127))) / nstage;
+  int64_t R = int64_t(budget / (row_bytes ? row_bytes : 1)) / 8 * 8;
+  if (R > nt) R = nt;
+  if (dia_rows_per_tile() >= 8 && dia_rows_per_tile() / 8 * 8 <= R) R = dia_rows_per_tile() / 8 * 8;
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) % 16 == 0) && ((R * row_bytes) % 16 == 0) &&
                        ((avail_rows * row_bytes) % 16 == 0);
   const bool use_bulk = nd > 0 && nd <= kMaxSmemOffsets && R >= 8 && aligned;
@@ -159,40 +197,38 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
   }
   const int64_t ntiles = (nrows + R - 1) / R;
   const uint32_t stage_bytes = uint32_t(((R * row_bytes) + 127) & ~size_t(127));
-  int stages = stage_bytes > 40960 ? 2 : 3;
-  if (dia_stages() == 2 || dia_stages() == 3) stages = dia_stages();
   const size_t off_bytes = (size_t(nd) * 4 + 127) & ~size_t(127);
-  const size_t smem = 128 + off_bytes + size_t(stages) * stage_bytes;
-  int ctas_per_sm = int((227 * 1024) / (smem + 1024));
-  if (ctas_per_sm < 1) ctas_per_sm = 1;
-  if (ctas_per_sm > 4) ctas_per_sm = 4;
-  int64_t grid = int64_t(sms) * ctas_per_sm;
-  if (grid > ntiles) grid = ntiles;
-  auto launch = [&](auto kernel) -> int {
+  auto launch = [&](auto kernel, int threads, int stages) -> int {
+    const size_t smem = 128 + off_bytes + size_t(stages) * stage_bytes;
     SPMV_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
-    kernel<<<unsigned(grid), kDiaThreads, smem, st>>>(vals, offsets, int(nd), x, y, nrows, avail_rows, ncols,
-                                                       row_base, col_base, int(R), ntiles, stage_bytes);
+    int per_sm = 0;
+    SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    if (per_sm < 1) return fail(SPMV_UNSUPPORTED, "DIA tile of %u bytes x %d stages does not fit", stage_bytes, stages);
+    int64_t grid = int64_t(sms) * per_sm;
+    if (grid > ntiles) grid = ntiles;
+    kernel<<<unsigned(grid), threads, smem, st>>>(vals, offsets, int(nd), x, y, nrows, avail_rows, ncols, row_base,
+                                                 col_base, int(R), ntiles, stage_bytes);
     return SPMV_OK;
   };
+  auto by_nd = [&](auto cfg) -> int {
+    using C = decltype(cfg);
+    constexpr int G = C::G, S = C::S, NT = C::NT;
+    switch (nd) {
+      case 27: return launch(dia_bulk_kernel<T, G, S, NT, 27>, G * NT, S);
+      case 11: return launch(dia_bulk_kernel<T, G, S, NT, 11>, G * NT, S);
+      case 7: return launch(dia_bulk_kernel<T, G, S, NT, 7>, G * NT, S);
+      case 5: return launch(dia_bulk_kernel<T, G, S, NT, 5>, G * NT, S);
+      case 3: return launch(dia_bulk_kernel<T, G, S, NT, 3>, G * NT, S);
+      default: return launch(dia_bulk_kernel<T, G, S, NT, 0>, G * NT, S);
+    }
+  };
   int rc;
-  if (stages == 2) {
-    switch (nd) {
-      case 27: rc = launch(dia_bulk_kernel<T, 2, 27>); break;
-      case 11: rc = launch(dia_bulk_kernel<T, 2, 11>); break;
-      case 7: rc = launch(dia_bulk_kernel<T, 2, 7>); break;
-      case 5: rc = launch(dia_bulk_kernel<T, 2, 5>); break;
-      case 3: rc = launch(dia_bulk_kernel<T, 2, 3>); break;
-      default: rc = launch(dia_bulk_kernel<T, 2, 0>); break;
-    }
-  } else {
-    switch (nd) {
-      case 27: rc = launch(dia_bulk_kernel<T, 3, 27>); break;
-      case 11: rc = launch(dia_bulk_kernel<T, 3, 11>); break;
-      case 7: rc = launch(dia_bulk_kernel<T, 3, 7>); break;
-      case 5: rc = launch(dia_bulk_kernel<T, 3, 5>); break;
-      case 3: rc = launch(dia_bulk_kernel<T, 3, 3>); break;
-      default: rc = launch(dia_bulk_kernel<T, 3, 0>); break;
-    }
+  switch (cfg) {
+    case 1: rc = by_nd(DiaCfg<1, 3, 256>{}); break;
+    case 2: rc = by_nd(DiaCfg<3, 4, 128>{}); break;
+    case 3: rc = by_nd(DiaCfg<3, 4, 256>{}); break;
+    case 4: rc = by_nd(DiaCfg<7, 8, 128>{}); break;
+    default: rc = by_nd(DiaCfg<1, 2, 256>{}); break;
   }
   if (rc) return rc;
   SPMV_LAUNCH_CHECK();
