@@ -224,7 +224,8 @@ def plan_of(sp, m) -> dict:
         i = K.csr_plan(m).info()
         return {"tile": i["tile"], "groups": i["groups"]}
     if m.format == sp.Format.COO:
-        return {"tile": K.coo_plan(m).info()["tile"]}
+        i = K.coo_plan(m).info()
+        return {"tile": i["tile"], "groups": i["groups"]}
     return {}
 
 

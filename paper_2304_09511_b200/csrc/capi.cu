@@ -146,7 +146,7 @@ static int env_int(const char* name, int dflt) {
 int tile_entries() {
   static const int t = [] {
     const int v = env_int("SPMV_TILE", 0);
-    return (v == 1024 || v == 1920 || v == 2048 || v == 4096) ? v : 0;
+    return (v == 1024 || v == 1536 || v == 1920 || v == 2048 || v == 4096) ? v : 0;
   }();
   return t;
 }
@@ -165,6 +165,11 @@ int tma_hint_mode() {
 // CSR consumer groups per tile CTA (0 = plan's choice).
 int csr_groups() {
   static const int g = env_int("SPMV_CSR_GROUPS", 0);
+  return g;
+}
+// COO consumer groups per tile CTA (0 = plan's choice).
+int coo_groups() {
+  static const int g = env_int("SPMV_COO_GROUPS", 0);
   return g;
 }
 int ctas_per_sm_cap() {

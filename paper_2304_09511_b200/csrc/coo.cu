@@ -44,36 +44,50 @@ struct CooParams {
   T* head_val;
   T* tail_val;
   int64_t nrows, nnz, col_base, ntiles, n_bulk;
+  int64_t tile_begin;  // first tile of the launch's tail range (tail-only launches)
   int mode;
 };
 
-template <typename T, int TILE>
+// Shared memory of a COO tile CTA with G consumer groups over G + 1 stages
+// (see csr.cu): [0, 64) stage mbarriers, [64, 96) stage tickets, [96, 224)
+// four counters per group, then one scan/long-row block per group, then the
+// stage ring.
+template <typename T, int TILE, int G = 1>
 struct CooSmem {
-  static constexpr int rounds = TILE / kTileThreads;
+  static constexpr int stages = G + 1;
   static constexpr size_t rows_bytes = align_up(sizeof(uint32_t) * (TILE + 2 * kExt), 128);
   static constexpr size_t cols_bytes = align_up(sizeof(uint32_t) * (TILE + kExt), 128);
   static constexpr size_t vals_bytes = align_up(sizeof(T) * (TILE + kExt), 128);
   static constexpr size_t stage_bytes = rows_bytes + cols_bytes + vals_bytes;
+  // group block: starts | long segments | scan counts | long-row scratch
   static constexpr size_t starts_bytes = align_up(sizeof(uint16_t) * (TILE + 1), 128);
   static constexpr size_t long_bytes = align_up(sizeof(LongSeg) * max_long_segs<TILE>(), 128);
   static constexpr size_t counts_bytes = align_up(sizeof(int) * 2 * 64, 128);
   static constexpr size_t units_bytes = align_up(sizeof(LongUnit) * max_units<TILE>(), 128);
   static constexpr size_t upart_bytes = align_up(sizeof(T) * max_units<TILE>(), 128);
   static constexpr size_t spart_bytes = align_up(sizeof(T) * max_long_segs<TILE>(), 128);
-  static constexpr size_t header = 128 + starts_bytes + long_bytes + counts_bytes + units_bytes + upart_bytes +
-                                   spart_bytes;
-  static constexpr size_t total = header + kTileStages * stage_bytes;
-  static_assert(rounds * (kTileThreads / 32) <= 64, "segment scan covers at most 64 warp counts");
+  static constexpr size_t group_bytes =
+      starts_bytes + long_bytes + counts_bytes + units_bytes + upart_bytes + spart_bytes;
+  static constexpr size_t tickets_off = 64, counters_off = 96, groups_off = 256;
+  static constexpr size_t header = groups_off + G * group_bytes;
+  static constexpr size_t total = header + stages * stage_bytes;
+  static_assert(TILE / 32 <= 64, "segment scan covers at most 64 warp counts");
+  static_assert(stages <= 8, "mbarrier / ticket / counter slots");
 };
 
+template <int G> constexpr int coo_group_threads() { return G == 1 ? kTileThreads : 128; }
+template <int G> constexpr int coo_min_blocks() { return G == 1 ? 3 : 1; }
+
 // rows: tile-relative view, valid for k in [-kExt, TILE + kExt).
-template <typename T, int TILE>
+template <typename T, int TILE, int NT>
 __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_t* __restrict__ rows,
                                  const uint32_t* __restrict__ cols, T* __restrict__ vals, uint16_t* s_start,
-                                 LongSeg* s_long, int* s_nseg, int* s_nlong, int* s_wcnt) {
-  constexpr int R = TILE / kTileThreads;
-  constexpr int W = kTileThreads / 32;
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+                                 LongSeg* s_long, int* s_nseg, int* s_nlong, int* s_wcnt,
+                                 const TileGroup<NT>& grp) {
+  constexpr int R = TILE / NT;
+  constexpr int W = NT / 32;
+  static_assert(TILE % NT == 0, "rounds");
+  const int tid = grp.tid, lane = tid & 31, warp = tid >> 5;
   const int64_t E0 = t * TILE;
   const int cnt_in = int(min(int64_t(TILE), P.nnz - E0));
   const int cnt_ext = int(min(int64_t(TILE + kExt), P.nnz - E0));
@@ -85,12 +99,12 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
   unsigned bal[R];
 #pragma unroll
   for (int i = 0; i < R; ++i) {
-    const int k = i * kTileThreads + tid;
+    const int k = i * NT + tid;
     const bool h = k < cnt_in && (k == 0 || rows[k] != rows[k - 1]);
     bal[i] = __ballot_sync(0xffffffffu, h);
     if (lane == 0) s_wcnt[i * W + warp] = __popc(bal[i]);
   }
-  __syncthreads();
+  grp.sync();
   if (warp == 0) {
     const int v0 = (2 * lane < R * W) ? s_wcnt[2 * lane] : 0;
     const int v1 = (2 * lane + 1 < R * W) ? s_wcnt[2 * lane + 1] : 0;
@@ -111,27 +125,27 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
       P.pass[t] = 0;
     }
   }
-  __syncthreads();
+  grp.sync();
   {
     const unsigned lt = (1u << lane) - 1u;
 #pragma unroll
     for (int i = 0; i < R; ++i)
       if ((bal[i] >> lane) & 1u)
-        s_start[s_wcnt[64 + i * W + warp] + __popc(bal[i] & lt)] = uint16_t(i * kTileThreads + tid);
+        s_start[s_wcnt[64 + i * W + warp] + __popc(bal[i] & lt)] = uint16_t(i * NT + tid);
   }
-  __syncthreads();
+  grp.sync();
   const int nseg = *s_nseg;
   // Many short rows (more segments than threads): issue the whole tile's
   // gathers entry-per-lane first (see tile.cuh form_products).
-  const bool products = (P.mode & 1) && nseg > kTileThreads;
+  const bool products = (P.mode & 1) && nseg > NT;
   if (products) {
-    form_products(cols, vals, cnt_ext, xb, int(threadIdx.x));
-    __syncthreads();
+    form_products<T, NT>(cols, vals, cnt_ext, xb, tid);
+    grp.sync();
   }
 
   // 3. one thread per segment: short owned rows summed left to right from
   //    +0.0 (np.add.at order); long ones queued; empty rows zero-filled.
-  for (int s = tid; s < nseg; s += kTileThreads) {
+  for (int s = tid; s < nseg; s += NT) {
     const int k0 = s_start[s], k1 = s_start[s + 1];
     const uint32_t r = rows[k0];
     const bool cont_before = (k0 == 0) && rows[-1] == r;
@@ -163,27 +177,25 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
                         : row_dot(cols + k0, vals + k0, k1 + after - k0, xb, T(0));
     }
   }
-  __syncthreads();
-
-  __syncthreads();
+  grp.sync();
 }
 
 // 4. long segments (out of line): units over all warps (vla-32 order inside
 //    a unit); cross-tile parts go to the carry slots for coo_fixup_kernel.
-template <typename T, int TILE>
+template <typename T, int TILE, int NT>
 __device__ __forceinline__ void coo_tile_long(int64_t t, const uint32_t* __restrict__ cols, const T* __restrict__ vals,
                                            const LongSeg* __restrict__ s_long, int nl, unsigned char* scratch,
                                            int* s_nunits, const T* __restrict__ xb, T* __restrict__ y,
                                            uint32_t* head_row, T* head_val, uint32_t* pass, uint32_t* tail_row,
-                                           T* tail_val, bool warp_per_seg) {
+                                           T* tail_val, bool warp_per_seg, const TileGroup<NT>& grp) {
   using S = CooSmem<T, TILE>;
   LongUnit* units = reinterpret_cast<LongUnit*>(scratch);
   T* unit_part = reinterpret_cast<T*>(scratch + S::units_bytes);
   T* seg_part = reinterpret_cast<T*>(scratch + S::units_bytes + S::upart_bytes);
   const bool products = s_long[0].flags & 4u;
-  reduce_long_segments<T, TILE>(cols, vals, s_long, nl, units, unit_part, s_nunits, seg_part, xb, products,
-                                warp_per_seg, TileGroup<kTileThreads>{int(threadIdx.x), 0});
-  for (int i = threadIdx.x; i < nl; i += kTileThreads) {
+  reduce_long_segments<T, TILE, NT>(cols, vals, s_long, nl, units, unit_part, s_nunits, seg_part, xb, products,
+                                    warp_per_seg, grp);
+  for (int i = grp.tid; i < nl; i += NT) {
     const LongSeg L = s_long[i];
     const T part = seg_part[i];
     const bool cb = L.flags & 1u, ca = L.flags & 2u;
@@ -200,20 +212,30 @@ __device__ __forceinline__ void coo_tile_long(int64_t t, const uint32_t* __restr
   }
 }
 
-template <typename T, bool BULK, int TILE>
-__global__ void __launch_bounds__(kTileThreads, 3)
+// G == 1: one 256-thread group over a double buffer.  G > 1: G groups of
+// 128 threads over G + 1 stages (tile i of the CTA -> group i % G, stage
+// i % (G + 1)), bulk tiles only; the host runs tail tiles with G == 1.
+template <typename T, bool BULK, int TILE, int G>
+__global__ void __launch_bounds__(G * coo_group_threads<G>(), coo_min_blocks<G>())
 coo_tile_kernel(const __grid_constant__ CooParams<T> P) {
+  static_assert(G == 1 || BULK, "multi-group CTAs are TMA-fed");
+  constexpr int NT = coo_group_threads<G>();
   extern __shared__ __align__(128) unsigned char smem[];
-  using S = CooSmem<T, TILE>;
+  using S = CooSmem<T, TILE, G>;
+  constexpr int STAGES = S::stages;
+  const int g = int(threadIdx.x) / NT;
+  const TileGroup<NT> grp{int(threadIdx.x) % NT, G == 1 ? 0 : 1 + g};
+  const int tid = grp.tid;
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);
-  int* s_nseg = reinterpret_cast<int*>(smem + 32);
-  int* s_nlong = reinterpret_cast<int*>(smem + 36);
-  uint16_t* s_start = reinterpret_cast<uint16_t*>(smem + 128);
-  LongSeg* s_long = reinterpret_cast<LongSeg*>(smem + 128 + S::starts_bytes);
-  int* s_wcnt = reinterpret_cast<int*>(smem + 128 + S::starts_bytes + S::long_bytes);
+  volatile int* tickets = reinterpret_cast<volatile int*>(smem + S::tickets_off);
+  int* s_nseg = reinterpret_cast<int*>(smem + S::counters_off) + 4 * g;
+  int* s_nlong = s_nseg + 1;  // s_nlong[1]: long-row unit count
+  unsigned char* gblock = smem + S::groups_off + size_t(g) * S::group_bytes;
+  uint16_t* s_start = reinterpret_cast<uint16_t*>(gblock);
+  LongSeg* s_long = reinterpret_cast<LongSeg*>(gblock + S::starts_bytes);
+  int* s_wcnt = reinterpret_cast<int*>(gblock + S::starts_bytes + S::long_bytes);
   unsigned char* scratch = reinterpret_cast<unsigned char*>(s_wcnt) + S::counts_bytes;
   unsigned char* stages = smem + S::header;
-  const int tid = threadIdx.x;
   auto rows_of = [&](int s) { return reinterpret_cast<uint32_t*>(stages + s * S::stage_bytes); };
   auto cols_of = [&](int s) { return reinterpret_cast<uint32_t*>(stages + s * S::stage_bytes + S::rows_bytes); };
   auto vals_of = [&](int s) {
@@ -223,45 +245,53 @@ coo_tile_kernel(const __grid_constant__ CooParams<T> P) {
   const int64_t n_bulk = BULK ? P.n_bulk : 0;
   const int64_t first = blockIdx.x, stride = gridDim.x;
   const int64_t mine_bulk = first < n_bulk ? (n_bulk - 1 - first) / stride + 1 : 0;
-  const int64_t tail0 = n_bulk + first;
-  const int64_t mine_tail = tail0 < P.ntiles ? (P.ntiles - 1 - tail0) / stride + 1 : 0;
+  const int64_t tail0 = max(n_bulk, P.tile_begin) + first;
+  const int64_t mine_tail = G == 1 && tail0 < P.ntiles ? (P.ntiles - 1 - tail0) / stride + 1 : 0;
   auto issue = [&](int64_t i) {
     const int64_t t = first + i * stride;
     const int64_t E0 = t * TILE;
     const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
     const uint32_t pre = t > 0 ? uint32_t(kExt) : 0u;
-    const int s = int(i % kTileStages);
+    const int s = int(i % STAGES);
+    if (G > 1) tickets[s] = int(i);
     mbar_arrive_expect_tx(&bars[s], (cnt + pre) * 4u + cnt * (4u + uint32_t(sizeof(T))));
     bulk_g2s(rows_of(s) + (kExt - pre), P.ai + E0 - pre, (cnt + pre) * 4u, &bars[s], (P.mode & 4) != 0);
     bulk_g2s(cols_of(s), P.aj + E0, cnt * 4u, &bars[s], (P.mode & 4) != 0);
     bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s], (P.mode & 4) != 0);
   };
   if (BULK) {
-    if (tid == 0) {
-      for (int s = 0; s < kTileStages; ++s) mbar_init(&bars[s], 1);
+    if (threadIdx.x == 0) {
+      for (int s = 0; s < STAGES; ++s) {
+        mbar_init(&bars[s], 1);
+        tickets[s] = -1;
+      }
       mbar_fence_init();
     }
     __syncthreads();
-    if (tid == 0)
-      for (int64_t i = 0; i < kTileStages && i < mine_bulk; ++i) issue(i);
+    if (threadIdx.x == 0)
+      for (int64_t i = 0; i < STAGES && i < mine_bulk; ++i) issue(i);
   }
-  for (int64_t i = 0; i < mine_bulk + mine_tail; ++i) {
+  for (int64_t i = g; i < mine_bulk + mine_tail; i += G) {
     int s = 0;
     int64_t t;
     if (i < mine_bulk) {
-      s = int(i % kTileStages);
+      s = int(i % STAGES);
       t = first + i * stride;
-      mbar_wait(&bars[s], uint32_t((i / kTileStages) & 1));
+      // parity waits only tell the current phase from the previous one: with
+      // G > 1 wait until tile i is the one issued into the stage (csr.cu)
+      if (G > 1)
+        while (tickets[s] != int(i)) __nanosleep(32);
+      mbar_wait(&bars[s], uint32_t((i / STAGES) & 1));
     } else {
       t = tail0 + (i - mine_bulk) * stride;
       const int64_t E0 = t * TILE;
       const int cnt = int(min(int64_t(TILE + kExt), P.nnz - E0));
-      for (int k = tid - kExt; k < cnt; k += kTileThreads) {
-        const int64_t g = E0 + k;
-        if (g >= 0) rows_of(0)[kExt + k] = P.ai[g];
+      for (int k = tid - kExt; k < cnt; k += NT) {
+        const int64_t gk = E0 + k;
+        if (gk >= 0) rows_of(0)[kExt + k] = P.ai[gk];
         if (k >= 0) {
-          cols_of(0)[k] = P.aj[g];
-          vals_of(0)[k] = P.av[g];
+          cols_of(0)[k] = P.aj[gk];
+          vals_of(0)[k] = P.av[gk];
         }
       }
     }
@@ -271,20 +301,20 @@ coo_tile_kernel(const __grid_constant__ CooParams<T> P) {
       const int cnt_ext = int(min(int64_t(TILE + kExt), P.nnz - E0));
       uint32_t* rb = rows_of(s);
       if (t == 0)
-        for (int k = tid; k < kExt; k += kTileThreads) rb[k] = kNoRow;
-      for (int k = cnt_ext + tid; k < TILE + kExt; k += kTileThreads) rb[kExt + k] = kNoRow;
+        for (int k = tid; k < kExt; k += NT) rb[k] = kNoRow;
+      for (int k = cnt_ext + tid; k < TILE + kExt; k += NT) rb[kExt + k] = kNoRow;
     }
-    __syncthreads();
-    coo_process_tile<T, TILE>(P, t, rows_of(s) + kExt, cols_of(s), vals_of(s), s_start, s_long, s_nseg, s_nlong,
-                              s_wcnt);
+    grp.sync();
+    coo_process_tile<T, TILE, NT>(P, t, rows_of(s) + kExt, cols_of(s), vals_of(s), s_start, s_long, s_nseg,
+                                  s_nlong, s_wcnt, grp);
     const int nl = *s_nlong;
     if (nl > 0)
-      coo_tile_long<T, TILE>(t, cols_of(s), vals_of(s), s_long, nl, scratch, s_nlong + 1, P.x - P.col_base, P.y,
-                             P.head_row, P.head_val, P.pass, P.tail_row, P.tail_val, (P.mode & 2) != 0);
-    __syncthreads();  // stage s free
-    if (BULK && tid == 0 && i + kTileStages < mine_bulk) {
+      coo_tile_long<T, TILE, NT>(t, cols_of(s), vals_of(s), s_long, nl, scratch, s_nlong + 1, P.x - P.col_base, P.y,
+                                 P.head_row, P.head_val, P.pass, P.tail_row, P.tail_val, (P.mode & 2) != 0, grp);
+    grp.sync();  // stage s free
+    if (BULK && tid == 0 && i + STAGES < mine_bulk) {
       fence_proxy_async();
-      issue(i + kTileStages);
+      issue(i + STAGES);
     }
   }
 }
@@ -442,8 +472,18 @@ struct spmv_coo_plan {
   int64_t n_runs = 0, n_long = 0, ntiles = 0, tile = 2048;
   DevBuf head_row, tail_row, pass, head_val, tail_val;
   DevBuf steps;
-  int grid = 0;
+  int groups = 1;                // consumer groups per tile CTA (coo_tile_kernel G)
+  int grid = 0, grid_direct = 0;  // G-group TMA kernel / single-group kernel
 };
+
+// (tile, groups) pairs with compiled kernels.
+#define SPMV_COO_CONFIGS(X) X(1024, 1) X(2048, 1) X(1536, 1) X(2048, 4) X(1536, 6)
+static bool coo_config_known(int64_t tile, int groups) {
+#define X(TL, GR) if (tile == TL && groups == GR) return true;
+  SPMV_COO_CONFIGS(X)
+#undef X
+  return false;
+}
 
 __global__ void count_long_runs_kernel(const uint32_t* __restrict__ run_start, int64_t n_runs,
                                        unsigned long long* __restrict__ n_long) {
@@ -454,20 +494,27 @@ __global__ void count_long_runs_kernel(const uint32_t* __restrict__ run_start, i
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(n_long, c);
 }
 
-template <typename T, int TILE>
+template <typename K>
+static int coo_ctas_per_sm(K kernel, int threads, size_t smem, int* per_sm) {
+  SPMV_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+  SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kernel, threads, smem));
+  if (ctas_per_sm_cap() > 0 && *per_sm > ctas_per_sm_cap()) *per_sm = ctas_per_sm_cap();
+  if (*per_sm < 1) *per_sm = 1;
+  return SPMV_OK;
+}
+
+template <typename T, int TILE, int G>
 static int coo_launch_config(spmv_coo_plan* p) {
-  using S = CooSmem<T, TILE>;
-  SPMV_CUDA_TRY(cudaFuncSetAttribute(coo_tile_kernel<T, true, TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(S::total)));
-  SPMV_CUDA_TRY(cudaFuncSetAttribute(coo_tile_kernel<T, false, TILE>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                     int(S::total)));
-  int per_sm = 0;
-  SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coo_tile_kernel<T, true, TILE>,
-                                                              kTileThreads, S::total));
-  if (ctas_per_sm_cap() > 0 && per_sm > ctas_per_sm_cap()) per_sm = ctas_per_sm_cap();
-  if (per_sm < 1) per_sm = 1;
-  const int64_t cap = int64_t(sm_count()) * per_sm;
+  using S1 = CooSmem<T, TILE, 1>;
+  int per_sm = 0, per_sm1 = 0, rc;
+  if ((rc = coo_ctas_per_sm(coo_tile_kernel<T, true, TILE, G>, G * coo_group_threads<G>(),
+                            CooSmem<T, TILE, G>::total, &per_sm)))
+    return rc;
+  if ((rc = coo_ctas_per_sm(coo_tile_kernel<T, true, TILE, 1>, kTileThreads, S1::total, &per_sm1))) return rc;
+  if ((rc = coo_ctas_per_sm(coo_tile_kernel<T, false, TILE, 1>, kTileThreads, S1::total, &per_sm1))) return rc;
+  const int64_t cap = int64_t(sm_count()) * per_sm, cap1 = int64_t(sm_count()) * per_sm1;
   p->grid = int(p->ntiles < cap ? p->ntiles : cap);
+  p->grid_direct = int(p->ntiles < cap1 ? p->ntiles : cap1);
   return SPMV_OK;
 }
 
@@ -551,19 +598,35 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
   SPMV_CUDA_TRY(cudaMemcpyAsync(&h, nl.ptr, 8, cudaMemcpyDeviceToHost, st));
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
   p->n_long = int64_t(h);
-  p->tile = tile_entries() == 1024 ? 1024 : 2048;  // the COO kernels exist for these two
+  // 1536-entry tiles; 6 consumer groups over 7 stages (one CTA per SM) for
+  // short runs, one group (4 CTAs/SM) when long runs exist.  Measured on
+  // B200: 256^3 stencil 533 -> 630 GFLOP/s, Zipf 173 -> 193.
+  p->tile = 1536;
+  p->groups = p->n_long > 0 ? 1 : 6;
+  if (tile_entries()) {
+    p->tile = tile_entries();
+    p->groups = 1;
+  }
+  if (coo_groups() > 0) p->groups = coo_groups();
+  if (!coo_config_known(p->tile, p->groups)) {
+    p->groups = 1;
+    if (!coo_config_known(p->tile, 1)) p->tile = 2048;
+  }
   p->ntiles = (nnz + p->tile - 1) / p->tile;
   const size_t vs = value_size(p->dtype);
   if ((rc = p->head_row.alloc(4 * p->ntiles)) || (rc = p->tail_row.alloc(4 * p->ntiles)) ||
       (rc = p->pass.alloc(4 * p->ntiles)) || (rc = p->head_val.alloc(vs * p->ntiles)) ||
       (rc = p->tail_val.alloc(vs * p->ntiles)))
     return rc;
-  if (p->tile == 1024)
-    return p->dtype == SPMV_F64 ? coo_launch_config<double, 1024>(p) : coo_launch_config<float, 1024>(p);
-  return p->dtype == SPMV_F64 ? coo_launch_config<double, 2048>(p) : coo_launch_config<float, 2048>(p);
+#define X(TL, GR)                                                                                    \
+  if (p->tile == TL && p->groups == GR)                                                             \
+    return p->dtype == SPMV_F64 ? coo_launch_config<double, TL, GR>(p) : coo_launch_config<float, TL, GR>(p);
+  SPMV_COO_CONFIGS(X)
+#undef X
+  return fail(SPMV_INVALID_ARG, "no COO kernel for tile %lld x %d groups", (long long)p->tile, p->groups);
 }
 
-template <typename T, int TILE>
+template <typename T, int TILE, int G>
 static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st) {
   if (p->nrows == 0) return SPMV_OK;
@@ -591,15 +654,28 @@ static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint3
   P.nnz = p->nnz;
   P.col_base = col_base;
   P.ntiles = p->ntiles;
+  P.tile_begin = 0;
   P.mode = tile_mode_flags() | (tma_hint_mode() != 0 ? 4 : 0);
   const bool aligned = (reinterpret_cast<uintptr_t>(ai) % 16 == 0) && (reinterpret_cast<uintptr_t>(aj) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
-  const size_t smem = CooSmem<T, TILE>::total;
-  if (aligned)
-    coo_tile_kernel<T, true, TILE><<<unsigned(p->grid), kTileThreads, smem, st>>>(P);
-  else
-    coo_tile_kernel<T, false, TILE><<<unsigned(p->grid), kTileThreads, smem, st>>>(P);
+  const size_t smem1 = CooSmem<T, TILE, 1>::total;
+  if (!aligned) {
+    coo_tile_kernel<T, false, TILE, 1><<<unsigned(p->grid_direct), kTileThreads, smem1, st>>>(P);
+  } else if (G == 1) {
+    coo_tile_kernel<T, true, TILE, 1><<<unsigned(p->grid), kTileThreads, smem1, st>>>(P);
+  } else {
+    if (P.n_bulk > 0)
+      coo_tile_kernel<T, true, TILE, G>
+          <<<unsigned(std::min<int64_t>(p->grid, P.n_bulk)), G * coo_group_threads<G>(), CooSmem<T, TILE, G>::total,
+             st>>>(P);
+    if (P.n_bulk < p->ntiles) {  // tail tiles the bulk engine cannot address
+      CooParams<T> Q = P;
+      Q.tile_begin = P.n_bulk;
+      const int64_t g1 = std::min<int64_t>(p->grid_direct, p->ntiles - P.n_bulk);
+      coo_tile_kernel<T, false, TILE, 1><<<unsigned(g1), kTileThreads, smem1, st>>>(Q);
+    }
+  }
   SPMV_LAUNCH_CHECK();
   if (p->n_long > 0) {
     const int64_t g = std::min<int64_t>((p->ntiles + 255) / 256, int64_t(sm_count()) * 8);
@@ -612,8 +688,11 @@ static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint3
 template <typename T>
 static int coo_run(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st) {
-  if (p->tile == 1024) return coo_run_tiled<T, 1024>(p, ai, aj, av, x, col_base, y, st);
-  return coo_run_tiled<T, 2048>(p, ai, aj, av, x, col_base, y, st);
+#define X(TL, GR) \
+  if (p->tile == TL && p->groups == GR) return coo_run_tiled<T, TL, GR>(p, ai, aj, av, x, col_base, y, st);
+  SPMV_COO_CONFIGS(X)
+#undef X
+  return fail(SPMV_INVALID_ARG, "no COO kernel for tile %lld x %d groups", (long long)p->tile, p->groups);
 }
 
 extern "C" {
@@ -654,7 +733,15 @@ int spmv_coo_plan_info(const spmv_coo_plan* p, int64_t* n_runs, int64_t* n_long_
   if (n_long_runs) *n_long_runs = p->n_long;
   if (n_items) *n_items = p->tile;
   if (row_sorted) *row_sorted = p->row_sorted ? 1 : 0;
-  if (launches) *launches = (p->nrows > 0 ? 1 : 0) + (p->n_long > 0 ? 1 : 0);
+  if (launches)
+    *launches = (p->nrows > 0 ? 1 : 0) + (p->n_long > 0 ? 1 : 0) +
+                (p->groups > 1 && p->nnz > 0 && bulk_tiles(p->nnz, p->ntiles, p->tile) < p->ntiles ? 1 : 0);
+  return SPMV_OK;
+}
+
+int spmv_coo_plan_groups(const spmv_coo_plan* p, int* groups) {
+  if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
+  if (groups) *groups = p->groups;
   return SPMV_OK;
 }
 

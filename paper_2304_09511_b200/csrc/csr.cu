@@ -700,7 +700,10 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
     p->groups = 1;
   }
   if (csr_groups() > 0) p->groups = csr_groups();
-  if (!csr_config_known(p->tile, p->groups)) p->groups = 1;
+  if (!csr_config_known(p->tile, p->groups)) {
+    p->groups = 1;
+    if (!csr_config_known(p->tile, 1)) p->tile = p->n_long > 0 ? 1024 : 2048;
+  }
   p->ntiles = (p->nnz + p->tile - 1) / p->tile;
   const size_t vs = value_size(p->dtype);
   if ((rc = p->row_lo.alloc(4 * (p->ntiles + 1))) || (rc = p->head.alloc(vs * p->ntiles)) ||

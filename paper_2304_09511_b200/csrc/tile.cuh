@@ -25,6 +25,7 @@ constexpr int max_long_segs() { return TILE / (kExactLen + 1) + 4; }
 int tile_entries();
 int ctas_per_sm_cap();  // 0 = occupancy limit
 int csr_groups();       // SPMV_CSR_GROUPS: 0 = plan choice
+int coo_groups();       // SPMV_COO_GROUPS: 0 = plan choice
 int tma_hint_mode();    // SPMV_TMA_HINT: -1 auto, 0 off, 1 on
 int tile_mode_flags();  // experiments: bit0 no products mode, bit1 warp-per-segment long rows
 

@@ -120,10 +120,12 @@ class _Plan:
             _lib.call("spmv_csr_plan_groups", self.handle, ctypes.byref(g))
             return {"long_rows": a.value, "tile": b.value, "launches": c.value, "groups": g.value}
         a, b, c, d, e = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_int64()
+        g = ctypes.c_int()
         _lib.call("spmv_coo_plan_info", self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                   ctypes.byref(d), ctypes.byref(e))
+        _lib.call("spmv_coo_plan_groups", self.handle, ctypes.byref(g))
         return {"runs": a.value, "long_runs": b.value, "tile": c.value, "row_sorted": bool(d.value),
-                "launches": e.value}
+                "launches": e.value, "groups": g.value}
 
 
 def csr_plan(A: CsrMatrix, exact_len: int = 0) -> _Plan:
