@@ -263,6 +263,59 @@ def cpu_baseline_csr(irp, cols, vals, x, budget_s: float = 10.0, y_check=None) -
     return out
 
 
+# ------------------------------------------------------------ conversions --
+def conversions_measure(torch, sp, mats, pk, reps: int = 3) -> dict:
+    """SURVEY.md §8(a) rows G1 and C1c-C5c at the bench config: each public
+    conversion timed with CUDA events (warm-up 1, median of `reps`), with
+    its minimum-byte model (containers are copied, like convert.py; two-pass
+    conversions read their indices twice)."""
+    from paper_2304_09511_b200 import convert as C
+    from paper_2304_09511_b200 import matrixio as M
+    csr = mats["csr"]
+    n, nnz, sv = csr.nrows, csr.nnz, csr.values.element_size()
+    coo = C.csr_to_coo(csr)
+    dia = C.coo_to_dia(coo)
+    nd, prow = dia.ndiags, dia.values.shape[0]
+    gen_args = CONFIGS["c5"]["grid"] if n == 256 ** 3 else None
+    g = torch.Generator(device=csr.values.device)
+    g.manual_seed(7)
+    perm = torch.randperm(nnz, device=csr.values.device, generator=g)
+    shuffled = sp.CooMatrix(coo.shape, coo.row_indices[perm], coo.col_indices[perm], coo.values[perm], sorted=False)
+    del perm
+    idx = 4 * nnz
+    cases = {
+        # name: (callable, algorithmic bytes)
+        "csr_to_coo": (lambda: C.csr_to_coo(csr), 4 * (n + 1) + nnz * (4 + sv) + nnz * (8 + sv)),
+        "coo_to_csr": (lambda: C.coo_to_csr(coo), nnz * (8 + sv) + 4 * (n + 1) + nnz * (4 + sv)),
+        "coo_to_dia": (lambda: C.coo_to_dia(coo), 2 * idx + nnz * (8 + sv) + prow * nd * sv),
+        "dia_to_coo": (lambda: C.dia_to_coo(dia), 2 * prow * nd * sv + nnz * (8 + sv)),
+        "sort_coo": (lambda: C.sort_coo(shuffled), 2 * nnz * (8 + sv)),
+    }
+    if gen_args is not None:
+        cases["gen_stencil27"] = (lambda: M.gen_stencil27(*gen_args), 4 * (n + 1) + nnz * (4 + sv))
+    out = {}
+    stream = torch.cuda.current_stream()
+    for name, (fn, b) in cases.items():
+        r = fn()
+        del r
+        torch.cuda.synchronize()
+        ts = []
+        for _ in range(reps):
+            a, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            a.record(stream)
+            r = fn()
+            e.record(stream)
+            torch.cuda.synchronize()
+            ts.append(a.elapsed_time(e) / 1e3)
+            del r
+        t = sorted(ts)[len(ts) // 2]
+        out[name] = {"ms": round(t * 1e3, 3), "bytes": int(b), "gbs": round(b / t / 1e9, 1),
+                     "roofline_frac": round(b / t / 1e9 / pk["hbm_gbs"], 4)}
+    out["_note"] = ("event-timed public calls (incl. host syncs of the analyze steps); bytes = minimum model: "
+                    "outputs written once, inputs read once per pass")
+    return out
+
+
 # ------------------------------------------------------------------- ours --
 def run_ours(args, torch, dist, rank, world, local_rank):
     import paper_2304_09511_b200 as sp
@@ -273,6 +326,9 @@ def run_ours(args, torch, dist, rank, world, local_rank):
     if world > 1 or args.force_dist:
         return run_ours_multi(args, torch, dist, rank, world, local_rank, pk)
     mats, x = build_workload(torch, sp, args.config, device)
+    if args.conversions:
+        print(json.dumps({"config": args.config, "conversions": conversions_measure(torch, sp, mats, pk)}), flush=True)
+        return
     flush_buf = None
     flush = None
     if args.config == "c1":
@@ -318,6 +374,8 @@ def run_ours(args, torch, dist, rank, world, local_rank):
     }
     if not args.no_extras:
         line["e2e"] = e2e_measure(args, torch, sp, m, x, head)
+        if "csr" in mats and "dia" in mats:  # Zipf has no DIA form (fill ratio)
+            line["conversions"] = conversions_measure(torch, sp, mats, pk)
         if args.config in ("c5", "c1", "c3", "c4"):
             csr = mats["csr"]
             h = csr.to_host()
@@ -491,6 +549,7 @@ def main():
     ap.add_argument("--config", choices=tuple(CONFIGS), default="c5")
     ap.add_argument("--format", default=None, help="headline format (default: the config's first)")
     ap.add_argument("--no-extras", action="store_true", help="headline format only (profiling runs)")
+    ap.add_argument("--conversions", action="store_true", help="time the format conversions only")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
     ap.add_argument("--force-dist", action="store_true",
                     help="use the row-partitioned path even at world size 1 (exercises it on one GPU)")

@@ -230,6 +230,12 @@ typedef struct spmv_coo_sorter spmv_coo_sorter;
 int spmv_sort_coo_analyze(int dtype, int64_t nnz, const uint32_t* row_indices,
                           const uint32_t* col_indices, void* stream,
                           spmv_coo_sorter** out, int64_t* nnz_out);
+/* Same, with the shape: the sort key packs (row, col) into
+ * bits(nrows) + bits(ncols) bits, so the radix sort runs fewer passes. */
+int spmv_sort_coo_analyze_shape(int dtype, int64_t nrows, int64_t ncols,
+                                int64_t nnz, const uint32_t* row_indices,
+                                const uint32_t* col_indices, void* stream,
+                                spmv_coo_sorter** out, int64_t* nnz_out);
 int spmv_sort_coo_emit(const spmv_coo_sorter* s, int dtype,
                        const void* values, uint32_t* row_indices_out,
                        uint32_t* col_indices_out, void* values_out,

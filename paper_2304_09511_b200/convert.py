@@ -83,8 +83,8 @@ def sort_coo(coo) -> CooMatrix:
     code = _lib.dtype_code(coo.values.dtype)
     h = ctypes.c_void_p()
     n_out = ctypes.c_int64()
-    _lib.call("spmv_sort_coo_analyze", code, coo.nnz, _ptr(coo.row_indices), _ptr(coo.col_indices), _stream(coo.values),
-              ctypes.byref(h), ctypes.byref(n_out))
+    _lib.call("spmv_sort_coo_analyze_shape", code, max(coo.nrows, 1), max(coo.ncols, 1), coo.nnz,
+              _ptr(coo.row_indices), _ptr(coo.col_indices), _stream(coo.values), ctypes.byref(h), ctypes.byref(n_out))
     try:
         n = int(n_out.value)
         ai, aj = _empty_idx(n, dev), _empty_idx(n, dev)

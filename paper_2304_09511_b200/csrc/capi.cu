@@ -172,6 +172,23 @@ int coo_groups() {
   static const int g = env_int("SPMV_COO_GROUPS", 0);
   return g;
 }
+int pool_keep_memory() {
+  static std::mutex mu;
+  static bool done[64] = {false};
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e != cudaSuccess) return fail(SPMV_CUDA_ERROR, "cudaGetDevice: %s", cudaGetErrorString(e));
+  std::lock_guard<std::mutex> lock(mu);
+  if (dev < 64 && done[dev]) return SPMV_OK;
+  cudaMemPool_t pool;
+  e = cudaDeviceGetDefaultMemPool(&pool, dev);
+  if (e != cudaSuccess) return fail(SPMV_CUDA_ERROR, "cudaDeviceGetDefaultMemPool: %s", cudaGetErrorString(e));
+  uint64_t keep = kPoolKeepBytes;
+  e = cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+  if (e != cudaSuccess) return fail(SPMV_CUDA_ERROR, "cudaMemPoolSetAttribute: %s", cudaGetErrorString(e));
+  if (dev < 64) done[dev] = true;
+  return SPMV_OK;
+}
 int ctas_per_sm_cap() {
   static const int c = env_int("SPMV_CTAS_PER_SM", 0);
   return c;

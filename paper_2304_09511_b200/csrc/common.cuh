@@ -63,6 +63,42 @@ struct DevBuf {
   DevBuf& operator=(const DevBuf&) = delete;
 };
 
+// Stream-ordered scratch from the device's default memory pool (conversions
+// allocate GB-sized temporaries per call; cudaMalloc/cudaFree would map and
+// unmap them and synchronise the device every time).  The pool keeps up to
+// kPoolKeepBytes cached between calls.
+constexpr uint64_t kPoolKeepBytes = uint64_t(32) << 30;
+int pool_keep_memory();  // once per device; capi.cu
+struct ScratchBuf {
+  void* ptr = nullptr;
+  size_t bytes = 0;
+  cudaStream_t st = nullptr;
+  int alloc(size_t n, cudaStream_t s) {
+    release();
+    if (n == 0) return SPMV_OK;
+    int rc = pool_keep_memory();
+    if (rc) return rc;
+    cudaError_t e = cudaMallocAsync(&ptr, n, s);
+    if (e != cudaSuccess) {
+      ptr = nullptr;
+      return fail(SPMV_CUDA_ERROR, "cudaMallocAsync(%zu) failed: %s", n, cudaGetErrorString(e));
+    }
+    bytes = n;
+    st = s;
+    return SPMV_OK;
+  }
+  void release() {
+    if (ptr) cudaFreeAsync(ptr, st);
+    ptr = nullptr;
+    bytes = 0;
+  }
+  template <typename T> T* as() const { return reinterpret_cast<T*>(ptr); }
+  ~ScratchBuf() { release(); }
+  ScratchBuf() = default;
+  ScratchBuf(const ScratchBuf&) = delete;
+  ScratchBuf& operator=(const ScratchBuf&) = delete;
+};
+
 inline size_t value_size(int dtype) { return dtype == SPMV_F64 ? 8 : 4; }
 inline bool valid_dtype(int dtype) { return dtype == SPMV_F32 || dtype == SPMV_F64; }
 

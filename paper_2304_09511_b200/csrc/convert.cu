@@ -37,42 +37,52 @@ __global__ void coo_irp_kernel(const uint32_t* __restrict__ ai, int64_t nnz, int
 }
 
 // ---- csr -> coo ------------------------------------------------------------
-// Thread per row for rows of <= 64 entries, warp per row for longer ones.
-__global__ void csr_expand_short_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj,
-                                        int64_t nrows, uint32_t* __restrict__ ai, int* __restrict__ unsorted) {
-  GRID_STRIDE(r, nrows) {
-    const uint32_t s = irp[r], e = irp[r + 1];
-    if (e - s > 64) continue;
-    bool bad = false;
-    for (uint32_t j = s; j < e; ++j) {
-      ai[j] = uint32_t(r);
-      if (j > s && aj[j] <= aj[j - 1]) bad = true;
-    }
-    if (bad) *unsorted = 1;
-  }
-}
+// A block takes kExpandRows rows, stages their row pointers in shared memory
+// and walks the rows' entries entry-parallel: every thread finds its entry's
+// row by binary search, so the row, column and value streams are read and
+// written coalesced whatever the row lengths.  The column copy doubles as the
+// strictly-increasing check (convert.py:104-108).
+constexpr int kExpandRows = 256;
 
-__global__ void csr_expand_long_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj,
-                                       int64_t nrows, uint32_t* __restrict__ ai, int* __restrict__ unsorted) {
-  const int lane = threadIdx.x & 31;
-  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
-  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
-  for (int64_t r = warp; r < nrows; r += nwarps) {
-    const uint32_t s = irp[r], e = irp[r + 1];
-    if (e - s <= 64) continue;
-    bool bad = false;
-    for (uint32_t j = s + lane; j < e; j += 32) {
-      ai[j] = uint32_t(r);
-      if (j > s && aj[j] <= aj[j - 1]) bad = true;
+template <typename T>
+__global__ void __launch_bounds__(256) csr_expand_kernel(const uint32_t* __restrict__ irp,
+                                                         const uint32_t* __restrict__ aj, const T* __restrict__ av,
+                                                         int64_t nrows, uint32_t* __restrict__ ai_out,
+                                                         uint32_t* __restrict__ aj_out, T* __restrict__ av_out,
+                                                         int* __restrict__ unsorted) {
+  __shared__ uint32_t s_irp[kExpandRows + 1];
+  bool bad = false;
+  for (int64_t r0 = int64_t(blockIdx.x) * kExpandRows; r0 < nrows; r0 += int64_t(gridDim.x) * kExpandRows) {
+    const int nr = int(min(int64_t(kExpandRows), nrows - r0));
+    for (int i = threadIdx.x; i <= nr; i += blockDim.x) s_irp[i] = irp[r0 + i];
+    __syncthreads();
+    const uint32_t e0 = s_irp[0], e1 = s_irp[nr];
+    for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      int lo = 0, hi = nr - 1;  // last local row with s_irp[row] <= e
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_irp[mid] <= e) lo = mid; else hi = mid - 1;
+      }
+      const uint32_t c = aj[e];
+      if (e > s_irp[lo] && c <= aj[e - 1]) bad = true;
+      ai_out[e] = uint32_t(r0 + lo);
+      aj_out[e] = c;
+      av_out[e] = av[e];
     }
-    if (__any_sync(0xffffffffu, bad) && lane == 0) *unsorted = 1;
+    __syncthreads();
   }
+  if (__syncthreads_or(bad) && threadIdx.x == 0) *unsorted = 1;
 }
 
 // ---- coo -> dia --------------------------------------------------------------
 __global__ void diag_mark_kernel(const uint32_t* __restrict__ ai, const uint32_t* __restrict__ aj, int64_t nnz,
                                  int64_t nrows, uint32_t* __restrict__ flags) {
-  GRID_STRIDE(k, nnz) flags[int64_t(aj[k]) - int64_t(ai[k]) + nrows - 1] = 1u;
+  // A matrix has few distinct diagonals: reading first (through L1) keeps
+  // the flag lines shared instead of storing to the same words nnz times.
+  GRID_STRIDE(k, nnz) {
+    uint32_t* f = flags + (int64_t(aj[k]) - int64_t(ai[k]) + nrows - 1);
+    if (__ldg(f) == 0u) *f = 1u;  // a stale 0 only repeats an idempotent store
+  }
 }
 
 __global__ void diag_offsets_kernel(const uint32_t* __restrict__ flags, const uint32_t* __restrict__ pos, int64_t nd_all,
@@ -92,33 +102,69 @@ __global__ void diag_scatter_kernel(const uint32_t* __restrict__ ai, const uint3
 }
 
 // ---- dia -> coo --------------------------------------------------------------
-template <typename T>
-__global__ void dia_count_kernel(const int32_t* __restrict__ offs, const T* __restrict__ vals, int64_t nrows,
-                                 int64_t ncols, int64_t nd, unsigned long long* __restrict__ counts) {
-  GRID_STRIDE(i, nrows) {
-    unsigned long long c = 0;
-    for (int64_t d = 0; d < nd; ++d) {
-      const int64_t col = i + offs[d];
-      if (col >= 0 && col < ncols && vals[i * nd + d] != T(0)) ++c;
-    }
-    counts[i] = c;
-  }
+// Groups of W = next_pow2(ndiags) <= 32 lanes take one row each; lane d reads
+// diagonal d (d + 32k when ndiags > 32), so a group reads its row's cells as
+// one contiguous run and the kept cells (in-bounds, != 0: -0.0 dropped, NaN
+// kept, convert.py:155-163) are compacted with a ballot: the emit pass writes
+// each row's entries as a contiguous run in (row, col) order.  Four rows per
+// group are loaded before they are compacted.
+constexpr int kDiaRowsInFlight = 4;
+inline int dia_group_width(int64_t nd) {
+  int w = 1;
+  while (w < nd && w < 32) w <<= 1;
+  return w;
 }
 
-template <typename T>
-__global__ void dia_emit_kernel(const int32_t* __restrict__ offs, const T* __restrict__ vals, int64_t nrows,
-                                int64_t ncols, int64_t nd, const unsigned long long* __restrict__ starts,
-                                uint32_t* __restrict__ ai, uint32_t* __restrict__ aj, T* __restrict__ av) {
-  GRID_STRIDE(i, nrows) {
-    unsigned long long o = starts[i];
-    for (int64_t d = 0; d < nd; ++d) {
-      const int64_t col = i + offs[d];
-      const T v = vals[i * nd + d];
-      if (col >= 0 && col < ncols && v != T(0)) {
-        ai[o] = uint32_t(i);
-        aj[o] = uint32_t(col);
-        av[o] = v;
-        ++o;
+template <typename T, bool EMIT>
+__global__ void __launch_bounds__(256) dia_rows_kernel(const int32_t* __restrict__ offs, const T* __restrict__ vals,
+                                                       int64_t nrows, int64_t ncols, int nd, int W,
+                                                       unsigned long long* __restrict__ counts,
+                                                       const unsigned long long* __restrict__ starts,
+                                                       uint32_t* __restrict__ ai, uint32_t* __restrict__ aj,
+                                                       T* __restrict__ av) {
+  const int lane = threadIdx.x & 31, sub = lane / W, gl = lane % W;
+  const int gpw = 32 / W;  // groups (rows) per warp
+  const unsigned gmask = W == 32 ? 0xffffffffu : ((1u << W) - 1u) << (sub * W);
+  const unsigned below = (1u << lane) - 1u;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  constexpr int U = kDiaRowsInFlight;
+  for (int64_t base = warp * gpw * U; base < nrows; base += nwarps * gpw * U) {
+    unsigned long long o[U];  // EMIT: next output slot of each row; else its count
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t i = base + int64_t(u) * gpw + sub;
+      o[u] = EMIT && i < nrows ? starts[i] : 0ull;
+    }
+    for (int d0 = 0; d0 < nd; d0 += W) {
+      const int d = d0 + gl;
+      const int64_t off = d < nd ? int64_t(__ldg(offs + d)) : 0;
+      T v[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = base + int64_t(u) * gpw + sub;
+        v[u] = (i < nrows && d < nd) ? vals[i * nd + d] : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = base + int64_t(u) * gpw + sub;
+        const int64_t col = i + off;
+        const bool keep = i < nrows && d < nd && col >= 0 && col < ncols && v[u] != T(0);
+        const unsigned bal = __ballot_sync(0xffffffffu, keep) & gmask;
+        if (EMIT && keep) {
+          const unsigned long long q = o[u] + __popc(bal & below);
+          ai[q] = uint32_t(i);
+          aj[q] = uint32_t(col);
+          av[q] = v[u];
+        }
+        o[u] += __popc(bal);
+      }
+    }
+    if (!EMIT && gl == 0) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int64_t i = base + int64_t(u) * gpw + sub;
+        if (i < nrows) counts[i] = o[u];
       }
     }
   }
@@ -126,9 +172,9 @@ __global__ void dia_emit_kernel(const int32_t* __restrict__ offs, const T* __res
 
 // ---- sort_coo ------------------------------------------------------------------
 __global__ void make_keys_kernel(const uint32_t* __restrict__ ai, const uint32_t* __restrict__ aj, int64_t nnz,
-                                 unsigned long long* __restrict__ keys, uint32_t* __restrict__ idx) {
+                                 int col_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ idx) {
   GRID_STRIDE(k, nnz) {
-    keys[k] = (static_cast<unsigned long long>(ai[k]) << 32) | aj[k];
+    keys[k] = (static_cast<unsigned long long>(ai[k]) << col_bits) | aj[k];
     idx[k] = uint32_t(k);
   }
 }
@@ -172,15 +218,15 @@ __device__ T np_pairwise(const T* __restrict__ av, const uint32_t* __restrict__ 
 
 template <typename T>
 __global__ void sort_emit_kernel(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ perm,
-                                 const uint32_t* __restrict__ run_start, int64_t n_runs, int64_t nnz,
+                                 const uint32_t* __restrict__ run_start, int64_t n_runs, int64_t nnz, int col_bits,
                                  const T* __restrict__ av, uint32_t* __restrict__ ai, uint32_t* __restrict__ aj,
                                  T* __restrict__ out) {
   GRID_STRIDE(i, n_runs) {
     const uint32_t a = run_start[i];
     const uint32_t b = (i + 1 < n_runs) ? run_start[i + 1] : uint32_t(nnz);
     const unsigned long long key = keys[a];
-    ai[i] = uint32_t(key >> 32);
-    aj[i] = uint32_t(key & 0xffffffffull);
+    ai[i] = uint32_t(key >> col_bits);
+    aj[i] = uint32_t(key & ((1ull << col_bits) - 1ull));
     T v = av[perm[a]];
     if (b - a > 1) v = add_rn(v, np_pairwise(av, perm, a + 1, b - a - 1));
     out[i] = v;
@@ -193,25 +239,26 @@ using namespace spmv;
 
 struct spmv_dia_builder {
   int64_t nrows = 0, ncols = 0, nnz = 0, nd_all = 0, ndiags = 0;
-  DevBuf flags, pos;
+  ScratchBuf flags, pos;
 };
 
 struct spmv_dia_collect {
   int64_t nrows = 0, ncols = 0, ndiags = 0, nnz = 0;
-  DevBuf counts, starts;
+  ScratchBuf counts, starts;
 };
 
 struct spmv_coo_sorter {
   int64_t nnz = 0, n_runs = 0;
-  DevBuf keys, perm, run_start;
+  int col_bits = 32;  // key = row << col_bits | col
+  ScratchBuf keys, perm, run_start;
 };
 
 template <typename V>
 static int excl_scan(const V* in, V* out, int64_t n, cudaStream_t st) {
   size_t tmp_bytes = 0;
   SPMV_CUDA_TRY(cub::DeviceScan::ExclusiveSum(nullptr, tmp_bytes, in, out, n, st));
-  DevBuf tmp;
-  int rc = tmp.alloc(tmp_bytes);
+  ScratchBuf tmp;
+  int rc = tmp.alloc(tmp_bytes, st);
   if (rc) return rc;
   SPMV_CUDA_TRY(cub::DeviceScan::ExclusiveSum(tmp.ptr, tmp_bytes, in, out, n, st));
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
@@ -254,16 +301,22 @@ int spmv_csr_to_coo(int dtype, int64_t nrows, int64_t nnz, const uint32_t* irp, 
   cudaStream_t st = as_stream(stream);
   if (sorted_out) *sorted_out = 1;
   if (nnz == 0 || nrows == 0) return SPMV_OK;
-  DevBuf flag;
-  int rc = flag.alloc(sizeof(int));
+  ScratchBuf flag;
+  int rc = flag.alloc(sizeof(int), st);
   if (rc) return rc;
   SPMV_CUDA_TRY(cudaMemsetAsync(flag.ptr, 0, sizeof(int), st));
-  csr_expand_short_kernel<<<unsigned(grid_for(nrows)), 256, 0, st>>>(irp, aj, nrows, ai_out, flag.as<int>());
-  SPMV_LAUNCH_CHECK();
-  csr_expand_long_kernel<<<unsigned(grid_for(nrows * 32)), 256, 0, st>>>(irp, aj, nrows, ai_out, flag.as<int>());
-  SPMV_LAUNCH_CHECK();
-  SPMV_CUDA_TRY(cudaMemcpyAsync(aj_out, aj, 4 * nnz, cudaMemcpyDeviceToDevice, st));
-  SPMV_CUDA_TRY(cudaMemcpyAsync(av_out, av, value_size(dtype) * nnz, cudaMemcpyDeviceToDevice, st));
+  {
+    int64_t g = (nrows + kExpandRows - 1) / kExpandRows;
+    const int64_t cap = int64_t(sm_count()) * 8;
+    if (g > cap) g = cap;
+    if (dtype == SPMV_F64)
+      csr_expand_kernel<double><<<unsigned(g), 256, 0, st>>>(irp, aj, static_cast<const double*>(av), nrows, ai_out,
+                                                            aj_out, static_cast<double*>(av_out), flag.as<int>());
+    else
+      csr_expand_kernel<float><<<unsigned(g), 256, 0, st>>>(irp, aj, static_cast<const float*>(av), nrows, ai_out,
+                                                           aj_out, static_cast<float*>(av_out), flag.as<int>());
+    SPMV_LAUNCH_CHECK();
+  }
   int h = 0;
   SPMV_CUDA_TRY(cudaMemcpyAsync(&h, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
@@ -284,7 +337,7 @@ int spmv_coo_to_dia_analyze(int64_t nrows, int64_t ncols, int64_t nnz, const uin
   int rc = SPMV_OK;
   if (nnz > 0) {
     b->nd_all = nrows + ncols - 1;
-    if (!(rc = b->flags.alloc(4 * b->nd_all)) && !(rc = b->pos.alloc(4 * b->nd_all))) {
+    if (!(rc = b->flags.alloc(4 * b->nd_all, st)) && !(rc = b->pos.alloc(4 * b->nd_all, st))) {
       cudaError_t e = cudaMemsetAsync(b->flags.ptr, 0, 4 * b->nd_all, st);
       if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "memset: %s", cudaGetErrorString(e));
       if (!rc) {
@@ -354,15 +407,19 @@ int spmv_dia_to_coo_count(int dtype, int64_t nrows, int64_t ncols, int64_t ndiag
   c->ndiags = ndiags;
   int rc = SPMV_OK;
   if (nrows > 0 && ndiags > 0) {
-    rc = c->counts.alloc(8 * nrows);
-    if (!rc) rc = c->starts.alloc(8 * nrows);
+    rc = c->counts.alloc(8 * nrows, st);
+    if (!rc) rc = c->starts.alloc(8 * nrows, st);
     if (!rc) {
+      const int W = dia_group_width(ndiags);
+      const int64_t g = grid_for(nrows * W / kDiaRowsInFlight);
       if (dtype == SPMV_F64)
-        dia_count_kernel<double><<<unsigned(grid_for(nrows)), 256, 0, st>>>(
-            offsets, static_cast<const double*>(values), nrows, ncols, ndiags, c->counts.as<unsigned long long>());
+        dia_rows_kernel<double, false><<<unsigned(g), 256, 0, st>>>(
+            offsets, static_cast<const double*>(values), nrows, ncols, int(ndiags), W,
+            c->counts.as<unsigned long long>(), nullptr, nullptr, nullptr, nullptr);
       else
-        dia_count_kernel<float><<<unsigned(grid_for(nrows)), 256, 0, st>>>(
-            offsets, static_cast<const float*>(values), nrows, ncols, ndiags, c->counts.as<unsigned long long>());
+        dia_rows_kernel<float, false><<<unsigned(g), 256, 0, st>>>(
+            offsets, static_cast<const float*>(values), nrows, ncols, int(ndiags), W,
+            c->counts.as<unsigned long long>(), nullptr, nullptr, nullptr, nullptr);
       cudaError_t e = cudaGetLastError();
       if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "dia_count: %s", cudaGetErrorString(e));
     }
@@ -389,13 +446,15 @@ int spmv_dia_to_coo_fill(const spmv_dia_collect* c, int dtype, const int32_t* of
   if (!c) return fail(SPMV_INVALID_ARG, "collector is NULL");
   if (c->nnz == 0) return SPMV_OK;
   cudaStream_t st = as_stream(stream);
+  const int W = dia_group_width(c->ndiags);
+  const int64_t g = grid_for(c->nrows * W / kDiaRowsInFlight);
   if (dtype == SPMV_F64)
-    dia_emit_kernel<double><<<unsigned(grid_for(c->nrows)), 256, 0, st>>>(
-        offsets, static_cast<const double*>(values), c->nrows, c->ncols, c->ndiags,
+    dia_rows_kernel<double, true><<<unsigned(g), 256, 0, st>>>(
+        offsets, static_cast<const double*>(values), c->nrows, c->ncols, int(c->ndiags), W, nullptr,
         c->starts.as<unsigned long long>(), ai, aj, static_cast<double*>(av));
   else
-    dia_emit_kernel<float><<<unsigned(grid_for(c->nrows)), 256, 0, st>>>(
-        offsets, static_cast<const float*>(values), c->nrows, c->ncols, c->ndiags,
+    dia_rows_kernel<float, true><<<unsigned(g), 256, 0, st>>>(
+        offsets, static_cast<const float*>(values), c->nrows, c->ncols, int(c->ndiags), W, nullptr,
         c->starts.as<unsigned long long>(), ai, aj, static_cast<float*>(av));
   SPMV_LAUNCH_CHECK();
   return SPMV_OK;
@@ -406,37 +465,54 @@ int spmv_dia_collect_destroy(spmv_dia_collect* c) {
   return SPMV_OK;
 }
 
+static int bits_for(int64_t n) {  // bits holding 0 .. n-1 (at least 1)
+  int b = 1;
+  while (b < 32 && (int64_t(1) << b) < n) ++b;
+  return b;
+}
+
 int spmv_sort_coo_analyze(int dtype, int64_t nnz, const uint32_t* ai, const uint32_t* aj, void* stream,
                           spmv_coo_sorter** out, int64_t* nnz_out) {
+  return spmv_sort_coo_analyze_shape(dtype, int64_t(1) << 32, int64_t(1) << 32, nnz, ai, aj, stream, out, nnz_out);
+}
+
+int spmv_sort_coo_analyze_shape(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* ai,
+                                const uint32_t* aj, void* stream, spmv_coo_sorter** out, int64_t* nnz_out) {
   if (!out || !nnz_out) return fail(SPMV_INVALID_ARG, "NULL output");
   *out = nullptr;
   if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
   if (nnz < 0 || nnz > int64_t(UINT32_MAX)) return fail(SPMV_INVALID_ARG, "bad nnz");
   cudaStream_t st = as_stream(stream);
+  if (nrows < 1 || ncols < 1 || nrows > (int64_t(1) << 32) || ncols > (int64_t(1) << 32))
+    return fail(SPMV_INVALID_ARG, "bad COO shape");
   auto* s = new spmv_coo_sorter();
   s->nnz = nnz;
+  // Pack (row, col) into bits(nrows) + bits(ncols) bits so the radix sort
+  // runs only the passes it needs (48 bits = 6 passes at 256^3, not 8).
+  s->col_bits = bits_for(ncols);
+  const int key_bits = bits_for(nrows) + s->col_bits;
   int rc = SPMV_OK;
   if (nnz > 0) {
-    DevBuf keys_in, idx_in, head, pos, tmp;
-    rc = keys_in.alloc(8 * nnz);
-    if (!rc) rc = idx_in.alloc(4 * nnz);
-    if (!rc) rc = s->keys.alloc(8 * nnz);
-    if (!rc) rc = s->perm.alloc(4 * nnz);
-    if (!rc) rc = head.alloc(4 * nnz);
-    if (!rc) rc = pos.alloc(4 * nnz);
+    ScratchBuf keys_in, idx_in, head, pos, tmp;
+    rc = keys_in.alloc(8 * nnz, st);
+    if (!rc) rc = idx_in.alloc(4 * nnz, st);
+    if (!rc) rc = s->keys.alloc(8 * nnz, st);
+    if (!rc) rc = s->perm.alloc(4 * nnz, st);
+    if (!rc) rc = head.alloc(4 * nnz, st);
+    if (!rc) rc = pos.alloc(4 * nnz, st);
     if (!rc) {
-      make_keys_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, aj, nnz, keys_in.as<unsigned long long>(),
-                                                                idx_in.as<uint32_t>());
+      make_keys_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, aj, nnz, s->col_bits,
+                                                                keys_in.as<unsigned long long>(), idx_in.as<uint32_t>());
       size_t tmp_bytes = 0;
       cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in.as<unsigned long long>(),
                                                       s->keys.as<unsigned long long>(), idx_in.as<uint32_t>(),
-                                                      s->perm.as<uint32_t>(), nnz, 0, 64, st);
+                                                      s->perm.as<uint32_t>(), nnz, 0, key_bits, st);
       if (e == cudaSuccess) {
-        rc = tmp.alloc(tmp_bytes);
+        rc = tmp.alloc(tmp_bytes, st);
         if (!rc)
           e = cub::DeviceRadixSort::SortPairs(tmp.ptr, tmp_bytes, keys_in.as<unsigned long long>(),
                                               s->keys.as<unsigned long long>(), idx_in.as<uint32_t>(),
-                                              s->perm.as<uint32_t>(), nnz, 0, 64, st);
+                                              s->perm.as<uint32_t>(), nnz, 0, key_bits, st);
       }
       if (!rc && e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "radix sort: %s", cudaGetErrorString(e));
     }
@@ -446,7 +522,7 @@ int spmv_sort_coo_analyze(int dtype, int64_t nnz, const uint32_t* ai, const uint
       rc = excl_scan<uint32_t>(head.as<uint32_t>(), pos.as<uint32_t>(), nnz, st);
     }
     if (!rc) rc = scan_total<uint32_t>(head.as<uint32_t>(), pos.as<uint32_t>(), nnz, st, &s->n_runs);
-    if (!rc) rc = s->run_start.alloc(4 * s->n_runs);
+    if (!rc) rc = s->run_start.alloc(4 * s->n_runs, st);
     if (!rc) {
       key_runs_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(head.as<uint32_t>(), pos.as<uint32_t>(), nnz,
                                                                s->run_start.as<uint32_t>());
@@ -472,11 +548,11 @@ int spmv_sort_coo_emit(const spmv_coo_sorter* s, int dtype, const void* av, uint
   if (dtype == SPMV_F64)
     sort_emit_kernel<double><<<unsigned(grid_for(s->n_runs)), 256, 0, st>>>(
         s->keys.as<unsigned long long>(), s->perm.as<uint32_t>(), s->run_start.as<uint32_t>(), s->n_runs, s->nnz,
-        static_cast<const double*>(av), ai_out, aj_out, static_cast<double*>(av_out));
+        s->col_bits, static_cast<const double*>(av), ai_out, aj_out, static_cast<double*>(av_out));
   else
     sort_emit_kernel<float><<<unsigned(grid_for(s->n_runs)), 256, 0, st>>>(
         s->keys.as<unsigned long long>(), s->perm.as<uint32_t>(), s->run_start.as<uint32_t>(), s->n_runs, s->nnz,
-        static_cast<const float*>(av), ai_out, aj_out, static_cast<float*>(av_out));
+        s->col_bits, static_cast<const float*>(av), ai_out, aj_out, static_cast<float*>(av_out));
   SPMV_LAUNCH_CHECK();
   return SPMV_OK;
 }

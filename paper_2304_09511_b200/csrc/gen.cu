@@ -28,33 +28,54 @@ __host__ __device__ inline int64_t stencil_irp(int64_t nx, int64_t ny, int64_t n
          axis_count(nz, z) * axis_count(ny, y) * axis_prefix(nx, x);
 }
 
+// Entry-parallel fill: a block stages the row pointers and (x, y, z) of
+// kGenRows rows in shared memory; every thread then takes entries of the
+// block's range, finds its row by binary search and decodes the entry's
+// neighbour from the per-axis counts (dz outer, dx inner = ascending columns),
+// so the column and value streams are written coalesced.
+constexpr int kGenRows = 256;
+
 template <typename T>
-__global__ void stencil27_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_begin, int64_t row_end,
-                                 uint32_t* __restrict__ irp, uint32_t* __restrict__ aj, T* __restrict__ av) {
+__global__ void __launch_bounds__(256) stencil27_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_begin,
+                                                        int64_t row_end, uint32_t* __restrict__ irp,
+                                                        uint32_t* __restrict__ aj, T* __restrict__ av) {
+  __shared__ uint32_t s_o[kGenRows + 1];
+  __shared__ uint32_t s_x[kGenRows], s_y[kGenRows], s_z[kGenRows];
   const int64_t nloc = row_end - row_begin;
   const int64_t base = stencil_irp(nx, ny, nz, row_begin);
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= nloc; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t p = row_begin + i;
-    const int64_t o = stencil_irp(nx, ny, nz, p) - base;
-    irp[i] = uint32_t(o);
-    if (i == nloc) continue;
-    const int64_t x = p % nx, y = (p / nx) % ny, z = p / (nx * ny);
-    int64_t k = o;
-    for (int dz = -1; dz <= 1; ++dz) {
-      const int64_t qz = z + dz;
-      if (qz < 0 || qz >= nz) continue;
-      for (int dy = -1; dy <= 1; ++dy) {
-        const int64_t qy = y + dy;
-        if (qy < 0 || qy >= ny) continue;
-        for (int dx = -1; dx <= 1; ++dx) {
-          const int64_t qx = x + dx;
-          if (qx < 0 || qx >= nx) continue;
-          aj[k] = uint32_t((qz * ny + qy) * nx + qx);
-          av[k] = (dx == 0 && dy == 0 && dz == 0) ? T(26.0) : T(-1.0);
-          ++k;
-        }
+  for (int64_t r0 = int64_t(blockIdx.x) * kGenRows; r0 <= nloc; r0 += int64_t(gridDim.x) * kGenRows) {
+    const int nr = int(min(int64_t(kGenRows), nloc - r0));
+    for (int i = threadIdx.x; i <= nr; i += blockDim.x) {
+      const int64_t p = row_begin + r0 + i;
+      const uint32_t o = uint32_t(stencil_irp(nx, ny, nz, p) - base);
+      s_o[i] = o;
+      if (i < nr || r0 + nr == nloc) irp[r0 + i] = o;  // irp[r0 + nr] belongs to the next block
+      if (i < nr) {
+        const uint32_t q = uint32_t(p), ux = uint32_t(nx), uy = uint32_t(ny);
+        s_x[i] = q % ux;
+        s_y[i] = (q / ux) % uy;
+        s_z[i] = q / (ux * uy);
       }
     }
+    __syncthreads();
+    const uint32_t e0 = s_o[0], e1 = s_o[nr];
+    for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
+      int lo = 0, hi = nr - 1;  // last local row with s_o[row] <= e
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (s_o[mid] <= e) lo = mid; else hi = mid - 1;
+      }
+      const uint32_t j = e - s_o[lo];
+      const int64_t x = s_x[lo], y = s_y[lo], z = s_z[lo];
+      const uint32_t cx = uint32_t(axis_count(nx, x)), cy = uint32_t(axis_count(ny, y));
+      const uint32_t jx = j % cx, t = j / cx, jy = t % cy, jz = t / cy;
+      const int64_t dx = int64_t(jx) - (nx == 1 || x == 0 ? 0 : 1);
+      const int64_t dy = int64_t(jy) - (ny == 1 || y == 0 ? 0 : 1);
+      const int64_t dz = int64_t(jz) - (nz == 1 || z == 0 ? 0 : 1);
+      aj[e] = uint32_t(((z + dz) * ny + (y + dy)) * nx + (x + dx));
+      av[e] = (dx == 0 && dy == 0 && dz == 0) ? T(26.0) : T(-1.0);
+    }
+    __syncthreads();
   }
 }
 
@@ -86,8 +107,8 @@ int spmv_stencil27_fill(int dtype, int64_t nx, int64_t ny, int64_t nz, int64_t r
   if (!irp) return fail(SPMV_INVALID_ARG, "row_pointers_out is NULL");
   cudaStream_t st = as_stream(stream);
   const int64_t work = row_end - row_begin + 1;
-  int64_t grid = (work + 255) / 256;
-  const int64_t cap = int64_t(sm_count()) * 32;
+  int64_t grid = (work + kGenRows - 1) / kGenRows;
+  const int64_t cap = int64_t(sm_count()) * 8;
   if (grid > cap) grid = cap;
   if (dtype == SPMV_F64)
     stencil27_kernel<double><<<unsigned(grid), 256, 0, st>>>(nx, ny, nz, row_begin, row_end, irp, aj,
