@@ -26,13 +26,20 @@ static int64_t grid_for(int64_t n, int tb = 256) {
   for (int64_t k = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k < (n); k += int64_t(gridDim.x) * blockDim.x)
 
 // ---- coo -> csr: irp[r] = first entry with row >= r -----------------------
-__global__ void coo_irp_kernel(const uint32_t* __restrict__ ai, int64_t nnz, int64_t nrows, uint32_t* __restrict__ irp) {
+// One pass: the row boundaries and the column / value copies (convert.py
+// copies AJ and AV) share the read of each entry.
+template <typename T>
+__global__ void coo_to_csr_kernel(const uint32_t* __restrict__ ai, const uint32_t* __restrict__ aj,
+                                  const T* __restrict__ av, int64_t nnz, int64_t nrows, uint32_t* __restrict__ irp,
+                                  uint32_t* __restrict__ aj_out, T* __restrict__ av_out) {
   GRID_STRIDE(k, nnz) {
     const int64_t rk = ai[k];
     const int64_t rp = k == 0 ? -1 : int64_t(ai[k - 1]);
     for (int64_t r = rp + 1; r <= rk; ++r) irp[r] = uint32_t(k);
     if (k == nnz - 1)
       for (int64_t r = rk + 1; r <= nrows; ++r) irp[r] = uint32_t(nnz);
+    aj_out[k] = aj[k];
+    av_out[k] = av[k];
   }
 }
 
@@ -287,10 +294,13 @@ int spmv_coo_to_csr(int dtype, int64_t nrows, int64_t nnz, const uint32_t* ai, c
     SPMV_CUDA_TRY(cudaMemsetAsync(irp, 0, sizeof(uint32_t) * (nrows + 1), st));
     return SPMV_OK;
   }
-  coo_irp_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, nnz, nrows, irp);
+  if (dtype == SPMV_F64)
+    coo_to_csr_kernel<double><<<unsigned(grid_for(nnz)), 256, 0, st>>>(
+        ai, aj, static_cast<const double*>(av), nnz, nrows, irp, aj_out, static_cast<double*>(av_out));
+  else
+    coo_to_csr_kernel<float><<<unsigned(grid_for(nnz)), 256, 0, st>>>(
+        ai, aj, static_cast<const float*>(av), nnz, nrows, irp, aj_out, static_cast<float*>(av_out));
   SPMV_LAUNCH_CHECK();
-  SPMV_CUDA_TRY(cudaMemcpyAsync(aj_out, aj, 4 * nnz, cudaMemcpyDeviceToDevice, st));
-  SPMV_CUDA_TRY(cudaMemcpyAsync(av_out, av, value_size(dtype) * nnz, cudaMemcpyDeviceToDevice, st));
   return SPMV_OK;
 }
 

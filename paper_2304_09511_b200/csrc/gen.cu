@@ -28,52 +28,61 @@ __host__ __device__ inline int64_t stencil_irp(int64_t nx, int64_t ny, int64_t n
          axis_count(nz, z) * axis_count(ny, y) * axis_prefix(nx, x);
 }
 
-// Entry-parallel fill: a block stages the row pointers and (x, y, z) of
-// kGenRows rows in shared memory; every thread then takes entries of the
-// block's range, finds its row by binary search and decodes the entry's
-// neighbour from the per-axis counts (dz outer, dx inner = ascending columns),
-// so the column and value streams are written coalesced.
-constexpr int kGenRows = 256;
+// Staged fill: a block of kGenRows threads builds kGenRows consecutive rows,
+// one row per thread, into shared memory (row r's entries at its closed-form
+// offset; the stride-27 stores are bank-conflict free), then copies the
+// block's contiguous entry range out with coalesced stores.  Columns ascend
+// within a row (dz outer, dx inner), as in matrixio.py:196-205.
+constexpr int kGenRows = 128;
+constexpr int kGenMaxEntries = 27 * kGenRows;
 
 template <typename T>
-__global__ void __launch_bounds__(256) stencil27_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_begin,
-                                                        int64_t row_end, uint32_t* __restrict__ irp,
-                                                        uint32_t* __restrict__ aj, T* __restrict__ av) {
-  __shared__ uint32_t s_o[kGenRows + 1];
-  __shared__ uint32_t s_x[kGenRows], s_y[kGenRows], s_z[kGenRows];
+__global__ void __launch_bounds__(kGenRows) stencil27_kernel(int64_t nx, int64_t ny, int64_t nz, int64_t row_begin,
+                                                             int64_t row_end, uint32_t* __restrict__ irp,
+                                                             uint32_t* __restrict__ aj, T* __restrict__ av) {
+  __shared__ uint32_t s_aj[kGenMaxEntries];
+  __shared__ T s_av[kGenMaxEntries];
+  __shared__ uint32_t s_span[2];
   const int64_t nloc = row_end - row_begin;
   const int64_t base = stencil_irp(nx, ny, nz, row_begin);
+  const int tid = threadIdx.x;
   for (int64_t r0 = int64_t(blockIdx.x) * kGenRows; r0 <= nloc; r0 += int64_t(gridDim.x) * kGenRows) {
     const int nr = int(min(int64_t(kGenRows), nloc - r0));
-    for (int i = threadIdx.x; i <= nr; i += blockDim.x) {
-      const int64_t p = row_begin + r0 + i;
+    if (tid == 0) {
+      s_span[0] = uint32_t(stencil_irp(nx, ny, nz, row_begin + r0) - base);
+      s_span[1] = uint32_t(stencil_irp(nx, ny, nz, row_begin + r0 + nr) - base);
+      if (r0 + nr == nloc) irp[nloc] = s_span[1];
+    }
+    __syncthreads();
+    const uint32_t e0 = s_span[0];
+    if (tid < nr) {
+      const int64_t p = row_begin + r0 + tid;
       const uint32_t o = uint32_t(stencil_irp(nx, ny, nz, p) - base);
-      s_o[i] = o;
-      if (i < nr || r0 + nr == nloc) irp[r0 + i] = o;  // irp[r0 + nr] belongs to the next block
-      if (i < nr) {
-        const uint32_t q = uint32_t(p), ux = uint32_t(nx), uy = uint32_t(ny);
-        s_x[i] = q % ux;
-        s_y[i] = (q / ux) % uy;
-        s_z[i] = q / (ux * uy);
+      irp[r0 + tid] = o;
+      const uint32_t q = uint32_t(p), ux = uint32_t(nx), uy = uint32_t(ny);
+      const int64_t x = q % ux, y = (q / ux) % uy, z = q / (ux * uy);
+      uint32_t k = o - e0;
+      for (int dz = -1; dz <= 1; ++dz) {
+        const int64_t qz = z + dz;
+        if (qz < 0 || qz >= nz) continue;
+        for (int dy = -1; dy <= 1; ++dy) {
+          const int64_t qy = y + dy;
+          if (qy < 0 || qy >= ny) continue;
+          for (int dx = -1; dx <= 1; ++dx) {
+            const int64_t qx = x + dx;
+            if (qx < 0 || qx >= nx) continue;
+            s_aj[k] = uint32_t((qz * ny + qy) * nx + qx);
+            s_av[k] = (dx == 0 && dy == 0 && dz == 0) ? T(26.0) : T(-1.0);
+            ++k;
+          }
+        }
       }
     }
     __syncthreads();
-    const uint32_t e0 = s_o[0], e1 = s_o[nr];
-    for (uint32_t e = e0 + threadIdx.x; e < e1; e += blockDim.x) {
-      int lo = 0, hi = nr - 1;  // last local row with s_o[row] <= e
-      while (lo < hi) {
-        const int mid = (lo + hi + 1) >> 1;
-        if (s_o[mid] <= e) lo = mid; else hi = mid - 1;
-      }
-      const uint32_t j = e - s_o[lo];
-      const int64_t x = s_x[lo], y = s_y[lo], z = s_z[lo];
-      const uint32_t cx = uint32_t(axis_count(nx, x)), cy = uint32_t(axis_count(ny, y));
-      const uint32_t jx = j % cx, t = j / cx, jy = t % cy, jz = t / cy;
-      const int64_t dx = int64_t(jx) - (nx == 1 || x == 0 ? 0 : 1);
-      const int64_t dy = int64_t(jy) - (ny == 1 || y == 0 ? 0 : 1);
-      const int64_t dz = int64_t(jz) - (nz == 1 || z == 0 ? 0 : 1);
-      aj[e] = uint32_t(((z + dz) * ny + (y + dy)) * nx + (x + dx));
-      av[e] = (dx == 0 && dy == 0 && dz == 0) ? T(26.0) : T(-1.0);
+    const uint32_t cnt = s_span[1] - e0;
+    for (uint32_t k = tid; k < cnt; k += kGenRows) {
+      aj[e0 + k] = s_aj[k];
+      av[e0 + k] = s_av[k];
     }
     __syncthreads();
   }
@@ -108,13 +117,13 @@ int spmv_stencil27_fill(int dtype, int64_t nx, int64_t ny, int64_t nz, int64_t r
   cudaStream_t st = as_stream(stream);
   const int64_t work = row_end - row_begin + 1;
   int64_t grid = (work + kGenRows - 1) / kGenRows;
-  const int64_t cap = int64_t(sm_count()) * 8;
+  const int64_t cap = int64_t(sm_count()) * 16;
   if (grid > cap) grid = cap;
   if (dtype == SPMV_F64)
-    stencil27_kernel<double><<<unsigned(grid), 256, 0, st>>>(nx, ny, nz, row_begin, row_end, irp, aj,
+    stencil27_kernel<double><<<unsigned(grid), kGenRows, 0, st>>>(nx, ny, nz, row_begin, row_end, irp, aj,
                                                               static_cast<double*>(av));
   else
-    stencil27_kernel<float><<<unsigned(grid), 256, 0, st>>>(nx, ny, nz, row_begin, row_end, irp, aj,
+    stencil27_kernel<float><<<unsigned(grid), kGenRows, 0, st>>>(nx, ny, nz, row_begin, row_end, irp, aj,
                                                              static_cast<float*>(av));
   SPMV_LAUNCH_CHECK();
   return SPMV_OK;
