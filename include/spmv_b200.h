@@ -114,7 +114,9 @@ int spmv_csr_range(const spmv_csr_plan* plan, const uint32_t* row_pointers,
  * downloaded on a second copy stream while later tiles run (PCIe is full
  * duplex).  Device staging lives in the plan (not reentrant per plan).
  * Asynchronous: y_host is valid once `stream` is synchronised.
- * chunks <= 0 selects the default (48). */
+ * x goes up in chunks that ramp up to ncols / chunks columns (at least 1M)
+ * and down again at the end; each tile range runs once the x it reads has
+ * arrived.  chunks <= 0 selects the default (16). */
 int spmv_csr_host(spmv_csr_plan* plan, const uint32_t* row_pointers,
                   const uint32_t* col_indices, const void* values,
                   const void* x_host, void* y_host, int chunks, void* stream);

@@ -23,6 +23,7 @@
 // overlap that hits L2), the row pointers once, x through L2, y written
 // once: the minimum-byte model of SURVEY.md §8(d).
 #include <algorithm>
+#include <cstdlib>
 #include <vector>
 
 #include "tile.cuh"
@@ -614,52 +615,130 @@ static int csr_host_prepare(spmv_csr_plan* p, const uint32_t* aj, int chunks, cu
   return SPMV_OK;
 }
 
+// SPMV_HOST_TRACE=1: timing events after every H2D chunk, tile range and
+// D2H copy of spmv_csr_host, printed to stderr (pipeline tuning only).
+struct HostTrace {
+  bool on = false;
+  int flags = 0;  // SPMV_HOST_TRACE value - 1: bit 0 skips compute, bit 1 skips D2H
+  cudaEvent_t t0 = nullptr;
+  std::vector<std::pair<char, cudaEvent_t>> marks;
+  void begin(cudaStream_t s) {
+    static const int level = [] {
+      const char* v = getenv("SPMV_HOST_TRACE");
+      return v && *v ? atoi(v) : 0;
+    }();
+    on = level > 0;
+    flags = level > 0 ? level - 1 : 0;
+    if (!on) return;
+    cudaEventCreate(&t0);
+    cudaEventRecord(t0, s);
+  }
+  void mark(char kind, cudaStream_t s) {
+    if (!on) return;
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    cudaEventRecord(e, s);
+    marks.emplace_back(kind, e);
+  }
+  void dump(cudaStream_t s) {
+    if (!on) return;
+    cudaStreamSynchronize(s);
+    cudaDeviceSynchronize();
+    fprintf(stderr, "host-trace");
+    for (auto& m : marks) {
+      float ms = 0;
+      cudaEventElapsedTime(&ms, t0, m.second);
+      fprintf(stderr, " %c%.3f", m.first, ms);
+      cudaEventDestroy(m.second);
+    }
+    fprintf(stderr, "\n");
+    cudaEventDestroy(t0);
+    marks.clear();
+  }
+};
+
 template <typename T>
 static int csr_host_run(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* xh, T* yh,
                         int chunks, cudaStream_t st) {
   int rc = csr_host_prepare(p, aj, chunks, st);
   if (rc) return rc;
+  HostTrace tr;
   T* xd = p->xd.as<T>();
   T* yd = p->yd.as<T>();
-  cudaEvent_t* ev = p->events.data();  // [0..chunks): x chunks, [chunks..2chunks): tiles, 2chunks: start, +1: end
-  SPMV_CUDA_TRY(cudaEventRecord(ev[2 * chunks], st));
-  SPMV_CUDA_TRY(cudaStreamWaitEvent(p->h2d, ev[2 * chunks], 0));
-  SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[2 * chunks], 0));
-  std::vector<int64_t> xb(chunks + 1);
-  for (int j = 0; j <= chunks; ++j) xb[j] = p->ncols * j / chunks;
-  for (int j = 0; j < chunks; ++j) {
+  // x schedule: copies below ~8 MB lose PCIe bandwidth when both directions
+  // run, but the first y rows can only leave once their x has arrived.  So
+  // the chunks ramp up (1/16 .. 1/2 of a full chunk) to start the D2H stream
+  // early, run at full size (ncols / chunks) in the middle, and ramp down at
+  // the end so that little y is left to copy after the last tile range.
+  std::vector<int64_t> xb{0};
+  {
+    const int64_t n = p->ncols;
+    const int64_t big = std::max<int64_t>(std::max<int64_t>(1, n / chunks), std::min<int64_t>(n, int64_t(1) << 20));
+    std::vector<int64_t> ramp;
+    for (int sh = 4; sh >= 1; --sh)
+      if ((big >> sh) >= 4096) ramp.push_back(big >> sh);
+    int64_t ramp_total = 0;
+    for (int64_t r : ramp) ramp_total += 2 * r;
+    if (2 * ramp_total > n) ramp.clear(), ramp_total = 0;
+    for (int64_t r : ramp) xb.push_back(xb.back() + r);
+    const int64_t mid = n - ramp_total, nmid = std::max<int64_t>(1, (mid + big / 2) / big);
+    const int64_t m0 = xb.back();
+    for (int64_t j = 1; j <= nmid; ++j) xb.push_back(m0 + mid * j / nmid);
+    for (auto it = ramp.rbegin(); it != ramp.rend(); ++it) xb.push_back(xb.back() + *it);
+    xb.back() = n;
+  }
+  const int nx = int(xb.size()) - 1;
+  while (int(p->events.size()) < 2 * nx + 2) {
+    cudaEvent_t e;
+    SPMV_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+    p->events.push_back(e);
+  }
+  cudaEvent_t* ev = p->events.data();  // [0, nx): x chunks, [nx, 2nx): tile ranges, 2nx: start, 2nx+1: end
+  SPMV_CUDA_TRY(cudaEventRecord(ev[2 * nx], st));
+  tr.begin(st);
+  SPMV_CUDA_TRY(cudaStreamWaitEvent(p->h2d, ev[2 * nx], 0));
+  SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[2 * nx], 0));
+  for (int j = 0; j < nx; ++j) {
     if (xb[j + 1] > xb[j])
       SPMV_CUDA_TRY(cudaMemcpyAsync(xd + xb[j], xh + xb[j], sizeof(T) * (xb[j + 1] - xb[j]), cudaMemcpyHostToDevice,
                                     p->h2d));
     SPMV_CUDA_TRY(cudaEventRecord(ev[j], p->h2d));
+    tr.mark('h', p->h2d);
   }
+  // After x chunk j has landed, run every tile whose columns are all below
+  // xb[j + 1] (h_maxcol_prefix is non-decreasing), then copy its rows of y.
   const bool spans = p->n_span > 0;  // y final only after the fix-up
-  int64_t done = 0;
-  int xj = 0;
-  for (int k = 0; k < chunks; ++k) {
-    const int64_t tb = p->ntiles * k / chunks, te = p->ntiles * (k + 1) / chunks;
+  int64_t done = 0, tb = 0;
+  for (int j = 0; j < nx && tb < p->ntiles; ++j) {
+    int64_t te = j == nx - 1 ? p->ntiles
+                             : int64_t(std::lower_bound(p->h_maxcol_prefix.begin(), p->h_maxcol_prefix.end(),
+                                                        xb[j + 1]) - p->h_maxcol_prefix.begin());
     if (te <= tb) continue;
-    const int64_t col_hi = p->h_maxcol_prefix[te - 1];
-    while (xj + 1 < chunks && xb[xj + 1] <= col_hi) ++xj;
-    SPMV_CUDA_TRY(cudaStreamWaitEvent(st, ev[xj], 0));
-    if ((rc = csr_run<T>(p, irp, aj, av, xd, 0, yd, st, tb, te, k == chunks - 1))) return rc;
+    SPMV_CUDA_TRY(cudaStreamWaitEvent(st, ev[j], 0));
+    if (!(tr.on && tr.flags & 1))  // trace flag 1: skip the compute (pipeline analysis)
+      if ((rc = csr_run<T>(p, irp, aj, av, xd, 0, yd, st, tb, te, te == p->ntiles))) return rc;
+    tr.mark('k', st);
     const int64_t rows_done = te < p->ntiles ? int64_t(p->h_row_lo[te]) : p->nrows;
-    if (!spans && rows_done > done) {
-      SPMV_CUDA_TRY(cudaEventRecord(ev[chunks + k], st));
-      SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[chunks + k], 0));
+    if (!spans && rows_done > done && !(tr.on && tr.flags & 2)) {  // flag 2: no D2H
+      SPMV_CUDA_TRY(cudaEventRecord(ev[nx + j], st));
+      SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[nx + j], 0));
       SPMV_CUDA_TRY(cudaMemcpyAsync(yh + done, yd + done, sizeof(T) * (rows_done - done), cudaMemcpyDeviceToHost,
                                     p->d2h));
+      tr.mark('d', p->d2h);
       done = rows_done;
     }
+    tb = te;
   }
   if (done < p->nrows) {
-    SPMV_CUDA_TRY(cudaEventRecord(ev[2 * chunks - 1], st));
-    SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[2 * chunks - 1], 0));
+    SPMV_CUDA_TRY(cudaEventRecord(ev[2 * nx - 1], st));
+    SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[2 * nx - 1], 0));
     SPMV_CUDA_TRY(cudaMemcpyAsync(yh + done, yd + done, sizeof(T) * (p->nrows - done), cudaMemcpyDeviceToHost,
                                   p->d2h));
   }
-  SPMV_CUDA_TRY(cudaEventRecord(ev[2 * chunks + 1], p->d2h));
-  SPMV_CUDA_TRY(cudaStreamWaitEvent(st, ev[2 * chunks + 1], 0));
+  SPMV_CUDA_TRY(cudaEventRecord(ev[2 * nx + 1], p->d2h));
+  SPMV_CUDA_TRY(cudaStreamWaitEvent(st, ev[2 * nx + 1], 0));
+  tr.mark('e', st);
+  tr.dump(st);
   return SPMV_OK;
 }
 
@@ -682,7 +761,6 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
   SPMV_LAUNCH_CHECK();
   if ((rc = count_async(ctr, &h, st))) return rc;
   p->n_long = int64_t(h);
-  // Long rows leave gathers to the warps: smaller tiles keep more CTAs per SM.
   // Long rows: 1024-entry tiles, one group (more CTAs hide the long-row
   // gathers).  Otherwise 2048-entry tiles with G consumer groups sharing a
   // G + 1 stage ring: 3 groups (2 CTAs/SM) for stencil-like rows, 7 groups
@@ -851,7 +929,7 @@ int spmv_csr_host(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, con
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (!x_host || !y_host) return fail(SPMV_INVALID_ARG, "NULL host buffer");
   if (p->nrows == 0 || p->nnz == 0) return fail(SPMV_INVALID_ARG, "host pipeline needs a non-empty matrix");
-  if (chunks <= 0) chunks = 48;
+  if (chunks <= 0) chunks = 16;
   if (chunks > 1024) chunks = 1024;
   if (chunks > p->ntiles) chunks = int(p->ntiles);
   cudaStream_t st = as_stream(stream);
