@@ -27,6 +27,7 @@ from .errors import (
     AllCandidatesFailed,
     EmptyInput,
     IndexOverflow,
+    MissingBaseline,
     ParseError,
     SparseError,
     UnsupportedField,
@@ -56,8 +57,19 @@ from .kernels import (
     spmv_dia_vla,
 )
 from .lanes import LaneConfig
-from .matrixio import gen_stencil27, gen_stencil27_rows, read_matrix_market, write_matrix_market
+from .matrixio import (
+    CorpusEntry,
+    gen_banded,
+    gen_random_sparse,
+    gen_stencil27,
+    gen_stencil27_rows,
+    load_entry,
+    load_manifest,
+    read_matrix_market,
+    write_matrix_market,
+)
 from .cg import CgState, cg_solve
 from .autotune import Measurement, TuneChoice, distribution_report, measure, tune
+from .sweep import BenchRecord, compare_records, make_report, read_records, render_report, run_corpus, write_records
 
 __version__ = "0.1.0"

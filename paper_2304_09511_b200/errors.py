@@ -51,3 +51,7 @@ class ParseError(SparseError):
 
 class UnsupportedField(SparseError):
     """Matrix Market field or symmetry this reader does not support (errors.py:32)."""
+
+
+class MissingBaseline(SparseError):
+    """Report input lacks the baseline pair for a matrix (errors.py:48-49)."""

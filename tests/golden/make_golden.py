@@ -20,6 +20,8 @@ Files written:
   stencil.npz     gen_stencil27 on small grids
   cg.npz          hpcg.cg_solve: iterations, residual histories, solutions
   mm.npz          read_matrix_market on small hand-written files
+  sweep.npz       bench.py CSV records and reports, corpus manifest parsing,
+                  gen_banded / gen_random_sparse generator specs
 """
 
 from __future__ import annotations
@@ -292,8 +294,76 @@ def make_cg() -> None:
     np.savez_compressed(OUT / "cg.npz", **d)
 
 
+SWEEP_MANIFEST = ("# corpus\n"
+                  "canon\tgeneral.mtx\n"
+                  "cube  stencil27:2,2,3\n"
+                  "\n"
+                  "band\tbanded:12,-2,0,1\n"
+                  "rnd\trandom:20,0.1,5\n")
+
+
+def _sweep_records():
+    from spmvkit.bench import BenchRecord
+    from spmvkit.kernels import KernelVersion as V
+    C, O, D = Format.CSR, Format.COO, Format.DIA
+    P, L = V.PLAIN, V.VLA
+
+    def rec(mid, fmt, ver, median, nnz=10, status="ok"):
+        return BenchRecord(mid, 4, 4, nnz, fmt, ver, 100, 10, median if status == "ok" else None,
+                           (2.0 * nnz * 100 / median / 1e9) if status == "ok" else None, None, status)
+
+    return {
+        "basic": [rec("m1", C, P, 2e-3), rec("m1", O, P, 1e-3), rec("m2", C, P, 2e-3), rec("m2", O, P, 4e-3),
+                  rec("m2", D, P, None, status="fill_exceeded")],
+        "mixed": [rec("a", C, P, 3.25e-4, nnz=27), rec("a", O, P, 2.5e-4, nnz=27), rec("a", D, P, 1.5e-4, nnz=27),
+                  rec("a", C, L, 9e-4, nnz=27), rec("a", O, L, 8e-4, nnz=27), rec("a", D, L, 7e-4, nnz=27),
+                  rec("b", C, P, 1e-3, nnz=5), rec("b", O, P, 1e-3, nnz=5),
+                  rec("b", D, P, None, nnz=5, status="unsupported"),
+                  rec("b", C, L, 2e-3, nnz=5), rec("gone", None, None, None, status="error")],
+        "missing_pair": [rec("m1", C, P, 2e-3), rec("m1", O, P, 1e-3), rec("m2", C, P, 2e-3)],
+    }
+
+
+def make_sweep() -> None:
+    """bench.py records, CSV text and reports; matrixio manifest and
+    generator specs."""
+    import io
+
+    from spmvkit.bench import make_report, render_report, write_records
+    from spmvkit.kernels import KernelVersion as V
+    from spmvkit.matrixio import gen_banded, gen_random_sparse, load_manifest
+    d: dict = {}
+    for name, records in _sweep_records().items():
+        buf = io.StringIO()
+        write_records(records, buf)
+        d[f"records/{name}/csv"] = np.array(buf.getvalue())
+        for bname, base in (("csr_plain", (Format.CSR, V.PLAIN)), ("coo_vla", (Format.COO, V.VLA))):
+            try:
+                d[f"records/{name}/report_{bname}"] = np.array(render_report(make_report(records, base)))
+            except Exception as exc:  # MissingBaseline / EmptyInput
+                d[f"records/{name}/report_{bname}"] = np.array(f"raises {type(exc).__name__}")
+    d["records/names"] = np.array(list(_sweep_records()))
+    import tempfile
+    with tempfile.TemporaryDirectory() as tmp:
+        mf = Path(tmp) / "m.txt"
+        mf.write_text(SWEEP_MANIFEST)
+        ents = load_manifest(mf)
+    d["manifest/text"] = np.array(SWEEP_MANIFEST)
+    d["manifest/ids"] = np.array([e.id for e in ents])
+    d["manifest/sources"] = np.array([e.source for e in ents])
+    for key, (n, offs) in {"b12": (12, (-2, 0, 1)), "b9": (9, (3, -4, 0, 3)), "b1": (1, (0,))}.items():
+        put_matrix(d, f"banded/{key}", gen_banded(n, offs))
+        d[f"banded/{key}/spec"] = np.array([n, *offs], dtype=np.int64)
+    for key, (nr, nc, dens, seed) in {"r20": (20, 20, 0.1, 5), "r7x13": (7, 13, 0.3, 11),
+                                      "r0": (6, 6, 0.0, 1)}.items():
+        put_matrix(d, f"random/{key}", gen_random_sparse(nr, nc, dens, seed))
+        d[f"random/{key}/spec"] = np.array([nr, nc, dens, seed], dtype=np.float64)
+    np.savez_compressed(OUT / "sweep.npz", **d)
+
+
 if __name__ == "__main__":
     os.environ.setdefault("PYTHONDONTWRITEBYTECODE", "1")
+    make_sweep()
     make_mm()
     make_cg()
     make_canonical()
