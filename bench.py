@@ -357,6 +357,23 @@ def run_ours(args, torch, dist, rank, world, local_rank):
         results[fmt] = {"gflops": round(2.0 * m.nnz / t / 1e9, 2), "ms_per_spmv": round(t * 1e3, 4),
                         "gbs": round(b / t / 1e9, 1), "bytes_per_spmv": b, "launches": launches_per_spmv(sp, m),
                         "plan": plan_of(sp, m), "roofline_frac": round(b / t / 1e9 / pk["hbm_gbs"], 4), "nnz": m.nnz}
+    vla_results = {}
+    if not args.no_extras:
+        # the vla kernels (kernels.py:104-210) at the reference's default lane count
+        cfg_l = sp.LaneConfig()
+        for fmt, m in mats.items():
+            if fmt not in ("csr", "coo", "dia"):
+                continue
+            fn_ = {"csr": sp.spmv_csr_vla, "coo": sp.spmv_coo_vla, "dia": sp.spmv_dia_vla}[fmt]
+            y = torch.empty(m.nrows, dtype=m.values.dtype, device=device)
+            fn = lambda: fn_(m, x, cfg_l, out=y)  # noqa: E731
+            fn()
+            torch.cuda.synchronize()
+            t = time_steps(torch, fn, max(10, args.steps // 4), args.warmup, flush)
+            b = bytes_of(m, fmt)
+            vla_results[fmt] = {"lanes": cfg_l.lanes, "gflops": round(2.0 * m.nnz / t / 1e9, 2),
+                                "ms_per_spmv": round(t * 1e3, 4), "gbs": round(b / t / 1e9, 1),
+                                "roofline_frac": round(b / t / 1e9 / pk["hbm_gbs"], 4)}
     m = mats[head]
     t = results[head]["ms_per_spmv"] / 1e3
     line = {
@@ -372,6 +389,8 @@ def run_ours(args, torch, dist, rank, world, local_rank):
         "clocks": clocks,
         "per_format": results,
     }
+    if vla_results:
+        line["per_format_vla"] = vla_results
     if not args.no_extras:
         line["e2e"] = e2e_measure(args, torch, sp, m, x, head)
         if "csr" in mats and "dia" in mats:  # Zipf has no DIA form (fill ratio)
