@@ -400,15 +400,25 @@ coo_vla_warp_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __re
     const uint32_t nsteps = (b - a + uint32_t(lanes) - 1) / uint32_t(lanes);
     unsigned max_steps = __reduce_max_sync(0xffffffffu, nsteps);
     T yv = T(0);
-    for (uint32_t st = 0; st < max_steps; ++st) {
-      const uint32_t c0 = a + st * uint32_t(lanes);
-      T p = T(0);
-      if (st < nsteps && lane < lanes && c0 + lane < b) {
-        const uint32_t j = c0 + lane;
-        p = mul_rn(ld_stream(av + j), ldx(xb + ld_stream(aj + j)));
+    // Four steps' products are loaded before their trees run (in step
+    // order), so a short run costs one gather round trip.
+    for (uint32_t st0 = 0; st0 < max_steps; st0 += 4) {
+      T p[4];
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t st = st0 + uint32_t(k);
+        const uint32_t j = a + st * uint32_t(lanes) + uint32_t(lane);
+        p[k] = (st < nsteps && lane < lanes && j < b) ? mul_rn(ld_stream(av + j), ldx(xb + ld_stream(aj + j)))
+                                                      : T(0);
       }
-      p = tree_reduce_warp(p, width);
-      if (st < nsteps) yv = add_rn(yv, p);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) {
+        const uint32_t st = st0 + uint32_t(k);
+        if (st < max_steps) {  // warp-uniform: every lane joins the shuffles
+          const T q = tree_reduce_warp(p[k], width);
+          if (st < nsteps) yv = add_rn(yv, q);
+        }
+      }
     }
     if (lane == 0 && ri < n_runs) {
       y[row] = yv;

@@ -413,9 +413,23 @@ csr_vla_warp_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict
       e = irp[r + 1];
     }
     T acc = T(0);
-    if (lane < lanes)
-      for (uint32_t j = s + lane; j < e; j += uint32_t(lanes))
-        acc = add_rn(acc, mul_rn(ld_stream(av + j), ldx(xb + ld_stream(aj + j))));
+    if (lane < lanes) {
+      // The lane's entries j, j+L, j+2L, j+3L are loaded as one predicated
+      // batch and added in that order (skipped slots add nothing), so a
+      // short row costs one gather round trip instead of one per entry.
+      const uint32_t L = uint32_t(lanes);
+      for (uint32_t j = s + lane; j < e; j += 4 * L) {
+        T p[4];
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const uint32_t jj = j + uint32_t(k) * L;
+          p[k] = jj < e ? mul_rn(ld_stream(av + jj), ldx(xb + ld_stream(aj + jj))) : T(0);
+        }
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+          if (j + uint32_t(k) * L < e) acc = add_rn(acc, p[k]);
+      }
+    }
     acc = tree_reduce_warp(acc, width);
     if (lane == 0 && r < nrows) y[r] = (s == e) ? T(0) : acc;
   }
