@@ -193,14 +193,19 @@ __device__ __forceinline__ void reduce_long_segments(const uint32_t* __restrict_
     if (products) {
       for (; j < uhi; j += 32) acc = add_rn(acc, vals[j]);
     } else {
-      for (; j + 96 < uhi; j += 128) {  // 4 gathers in flight per lane, adds in order
-        const T p0 = mul_rn(vals[j], ldx(xb + cols[j]));
-        const T p1 = mul_rn(vals[j + 32], ldx(xb + cols[j + 32]));
-        const T p2 = mul_rn(vals[j + 64], ldx(xb + cols[j + 64]));
-        const T p3 = mul_rn(vals[j + 96], ldx(xb + cols[j + 96]));
-        acc = add_rn(add_rn(add_rn(add_rn(acc, p0), p1), p2), p3);
+      // A unit is at most kUnit / 32 = 8 entries per lane: all of them are
+      // gathered at once (predicated), then added in lane order, so a unit
+      // costs one L2 round trip whatever its length.
+      constexpr int PER_LANE = kUnit / 32;
+      T p[PER_LANE];
+#pragma unroll
+      for (int k = 0; k < PER_LANE; ++k) {
+        const uint32_t jk = j + 32u * uint32_t(k);
+        p[k] = jk < uhi ? mul_rn(vals[jk], ldx(xb + cols[jk])) : T(0);
       }
-      for (; j < uhi; j += 32) acc = add_rn(acc, mul_rn(vals[j], ldx(xb + cols[j])));
+#pragma unroll
+      for (int k = 0; k < PER_LANE; ++k)
+        if (j + 32u * uint32_t(k) < uhi) acc = add_rn(acc, p[k]);
     }
     acc = tree_reduce_warp(acc, 32);
     if (lane == 0) unit_part[u] = acc;
