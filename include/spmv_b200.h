@@ -61,7 +61,7 @@ typedef struct spmv_csr_plan spmv_csr_plan;
 /* Analyse the matrix once: long-row census (rows > exact_len entries), tile
  * size (2048 entries, 1024 when long rows exist), consumer groups per CTA
  * (G groups share a G+1 stage ring: 3, or 7 for rows averaging < 16
- * entries, 1 with long rows), the row range of every tile and the list of
+ * entries), the row range of every tile and the list of
  * long rows spanning tiles.  The SpMV kernel streams
  * fixed entry tiles with TMA bulk copies; rows of <= exact_len entries are
  * summed left to right by one thread (bit-exact with spmv_csr_plain); longer

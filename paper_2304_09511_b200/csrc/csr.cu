@@ -495,7 +495,7 @@ struct spmv_csr_plan {
 
 // (tile, groups) pairs with compiled kernels.
 #define SPMV_CSR_CONFIGS(X) \
-  X(1024, 1) X(2048, 1) X(4096, 1) X(1920, 1) X(1920, 2) X(2048, 3) X(2048, 7) X(1792, 7)
+  X(1024, 1) X(2048, 1) X(4096, 1) X(1920, 1) X(1920, 2) X(2048, 3) X(2048, 7) X(1792, 7) X(1024, 3)
 static bool csr_config_known(int64_t tile, int groups) {
 #define X(TL, GR) if (tile == TL && groups == GR) return true;
   SPMV_CSR_CONFIGS(X)
@@ -775,14 +775,14 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
   SPMV_LAUNCH_CHECK();
   if ((rc = count_async(ctr, &h, st))) return rc;
   p->n_long = int64_t(h);
-  // Long rows: 1024-entry tiles, one group (more CTAs hide the long-row
-  // gathers).  Otherwise 2048-entry tiles with G consumer groups sharing a
+  // Long rows: 1024-entry tiles, 3 groups (2 CTAs/SM: six tiles in flight
+  // hide the long-row gathers).  Otherwise 2048-entry tiles with G consumer groups sharing a
   // G + 1 stage ring: 3 groups (2 CTAs/SM) for stencil-like rows, 7 groups
   // (1 CTA/SM) for short rows (average < 16 entries), measured best on the
   // 27-point stencil and the 11-diagonal banded matrix respectively.
   if (p->n_long > 0) {
     p->tile = 1024;
-    p->groups = 1;
+    p->groups = 3;  // Zipf: 269 -> 276 GFLOP/s over one group (long-row phases overlap other groups' rows)
   } else {
     p->tile = 2048;
     p->groups = p->nnz < 16 * p->nrows ? 7 : 3;
