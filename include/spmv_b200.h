@@ -128,6 +128,13 @@ int spmv_csr_vla(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
                  const uint32_t* row_pointers, const uint32_t* col_indices,
                  const void* values, const void* x, int64_t col_base,
                  int64_t x_len, void* y, int lanes, void* stream);
+/* Same, with the CSR plan of the matrix: its long-row census lets the call
+ * skip the long-row pass (rows over 256 entries get a warp each) when no
+ * row can need it. */
+int spmv_csr_vla_planned(const spmv_csr_plan* plan, const uint32_t* row_pointers,
+                         const uint32_t* col_indices, const void* values,
+                         const void* x, int64_t col_base, int64_t x_len, void* y,
+                         int lanes, void* stream);
 
 /* ---- COO (kernels.py:56-66 spmv_coo_plain, :104-140 spmv_coo_vla) ------ */
 typedef struct spmv_coo_plan spmv_coo_plan;

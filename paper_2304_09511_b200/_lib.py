@@ -63,6 +63,7 @@ SIGNATURES = {
     "spmv_csr_plan_tile_info": [_vp, _vp, _vp, _vp, _vp],
     "spmv_csr_range": [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _c_int, _vp],
     "spmv_csr_vla": [_c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _c_int, _vp],
+    "spmv_csr_vla_planned": [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _c_int, _vp],
     "spmv_coo_plan_create": [_c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _pvp],
     "spmv_coo_plan_destroy": [_vp],
     "spmv_coo_plan_info": [_vp, _pi64, _pi64, _pi64, _pint, _pi64],

@@ -26,6 +26,7 @@
 #include <cub/cub.cuh>
 
 #include <algorithm>
+#include <type_traits>
 
 #include "tile.cuh"
 
@@ -377,7 +378,70 @@ __global__ void run_scatter_kernel(const uint32_t* __restrict__ ai, int64_t nnz,
 }
 
 // ---- vla: L-entry steps per run, tree per step ----------------------------
+// Runs longer than kVlaLong entries go to coo_vla_long_kernel (L <= 32).
+constexpr uint32_t kVlaLong = 256;
+
+// One warp per long run.  Sub-groups of W = next_pow2(L) lanes take one
+// step each (lane l < L: entry a + step*L + l), eight sub-passes of loads
+// in flight per lane; each step's tree runs in its sub-group and the step
+// sums are folded into the run's y value in step order (kernels.py:129-137),
+// so the result equals the sub-warp kernel's bit for bit.
 template <typename T>
+__global__ void __launch_bounds__(256)
+coo_vla_long_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __restrict__ run_row, int64_t n_runs,
+                    const uint32_t* __restrict__ aj, const T* __restrict__ av, const T* __restrict__ x,
+                    int64_t col_base, T* __restrict__ y, int lanes, int width,
+                    unsigned long long* __restrict__ steps_out) {
+  constexpr int U = 8;
+  const T* xb = x - col_base;
+  const int lane = threadIdx.x & 31;
+  const int W = width, G = 32 / width;  // steps per sub-pass
+  const int sub = lane / W, l = lane % W;
+  const uint32_t L = uint32_t(lanes);
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long my_steps = 0;
+  for (int64_t r0 = warp * 32; r0 < n_runs; r0 += nwarps * 32) {
+    const int64_t rl = r0 + lane;
+    const uint32_t al = rl < n_runs ? run_start[rl] : 0u, bl = rl < n_runs ? run_start[rl + 1] : 0u;
+    unsigned long_runs = __ballot_sync(0xffffffffu, bl - al > kVlaLong);
+    while (long_runs) {
+      const int k = __ffs(long_runs) - 1;
+      long_runs &= long_runs - 1;
+      const uint32_t a = __shfl_sync(0xffffffffu, al, k), b = __shfl_sync(0xffffffffu, bl, k);
+      const uint32_t nsteps = (b - a + L - 1) / L;
+      T yv = T(0);
+      for (uint32_t st0 = 0; st0 < nsteps; st0 += uint32_t(U * G)) {
+        T p[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const uint32_t step = st0 + uint32_t(u * G + sub);
+          const uint32_t j = a + step * L + uint32_t(l);
+          p[u] = (uint32_t(l) < L && step < nsteps && j < b) ? mul_rn(ld_stream(av + j), ldx(xb + ld_stream(aj + j)))
+                                                            : T(0);
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const T q = tree_reduce_warp(p[u], W);  // lane g*W: sum of step st0 + u*G + g
+          for (int g = 0; g < G; ++g) {
+            const T v = __shfl_sync(0xffffffffu, q, g * W);
+            if (st0 + uint32_t(u * G + g) < nsteps) yv = add_rn(yv, v);
+          }
+        }
+      }
+      if (lane == 0) {
+        y[run_row[r0 + k]] = yv;
+        my_steps += nsteps;
+      }
+    }
+  }
+  if (steps_out) {
+    for (int o = 16; o >= 1; o >>= 1) my_steps += __shfl_down_sync(0xffffffffu, my_steps, o);
+    if (lane == 0 && my_steps) atomicAdd(steps_out, my_steps);
+  }
+}
+
+template <typename T, bool SKIP_LONG>
 __global__ void __launch_bounds__(256)
 coo_vla_warp_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __restrict__ run_row, int64_t n_runs,
                     const uint32_t* __restrict__ aj, const T* __restrict__ av, const T* __restrict__ x,
@@ -397,7 +461,8 @@ coo_vla_warp_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __re
       b = run_start[ri + 1];
       row = run_row[ri];
     }
-    const uint32_t nsteps = (b - a + uint32_t(lanes) - 1) / uint32_t(lanes);
+    const bool mine = !SKIP_LONG || b - a <= kVlaLong;  // longer runs: coo_vla_long_kernel
+    const uint32_t nsteps = mine ? (b - a + uint32_t(lanes) - 1) / uint32_t(lanes) : 0u;
     unsigned max_steps = __reduce_max_sync(0xffffffffu, nsteps);
     T yv = T(0);
     // Four steps' products are loaded before their trees run (in step
@@ -420,7 +485,7 @@ coo_vla_warp_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __re
         }
       }
     }
-    if (lane == 0 && ri < n_runs) {
+    if (lane == 0 && ri < n_runs && mine) {
       y[row] = yv;
       my_steps += nsteps;
     }
@@ -796,15 +861,36 @@ int spmv_coo_vla(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj,
     const int tb = 256;
     int64_t grid = (p->n_runs * width + tb - 1) / tb;
     if (grid > cap) grid = cap;
-    if (p->dtype == SPMV_F64)
-      coo_vla_warp_kernel<double><<<unsigned(grid), tb, 0, st>>>(rs, rr, p->n_runs, aj,
-                                                                  static_cast<const double*>(av),
-                                                                  static_cast<const double*>(x), col_base,
-                                                                  static_cast<double*>(y), lanes, width, steps);
+    const bool long_runs = p->n_long > 0;  // runs over 32 entries exist, so maybe over kVlaLong
+    auto warp_kernel = [&](auto skip) {
+      constexpr bool SKIP = decltype(skip)::value;
+      if (p->dtype == SPMV_F64)
+        coo_vla_warp_kernel<double, SKIP><<<unsigned(grid), tb, 0, st>>>(
+            rs, rr, p->n_runs, aj, static_cast<const double*>(av), static_cast<const double*>(x), col_base,
+            static_cast<double*>(y), lanes, width, steps);
+      else
+        coo_vla_warp_kernel<float, SKIP><<<unsigned(grid), tb, 0, st>>>(
+            rs, rr, p->n_runs, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
+            static_cast<float*>(y), lanes, width, steps);
+    };
+    if (long_runs)
+      warp_kernel(std::true_type{});
     else
-      coo_vla_warp_kernel<float><<<unsigned(grid), tb, 0, st>>>(rs, rr, p->n_runs, aj, static_cast<const float*>(av),
-                                                                 static_cast<const float*>(x), col_base,
-                                                                 static_cast<float*>(y), lanes, width, steps);
+      warp_kernel(std::false_type{});
+    if (long_runs) {
+      int64_t grid_long = (p->n_runs + tb - 1) / tb;  // a warp tests 32 runs at a time
+      if (grid_long > cap) grid_long = cap;
+      if (p->dtype == SPMV_F64)
+        coo_vla_long_kernel<double><<<unsigned(grid_long), tb, 0, st>>>(rs, rr, p->n_runs, aj,
+                                                                         static_cast<const double*>(av),
+                                                                         static_cast<const double*>(x), col_base,
+                                                                         static_cast<double*>(y), lanes, width, steps);
+      else
+        coo_vla_long_kernel<float><<<unsigned(grid_long), tb, 0, st>>>(rs, rr, p->n_runs, aj,
+                                                                        static_cast<const float*>(av),
+                                                                        static_cast<const float*>(x), col_base,
+                                                                        static_cast<float*>(y), lanes, width, steps);
+    }
   } else {
     int64_t grid = p->n_runs < cap ? p->n_runs : cap;
     const size_t sm = value_size(p->dtype) * width;

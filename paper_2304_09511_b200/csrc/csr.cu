@@ -394,7 +394,60 @@ __global__ void count_long_rows_kernel(const uint32_t* __restrict__ irp, int64_t
 }
 
 // ---- vla: sub-warp (L <= 32) or CTA (32 < L <= 1024) per row ------------
+// Rows longer than kVlaLong entries go to csr_vla_long_kernel (L <= 32).
+constexpr uint32_t kVlaLong = 256;
+
+// One warp per long row.  The 32 lanes gather a 256-entry chunk of rounded
+// products into shared memory at once (8 loads in flight per lane); then
+// logical lane l < L folds its entries s+l, s+l+L, ... from shared memory in
+// order — the same add sequence as csr_vla_warp_kernel, so bit-identical —
+// and the tree over next_pow2(L) lanes follows (lanes.py:107-128).
 template <typename T>
+__global__ void __launch_bounds__(256)
+csr_vla_long_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj, const T* __restrict__ av,
+                    const T* __restrict__ x, int64_t col_base, T* __restrict__ y, int64_t nrows, int lanes,
+                    int width) {
+  __shared__ T s_p[8][kVlaLong];
+  const T* xb = x - col_base;
+  const int lane = threadIdx.x & 31;
+  T* buf = s_p[threadIdx.x >> 5];
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  const uint32_t L = uint32_t(lanes);
+  for (int64_t r0 = warp * 32; r0 < nrows; r0 += nwarps * 32) {
+    // 32 rows per coalesced load; only the long ones are processed
+    const int64_t rl = r0 + lane;
+    const uint32_t sl = rl < nrows ? irp[rl] : 0u, el = rl < nrows ? irp[rl + 1] : 0u;
+    unsigned long_rows = __ballot_sync(0xffffffffu, el - sl > kVlaLong);
+    while (long_rows) {
+    const int k = __ffs(long_rows) - 1;
+    long_rows &= long_rows - 1;
+    const int64_t r = r0 + k;
+    const uint32_t s = __shfl_sync(0xffffffffu, sl, k), e = __shfl_sync(0xffffffffu, el, k);
+    T acc = T(0);
+    uint32_t n = s + uint32_t(lane);  // next entry of logical lane `lane`
+    for (uint32_t c0 = s; c0 < e; c0 += kVlaLong) {
+      const uint32_t c1 = min(e, c0 + kVlaLong);
+      T p[kVlaLong / 32];
+#pragma unroll
+      for (int u = 0; u < int(kVlaLong / 32); ++u) {
+        const uint32_t j = c0 + uint32_t(lane) + 32u * uint32_t(u);
+        p[u] = j < c1 ? mul_rn(ld_stream(av + j), ldx(xb + ld_stream(aj + j))) : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < int(kVlaLong / 32); ++u) buf[lane + 32 * u] = p[u];
+      __syncwarp();
+      if (uint32_t(lane) < L)
+        for (; n < c1; n += L) acc = add_rn(acc, buf[n - c0]);
+      __syncwarp();
+    }
+    acc = tree_reduce_warp(acc, width);
+    if (lane == 0) y[r] = acc;
+    }
+  }
+}
+
+template <typename T, bool SKIP_LONG>
 __global__ void __launch_bounds__(256)
 csr_vla_warp_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj,
                     const T* __restrict__ av, const T* __restrict__ x, int64_t col_base,
@@ -412,8 +465,9 @@ csr_vla_warp_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict
       s = irp[r];
       e = irp[r + 1];
     }
+    const bool mine = !SKIP_LONG || e - s <= kVlaLong;  // longer rows: csr_vla_long_kernel
     T acc = T(0);
-    if (lane < lanes) {
+    if (lane < lanes && mine) {
       // The lane's entries j, j+L, j+2L, j+3L are loaded as one predicated
       // batch and added in that order (skipped slots add nothing), so a
       // short row costs one gather round trip instead of one per entry.
@@ -431,7 +485,7 @@ csr_vla_warp_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict
       }
     }
     acc = tree_reduce_warp(acc, width);
-    if (lane == 0 && r < nrows) y[r] = (s == e) ? T(0) : acc;
+    if (lane == 0 && r < nrows && mine) y[r] = (s == e) ? T(0) : acc;
   }
 }
 
@@ -968,31 +1022,50 @@ int spmv_csr(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, co
                         static_cast<float*>(y), st);
 }
 
-int spmv_csr_vla(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* irp, const uint32_t* aj,
-                 const void* av, const void* x, int64_t col_base, int64_t x_len, void* y, int lanes,
-                 void* stream) {
+static int csr_vla_launch(int dtype, int64_t nrows, int64_t nnz, const uint32_t* irp, const uint32_t* aj,
+                          const void* av, const void* x, int64_t col_base, int64_t x_len, void* y, int lanes,
+                          bool long_rows, cudaStream_t st) {
   if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
   if (lanes < 1) return fail(SPMV_INVALID_ARG, "lane count must be >= 1");
   if (lanes > 1024) return fail(SPMV_UNSUPPORTED, "vla CSR supports at most 1024 lanes, got %d", lanes);
   if (nrows < 0 || nnz < 0 || x_len < 0) return fail(SPMV_INVALID_ARG, "bad sizes");
-  (void)ncols;
   if (nrows == 0) return SPMV_OK;
   int width = 1;
   while (width < lanes) width <<= 1;
-  cudaStream_t st = as_stream(stream);
   const int64_t cap = int64_t(sm_count()) * 16;
   if (width <= 32) {
     const int tb = 256;
     int64_t grid = (nrows * width + tb - 1) / tb;
     if (grid > cap) grid = cap;
-    if (dtype == SPMV_F64)
-      csr_vla_warp_kernel<double><<<unsigned(grid), tb, 0, st>>>(irp, aj, static_cast<const double*>(av),
-                                                                  static_cast<const double*>(x), col_base,
-                                                                  static_cast<double*>(y), nrows, lanes, width);
-    else
-      csr_vla_warp_kernel<float><<<unsigned(grid), tb, 0, st>>>(irp, aj, static_cast<const float*>(av),
-                                                                 static_cast<const float*>(x), col_base,
-                                                                 static_cast<float*>(y), nrows, lanes, width);
+    int64_t grid_long = (nrows + tb - 1) / tb;  // a warp tests 32 rows at a time
+    if (grid_long > cap) grid_long = cap;
+    if (dtype == SPMV_F64) {
+      if (long_rows)
+        csr_vla_warp_kernel<double, true><<<unsigned(grid), tb, 0, st>>>(
+            irp, aj, static_cast<const double*>(av), static_cast<const double*>(x), col_base,
+            static_cast<double*>(y), nrows, lanes, width);
+      else
+        csr_vla_warp_kernel<double, false><<<unsigned(grid), tb, 0, st>>>(
+            irp, aj, static_cast<const double*>(av), static_cast<const double*>(x), col_base,
+            static_cast<double*>(y), nrows, lanes, width);
+      if (long_rows)
+        csr_vla_long_kernel<double><<<unsigned(grid_long), tb, 0, st>>>(irp, aj, static_cast<const double*>(av),
+                                                                       static_cast<const double*>(x), col_base,
+                                                                       static_cast<double*>(y), nrows, lanes, width);
+    } else {
+      if (long_rows)
+        csr_vla_warp_kernel<float, true><<<unsigned(grid), tb, 0, st>>>(
+            irp, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
+            static_cast<float*>(y), nrows, lanes, width);
+      else
+        csr_vla_warp_kernel<float, false><<<unsigned(grid), tb, 0, st>>>(
+            irp, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
+            static_cast<float*>(y), nrows, lanes, width);
+      if (long_rows)
+        csr_vla_long_kernel<float><<<unsigned(grid_long), tb, 0, st>>>(irp, aj, static_cast<const float*>(av),
+                                                                      static_cast<const float*>(x), col_base,
+                                                                      static_cast<float*>(y), nrows, lanes, width);
+    }
   } else {
     int64_t grid = nrows < cap ? nrows : cap;
     const size_t sm = value_size(dtype) * width;
@@ -1007,6 +1080,22 @@ int spmv_csr_vla(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uin
   }
   SPMV_LAUNCH_CHECK();
   return SPMV_OK;
+}
+
+int spmv_csr_vla(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* irp, const uint32_t* aj,
+                 const void* av, const void* x, int64_t col_base, int64_t x_len, void* y, int lanes,
+                 void* stream) {
+  (void)ncols;
+  return csr_vla_launch(dtype, nrows, nnz, irp, aj, av, x, col_base, x_len, y, lanes, true, as_stream(stream));
+}
+
+int spmv_csr_vla_planned(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av,
+                         const void* x, int64_t col_base, int64_t x_len, void* y, int lanes, void* stream) {
+  if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
+  // the long-row kernel only when the plan saw rows that may exceed kVlaLong
+  const bool long_rows = p->n_long > 0 || p->exact_len >= int(kVlaLong);
+  return csr_vla_launch(p->dtype, p->nrows, p->nnz, irp, aj, av, x, col_base, x_len, y, lanes, long_rows,
+                        as_stream(stream));
 }
 
 }  // extern "C"

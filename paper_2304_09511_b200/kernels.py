@@ -355,9 +355,8 @@ def spmv_csr_vla(A, x, config: LaneConfig | None = None, out=None):
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
-        _lib.call("spmv_csr_vla", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.nnz, _ptr(A.row_pointers),
-                  _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0, A.ncols, _ptr(y), int(cfg.lanes),
-                  _stream(A.device))
+        _lib.call("spmv_csr_vla_planned", csr_plan(A).handle, _ptr(A.row_pointers), _ptr(A.col_indices),
+                  _ptr(A.values), _ptr(xv), 0, A.ncols, _ptr(y), int(cfg.lanes), _stream(A.device))
     return _finish(y, origin, out)
 
 
