@@ -129,9 +129,11 @@ int spmv_csr_vla(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
                  const void* values, const void* x, int64_t col_base,
                  int64_t x_len, void* y, int lanes, void* stream);
 /* Same, with the CSR plan of the matrix: its long-row census lets the call
- * skip the long-row pass (rows over 256 entries get a warp each) when no
- * row can need it. */
-int spmv_csr_vla_planned(const spmv_csr_plan* plan, const uint32_t* row_pointers,
+ * skip the long-row pass when no row can need it, and rows over 256 entries
+ * take a two-phase path (products gathered by all warps, then one ordered
+ * fold per row) whose row list and product buffer the plan keeps (built on
+ * the first call; not reentrant per plan). */
+int spmv_csr_vla_planned(spmv_csr_plan* plan, const uint32_t* row_pointers,
                          const uint32_t* col_indices, const void* values,
                          const void* x, int64_t col_base, int64_t x_len, void* y,
                          int lanes, void* stream);

@@ -31,16 +31,23 @@ static int64_t grid_for(int64_t n, int tb = 256) {
 template <typename T>
 __global__ void coo_to_csr_kernel(const uint32_t* __restrict__ ai, const uint32_t* __restrict__ aj,
                                   const T* __restrict__ av, int64_t nnz, int64_t nrows, uint32_t* __restrict__ irp,
-                                  uint32_t* __restrict__ aj_out, T* __restrict__ av_out) {
+                                  uint32_t* __restrict__ aj_out, T* __restrict__ av_out, int* __restrict__ descending) {
   GRID_STRIDE(k, nnz) {
     const int64_t rk = ai[k];
     const int64_t rp = k == 0 ? -1 : int64_t(ai[k - 1]);
+    if (rk < rp) *descending = 1;  // a mis-flagged input: irp is rebuilt from counts
     for (int64_t r = rp + 1; r <= rk; ++r) irp[r] = uint32_t(k);
     if (k == nnz - 1)
       for (int64_t r = rk + 1; r <= nrows; ++r) irp[r] = uint32_t(nnz);
     aj_out[k] = aj[k];
     av_out[k] = av[k];
   }
+}
+
+// irp from per-row counts (np.bincount + cumsum, convert.py:92-93): the
+// reference's result for any row order, used when the sorted flag is wrong.
+__global__ void row_count_kernel(const uint32_t* __restrict__ ai, int64_t nnz, uint32_t* __restrict__ cnt) {
+  GRID_STRIDE(k, nnz) atomicAdd(cnt + ai[k], 1u);
 }
 
 // ---- csr -> coo ------------------------------------------------------------
@@ -294,13 +301,30 @@ int spmv_coo_to_csr(int dtype, int64_t nrows, int64_t nnz, const uint32_t* ai, c
     SPMV_CUDA_TRY(cudaMemsetAsync(irp, 0, sizeof(uint32_t) * (nrows + 1), st));
     return SPMV_OK;
   }
+  ScratchBuf flag;
+  int rc = flag.alloc(sizeof(int), st);
+  if (rc) return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(flag.ptr, 0, sizeof(int), st));
   if (dtype == SPMV_F64)
     coo_to_csr_kernel<double><<<unsigned(grid_for(nnz)), 256, 0, st>>>(
-        ai, aj, static_cast<const double*>(av), nnz, nrows, irp, aj_out, static_cast<double*>(av_out));
+        ai, aj, static_cast<const double*>(av), nnz, nrows, irp, aj_out, static_cast<double*>(av_out),
+        flag.as<int>());
   else
     coo_to_csr_kernel<float><<<unsigned(grid_for(nnz)), 256, 0, st>>>(
-        ai, aj, static_cast<const float*>(av), nnz, nrows, irp, aj_out, static_cast<float*>(av_out));
+        ai, aj, static_cast<const float*>(av), nnz, nrows, irp, aj_out, static_cast<float*>(av_out),
+        flag.as<int>());
   SPMV_LAUNCH_CHECK();
+  int h = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&h, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  if (h) {  // rows not actually non-decreasing: counts + exclusive scan, like bincount/cumsum
+    ScratchBuf cnt;
+    if ((rc = cnt.alloc(sizeof(uint32_t) * (nrows + 1), st))) return rc;
+    SPMV_CUDA_TRY(cudaMemsetAsync(cnt.ptr, 0, sizeof(uint32_t) * (nrows + 1), st));
+    row_count_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, nnz, cnt.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+    if ((rc = excl_scan<uint32_t>(cnt.as<uint32_t>(), irp, nrows + 1, st))) return rc;
+  }
   return SPMV_OK;
 }
 

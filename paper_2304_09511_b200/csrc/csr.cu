@@ -388,7 +388,7 @@ __global__ void count_long_rows_kernel(const uint32_t* __restrict__ irp, int64_t
                                        unsigned long long* __restrict__ n_long) {
   unsigned long long c = 0;
   for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += int64_t(gridDim.x) * blockDim.x)
-    c += (irp[r + 1] - irp[r]) > uint32_t(exact_len);
+    c += irp[r + 1] > irp[r] && (irp[r + 1] - irp[r]) > uint32_t(exact_len);
   for (int o = 16; o >= 1; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(n_long, c);
 }
@@ -447,6 +447,112 @@ csr_vla_long_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict
   }
 }
 
+// Planned long-row vla path, two phases.  Phase 1 gathers the rounded
+// products of every long row in 256-entry chunks spread over all warps
+// (chunk_row: chunk -> long-row index, built by the plan).  Phase 2 folds
+// each row per logical lane in order (one warp per row; chunks staged
+// through shared memory, the next one prefetched), so a 50k-entry row costs a
+// short sequential fold rather than ~200 gather round trips on one warp.
+// Same products, same add order: bit-identical with csr_vla_warp_kernel.
+template <typename T>
+__global__ void __launch_bounds__(256)
+csr_vla_products_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj, const T* __restrict__ av,
+                        const T* __restrict__ x, int64_t col_base, const uint32_t* __restrict__ rows,
+                        const uint32_t* __restrict__ chunk_pre, const uint32_t* __restrict__ chunk_row,
+                        int64_t n_chunks, T* __restrict__ P) {
+  const T* xb = x - col_base;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t c = warp; c < n_chunks; c += nwarps) {
+    const uint32_t i = chunk_row[c];
+    const uint32_t r = rows[i];
+    const uint32_t s = irp[r], e = irp[r + 1];
+    const uint32_t c0 = s + (uint32_t(c) - chunk_pre[i]) * kVlaLong, c1 = min(e, c0 + kVlaLong);
+    T p[kVlaLong / 32];
+#pragma unroll
+    for (int u = 0; u < int(kVlaLong / 32); ++u) {
+      const uint32_t j = c0 + uint32_t(lane) + 32u * uint32_t(u);
+      p[u] = j < c1 ? mul_rn(ld_stream(av + j), ldx(xb + ld_stream(aj + j))) : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < int(kVlaLong / 32); ++u) {
+      const uint32_t j = c0 + uint32_t(lane) + 32u * uint32_t(u);
+      if (j < c1) P[j] = p[u];
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+csr_vla_fold_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ rows, int64_t n_long,
+                    const T* __restrict__ P, T* __restrict__ y, int lanes, int width) {
+  constexpr int PER = kVlaLong / 32;
+  __shared__ T s_p[8][kVlaLong];
+  const int lane = threadIdx.x & 31;
+  T* buf = s_p[threadIdx.x >> 5];
+  const uint32_t L = uint32_t(lanes);
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = warp; i < n_long; i += nwarps) {
+    const uint32_t r = rows[i];
+    const uint32_t s = irp[r], e = irp[r + 1];
+    T cur[PER], nxt[PER];
+#pragma unroll
+    for (int u = 0; u < PER; ++u) {
+      const uint32_t j = s + uint32_t(lane) + 32u * uint32_t(u);
+      cur[u] = j < e ? P[j] : T(0);
+    }
+    T acc = T(0);
+    uint32_t n = s + uint32_t(lane);  // next entry of logical lane `lane`
+    for (uint32_t c0 = s; c0 < e; c0 += kVlaLong) {
+      const uint32_t c1 = min(e, c0 + kVlaLong);
+      if (c1 < e) {
+#pragma unroll
+        for (int u = 0; u < PER; ++u) {
+          const uint32_t j = c1 + uint32_t(lane) + 32u * uint32_t(u);
+          nxt[u] = j < e ? P[j] : T(0);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < PER; ++u) buf[lane + 32 * u] = cur[u];
+      __syncwarp();
+      if (uint32_t(lane) < L) {
+        for (; n + 3 * L < c1; n += 4 * L) {  // loads ahead of the (ordered) adds
+          const T q0 = buf[n - c0], q1 = buf[n + L - c0], q2 = buf[n + 2 * L - c0], q3 = buf[n + 3 * L - c0];
+          acc = add_rn(add_rn(add_rn(add_rn(acc, q0), q1), q2), q3);
+        }
+        for (; n < c1; n += L) acc = add_rn(acc, buf[n - c0]);
+      }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < PER; ++u) cur[u] = nxt[u];
+    }
+    acc = tree_reduce_warp(acc, width);
+    if (lane == 0) y[r] = acc;
+  }
+}
+
+__global__ void vla_long_rows_kernel(const uint32_t* __restrict__ irp, int64_t nrows, uint32_t* __restrict__ rows,
+                                     unsigned long long* __restrict__ n) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += int64_t(gridDim.x) * blockDim.x)
+    if (irp[r + 1] > irp[r] && irp[r + 1] - irp[r] > kVlaLong) rows[atomicAdd(n, 1ull)] = uint32_t(r);
+}
+
+__global__ void vla_chunk_count_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ rows,
+                                       int64_t n_long, uint32_t* __restrict__ cnt) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_long; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t r = rows[i];
+    cnt[i] = (irp[r + 1] - irp[r] + kVlaLong - 1) / kVlaLong;
+  }
+}
+
+__global__ void vla_chunk_row_kernel(const uint32_t* __restrict__ pre, const uint32_t* __restrict__ cnt,
+                                     int64_t n_long, uint32_t* __restrict__ chunk_row) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_long; i += int64_t(gridDim.x) * blockDim.x)
+    for (uint32_t k = 0; k < cnt[i]; ++k) chunk_row[pre[i] + k] = uint32_t(i);
+}
+
 template <typename T, bool SKIP_LONG>
 __global__ void __launch_bounds__(256)
 csr_vla_warp_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj,
@@ -465,7 +571,7 @@ csr_vla_warp_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict
       s = irp[r];
       e = irp[r + 1];
     }
-    const bool mine = !SKIP_LONG || e - s <= kVlaLong;  // longer rows: csr_vla_long_kernel
+    const bool mine = !SKIP_LONG || e <= s || e - s <= kVlaLong;  // longer rows: csr_vla_long_kernel
     T acc = T(0);
     if (lane < lanes && mine) {
       // The lane's entries j, j+L, j+2L, j+3L are loaded as one predicated
@@ -544,6 +650,11 @@ struct spmv_csr_plan {
     for (auto e : events) cudaEventDestroy(e);
   }
   int groups = 1;                    // consumer groups per tile CTA (csr_tile_kernel G)
+  // planned vla path: rows over kVlaLong entries, their 256-entry chunks and
+  // a product buffer (built on the first spmv_csr_vla_planned call)
+  bool vla_built = false;
+  int64_t vla_n = 0, vla_chunks = 0;
+  DevBuf vla_rows, vla_pre, vla_chunk_row, vla_prod;
   int grid_bulk = 0, grid_direct = 0;  // G-group TMA kernel / single-group kernel
 };
 
@@ -1022,9 +1133,57 @@ int spmv_csr(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, co
                         static_cast<float*>(y), st);
 }
 
+// The planned vla path's row list: rows over kVlaLong entries, their chunk
+// offsets (host prefix sum, once per plan) and chunk -> row map.
+static int csr_vla_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st) {
+  int rc;
+  const int64_t g = std::min<int64_t>((p->nrows + 255) / 256, int64_t(sm_count()) * 16);
+  DevBuf ctr;
+  if ((rc = ctr.alloc(16))) return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(ctr.ptr, 0, 16, st));
+  count_long_rows_kernel<<<unsigned(g), 256, 0, st>>>(irp, p->nrows, int(kVlaLong), ctr.as<unsigned long long>());
+  SPMV_LAUNCH_CHECK();
+  unsigned long long n = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&n, ctr.ptr, 8, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  p->vla_n = int64_t(n);
+  if (p->vla_n > 0) {
+    if ((rc = p->vla_rows.alloc(4 * p->vla_n))) return rc;
+    vla_long_rows_kernel<<<unsigned(g), 256, 0, st>>>(irp, p->nrows, p->vla_rows.as<uint32_t>(),
+                                                       ctr.as<unsigned long long>() + 1);
+    SPMV_LAUNCH_CHECK();
+  }
+  if (p->vla_n > 0) {
+    DevBuf cnt;
+    if ((rc = cnt.alloc(4 * p->vla_n)) || (rc = p->vla_pre.alloc(4 * (p->vla_n + 1)))) return rc;
+    const int64_t gi = std::min<int64_t>((p->vla_n + 255) / 256, int64_t(sm_count()) * 16);
+    vla_chunk_count_kernel<<<unsigned(gi), 256, 0, st>>>(irp, p->vla_rows.as<uint32_t>(), p->vla_n,
+                                                          cnt.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+    std::vector<uint32_t> h(p->vla_n), pre(p->vla_n + 1);
+    SPMV_CUDA_TRY(cudaMemcpyAsync(h.data(), cnt.ptr, 4 * p->vla_n, cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    pre[0] = 0;
+    for (int64_t i = 0; i < p->vla_n; ++i) pre[i + 1] = pre[i] + h[i];
+    p->vla_chunks = pre[p->vla_n];
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->vla_pre.ptr, pre.data(), 4 * (p->vla_n + 1), cudaMemcpyHostToDevice, st));
+    if ((rc = p->vla_chunk_row.alloc(4 * p->vla_chunks)) || (rc = p->vla_prod.alloc(value_size(p->dtype) * p->nnz)))
+      return rc;
+    vla_chunk_row_kernel<<<unsigned(gi), 256, 0, st>>>(p->vla_pre.as<uint32_t>(), cnt.as<uint32_t>(), p->vla_n,
+                                                        p->vla_chunk_row.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));  // cnt and the host vector go out of scope
+  }
+  p->vla_built = true;
+  return SPMV_OK;
+}
+
+// long_mode: 0 no row over kVlaLong; 1 such rows, csr_vla_long_kernel
+// takes them; 2 such rows, the caller runs the two-phase path for them.
 static int csr_vla_launch(int dtype, int64_t nrows, int64_t nnz, const uint32_t* irp, const uint32_t* aj,
                           const void* av, const void* x, int64_t col_base, int64_t x_len, void* y, int lanes,
-                          bool long_rows, cudaStream_t st) {
+                          int long_mode, cudaStream_t st) {
+  const bool long_rows = long_mode != 0;
   if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
   if (lanes < 1) return fail(SPMV_INVALID_ARG, "lane count must be >= 1");
   if (lanes > 1024) return fail(SPMV_UNSUPPORTED, "vla CSR supports at most 1024 lanes, got %d", lanes);
@@ -1048,7 +1207,7 @@ static int csr_vla_launch(int dtype, int64_t nrows, int64_t nnz, const uint32_t*
         csr_vla_warp_kernel<double, false><<<unsigned(grid), tb, 0, st>>>(
             irp, aj, static_cast<const double*>(av), static_cast<const double*>(x), col_base,
             static_cast<double*>(y), nrows, lanes, width);
-      if (long_rows)
+      if (long_mode == 1)
         csr_vla_long_kernel<double><<<unsigned(grid_long), tb, 0, st>>>(irp, aj, static_cast<const double*>(av),
                                                                        static_cast<const double*>(x), col_base,
                                                                        static_cast<double*>(y), nrows, lanes, width);
@@ -1061,7 +1220,7 @@ static int csr_vla_launch(int dtype, int64_t nrows, int64_t nnz, const uint32_t*
         csr_vla_warp_kernel<float, false><<<unsigned(grid), tb, 0, st>>>(
             irp, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
             static_cast<float*>(y), nrows, lanes, width);
-      if (long_rows)
+      if (long_mode == 1)
         csr_vla_long_kernel<float><<<unsigned(grid_long), tb, 0, st>>>(irp, aj, static_cast<const float*>(av),
                                                                       static_cast<const float*>(x), col_base,
                                                                       static_cast<float*>(y), nrows, lanes, width);
@@ -1086,16 +1245,45 @@ int spmv_csr_vla(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uin
                  const void* av, const void* x, int64_t col_base, int64_t x_len, void* y, int lanes,
                  void* stream) {
   (void)ncols;
-  return csr_vla_launch(dtype, nrows, nnz, irp, aj, av, x, col_base, x_len, y, lanes, true, as_stream(stream));
+  return csr_vla_launch(dtype, nrows, nnz, irp, aj, av, x, col_base, x_len, y, lanes, 1, as_stream(stream));
 }
 
-int spmv_csr_vla_planned(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av,
+int spmv_csr_vla_planned(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av,
                          const void* x, int64_t col_base, int64_t x_len, void* y, int lanes, void* stream) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
-  // the long-row kernel only when the plan saw rows that may exceed kVlaLong
+  cudaStream_t st = as_stream(stream);
+  // rows over kVlaLong entries are only possible when the plan saw long rows
   const bool long_rows = p->n_long > 0 || p->exact_len >= int(kVlaLong);
-  return csr_vla_launch(p->dtype, p->nrows, p->nnz, irp, aj, av, x, col_base, x_len, y, lanes, long_rows,
-                        as_stream(stream));
+  if (!long_rows || lanes > 32 || lanes < 1)
+    return csr_vla_launch(p->dtype, p->nrows, p->nnz, irp, aj, av, x, col_base, x_len, y, lanes, long_rows ? 1 : 0,
+                          st);
+  int rc;
+  if (!p->vla_built && (rc = csr_vla_build(p, irp, st))) return rc;
+  if ((rc = csr_vla_launch(p->dtype, p->nrows, p->nnz, irp, aj, av, x, col_base, x_len, y, lanes, 2, st))) return rc;
+  if (p->vla_n == 0) return SPMV_OK;
+  int width = 1;
+  while (width < lanes) width <<= 1;
+  const int64_t cap = int64_t(sm_count()) * 16;
+  const int64_t g1 = std::min<int64_t>((p->vla_chunks * 32 + 255) / 256, cap);
+  const int64_t g2 = std::min<int64_t>((p->vla_n * 32 + 255) / 256, cap);
+  const uint32_t* rows = p->vla_rows.as<uint32_t>();
+  if (p->dtype == SPMV_F64) {
+    double* P = p->vla_prod.as<double>();
+    csr_vla_products_kernel<double><<<unsigned(g1), 256, 0, st>>>(
+        irp, aj, static_cast<const double*>(av), static_cast<const double*>(x), col_base, rows,
+        p->vla_pre.as<uint32_t>(), p->vla_chunk_row.as<uint32_t>(), p->vla_chunks, P);
+    csr_vla_fold_kernel<double><<<unsigned(g2), 256, 0, st>>>(irp, rows, p->vla_n, P, static_cast<double*>(y),
+                                                               lanes, width);
+  } else {
+    float* P = p->vla_prod.as<float>();
+    csr_vla_products_kernel<float><<<unsigned(g1), 256, 0, st>>>(
+        irp, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base, rows,
+        p->vla_pre.as<uint32_t>(), p->vla_chunk_row.as<uint32_t>(), p->vla_chunks, P);
+    csr_vla_fold_kernel<float><<<unsigned(g2), 256, 0, st>>>(irp, rows, p->vla_n, P, static_cast<float*>(y), lanes,
+                                                              width);
+  }
+  SPMV_LAUNCH_CHECK();
+  return SPMV_OK;
 }
 
 }  // extern "C"

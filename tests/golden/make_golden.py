@@ -219,6 +219,12 @@ def make_convert() -> None:
     put_matrix(d, "rand/coo", coo)
     put_matrix(d, "rand/csr", coo_to_csr(coo))
     put_matrix(d, "rand/dia", coo_to_dia(coo, LOOSE))
+    # COO flagged sorted whose rows are not: coo_to_csr trusts the flag and
+    # builds row pointers from counts (bincount + cumsum, convert.py:92-93)
+    flat = np.random.default_rng(1).choice(3600, 180, replace=False)
+    mis = CooMatrix.from_arrays(60, 60, flat // 60, flat % 60, np.linspace(-1.0, 1.0, 180), sorted=True)
+    put_matrix(d, "misflagged/coo", mis)
+    put_matrix(d, "misflagged/csr", coo_to_csr(mis))
     np.savez_compressed(OUT / "convert.npz", **d)
 
 

@@ -88,6 +88,18 @@ def test_csr_to_coo_unsorted_and_dia_specials(sp):
     assert bit_equal(h["values"], matrix_arrays(d, "rand/dia")["values"])
 
 
+def test_coo_to_csr_misflagged_rows(sp):
+    """A COO flagged sorted whose rows are not: row pointers come from the
+    per-row counts like the reference's bincount + cumsum (convert.py:92-93);
+    columns and values are copied as stored."""
+    d = load_golden("convert")
+    want = matrix_arrays(d, "misflagged/csr")
+    h = sp.coo_to_csr(dev_matrix(sp, matrix_arrays(d, "misflagged/coo"), "coo")).to_host()
+    assert np.array_equal(h["row_pointers"], want["row_pointers"])
+    assert np.array_equal(h["col_indices"], want["col_indices"])
+    assert bit_equal(h["values"], want["values"])
+
+
 def test_canonical_conversion_kats(sp):
     d = load_golden("canonical")
     can = dev_matrix(sp, matrix_arrays(d, "coo"), "coo")
