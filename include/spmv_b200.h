@@ -170,8 +170,11 @@ int spmv_coo(const spmv_coo_plan* plan, const uint32_t* row_indices,
 /* Requires the reference's `sorted` flag (kernels.py:119-120; checked by
  * the caller).  Per row: chunks of L entries, each tree-reduced, added once
  * into y: bit-exact with spmv_coo_vla.  outer_steps (may be NULL) receives
- * the reference's step count (kernels.py:138-140); non-NULL synchronises. */
-int spmv_coo_vla(const spmv_coo_plan* plan, const uint32_t* row_indices,
+ * the reference's step count (kernels.py:138-140); non-NULL synchronises.
+ * Runs over 256 entries take a two-phase path (step trees over all warps,
+ * then an ordered fold per run) whose buffers the plan keeps (built on the
+ * first call that needs them; not reentrant per plan). */
+int spmv_coo_vla(spmv_coo_plan* plan, const uint32_t* row_indices,
                  const uint32_t* col_indices, const void* values,
                  const void* x, int64_t col_base, int64_t x_len, void* y,
                  int lanes, int64_t* outer_steps, void* stream);

@@ -27,6 +27,7 @@
 
 #include <algorithm>
 #include <type_traits>
+#include <vector>
 
 #include "tile.cuh"
 
@@ -381,64 +382,125 @@ __global__ void run_scatter_kernel(const uint32_t* __restrict__ ai, int64_t nnz,
 // Runs longer than kVlaLong entries go to coo_vla_long_kernel (L <= 32).
 constexpr uint32_t kVlaLong = 256;
 
-// One warp per long run.  Sub-groups of W = next_pow2(L) lanes take one
-// step each (lane l < L: entry a + step*L + l), eight sub-passes of loads
-// in flight per lane; each step's tree runs in its sub-group and the step
-// sums are folded into the run's y value in step order (kernels.py:129-137),
-// so the result equals the sub-warp kernel's bit for bit.
+// Planned long-run path, two phases.  Phase 1: a warp per 256-entry chunk
+// of a long run computes the tree sum of every step whose first entry lies
+// in the chunk (gathers for 8 sub-passes in flight) and stores step st of
+// the run starting at a in S[a + st] (st < run length, so runs never
+// collide and a run's step sums are contiguous).  Phase 2: a warp per long
+// run folds its step sums in step order (kernels.py:129-137), 256 at a
+// time through shared memory with the next chunk prefetched.
 template <typename T>
 __global__ void __launch_bounds__(256)
-coo_vla_long_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __restrict__ run_row, int64_t n_runs,
-                    const uint32_t* __restrict__ aj, const T* __restrict__ av, const T* __restrict__ x,
-                    int64_t col_base, T* __restrict__ y, int lanes, int width,
-                    unsigned long long* __restrict__ steps_out) {
+coo_vla_steps_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __restrict__ runs,
+                     const uint32_t* __restrict__ chunk_pre, const uint32_t* __restrict__ chunk_run, int64_t n_chunks,
+                     const uint32_t* __restrict__ aj, const T* __restrict__ av, const T* __restrict__ x,
+                     int64_t col_base, int lanes, int width, T* __restrict__ S) {
   constexpr int U = 8;
   const T* xb = x - col_base;
   const int lane = threadIdx.x & 31;
-  const int W = width, G = 32 / width;  // steps per sub-pass
-  const int sub = lane / W, l = lane % W;
+  const int W = width, G = 32 / width, sub = lane / W, l = lane % W;
+  const uint32_t L = uint32_t(lanes);
+  const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
+  const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t c = warp; c < n_chunks; c += nwarps) {
+    const uint32_t i = chunk_run[c], ri = runs[i];
+    const uint32_t a = run_start[ri], b = run_start[ri + 1];
+    const uint32_t e0 = a + (uint32_t(c) - chunk_pre[i]) * kVlaLong, e1 = min(b, e0 + kVlaLong);
+    const uint32_t st_lo = (e0 - a + L - 1) / L, st_hi = (e1 - a + L - 1) / L;
+    for (uint32_t st0 = st_lo; st0 < st_hi; st0 += uint32_t(U * G)) {
+      T p[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const uint32_t st = st0 + uint32_t(u * G + sub);
+        const uint32_t j = a + st * L + uint32_t(l);
+        p[u] = (uint32_t(l) < L && st < st_hi && j < b) ? mul_rn(ld_stream(av + j), ldx(xb + ld_stream(aj + j)))
+                                                       : T(0);
+      }
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const T q = tree_reduce_warp(p[u], W);
+        const uint32_t st = st0 + uint32_t(u * G + sub);
+        if (l == 0 && st < st_hi) S[a + st] = q;
+      }
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256)
+coo_vla_fold_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __restrict__ run_row,
+                    const uint32_t* __restrict__ runs, int64_t n_long, const T* __restrict__ S, int lanes,
+                    T* __restrict__ y, unsigned long long* __restrict__ steps_out) {
+  constexpr int PER = kVlaLong / 32;
+  __shared__ T s_q[8][kVlaLong];
+  const int lane = threadIdx.x & 31;
+  T* buf = s_q[threadIdx.x >> 5];
   const uint32_t L = uint32_t(lanes);
   const int64_t warp = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5;
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   unsigned long long my_steps = 0;
-  for (int64_t r0 = warp * 32; r0 < n_runs; r0 += nwarps * 32) {
-    const int64_t rl = r0 + lane;
-    const uint32_t al = rl < n_runs ? run_start[rl] : 0u, bl = rl < n_runs ? run_start[rl + 1] : 0u;
-    unsigned long_runs = __ballot_sync(0xffffffffu, bl - al > kVlaLong);
-    while (long_runs) {
-      const int k = __ffs(long_runs) - 1;
-      long_runs &= long_runs - 1;
-      const uint32_t a = __shfl_sync(0xffffffffu, al, k), b = __shfl_sync(0xffffffffu, bl, k);
-      const uint32_t nsteps = (b - a + L - 1) / L;
-      T yv = T(0);
-      for (uint32_t st0 = 0; st0 < nsteps; st0 += uint32_t(U * G)) {
-        T p[U];
+  for (int64_t i = warp; i < n_long; i += nwarps) {
+    const uint32_t ri = runs[i];
+    const uint32_t a = run_start[ri], b = run_start[ri + 1];
+    const uint32_t nsteps = (b - a + L - 1) / L;
+    T cur[PER], nxt[PER];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const uint32_t step = st0 + uint32_t(u * G + sub);
-          const uint32_t j = a + step * L + uint32_t(l);
-          p[u] = (uint32_t(l) < L && step < nsteps && j < b) ? mul_rn(ld_stream(av + j), ldx(xb + ld_stream(aj + j)))
-                                                            : T(0);
-        }
+    for (int u = 0; u < PER; ++u) {
+      const uint32_t st = uint32_t(lane) + 32u * uint32_t(u);
+      cur[u] = st < nsteps ? S[a + st] : T(0);
+    }
+    T yv = T(0);
+    for (uint32_t c0 = 0; c0 < nsteps; c0 += kVlaLong) {
+      const uint32_t c1 = min(nsteps, c0 + kVlaLong);
+      if (c1 < nsteps) {
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const T q = tree_reduce_warp(p[u], W);  // lane g*W: sum of step st0 + u*G + g
-          for (int g = 0; g < G; ++g) {
-            const T v = __shfl_sync(0xffffffffu, q, g * W);
-            if (st0 + uint32_t(u * G + g) < nsteps) yv = add_rn(yv, v);
-          }
+        for (int u = 0; u < PER; ++u) {
+          const uint32_t st = c1 + uint32_t(lane) + 32u * uint32_t(u);
+          nxt[u] = st < nsteps ? S[a + st] : T(0);
         }
       }
+#pragma unroll
+      for (int u = 0; u < PER; ++u) buf[lane + 32 * u] = cur[u];
+      __syncwarp();
       if (lane == 0) {
-        y[run_row[r0 + k]] = yv;
-        my_steps += nsteps;
+        uint32_t k = 0;
+        for (; k + 3 < c1 - c0; k += 4) {
+          const T q0 = buf[k], q1 = buf[k + 1], q2 = buf[k + 2], q3 = buf[k + 3];
+          yv = add_rn(add_rn(add_rn(add_rn(yv, q0), q1), q2), q3);
+        }
+        for (; k < c1 - c0; ++k) yv = add_rn(yv, buf[k]);
       }
+      __syncwarp();
+#pragma unroll
+      for (int u = 0; u < PER; ++u) cur[u] = nxt[u];
+    }
+    if (lane == 0) {
+      y[run_row[ri]] = yv;
+      my_steps += nsteps;
     }
   }
-  if (steps_out) {
-    for (int o = 16; o >= 1; o >>= 1) my_steps += __shfl_down_sync(0xffffffffu, my_steps, o);
-    if (lane == 0 && my_steps) atomicAdd(steps_out, my_steps);
-  }
+  if (steps_out && lane == 0 && my_steps) atomicAdd(steps_out, my_steps);
+}
+
+__global__ void vla_long_runs_kernel(const uint32_t* __restrict__ run_start, int64_t n_runs,
+                                     uint32_t* __restrict__ runs, unsigned long long* __restrict__ n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_runs; i += int64_t(gridDim.x) * blockDim.x)
+    if (run_start[i + 1] - run_start[i] > kVlaLong) {
+      if (runs) runs[atomicAdd(n, 1ull)] = uint32_t(i);
+      else atomicAdd(n, 1ull);
+    }
+}
+
+__global__ void vla_run_chunks_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __restrict__ runs,
+                                      int64_t n_long, uint32_t* __restrict__ cnt) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_long; i += int64_t(gridDim.x) * blockDim.x)
+    cnt[i] = (run_start[runs[i] + 1] - run_start[runs[i]] + kVlaLong - 1) / kVlaLong;
+}
+
+__global__ void vla_run_chunk_map_kernel(const uint32_t* __restrict__ pre, const uint32_t* __restrict__ cnt,
+                                         int64_t n_long, uint32_t* __restrict__ chunk_run) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_long; i += int64_t(gridDim.x) * blockDim.x)
+    for (uint32_t k = 0; k < cnt[i]; ++k) chunk_run[pre[i] + k] = uint32_t(i);
 }
 
 template <typename T, bool SKIP_LONG>
@@ -549,7 +611,53 @@ struct spmv_coo_plan {
   DevBuf steps;
   int groups = 1;                // consumer groups per tile CTA (coo_tile_kernel G)
   int grid = 0, grid_direct = 0;  // G-group TMA kernel / single-group kernel
+  // vla long runs (over kVlaLong entries): list, 256-entry chunk map and the
+  // step-sum buffer, built on the first vla call that needs them
+  bool vla_built = false;
+  int64_t vla_n = 0, vla_chunks = 0;
+  DevBuf vla_runs, vla_pre, vla_chunk_run, vla_S;
 };
+
+static int coo_vla_build(spmv_coo_plan* p, cudaStream_t st) {
+  int rc;
+  const uint32_t* rs = p->run_start.as<uint32_t>();
+  const int64_t g = std::min<int64_t>((p->n_runs + 255) / 256, int64_t(sm_count()) * 16);
+  DevBuf ctr;
+  if ((rc = ctr.alloc(16))) return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(ctr.ptr, 0, 16, st));
+  vla_long_runs_kernel<<<unsigned(g), 256, 0, st>>>(rs, p->n_runs, nullptr, ctr.as<unsigned long long>());
+  SPMV_LAUNCH_CHECK();
+  unsigned long long n = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&n, ctr.ptr, 8, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  p->vla_n = int64_t(n);
+  if (p->vla_n > 0) {
+    DevBuf cnt;
+    if ((rc = p->vla_runs.alloc(4 * p->vla_n)) || (rc = cnt.alloc(4 * p->vla_n)) ||
+        (rc = p->vla_pre.alloc(4 * (p->vla_n + 1))))
+      return rc;
+    vla_long_runs_kernel<<<unsigned(g), 256, 0, st>>>(rs, p->n_runs, p->vla_runs.as<uint32_t>(),
+                                                       ctr.as<unsigned long long>() + 1);
+    const int64_t gi = std::min<int64_t>((p->vla_n + 255) / 256, int64_t(sm_count()) * 16);
+    vla_run_chunks_kernel<<<unsigned(gi), 256, 0, st>>>(rs, p->vla_runs.as<uint32_t>(), p->vla_n, cnt.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+    std::vector<uint32_t> h(p->vla_n), pre(p->vla_n + 1);
+    SPMV_CUDA_TRY(cudaMemcpyAsync(h.data(), cnt.ptr, 4 * p->vla_n, cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    pre[0] = 0;
+    for (int64_t i = 0; i < p->vla_n; ++i) pre[i + 1] = pre[i] + h[i];
+    p->vla_chunks = pre[p->vla_n];
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->vla_pre.ptr, pre.data(), 4 * (p->vla_n + 1), cudaMemcpyHostToDevice, st));
+    if ((rc = p->vla_chunk_run.alloc(4 * p->vla_chunks)) || (rc = p->vla_S.alloc(value_size(p->dtype) * p->nnz)))
+      return rc;
+    vla_run_chunk_map_kernel<<<unsigned(gi), 256, 0, st>>>(p->vla_pre.as<uint32_t>(), cnt.as<uint32_t>(), p->vla_n,
+                                                            p->vla_chunk_run.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  p->vla_built = true;
+  return SPMV_OK;
+}
 
 // (tile, groups) pairs with compiled kernels.
 #define SPMV_COO_CONFIGS(X) X(1024, 1) X(2048, 1) X(1536, 1) X(2048, 4) X(1536, 6)
@@ -834,7 +942,7 @@ int spmv_coo(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, con
                         static_cast<float*>(y), st);
 }
 
-int spmv_coo_vla(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const void* av, const void* x,
+int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const void* av, const void* x,
                  int64_t col_base, int64_t x_len, void* y, int lanes, int64_t* outer_steps, void* stream) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (lanes < 1) return fail(SPMV_INVALID_ARG, "lane count must be >= 1");
@@ -877,19 +985,29 @@ int spmv_coo_vla(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj,
       warp_kernel(std::true_type{});
     else
       warp_kernel(std::false_type{});
-    if (long_runs) {
-      int64_t grid_long = (p->n_runs + tb - 1) / tb;  // a warp tests 32 runs at a time
-      if (grid_long > cap) grid_long = cap;
-      if (p->dtype == SPMV_F64)
-        coo_vla_long_kernel<double><<<unsigned(grid_long), tb, 0, st>>>(rs, rr, p->n_runs, aj,
-                                                                         static_cast<const double*>(av),
-                                                                         static_cast<const double*>(x), col_base,
-                                                                         static_cast<double*>(y), lanes, width, steps);
-      else
-        coo_vla_long_kernel<float><<<unsigned(grid_long), tb, 0, st>>>(rs, rr, p->n_runs, aj,
-                                                                        static_cast<const float*>(av),
-                                                                        static_cast<const float*>(x), col_base,
-                                                                        static_cast<float*>(y), lanes, width, steps);
+    if (long_runs) {  // runs over 32 entries exist: two-phase path for those over kVlaLong
+      int rc;
+      if (!p->vla_built && (rc = coo_vla_build(p, st))) return rc;
+      if (p->vla_n > 0) {
+        const int64_t g1 = std::min<int64_t>((p->vla_chunks * 32 + tb - 1) / tb, cap);
+        const int64_t g2 = std::min<int64_t>((p->vla_n * 32 + tb - 1) / tb, cap);
+        const uint32_t* runs = p->vla_runs.as<uint32_t>();
+        if (p->dtype == SPMV_F64) {
+          double* S = p->vla_S.as<double>();
+          coo_vla_steps_kernel<double><<<unsigned(g1), tb, 0, st>>>(
+              rs, runs, p->vla_pre.as<uint32_t>(), p->vla_chunk_run.as<uint32_t>(), p->vla_chunks, aj,
+              static_cast<const double*>(av), static_cast<const double*>(x), col_base, lanes, width, S);
+          coo_vla_fold_kernel<double><<<unsigned(g2), tb, 0, st>>>(rs, rr, runs, p->vla_n, S, lanes,
+                                                                    static_cast<double*>(y), steps);
+        } else {
+          float* S = p->vla_S.as<float>();
+          coo_vla_steps_kernel<float><<<unsigned(g1), tb, 0, st>>>(
+              rs, runs, p->vla_pre.as<uint32_t>(), p->vla_chunk_run.as<uint32_t>(), p->vla_chunks, aj,
+              static_cast<const float*>(av), static_cast<const float*>(x), col_base, lanes, width, S);
+          coo_vla_fold_kernel<float><<<unsigned(g2), tb, 0, st>>>(rs, rr, runs, p->vla_n, S, lanes,
+                                                                   static_cast<float*>(y), steps);
+        }
+      }
     }
   } else {
     int64_t grid = p->n_runs < cap ? p->n_runs : cap;
