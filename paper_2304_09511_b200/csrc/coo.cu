@@ -64,7 +64,8 @@ struct CooSmem {
   // group block: starts | long segments | scan counts | long-row scratch
   static constexpr size_t starts_bytes = align_up(sizeof(uint16_t) * (TILE + 1), 128);
   static constexpr size_t long_bytes = align_up(sizeof(LongSeg) * max_long_segs<TILE>(), 128);
-  static constexpr size_t counts_bytes = align_up(sizeof(int) * 2 * 64, 128);
+  // warp counts, their offsets, and the boundary-row extents [128], [129]
+  static constexpr size_t counts_bytes = align_up(sizeof(int) * (2 * 64 + 2), 128);
   static constexpr size_t units_bytes = align_up(sizeof(LongUnit) * max_units<TILE>(), 128);
   static constexpr size_t upart_bytes = align_up(sizeof(T) * max_units<TILE>(), 128);
   static constexpr size_t spart_bytes = align_up(sizeof(T) * max_long_segs<TILE>(), 128);
@@ -118,6 +119,14 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
     const int excl = incl - v0 - v1;
     s_wcnt[64 + 2 * lane] = excl;
     s_wcnt[64 + 2 * lane + 1] = excl + v0;
+    // How far the tile's first / last row extends into the 32-entry windows
+    // before / after it: one ballot each instead of a serial scan.
+    const unsigned bb = __ballot_sync(0xffffffffu, rows[-1 - lane] == rows[0]);
+    const unsigned ba = __ballot_sync(0xffffffffu, rows[cnt_in + lane] == rows[cnt_in - 1]);
+    if (lane == 0) {
+      s_wcnt[128] = bb == 0xffffffffu ? kExt : __ffs(~bb) - 1;
+      s_wcnt[129] = ba == 0xffffffffu ? kExt : __ffs(~ba) - 1;
+    }
     if (lane == 31) {
       *s_nseg = incl;
       *s_nlong = 0;
@@ -151,11 +160,8 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
     const int k0 = s_start[s], k1 = s_start[s + 1];
     const uint32_t r = rows[k0];
     const bool cont_before = (k0 == 0) && rows[-1] == r;
-    int before = 0, after = 0;
-    if (cont_before)
-      while (before < kExt && rows[-1 - before] == r) ++before;
-    if (k1 == cnt_in)
-      while (after < kExt && rows[cnt_in + after] == r) ++after;
+    const int before = cont_before ? s_wcnt[128] : 0;
+    const int after = k1 == cnt_in ? s_wcnt[129] : 0;
     const int n = before + (k1 - k0) + after;
     const bool is_long = before == kExt || after == kExt || n > kExactLen;
     if (!cont_before) {
