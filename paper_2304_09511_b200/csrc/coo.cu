@@ -164,12 +164,17 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
     const int after = k1 == cnt_in ? s_wcnt[129] : 0;
     const int n = before + (k1 - k0) + after;
     const bool is_long = before == kExt || after == kExt || n > kExactLen;
-    if (!cont_before) {
-      const int64_t prev = k0 > 0 ? int64_t(rows[k0 - 1]) : (E0 > 0 ? int64_t(rows[-1]) : int64_t(-1));
-      for (int64_t q = prev + 1; q < int64_t(r); ++q) P.y[q] = T(0);
+    // Empty rows: zero-filled here by the tile owning the next row start
+    // (no y pass) unless the plan saw empty rows and pre-zeroed y (mode bit
+    // 3), which keeps long gaps off a single thread.
+    if (!(P.mode & 8)) {
+      if (!cont_before) {
+        const int64_t prev = k0 > 0 ? int64_t(rows[k0 - 1]) : (E0 > 0 ? int64_t(rows[-1]) : int64_t(-1));
+        for (int64_t q = prev + 1; q < int64_t(r); ++q) P.y[q] = T(0);
+      }
+      if (k1 == cnt_in && E0 + cnt_in == P.nnz)
+        for (int64_t q = int64_t(r) + 1; q < P.nrows; ++q) P.y[q] = T(0);
     }
-    if (k1 == cnt_in && E0 + cnt_in == P.nnz)
-      for (int64_t q = int64_t(r) + 1; q < P.nrows; ++q) P.y[q] = T(0);
     if (is_long) {
       const int idx = atomicAdd(s_nlong, 1);
       LongSeg L;
@@ -845,6 +850,10 @@ static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint3
   P.ntiles = p->ntiles;
   P.tile_begin = 0;
   P.mode = tile_mode_flags() | (tma_hint_mode() != 0 ? 4 : 0);
+  if (p->n_runs < p->nrows) {  // empty rows exist: one memset instead of per-gap loops
+    SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
+    P.mode |= 8;
+  }
   const bool aligned = (reinterpret_cast<uintptr_t>(ai) % 16 == 0) && (reinterpret_cast<uintptr_t>(aj) % 16 == 0) &&
                        (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;

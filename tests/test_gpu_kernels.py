@@ -199,6 +199,24 @@ def test_empty_and_errors(sp):
     assert sp.spmv_dia_plain(dia, np.arange(1.0, 6.0)).tolist() == [0.0] * 5
 
 
+def test_large_empty_row_gaps(sp):
+    """Rows with long empty stretches before, between and after them (the
+    COO kernel pre-zeroes y instead of filling gaps per thread)."""
+    n = 3_000_000
+    rows = np.array([5, 5, 1_000_000, 1_000_000, 1_000_001, 2_000_000])
+    cols = np.array([0, 7, 3, 4, 4, 9])
+    vals = np.array([1.5, -2.0, 3.0, 0.25, -1.0, 4.0])
+    x = np.arange(1.0, 11.0)
+    want = np.zeros(n)
+    np.add.at(want, rows, vals * x[cols])
+    coo = sp.CooMatrix.from_arrays(n, 10, rows, cols, vals, sorted=True)
+    for fmt in ("coo", "csr"):
+        m = sp.to_format(coo, fmt)
+        for version in ("plain", "vla"):
+            y = sp.dispatch(m, x, version)
+            assert bit_equal(y, want), (fmt, version)
+
+
 def test_device_io_and_out(sp):
     d = load_golden("corpus")
     name = "stencil-8"
