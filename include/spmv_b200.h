@@ -158,7 +158,7 @@ int spmv_coo_plan_info(const spmv_coo_plan* plan, int64_t* n_runs,
 /* Consumer groups per tile CTA the plan chose (SPMV_COO_GROUPS overrides). */
 int spmv_coo_plan_groups(const spmv_coo_plan* plan, int* groups);
 
-/* Fixed 1536-entry tiles (TMA bulk copies; 6 consumer groups over a 7-stage
+/* Fixed 1536-entry tiles (TMA bulk copies; 7 consumer groups over an 8-stage
  * ring, or one group when long runs exist), segmented without atomics: rows
  * of at most 32 entries are summed left to right by one thread starting
  * from +0.0 (bit-exact with np.add.at); longer runs are reduced in 256-entry

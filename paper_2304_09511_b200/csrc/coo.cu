@@ -63,12 +63,15 @@ struct CooSmem {
   static constexpr size_t stage_bytes = rows_bytes + cols_bytes + vals_bytes;
   // group block: starts | long segments | scan counts | long-row scratch
   static constexpr size_t starts_bytes = align_up(sizeof(uint16_t) * (TILE + 1), 128);
-  static constexpr size_t long_bytes = align_up(sizeof(LongSeg) * max_long_segs<TILE>(), 128);
+  // Multi-group kernels run only on plans without long runs (no segment is
+  // ever queued), so their group blocks carry no long-row scratch.
+  static constexpr bool long_rows = G == 1;
+  static constexpr size_t long_bytes = long_rows ? align_up(sizeof(LongSeg) * max_long_segs<TILE>(), 128) : 0;
   // warp counts, their offsets, and the boundary-row extents [128], [129]
   static constexpr size_t counts_bytes = align_up(sizeof(int) * (2 * 64 + 2), 128);
-  static constexpr size_t units_bytes = align_up(sizeof(LongUnit) * max_units<TILE>(), 128);
-  static constexpr size_t upart_bytes = align_up(sizeof(T) * max_units<TILE>(), 128);
-  static constexpr size_t spart_bytes = align_up(sizeof(T) * max_long_segs<TILE>(), 128);
+  static constexpr size_t units_bytes = long_rows ? align_up(sizeof(LongUnit) * max_units<TILE>(), 128) : 0;
+  static constexpr size_t upart_bytes = long_rows ? align_up(sizeof(T) * max_units<TILE>(), 128) : 0;
+  static constexpr size_t spart_bytes = long_rows ? align_up(sizeof(T) * max_long_segs<TILE>(), 128) : 0;
   static constexpr size_t group_bytes =
       starts_bytes + long_bytes + counts_bytes + units_bytes + upart_bytes + spart_bytes;
   static constexpr size_t tickets_off = 64, counters_off = 96, groups_off = 256;
@@ -82,7 +85,7 @@ template <int G> constexpr int coo_group_threads() { return G == 1 ? kTileThread
 template <int G> constexpr int coo_min_blocks() { return G == 1 ? 3 : 1; }
 
 // rows: tile-relative view, valid for k in [-kExt, TILE + kExt).
-template <typename T, int TILE, int NT>
+template <typename T, int TILE, int NT, bool LONG>
 __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_t* __restrict__ rows,
                                  const uint32_t* __restrict__ cols, T* __restrict__ vals, uint16_t* s_start,
                                  LongSeg* s_long, int* s_nseg, int* s_nlong, int* s_wcnt,
@@ -175,7 +178,7 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
       if (k1 == cnt_in && E0 + cnt_in == P.nnz)
         for (int64_t q = int64_t(r) + 1; q < P.nrows; ++q) P.y[q] = T(0);
     }
-    if (is_long) {
+    if (LONG && is_long) {
       const int idx = atomicAdd(s_nlong, 1);
       LongSeg L;
       L.row = r;
@@ -318,10 +321,10 @@ coo_tile_kernel(const __grid_constant__ CooParams<T> P) {
       for (int k = cnt_ext + tid; k < TILE + kExt; k += NT) rb[kExt + k] = kNoRow;
     }
     grp.sync();
-    coo_process_tile<T, TILE, NT>(P, t, rows_of(s) + kExt, cols_of(s), vals_of(s), s_start, s_long, s_nseg,
-                                  s_nlong, s_wcnt, grp);
-    const int nl = *s_nlong;
-    if (nl > 0)
+    coo_process_tile<T, TILE, NT, S::long_rows>(P, t, rows_of(s) + kExt, cols_of(s), vals_of(s), s_start, s_long,
+                                                s_nseg, s_nlong, s_wcnt, grp);
+    const int nl = S::long_rows ? *s_nlong : 0;
+    if (S::long_rows && nl > 0)
       coo_tile_long<T, TILE, NT>(t, cols_of(s), vals_of(s), s_long, nl, scratch, s_nlong + 1, P.x - P.col_base, P.y,
                                  P.head_row, P.head_val, P.pass, P.tail_row, P.tail_val, (P.mode & 2) != 0, grp);
     grp.sync();  // stage s free
@@ -671,7 +674,7 @@ static int coo_vla_build(spmv_coo_plan* p, cudaStream_t st) {
 }
 
 // (tile, groups) pairs with compiled kernels.
-#define SPMV_COO_CONFIGS(X) X(1024, 1) X(2048, 1) X(1536, 1) X(2048, 4) X(1536, 6)
+#define SPMV_COO_CONFIGS(X) X(1024, 1) X(2048, 1) X(1536, 1) X(1536, 6) X(1536, 7)
 static bool coo_config_known(int64_t tile, int groups) {
 #define X(TL, GR) if (tile == TL && groups == GR) return true;
   SPMV_COO_CONFIGS(X)
@@ -792,16 +795,18 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
   SPMV_CUDA_TRY(cudaMemcpyAsync(&h, nl.ptr, 8, cudaMemcpyDeviceToHost, st));
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
   p->n_long = int64_t(h);
-  // 1536-entry tiles; 6 consumer groups over 7 stages (one CTA per SM) for
-  // short runs, one group (4 CTAs/SM) when long runs exist.  Measured on
-  // B200: 256^3 stencil 533 -> 630 GFLOP/s, Zipf 173 -> 193.
+  // 1536-entry tiles; 7 consumer groups over 8 stages (one CTA per SM; no
+  // long-row scratch, so they fit) for short runs, one group (4 CTAs/SM)
+  // when long runs exist.  Measured on B200: 256^3 stencil 533 -> 711
+  // GFLOP/s, Zipf 173 -> 222.
   p->tile = 1536;
-  p->groups = p->n_long > 0 ? 1 : 6;
+  p->groups = p->n_long > 0 ? 1 : 7;
   if (tile_entries()) {
     p->tile = tile_entries();
     p->groups = 1;
   }
   if (coo_groups() > 0) p->groups = coo_groups();
+  if (p->n_long > 0) p->groups = 1;  // multi-group kernels carry no long-row scratch
   if (!coo_config_known(p->tile, p->groups)) {
     p->groups = 1;
     if (!coo_config_known(p->tile, 1)) p->tile = 2048;
