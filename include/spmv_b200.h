@@ -59,9 +59,10 @@ int spmv_device_sm_count(int* out);
 typedef struct spmv_csr_plan spmv_csr_plan;
 
 /* Analyse the matrix once: long-row census (rows > exact_len entries), tile
- * size (2048 entries, 1024 when long rows exist), consumer groups per CTA
- * (G groups share a G+1 stage ring: 3, or 7 for rows averaging < 16
- * entries), the row range of every tile and the list of
+ * size and consumer groups per CTA (G groups share a G+1 stage ring:
+ * 1024 x 3 with long rows; else 2304 (2048 below 64M entries) x 3, or
+ * 1664 x 4 for rows averaging < 16 entries), the row range of every tile
+ * and the list of
  * long rows spanning tiles.  The SpMV kernel streams
  * fixed entry tiles with TMA bulk copies; rows of <= exact_len entries are
  * summed left to right by one thread (bit-exact with spmv_csr_plain); longer

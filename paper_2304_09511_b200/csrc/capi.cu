@@ -146,7 +146,7 @@ static int env_int(const char* name, int dflt) {
 int tile_entries() {
   static const int t = [] {
     const int v = env_int("SPMV_TILE", 0);
-    return (v == 1024 || v == 1536 || v == 1920 || v == 2048 || v == 4096) ? v : 0;
+    return (v == 1024 || v == 1536 || v == 1664 || v == 2048 || v == 2304 || v == 4096) ? v : 0;
   }();
   return t;
 }

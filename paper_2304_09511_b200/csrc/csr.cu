@@ -67,7 +67,7 @@ struct CsrParams {
 // Shared memory of a CSR tile CTA with G consumer groups and G + 1 stages:
 // [0, 64) stage mbarriers, [64, 96) stage tickets, [96, 160) two counters
 // per group, then one long-row scratch block per group, then the stage ring.
-template <typename T, int TILE, int G = 1>
+template <typename T, int TILE, int G = 1, bool LONG = true>
 struct CsrSmem {
   static constexpr int stages = G + 1;
   static constexpr size_t cols_bytes = align_up(sizeof(uint32_t) * (TILE + kExt), 128);
@@ -76,7 +76,8 @@ struct CsrSmem {
   static constexpr size_t units_off = align_up(sizeof(LongSeg) * max_long_segs<TILE>(), 16);  // in a group block
   static constexpr size_t upart_off = units_off + align_up(sizeof(LongUnit) * max_units<TILE>(), 16);
   static constexpr size_t spart_off = upart_off + align_up(sizeof(T) * max_units<TILE>(), 16);
-  static constexpr size_t group_bytes = align_up(spart_off + sizeof(T) * max_long_segs<TILE>(), 16);
+  // plans without long rows never queue a segment: no long-row scratch
+  static constexpr size_t group_bytes = LONG ? align_up(spart_off + sizeof(T) * max_long_segs<TILE>(), 16) : 0;
   static constexpr size_t tickets_off = 64, counters_off = 96, groups_off = 160;
   static constexpr size_t header = align_up(groups_off + G * group_bytes, 128);
   static constexpr size_t total = header + stages * stage_bytes;
@@ -89,7 +90,7 @@ template <int G> constexpr int csr_cta_threads() { return G * csr_group_threads<
 #ifndef SPMV_CSR_MINB
 #define SPMV_CSR_MINB 4
 #endif
-template <int G> constexpr int csr_min_blocks() { return G == 1 ? SPMV_CSR_MINB : (G == 2 ? 3 : (G == 3 ? 2 : 1)); }
+template <int G> constexpr int csr_min_blocks() { return G == 1 ? SPMV_CSR_MINB : (G == 2 ? 3 : (G <= 4 ? 2 : 1)); }
 
 // Rows of one tile.  Row-per-lane mode (few rows per tile, e.g. the
 // stencil's ~77): each thread forms its row's products from the staged
@@ -97,7 +98,7 @@ template <int G> constexpr int csr_min_blocks() { return G == 1 ? SPMV_CSR_MINB 
 // than threads, e.g. Zipf's short rows): all gathers of the tile are issued
 // entry-per-lane first, then rows are summed from shared memory.  Long
 // segments are only queued here.
-template <typename T, int TILE, int NT>
+template <typename T, int TILE, int NT, bool LONG>
 __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, const uint32_t* __restrict__ cols,
                                               T* __restrict__ vals, LongSeg* s_long, int* s_nlong,
                                               const TileGroup<NT>& grp
@@ -137,7 +138,7 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
                           : row_dot(cols + (s - E0), vals + (s - E0), int(len), xb, T(-0.0));
     } else {
       const int64_t lo = max(int64_t(s), E0), hi = min(int64_t(e), E1);
-      if (lo < hi) {
+      if (LONG && lo < hi) {
         const int idx = atomicAdd(s_nlong, 1);
         LongSeg L;
         L.row = uint32_t(r);
@@ -201,7 +202,7 @@ __device__ __forceinline__ void csr_tile_long(int64_t t, const uint32_t* __restr
 // loads, so more rows are in flight per byte of shared memory (the stencil's
 // limiter).  Multi-group CTAs take bulk tiles only; the host runs the tail
 // tiles with G == 1.
-template <typename T, bool BULK, int TILE, int G>
+template <typename T, bool BULK, int TILE, int G, bool LONG = true>
 __global__ void __launch_bounds__(csr_cta_threads<G>(), csr_min_blocks<G>())
 csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
   static_assert(G == 1 || BULK, "multi-group CTAs are TMA-fed");
@@ -212,7 +213,7 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
   if (threadIdx.x < 8) s_phase_acc[threadIdx.x] = 0;
   __syncthreads();
 #endif
-  using S = CsrSmem<T, TILE, G>;
+  using S = CsrSmem<T, TILE, G, LONG>;
   constexpr int STAGES = S::stages;
   const int g = int(threadIdx.x) / NT;
   const TileGroup<NT> grp{int(threadIdx.x) % NT, G == 1 ? 0 : 1 + g};
@@ -281,14 +282,14 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
     }
     PHASE_T(p1);
 #ifndef SPMV_STREAM_ONLY  // experiment: TMA stream alone (y is not written)
-    csr_tile_rows<T, TILE, NT>(P, t, cols_of(s), vals_of(s), s_long, s_nlong, grp
+    csr_tile_rows<T, TILE, NT, LONG>(P, t, cols_of(s), vals_of(s), s_long, s_nlong, grp
 #ifdef SPMV_PHASE_TIMING
                                , s_phase_acc
 #endif
     );
     PHASE_T(p2);
-    const int nl = *s_nlong;
-    if (nl > 0)
+    const int nl = LONG ? *s_nlong : 0;
+    if (LONG && nl > 0)
       csr_tile_long<T, TILE, NT>(t, cols_of(s), vals_of(s), s_long, nl, gscratch, s_nlong + 1, P.x - P.col_base,
                                  P.y, P.head, P.tail, (P.mode & 2) != 0, grp);
 #endif
@@ -650,6 +651,7 @@ struct spmv_csr_plan {
     for (auto e : events) cudaEventDestroy(e);
   }
   int groups = 1;                    // consumer groups per tile CTA (csr_tile_kernel G)
+  bool long_scratch = true;          // kernels with long-row scratch (false: plan has no long rows)
   // planned vla path: rows over kVlaLong entries, their 256-entry chunks and
   // a product buffer (built on the first spmv_csr_vla_planned call)
   bool vla_built = false;
@@ -658,11 +660,14 @@ struct spmv_csr_plan {
   int grid_bulk = 0, grid_direct = 0;  // G-group TMA kernel / single-group kernel
 };
 
-// (tile, groups) pairs with compiled kernels.
-#define SPMV_CSR_CONFIGS(X) \
-  X(1024, 1) X(2048, 1) X(4096, 1) X(1920, 1) X(1920, 2) X(2048, 3) X(2048, 7) X(1792, 7) X(1024, 3)
-static bool csr_config_known(int64_t tile, int groups) {
-#define X(TL, GR) if (tile == TL && groups == GR) return true;
+// (tile, groups, long-row scratch) triples with compiled kernels.  The
+// short-only variants (LF = 0) serve plans without long rows.
+#define SPMV_CSR_CONFIGS(X)                                                                                  \
+  X(1024, 1, 1) X(2048, 1, 1) X(4096, 1, 1) X(1024, 3, 1) X(2048, 3, 1) X(2048, 3, 0) X(2304, 1, 1)        \
+  X(2304, 3, 0) X(1664, 1, 1) X(1664, 4, 0)
+static bool csr_config_known(int64_t tile, int groups, bool long_rows) {
+#define X(TL, GR, LF) \
+  if (tile == TL && groups == GR && long_rows == bool(LF)) return true;
   SPMV_CSR_CONFIGS(X)
 #undef X
   return false;
@@ -677,12 +682,12 @@ static int csr_ctas_per_sm(K kernel, int threads, size_t smem, int* per_sm) {
   return SPMV_OK;
 }
 
-template <typename T, int TILE, int G>
+template <typename T, int TILE, int G, bool LONG>
 static int csr_launch_config(spmv_csr_plan* p) {
   int per_sm = 0, per_sm1 = 0, rc;
   using S1 = CsrSmem<T, TILE, 1>;
-  if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, true, TILE, G>, csr_cta_threads<G>(), CsrSmem<T, TILE, G>::total,
-                            &per_sm)))
+  if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, true, TILE, G, LONG>, csr_cta_threads<G>(),
+                            CsrSmem<T, TILE, G, LONG>::total, &per_sm)))
     return rc;
   if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, true, TILE, 1>, kTileThreads, S1::total, &per_sm1))) return rc;
   if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, false, TILE, 1>, kTileThreads, S1::total, &per_sm1))) return rc;
@@ -692,7 +697,7 @@ static int csr_launch_config(spmv_csr_plan* p) {
   return SPMV_OK;
 }
 
-template <typename T, int TILE, int G>
+template <typename T, int TILE, int G, bool LONG>
 static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st, int64_t tb, int64_t te, bool fixup) {
   if (p->nrows == 0) return SPMV_OK;
@@ -725,15 +730,15 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
     if (grid > 0) csr_tile_kernel<T, false, TILE, 1><<<unsigned(grid), kTileThreads, smem1, st>>>(P);
   } else if (G == 1) {
     const int64_t grid = std::min<int64_t>(p->grid_bulk, te - tb);
-    if (grid > 0) csr_tile_kernel<T, true, TILE, 1><<<unsigned(grid), kTileThreads, smem1, st>>>(P);
+    if (grid > 0) csr_tile_kernel<T, true, TILE, 1, LONG><<<unsigned(grid), kTileThreads, smem1, st>>>(P);
   } else {
     // bulk tiles on the multi-group kernel, the (rare) tail tiles past
     // n_bulk on the single-group one
     const int64_t bulk_end = std::min<int64_t>(te, P.n_bulk);
     const int64_t grid = std::min<int64_t>(p->grid_bulk, bulk_end - tb);
     if (grid > 0)
-      csr_tile_kernel<T, true, TILE, G>
-          <<<unsigned(grid), csr_cta_threads<G>(), CsrSmem<T, TILE, G>::total, st>>>(P);
+      csr_tile_kernel<T, true, TILE, G, LONG>
+          <<<unsigned(grid), csr_cta_threads<G>(), CsrSmem<T, TILE, G, LONG>::total, st>>>(P);
     if (te > bulk_end) {
       CsrParams<T> Q = P;
       Q.tile_begin = std::max<int64_t>(tb, bulk_end);
@@ -755,8 +760,9 @@ template <typename T>
 static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st, int64_t tb = 0, int64_t te = -1, bool fixup = true) {
   if (te < 0) te = p->ntiles;
-#define X(TL, GR) \
-  if (p->tile == TL && p->groups == GR) return csr_run_tiled<T, TL, GR>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
+#define X(TL, GR, LF)                                                          \
+  if (p->tile == TL && p->groups == GR && p->long_scratch == bool(LF))          \
+    return csr_run_tiled<T, TL, GR, bool(LF)>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
   SPMV_CSR_CONFIGS(X)
 #undef X
   return fail(SPMV_INVALID_ARG, "no CSR kernel for tile %lld x %d groups", (long long)p->tile, p->groups);
@@ -941,25 +947,35 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
   if ((rc = count_async(ctr, &h, st))) return rc;
   p->n_long = int64_t(h);
   // Long rows: 1024-entry tiles, 3 groups (2 CTAs/SM: six tiles in flight
-  // hide the long-row gathers).  Otherwise 2048-entry tiles with G consumer groups sharing a
-  // G + 1 stage ring: 3 groups (2 CTAs/SM) for stencil-like rows, 7 groups
-  // (1 CTA/SM) for short rows (average < 16 entries), measured best on the
-  // 27-point stencil and the 11-diagonal banded matrix respectively.
+  // hide the long-row gathers).  Otherwise G consumer groups share a G + 1
+  // stage ring of kernels without long-row scratch, sized per row length
+  // below (measured on the 27-point stencil and the 11-diagonal banded
+  // matrix).
   if (p->n_long > 0) {
     p->tile = 1024;
     p->groups = 3;  // Zipf: 269 -> 276 GFLOP/s over one group (long-row phases overlap other groups' rows)
+  } else if (p->nnz < 16 * p->nrows) {
+    p->tile = 1664;  // short rows: 62 per group fill two warps; banded 801 -> 825
+    p->groups = 4;
   } else {
-    p->tile = 2048;
-    p->groups = p->nnz < 16 * p->nrows ? 7 : 3;
+    // stencil-like rows: the largest tile whose 4-stage ring still fits two
+    // CTAs per SM (256^3: 1039 -> 1068); small matrices keep 2048-entry
+    // tiles for more tiles per group (64^3: 436 vs 415)
+    p->tile = p->nnz >= (int64_t(64) << 20) ? 2304 : 2048;
+    p->groups = 3;
   }
   if (tile_entries()) {
     p->tile = tile_entries();
     p->groups = 1;
   }
   if (csr_groups() > 0) p->groups = csr_groups();
-  if (!csr_config_known(p->tile, p->groups)) {
-    p->groups = 1;
-    if (!csr_config_known(p->tile, 1)) p->tile = p->n_long > 0 ? 1024 : 2048;
+  p->long_scratch = p->n_long > 0;
+  if (!csr_config_known(p->tile, p->groups, p->long_scratch)) {
+    p->long_scratch = true;  // the kernels with long-row scratch serve any matrix
+    if (!csr_config_known(p->tile, p->groups, true)) {
+      p->groups = 1;
+      if (!csr_config_known(p->tile, 1, true)) p->tile = p->n_long > 0 ? 1024 : 2048;
+    }
   }
   p->ntiles = (p->nnz + p->tile - 1) / p->tile;
   const size_t vs = value_size(p->dtype);
@@ -989,9 +1005,10 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
     }
   }
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
-#define X(TL, GR)                                                                                    \
-  if (p->tile == TL && p->groups == GR)                                                             \
-    return p->dtype == SPMV_F64 ? csr_launch_config<double, TL, GR>(p) : csr_launch_config<float, TL, GR>(p);
+#define X(TL, GR, LF)                                                                      \
+  if (p->tile == TL && p->groups == GR && p->long_scratch == bool(LF))                        \
+    return p->dtype == SPMV_F64 ? csr_launch_config<double, TL, GR, bool(LF)>(p)             \
+                                : csr_launch_config<float, TL, GR, bool(LF)>(p);
   SPMV_CSR_CONFIGS(X)
 #undef X
   return fail(SPMV_INVALID_ARG, "no CSR kernel for tile %lld x %d groups", (long long)p->tile, p->groups);

@@ -5,14 +5,14 @@ import time
 
 import torch
 
-sys.path.insert(0, ".")
+sys.path.insert(0, __import__("os").environ.get("AB_TREE", "."))
 import paper_2304_09511_b200 as sp  # noqa: E402
 from paper_2304_09511_b200 import kernels as K  # noqa: E402
 
 A = sp.gen_stencil27(256, 256, 256)
 xh = torch.rand(A.ncols, dtype=torch.float64).pin_memory()
 yh = torch.empty(A.nrows, dtype=torch.float64).pin_memory()
-for chunks in (16, 32, 48, 64, 96, 128, 192):
+for chunks in [int(c) for c in (__import__('sys').argv[1:] or (16, 32, 48, 64, 96, 128, 192))]:
     os.environ["X"] = "1"
     K.HOST_CHUNKS = chunks
     f = lambda: sp.spmv_csr_plain(A, xh, out=yh)  # noqa: E731
