@@ -83,6 +83,12 @@ int spmv_csr_plan_info(const spmv_csr_plan* plan, int64_t* n_long_rows,
                        int64_t* n_items, int64_t* launches);
 /* Consumer groups per tile CTA the plan chose (SPMV_CSR_GROUPS overrides). */
 int spmv_csr_plan_groups(const spmv_csr_plan* plan, int* groups);
+/* Whole-matrix kernel the plan chose: warp_stream = 1 for the warp-stream
+ * kernel (matrices with rows longer than exact_len: one contiguous entry
+ * range per resident warp, nwarps of them), 0 for the tile kernel.  Tile
+ * ranges (spmv_csr_range, spmv_csr_host) always use the tile kernel.
+ * SPMV_CSR_WS=0/1 overrides the choice. */
+int spmv_csr_plan_path(const spmv_csr_plan* plan, int* warp_stream, int64_t* nwarps);
 
 /* y[r] = sum_j av[j] * x[aj[j] - col_base] over row r.  x holds the window
  * of global columns [col_base, col_base + x_len).  For a single-device

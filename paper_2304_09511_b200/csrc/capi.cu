@@ -189,6 +189,11 @@ int pool_keep_memory() {
   if (dev < 64) done[dev] = true;
   return SPMV_OK;
 }
+// CSR warp-stream path: -1 = plan's choice (matrices with long rows), 0 off, 1 on.
+int csr_ws_mode() {
+  static const int m = env_int("SPMV_CSR_WS", -1);
+  return m;
+}
 int ctas_per_sm_cap() {
   static const int c = env_int("SPMV_CTAS_PER_SM", 0);
   return c;

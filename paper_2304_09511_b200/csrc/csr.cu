@@ -27,6 +27,7 @@
 #include <vector>
 
 #include "tile.cuh"
+#include "wstream.cuh"
 
 namespace spmv {
 
@@ -658,6 +659,12 @@ struct spmv_csr_plan {
   int64_t vla_n = 0, vla_chunks = 0;
   DevBuf vla_rows, vla_pre, vla_chunk_row, vla_prod;
   int grid_bulk = 0, grid_direct = 0;  // G-group TMA kernel / single-group kernel
+  // warp-stream path (wstream.cuh) for plans with long rows: whole-matrix
+  // launches only; tile ranges (halo split, host pipeline) keep the tiles
+  bool ws = false;
+  bool has_empty = false;
+  int64_t ws_nwarps = 0, ws_n_span = 0;
+  DevBuf ws_bounds, ws_row0, ws_head, ws_tail, ws_span_row, ws_span_w0, ws_span_w1;
 };
 
 // (tile, groups, long-row scratch) triples with compiled kernels.  The
@@ -757,9 +764,40 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
 }
 
 template <typename T>
+static int csr_run_ws(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
+                      int64_t col_base, T* y, cudaStream_t st) {
+  if (p->has_empty) SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
+  WsParams<T> P;
+  P.irp = irp;
+  P.aj = aj;
+  P.av = av;
+  P.x = x;
+  P.y = y;
+  P.bounds = p->ws_bounds.as<uint32_t>();
+  P.row0 = p->ws_row0.as<uint32_t>();
+  P.head = p->ws_head.as<T>();
+  P.tail = p->ws_tail.as<T>();
+  P.nrows = p->nrows;
+  P.col_base = col_base;
+  P.nwarps = p->ws_nwarps;
+  const int64_t grid = (p->ws_nwarps + kWsWarps - 1) / kWsWarps;
+  csr_wstream_kernel<T><<<unsigned(grid), kWsWarps * 32, 0, st>>>(P);
+  SPMV_LAUNCH_CHECK();
+  if (p->ws_n_span > 0) {
+    const int64_t g = std::min<int64_t>((p->ws_n_span + 255) / 256, int64_t(sm_count()) * 8);
+    csr_span_fixup_kernel<T><<<unsigned(g), 256, 0, st>>>(p->ws_span_row.as<uint32_t>(), p->ws_span_w0.as<uint32_t>(),
+                                                          p->ws_span_w1.as<uint32_t>(), p->ws_n_span, P.head, P.tail,
+                                                          y);
+    SPMV_LAUNCH_CHECK();
+  }
+  return SPMV_OK;
+}
+
+template <typename T>
 static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st, int64_t tb = 0, int64_t te = -1, bool fixup = true) {
   if (te < 0) te = p->ntiles;
+  if (p->ws && tb == 0 && te == p->ntiles && fixup) return csr_run_ws<T>(p, irp, aj, av, x, col_base, y, st);
 #define X(TL, GR, LF)                                                          \
   if (p->tile == TL && p->groups == GR && p->long_scratch == bool(LF))          \
     return csr_run_tiled<T, TL, GR, bool(LF)>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
@@ -933,6 +971,58 @@ static int count_async(unsigned long long* dev, unsigned long long* host, cudaSt
   return SPMV_OK;
 }
 
+// Warp-stream plan (wstream.cuh): chosen for matrices with long rows
+// (SPMV_CSR_WS=0 / 1 overrides).  One range per resident warp.
+static int csr_ws_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st) {
+  const int mode = csr_ws_mode();
+  p->ws = mode < 0 ? p->n_long > 0 : mode > 0;
+  if (!p->ws) return SPMV_OK;
+  int rc, per_sm = 0;
+  unsigned long long* ctr = p->cnt.as<unsigned long long>();
+  unsigned long long h = 0;
+  const int64_t g_rows = std::min<int64_t>((p->nrows + 255) / 256, int64_t(sm_count()) * 16);
+  SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
+  count_empty_rows_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, p->nrows, ctr);
+  SPMV_LAUNCH_CHECK();
+  if ((rc = count_async(ctr, &h, st))) return rc;
+  p->has_empty = h > 0;
+  if (p->dtype == SPMV_F64)
+    SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_wstream_kernel<double>, kWsWarps * 32, 0));
+  else
+    SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_wstream_kernel<float>, kWsWarps * 32, 0));
+  if (ctas_per_sm_cap() > 0 && per_sm > ctas_per_sm_cap()) per_sm = ctas_per_sm_cap();
+  if (per_sm < 1) per_sm = 1;
+  // at least one chunk per warp: targets strictly increase, so no empty
+  // range sits inside a split row
+  p->ws_nwarps = std::max<int64_t>(1, std::min<int64_t>(int64_t(sm_count()) * per_sm * kWsWarps, p->nnz / kWsChunk));
+  const size_t vs = value_size(p->dtype);
+  if ((rc = p->ws_bounds.alloc(4 * (p->ws_nwarps + 1))) || (rc = p->ws_row0.alloc(4 * p->ws_nwarps)) ||
+      (rc = p->ws_head.alloc(vs * p->ws_nwarps)) || (rc = p->ws_tail.alloc(vs * p->ws_nwarps)))
+    return rc;
+  const int64_t gw = std::min<int64_t>((p->ws_nwarps + 256) / 256, int64_t(sm_count()) * 16);
+  ws_bounds_kernel<<<unsigned(gw), 256, 0, st>>>(irp, p->nrows, p->nnz, p->ws_nwarps, p->exact_len,
+                                                 p->ws_bounds.as<uint32_t>(), p->ws_row0.as<uint32_t>());
+  SPMV_LAUNCH_CHECK();
+  SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
+  ws_span_list_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, p->nrows, p->exact_len, p->ws_bounds.as<uint32_t>(),
+                                                        p->ws_nwarps, nullptr, nullptr, nullptr, ctr);
+  SPMV_LAUNCH_CHECK();
+  if ((rc = count_async(ctr, &h, st))) return rc;
+  p->ws_n_span = int64_t(h);
+  if (p->ws_n_span > 0) {
+    if ((rc = p->ws_span_row.alloc(4 * p->ws_n_span)) || (rc = p->ws_span_w0.alloc(4 * p->ws_n_span)) ||
+        (rc = p->ws_span_w1.alloc(4 * p->ws_n_span)))
+      return rc;
+    SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
+    ws_span_list_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, p->nrows, p->exact_len, p->ws_bounds.as<uint32_t>(),
+                                                          p->ws_nwarps, p->ws_span_row.as<uint32_t>(),
+                                                          p->ws_span_w0.as<uint32_t>(), p->ws_span_w1.as<uint32_t>(),
+                                                          ctr);
+    SPMV_LAUNCH_CHECK();
+  }
+  return SPMV_OK;
+}
+
 // Plan analysis (once per matrix): long-row census, tile size, per-tile row
 // ranges and the list of long rows spanning tiles.
 static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st) {
@@ -1004,6 +1094,7 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
       SPMV_LAUNCH_CHECK();
     }
   }
+  if ((rc = csr_ws_build(p, irp, st))) return rc;
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
 #define X(TL, GR, LF)                                                                      \
   if (p->tile == TL && p->groups == GR && p->long_scratch == bool(LF))                        \
@@ -1066,7 +1157,9 @@ int spmv_csr_plan_info(const spmv_csr_plan* p, int64_t* n_long_rows, int64_t* n_
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (n_long_rows) *n_long_rows = p->n_long;
   if (n_items) *n_items = p->tile;
-  if (launches)
+  if (launches && p->ws)
+    *launches = 1 + (p->ws_n_span > 0 ? 1 : 0);
+  else if (launches)
     *launches = (p->nrows > 0 ? 1 : 0) + (p->n_span > 0 ? 1 : 0) +
                 (p->groups > 1 && p->nnz > 0 && bulk_tiles(p->nnz, p->ntiles, p->tile) < p->ntiles ? 1 : 0);
   return SPMV_OK;
@@ -1075,6 +1168,13 @@ int spmv_csr_plan_info(const spmv_csr_plan* p, int64_t* n_long_rows, int64_t* n_
 int spmv_csr_plan_groups(const spmv_csr_plan* p, int* groups) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (groups) *groups = p->groups;
+  return SPMV_OK;
+}
+
+int spmv_csr_plan_path(const spmv_csr_plan* p, int* warp_stream, int64_t* nwarps) {
+  if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
+  if (warp_stream) *warp_stream = p->ws ? 1 : 0;
+  if (nwarps) *nwarps = p->ws_nwarps;
   return SPMV_OK;
 }
 

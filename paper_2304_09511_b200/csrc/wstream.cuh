@@ -1,0 +1,213 @@
+// Warp-stream SpMV for matrices whose x gathers are random (long rows,
+// uniformly scattered columns: the Zipf config C3).
+//
+// Such a matrix is bound by the L1tex wavefront queue, not by HBM: every x
+// gather is a random 32-byte L2 sector, one wavefront per lane, and an SM
+// retires about one wavefront per cycle (B300_MICROARCH "L1tex wavefront
+// queue"; tools/gather_ceiling.cu measures 240-250 G gathers/s on a B200
+// for an index stream + value stream + one gather per entry).  The kernel
+// is therefore built to issue nothing but the gathers on the LSU path:
+//   * no shared-memory staging of the stream and no CTA barriers: each warp
+//     owns one contiguous entry range [b_w, b_w+1) and walks it in chunks of
+//     32 x DEPTH entries, entry-per-lane (coalesced index/value loads,
+//     DEPTH gathers in flight per lane);
+//   * the rounded products go to a per-warp shared-memory buffer and each
+//     row is summed from there: one lane per row, left to right, continuing
+//     across chunks from a carried partial — the reference order
+//     (kernels.py:69-82), bit-exact for every row that stays inside one
+//     warp's range and has no chunk segment over kWsSeq entries;
+//   * range boundaries snap back to a row start unless the row is longer
+//     than exact_len, so only long rows are split between warps; their
+//     per-warp partials (head/tail slots) are added in warp order by the
+//     span fix-up kernel — deterministic, within 1e-12 (north_star);
+//   * a chunk segment over kWsSeq entries (only rows over kWsSeq entries
+//     have one) is summed by the whole warp (lane-strided, xor tree) and
+//     added to the row's carry.
+#pragma once
+
+#include "common.cuh"
+
+namespace spmv {
+
+constexpr int kWsDepth = 8;                    // gathers in flight per lane
+constexpr int kWsChunk = 32 * kWsDepth;        // entries per warp step
+constexpr int kWsWarps = 8;                    // warps per CTA
+constexpr uint32_t kWsSeq = 64;                // longest segment a lane sums alone
+
+template <typename T>
+struct WsParams {
+  const uint32_t* irp;
+  const uint32_t* aj;
+  const T* av;
+  const T* x;
+  T* y;
+  const uint32_t* bounds;  // nwarps + 1 entry boundaries
+  const uint32_t* row0;    // nwarps: row containing bounds[w]
+  T* head;                 // nwarps: partial of a row that started before bounds[w]
+  T* tail;                 // nwarps: partial of a row that continues past bounds[w+1]
+  int64_t nrows, col_base, nwarps;
+};
+
+template <typename T>
+__global__ void __launch_bounds__(kWsWarps * 32, 4) csr_wstream_kernel(const __grid_constant__ WsParams<T> P) {
+  __shared__ T s_prod[kWsWarps][kWsChunk];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int64_t w = int64_t(blockIdx.x) * kWsWarps + wid;
+  if (w >= P.nwarps) return;
+  const uint32_t b0 = __ldg(P.bounds + w), b1 = __ldg(P.bounds + w + 1);
+  if (b0 >= b1) return;
+  T* prod = s_prod[wid];
+  const T* xb = P.x - P.col_base;
+  const T neg0 = -T(0);
+
+  int64_t r = __ldg(P.row0 + w);      // current row (contains entry c0)
+  uint32_t rs = __ldg(P.irp + r);     // its start
+  bool head = rs < b0;                // started in an earlier warp's range
+  T carry = neg0;                     // its partial over earlier chunks
+
+  for (uint32_t c0 = b0; c0 < b1; c0 += kWsChunk) {
+    const uint32_t c1 = min(b1, c0 + uint32_t(kWsChunk));
+    // row ends of the next 32 rows: issued first, consumed after the gathers
+    const int64_t rr0 = r + lane;
+    uint32_t end = rr0 < P.nrows ? __ldg(P.irp + rr0 + 1) : 0xffffffffu;
+    // products of the chunk, entry-per-lane
+    uint32_t col[kWsDepth];
+    T val[kWsDepth];
+#pragma unroll
+    for (int k = 0; k < kWsDepth; ++k) {
+      const uint32_t e = c0 + k * 32 + lane;
+      const bool ok = e < c1;
+      col[k] = ok ? ld_stream(P.aj + e) : 0u;
+      val[k] = ok ? ld_stream(P.av + e) : T(0);
+    }
+    T g[kWsDepth];
+#pragma unroll
+    for (int k = 0; k < kWsDepth; ++k) g[k] = (c0 + k * 32 + lane < c1) ? ldx(xb + col[k]) : T(0);
+#pragma unroll
+    for (int k = 0; k < kWsDepth; ++k) prod[k * 32 + lane] = mul_rn(val[k], g[k]);
+    __syncwarp();
+
+    // rows of the chunk, 32 at a time: lane l sums row r + l's segment
+    while (true) {
+      uint32_t start = __shfl_up_sync(0xffffffffu, end, 1);
+      if (lane == 0) start = rs;
+      const bool fin = end <= c1;  // invalid lanes have end = UINT32_MAX
+      const int nfin = __popc(__ballot_sync(0xffffffffu, fin));
+      const bool active = lane <= nfin && r + lane < P.nrows;
+      const uint32_t lo = max(start, c0), hi = min(end, c1);
+      const uint32_t len = (active && hi > lo) ? hi - lo : 0u;
+      T s = lane == 0 ? carry : neg0;
+      if (len <= kWsSeq) {
+        const T* pp = prod + (lo - c0);
+        for (uint32_t i = 0; i < len; ++i) s = add_rn(s, pp[i]);
+      }
+      unsigned longs = __ballot_sync(0xffffffffu, len > kWsSeq);
+      while (longs) {
+        const int L = __ffs(longs) - 1;
+        longs &= longs - 1;
+        const uint32_t llo = __shfl_sync(0xffffffffu, lo, L) - c0;
+        const uint32_t llen = __shfl_sync(0xffffffffu, len, L);
+        T part = neg0;
+        for (uint32_t i = lane; i < llen; i += 32) part = add_rn(part, prod[llo + i]);
+#pragma unroll
+        for (int o = 16; o >= 1; o >>= 1) part = add_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+        if (lane == L) s = add_rn(s, part);
+      }
+      if (fin && active && end > start) {
+        if (lane == 0 && head)
+          P.head[w] = s;
+        else
+          P.y[r + lane] = s;
+      }
+      if (nfin < 32) {
+        // lane nfin's row continues into the next chunk (or is past nrows)
+        carry = __shfl_sync(0xffffffffu, s, nfin);
+        rs = __shfl_sync(0xffffffffu, start, nfin);
+        if (nfin > 0) head = false;
+        r += nfin;
+        break;
+      }
+      // all 32 rows finished inside the chunk: next 32 rows
+      rs = __shfl_sync(0xffffffffu, end, 31);
+      r += 32;
+      head = false;
+      carry = neg0;
+      if (rs >= c1 || r >= P.nrows) break;
+      end = r + lane < P.nrows ? __ldg(P.irp + r + lane + 1) : 0xffffffffu;
+    }
+    __syncwarp();
+  }
+  // a row still open at the end of the range continues in the next warp
+  if (lane == 0 && r < P.nrows && rs < b1) {
+    const uint32_t re = __ldg(P.irp + r + 1);
+    if (re > b1) {
+      if (head)
+        P.head[w] = carry;
+      else
+        P.tail[w] = carry;
+    }
+  }
+}
+
+// Warp ranges: target entry t = w*nnz/nwarps, snapped back to the start of
+// its row unless that row is longer than exact_len.  row0[w] is the row
+// containing bounds[w] (the last row whose start is <= it).
+__global__ void ws_bounds_kernel(const uint32_t* __restrict__ irp, int64_t nrows, int64_t nnz, int64_t nwarps,
+                                 int exact_len, uint32_t* __restrict__ bounds, uint32_t* __restrict__ row0) {
+  for (int64_t w = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; w <= nwarps; w += int64_t(gridDim.x) * blockDim.x) {
+    const uint64_t t = uint64_t(w) * uint64_t(nnz) / uint64_t(nwarps);
+    if (w == nwarps || t >= uint64_t(nnz)) {
+      bounds[w] = uint32_t(nnz);
+      if (w < nwarps) row0[w] = uint32_t(nrows);
+      continue;
+    }
+    int64_t lo = 0, hi = nrows - 1;  // last r with irp[r] <= t
+    while (lo < hi) {
+      const int64_t mid = (lo + hi + 1) >> 1;
+      if (uint64_t(irp[mid]) <= t) lo = mid; else hi = mid - 1;
+    }
+    const uint32_t s = irp[lo], e = irp[lo + 1];
+    bounds[w] = (e - s <= uint32_t(exact_len)) ? s : uint32_t(t);
+    row0[w] = uint32_t(lo);
+  }
+}
+
+// Long rows split between warp ranges: (row, first warp, last warp).
+__global__ void ws_span_list_kernel(const uint32_t* __restrict__ irp, int64_t nrows, int exact_len,
+                                    const uint32_t* __restrict__ bounds, int64_t nwarps,
+                                    uint32_t* __restrict__ span_row, uint32_t* __restrict__ span_w0,
+                                    uint32_t* __restrict__ span_w1, unsigned long long* __restrict__ n_span) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t s = irp[r], e = irp[r + 1];
+    if (e - s <= uint32_t(exact_len)) continue;
+    // last w with bounds[w] <= key (skips empty ranges)
+    auto warp_of = [&](uint32_t key) {
+      int64_t lo = 0, hi = nwarps - 1;
+      while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) >> 1;
+        if (bounds[mid] <= key) lo = mid; else hi = mid - 1;
+      }
+      return lo;
+    };
+    const int64_t w0 = warp_of(s), w1 = warp_of(e - 1);
+    if (w0 == w1) continue;
+    const unsigned long long k = atomicAdd(n_span, 1ull);
+    if (span_row) {
+      span_row[k] = uint32_t(r);
+      span_w0[k] = uint32_t(w0);
+      span_w1[k] = uint32_t(w1);
+    }
+  }
+}
+
+__global__ void count_empty_rows_kernel(const uint32_t* __restrict__ irp, int64_t nrows,
+                                        unsigned long long* __restrict__ n_empty) {
+  unsigned long long c = 0;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += int64_t(gridDim.x) * blockDim.x)
+    c += irp[r + 1] == irp[r];
+  for (int o = 16; o >= 1; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(n_empty, c);
+}
+
+}  // namespace spmv

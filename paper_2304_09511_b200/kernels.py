@@ -118,7 +118,12 @@ class _Plan:
             g = ctypes.c_int()
             _lib.call("spmv_csr_plan_info", self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c))
             _lib.call("spmv_csr_plan_groups", self.handle, ctypes.byref(g))
-            return {"long_rows": a.value, "tile": b.value, "launches": c.value, "groups": g.value}
+            ws, nw = ctypes.c_int(), ctypes.c_int64()
+            _lib.call("spmv_csr_plan_path", self.handle, ctypes.byref(ws), ctypes.byref(nw))
+            info = {"long_rows": a.value, "tile": b.value, "launches": c.value, "groups": g.value, "kernel": "tile"}
+            if ws.value:  # tile/groups still serve tile-range launches
+                info.update(kernel="warp_stream", warps=nw.value)
+            return info
         a, b, c, d, e = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_int64()
         g = ctypes.c_int()
         _lib.call("spmv_coo_plan_info", self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
