@@ -194,6 +194,14 @@ int csr_ws_mode() {
   static const int m = env_int("SPMV_CSR_WS", -1);
   return m;
 }
+// CSR warp-stream ranges per resident warp (SPMV_WS_RANGES, default 8).
+int ws_ranges_per_warp() {
+  static const int n = [] {
+    const int v = env_int("SPMV_WS_RANGES", 8);
+    return v >= 1 && v <= 64 ? v : 8;
+  }();
+  return n;
+}
 int ctas_per_sm_cap() {
   static const int c = env_int("SPMV_CTAS_PER_SM", 0);
   return c;

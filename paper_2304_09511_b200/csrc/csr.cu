@@ -663,8 +663,8 @@ struct spmv_csr_plan {
   // launches only; tile ranges (halo split, host pipeline) keep the tiles
   bool ws = false;
   bool has_empty = false;
-  int64_t ws_nwarps = 0, ws_n_span = 0;
-  DevBuf ws_bounds, ws_row0, ws_head, ws_tail, ws_span_row, ws_span_w0, ws_span_w1;
+  int64_t ws_nwarps = 0, ws_nranges = 0, ws_n_span = 0;
+  DevBuf ws_bounds, ws_row0, ws_head, ws_tail, ws_span_row, ws_span_w0, ws_span_w1, ws_ctr;
 };
 
 // (tile, groups, long-row scratch) triples with compiled kernels.  The
@@ -775,19 +775,21 @@ static int csr_run_ws(const spmv_csr_plan* p, const uint32_t* irp, const uint32_
   P.y = y;
   P.bounds = p->ws_bounds.as<uint32_t>();
   P.row0 = p->ws_row0.as<uint32_t>();
-  P.head = p->ws_head.as<T>();
-  P.tail = p->ws_tail.as<T>();
+  P.head = p->ws_head.as<double>();
+  P.tail = p->ws_tail.as<double>();
+  P.exact_len = uint32_t(p->exact_len);
   P.nrows = p->nrows;
   P.col_base = col_base;
   P.nwarps = p->ws_nwarps;
+  P.nranges = p->ws_nranges;
+  P.ctr = p->ws_ctr.as<uint32_t>();
   const int64_t grid = (p->ws_nwarps + kWsWarps - 1) / kWsWarps;
   csr_wstream_kernel<T><<<unsigned(grid), kWsWarps * 32, 0, st>>>(P);
   SPMV_LAUNCH_CHECK();
   if (p->ws_n_span > 0) {
     const int64_t g = std::min<int64_t>((p->ws_n_span + 255) / 256, int64_t(sm_count()) * 8);
-    csr_span_fixup_kernel<T><<<unsigned(g), 256, 0, st>>>(p->ws_span_row.as<uint32_t>(), p->ws_span_w0.as<uint32_t>(),
-                                                          p->ws_span_w1.as<uint32_t>(), p->ws_n_span, P.head, P.tail,
-                                                          y);
+    ws_span_fixup_kernel<T><<<unsigned(g), 256, 0, st>>>(p->ws_span_row.as<uint32_t>(), p->ws_span_w0.as<uint32_t>(),
+                                                         p->ws_span_w1.as<uint32_t>(), p->ws_n_span, P.head, P.tail, y);
     SPMV_LAUNCH_CHECK();
   }
   return SPMV_OK;
@@ -994,18 +996,22 @@ static int csr_ws_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st) 
   if (per_sm < 1) per_sm = 1;
   // at least one chunk per warp: targets strictly increase, so no empty
   // range sits inside a split row
+  // ranges: kWsRangesPerWarp per resident warp (dynamic hand-out evens out
+  // uneven row work), at least one chunk each
   p->ws_nwarps = std::max<int64_t>(1, std::min<int64_t>(int64_t(sm_count()) * per_sm * kWsWarps, p->nnz / kWsChunk));
-  const size_t vs = value_size(p->dtype);
-  if ((rc = p->ws_bounds.alloc(4 * (p->ws_nwarps + 1))) || (rc = p->ws_row0.alloc(4 * p->ws_nwarps)) ||
-      (rc = p->ws_head.alloc(vs * p->ws_nwarps)) || (rc = p->ws_tail.alloc(vs * p->ws_nwarps)))
+  p->ws_nranges = std::max<int64_t>(p->ws_nwarps, std::min<int64_t>(p->ws_nwarps * ws_ranges_per_warp(), p->nnz / kWsChunk));
+  const int64_t nr = p->ws_nranges;
+  if ((rc = p->ws_bounds.alloc(4 * (nr + 1))) || (rc = p->ws_row0.alloc(4 * nr)) ||
+      (rc = p->ws_head.alloc(8 * nr)) || (rc = p->ws_tail.alloc(8 * nr)) || (rc = p->ws_ctr.alloc(8)))
     return rc;
-  const int64_t gw = std::min<int64_t>((p->ws_nwarps + 256) / 256, int64_t(sm_count()) * 16);
-  ws_bounds_kernel<<<unsigned(gw), 256, 0, st>>>(irp, p->nrows, p->nnz, p->ws_nwarps, p->exact_len,
+  SPMV_CUDA_TRY(cudaMemsetAsync(p->ws_ctr.ptr, 0, 8, st));
+  const int64_t gw = std::min<int64_t>((nr + 256) / 256, int64_t(sm_count()) * 16);
+  ws_bounds_kernel<<<unsigned(gw), 256, 0, st>>>(irp, p->nrows, p->nnz, nr, p->exact_len,
                                                  p->ws_bounds.as<uint32_t>(), p->ws_row0.as<uint32_t>());
   SPMV_LAUNCH_CHECK();
   SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
   ws_span_list_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, p->nrows, p->exact_len, p->ws_bounds.as<uint32_t>(),
-                                                        p->ws_nwarps, nullptr, nullptr, nullptr, ctr);
+                                                        nr, nullptr, nullptr, nullptr, ctr);
   SPMV_LAUNCH_CHECK();
   if ((rc = count_async(ctr, &h, st))) return rc;
   p->ws_n_span = int64_t(h);
@@ -1015,7 +1021,7 @@ static int csr_ws_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st) 
       return rc;
     SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
     ws_span_list_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, p->nrows, p->exact_len, p->ws_bounds.as<uint32_t>(),
-                                                          p->ws_nwarps, p->ws_span_row.as<uint32_t>(),
+                                                          nr, p->ws_span_row.as<uint32_t>(),
                                                           p->ws_span_w0.as<uint32_t>(), p->ws_span_w1.as<uint32_t>(),
                                                           ctr);
     SPMV_LAUNCH_CHECK();

@@ -7,9 +7,10 @@
 // queue"; tools/gather_ceiling.cu measures 240-250 G gathers/s on a B200
 // for an index stream + value stream + one gather per entry).  The kernel
 // is therefore built to issue nothing but the gathers on the LSU path:
-//   * no shared-memory staging of the stream and no CTA barriers: each warp
-//     owns one contiguous entry range [b_w, b_w+1) and walks it in chunks of
-//     32 x DEPTH entries, entry-per-lane (coalesced index/value loads,
+//   * no shared-memory staging of the stream and no CTA barriers: the
+//     entries are cut into contiguous ranges [b_w, b_w+1) (a few per warp,
+//     handed out by an atomic counter) and a warp walks a range in chunks
+//     of 32 x DEPTH entries, entry-per-lane (coalesced index/value loads,
 //     DEPTH gathers in flight per lane);
 //   * the rounded products go to a per-warp shared-memory buffer and each
 //     row is summed from there: one lane per row, left to right, continuing
@@ -29,10 +30,30 @@
 
 namespace spmv {
 
-constexpr int kWsDepth = 8;                    // gathers in flight per lane
+#ifndef SPMV_WS_DEPTH
+#define SPMV_WS_DEPTH 8
+#endif
+#ifndef SPMV_WS_SEQ
+#define SPMV_WS_SEQ 64
+#endif
+#ifndef SPMV_WS_MINB
+#define SPMV_WS_MINB 4
+#endif
+#ifndef SPMV_WS_LDG
+#define SPMV_WS_LDG 0
+#endif
+// matrix stream loads (column indices, values)
+template <typename T> __device__ __forceinline__ T ws_ld(const T* p) {
+#if SPMV_WS_LDG
+  return __ldg(p);
+#else
+  return ld_stream(p);
+#endif
+}
+constexpr int kWsDepth = SPMV_WS_DEPTH;        // gathers in flight per lane
 constexpr int kWsChunk = 32 * kWsDepth;        // entries per warp step
 constexpr int kWsWarps = 8;                    // warps per CTA
-constexpr uint32_t kWsSeq = 64;                // longest segment a lane sums alone
+constexpr uint32_t kWsSeq = SPMV_WS_SEQ;       // longest segment a lane sums alone
 
 template <typename T>
 struct WsParams {
@@ -41,51 +62,102 @@ struct WsParams {
   const T* av;
   const T* x;
   T* y;
-  const uint32_t* bounds;  // nwarps + 1 entry boundaries
-  const uint32_t* row0;    // nwarps: row containing bounds[w]
-  T* head;                 // nwarps: partial of a row that started before bounds[w]
-  T* tail;                 // nwarps: partial of a row that continues past bounds[w+1]
-  int64_t nrows, col_base, nwarps;
+  const uint32_t* bounds;  // nranges + 1 entry boundaries
+  const uint32_t* row0;    // nranges: row containing bounds[w]
+  double* head;            // nranges: partial of a row that started before bounds[w]
+  double* tail;            // nranges: partial of a row that continues past bounds[w+1]
+  uint32_t* ctr;           // [next range - nwarps, warps done]; zero between launches
+  int64_t nrows, col_base, nwarps, nranges;
+  uint32_t exact_len;
 };
 
+// Row sums accumulate in double.  f64: the plain rounded sum.  f32: rows of
+// at most exact_len entries add in float (every partial is a float, so this
+// is the reference's f32 left-to-right sum, bit-exact); longer rows keep a
+// double partial and round once at the end — no worse than the reference
+// against the exact sum (the f32 bar is 1e-5 against the
+// f64-evaluated product).
+__device__ __forceinline__ double ws_add(double s, double p, bool) { return __dadd_rn(s, p); }
+__device__ __forceinline__ double ws_add(double s, float p, bool exact) {
+  return exact ? double(__fadd_rn(float(s), p)) : __dadd_rn(s, double(p));
+}
+
+// One entry range [bounds[w], bounds[w+1]) walked by one warp.
 template <typename T>
-__global__ void __launch_bounds__(kWsWarps * 32, 4) csr_wstream_kernel(const __grid_constant__ WsParams<T> P) {
-  __shared__ T s_prod[kWsWarps][kWsChunk];
-  const int lane = threadIdx.x & 31;
-  const int wid = threadIdx.x >> 5;
-  const int64_t w = int64_t(blockIdx.x) * kWsWarps + wid;
-  if (w >= P.nwarps) return;
+__device__ __forceinline__ void csr_ws_range(const WsParams<T>& P, const int64_t w, T* __restrict__ prod,
+                                             const int lane) {
   const uint32_t b0 = __ldg(P.bounds + w), b1 = __ldg(P.bounds + w + 1);
   if (b0 >= b1) return;
-  T* prod = s_prod[wid];
   const T* xb = P.x - P.col_base;
-  const T neg0 = -T(0);
+  const double neg0 = -0.0;
 
   int64_t r = __ldg(P.row0 + w);      // current row (contains entry c0)
   uint32_t rs = __ldg(P.irp + r);     // its start
   bool head = rs < b0;                // started in an earlier warp's range
-  T carry = neg0;                     // its partial over earlier chunks
+  double carry = neg0;                // its partial over earlier chunks (see ws_add)
 
-  for (uint32_t c0 = b0; c0 < b1; c0 += kWsChunk) {
-    const uint32_t c1 = min(b1, c0 + uint32_t(kWsChunk));
+  // column indices run one chunk ahead: their HBM latency overlaps the
+  // previous chunk's gathers and row sums
+  uint32_t col[kWsDepth];
+#pragma unroll
+  for (int k = 0; k < kWsDepth; ++k) {
+    const uint32_t e = b0 + k * 32 + lane;
+    col[k] = e < b1 ? ws_ld(P.aj + e) : 0u;
+  }
+  for (uint32_t c0 = b0, c1; c0 < b1; c0 = c1) {
+    c1 = b1 - c0 > uint32_t(kWsChunk) ? c0 + uint32_t(kWsChunk) : b1;  // no uint32 wrap near 2^32 entries
     // row ends of the next 32 rows: issued first, consumed after the gathers
-    const int64_t rr0 = r + lane;
-    uint32_t end = rr0 < P.nrows ? __ldg(P.irp + rr0 + 1) : 0xffffffffu;
-    // products of the chunk, entry-per-lane
-    uint32_t col[kWsDepth];
-    T val[kWsDepth];
+    uint32_t end = r + lane < P.nrows ? __ldg(P.irp + r + lane + 1) : 0xffffffffu;
+    T p[kWsDepth];
+    {
+      T val[kWsDepth];
 #pragma unroll
-    for (int k = 0; k < kWsDepth; ++k) {
-      const uint32_t e = c0 + k * 32 + lane;
-      const bool ok = e < c1;
-      col[k] = ok ? ld_stream(P.aj + e) : 0u;
-      val[k] = ok ? ld_stream(P.av + e) : T(0);
+      for (int k = 0; k < kWsDepth; ++k) {
+        const uint32_t e = c0 + k * 32 + lane;
+        val[k] = e < c1 ? ws_ld(P.av + e) : T(0);
+      }
+#pragma unroll
+      for (int k = 0; k < kWsDepth; ++k) p[k] = (c0 + k * 32 + lane < c1) ? ldx(xb + col[k]) : T(0);
+#pragma unroll
+      for (int k = 0; k < kWsDepth; ++k) {
+        const uint32_t e = c1 + k * 32 + lane;
+        col[k] = (c1 < b1 && e < b1 && e >= c1) ? ws_ld(P.aj + e) : 0u;
+      }
+#pragma unroll
+      for (int k = 0; k < kWsDepth; ++k) p[k] = mul_rn(val[k], p[k]);
     }
-    T g[kWsDepth];
+#ifdef SPMV_WS_NOROWS  // experiment: gathers and products only (results wrong)
+    for (int k = 0; k < kWsDepth; ++k) carry = add_rn(carry, double(p[k]));
+    if (end == 0) P.head[w] = carry;
+    continue;
+#endif
+    const uint32_t end0 = __shfl_sync(0xffffffffu, end, 0);
+    if (end0 >= c1 && c1 - c0 == uint32_t(kWsChunk)) {
+      // the whole chunk lies in row r (so the row has over kWsChunk entries):
+      // lane partials in k order, xor tree, added to the carry — no shared
+      // memory round trip
+      double part = p[0];
 #pragma unroll
-    for (int k = 0; k < kWsDepth; ++k) g[k] = (c0 + k * 32 + lane < c1) ? ldx(xb + col[k]) : T(0);
+      for (int k = 1; k < kWsDepth; ++k) part = add_rn(part, double(p[k]));
 #pragma unroll
-    for (int k = 0; k < kWsDepth; ++k) prod[k * 32 + lane] = mul_rn(val[k], g[k]);
+      for (int o = 16; o >= 1; o >>= 1) part = add_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
+      carry = add_rn(carry, part);
+      if (end0 == c1) {  // row r ends exactly here
+        if (lane == 0) {
+          if (head)
+            P.head[w] = carry;
+          else
+            P.y[r] = T(carry);
+        }
+        r += 1;
+        rs = c1;
+        head = false;
+        carry = neg0;
+      }
+      continue;
+    }
+#pragma unroll
+    for (int k = 0; k < kWsDepth; ++k) prod[k * 32 + lane] = p[k];
     __syncwarp();
 
     // rows of the chunk, 32 at a time: lane l sums row r + l's segment
@@ -97,10 +169,11 @@ __global__ void __launch_bounds__(kWsWarps * 32, 4) csr_wstream_kernel(const __g
       const bool active = lane <= nfin && r + lane < P.nrows;
       const uint32_t lo = max(start, c0), hi = min(end, c1);
       const uint32_t len = (active && hi > lo) ? hi - lo : 0u;
-      T s = lane == 0 ? carry : neg0;
+      const bool exact = end - start <= P.exact_len;
+      double s = lane == 0 ? carry : neg0;
       if (len <= kWsSeq) {
         const T* pp = prod + (lo - c0);
-        for (uint32_t i = 0; i < len; ++i) s = add_rn(s, pp[i]);
+        for (uint32_t i = 0; i < len; ++i) s = ws_add(s, pp[i], exact);
       }
       unsigned longs = __ballot_sync(0xffffffffu, len > kWsSeq);
       while (longs) {
@@ -108,8 +181,8 @@ __global__ void __launch_bounds__(kWsWarps * 32, 4) csr_wstream_kernel(const __g
         longs &= longs - 1;
         const uint32_t llo = __shfl_sync(0xffffffffu, lo, L) - c0;
         const uint32_t llen = __shfl_sync(0xffffffffu, len, L);
-        T part = neg0;
-        for (uint32_t i = lane; i < llen; i += 32) part = add_rn(part, prod[llo + i]);
+        double part = neg0;
+        for (uint32_t i = lane; i < llen; i += 32) part = add_rn(part, double(prod[llo + i]));
 #pragma unroll
         for (int o = 16; o >= 1; o >>= 1) part = add_rn(part, __shfl_xor_sync(0xffffffffu, part, o));
         if (lane == L) s = add_rn(s, part);
@@ -118,7 +191,7 @@ __global__ void __launch_bounds__(kWsWarps * 32, 4) csr_wstream_kernel(const __g
         if (lane == 0 && head)
           P.head[w] = s;
         else
-          P.y[r + lane] = s;
+          P.y[r + lane] = T(s);
       }
       if (nfin < 32) {
         // lane nfin's row continues into the next chunk (or is past nrows)
@@ -147,6 +220,43 @@ __global__ void __launch_bounds__(kWsWarps * 32, 4) csr_wstream_kernel(const __g
       else
         P.tail[w] = carry;
     }
+  }
+}
+
+// Persistent warps over nranges ranges: warp w starts on range w, then takes
+// ranges nwarps, nwarps+1, ... from an atomic counter (uneven row work
+// evens out).  The last warp to finish resets the counters for the next
+// launch (stream order), so a plan must not run on two streams at once.
+template <typename T>
+__global__ void __launch_bounds__(kWsWarps * 32, SPMV_WS_MINB) csr_wstream_kernel(const __grid_constant__ WsParams<T> P) {
+  __shared__ T s_prod[kWsWarps][kWsChunk];
+  const int lane = threadIdx.x & 31;
+  const int wid = threadIdx.x >> 5;
+  const int64_t w = int64_t(blockIdx.x) * kWsWarps + wid;
+  if (w >= P.nwarps) return;
+  for (int64_t q = w; q < P.nranges;) {
+    csr_ws_range(P, q, s_prod[wid], lane);
+    uint32_t nq = 0;
+    if (lane == 0) nq = atomicAdd(P.ctr, 1u);
+    q = P.nwarps + int64_t(__shfl_sync(0xffffffffu, nq, 0));
+  }
+  if (lane == 0 && atomicAdd(P.ctr + 1, 1u) == uint32_t(P.nwarps - 1)) {
+    atomicExch(P.ctr, 0u);
+    atomicExch(P.ctr + 1, 0u);
+  }
+}
+
+// Rows split between ranges: y = tail[w0] + head[w0+1] + ... + head[w1].
+template <typename T>
+__global__ void ws_span_fixup_kernel(const uint32_t* __restrict__ span_row, const uint32_t* __restrict__ span_w0,
+                                     const uint32_t* __restrict__ span_w1, int64_t n_span,
+                                     const double* __restrict__ head, const double* __restrict__ tail,
+                                     T* __restrict__ y) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_span; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t w0 = span_w0[i], w1 = span_w1[i];
+    double sum = tail[w0];
+    for (uint32_t u = w0 + 1; u <= w1; ++u) sum = __dadd_rn(sum, head[u]);
+    y[span_row[i]] = T(sum);
   }
 }
 
