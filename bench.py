@@ -227,6 +227,8 @@ def plan_of(sp, m) -> dict:
         return {"tile": i["tile"], "groups": i["groups"]}
     if m.format == sp.Format.COO:
         i = K.coo_plan(m).info()
+        if i["kernel"] == "warp_stream":
+            return {"kernel": "warp_stream", "warps": i["warps"]}
         return {"tile": i["tile"], "groups": i["groups"]}
     return {}
 

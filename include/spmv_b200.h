@@ -163,6 +163,10 @@ int spmv_coo_plan_info(const spmv_coo_plan* plan, int64_t* n_runs,
                        int64_t* n_long_runs, int64_t* n_items,
                        int* row_sorted, int64_t* launches);
 /* Consumer groups per tile CTA the plan chose (SPMV_COO_GROUPS overrides). */
+/* Whole-matrix kernel the COO plan chose: warp_stream = 1 for the
+ * warp-stream kernel (plans with runs longer than 32 entries), else the
+ * tile kernel.  SPMV_COO_WS=0/1 overrides the choice. */
+int spmv_coo_plan_path(const spmv_coo_plan* plan, int* warp_stream, int64_t* nwarps);
 int spmv_coo_plan_groups(const spmv_coo_plan* plan, int* groups);
 
 /* Fixed 1536-entry tiles (TMA bulk copies; 7 consumer groups over an 8-stage

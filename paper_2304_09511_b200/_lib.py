@@ -60,6 +60,7 @@ SIGNATURES = {
     "spmv_csr_plan_groups": [_vp, _pint],
     "spmv_csr_plan_path": [_vp, _pint, _pi64],
     "spmv_coo_plan_groups": [_vp, _pint],
+    "spmv_coo_plan_path": [_vp, _pint, _pi64],
     "spmv_csr_host": [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _vp],
     "spmv_csr_plan_tile_info": [_vp, _vp, _vp, _vp, _vp],
     "spmv_csr_range": [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _c_int, _vp],

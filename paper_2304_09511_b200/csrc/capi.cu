@@ -194,6 +194,11 @@ int csr_ws_mode() {
   static const int m = env_int("SPMV_CSR_WS", -1);
   return m;
 }
+// COO warp-stream path: -1 = plan's choice (plans with long runs), 0 off, 1 on.
+int coo_ws_mode() {
+  static const int m = env_int("SPMV_COO_WS", -1);
+  return m;
+}
 // CSR warp-stream ranges per resident warp (SPMV_WS_RANGES, default 8).
 int ws_ranges_per_warp() {
   static const int n = [] {

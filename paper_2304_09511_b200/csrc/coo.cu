@@ -30,6 +30,7 @@
 #include <vector>
 
 #include "tile.cuh"
+#include "wstream.cuh"
 
 namespace spmv {
 
@@ -630,6 +631,10 @@ struct spmv_coo_plan {
   bool vla_built = false;
   int64_t vla_n = 0, vla_chunks = 0;
   DevBuf vla_runs, vla_pre, vla_chunk_run, vla_S;
+  // warp-stream path (wstream.cuh) for plans with long runs
+  bool ws = false;
+  int64_t ws_nwarps = 0, ws_nranges = 0, ws_n_span = 0;
+  DevBuf ws_bounds, ws_row0, ws_head, ws_tail, ws_ctr, ws_span_run, ws_span_w0, ws_span_w1;
 };
 
 static int coo_vla_build(spmv_coo_plan* p, cudaStream_t st) {
@@ -712,6 +717,58 @@ static int coo_launch_config(spmv_coo_plan* p) {
   const int64_t cap = int64_t(sm_count()) * per_sm, cap1 = int64_t(sm_count()) * per_sm1;
   p->grid = int(p->ntiles < cap ? p->ntiles : cap);
   p->grid_direct = int(p->ntiles < cap1 ? p->ntiles : cap1);
+  return SPMV_OK;
+}
+
+// Warp-stream plan: entry ranges snapped to run starts (short runs stay
+// whole), split long runs listed for the fix-up.  SPMV_COO_WS=0/1 overrides
+// the choice (plans with long runs).
+static int coo_ws_build(spmv_coo_plan* p, cudaStream_t st) {
+  const int mode = coo_ws_mode();
+  p->ws = mode < 0 ? p->n_long > 0 : mode > 0;
+  if (!p->ws) return SPMV_OK;
+  int rc, per_sm = 0;
+  if (p->dtype == SPMV_F64)
+    SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coo_wstream_kernel<double>, kWsWarps * 32, 0));
+  else
+    SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coo_wstream_kernel<float>, kWsWarps * 32, 0));
+  if (ctas_per_sm_cap() > 0 && per_sm > ctas_per_sm_cap()) per_sm = ctas_per_sm_cap();
+  if (per_sm < 1) per_sm = 1;
+  p->ws_nwarps = std::max<int64_t>(1, std::min<int64_t>(int64_t(sm_count()) * per_sm * kWsWarps, p->nnz / kWsChunk));
+  p->ws_nranges =
+      std::max<int64_t>(p->ws_nwarps, std::min<int64_t>(p->ws_nwarps * ws_ranges_per_warp(), p->nnz / kWsChunk));
+  const int64_t nr = p->ws_nranges;
+  if ((rc = p->ws_bounds.alloc(4 * (nr + 1))) || (rc = p->ws_row0.alloc(4 * nr)) || (rc = p->ws_head.alloc(8 * nr)) ||
+      (rc = p->ws_tail.alloc(8 * nr)) || (rc = p->ws_ctr.alloc(8)))
+    return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(p->ws_ctr.ptr, 0, 8, st));
+  const uint32_t* rs = p->run_start.as<uint32_t>();
+  const int64_t gw = std::min<int64_t>((nr + 256) / 256, int64_t(sm_count()) * 16);
+  ws_bounds_kernel<<<unsigned(gw), 256, 0, st>>>(rs, p->n_runs, p->nnz, nr, kExactLen, p->ws_bounds.as<uint32_t>(),
+                                                 p->ws_row0.as<uint32_t>());
+  SPMV_LAUNCH_CHECK();
+  DevBuf ctr;
+  if ((rc = ctr.alloc(8))) return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(ctr.ptr, 0, 8, st));
+  const int64_t g_runs = std::min<int64_t>((p->n_runs + 255) / 256, int64_t(sm_count()) * 16);
+  ws_span_list_kernel<<<unsigned(g_runs), 256, 0, st>>>(rs, p->n_runs, kExactLen, p->ws_bounds.as<uint32_t>(), nr,
+                                                        nullptr, nullptr, nullptr, ctr.as<unsigned long long>());
+  SPMV_LAUNCH_CHECK();
+  unsigned long long h = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&h, ctr.ptr, 8, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  p->ws_n_span = int64_t(h);
+  if (p->ws_n_span > 0) {
+    if ((rc = p->ws_span_run.alloc(4 * p->ws_n_span)) || (rc = p->ws_span_w0.alloc(4 * p->ws_n_span)) ||
+        (rc = p->ws_span_w1.alloc(4 * p->ws_n_span)))
+      return rc;
+    SPMV_CUDA_TRY(cudaMemsetAsync(ctr.ptr, 0, 8, st));
+    ws_span_list_kernel<<<unsigned(g_runs), 256, 0, st>>>(rs, p->n_runs, kExactLen, p->ws_bounds.as<uint32_t>(), nr,
+                                                          p->ws_span_run.as<uint32_t>(), p->ws_span_w0.as<uint32_t>(),
+                                                          p->ws_span_w1.as<uint32_t>(), ctr.as<unsigned long long>());
+    SPMV_LAUNCH_CHECK();
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  }
   return SPMV_OK;
 }
 
@@ -812,6 +869,7 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
     if (!coo_config_known(p->tile, 1)) p->tile = 2048;
   }
   p->ntiles = (nnz + p->tile - 1) / p->tile;
+  if ((rc = coo_ws_build(p, st))) return rc;
   const size_t vs = value_size(p->dtype);
   if ((rc = p->head_row.alloc(4 * p->ntiles)) || (rc = p->tail_row.alloc(4 * p->ntiles)) ||
       (rc = p->pass.alloc(4 * p->ntiles)) || (rc = p->head_val.alloc(vs * p->ntiles)) ||
@@ -889,8 +947,46 @@ static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint3
 }
 
 template <typename T>
+static int coo_run_ws(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const T* av, const T* x,
+                      int64_t col_base, T* y, cudaStream_t st) {
+  if (!p->row_sorted) {
+    ai = p->sorted_ai.as<uint32_t>();
+    aj = p->sorted_aj.as<uint32_t>();
+    av = p->sorted_av.as<T>();
+  }
+  if (p->n_runs < p->nrows) SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));  // empty rows
+  CooWsParams<T> P;
+  P.ai = ai;
+  P.aj = aj;
+  P.av = av;
+  P.x = x;
+  P.y = y;
+  P.bounds = p->ws_bounds.as<uint32_t>();
+  P.head = p->ws_head.as<double>();
+  P.tail = p->ws_tail.as<double>();
+  P.ctr = p->ws_ctr.as<uint32_t>();
+  P.col_base = col_base;
+  P.nwarps = p->ws_nwarps;
+  P.nranges = p->ws_nranges;
+  P.nnz = p->nnz;
+  P.exact_len = uint32_t(kExactLen);
+  const int64_t grid = (p->ws_nwarps + kWsWarps - 1) / kWsWarps;
+  coo_wstream_kernel<T><<<unsigned(grid), kWsWarps * 32, 0, st>>>(P);
+  SPMV_LAUNCH_CHECK();
+  if (p->ws_n_span > 0) {
+    const int64_t g = std::min<int64_t>((p->ws_n_span + 255) / 256, int64_t(sm_count()) * 8);
+    ws_span_fixup_kernel<T><<<unsigned(g), 256, 0, st>>>(p->ws_span_run.as<uint32_t>(), p->ws_span_w0.as<uint32_t>(),
+                                                         p->ws_span_w1.as<uint32_t>(), p->ws_n_span, P.head, P.tail, y,
+                                                         p->run_row.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+  }
+  return SPMV_OK;
+}
+
+template <typename T>
 static int coo_run(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st) {
+  if (p->ws && p->nrows > 0 && p->nnz > 0) return coo_run_ws<T>(p, ai, aj, av, x, col_base, y, st);
 #define X(TL, GR) \
   if (p->tile == TL && p->groups == GR) return coo_run_tiled<T, TL, GR>(p, ai, aj, av, x, col_base, y, st);
   SPMV_COO_CONFIGS(X)
@@ -936,9 +1032,18 @@ int spmv_coo_plan_info(const spmv_coo_plan* p, int64_t* n_runs, int64_t* n_long_
   if (n_long_runs) *n_long_runs = p->n_long;
   if (n_items) *n_items = p->tile;
   if (row_sorted) *row_sorted = p->row_sorted ? 1 : 0;
-  if (launches)
+  if (launches && p->ws)
+    *launches = 1 + (p->ws_n_span > 0 ? 1 : 0);
+  else if (launches)
     *launches = (p->nrows > 0 ? 1 : 0) + (p->n_long > 0 ? 1 : 0) +
                 (p->groups > 1 && p->nnz > 0 && bulk_tiles(p->nnz, p->ntiles, p->tile) < p->ntiles ? 1 : 0);
+  return SPMV_OK;
+}
+
+int spmv_coo_plan_path(const spmv_coo_plan* p, int* warp_stream, int64_t* nwarps) {
+  if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
+  if (warp_stream) *warp_stream = p->ws ? 1 : 0;
+  if (nwarps) *nwarps = p->ws_nwarps;
   return SPMV_OK;
 }
 

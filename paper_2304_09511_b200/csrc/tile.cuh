@@ -29,6 +29,7 @@ int coo_groups();       // SPMV_COO_GROUPS: 0 = plan choice
 int tma_hint_mode();    // SPMV_TMA_HINT: -1 auto, 0 off, 1 on
 int tile_mode_flags();
 int csr_ws_mode();      // SPMV_CSR_WS: -1 plan choice, 0 off, 1 on
+int coo_ws_mode();      // SPMV_COO_WS: -1 plan choice, 0 off, 1 on
 int ws_ranges_per_warp();  // SPMV_WS_RANGES: entry ranges per resident warp  // experiments: bit0 no products mode, bit1 warp-per-segment long rows
 
 static_assert(kExt == kExactLen, "extension must cover a whole short row");

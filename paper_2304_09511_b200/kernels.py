@@ -129,8 +129,13 @@ class _Plan:
         _lib.call("spmv_coo_plan_info", self.handle, ctypes.byref(a), ctypes.byref(b), ctypes.byref(c),
                   ctypes.byref(d), ctypes.byref(e))
         _lib.call("spmv_coo_plan_groups", self.handle, ctypes.byref(g))
-        return {"runs": a.value, "long_runs": b.value, "tile": c.value, "row_sorted": bool(d.value),
-                "launches": e.value, "groups": g.value}
+        ws, nw = ctypes.c_int(), ctypes.c_int64()
+        _lib.call("spmv_coo_plan_path", self.handle, ctypes.byref(ws), ctypes.byref(nw))
+        info = {"runs": a.value, "long_runs": b.value, "tile": c.value, "row_sorted": bool(d.value),
+                "launches": e.value, "groups": g.value, "kernel": "tile"}
+        if ws.value:
+            info.update(kernel="warp_stream", warps=nw.value)
+        return info
 
 
 def csr_plan(A: CsrMatrix, exact_len: int = 0) -> _Plan:
