@@ -49,6 +49,7 @@ struct CooParams {
   int64_t nrows, nnz, col_base, ntiles, n_bulk;
   int64_t tile_begin;  // first tile of the launch's tail range (tail-only launches)
   int mode;
+  int vla;  // lanes L of a vla tile launch (template VW = next_pow2(L) > 0)
 };
 
 // Shared memory of a COO tile CTA with G consumer groups over G + 1 stages
@@ -86,7 +87,7 @@ template <int G> constexpr int coo_group_threads() { return G == 1 ? kTileThread
 template <int G> constexpr int coo_min_blocks() { return G == 1 ? 3 : 1; }
 
 // rows: tile-relative view, valid for k in [-kExt, TILE + kExt).
-template <typename T, int TILE, int NT, bool LONG>
+template <typename T, int TILE, int NT, bool LONG, int VW = 0>
 __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_t* __restrict__ rows,
                                  const uint32_t* __restrict__ cols, T* __restrict__ vals, uint16_t* s_start,
                                  LongSeg* s_long, int* s_nseg, int* s_nlong, int* s_wcnt,
@@ -152,7 +153,7 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
   const int nseg = *s_nseg;
   // Many short rows (more segments than threads): issue the whole tile's
   // gathers entry-per-lane first (see tile.cuh form_products).
-  const bool products = (P.mode & 1) && nseg > NT;
+  const bool products = VW == 0 && (P.mode & 1) && nseg > NT;
   if (products) {
     form_products<T, NT>(cols, vals, cnt_ext, xb, tid);
     grp.sync();
@@ -189,9 +190,12 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
       L.s = L.e = 0;
       s_long[idx] = L;
     } else if (!cont_before) {
-      // +0.0 seed: np.add.at accumulates into a zeroed y
-      P.y[r] = products ? row_sum(vals + k0, k1 + after - k0, T(0))
-                        : row_dot(cols + k0, vals + k0, k1 + after - k0, xb, T(0));
+      if constexpr (VW > 0)
+        P.y[r] = row_vla_coo<T, VW>(cols + k0, vals + k0, k1 + after - k0, xb, P.vla);
+      else
+        // +0.0 seed: np.add.at accumulates into a zeroed y
+        P.y[r] = products ? row_sum(vals + k0, k1 + after - k0, T(0))
+                          : row_dot(cols + k0, vals + k0, k1 + after - k0, xb, T(0));
     }
   }
   grp.sync();
@@ -232,7 +236,7 @@ __device__ __forceinline__ void coo_tile_long(int64_t t, const uint32_t* __restr
 // G == 1: one 256-thread group over a double buffer.  G > 1: G groups of
 // 128 threads over G + 1 stages (tile i of the CTA -> group i % G, stage
 // i % (G + 1)), bulk tiles only; the host runs tail tiles with G == 1.
-template <typename T, bool BULK, int TILE, int G>
+template <typename T, bool BULK, int TILE, int G, int VW = 0>
 __global__ void __launch_bounds__(G * coo_group_threads<G>(), coo_min_blocks<G>())
 coo_tile_kernel(const __grid_constant__ CooParams<T> P) {
   static_assert(G == 1 || BULK, "multi-group CTAs are TMA-fed");
@@ -322,7 +326,7 @@ coo_tile_kernel(const __grid_constant__ CooParams<T> P) {
       for (int k = cnt_ext + tid; k < TILE + kExt; k += NT) rb[kExt + k] = kNoRow;
     }
     grp.sync();
-    coo_process_tile<T, TILE, NT, S::long_rows>(P, t, rows_of(s) + kExt, cols_of(s), vals_of(s), s_start, s_long,
+    coo_process_tile<T, TILE, NT, S::long_rows, VW>(P, t, rows_of(s) + kExt, cols_of(s), vals_of(s), s_start, s_long,
                                                 s_nseg, s_nlong, s_wcnt, grp);
     const int nl = S::long_rows ? *s_nlong : 0;
     if (S::long_rows && nl > 0)
@@ -883,9 +887,9 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
   return fail(SPMV_INVALID_ARG, "no COO kernel for tile %lld x %d groups", (long long)p->tile, p->groups);
 }
 
-template <typename T, int TILE, int G>
+template <typename T, int TILE, int G, int VW = 0>
 static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const T* av, const T* x,
-                   int64_t col_base, T* y, cudaStream_t st) {
+                   int64_t col_base, T* y, cudaStream_t st, int vla = 0) {
   if (p->nrows == 0) return SPMV_OK;
   if (p->nnz == 0) {
     SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
@@ -913,6 +917,7 @@ static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint3
   P.ntiles = p->ntiles;
   P.tile_begin = 0;
   P.mode = tile_mode_flags() | (tma_hint_mode() != 0 ? 4 : 0);
+  P.vla = vla;
   if (p->n_runs < p->nrows) {  // empty rows exist: one memset instead of per-gap loops
     SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
     P.mode |= 8;
@@ -921,20 +926,33 @@ static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint3
                        (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
   const size_t smem1 = CooSmem<T, TILE, 1>::total;
+  if constexpr (VW > 0) {
+    // vla instantiations are not touched by the plan's occupancy queries
+    static bool attrs = [] {
+      cudaFuncSetAttribute(coo_tile_kernel<T, false, TILE, 1, VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(CooSmem<T, TILE, 1>::total));
+      cudaFuncSetAttribute(coo_tile_kernel<T, true, TILE, 1, VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(CooSmem<T, TILE, 1>::total));
+      cudaFuncSetAttribute(coo_tile_kernel<T, true, TILE, G, VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(CooSmem<T, TILE, G>::total));
+      return true;
+    }();
+    (void)attrs;
+  }
   if (!aligned) {
-    coo_tile_kernel<T, false, TILE, 1><<<unsigned(p->grid_direct), kTileThreads, smem1, st>>>(P);
+    coo_tile_kernel<T, false, TILE, 1, VW><<<unsigned(p->grid_direct), kTileThreads, smem1, st>>>(P);
   } else if (G == 1) {
-    coo_tile_kernel<T, true, TILE, 1><<<unsigned(p->grid), kTileThreads, smem1, st>>>(P);
+    coo_tile_kernel<T, true, TILE, 1, VW><<<unsigned(p->grid), kTileThreads, smem1, st>>>(P);
   } else {
     if (P.n_bulk > 0)
-      coo_tile_kernel<T, true, TILE, G>
+      coo_tile_kernel<T, true, TILE, G, VW>
           <<<unsigned(std::min<int64_t>(p->grid, P.n_bulk)), G * coo_group_threads<G>(), CooSmem<T, TILE, G>::total,
              st>>>(P);
     if (P.n_bulk < p->ntiles) {  // tail tiles the bulk engine cannot address
       CooParams<T> Q = P;
       Q.tile_begin = P.n_bulk;
       const int64_t g1 = std::min<int64_t>(p->grid_direct, p->ntiles - P.n_bulk);
-      coo_tile_kernel<T, false, TILE, 1><<<unsigned(g1), kTileThreads, smem1, st>>>(Q);
+      coo_tile_kernel<T, false, TILE, 1, VW><<<unsigned(g1), kTileThreads, smem1, st>>>(Q);
     }
   }
   SPMV_LAUNCH_CHECK();
@@ -974,7 +992,7 @@ static int coo_run_ws(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t
   coo_wstream_kernel<T><<<unsigned(grid), kWsWarps * 32, 0, st>>>(P);
   SPMV_LAUNCH_CHECK();
   if (p->ws_n_span > 0) {
-    const int64_t g = std::min<int64_t>((p->ws_n_span + 255) / 256, int64_t(sm_count()) * 8);
+    const int64_t g = std::min<int64_t>((p->ws_n_span + 7) / 8, int64_t(sm_count()) * 8);  // a warp per row
     ws_span_fixup_kernel<T><<<unsigned(g), 256, 0, st>>>(p->ws_span_run.as<uint32_t>(), p->ws_span_w0.as<uint32_t>(),
                                                          p->ws_span_w1.as<uint32_t>(), p->ws_n_span, P.head, P.tail, y,
                                                          p->run_row.as<uint32_t>());
@@ -992,6 +1010,41 @@ static int coo_run(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* a
   SPMV_COO_CONFIGS(X)
 #undef X
   return fail(SPMV_INVALID_ARG, "no COO kernel for tile %lld x %d groups", (long long)p->tile, p->groups);
+}
+
+// vla through the tile kernels (row-per-lane vla, tile.cuh row_vla_coo):
+// plans without runs over 32 entries whose tile configuration has vla
+// instantiations, lane counts whose register width next_pow2(L) is <= 8.
+#define SPMV_COO_VLA_CONFIGS(X) X(1536, 7)
+template <typename T>
+static int coo_run_vla_tiles(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const T* av,
+                             const T* x, int64_t col_base, T* y, int lanes, cudaStream_t st, bool* done) {
+  *done = false;
+  if (p->n_long > 0 || lanes < 1 || lanes > 8) return SPMV_OK;
+  const int w = lanes <= 1 ? 1 : lanes <= 2 ? 2 : lanes <= 4 ? 4 : 8;
+#define X(TL, GR)                                                                              \
+  if (p->tile == TL && p->groups == GR) {                                                      \
+    *done = true;                                                                              \
+    switch (w) {                                                                               \
+      case 1: return coo_run_tiled<T, TL, GR, 1>(p, ai, aj, av, x, col_base, y, st, lanes);     \
+      case 2: return coo_run_tiled<T, TL, GR, 2>(p, ai, aj, av, x, col_base, y, st, lanes);     \
+      case 4: return coo_run_tiled<T, TL, GR, 4>(p, ai, aj, av, x, col_base, y, st, lanes);     \
+      default: return coo_run_tiled<T, TL, GR, 8>(p, ai, aj, av, x, col_base, y, st, lanes);    \
+    }                                                                                          \
+  }
+  SPMV_COO_VLA_CONFIGS(X)
+#undef X
+  return SPMV_OK;
+}
+
+// outer_steps of spmv_coo_vla: ceil(run length / L) per run.
+__global__ void coo_vla_count_steps_kernel(const uint32_t* __restrict__ run_start, int64_t n_runs, int lanes,
+                                           unsigned long long* __restrict__ steps) {
+  unsigned long long c = 0;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_runs; i += int64_t(gridDim.x) * blockDim.x)
+    c += (run_start[i + 1] - run_start[i] + uint32_t(lanes) - 1) / uint32_t(lanes);
+  for (int o = 16; o >= 1; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(steps, c);
 }
 
 extern "C" {
@@ -1073,10 +1126,34 @@ int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const
   if (lanes < 1) return fail(SPMV_INVALID_ARG, "lane count must be >= 1");
   if (lanes > 1024) return fail(SPMV_UNSUPPORTED, "vla COO supports at most 1024 lanes, got %d", lanes);
   if (x_len < 0 || col_base < 0) return fail(SPMV_DIMENSION_MISMATCH, "bad x window");
-  (void)ai;
   cudaStream_t st = as_stream(stream);
   if (outer_steps) *outer_steps = 0;
   if (p->nrows == 0) return SPMV_OK;
+  if (p->nnz > 0) {
+    bool done = false;
+    const int rc = p->dtype == SPMV_F64
+                       ? coo_run_vla_tiles<double>(p, ai, aj, static_cast<const double*>(av),
+                                                   static_cast<const double*>(x), col_base, static_cast<double*>(y),
+                                                   lanes, st, &done)
+                       : coo_run_vla_tiles<float>(p, ai, aj, static_cast<const float*>(av),
+                                                  static_cast<const float*>(x), col_base, static_cast<float*>(y), lanes,
+                                                  st, &done);
+    if (rc) return rc;
+    if (done) {
+      if (outer_steps) {
+        unsigned long long* steps = p->steps.as<unsigned long long>();
+        unsigned long long h = 0;
+        SPMV_CUDA_TRY(cudaMemsetAsync(steps, 0, sizeof(h), st));
+        const int64_t g = std::min<int64_t>((p->n_runs + 255) / 256, int64_t(sm_count()) * 16);
+        coo_vla_count_steps_kernel<<<unsigned(g), 256, 0, st>>>(p->run_start.as<uint32_t>(), p->n_runs, lanes, steps);
+        SPMV_LAUNCH_CHECK();
+        SPMV_CUDA_TRY(cudaMemcpyAsync(&h, steps, sizeof(h), cudaMemcpyDeviceToHost, st));
+        SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+        *outer_steps = int64_t(h);
+      }
+      return SPMV_OK;
+    }
+  }
   SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, value_size(p->dtype) * p->nrows, st));
   if (p->nnz == 0) return SPMV_OK;
   if (!p->row_sorted) {

@@ -63,6 +63,7 @@ struct CsrParams {
   int64_t tile_begin, tile_end;  // tiles [tile_begin, tile_end) of this launch
   int exact_len;
   int mode;
+  int vla;  // lanes L of a vla tile launch (template VW = next_pow2(L) > 0)
 };
 
 // Shared memory of a CSR tile CTA with G consumer groups and G + 1 stages:
@@ -99,7 +100,7 @@ template <int G> constexpr int csr_min_blocks() { return G == 1 ? SPMV_CSR_MINB 
 // than threads, e.g. Zipf's short rows): all gathers of the tile are issued
 // entry-per-lane first, then rows are summed from shared memory.  Long
 // segments are only queued here.
-template <typename T, int TILE, int NT, bool LONG>
+template <typename T, int TILE, int NT, bool LONG, int VW = 0>
 __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, const uint32_t* __restrict__ cols,
                                               T* __restrict__ vals, LongSeg* s_long, int* s_nlong,
                                               const TileGroup<NT>& grp
@@ -120,7 +121,7 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
     s = __ldg(P.irp + r);
     e = __ldg(P.irp + r + 1);
   }
-  const bool products = (P.mode & 1) && (rend - R0) > NT;
+  const bool products = VW == 0 && (P.mode & 1) && (rend - R0) > NT;
   if (products) form_products<T, NT>(cols, vals, int(min(int64_t(TILE + kExt), P.nnz - E0)), xb, tid);
   if (tid == 0) *s_nlong = 0;
   grp.sync();
@@ -133,10 +134,14 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
     if (len == 0) {
       if (r < R1) P.y[r] = T(0);
     } else if (len <= uint32_t(P.exact_len)) {
-      if (int64_t(s) >= E0 && int64_t(s) < E1)
-        // -0.0 seed: the sum starts from the first product, like cumsum
-        P.y[r] = products ? row_sum(vals + (s - E0), int(len), T(-0.0))
-                          : row_dot(cols + (s - E0), vals + (s - E0), int(len), xb, T(-0.0));
+      if (int64_t(s) >= E0 && int64_t(s) < E1) {
+        if constexpr (VW > 0)
+          P.y[r] = row_vla_csr<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla);
+        else
+          // -0.0 seed: the sum starts from the first product, like cumsum
+          P.y[r] = products ? row_sum(vals + (s - E0), int(len), T(-0.0))
+                            : row_dot(cols + (s - E0), vals + (s - E0), int(len), xb, T(-0.0));
+      }
     } else {
       const int64_t lo = max(int64_t(s), E0), hi = min(int64_t(e), E1);
       if (LONG && lo < hi) {
@@ -203,9 +208,10 @@ __device__ __forceinline__ void csr_tile_long(int64_t t, const uint32_t* __restr
 // loads, so more rows are in flight per byte of shared memory (the stencil's
 // limiter).  Multi-group CTAs take bulk tiles only; the host runs the tail
 // tiles with G == 1.
-template <typename T, bool BULK, int TILE, int G, bool LONG = true>
+template <typename T, bool BULK, int TILE, int G, bool LONG = true, int VW = 0>
 __global__ void __launch_bounds__(csr_cta_threads<G>(), csr_min_blocks<G>())
 csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
+  static_assert(VW == 0 || !LONG, "vla tile launches serve plans without long rows");
   static_assert(G == 1 || BULK, "multi-group CTAs are TMA-fed");
   constexpr int NT = csr_group_threads<G>();
   extern __shared__ __align__(128) unsigned char smem[];
@@ -283,7 +289,7 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
     }
     PHASE_T(p1);
 #ifndef SPMV_STREAM_ONLY  // experiment: TMA stream alone (y is not written)
-    csr_tile_rows<T, TILE, NT, LONG>(P, t, cols_of(s), vals_of(s), s_long, s_nlong, grp
+    csr_tile_rows<T, TILE, NT, LONG, VW>(P, t, cols_of(s), vals_of(s), s_long, s_nlong, grp
 #ifdef SPMV_PHASE_TIMING
                                , s_phase_acc
 #endif
@@ -704,9 +710,9 @@ static int csr_launch_config(spmv_csr_plan* p) {
   return SPMV_OK;
 }
 
-template <typename T, int TILE, int G, bool LONG>
+template <typename T, int TILE, int G, bool LONG, int VW = 0>
 static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
-                   int64_t col_base, T* y, cudaStream_t st, int64_t tb, int64_t te, bool fixup) {
+                   int64_t col_base, T* y, cudaStream_t st, int64_t tb, int64_t te, bool fixup, int vla = 0) {
   if (p->nrows == 0) return SPMV_OK;
   if (p->nnz == 0) {
     SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
@@ -728,29 +734,43 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
   P.tile_begin = tb;
   P.tile_end = te;
   P.exact_len = p->exact_len;
+  P.vla = vla;
   P.mode = tile_mode_flags() | ((tma_hint_mode() < 0 ? p->n_long > 0 : tma_hint_mode() > 0) ? 4 : 0);
   const bool aligned = (reinterpret_cast<uintptr_t>(aj) % 16 == 0) && (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
   const size_t smem1 = CsrSmem<T, TILE, 1>::total;
+  if constexpr (VW > 0) {
+    // vla instantiations are not touched by the plan's occupancy queries
+    static bool attrs = [] {
+      cudaFuncSetAttribute(csr_tile_kernel<T, false, TILE, 1, false, VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(CsrSmem<T, TILE, 1>::total));
+      cudaFuncSetAttribute(csr_tile_kernel<T, true, TILE, 1, false, VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(CsrSmem<T, TILE, 1>::total));
+      cudaFuncSetAttribute(csr_tile_kernel<T, true, TILE, G, LONG, VW>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           int(CsrSmem<T, TILE, G, LONG>::total));
+      return true;
+    }();
+    (void)attrs;
+  }
   if (!aligned) {
     const int64_t grid = std::min<int64_t>(p->grid_direct, te - tb);
-    if (grid > 0) csr_tile_kernel<T, false, TILE, 1><<<unsigned(grid), kTileThreads, smem1, st>>>(P);
+    if (grid > 0) csr_tile_kernel<T, false, TILE, 1, VW == 0, VW><<<unsigned(grid), kTileThreads, smem1, st>>>(P);
   } else if (G == 1) {
     const int64_t grid = std::min<int64_t>(p->grid_bulk, te - tb);
-    if (grid > 0) csr_tile_kernel<T, true, TILE, 1, LONG><<<unsigned(grid), kTileThreads, smem1, st>>>(P);
+    if (grid > 0) csr_tile_kernel<T, true, TILE, 1, LONG, VW><<<unsigned(grid), kTileThreads, smem1, st>>>(P);
   } else {
     // bulk tiles on the multi-group kernel, the (rare) tail tiles past
     // n_bulk on the single-group one
     const int64_t bulk_end = std::min<int64_t>(te, P.n_bulk);
     const int64_t grid = std::min<int64_t>(p->grid_bulk, bulk_end - tb);
     if (grid > 0)
-      csr_tile_kernel<T, true, TILE, G, LONG>
+      csr_tile_kernel<T, true, TILE, G, LONG, VW>
           <<<unsigned(grid), csr_cta_threads<G>(), CsrSmem<T, TILE, G, LONG>::total, st>>>(P);
     if (te > bulk_end) {
       CsrParams<T> Q = P;
       Q.tile_begin = std::max<int64_t>(tb, bulk_end);
       const int64_t g1 = std::min<int64_t>(p->grid_direct, te - Q.tile_begin);
-      csr_tile_kernel<T, true, TILE, 1><<<unsigned(g1), kTileThreads, smem1, st>>>(Q);
+      csr_tile_kernel<T, true, TILE, 1, VW == 0, VW><<<unsigned(g1), kTileThreads, smem1, st>>>(Q);
     }
   }
   SPMV_LAUNCH_CHECK();
@@ -787,7 +807,7 @@ static int csr_run_ws(const spmv_csr_plan* p, const uint32_t* irp, const uint32_
   csr_wstream_kernel<T><<<unsigned(grid), kWsWarps * 32, 0, st>>>(P);
   SPMV_LAUNCH_CHECK();
   if (p->ws_n_span > 0) {
-    const int64_t g = std::min<int64_t>((p->ws_n_span + 255) / 256, int64_t(sm_count()) * 8);
+    const int64_t g = std::min<int64_t>((p->ws_n_span + 7) / 8, int64_t(sm_count()) * 8);  // a warp per row
     ws_span_fixup_kernel<T><<<unsigned(g), 256, 0, st>>>(p->ws_span_row.as<uint32_t>(), p->ws_span_w0.as<uint32_t>(),
                                                          p->ws_span_w1.as<uint32_t>(), p->ws_n_span, P.head, P.tail, y);
     SPMV_LAUNCH_CHECK();
@@ -806,6 +826,31 @@ static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* 
   SPMV_CSR_CONFIGS(X)
 #undef X
   return fail(SPMV_INVALID_ARG, "no CSR kernel for tile %lld x %d groups", (long long)p->tile, p->groups);
+}
+
+// vla through the tile kernels (row-per-lane vla, tile.cuh row_vla_csr):
+// plans without long rows whose tile configuration has vla instantiations,
+// lane counts whose register width next_pow2(L) is at most 8.
+#define SPMV_CSR_VLA_CONFIGS(X) X(2304, 3, 0) X(1664, 4, 0) X(2048, 3, 0)
+template <typename T>
+static int csr_run_vla_tiles(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av,
+                             const T* x, int64_t col_base, T* y, int lanes, cudaStream_t st, bool* done) {
+  *done = false;
+  if (p->n_long > 0 || p->long_scratch || lanes < 1 || lanes > 8) return SPMV_OK;
+  const int w = lanes <= 1 ? 1 : lanes <= 2 ? 2 : lanes <= 4 ? 4 : 8;
+#define X(TL, GR, LF)                                                                                           \
+  if (p->tile == TL && p->groups == GR && !p->long_scratch) {                                                    \
+    *done = true;                                                                                               \
+    switch (w) {                                                                                                \
+      case 1: return csr_run_tiled<T, TL, GR, false, 1>(p, irp, aj, av, x, col_base, y, st, 0, p->ntiles, true, lanes); \
+      case 2: return csr_run_tiled<T, TL, GR, false, 2>(p, irp, aj, av, x, col_base, y, st, 0, p->ntiles, true, lanes); \
+      case 4: return csr_run_tiled<T, TL, GR, false, 4>(p, irp, aj, av, x, col_base, y, st, 0, p->ntiles, true, lanes); \
+      default: return csr_run_tiled<T, TL, GR, false, 8>(p, irp, aj, av, x, col_base, y, st, 0, p->ntiles, true, lanes); \
+    }                                                                                                           \
+  }
+  SPMV_CSR_VLA_CONFIGS(X)
+#undef X
+  return SPMV_OK;
 }
 
 // Host x -> host y product with H2D / compute / D2H overlap (see
@@ -1375,6 +1420,17 @@ int spmv_csr_vla_planned(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* 
                          const void* x, int64_t col_base, int64_t x_len, void* y, int lanes, void* stream) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   cudaStream_t st = as_stream(stream);
+  if (p->nrows > 0 && p->nnz > 0 && x_len >= 0 && col_base >= 0) {
+    bool done = false;
+    const int rc = p->dtype == SPMV_F64
+                       ? csr_run_vla_tiles<double>(p, irp, aj, static_cast<const double*>(av),
+                                                   static_cast<const double*>(x), col_base, static_cast<double*>(y),
+                                                   lanes, st, &done)
+                       : csr_run_vla_tiles<float>(p, irp, aj, static_cast<const float*>(av),
+                                                  static_cast<const float*>(x), col_base, static_cast<float*>(y), lanes,
+                                                  st, &done);
+    if (done || rc) return rc;
+  }
   // rows over kVlaLong entries are only possible when the plan saw long rows
   const bool long_rows = p->n_long > 0 || p->exact_len >= int(kVlaLong);
   if (!long_rows || lanes > 32 || lanes < 1)

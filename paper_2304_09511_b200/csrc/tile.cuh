@@ -95,6 +95,55 @@ __device__ __forceinline__ T row_dot(const uint32_t* __restrict__ c, const T* __
   return acc;
 }
 
+// vla rows from staged entries, one thread per row (rows of <= 32 entries).
+// The reference's lane arithmetic does not depend on which hardware lane
+// holds a logical lane, so one thread can play all W = next_pow2(L) of them
+// in registers with the same adds in the same order — bit-exact, with the
+// row-per-lane gather pattern of the plain tile kernels.
+//   CSR (kernels.py:143-171): acc[l] = +0.0, then acc[l] += p_j for
+//     j = l, l+L, ... (masked_fma, lanes.py:101-104); tree over W lanes,
+//     vals[:w] + vals[w:2w] (lanes.py:107-128); inactive lanes stay 0.
+//   COO (kernels.py:104-140): steps of L entries; each step's products
+//     (0 on inactive lanes) tree-reduce to t_k; y = ((+0.0 + t_0) + t_1)...
+template <typename T, int W>
+__device__ __forceinline__ T tree_regs(T (&v)[W]) {
+#pragma unroll
+  for (int w = W / 2; w >= 1; w >>= 1)
+#pragma unroll
+    for (int i = 0; i < w; ++i) v[i] = add_rn(v[i], v[i + w]);
+  return v[0];
+}
+
+template <typename T, int W>
+__device__ __forceinline__ T row_vla_csr(const uint32_t* __restrict__ c, const T* __restrict__ v, int len,
+                                         const T* __restrict__ xb, int L) {
+  T acc[W];
+#pragma unroll
+  for (int l = 0; l < W; ++l) acc[l] = T(0);
+  for (int base = 0; base < len; base += L) {
+    T p[W];
+#pragma unroll
+    for (int l = 0; l < W; ++l) p[l] = (l < L && base + l < len) ? mul_rn(v[base + l], ldx(xb + c[base + l])) : T(0);
+#pragma unroll
+    for (int l = 0; l < W; ++l)
+      if (l < L && base + l < len) acc[l] = add_rn(acc[l], p[l]);
+  }
+  return tree_regs<T, W>(acc);
+}
+
+template <typename T, int W>
+__device__ __forceinline__ T row_vla_coo(const uint32_t* __restrict__ c, const T* __restrict__ v, int len,
+                                         const T* __restrict__ xb, int L) {
+  T y = T(0);
+  for (int base = 0; base < len; base += L) {
+    T p[W];
+#pragma unroll
+    for (int l = 0; l < W; ++l) p[l] = (l < L && base + l < len) ? mul_rn(v[base + l], ldx(xb + c[base + l])) : T(0);
+    y = add_rn(y, tree_regs<T, W>(p));
+  }
+  return y;
+}
+
 // Left-to-right sum of already-formed products (the "products" tile mode).
 template <typename T>
 __device__ __forceinline__ T row_sum(const T* __restrict__ p, int len, T acc) {

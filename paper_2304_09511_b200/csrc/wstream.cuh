@@ -246,18 +246,24 @@ __global__ void __launch_bounds__(kWsWarps * 32, SPMV_WS_MINB) csr_wstream_kerne
   }
 }
 
-// Rows split between ranges: y = tail[w0] + head[w0+1] + ... + head[w1].
-// COO plans list runs (run_row maps a run to its row); CSR passes nullptr.
+// Rows split between ranges: y = tail[w0] + head[w0+1] + ... + head[w1],
+// one warp per row: lane l sums partials l, l+32, ... in order, then a fixed
+// xor tree (deterministic; these rows are longer than exact_len).  COO plans
+// list runs (run_row maps a run to its row); CSR passes nullptr.
 template <typename T>
 __global__ void ws_span_fixup_kernel(const uint32_t* __restrict__ span_row, const uint32_t* __restrict__ span_w0,
                                      const uint32_t* __restrict__ span_w1, int64_t n_span,
                                      const double* __restrict__ head, const double* __restrict__ tail,
                                      T* __restrict__ y, const uint32_t* __restrict__ run_row = nullptr) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_span; i += int64_t(gridDim.x) * blockDim.x) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  for (int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < n_span; i += nw) {
     const uint32_t w0 = span_w0[i], w1 = span_w1[i];
-    double sum = tail[w0];
-    for (uint32_t u = w0 + 1; u <= w1; ++u) sum = __dadd_rn(sum, head[u]);
-    y[run_row ? run_row[span_row[i]] : span_row[i]] = T(sum);
+    double sum = -0.0;
+    for (uint32_t u = w0 + lane; u <= w1; u += 32) sum = __dadd_rn(sum, u == w0 ? tail[u] : head[u]);
+#pragma unroll
+    for (int o = 16; o >= 1; o >>= 1) sum = __dadd_rn(sum, __shfl_xor_sync(0xffffffffu, sum, o));
+    if (lane == 0) y[run_row ? run_row[span_row[i]] : span_row[i]] = T(sum);
   }
 }
 
