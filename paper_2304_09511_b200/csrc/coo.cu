@@ -190,7 +190,9 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
       L.s = L.e = 0;
       s_long[idx] = L;
     } else if (!cont_before) {
-      if constexpr (VW > 0)
+      if constexpr (VW >= 16)
+        P.y[r] = row_vla_coo_wide<T, VW>(cols + k0, vals + k0, k1 + after - k0, xb, P.vla, P.vla > 32);
+      else if constexpr (VW > 0)
         P.y[r] = row_vla_coo<T, VW>(cols + k0, vals + k0, k1 + after - k0, xb, P.vla);
       else
         // +0.0 seed: np.add.at accumulates into a zeroed y
@@ -1014,14 +1016,14 @@ static int coo_run(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* a
 
 // vla through the tile kernels (row-per-lane vla, tile.cuh row_vla_coo):
 // plans without runs over 32 entries whose tile configuration has vla
-// instantiations, lane counts whose register width next_pow2(L) is <= 8.
+// instantiations (any lane count).
 #define SPMV_COO_VLA_CONFIGS(X) X(1536, 7)
 template <typename T>
 static int coo_run_vla_tiles(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const T* av,
                              const T* x, int64_t col_base, T* y, int lanes, cudaStream_t st, bool* done) {
   *done = false;
-  if (p->n_long > 0 || lanes < 1 || lanes > 8) return SPMV_OK;
-  const int w = lanes <= 1 ? 1 : lanes <= 2 ? 2 : lanes <= 4 ? 4 : 8;
+  if (p->n_long > 0 || lanes < 1) return SPMV_OK;
+  const int w = lanes <= 1 ? 1 : lanes <= 2 ? 2 : lanes <= 4 ? 4 : lanes <= 8 ? 8 : lanes <= 16 ? 16 : 32;
 #define X(TL, GR)                                                                              \
   if (p->tile == TL && p->groups == GR) {                                                      \
     *done = true;                                                                              \
@@ -1029,7 +1031,9 @@ static int coo_run_vla_tiles(const spmv_coo_plan* p, const uint32_t* ai, const u
       case 1: return coo_run_tiled<T, TL, GR, 1>(p, ai, aj, av, x, col_base, y, st, lanes);     \
       case 2: return coo_run_tiled<T, TL, GR, 2>(p, ai, aj, av, x, col_base, y, st, lanes);     \
       case 4: return coo_run_tiled<T, TL, GR, 4>(p, ai, aj, av, x, col_base, y, st, lanes);     \
-      default: return coo_run_tiled<T, TL, GR, 8>(p, ai, aj, av, x, col_base, y, st, lanes);    \
+      case 8: return coo_run_tiled<T, TL, GR, 8>(p, ai, aj, av, x, col_base, y, st, lanes);      \
+      case 16: return coo_run_tiled<T, TL, GR, 16>(p, ai, aj, av, x, col_base, y, st, lanes);    \
+      default: return coo_run_tiled<T, TL, GR, 32>(p, ai, aj, av, x, col_base, y, st, lanes);    \
     }                                                                                          \
   }
   SPMV_COO_VLA_CONFIGS(X)

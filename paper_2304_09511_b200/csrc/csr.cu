@@ -135,7 +135,9 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
       if (r < R1) P.y[r] = T(0);
     } else if (len <= uint32_t(P.exact_len)) {
       if (int64_t(s) >= E0 && int64_t(s) < E1) {
-        if constexpr (VW > 0)
+        if constexpr (VW >= 16)
+          P.y[r] = row_vla_csr_wide<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla);
+        else if constexpr (VW > 0)
           P.y[r] = row_vla_csr<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla);
         else
           // -0.0 seed: the sum starts from the first product, like cumsum
@@ -829,15 +831,16 @@ static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* 
 }
 
 // vla through the tile kernels (row-per-lane vla, tile.cuh row_vla_csr):
-// plans without long rows whose tile configuration has vla instantiations,
-// lane counts whose register width next_pow2(L) is at most 8.
+// plans without long rows whose tile configuration has vla instantiations
+// (any lane count: rows of <= 32 entries never reach lanes past 32).
 #define SPMV_CSR_VLA_CONFIGS(X) X(2304, 3, 0) X(1664, 4, 0) X(2048, 3, 0)
 template <typename T>
 static int csr_run_vla_tiles(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av,
                              const T* x, int64_t col_base, T* y, int lanes, cudaStream_t st, bool* done) {
   *done = false;
-  if (p->n_long > 0 || p->long_scratch || lanes < 1 || lanes > 8) return SPMV_OK;
-  const int w = lanes <= 1 ? 1 : lanes <= 2 ? 2 : lanes <= 4 ? 4 : 8;
+  if (p->n_long > 0 || p->long_scratch || lanes < 1) return SPMV_OK;
+  // rows have <= 32 entries: lanes past 32 only add zero lanes (see tile.cuh)
+  const int w = lanes <= 1 ? 1 : lanes <= 2 ? 2 : lanes <= 4 ? 4 : lanes <= 8 ? 8 : lanes <= 16 ? 16 : 32;
 #define X(TL, GR, LF)                                                                                           \
   if (p->tile == TL && p->groups == GR && !p->long_scratch) {                                                    \
     *done = true;                                                                                               \
@@ -845,7 +848,9 @@ static int csr_run_vla_tiles(const spmv_csr_plan* p, const uint32_t* irp, const 
       case 1: return csr_run_tiled<T, TL, GR, false, 1>(p, irp, aj, av, x, col_base, y, st, 0, p->ntiles, true, lanes); \
       case 2: return csr_run_tiled<T, TL, GR, false, 2>(p, irp, aj, av, x, col_base, y, st, 0, p->ntiles, true, lanes); \
       case 4: return csr_run_tiled<T, TL, GR, false, 4>(p, irp, aj, av, x, col_base, y, st, 0, p->ntiles, true, lanes); \
-      default: return csr_run_tiled<T, TL, GR, false, 8>(p, irp, aj, av, x, col_base, y, st, 0, p->ntiles, true, lanes); \
+      case 8: return csr_run_tiled<T, TL, GR, false, 8>(p, irp, aj, av, x, col_base, y, st, 0, p->ntiles, true, lanes); \
+      case 16: return csr_run_tiled<T, TL, GR, false, 16>(p, irp, aj, av, x, col_base, y, st, 0, p->ntiles, true, lanes); \
+      default: return csr_run_tiled<T, TL, GR, false, 32>(p, irp, aj, av, x, col_base, y, st, 0, p->ntiles, true, lanes); \
     }                                                                                                           \
   }
   SPMV_CSR_VLA_CONFIGS(X)

@@ -144,6 +144,85 @@ __device__ __forceinline__ T row_vla_coo(const uint32_t* __restrict__ c, const T
   return y;
 }
 
+// W = 16 / 32 (and L > 32): too many registers for a lane array.  The
+// row's rounded products are formed in place in the staged values (the row
+// is this thread's alone), then the tree is evaluated as an adjacent
+// pairwise sum over the logical lanes in bit-reversed order — the same
+// pairs as vals[:w] + vals[w:2w] — with a log2(W)-deep stack.
+template <int W>
+__device__ __forceinline__ constexpr int bitrev(int k) {
+  int r = 0;
+  for (int b = 1; b < W; b <<= 1) {
+    r = (r << 1) | (k & 1);
+    k >>= 1;
+  }
+  return r;
+}
+
+template <typename T, int W, typename Leaf>
+__device__ __forceinline__ T tree_stack(Leaf leaf) {
+  constexpr int LOG = W == 16 ? 4 : 5;
+  static_assert(W == 16 || W == 32, "wide trees");
+  T st[LOG];
+  T v = T(0);
+#pragma unroll
+  for (int k = 0; k < W; ++k) {
+    v = leaf(bitrev<W>(k));
+#pragma unroll
+    for (int b = 0; b < LOG; ++b) {
+      if (!((k >> b) & 1)) {
+        st[b] = v;
+        break;
+      }
+      v = add_rn(st[b], v);
+    }
+  }
+  return v;
+}
+
+template <typename T>
+__device__ __forceinline__ void products_in_place(const uint32_t* __restrict__ c, T* __restrict__ v, int len,
+                                                  const T* __restrict__ xb) {
+  int i = 0;
+  for (; i + 8 <= len; i += 8) {
+    T x[8];
+#pragma unroll
+    for (int j = 0; j < 8; ++j) x[j] = ldx(xb + c[i + j]);
+#pragma unroll
+    for (int j = 0; j < 8; ++j) v[i + j] = mul_rn(v[i + j], x[j]);
+  }
+  for (; i < len; ++i) v[i] = mul_rn(v[i], ldx(xb + c[i]));
+}
+
+template <typename T, int W>
+__device__ __forceinline__ T row_vla_csr_wide(const uint32_t* __restrict__ c, T* __restrict__ v, int len,
+                                              const T* __restrict__ xb, int L) {
+  products_in_place(c, v, len, xb);
+  return tree_stack<T, W>([&](int l) {
+    T a = T(0);
+    if (l < L)
+      for (int j = l; j < len; j += L) a = add_rn(a, v[j]);
+    return a;
+  });
+}
+
+// upper: next_pow2(L) > 32 — the tree levels above 32 lanes add +0.0 to
+// every live lane once (which turns a -0.0 product into +0.0).
+template <typename T, int W>
+__device__ __forceinline__ T row_vla_coo_wide(const uint32_t* __restrict__ c, T* __restrict__ v, int len,
+                                              const T* __restrict__ xb, int L, bool upper) {
+  products_in_place(c, v, len, xb);
+  T y = T(0);
+  for (int base = 0; base < len; base += L) {
+    const int cnt = min(L, len - base);
+    y = add_rn(y, tree_stack<T, W>([&](int l) {
+      const T p = l < cnt ? v[base + l] : T(0);
+      return upper ? add_rn(p, T(0)) : p;
+    }));
+  }
+  return y;
+}
+
 // Left-to-right sum of already-formed products (the "products" tile mode).
 template <typename T>
 __device__ __forceinline__ T row_sum(const T* __restrict__ p, int len, T acc) {

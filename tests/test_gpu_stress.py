@@ -179,3 +179,31 @@ def test_stencil_slab_generator(sp):
     irp = full["row_pointers"].astype(np.int64)
     assert np.array_equal(slab["row_pointers"].astype(np.int64), irp[r0:r1 + 1] - irp[r0])
     assert np.array_equal(slab["col_indices"], full["col_indices"][irp[r0]:irp[r1]])
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_vla_tile_path_all_lane_widths(sp, dtype):
+    """Short-row plans run vla through the tile kernels (one thread plays all
+    next_pow2(L) logical lanes; W >= 16 via the in-place product stack tree).
+    Every width class, non-powers of two and L > 32 against the oracle,
+    bit for bit, with signed zeros in the products."""
+    rng = np.random.default_rng(7)
+    nrows, ncols = 4_000, 6_000
+    lens = rng.integers(0, 33, nrows)
+    irp, cols, vals = random_csr(rng, nrows, ncols, lens)
+    vals[rng.random(vals.shape[0]) < 0.05] = -0.0
+    vals = vals.astype(dtype)
+    x = rng.uniform(-1, 1, ncols).astype(dtype)
+    x[rng.random(ncols) < 0.05] = 0.0
+    csr = sp.CsrMatrix.from_arrays(nrows, ncols, irp, cols, vals)
+    coo = sp.csr_to_coo(csr)
+    rows = np.repeat(np.arange(nrows), lens).astype(np.uint32)
+    for lanes in (1, 2, 3, 5, 8, 9, 16, 17, 32, 33, 100):
+        y = sp.spmv_csr_vla(csr, x, sp.LaneConfig(lanes))
+        assert bit_equal(y, O.csr_vla(nrows, irp, cols, vals, x, lanes)), ("csr", lanes)
+        stats = {}
+        ref_stats = {}
+        y = sp.spmv_coo_vla(coo, x, sp.LaneConfig(lanes), stats)
+        ref = O.coo_vla(nrows, rows, cols, vals, x, lanes, ref_stats)
+        assert bit_equal(y, ref), ("coo", lanes, first_diff(y, ref))
+        assert stats["outer_steps"] == ref_stats["outer_steps"]
