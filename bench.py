@@ -399,6 +399,8 @@ def run_ours(args, torch, dist, rank, world, local_rank):
         line["e2e"] = e2e_measure(args, torch, sp, m, x, head)
         if "csr" in mats and "dia" in mats:  # Zipf has no DIA form (fill ratio)
             line["conversions"] = conversions_measure(torch, sp, mats, pk)
+        if args.config == "c5":
+            line["cg"] = cg_measure(torch, sp, mats["csr"], pk)
         if args.config in ("c5", "c1", "c3", "c4"):
             csr = mats["csr"]
             h = csr.to_host()
@@ -487,6 +489,30 @@ def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
                        "path": "DistributedMatrix.spmv per rank, pinned host x slice in, pinned host y slice out"}
     if rank == 0:
         print(json.dumps(line), flush=True)
+
+
+def cg_measure(torch, sp, m, pk, iters: int = 20) -> dict:
+    """The reference's HPCG vehicle (hpcg.py:211-258) on the device: CG with
+    a fixed iteration count (tol 0) on A x = A 1, device-timed; two host
+    syncs per iteration for p.Ap and r.r, as in the reference."""
+    b = sp.spmv_csr_plain(m, torch.ones(m.ncols, dtype=m.values.dtype, device=m.values.device))
+    sp.cg_solve(m, b, tol=0.0, max_iters=2)  # warm-up (plans, workspaces)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    st = sp.cg_solve(m, b, tol=0.0, max_iters=iters)
+    e1.record()
+    torch.cuda.synchronize()
+    t = e0.elapsed_time(e1) / 1e3 / st.iterations
+    # per iteration: one SpMV + p.Ap (2 reads) + fused x/r update and r.r
+    # (3 reads, 2 writes) + p = r + beta p (2 reads, 1 write) = 10 vectors
+    vec_bytes = 10 * m.nrows * m.values.element_size()
+    b_iter = bytes_of(m, "csr") + vec_bytes
+    return {"iterations": st.iterations, "ms_per_iter": round(t * 1e3, 4),
+            "spmv_gflops_equiv": round(2.0 * m.nnz / t / 1e9, 2), "gbs": round(b_iter / t / 1e9, 1),
+            "roofline_frac": round(b_iter / t / 1e9 / pk["hbm_gbs"], 4),
+            "relative_residual": st.relative_residual,
+            "note": "cg.cg_solve (hpcg.cg_solve semantics), CSR plain; bytes = matrix + 10 vector passes"}
 
 
 def e2e_measure(args, torch, sp, m, x, fmt) -> dict:
