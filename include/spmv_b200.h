@@ -17,8 +17,10 @@
  *     the reference's exception classes (errors.py:4-37).
  *   - SpMV calls never allocate and never write caller memory other than y
  *     (kernels.py:59,72,94: the kernel owns a fresh y).  Workspace lives in
- *     the plan objects.  All calls are reentrant (bench.py:167-172 calls
- *     kernels from several threads).
+ *     the plan objects.  Calls on different plans are reentrant
+ *     (bench.py:167-172 calls kernels from several threads on different
+ *     matrices); calls that share a plan must be ordered on one stream
+ *     (the plan owns partial-sum slots and the warp-stream range counter).
  *   - Calls that return a host-visible count (plan creation, conversion
  *     analyze steps) synchronise `stream`; SpMV calls are asynchronous.
  */
