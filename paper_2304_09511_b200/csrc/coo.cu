@@ -529,7 +529,8 @@ __global__ void __launch_bounds__(256)
 coo_vla_warp_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __restrict__ run_row, int64_t n_runs,
                     const uint32_t* __restrict__ aj, const T* __restrict__ av, const T* __restrict__ x,
                     int64_t col_base, T* __restrict__ y, int lanes, int width,
-                    unsigned long long* __restrict__ steps_out) {
+                    unsigned long long* __restrict__ steps_out,
+                    const uint32_t* __restrict__ list = nullptr) {  // list: runs to do (n_runs of them)
   const T* xb = x - col_base;
   const int lane = threadIdx.x % width;
   const int rows_per_warp = 32 / width;
@@ -537,9 +538,10 @@ coo_vla_warp_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __re
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   unsigned long long my_steps = 0;
   for (int64_t bidx = warp * rows_per_warp; bidx < n_runs; bidx += nwarps * rows_per_warp) {
-    const int64_t ri = bidx + (threadIdx.x & 31) / width;
+    const int64_t li = bidx + (threadIdx.x & 31) / width;
+    const int64_t ri = list && li < n_runs ? int64_t(list[li]) : li;
     uint32_t a = 0, b = 0, row = 0;
-    if (ri < n_runs) {
+    if (li < n_runs) {
       a = run_start[ri];
       b = run_start[ri + 1];
       row = run_row[ri];
@@ -568,7 +570,7 @@ coo_vla_warp_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __re
         }
       }
     }
-    if (lane == 0 && ri < n_runs && mine) {
+    if (lane == 0 && li < n_runs && mine) {
       y[row] = yv;
       my_steps += nsteps;
     }
@@ -576,6 +578,21 @@ coo_vla_warp_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __re
   if (steps_out) {
     for (int o = 16; o >= 1; o >>= 1) my_steps += __shfl_down_sync(0xffffffffu, my_steps, o);
     if ((threadIdx.x & 31) == 0 && my_steps) atomicAdd(steps_out, my_steps);
+  }
+}
+
+// Runs of <= 32 entries, one thread per run playing all W = next_pow2(L)
+// logical lanes in registers (tile.cuh row_vla_coo; same adds, bit-exact).
+template <typename T, int W>
+__global__ void __launch_bounds__(256)
+coo_vla_short_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __restrict__ run_row, int64_t n_runs,
+                     const uint32_t* __restrict__ aj, const T* __restrict__ av, const T* __restrict__ x,
+                     int64_t col_base, T* __restrict__ y, int lanes) {
+  const T* xb = x - col_base;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_runs; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t a = __ldg(run_start + i), b = __ldg(run_start + i + 1);
+    if (b - a > uint32_t(kExactLen)) continue;
+    y[__ldg(run_row + i)] = row_vla_coo<T, W>(aj + a, av + a, int(b - a), xb, lanes);
   }
 }
 
@@ -637,6 +654,8 @@ struct spmv_coo_plan {
   bool vla_built = false;
   int64_t vla_n = 0, vla_chunks = 0;
   DevBuf vla_runs, vla_pre, vla_chunk_run, vla_S;
+  int64_t vla_n_mid = 0;  // runs of 33..kVlaLong entries (list for coo_vla_warp_kernel)
+  DevBuf vla_mid;
   // warp-stream path (wstream.cuh) for plans with long runs
   bool ws = false;
   int64_t ws_nwarps = 0, ws_nranges = 0, ws_n_span = 0;
@@ -679,6 +698,24 @@ static int coo_vla_build(spmv_coo_plan* p, cudaStream_t st) {
                                                             p->vla_chunk_run.as<uint32_t>());
     SPMV_LAUNCH_CHECK();
     SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  {
+    SPMV_CUDA_TRY(cudaMemsetAsync(ctr.ptr, 0, 8, st));
+    len_class_list_kernel<<<unsigned(g), 256, 0, st>>>(rs, p->n_runs, uint32_t(kExactLen), kVlaLong, nullptr,
+                                                       ctr.as<unsigned long long>());
+    SPMV_LAUNCH_CHECK();
+    unsigned long long m = 0;
+    SPMV_CUDA_TRY(cudaMemcpyAsync(&m, ctr.ptr, 8, cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    p->vla_n_mid = int64_t(m);
+    if (p->vla_n_mid > 0) {
+      if ((rc = p->vla_mid.alloc(4 * p->vla_n_mid))) return rc;
+      SPMV_CUDA_TRY(cudaMemsetAsync(ctr.ptr, 0, 8, st));
+      len_class_list_kernel<<<unsigned(g), 256, 0, st>>>(rs, p->n_runs, uint32_t(kExactLen), kVlaLong,
+                                                         p->vla_mid.as<uint32_t>(), ctr.as<unsigned long long>());
+      SPMV_LAUNCH_CHECK();
+      SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    }
   }
   p->vla_built = true;
   return SPMV_OK;
@@ -1187,10 +1224,47 @@ int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const
             rs, rr, p->n_runs, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
             static_cast<float*>(y), lanes, width, steps);
     };
-    if (long_runs)
+    // long runs, L <= 8: runs <= 32 one thread each, runs of 33..kVlaLong
+    // by sub-warp groups over the plan's list, longer ones two-phase; the
+    // step count then comes from the run lengths
+    const bool split = long_runs && lanes <= 8;
+    if (split) {
+      int rc;
+      if (!p->vla_built && (rc = coo_vla_build(p, st))) return rc;
+      const int64_t gs = std::min<int64_t>((p->n_runs + 255) / 256, cap);
+      auto short_kernel = [&](auto* tag) {
+        using TT = std::remove_pointer_t<decltype(tag)>;
+        const TT* avt = static_cast<const TT*>(av);
+        const TT* xt = static_cast<const TT*>(x);
+        TT* yt = static_cast<TT*>(y);
+        switch (lanes <= 1 ? 1 : lanes <= 2 ? 2 : lanes <= 4 ? 4 : 8) {
+          case 1: coo_vla_short_kernel<TT, 1><<<unsigned(gs), 256, 0, st>>>(rs, rr, p->n_runs, aj, avt, xt, col_base, yt, lanes); break;
+          case 2: coo_vla_short_kernel<TT, 2><<<unsigned(gs), 256, 0, st>>>(rs, rr, p->n_runs, aj, avt, xt, col_base, yt, lanes); break;
+          case 4: coo_vla_short_kernel<TT, 4><<<unsigned(gs), 256, 0, st>>>(rs, rr, p->n_runs, aj, avt, xt, col_base, yt, lanes); break;
+          default: coo_vla_short_kernel<TT, 8><<<unsigned(gs), 256, 0, st>>>(rs, rr, p->n_runs, aj, avt, xt, col_base, yt, lanes);
+        }
+        if (p->vla_n_mid > 0) {
+          const int64_t gm = std::min<int64_t>((p->vla_n_mid * width + tb - 1) / tb, cap);
+          coo_vla_warp_kernel<TT, true><<<unsigned(gm), tb, 0, st>>>(rs, rr, p->vla_n_mid, aj, avt, xt, col_base, yt,
+                                                                     lanes, width, nullptr, p->vla_mid.as<uint32_t>());
+        }
+      };
+      if (p->dtype == SPMV_F64)
+        short_kernel(static_cast<double*>(nullptr));
+      else
+        short_kernel(static_cast<float*>(nullptr));
+      SPMV_LAUNCH_CHECK();
+      if (steps) {
+        const int64_t g = std::min<int64_t>((p->n_runs + 255) / 256, cap);
+        coo_vla_count_steps_kernel<<<unsigned(g), 256, 0, st>>>(rs, p->n_runs, lanes, steps);
+        SPMV_LAUNCH_CHECK();
+        steps = nullptr;  // counted: the two-phase kernels below must not add theirs
+      }
+    } else if (long_runs) {
       warp_kernel(std::true_type{});
-    else
+    } else {
       warp_kernel(std::false_type{});
+    }
     if (long_runs) {  // runs over 32 entries exist: two-phase path for those over kVlaLong
       int rc;
       if (!p->vla_built && (rc = coo_vla_build(p, st))) return rc;
@@ -1232,7 +1306,7 @@ int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const
   SPMV_LAUNCH_CHECK();
   if (outer_steps) {
     unsigned long long h = 0;
-    SPMV_CUDA_TRY(cudaMemcpyAsync(&h, steps, sizeof(h), cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(&h, p->steps.ptr, sizeof(h), cudaMemcpyDeviceToHost, st));
     SPMV_CUDA_TRY(cudaStreamSynchronize(st));
     *outer_steps = int64_t(h);
   }

@@ -567,7 +567,8 @@ template <typename T, bool SKIP_LONG>
 __global__ void __launch_bounds__(256)
 csr_vla_warp_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj,
                     const T* __restrict__ av, const T* __restrict__ x, int64_t col_base,
-                    T* __restrict__ y, int64_t nrows, int lanes, int width) {
+                    T* __restrict__ y, int64_t nrows, int lanes, int width,
+                    const uint32_t* __restrict__ list = nullptr) {  // list: rows to do (nrows of them)
   const T* xb = x - col_base;
   const int lane = threadIdx.x % width;
   const int rows_per_warp = 32 / width;
@@ -575,9 +576,10 @@ csr_vla_warp_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict
   const int64_t nwarps = (int64_t(gridDim.x) * blockDim.x) >> 5;
   // Uniform trip count per warp so the shuffles see every lane.
   for (int64_t base = warp * rows_per_warp; base < nrows; base += nwarps * rows_per_warp) {
-    const int64_t r = base + (threadIdx.x & 31) / width;
+    const int64_t ri = base + (threadIdx.x & 31) / width;
+    const int64_t r = list && ri < nrows ? int64_t(list[ri]) : ri;
     uint32_t s = 0, e = 0;
-    if (r < nrows) {
+    if (ri < nrows) {
       s = irp[r];
       e = irp[r + 1];
     }
@@ -601,7 +603,22 @@ csr_vla_warp_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict
       }
     }
     acc = tree_reduce_warp(acc, width);
-    if (lane == 0 && r < nrows && mine) y[r] = (s == e) ? T(0) : acc;
+    if (lane == 0 && ri < nrows && mine) y[r] = (s == e) ? T(0) : acc;
+  }
+}
+
+// Rows of <= 32 entries, one thread per row playing all W = next_pow2(L)
+// logical lanes in registers (tile.cuh row_vla_csr; same adds, bit-exact).
+// Longer rows are left to csr_vla_warp_kernel (list) and the two-phase path.
+template <typename T, int W>
+__global__ void __launch_bounds__(256)
+csr_vla_short_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj, const T* __restrict__ av,
+                     const T* __restrict__ x, int64_t col_base, T* __restrict__ y, int64_t nrows, int lanes) {
+  const T* xb = x - col_base;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t s = __ldg(irp + r), e = __ldg(irp + r + 1);
+    if (e - s > uint32_t(kExactLen)) continue;
+    y[r] = e == s ? T(0) : row_vla_csr<T, W>(aj + s, av + s, int(e - s), xb, lanes);
   }
 }
 
@@ -666,6 +683,8 @@ struct spmv_csr_plan {
   bool vla_built = false;
   int64_t vla_n = 0, vla_chunks = 0;
   DevBuf vla_rows, vla_pre, vla_chunk_row, vla_prod;
+  int64_t vla_n_mid = 0;  // rows of 33..kVlaLong entries (list for csr_vla_warp_kernel)
+  DevBuf vla_mid;
   int grid_bulk = 0, grid_direct = 0;  // G-group TMA kernel / single-group kernel
   // warp-stream path (wstream.cuh) for plans with long rows: whole-matrix
   // launches only; tile ranges (halo split, host pipeline) keep the tiles
@@ -1161,6 +1180,29 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
   return fail(SPMV_INVALID_ARG, "no CSR kernel for tile %lld x %d groups", (long long)p->tile, p->groups);
 }
 
+template <typename T>
+static int csr_vla_split_launch(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av,
+                                const T* x, int64_t col_base, T* y, int lanes, cudaStream_t st) {
+  const int64_t cap = int64_t(sm_count()) * 16;
+  const int64_t gs = std::min<int64_t>((p->nrows + 255) / 256, cap);
+  switch (lanes <= 1 ? 1 : lanes <= 2 ? 2 : lanes <= 4 ? 4 : 8) {
+    case 1: csr_vla_short_kernel<T, 1><<<unsigned(gs), 256, 0, st>>>(irp, aj, av, x, col_base, y, p->nrows, lanes); break;
+    case 2: csr_vla_short_kernel<T, 2><<<unsigned(gs), 256, 0, st>>>(irp, aj, av, x, col_base, y, p->nrows, lanes); break;
+    case 4: csr_vla_short_kernel<T, 4><<<unsigned(gs), 256, 0, st>>>(irp, aj, av, x, col_base, y, p->nrows, lanes); break;
+    default: csr_vla_short_kernel<T, 8><<<unsigned(gs), 256, 0, st>>>(irp, aj, av, x, col_base, y, p->nrows, lanes);
+  }
+  SPMV_LAUNCH_CHECK();
+  if (p->vla_n_mid > 0) {
+    int width = 1;
+    while (width < lanes) width <<= 1;
+    const int64_t gm = std::min<int64_t>((p->vla_n_mid * width + 255) / 256, cap);
+    csr_vla_warp_kernel<T, true><<<unsigned(gm), 256, 0, st>>>(irp, aj, av, x, col_base, y, p->vla_n_mid, lanes, width,
+                                                               p->vla_mid.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+  }
+  return SPMV_OK;
+}
+
 extern "C" {
 
 int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* row_pointers,
@@ -1347,6 +1389,24 @@ static int csr_vla_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st)
     SPMV_LAUNCH_CHECK();
     SPMV_CUDA_TRY(cudaStreamSynchronize(st));  // cnt and the host vector go out of scope
   }
+  {
+    SPMV_CUDA_TRY(cudaMemsetAsync(ctr.ptr, 0, 8, st));
+    len_class_list_kernel<<<unsigned(g), 256, 0, st>>>(irp, p->nrows, uint32_t(kExactLen), kVlaLong, nullptr,
+                                                       ctr.as<unsigned long long>());
+    SPMV_LAUNCH_CHECK();
+    unsigned long long m = 0;
+    SPMV_CUDA_TRY(cudaMemcpyAsync(&m, ctr.ptr, 8, cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    p->vla_n_mid = int64_t(m);
+    if (p->vla_n_mid > 0) {
+      if ((rc = p->vla_mid.alloc(4 * p->vla_n_mid))) return rc;
+      SPMV_CUDA_TRY(cudaMemsetAsync(ctr.ptr, 0, 8, st));
+      len_class_list_kernel<<<unsigned(g), 256, 0, st>>>(irp, p->nrows, uint32_t(kExactLen), kVlaLong,
+                                                         p->vla_mid.as<uint32_t>(), ctr.as<unsigned long long>());
+      SPMV_LAUNCH_CHECK();
+      SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    }
+  }
   p->vla_built = true;
   return SPMV_OK;
 }
@@ -1443,7 +1503,21 @@ int spmv_csr_vla_planned(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* 
                           st);
   int rc;
   if (!p->vla_built && (rc = csr_vla_build(p, irp, st))) return rc;
-  if ((rc = csr_vla_launch(p->dtype, p->nrows, p->nnz, irp, aj, av, x, col_base, x_len, y, lanes, 2, st))) return rc;
+  if (lanes <= 8) {
+    // rows <= 32: one thread per row (all logical lanes in registers);
+    // rows of 33..kVlaLong: sub-warp groups over the plan's list; longer:
+    // the two-phase path below
+    if ((rc = p->dtype == SPMV_F64
+                  ? csr_vla_split_launch<double>(p, irp, aj, static_cast<const double*>(av),
+                                                 static_cast<const double*>(x), col_base, static_cast<double*>(y),
+                                                 lanes, st)
+                  : csr_vla_split_launch<float>(p, irp, aj, static_cast<const float*>(av),
+                                                static_cast<const float*>(x), col_base, static_cast<float*>(y), lanes,
+                                                st)))
+      return rc;
+  } else if ((rc = csr_vla_launch(p->dtype, p->nrows, p->nnz, irp, aj, av, x, col_base, x_len, y, lanes, 2, st))) {
+    return rc;
+  }
   if (p->vla_n == 0) return SPMV_OK;
   int width = 1;
   while (width < lanes) width <<= 1;

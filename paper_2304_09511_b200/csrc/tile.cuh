@@ -223,6 +223,20 @@ __device__ __forceinline__ T row_vla_coo_wide(const uint32_t* __restrict__ c, T*
   return y;
 }
 
+// Indices i whose segment starts[i+1] - starts[i] lies in (lo, hi] (CSR rows
+// or COO runs of one length class; order irrelevant).  out == nullptr counts.
+static __global__ void len_class_list_kernel(const uint32_t* __restrict__ starts, int64_t n, uint32_t lo,
+                                             uint32_t hi, uint32_t* __restrict__ out,
+                                             unsigned long long* __restrict__ cnt) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t len = starts[i + 1] - starts[i];
+    if (len > lo && len <= hi) {
+      const unsigned long long k = atomicAdd(cnt, 1ull);
+      if (out) out[k] = uint32_t(i);
+    }
+  }
+}
+
 // Left-to-right sum of already-formed products (the "products" tile mode).
 template <typename T>
 __device__ __forceinline__ T row_sum(const T* __restrict__ p, int len, T acc) {
