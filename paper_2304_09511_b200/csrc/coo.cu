@@ -274,13 +274,23 @@ coo_tile_kernel(const __grid_constant__ CooParams<T> P) {
     const int64_t t = first + i * stride;
     const int64_t E0 = t * TILE;
     const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
+    const uint32_t cb = cnt & ~3u;  // bulk part: 16-byte multiples
     const uint32_t pre = t > 0 ? uint32_t(kExt) : 0u;
     const int s = int(i % STAGES);
     if (G > 1) tickets[s] = int(i);
-    mbar_arrive_expect_tx(&bars[s], (cnt + pre) * 4u + cnt * (4u + uint32_t(sizeof(T))));
-    bulk_g2s(rows_of(s) + (kExt - pre), P.ai + E0 - pre, (cnt + pre) * 4u, &bars[s], (P.mode & 4) != 0);
-    bulk_g2s(cols_of(s), P.aj + E0, cnt * 4u, &bars[s], (P.mode & 4) != 0);
-    bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s], (P.mode & 4) != 0);
+    // the last tiles' 1..3 odd entries: plain copies, published by the
+    // arrive below (release) like the bulk bytes by complete_tx
+    for (uint32_t k = cb; k < cnt; ++k) {
+      rows_of(s)[kExt + k] = P.ai[E0 + k];
+      cols_of(s)[k] = P.aj[E0 + k];
+      vals_of(s)[k] = P.av[E0 + k];
+    }
+    mbar_arrive_expect_tx(&bars[s], (cb + pre) * 4u + cb * (4u + uint32_t(sizeof(T))));
+    if (cb + pre) bulk_g2s(rows_of(s) + (kExt - pre), P.ai + E0 - pre, (cb + pre) * 4u, &bars[s], (P.mode & 4) != 0);
+    if (cb) {
+      bulk_g2s(cols_of(s), P.aj + E0, cb * 4u, &bars[s], (P.mode & 4) != 0);
+      bulk_g2s(vals_of(s), P.av + E0, cb * uint32_t(sizeof(T)), &bars[s], (P.mode & 4) != 0);
+    }
   };
   if (BULK) {
     if (threadIdx.x == 0) {

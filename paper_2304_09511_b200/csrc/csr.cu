@@ -247,11 +247,20 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
   auto issue = [&](int64_t i) {
     const int64_t E0 = (first + i * stride) * TILE;
     const uint32_t cnt = uint32_t(min(int64_t(TILE + kExt), P.nnz - E0));
+    const uint32_t cb = cnt & ~3u;  // bulk part: 16-byte multiples
     const int s = int(i % STAGES);
     if (G > 1) tickets[s] = int(i);
-    mbar_arrive_expect_tx(&bars[s], cnt * uint32_t(sizeof(uint32_t) + sizeof(T)));
-    bulk_g2s(cols_of(s), P.aj + E0, cnt * uint32_t(sizeof(uint32_t)), &bars[s], (P.mode & 4) != 0);
-    bulk_g2s(vals_of(s), P.av + E0, cnt * uint32_t(sizeof(T)), &bars[s], (P.mode & 4) != 0);
+    // the last tiles' 1..3 odd entries: plain copies, published by the
+    // arrive below (release) like the bulk bytes by complete_tx
+    for (uint32_t k = cb; k < cnt; ++k) {
+      cols_of(s)[k] = P.aj[E0 + k];
+      vals_of(s)[k] = P.av[E0 + k];
+    }
+    mbar_arrive_expect_tx(&bars[s], cb * uint32_t(sizeof(uint32_t) + sizeof(T)));
+    if (cb) {
+      bulk_g2s(cols_of(s), P.aj + E0, cb * uint32_t(sizeof(uint32_t)), &bars[s], (P.mode & 4) != 0);
+      bulk_g2s(vals_of(s), P.av + E0, cb * uint32_t(sizeof(T)), &bars[s], (P.mode & 4) != 0);
+    }
   };
   if (BULK) {
     if (threadIdx.x == 0) {
