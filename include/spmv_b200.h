@@ -79,8 +79,8 @@ int spmv_csr_plan_destroy(spmv_csr_plan* plan);
  * the CSR tile kernel, read and reset (8 entries); else SPMV_UNSUPPORTED. */
 int spmv_debug_csr_phases(unsigned long long* out8);
 /* n_long_rows: rows longer than exact_len; n_items: entries per tile;
- * launches: kernels one spmv_csr call launches (1; +1 for tail tiles the
- * bulk engine cannot address when groups > 1; +1 for the span fix-up). */
+ * launches: kernels one spmv_csr call launches (1; +1 for the span
+ * fix-up of rows split between tiles or warp-stream ranges). */
 int spmv_csr_plan_info(const spmv_csr_plan* plan, int64_t* n_long_rows,
                        int64_t* n_items, int64_t* launches);
 /* Consumer groups per tile CTA the plan chose (SPMV_CSR_GROUPS overrides). */
