@@ -16,6 +16,11 @@
 // ndiags, odd strides are bank-conflict free for 8-byte words) and gathers
 // x through L1: the x window of a tile is re-read by every diagonal with
 // the same (dz, dy), so it stays L1/L2 resident.
+#include <map>
+#include <mutex>
+#include <tuple>
+#include <utility>
+
 #include "tma.cuh"
 
 namespace spmv {
@@ -200,9 +205,31 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
   const size_t off_bytes = (size_t(nd) * 4 + 127) & ~size_t(127);
   auto launch = [&](auto kernel, int threads, int stages) -> int {
     const size_t smem = 128 + off_bytes + size_t(stages) * stage_bytes;
-    SPMV_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+    // the attribute and occupancy of a (device, kernel, shared-memory size)
+    // are queried once; these host calls used to run on every product
+    static std::mutex mu;
+    static std::map<std::pair<int, const void*>, size_t> attr;      // largest smem allowed so far
+    static std::map<std::tuple<int, const void*, size_t>, int> occ;  // CTAs per SM at a smem size
     int per_sm = 0;
-    SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    {
+      int dev = 0;
+      SPMV_CUDA_TRY(cudaGetDevice(&dev));
+      const void* kp = reinterpret_cast<const void*>(kernel);
+      std::lock_guard<std::mutex> lock(mu);
+      size_t& allowed = attr[{dev, kp}];
+      if (smem > allowed) {  // the attribute only ever grows
+        SPMV_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
+        allowed = smem;
+      }
+      const auto key = std::make_tuple(dev, kp, smem);
+      auto it = occ.find(key);
+      if (it != occ.end()) {
+        per_sm = it->second;
+      } else {
+        SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+        occ[key] = per_sm;
+      }
+    }
     if (per_sm < 1) return fail(SPMV_UNSUPPORTED, "DIA tile of %u bytes x %d stages does not fit", stage_bytes, stages);
     int64_t grid = int64_t(sms) * per_sm;
     if (grid > ntiles) grid = ntiles;
