@@ -331,7 +331,7 @@ def run_ours(args, torch, dist, rank, world, local_rank):
         return run_ours_multi(args, torch, dist, rank, world, local_rank, pk)
     mats, x = build_workload(torch, sp, args.config, device)
     if args.conversions:
-        print(json.dumps({"config": args.config, "conversions": conversions_measure(torch, sp, mats, pk)}), flush=True)
+        emit({"config": args.config, "conversions": conversions_measure(torch, sp, mats, pk)})
         return
     flush_buf = None
     flush = None
@@ -414,7 +414,7 @@ def run_ours(args, torch, dist, rank, world, local_rank):
             y_gpu = sp.spmv_csr_plain(csr, x).cpu().numpy()
             line["cpu_baseline"] = cpu_baseline_csr(h["row_pointers"], h["col_indices"], h["values"],
                                                     x.cpu().numpy(), args.cpu_budget, y_check=y_gpu)
-    print(json.dumps(line), flush=True)
+    emit(line)
 
 
 def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
@@ -423,19 +423,43 @@ def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
     the interior rows overlapping the exchange; time = max over ranks."""
     import paper_2304_09511_b200 as sp
     from paper_2304_09511_b200 import synthetic
-    from paper_2304_09511_b200.dist import DistributedMatrix, RowPartition
+    from paper_2304_09511_b200.dist import DistributedMatrix, RowPartition, _csr_rows
     from paper_2304_09511_b200.matrixio import stencil27_nnz
 
-    if args.config not in ("c5", "c1"):
-        raise SystemExit("multi-GPU bench implemented for the stencil configs (c5, c1)")
     device = torch.device("cuda", local_rank)
     cfg = CONFIGS[args.config]
-    nx, ny, nz = cfg["grid"]
-    n = nx * ny * nz
-    nnz_total = stencil27_nnz(nx, ny, nz)
-    part = RowPartition.contiguous(n, world, unit=nx * ny)
-    r0, r1 = part.rows(rank)
-    rows = sp.gen_stencil27_rows(nx, ny, nz, r0, r1)
+    nd = 27
+    if args.config in ("c5", "c1"):
+        # z-slabs of the stencil, generated per rank on the device
+        nx, ny, nz = cfg["grid"]
+        n = nx * ny * nz
+        nnz_total = stencil27_nnz(nx, ny, nz)
+        part = RowPartition.contiguous(n, world, unit=nx * ny)
+        r0, r1 = part.rows(rank)
+        rows = sp.gen_stencil27_rows(nx, ny, nz, r0, r1)
+        exchange = "NCCL halo exchange of x planes"
+    elif args.config == "c4":
+        # banded 2^23: row blocks (multiples of ROW_PAD), 4096-entry halos
+        n = 1 << 23
+        offs, vals, nnz_total = synthetic.banded_dia(n, synthetic.BANDED_OFFSETS, synthetic.BANDED_SEED)
+        nd = len(offs)
+        part = RowPartition.contiguous(n, world, unit=8)
+        r0, r1 = part.rows(rank)
+        full = sp.to_format(sp.DiaMatrix(sp.MatrixShape(n, n, nnz_total), offs, vals), "csr")
+        rows = _csr_rows(full, r0, r1)
+        del full
+        exchange = "NCCL halo exchange of 4096-entry x blocks"
+    else:
+        # Zipf: every rank needs all of x (uniform columns): NCCL all-gather
+        n = 2_000_000
+        irp, cols, vals = synthetic.zipf_csr(n, n, synthetic.ZIPF_SEED)
+        nnz_total = int(irp[-1])
+        part = RowPartition.contiguous(n, world)
+        r0, r1 = part.rows(rank)
+        e0, e1 = int(irp[r0]), int(irp[r1])
+        rows = sp.CsrMatrix.from_arrays(r1 - r0, n, (irp[r0:r1 + 1].astype(np.int64) - e0).astype(np.uint32),
+                                        cols[e0:e1], vals[e0:e1])
+        exchange = "NCCL all-gather of x"
     x_full = synthetic.probe_x(n, synthetic.X_SEED)
     x_local = torch.from_numpy(x_full[r0:r1]).to(device)
     head = args.format or cfg["formats"][0]
@@ -456,7 +480,6 @@ def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
             clocks = sampler.summary()
         else:
             t = time_steps(torch, fn, max(10, args.steps // 4), args.warmup, dist=dist)
-        nd = 27
         b_total = algo_bytes(fmt, n, n, nnz_total, 8, nd)
         agg = b_total / t / 1e9
         results[fmt] = {"gflops": round(2.0 * nnz_total / t / 1e9, 2), "ms_per_spmv": round(t * 1e3, 4),
@@ -470,7 +493,7 @@ def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
         "config": {"workload": cfg["workload"], "config": args.config, "format": head, "nrows": n, "nnz": nnz_total,
                    "l2": "inputs larger than L2 (126 MB), no flush",
-                   "parallelism": f"row-partition: {world} z-slabs, NCCL halo exchange of x planes, "
+                   "parallelism": f"row-partition: {world} contiguous row blocks, {exchange}, "
                                   "interior rows overlapped with the exchange"},
         "roofline": roofline(results[head]["bytes_per_spmv"] // world, t, pk, traffic_for(f"{args.config}/{head}")),
         "gpu_launches": args.steps * results[head]["launches"],
@@ -495,7 +518,7 @@ def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
                        "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8, "ms_per_step": round(te * 1e3, 3),
                        "path": "DistributedMatrix.spmv per rank, pinned host x slice in, pinned host y slice out"}
     if rank == 0:
-        print(json.dumps(line), flush=True)
+        emit(line)
 
 
 def cg_measure(torch, sp, m, pk, iters: int = 20) -> dict:
@@ -559,7 +582,7 @@ def run_reference(args, rank, world):
     from paper_2304_09511_b200 import synthetic
     cfg = CONFIGS[args.config]
     if args.config not in ("c5", "c1"):
-        print(json.dumps({"impl": "reference", "unavailable": f"reference arm implemented for c1/c5, not {args.config}"}))
+        emit({"impl": "reference", "unavailable": f"reference arm implemented for c1/c5, not {args.config}"})
         return
     nx, ny, nz = cfg["grid"]
     n = nx * ny * nz
@@ -593,10 +616,24 @@ def run_reference(args, rank, world):
             "cpu_baseline": {"value": v, "unit": UNIT, "kind": "port", "cores": c_oracle.max_threads(),
                              "sample": sample + "; oracle/spmv_oracle.c csr_plain (restates kernels.py:69-82)"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
-    print(json.dumps(line), flush=True)
+    emit(line)
+
+
+_JSON_FD = None
+
+
+def emit(line: dict) -> None:
+    """The one JSON line, on the real stdout (see main)."""
+    os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
 
 
 def main():
+    global _JSON_FD
+    # Only the JSON line goes to stdout: everything else that writes to fd 1
+    # (NCCL's version banner, library chatter) is sent to stderr.
+    sys.stdout.flush()
+    _JSON_FD = os.dup(1)
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
