@@ -573,48 +573,94 @@ def e2e_measure(args, torch, sp, m, x, fmt) -> dict:
 
 
 # -------------------------------------------------------------- reference --
+def _reference_sample(args, c_oracle, synthetic):
+    """The bounded CPU sample of the config's headline workload: returns
+    (step function, entries per step, description, format).  A sample is a
+    contiguous block of rows sized so that one step takes ~0.25 s."""
+    cfg = CONFIGS[args.config]
+
+    def calibrate(build, total_rows, unit):
+        # time a 1/16 sample after a warm-up call (thread-pool start-up),
+        # then size the step for ~0.25 s
+        k = max(unit, total_rows // 16 // unit * unit)
+        fn, nnz, _ = build(k)
+        fn()
+        t0 = time.perf_counter()
+        fn()
+        per_row = (time.perf_counter() - t0) / k
+        k = int(max(unit, min(total_rows, 0.25 / max(per_row, 1e-12)))) // unit * unit
+        return build(max(unit, k))
+
+    if args.config in ("c5", "c1"):
+        nx, ny, nz = cfg["grid"]
+        n, plane = nx * ny * nz, nx * ny
+        x = synthetic.probe_x(n, synthetic.X_SEED)
+
+        def build(k):
+            planes = k // plane
+            r0 = (nz // 2 - planes // 2) * plane if planes < nz else 0
+            r1 = r0 + planes * plane
+            irp, cols, vals = c_oracle.stencil27_rows(nx, ny, nz, r0, r1)
+            desc = (f"z-planes {r0 // plane}..{r1 // plane - 1} of the {nx}x{ny}x{nz} stencil "
+                    f"({r1 - r0} rows, {vals.shape[0]} entries) per step; oracle/spmv_oracle.c csr_plain "
+                    "(restates kernels.py:69-82)")
+            return (lambda: c_oracle.csr_plain(r1 - r0, irp, cols, vals, x)), vals.shape[0], desc
+
+        fn, nnz, desc = calibrate(build, n, plane)
+        return fn, nnz, desc, "csr"
+    if args.config == "c3":
+        n = 2_000_000
+        irp, cols, vals = synthetic.zipf_csr(n, n, synthetic.ZIPF_SEED)
+        x = synthetic.probe_x(n, synthetic.X_SEED)
+
+        def build(k):
+            e = int(irp[k])
+            sirp, scols, svals = irp[:k + 1], cols[:e], vals[:e]
+            desc = (f"rows 0..{k - 1} of the Zipf matrix ({e} entries) per step; oracle/spmv_oracle.c csr_plain "
+                    "(restates kernels.py:69-82)")
+            return (lambda: c_oracle.csr_plain(k, sirp, scols, svals, x)), e, desc
+
+        fn, nnz, desc = calibrate(build, n, 1024)
+        return fn, nnz, desc, "csr"
+    # c4: banded DIA, the config's headline format
+    n = 1 << 23
+    offs, vals, _ = synthetic.banded_dia(n, synthetic.BANDED_OFFSETS, synthetic.BANDED_SEED)
+    x = synthetic.probe_x(n, synthetic.X_SEED)
+    o64 = offs.astype(np.int64)
+
+    def build(k):
+        cells = int(np.maximum(0, np.minimum(k, n - o64) - np.maximum(0, -o64)).sum())
+        sv = np.ascontiguousarray(vals[:k])
+        desc = (f"rows 0..{k - 1} of the banded matrix ({cells} in-bounds cells) per step; oracle/spmv_oracle.c "
+                "dia_plain (restates kernels.py:85-101)")
+        return (lambda: c_oracle.dia_plain(k, n, offs, sv, x)), cells, desc
+
+    fn, nnz, desc = calibrate(build, n, 8)
+    return fn, nnz, desc, "dia"
+
+
 def run_reference(args, rank, world):
-    """The reference's CPU SpMV (C restatement of kernels.py:69-82, all host
+    """The reference's CPU SpMV (C restatement of kernels.py, all host
     threads) on a bounded sample of the same workload; no GPU touched."""
     if rank != 0:
         return
     from oracle import c_oracle
     from paper_2304_09511_b200 import synthetic
     cfg = CONFIGS[args.config]
-    if args.config not in ("c5", "c1"):
-        emit({"impl": "reference", "unavailable": f"reference arm implemented for c1/c5, not {args.config}"})
-        return
-    nx, ny, nz = cfg["grid"]
-    n = nx * ny * nz
-    x = synthetic.probe_x(n, synthetic.X_SEED)
-    # calibrate the sample: a z-slab sized so one step takes <= ~0.25 s
-    plane = nx * ny
-    slab = max(1, min(nz, 16))
-    irp, cols, vals = c_oracle.stencil27_rows(nx, ny, nz, 0, slab * plane)
-    t0 = time.perf_counter()
-    c_oracle.csr_plain(slab * plane, irp, cols, vals, x)
-    t1 = time.perf_counter() - t0
-    per_plane = t1 / slab
-    planes = int(max(1, min(nz, 0.25 / max(per_plane, 1e-6))))
-    r0 = (nz // 2 - planes // 2) * plane if planes < nz else 0
-    r1 = r0 + planes * plane
-    irp, cols, vals = c_oracle.stencil27_rows(nx, ny, nz, r0, r1)
-    fn = lambda: c_oracle.csr_plain(r1 - r0, irp, cols, vals, x)  # noqa: E731
+    fn, nnz, sample, fmt = _reference_sample(args, c_oracle, synthetic)
     for _ in range(args.warmup):
         fn()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         fn()
     t = (time.perf_counter() - t0) / args.steps
-    v = round(2.0 * vals.shape[0] / t / 1e9, 3)
-    sample = (f"z-planes {r0 // plane}..{r1 // plane - 1} of the {nx}x{ny}x{nz} stencil "
-              f"({r1 - r0} rows, {vals.shape[0]} entries) per step")
+    v = round(2.0 * nnz / t / 1e9, 3)
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
-            "config": {"workload": cfg["workload"], "config": args.config, "format": "csr"},
+            "config": {"workload": cfg["workload"], "config": args.config, "format": fmt},
             "cpu_baseline": {"value": v, "unit": UNIT, "kind": "port", "cores": c_oracle.max_threads(),
-                             "sample": sample + "; oracle/spmv_oracle.c csr_plain (restates kernels.py:69-82)"},
+                             "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     emit(line)
 
