@@ -207,3 +207,33 @@ def test_vla_tile_path_all_lane_widths(sp, dtype):
         ref = O.coo_vla(nrows, rows, cols, vals, x, lanes, ref_stats)
         assert bit_equal(y, ref), ("coo", lanes, first_diff(y, ref))
         assert stats["outer_steps"] == ref_stats["outer_steps"]
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_warp_stream_threshold_lengths(sp, dtype):
+    """Warp-stream plans (rows over 32 entries): row lengths on every
+    threshold the kernels branch on (32 exact / 64 lane-serial / 256 chunk),
+    empty rows between them, a row spanning many chunks and ranges, and a
+    length total that is no multiple of the chunk."""
+    rng = np.random.default_rng(11)
+    base = [0, 1, 31, 32, 33, 63, 64, 65, 255, 256, 257, 511, 512, 513, 0, 0, 7]
+    lens = np.array(base * 40 + [20_000] + base * 40 + [3], dtype=np.int64)
+    nrows, ncols = lens.shape[0], 30_000
+    irp, cols, vals = random_csr(rng, nrows, ncols, lens)
+    vals = vals.astype(dtype)
+    x = rng.uniform(-1, 1, ncols).astype(dtype)
+    ref = c_oracle.csr_plain(nrows, irp, cols, vals, x)
+    ref64 = c_oracle.csr_plain(nrows, irp, cols, vals.astype(np.float64), x.astype(np.float64))
+    tol = 1e-12 if dtype == np.float64 else 1e-5
+    csr = sp.CsrMatrix.from_arrays(nrows, ncols, irp, cols, vals)
+    from paper_2304_09511_b200 import kernels as K
+    assert K.csr_plan(csr).info()["kernel"] == "warp_stream"
+    check(sp.spmv_csr_plain(csr, x), ref, ref64, lens, tol)
+    coo = sp.csr_to_coo(csr)
+    assert K.coo_plan(coo).info()["kernel"] == "warp_stream"
+    rows = np.repeat(np.arange(nrows), lens)
+    check(sp.spmv_coo_plain(coo, x), c_oracle.coo_plain(nrows, rows, cols, vals, x), ref64, lens, tol)
+    # determinism: dynamic range hand-out must not change a bit
+    a = sp.spmv_csr_plain(csr, x)
+    b = sp.spmv_csr_plain(csr, x)
+    assert bit_equal(a, b)
