@@ -61,6 +61,8 @@ def main():
                 slab.run_part(p, y)
 
         t = time_fn(step)
+        if world == max(args.worlds) and rank == 1:
+            res["parts_ms_rank1"] = [round(time_fn(lambda p=p: slab.run_part(p, y)) * 1e3, 4) for p in slab.parts]
         del slab, rows, y
         torch.cuda.empty_cache()
         return t
