@@ -85,6 +85,15 @@ int spmv_csr_plan_info(const spmv_csr_plan* plan, int64_t* n_long_rows,
                        int64_t* n_items, int64_t* launches);
 /* Consumer groups per tile CTA the plan chose (SPMV_CSR_GROUPS overrides). */
 int spmv_csr_plan_groups(const spmv_csr_plan* plan, int* groups);
+/* spmv_csr with a gap in y: rows >= y_split are stored at y[row + y_gap].
+ * A rank's two boundary planes (its first and last halo-reading rows, one
+ * CSR matrix) then run in one launch after the halo exchange while y keeps
+ * the slab's row order.  Plans without rows over exact_len only
+ * (SPMV_UNSUPPORTED otherwise). */
+int spmv_csr_gapped(const spmv_csr_plan* plan, const uint32_t* row_pointers,
+                    const uint32_t* col_indices, const void* values,
+                    const void* x, int64_t col_base, int64_t x_len, void* y,
+                    int64_t y_split, int64_t y_gap, void* stream);
 /* Whole-matrix kernel the plan chose: warp_stream = 1 for the warp-stream
  * kernel (matrices with rows longer than exact_len: one contiguous entry
  * range per resident warp, nwarps of them), 0 for the tile kernel.  Tile

@@ -59,6 +59,7 @@ SIGNATURES = {
     "spmv_csr_plan_tiles": [_vp, _pi64, _pi64],
     "spmv_csr_plan_groups": [_vp, _pint],
     "spmv_csr_plan_path": [_vp, _pint, _pi64],
+    "spmv_csr_gapped": [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _vp],
     "spmv_coo_plan_groups": [_vp, _pint],
     "spmv_coo_plan_path": [_vp, _pint, _pi64],
     "spmv_csr_host": [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _vp],

@@ -64,7 +64,15 @@ struct CsrParams {
   int exact_len;
   int mode;
   int vla;  // lanes L of a vla tile launch (template VW = next_pow2(L) > 0)
+  // rows >= y_split are stored y_gap entries further on (spmv_csr_gapped:
+  // a slab's two boundary planes in one launch); y_split = INT64_MAX else
+  int64_t y_split, y_gap;
 };
+
+template <typename T>
+__device__ __forceinline__ int64_t yrow(const CsrParams<T>& P, int64_t r) {
+  return r >= P.y_split ? r + P.y_gap : r;
+}
 
 // Shared memory of a CSR tile CTA with G consumer groups and G + 1 stages:
 // [0, 64) stage mbarriers, [64, 96) stage tickets, [96, 160) two counters
@@ -132,16 +140,16 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
   while (r < rend) {
     const uint32_t len = e - s;
     if (len == 0) {
-      if (r < R1) P.y[r] = T(0);
+      if (r < R1) P.y[yrow(P, r)] = T(0);
     } else if (len <= uint32_t(P.exact_len)) {
       if (int64_t(s) >= E0 && int64_t(s) < E1) {
         if constexpr (VW >= 16)
-          P.y[r] = row_vla_csr_wide<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla);
+          P.y[yrow(P, r)] = row_vla_csr_wide<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla);
         else if constexpr (VW > 0)
-          P.y[r] = row_vla_csr<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla);
+          P.y[yrow(P, r)] = row_vla_csr<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla);
         else
           // -0.0 seed: the sum starts from the first product, like cumsum
-          P.y[r] = products ? row_sum(vals + (s - E0), int(len), T(-0.0))
+          P.y[yrow(P, r)] = products ? row_sum(vals + (s - E0), int(len), T(-0.0))
                             : row_dot(cols + (s - E0), vals + (s - E0), int(len), xb, T(-0.0));
       }
     } else {
@@ -742,7 +750,8 @@ static int csr_launch_config(spmv_csr_plan* p) {
 
 template <typename T, int TILE, int G, bool LONG, int VW = 0>
 static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
-                   int64_t col_base, T* y, cudaStream_t st, int64_t tb, int64_t te, bool fixup, int vla = 0) {
+                   int64_t col_base, T* y, cudaStream_t st, int64_t tb, int64_t te, bool fixup, int vla = 0,
+                   int64_t y_split = INT64_MAX, int64_t y_gap = 0) {
   if (p->nrows == 0) return SPMV_OK;
   if (p->nnz == 0) {
     SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
@@ -765,6 +774,8 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
   P.tile_end = te;
   P.exact_len = p->exact_len;
   P.vla = vla;
+  P.y_split = y_split;
+  P.y_gap = y_gap;
   P.mode = tile_mode_flags() | ((tma_hint_mode() < 0 ? p->n_long > 0 : tma_hint_mode() > 0) ? 4 : 0);
   const bool aligned = (reinterpret_cast<uintptr_t>(aj) % 16 == 0) && (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
@@ -847,12 +858,14 @@ static int csr_run_ws(const spmv_csr_plan* p, const uint32_t* irp, const uint32_
 
 template <typename T>
 static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
-                   int64_t col_base, T* y, cudaStream_t st, int64_t tb = 0, int64_t te = -1, bool fixup = true) {
+                   int64_t col_base, T* y, cudaStream_t st, int64_t tb = 0, int64_t te = -1, bool fixup = true,
+                   int64_t y_split = INT64_MAX, int64_t y_gap = 0) {
   if (te < 0) te = p->ntiles;
-  if (p->ws && tb == 0 && te == p->ntiles && fixup) return csr_run_ws<T>(p, irp, aj, av, x, col_base, y, st);
+  if (p->ws && tb == 0 && te == p->ntiles && fixup && y_gap == 0)
+    return csr_run_ws<T>(p, irp, aj, av, x, col_base, y, st);
 #define X(TL, GR, LF)                                                          \
   if (p->tile == TL && p->groups == GR && p->long_scratch == bool(LF))          \
-    return csr_run_tiled<T, TL, GR, bool(LF)>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup);
+    return csr_run_tiled<T, TL, GR, bool(LF)>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup, 0, y_split, y_gap);
   SPMV_CSR_CONFIGS(X)
 #undef X
   return fail(SPMV_INVALID_ARG, "no CSR kernel for tile %lld x %d groups", (long long)p->tile, p->groups);
@@ -1325,6 +1338,22 @@ int spmv_csr_range(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* 
                            static_cast<double*>(y), st, tile_begin, tile_end, fixup != 0);
   return csr_run<float>(p, irp, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
                         static_cast<float*>(y), st, tile_begin, tile_end, fixup != 0);
+}
+
+int spmv_csr_gapped(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av, const void* x,
+                    int64_t col_base, int64_t x_len, void* y, int64_t y_split, int64_t y_gap, void* stream) {
+  if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
+  if (p->nrows == 0 || p->nnz == 0) return fail(SPMV_INVALID_ARG, "gapped products need a non-empty matrix");
+  if (y_split < 0 || y_split > p->nrows || y_gap < 0) return fail(SPMV_INVALID_ARG, "bad y split / gap");
+  if (p->n_long > 0 || p->ws)
+    return fail(SPMV_UNSUPPORTED, "gapped products serve plans without rows over %d entries", p->exact_len);
+  if (x_len < 0 || col_base < 0) return fail(SPMV_DIMENSION_MISMATCH, "bad x window");
+  cudaStream_t st = as_stream(stream);
+  if (p->dtype == SPMV_F64)
+    return csr_run<double>(p, irp, aj, static_cast<const double*>(av), static_cast<const double*>(x), col_base,
+                           static_cast<double*>(y), st, 0, p->ntiles, true, y_split, y_gap);
+  return csr_run<float>(p, irp, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
+                        static_cast<float*>(y), st, 0, p->ntiles, true, y_split, y_gap);
 }
 
 int spmv_csr_host(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av, const void* x_host,

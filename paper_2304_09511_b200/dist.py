@@ -175,6 +175,17 @@ class _Part:
     lo: int
     hi: int
     matrix: object  # CsrMatrix / CooMatrix / DiaMatrix view
+    gap: int = 0    # CSR rows >= hi write y[row + gap] (spmv_csr_gapped)
+
+
+def _csr_rows2(csr: CsrMatrix, a0: int, b0: int, a1: int, b1: int) -> CsrMatrix:
+    """Rows [a0, b0) then [a1, b1) as one standalone CSR."""
+    irp = csr.row_pointers.to(torch.int64) & 0xFFFFFFFF
+    s0, e0, s1, e1 = int(irp[a0]), int(irp[b0]), int(irp[a1]), int(irp[b1])
+    new_irp = torch.cat([irp[a0:b0 + 1] - s0, irp[a1 + 1:b1 + 1] - s1 + (e0 - s0)]).to(torch.int32)
+    cols = torch.cat([csr.col_indices[s0:e0], csr.col_indices[s1:e1]])
+    vals = torch.cat([csr.values[s0:e0], csr.values[s1:e1]])
+    return CsrMatrix(MatrixShape((b0 - a0) + (b1 - a1), csr.ncols, (e0 - s0) + (e1 - s1)), new_irp, cols, vals)
 
 
 @dataclass
@@ -189,6 +200,9 @@ class LocalSlab:
     parts: list = field(default_factory=list)   # [lower, interior, upper]
     nnz: int = 0
     xw: torch.Tensor = None
+    # CSR: lower + upper rows as one matrix, one launch after the exchange
+    # (y gap over the interior rows); None when not applicable
+    boundary: _Part = None
 
     @property
     def nloc(self) -> int:
@@ -208,7 +222,12 @@ class LocalSlab:
         yv = y[part.lo:part.hi]
         st = _stream(y.device)
         xw = self.xw
-        if isinstance(m, CsrMatrix):
+        if isinstance(m, CsrMatrix) and part.gap:
+            p = csr_plan(m)
+            _lib.call("spmv_csr_gapped", p.handle, m.row_pointers.data_ptr(), m.col_indices.data_ptr(),
+                      m.values.data_ptr(), xw.data_ptr(), self.window[0], xw.shape[0], y.data_ptr(), part.hi,
+                      part.gap, st)
+        elif isinstance(m, CsrMatrix):
             p = csr_plan(m)
             _lib.call("spmv_csr", p.handle, m.row_pointers.data_ptr(), m.col_indices.data_ptr() if m.nnz else 0,
                       m.values.data_ptr() if m.nnz else 0, xw.data_ptr(), self.window[0], xw.shape[0],
@@ -290,6 +309,11 @@ def build_local_slab(csr_rows: CsrMatrix, r0: int, r1: int, fmt: str = "csr") ->
                 raise ValueError(f"unknown format {fmt}")
             pieces.append(_Part(a, b, part))
         slab = LocalSlab(fmt, (r0, r1), win, ncols, pieces, csr_rows.nnz)
+        if fmt == "csr" and 0 < i_lo and i_hi < nloc and dev.type == "cuda":
+            from .kernels import csr_plan
+            both = _csr_rows2(csr_rows, 0, i_lo, i_hi, nloc)
+            if csr_plan(both).info()["long_rows"] == 0:
+                slab.boundary = _Part(0, i_lo, both, gap=i_hi - i_lo)
     slab.xw = torch.zeros(win[1] - win[0], dtype=csr_rows.values.dtype, device=dev)
     return slab
 
@@ -329,8 +353,11 @@ class DistributedMatrix:
             s.run_part(interior, y)
             for w in works:
                 w.wait()
-            s.run_part(lower, y)
-            s.run_part(upper, y)
+            if s.boundary is not None:  # both boundary planes, one launch
+                s.run_part(s.boundary, y)
+            else:
+                s.run_part(lower, y)
+                s.run_part(upper, y)
         else:
             for w in halo_exchange(self.plan, s.xw, self.group):
                 w.wait()
@@ -339,6 +366,8 @@ class DistributedMatrix:
         return y
 
     def launches_per_spmv(self) -> int:
+        if self.overlap and self.slab.boundary is not None:
+            return 2
         return sum(1 for p in self.slab.parts if p.matrix is not None and p.hi > p.lo)
 
 
