@@ -122,7 +122,16 @@ __device__ __forceinline__ T row_vla_csr(const uint32_t* __restrict__ c, const T
   T acc[W];
 #pragma unroll
   for (int l = 0; l < W; ++l) acc[l] = T(0);
-  for (int base = 0; base < len; base += L) {
+  int base = 0;
+  if (L == W)  // power-of-two lane count: whole blocks without predicates
+    for (; base + W <= len; base += W) {
+      T p[W];
+#pragma unroll
+      for (int l = 0; l < W; ++l) p[l] = mul_rn(v[base + l], ldx(xb + c[base + l]));
+#pragma unroll
+      for (int l = 0; l < W; ++l) acc[l] = add_rn(acc[l], p[l]);
+    }
+  for (; base < len; base += L) {
     T p[W];
 #pragma unroll
     for (int l = 0; l < W; ++l) p[l] = (l < L && base + l < len) ? mul_rn(v[base + l], ldx(xb + c[base + l])) : T(0);
@@ -137,7 +146,15 @@ template <typename T, int W>
 __device__ __forceinline__ T row_vla_coo(const uint32_t* __restrict__ c, const T* __restrict__ v, int len,
                                          const T* __restrict__ xb, int L) {
   T y = T(0);
-  for (int base = 0; base < len; base += L) {
+  int base = 0;
+  if (L == W)  // power-of-two lane count: whole steps without predicates
+    for (; base + W <= len; base += W) {
+      T p[W];
+#pragma unroll
+      for (int l = 0; l < W; ++l) p[l] = mul_rn(v[base + l], ldx(xb + c[base + l]));
+      y = add_rn(y, tree_regs<T, W>(p));
+    }
+  for (; base < len; base += L) {
     T p[W];
 #pragma unroll
     for (int l = 0; l < W; ++l) p[l] = (l < L && base + l < len) ? mul_rn(v[base + l], ldx(xb + c[base + l])) : T(0);
