@@ -510,11 +510,19 @@ csr_vla_products_kernel(const uint32_t* __restrict__ irp, const uint32_t* __rest
   }
 }
 
+// Long rows' fold: one warp per row (longest rows first, see
+// csr_vla_build).  The row's products stream through kVlaFoldDepth chunks
+// held in registers, so a 50k-entry row's ~200 chunks do not each wait a
+// DRAM round trip; each chunk is staged in shared memory and logical lane
+// l < L adds its entries s+l, s+l+L, ... in order (csr_vla_warp_kernel's
+// sequence, so bit-identical), then the tree over next_pow2(L) lanes.
+constexpr int kVlaFoldDepth = 4;
 template <typename T>
 __global__ void __launch_bounds__(256)
 csr_vla_fold_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ rows, int64_t n_long,
                     const T* __restrict__ P, T* __restrict__ y, int lanes, int width) {
   constexpr int PER = kVlaLong / 32;
+  constexpr int D = kVlaFoldDepth;
   __shared__ T s_p[8][kVlaLong];
   const int lane = threadIdx.x & 31;
   T* buf = s_p[threadIdx.x >> 5];
@@ -524,36 +532,38 @@ csr_vla_fold_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict
   for (int64_t i = warp; i < n_long; i += nwarps) {
     const uint32_t r = rows[i];
     const uint32_t s = irp[r], e = irp[r + 1];
-    T cur[PER], nxt[PER];
+    const uint32_t nch = (e - s + kVlaLong - 1) / kVlaLong;
+    T ring[D][PER];
+    auto load = [&](T(&dst)[PER], uint32_t c) {
 #pragma unroll
-    for (int u = 0; u < PER; ++u) {
-      const uint32_t j = s + uint32_t(lane) + 32u * uint32_t(u);
-      cur[u] = j < e ? P[j] : T(0);
-    }
+      for (int u = 0; u < PER; ++u) {
+        const uint32_t j = s + c * kVlaLong + uint32_t(lane) + 32u * uint32_t(u);
+        dst[u] = (c < nch && j < e) ? P[j] : T(0);
+      }
+    };
+#pragma unroll
+    for (int d = 0; d < D; ++d) load(ring[d], uint32_t(d));
     T acc = T(0);
     uint32_t n = s + uint32_t(lane);  // next entry of logical lane `lane`
-    for (uint32_t c0 = s; c0 < e; c0 += kVlaLong) {
-      const uint32_t c1 = min(e, c0 + kVlaLong);
-      if (c1 < e) {
+    for (uint32_t cb = 0; cb < nch; cb += D) {
 #pragma unroll
-        for (int u = 0; u < PER; ++u) {
-          const uint32_t j = c1 + uint32_t(lane) + 32u * uint32_t(u);
-          nxt[u] = j < e ? P[j] : T(0);
+      for (int d = 0; d < D; ++d) {
+        const uint32_t c = cb + uint32_t(d);
+        if (c >= nch) break;  // warp-uniform
+        const uint32_t c0 = s + c * kVlaLong, c1 = min(e, c0 + kVlaLong);
+#pragma unroll
+        for (int u = 0; u < PER; ++u) buf[lane + 32 * u] = ring[d][u];
+        __syncwarp();
+        load(ring[d], c + D);  // refill: D chunks stay in flight
+        if (uint32_t(lane) < L) {
+          for (; n + 3 * L < c1; n += 4 * L) {  // loads ahead of the (ordered) adds
+            const T q0 = buf[n - c0], q1 = buf[n + L - c0], q2 = buf[n + 2 * L - c0], q3 = buf[n + 3 * L - c0];
+            acc = add_rn(add_rn(add_rn(add_rn(acc, q0), q1), q2), q3);
+          }
+          for (; n < c1; n += L) acc = add_rn(acc, buf[n - c0]);
         }
+        __syncwarp();
       }
-#pragma unroll
-      for (int u = 0; u < PER; ++u) buf[lane + 32 * u] = cur[u];
-      __syncwarp();
-      if (uint32_t(lane) < L) {
-        for (; n + 3 * L < c1; n += 4 * L) {  // loads ahead of the (ordered) adds
-          const T q0 = buf[n - c0], q1 = buf[n + L - c0], q2 = buf[n + 2 * L - c0], q3 = buf[n + 3 * L - c0];
-          acc = add_rn(add_rn(add_rn(add_rn(acc, q0), q1), q2), q3);
-        }
-        for (; n < c1; n += L) acc = add_rn(acc, buf[n - c0]);
-      }
-      __syncwarp();
-#pragma unroll
-      for (int u = 0; u < PER; ++u) cur[u] = nxt[u];
     }
     acc = tree_reduce_warp(acc, width);
     if (lane == 0) y[r] = acc;
@@ -1405,6 +1415,19 @@ static int csr_vla_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st)
     vla_long_rows_kernel<<<unsigned(g), 256, 0, st>>>(irp, p->nrows, p->vla_rows.as<uint32_t>(),
                                                        ctr.as<unsigned long long>() + 1);
     SPMV_LAUNCH_CHECK();
+    // longest rows first: the fold runs one warp per row, so the longest
+    // rows' sequential folds must start in the first wave (the list order
+    // from the atomics is arbitrary; results do not depend on it)
+    std::vector<uint32_t> rows(p->vla_n), h_irp(p->nrows + 1);
+    SPMV_CUDA_TRY(cudaMemcpyAsync(rows.data(), p->vla_rows.ptr, 4 * p->vla_n, cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(h_irp.data(), irp, 4 * (p->nrows + 1), cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    std::sort(rows.begin(), rows.end(), [&](uint32_t a, uint32_t b) {
+      const uint32_t la = h_irp[a + 1] - h_irp[a], lb = h_irp[b + 1] - h_irp[b];
+      return la != lb ? la > lb : a < b;
+    });
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->vla_rows.ptr, rows.data(), 4 * p->vla_n, cudaMemcpyHostToDevice, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
   }
   if (p->vla_n > 0) {
     DevBuf cnt;
