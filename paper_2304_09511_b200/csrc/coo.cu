@@ -692,6 +692,21 @@ static int coo_vla_build(spmv_coo_plan* p, cudaStream_t st) {
       return rc;
     vla_long_runs_kernel<<<unsigned(g), 256, 0, st>>>(rs, p->n_runs, p->vla_runs.as<uint32_t>(),
                                                        ctr.as<unsigned long long>() + 1);
+    SPMV_LAUNCH_CHECK();
+    {
+      // longest runs first: the fold's single-lane step sum of a 50k-entry
+      // run is the critical path; the atomics' list order is arbitrary
+      std::vector<uint32_t> runs(p->vla_n), h_rs(p->n_runs + 1);
+      SPMV_CUDA_TRY(cudaMemcpyAsync(runs.data(), p->vla_runs.ptr, 4 * p->vla_n, cudaMemcpyDeviceToHost, st));
+      SPMV_CUDA_TRY(cudaMemcpyAsync(h_rs.data(), rs, 4 * (p->n_runs + 1), cudaMemcpyDeviceToHost, st));
+      SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+      std::sort(runs.begin(), runs.end(), [&](uint32_t a, uint32_t b) {
+        const uint32_t la = h_rs[a + 1] - h_rs[a], lb = h_rs[b + 1] - h_rs[b];
+        return la != lb ? la > lb : a < b;
+      });
+      SPMV_CUDA_TRY(cudaMemcpyAsync(p->vla_runs.ptr, runs.data(), 4 * p->vla_n, cudaMemcpyHostToDevice, st));
+      SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    }
     const int64_t gi = std::min<int64_t>((p->vla_n + 255) / 256, int64_t(sm_count()) * 16);
     vla_run_chunks_kernel<<<unsigned(gi), 256, 0, st>>>(rs, p->vla_runs.as<uint32_t>(), p->vla_n, cnt.as<uint32_t>());
     SPMV_LAUNCH_CHECK();
