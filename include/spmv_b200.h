@@ -89,7 +89,7 @@ int spmv_csr_plan_groups(const spmv_csr_plan* plan, int* groups);
  * A rank's two boundary planes (its first and last halo-reading rows, one
  * CSR matrix) then run in one launch after the halo exchange while y keeps
  * the slab's row order.  Plans without rows over exact_len only
- * (SPMV_UNSUPPORTED otherwise). */
+ * (SPMV_UNSUPPORTED otherwise); always runs the tile kernel. */
 int spmv_csr_gapped(const spmv_csr_plan* plan, const uint32_t* row_pointers,
                     const uint32_t* col_indices, const void* values,
                     const void* x, int64_t col_base, int64_t x_len, void* y,

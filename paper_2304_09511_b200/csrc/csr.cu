@@ -1355,7 +1355,9 @@ int spmv_csr_gapped(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t*
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (p->nrows == 0 || p->nnz == 0) return fail(SPMV_INVALID_ARG, "gapped products need a non-empty matrix");
   if (y_split < 0 || y_split > p->nrows || y_gap < 0) return fail(SPMV_INVALID_ARG, "bad y split / gap");
-  if (p->n_long > 0 || p->ws)
+  // long rows would need the span fix-up to honour the gap; a warp-stream
+  // choice without long rows (SPMV_CSR_WS=1) falls back to the tile kernel
+  if (p->n_long > 0)
     return fail(SPMV_UNSUPPORTED, "gapped products serve plans without rows over %d entries", p->exact_len);
   if (x_len < 0 || col_base < 0) return fail(SPMV_DIMENSION_MISMATCH, "bad x window");
   cudaStream_t st = as_stream(stream);
