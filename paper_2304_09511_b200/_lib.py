@@ -73,6 +73,8 @@ SIGNATURES = {
     "spmv_coo": [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _vp],
     "spmv_coo_vla": [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _c_int, _pi64, _vp],
     "spmv_dia": [_c_int, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp],
+    "spmv_dia_gapped": [_c_int, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _c_i64,
+                        _c_i64, _vp],
     "spmv_coo_to_csr": [_c_int, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp],
     "spmv_csr_to_coo": [_c_int, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _pint, _vp],
     "spmv_coo_to_dia_analyze": [_c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _pvp, _pi64],

@@ -71,11 +71,16 @@ __device__ __forceinline__ T dia_row(const T* __restrict__ v, const int32_t* __r
 // group i % G and stage i % S, so G tiles compute while S - G load (more
 // rows in flight per byte of shared memory than one group with a
 // double buffer).
-template <typename T, int G, int S, int NT, int ND>
+//
+// GAPPED (spmv_dia_gapped): launch rows v >= split are slab rows v + gap, so
+// a rank's two boundary blocks run as one launch; split is a multiple of
+// rows_per_tile, so no tile straddles the gap.
+template <typename T, int G, int S, int NT, int ND, bool GAPPED = false>
 __global__ void __launch_bounds__(G * NT)
 dia_bulk_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offsets, int nd, const T* __restrict__ x,
                 T* __restrict__ y, int64_t nrows, int64_t avail_rows, int64_t ncols, int64_t row_base,
-                int64_t col_base, int rows_per_tile, int64_t ntiles, uint32_t stage_bytes) {
+                int64_t col_base, int rows_per_tile, int64_t ntiles, uint32_t stage_bytes, int64_t split = 0,
+                int64_t gap = 0) {
   static_assert(S > G && S <= 8, "stages");
   extern __shared__ __align__(128) unsigned char smem[];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem);                 // [0, 64)
@@ -101,17 +106,19 @@ dia_bulk_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offsets,
   const int64_t my_tiles = first < ntiles ? (ntiles - 1 - first) / stride + 1 : 0;
   const size_t row_bytes = size_t(nd) * sizeof(T);
 
+  // launch row -> slab row (GAPPED: rows past split jump the gap)
+  auto slab_row = [&](int64_t lr) { return GAPPED && lr >= split ? lr + gap : lr; };
   auto issue = [&](int64_t i) {
     const int64_t t = first + i * stride;
     const int64_t lr0 = t * rows_per_tile;
-    int64_t rows = avail_rows - lr0;
+    int64_t rows = (GAPPED && lr0 < split ? split : avail_rows) - lr0;
     if (rows > rows_per_tile) rows = rows_per_tile;
     const uint32_t bytes = uint32_t(rows * row_bytes);
     const int s = int(i % S);
     if (G > 1) tickets[s] = int(i);
     mbar_arrive_expect_tx(&bars[s], bytes);
-    bulk_g2s(bufs + size_t(s) * stage_bytes, reinterpret_cast<const unsigned char*>(vals) + lr0 * row_bytes, bytes,
-             &bars[s]);
+    bulk_g2s(bufs + size_t(s) * stage_bytes,
+             reinterpret_cast<const unsigned char*>(vals) + slab_row(lr0) * int64_t(row_bytes), bytes, &bars[s]);
   };
   auto group_sync = [&]() {
     if (G == 1)
@@ -132,11 +139,12 @@ dia_bulk_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offsets,
     mbar_wait(&bars[s], uint32_t((i / S) & 1));
     const int64_t t = first + i * stride;
     const int64_t lr0 = t * rows_per_tile;
+    const int64_t sr0 = slab_row(lr0);
     const T* tile = reinterpret_cast<const T*>(bufs + size_t(s) * stage_bytes);
-    int64_t rows = nrows - lr0;
+    int64_t rows = (GAPPED && lr0 < split ? split : nrows) - lr0;
     if (rows > rows_per_tile) rows = rows_per_tile;
     for (int lr = tid; lr < rows; lr += NT)
-      y[lr0 + lr] = dia_row<T, ND>(tile + size_t(lr) * nd, s_off, nd, row_base + lr0 + lr, ncols, xb);
+      y[sr0 + lr] = dia_row<T, ND>(tile + size_t(lr) * nd, s_off, nd, row_base + sr0 + lr, ncols, xb);
     group_sync();  // every thread of the group is done with stage s
     if (tid == 0 && i + S < my_tiles) {
       fence_proxy_async();
@@ -166,8 +174,10 @@ dia_direct_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offset
 
 template <typename T>
 static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_rows, const int32_t* offsets,
-                      const T* vals, const T* x, int64_t row_base, int64_t col_base, T* y, cudaStream_t st) {
+                      const T* vals, const T* x, int64_t row_base, int64_t col_base, T* y, cudaStream_t st,
+                      int64_t split = -1, int64_t gap = 0) {
   if (nrows == 0) return SPMV_OK;
+  const bool gapped = split >= 0;
   const int sms = sm_count();
   const size_t row_bytes = size_t(nd) * sizeof(T);
   // Tile size: one row per thread (R = 256) when a stage fits ~56 KB, else
@@ -192,6 +202,9 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) % 16 == 0) && ((R * row_bytes) % 16 == 0) &&
                        ((avail_rows * row_bytes) % 16 == 0);
   const bool use_bulk = nd > 0 && nd <= kMaxSmemOffsets && R >= 8 && aligned;
+  if (gapped && (!use_bulk || split % R != 0 || (gap * int64_t(row_bytes)) % 16 != 0))
+    return fail(SPMV_UNSUPPORTED, "gapped DIA launch needs the bulk kernel and a split on a %lld-row tile boundary",
+                (long long)R);
   if (!use_bulk) {
     int64_t grid = (nrows + kDiaThreads - 1) / kDiaThreads;
     if (grid > int64_t(sms) * 32) grid = int64_t(sms) * 32;
@@ -234,12 +247,19 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
     int64_t grid = int64_t(sms) * per_sm;
     if (grid > ntiles) grid = ntiles;
     kernel<<<unsigned(grid), threads, smem, st>>>(vals, offsets, int(nd), x, y, nrows, avail_rows, ncols, row_base,
-                                                 col_base, int(R), ntiles, stage_bytes);
+                                                 col_base, int(R), ntiles, stage_bytes, split, gap);
     return SPMV_OK;
   };
   auto by_nd = [&](auto cfg) -> int {
     using C = decltype(cfg);
     constexpr int G = C::G, S = C::S, NT = C::NT;
+    if (gapped) {  // the stencil and the banded matrix; other widths run generic
+      switch (nd) {
+        case 27: return launch(dia_bulk_kernel<T, G, S, NT, 27, true>, G * NT, S);
+        case 11: return launch(dia_bulk_kernel<T, G, S, NT, 11, true>, G * NT, S);
+        default: return launch(dia_bulk_kernel<T, G, S, NT, 0, true>, G * NT, S);
+      }
+    }
     switch (nd) {
       case 27: return launch(dia_bulk_kernel<T, G, S, NT, 27>, G * NT, S);
       case 11: return launch(dia_bulk_kernel<T, G, S, NT, 11>, G * NT, S);
@@ -265,6 +285,25 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
 }  // namespace spmv
 
 using namespace spmv;
+
+extern "C" int spmv_dia_gapped(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags, int64_t avail_rows,
+                               const int32_t* offsets, const void* values, const void* x, int64_t row_base,
+                               int64_t col_base, int64_t x_len, void* y, int64_t y_split, int64_t y_gap,
+                               void* stream) {
+  if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
+  if (nrows <= 0 || ncols < 0 || ndiags <= 0 || avail_rows < nrows || row_base < 0 || col_base < 0 || x_len < 0 ||
+      y_split < 0 || y_split > nrows || y_gap < 0)
+    return fail(SPMV_INVALID_ARG, "bad gapped DIA sizes");
+  if (!offsets || !values || !x || !y) return fail(SPMV_INVALID_ARG, "NULL pointer");
+  cudaStream_t st = as_stream(stream);
+  if (dtype == SPMV_F64)
+    return dia_launch<double>(nrows, ncols, ndiags, avail_rows, offsets, static_cast<const double*>(values),
+                              static_cast<const double*>(x), row_base, col_base, static_cast<double*>(y), st, y_split,
+                              y_gap);
+  return dia_launch<float>(nrows, ncols, ndiags, avail_rows, offsets, static_cast<const float*>(values),
+                           static_cast<const float*>(x), row_base, col_base, static_cast<float*>(y), st, y_split,
+                           y_gap);
+}
 
 extern "C" int spmv_dia(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags, int64_t avail_rows,
                         const int32_t* offsets, const void* values, const void* x, int64_t row_base,

@@ -200,9 +200,11 @@ class LocalSlab:
     parts: list = field(default_factory=list)   # [lower, interior, upper]
     nnz: int = 0
     xw: torch.Tensor = None
-    # CSR: lower + upper rows as one matrix, one launch after the exchange
-    # (y gap over the interior rows); None when not applicable
+    # lower + upper rows in one launch after the exchange (CSR: one matrix
+    # of both blocks; DIA: one gapped launch), with the interior part that
+    # goes with it; None when not applicable
     boundary: _Part = None
+    interior_g: _Part = None
 
     @property
     def nloc(self) -> int:
@@ -222,7 +224,13 @@ class LocalSlab:
         yv = y[part.lo:part.hi]
         st = _stream(y.device)
         xw = self.xw
-        if isinstance(m, CsrMatrix) and part.gap:
+        if isinstance(m, tuple) and part.gap:
+            dia, _, pr = m
+            nv = part.hi + (self.nloc - part.hi - part.gap)  # launch rows: lower block + upper block
+            _lib.call("spmv_dia_gapped", _lib.dtype_code(dia.values.dtype), nv, self.ncols, dia.ndiags, pr - part.gap,
+                      dia.offsets.data_ptr(), dia.values.data_ptr(), xw.data_ptr(), 0, self.window[0], xw.shape[0],
+                      y.data_ptr(), part.hi, part.gap, st)
+        elif isinstance(m, CsrMatrix) and part.gap:
             p = csr_plan(m)
             _lib.call("spmv_csr_gapped", p.handle, m.row_pointers.data_ptr(), m.col_indices.data_ptr(),
                       m.values.data_ptr(), xw.data_ptr(), self.window[0], xw.shape[0], y.data_ptr(), part.hi,
@@ -293,6 +301,12 @@ def build_local_slab(csr_rows: CsrMatrix, r0: int, r1: int, fmt: str = "csr") ->
         pr = dia.padded_rows
         parts = [_Part(a, b, (dia, a, pr - a)) for a, b in ((0, i_lo), (i_lo, i_hi), (i_hi, nloc))]
         slab = LocalSlab("dia", (r0, r1), win, ncols, parts, csr_rows.nnz)
+        # both boundary blocks in one gapped launch: the lower block is
+        # extended to a 256-row tile boundary (those rows leave the interior)
+        split = round_up(i_lo, 256)
+        if 0 < i_lo and i_hi < nloc and split < i_hi and dev.type == "cuda":
+            slab.boundary = _Part(0, split, (dia, 0, pr), gap=i_hi - split)
+            slab.interior_g = _Part(split, i_hi, (dia, split, pr - split))
     else:
         cb = _col_bounds(csr_rows)
         win = (r0, r1) if cb is None else (min(r0, cb[0]), max(r1, cb[1] + 1))
@@ -314,6 +328,7 @@ def build_local_slab(csr_rows: CsrMatrix, r0: int, r1: int, fmt: str = "csr") ->
             both = _csr_rows2(csr_rows, 0, i_lo, i_hi, nloc)
             if csr_plan(both).info()["long_rows"] == 0:
                 slab.boundary = _Part(0, i_lo, both, gap=i_hi - i_lo)
+                slab.interior_g = pieces[1]
     slab.xw = torch.zeros(win[1] - win[0], dtype=csr_rows.values.dtype, device=dev)
     return slab
 
@@ -350,10 +365,10 @@ class DistributedMatrix:
         lower, interior, upper = s.parts
         if self.overlap:
             works = halo_exchange(self.plan, s.xw, self.group)
-            s.run_part(interior, y)
+            s.run_part(interior if s.boundary is None else s.interior_g, y)
             for w in works:
                 w.wait()
-            if s.boundary is not None:  # both boundary planes, one launch
+            if s.boundary is not None:  # both boundary blocks, one launch
                 s.run_part(s.boundary, y)
             else:
                 s.run_part(lower, y)

@@ -124,16 +124,16 @@ def test_emulated_ranks_bit_identical(lib_built, fmt, world):
         ys.append(y)
     got = torch.cat(ys).cpu().numpy()
     assert got.tobytes() == ref.tobytes()
-    # CSR: interior + both boundary planes in one gapped launch, as
+    # CSR / DIA: interior + both boundary blocks in one gapped launch, as
     # DistributedMatrix.spmv runs them
     gapped = [s for s in slabs if s.boundary is not None]
-    if fmt == "csr" and world > 2:
+    if fmt in ("csr", "dia") and world > 2:
         assert len(gapped) == world - 2  # every rank with two neighbours
     ys = []
     for s in slabs:
         y = torch.full((s.nloc,), float("nan"), dtype=torch.float64, device="cuda")
         if s.boundary is not None:
-            s.run_part(s.parts[1], y)
+            s.run_part(s.interior_g, y)
             s.run_part(s.boundary, y)
         else:
             for p in s.parts:

@@ -4,9 +4,9 @@ at a time on one GPU (this pool has one B200 per call).
 For an N-way z-slab partition (RowPartition.contiguous, hpcg.py:109 with
 procs (1,1,N)), builds rank r's slab exactly as DistributedMatrix does
 (window, interior / boundary parts) and times its launches back to back
-with CUDA events, in DistributedMatrix.spmv's order (CSR: interior, then
-both boundary planes in one gapped launch; DIA / COO: lower, interior,
-upper).  The halo exchange is not run: on the real
+with CUDA events, in DistributedMatrix.spmv's order (CSR and DIA:
+interior, then both boundary blocks in one gapped launch; COO: lower,
+interior, upper).  The halo exchange is not run: on the real
 path it overlaps the interior rows (512 KiB per neighbour per step over
 NVLink), so the per-rank time is interior + boundary launches.  The
 projection max over ranks, divided into the one-GPU time, is the scaling
@@ -59,7 +59,7 @@ def main():
         y = torch.empty(slab.nloc, dtype=torch.float64, device="cuda")
 
         lower, interior, upper = slab.parts
-        seq = [interior, slab.boundary] if slab.boundary is not None else [lower, interior, upper]
+        seq = [slab.interior_g, slab.boundary] if slab.boundary is not None else [lower, interior, upper]
 
         def step():  # as DistributedMatrix.spmv orders the launches
             for p in seq:
