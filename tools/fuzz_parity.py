@@ -53,6 +53,7 @@ def main():
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
     rng = np.random.default_rng(seed)
     fails = 0
+    refused = 0
     for case in range(cases):
         nrows = int(rng.integers(1, 6000))
         ncols = int(rng.integers(1, 40000))
@@ -98,7 +99,60 @@ def main():
             fails += 1
             print(f"case {case}: nrows={nrows} ncols={ncols} nnz={cols.shape[0]} {np.dtype(dtype).name} "
                   f"lanes={lanes} csr={ok} coo={ok_c} csr_vla={ok_v} coo_vla={ok_cv} max_len={lens.max()}")
-    print(f"fuzz: {cases} cases, {fails} failures (seed {seed})")
+    # DIA: random diagonal sets (conversions on the device, product and
+    # round trip bit-exact against the oracle)
+    for case in range(cases // 2):
+        n = int(rng.integers(8, 5000))
+        m = int(rng.integers(8, 5000))
+        nd = int(rng.integers(1, 12))
+        if rng.random() < 0.7:  # banded (the fill policy admits it)
+            offs = np.unique(rng.integers(-min(n - 1, 64), min(m, 65), nd))
+        else:
+            offs = np.unique(rng.integers(-(n - 1), m, nd))
+        rr, cc = [], []
+        for o in offs:
+            r = np.arange(max(0, -o), min(n, m - o))
+            keep = r[rng.random(r.shape[0]) < 0.8]
+            rr.append(keep)
+            cc.append(keep + o)
+        rows = np.concatenate(rr).astype(np.int64)
+        cols_ = np.concatenate(cc).astype(np.int64)
+        order = np.lexsort((cols_, rows))
+        rows, cols_ = rows[order].astype(np.uint32), cols_[order].astype(np.uint32)
+        dtype = np.float64 if rng.random() < 0.7 else np.float32
+        vals = rng.standard_normal(rows.shape[0]).astype(dtype)
+        x = rng.uniform(-1, 1, m).astype(dtype)
+        try:
+            coo = sp.CooMatrix.from_arrays(n, m, rows, cols_, vals, True)
+            if O.dia_fill_check(n, m, rows.shape[0], offs.shape[0]) is not None:
+                # the reference refuses this fill (convert.py:128-139): so must we
+                try:
+                    sp.coo_to_dia(coo)
+                    print(f"dia case {case}: fill policy not enforced")
+                    fails += 1
+                except sp.FillRatioExceeded:
+                    refused += 1
+                continue
+            dia = sp.coo_to_dia(coo)
+            h = dia.to_host()
+            ref_off, ref_vals = O.coo_to_dia(n, m, rows, cols_, vals)
+            ok_conv = np.array_equal(h["offsets"], ref_off) and bit_equal(h["values"], ref_vals)
+            y = sp.spmv_dia_plain(dia, x)
+            ok_y = bit_equal(y, O.dia_plain(n, m, ref_off, ref_vals, x))
+            back = sp.dia_to_coo(dia).to_host()
+            b_r, b_c, b_v = O.dia_to_coo(n, m, ref_off, ref_vals)
+            ok_back = np.array_equal(back["row_indices"], b_r) and np.array_equal(back["col_indices"], b_c) and \
+                bit_equal(back["values"], b_v)
+        except Exception as e:  # noqa: BLE001
+            print(f"dia case {case}: exception {type(e).__name__}: {e}")
+            fails += 1
+            continue
+        if not (ok_conv and ok_y and ok_back):
+            fails += 1
+            print(f"dia case {case}: n={n} m={m} nd={offs.shape[0]} {np.dtype(dtype).name} conv={ok_conv} "
+                  f"y={ok_y} back={ok_back}")
+    print(f"fuzz: {cases} CSR/COO cases + {cases // 2} DIA cases ({refused} refused by the fill policy, as the "
+          f"reference refuses them), {fails} failures (seed {seed})")
     sys.exit(1 if fails else 0)
 
 
