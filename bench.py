@@ -46,6 +46,11 @@ CONFIGS = {
 }
 
 
+# Random 8-byte gathers per second a B200 serves with a coalesced index and
+# value stream beside them (tools/gather_ceiling.cu, profiles/r1_gather_ceiling.txt).
+GATHER_CEILING_GS = 248.0
+
+
 def peaks() -> dict:
     p = ROOT / "MEASURED_PEAKS.json"
     if p.exists():
@@ -368,6 +373,14 @@ def run_ours(args, torch, dist, rank, world, local_rank):
         results[fmt] = {"gflops": round(2.0 * m.nnz / t / 1e9, 2), "ms_per_spmv": round(t * 1e3, 4),
                         "gbs": round(b / t / 1e9, 1), "bytes_per_spmv": b, "launches": launches_per_spmv(sp, m),
                         "plan": plan_of(sp, m), "roofline_frac": round(b / t / 1e9 / pk["hbm_gbs"], 4), "nnz": m.nnz}
+        if args.config == "c3":
+            # uniform random columns: every entry is one random 32-byte x
+            # sector; the bound is the measured random-gather rate, not HBM
+            results[fmt]["gather_roofline"] = {
+                "achieved_ggathers_s": round(m.nnz / t / 1e9, 1), "ceiling_ggathers_s": GATHER_CEILING_GS,
+                "frac": round(m.nnz / t / 1e9 / GATHER_CEILING_GS, 3),
+                "source": "tools/gather_ceiling.cu, profiles/r1_gather_ceiling.txt (index + value stream + one "
+                          "random gather per entry, best of LSU / TMA gather4 / both)"}
     vla_results = {}
     if not args.no_extras:
         # the vla kernels (kernels.py:104-210) at the reference's default lane count
