@@ -39,17 +39,9 @@ namespace spmv {
 #ifndef SPMV_WS_MINB
 #define SPMV_WS_MINB 4
 #endif
-#ifndef SPMV_WS_LDG
-#define SPMV_WS_LDG 0
-#endif
-// matrix stream loads (column indices, values)
-template <typename T> __device__ __forceinline__ T ws_ld(const T* p) {
-#if SPMV_WS_LDG
-  return __ldg(p);
-#else
-  return ld_stream(p);
-#endif
-}
+// matrix stream loads (column indices, values): read once, no L1 allocation
+// (`__ldg` streams were 7% slower on C3, profiles/r1_notes.md)
+template <typename T> __device__ __forceinline__ T ws_ld(const T* p) { return ld_stream(p); }
 constexpr int kWsDepth = SPMV_WS_DEPTH;        // gathers in flight per lane
 constexpr int kWsChunk = 32 * kWsDepth;        // entries per warp step
 constexpr int kWsWarps = 8;                    // warps per CTA
@@ -126,11 +118,6 @@ __device__ __forceinline__ void csr_ws_range(const WsParams<T>& P, const int64_t
 #pragma unroll
       for (int k = 0; k < kWsDepth; ++k) p[k] = mul_rn(val[k], p[k]);
     }
-#ifdef SPMV_WS_NOROWS  // experiment: gathers and products only (results wrong)
-    for (int k = 0; k < kWsDepth; ++k) carry = add_rn(carry, double(p[k]));
-    if (end == 0) P.head[w] = carry;
-    continue;
-#endif
     const uint32_t end0 = __shfl_sync(0xffffffffu, end, 0);
     if (end0 >= c1 && c1 - c0 == uint32_t(kWsChunk)) {
       // the whole chunk lies in row r (so the row has over kWsChunk entries):
