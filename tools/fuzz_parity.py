@@ -7,7 +7,7 @@ tests/test_gpu_kernels.py: rows <= 32 bit-exact, everything within 1e-12
 (f64) / 1e-5 of the f64-evaluated product (f32); vla bit-exact.  Prints
 one line per failure and a summary; exit code 1 on any failure.
 
-  python tools/fuzz_parity.py [cases=200] [seed=0]
+  python tools/fuzz_parity.py [cases=200] [seed=0] [scale=1]
 """
 import os
 import sys
@@ -51,12 +51,13 @@ def random_lens(rng, nrows, ncols):
 def main():
     cases = int(sys.argv[1]) if len(sys.argv) > 1 else 200
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 0
+    scale = int(sys.argv[3]) if len(sys.argv) > 3 else 1  # > 1: bigger matrices (many warp-stream ranges)
     rng = np.random.default_rng(seed)
     fails = 0
     refused = 0
     for case in range(cases):
-        nrows = int(rng.integers(1, 6000))
-        ncols = int(rng.integers(1, 40000))
+        nrows = int(rng.integers(1, 6000 * scale))
+        ncols = int(rng.integers(1, 40000 * scale))
         lens = random_lens(rng, nrows, ncols)
         irp = np.zeros(nrows + 1, dtype=np.int64)
         np.cumsum(lens, out=irp[1:])
