@@ -73,6 +73,20 @@ inline int64_t bulk_tiles(int64_t nnz, int64_t ntiles, int64_t tile) {
 #ifndef SPMV_ROW_BATCH
 #define SPMV_ROW_BATCH 8
 #endif
+#ifndef SPMV_ROW_TAIL_SWITCH
+#define SPMV_ROW_TAIL_SWITCH 1
+#endif
+template <typename T, int N>
+__device__ __forceinline__ T row_tail(const uint32_t* __restrict__ c, const T* __restrict__ v,
+                                      const T* __restrict__ xb, T acc) {
+  T p[N];
+#pragma unroll
+  for (int j = 0; j < N; ++j) p[j] = mul_rn(v[j], ldx(xb + c[j]));
+#pragma unroll
+  for (int j = 0; j < N; ++j) acc = add_rn(acc, p[j]);
+  return acc;
+}
+
 template <typename T>
 __device__ __forceinline__ T row_dot(const uint32_t* __restrict__ c, const T* __restrict__ v, int len,
                                      const T* __restrict__ xb, T acc) {
@@ -93,8 +107,23 @@ __device__ __forceinline__ T row_dot(const uint32_t* __restrict__ c, const T* __
 #pragma unroll
       for (int j = 0; j < 8; ++j) acc = add_rn(acc, p[j]);
     }
+#if SPMV_ROW_TAIL_SWITCH
+  // the last len - i < 8 entries: an exact-count batch (no predicates),
+  // their gathers in flight together rather than one round trip each
+  switch (len - i) {
+    case 7: return row_tail<T, 7>(c + i, v + i, xb, acc);
+    case 6: return row_tail<T, 6>(c + i, v + i, xb, acc);
+    case 5: return row_tail<T, 5>(c + i, v + i, xb, acc);
+    case 4: return row_tail<T, 4>(c + i, v + i, xb, acc);
+    case 3: return row_tail<T, 3>(c + i, v + i, xb, acc);
+    case 2: return row_tail<T, 2>(c + i, v + i, xb, acc);
+    case 1: return add_rn(acc, mul_rn(v[i], ldx(xb + c[i])));
+    default: return acc;
+  }
+#else
   for (; i < len; ++i) acc = add_rn(acc, mul_rn(v[i], ldx(xb + c[i])));
   return acc;
+#endif
 }
 
 // vla rows from staged entries, one thread per row (rows of <= 32 entries).
