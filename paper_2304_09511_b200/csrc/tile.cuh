@@ -145,6 +145,33 @@ __device__ __forceinline__ T tree_regs(T (&v)[W]) {
   return v[0];
 }
 
+// lanes 0..N-1 of a partial last block (exact count: no predicates)
+template <typename T, int W, int N>
+__device__ __forceinline__ void vla_block_part(T (&acc)[W], const uint32_t* __restrict__ c,
+                                               const T* __restrict__ v, const T* __restrict__ xb) {
+  if constexpr (N > 0 && N < W) {
+    T p[N];
+#pragma unroll
+    for (int l = 0; l < N; ++l) p[l] = mul_rn(v[l], ldx(xb + c[l]));
+#pragma unroll
+    for (int l = 0; l < N; ++l) acc[l] = add_rn(acc[l], p[l]);
+  }
+}
+
+// tree of a partial last step: lanes 0..N-1 products, the others 0
+template <typename T, int W, int N>
+__device__ __forceinline__ T vla_step_part(const uint32_t* __restrict__ c, const T* __restrict__ v,
+                                           const T* __restrict__ xb) {
+  T p[W];
+#pragma unroll
+  for (int l = 0; l < W; ++l) p[l] = T(0);
+  if constexpr (N > 0 && N < W) {
+#pragma unroll
+    for (int l = 0; l < N; ++l) p[l] = mul_rn(v[l], ldx(xb + c[l]));
+  }
+  return tree_regs<T, W>(p);
+}
+
 template <typename T, int W>
 __device__ __forceinline__ T row_vla_csr(const uint32_t* __restrict__ c, const T* __restrict__ v, int len,
                                          const T* __restrict__ xb, int L) {
@@ -152,7 +179,7 @@ __device__ __forceinline__ T row_vla_csr(const uint32_t* __restrict__ c, const T
 #pragma unroll
   for (int l = 0; l < W; ++l) acc[l] = T(0);
   int base = 0;
-  if (L == W)  // power-of-two lane count: whole blocks without predicates
+  if (L == W) {  // power-of-two lane count: whole blocks without predicates
     for (; base + W <= len; base += W) {
       T p[W];
 #pragma unroll
@@ -160,6 +187,21 @@ __device__ __forceinline__ T row_vla_csr(const uint32_t* __restrict__ c, const T
 #pragma unroll
       for (int l = 0; l < W; ++l) acc[l] = add_rn(acc[l], p[l]);
     }
+#if SPMV_ROW_TAIL_SWITCH
+    // the partial last block: its lanes as one exact-count batch
+    switch (len - base) {
+      case 1: vla_block_part<T, W, 1>(acc, c + base, v + base, xb); break;
+      case 2: vla_block_part<T, W, 2>(acc, c + base, v + base, xb); break;
+      case 3: vla_block_part<T, W, 3>(acc, c + base, v + base, xb); break;
+      case 4: vla_block_part<T, W, 4>(acc, c + base, v + base, xb); break;
+      case 5: vla_block_part<T, W, 5>(acc, c + base, v + base, xb); break;
+      case 6: vla_block_part<T, W, 6>(acc, c + base, v + base, xb); break;
+      case 7: vla_block_part<T, W, 7>(acc, c + base, v + base, xb); break;
+      default: break;
+    }
+    return tree_regs<T, W>(acc);
+#endif
+  }
   for (; base < len; base += L) {
     T p[W];
 #pragma unroll
@@ -176,13 +218,27 @@ __device__ __forceinline__ T row_vla_coo(const uint32_t* __restrict__ c, const T
                                          const T* __restrict__ xb, int L) {
   T y = T(0);
   int base = 0;
-  if (L == W)  // power-of-two lane count: whole steps without predicates
+  if (L == W) {  // power-of-two lane count: whole steps without predicates
     for (; base + W <= len; base += W) {
       T p[W];
 #pragma unroll
       for (int l = 0; l < W; ++l) p[l] = mul_rn(v[base + l], ldx(xb + c[base + l]));
       y = add_rn(y, tree_regs<T, W>(p));
     }
+#if SPMV_ROW_TAIL_SWITCH
+    // the partial last step: its lanes as one exact-count batch, the rest 0
+    switch (len - base) {
+      case 1: return add_rn(y, vla_step_part<T, W, 1>(c + base, v + base, xb));
+      case 2: return add_rn(y, vla_step_part<T, W, 2>(c + base, v + base, xb));
+      case 3: return add_rn(y, vla_step_part<T, W, 3>(c + base, v + base, xb));
+      case 4: return add_rn(y, vla_step_part<T, W, 4>(c + base, v + base, xb));
+      case 5: return add_rn(y, vla_step_part<T, W, 5>(c + base, v + base, xb));
+      case 6: return add_rn(y, vla_step_part<T, W, 6>(c + base, v + base, xb));
+      case 7: return add_rn(y, vla_step_part<T, W, 7>(c + base, v + base, xb));
+      default: return y;
+    }
+#endif
+  }
   for (; base < len; base += L) {
     T p[W];
 #pragma unroll
