@@ -602,7 +602,7 @@ coo_vla_short_kernel(const uint32_t* __restrict__ run_start, const uint32_t* __r
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n_runs; i += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t a = __ldg(run_start + i), b = __ldg(run_start + i + 1);
     if (b - a > uint32_t(kExactLen)) continue;
-    y[__ldg(run_row + i)] = row_vla_coo<T, W>(aj + a, av + a, int(b - a), xb, lanes);
+    y[__ldg(run_row + i)] = row_vla_coo<T, W, true>(aj + a, av + a, int(b - a), xb, lanes);
   }
 }
 

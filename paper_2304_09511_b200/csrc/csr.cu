@@ -645,7 +645,7 @@ csr_vla_short_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restric
   for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t s = __ldg(irp + r), e = __ldg(irp + r + 1);
     if (e - s > uint32_t(kExactLen)) continue;
-    y[r] = e == s ? T(0) : row_vla_csr<T, W>(aj + s, av + s, int(e - s), xb, lanes);
+    y[r] = e == s ? T(0) : row_vla_csr<T, W, true>(aj + s, av + s, int(e - s), xb, lanes);
   }
 }
 

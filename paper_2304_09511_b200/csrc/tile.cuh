@@ -76,6 +76,12 @@ inline int64_t bulk_tiles(int64_t nnz, int64_t ntiles, int64_t tile) {
 #ifndef SPMV_ROW_TAIL_SWITCH
 #define SPMV_ROW_TAIL_SWITCH 1
 #endif
+// True when every active lane of the warp has the same tail count.
+__device__ __forceinline__ bool tail_uniform(int r) {
+  const unsigned am = __activemask();
+  return __all_sync(am, r == __shfl_sync(am, r, __ffs(am) - 1));
+}
+
 template <typename T, int N>
 __device__ __forceinline__ T row_tail(const uint32_t* __restrict__ c, const T* __restrict__ v,
                                       const T* __restrict__ xb, T acc) {
@@ -172,7 +178,10 @@ __device__ __forceinline__ T vla_step_part(const uint32_t* __restrict__ c, const
   return tree_regs<T, W>(p);
 }
 
-template <typename T, int W>
+// MIXED: the warp's rows differ in length (the long-row plans' short-row
+// kernels): the tail switch runs only when the counts agree, a switch over
+// mixed counts would serialise its cases.
+template <typename T, int W, bool MIXED = false>
 __device__ __forceinline__ T row_vla_csr(const uint32_t* __restrict__ c, const T* __restrict__ v, int len,
                                          const T* __restrict__ xb, int L) {
   T acc[W];
@@ -189,6 +198,7 @@ __device__ __forceinline__ T row_vla_csr(const uint32_t* __restrict__ c, const T
     }
 #if SPMV_ROW_TAIL_SWITCH
     // the partial last block: its lanes as one exact-count batch
+    if (!MIXED || tail_uniform(len - base)) {
     switch (len - base) {
       case 1: vla_block_part<T, W, 1>(acc, c + base, v + base, xb); break;
       case 2: vla_block_part<T, W, 2>(acc, c + base, v + base, xb); break;
@@ -200,6 +210,7 @@ __device__ __forceinline__ T row_vla_csr(const uint32_t* __restrict__ c, const T
       default: break;
     }
     return tree_regs<T, W>(acc);
+    }
 #endif
   }
   for (; base < len; base += L) {
@@ -213,7 +224,7 @@ __device__ __forceinline__ T row_vla_csr(const uint32_t* __restrict__ c, const T
   return tree_regs<T, W>(acc);
 }
 
-template <typename T, int W>
+template <typename T, int W, bool MIXED = false>
 __device__ __forceinline__ T row_vla_coo(const uint32_t* __restrict__ c, const T* __restrict__ v, int len,
                                          const T* __restrict__ xb, int L) {
   T y = T(0);
@@ -227,7 +238,7 @@ __device__ __forceinline__ T row_vla_coo(const uint32_t* __restrict__ c, const T
     }
 #if SPMV_ROW_TAIL_SWITCH
     // the partial last step: its lanes as one exact-count batch, the rest 0
-    switch (len - base) {
+    if (!MIXED || tail_uniform(len - base)) switch (len - base) {
       case 1: return add_rn(y, vla_step_part<T, W, 1>(c + base, v + base, xb));
       case 2: return add_rn(y, vla_step_part<T, W, 2>(c + base, v + base, xb));
       case 3: return add_rn(y, vla_step_part<T, W, 3>(c + base, v + base, xb));
