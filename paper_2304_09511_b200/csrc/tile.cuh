@@ -93,9 +93,32 @@ __device__ __forceinline__ T row_tail(const uint32_t* __restrict__ c, const T* _
   return acc;
 }
 
-template <typename T>
+// Exact-count tail of r < N + 1 entries: compare chain over N .. 1.
+template <typename T, int N>
+__device__ __forceinline__ T row_tail_dispatch(int r, const uint32_t* __restrict__ c, const T* __restrict__ v,
+                                               const T* __restrict__ xb, T acc) {
+  if constexpr (N == 0) {
+    return acc;
+  } else {
+    if (r == N) return row_tail<T, N>(c, v, xb, acc);
+    return row_tail_dispatch<T, N - 1>(r, c, v, xb, acc);
+  }
+}
+
+// BIG: short-row plans (the 1664-entry tile configuration, rows averaging
+// under 16 entries): one 16-wide batch plus an exact-count tail of up to
+// 15, so rows of up to 16 entries (the banded matrix's 11) take one gather
+// round trip instead of two.
+template <typename T, bool BIG = false>
 __device__ __forceinline__ T row_dot(const uint32_t* __restrict__ c, const T* __restrict__ v, int len,
                                      const T* __restrict__ xb, T acc) {
+#if SPMV_ROW_TAIL_SWITCH
+  if constexpr (BIG) {
+    int i = 0;
+    for (; i + 16 <= len; i += 16) acc = row_tail<T, 16>(c + i, v + i, xb, acc);
+    return row_tail_dispatch<T, 15>(len - i, c + i, v + i, xb, acc);
+  }
+#endif
   constexpr int B = SPMV_ROW_BATCH;
   int i = 0;
   for (; i + B <= len; i += B) {
