@@ -197,7 +197,7 @@ __device__ void coo_process_tile(const CooParams<T>& P, int64_t t, const uint32_
       else
         // +0.0 seed: np.add.at accumulates into a zeroed y
         P.y[r] = products ? row_sum(vals + k0, k1 + after - k0, T(0))
-                          : row_dot(cols + k0, vals + k0, k1 + after - k0, xb, T(0));
+                          : row_dot<T, true>(cols + k0, vals + k0, k1 + after - k0, xb, T(0));
     }
   }
   grp.sync();

@@ -150,7 +150,7 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
         else
           // -0.0 seed: the sum starts from the first product, like cumsum
           P.y[yrow(P, r)] = products ? row_sum(vals + (s - E0), int(len), T(-0.0))
-                            : row_dot<T, TILE == 1664>(cols + (s - E0), vals + (s - E0), int(len), xb, T(-0.0));
+                            : row_dot<T, true>(cols + (s - E0), vals + (s - E0), int(len), xb, T(-0.0));
       }
     } else {
       const int64_t lo = max(int64_t(s), E0), hi = min(int64_t(e), E1);

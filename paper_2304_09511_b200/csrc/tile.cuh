@@ -76,6 +76,7 @@ inline int64_t bulk_tiles(int64_t nnz, int64_t ntiles, int64_t tile) {
 #ifndef SPMV_ROW_TAIL_SWITCH
 #define SPMV_ROW_TAIL_SWITCH 1
 #endif
+
 // True when every active lane of the warp has the same tail count.
 __device__ __forceinline__ bool tail_uniform(int r) {
   const unsigned am = __activemask();
@@ -105,10 +106,10 @@ __device__ __forceinline__ T row_tail_dispatch(int r, const uint32_t* __restrict
   }
 }
 
-// BIG: short-row plans (the 1664-entry tile configuration, rows averaging
-// under 16 entries): one 16-wide batch plus an exact-count tail of up to
-// 15, so rows of up to 16 entries (the banded matrix's 11) take one gather
-// round trip instead of two.
+// BIG (the tile kernels): 16-wide batches plus an exact-count tail of up
+// to 15, so a row of up to 16 entries (the banded matrix's 11) takes one
+// gather round trip and the stencil's 27 take two (8-wide batches with a
+// serial tail took four and six).
 template <typename T, bool BIG = false>
 __device__ __forceinline__ T row_dot(const uint32_t* __restrict__ c, const T* __restrict__ v, int len,
                                      const T* __restrict__ xb, T acc) {
