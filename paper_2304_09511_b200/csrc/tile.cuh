@@ -213,6 +213,16 @@ __device__ __forceinline__ T row_vla_csr(const uint32_t* __restrict__ c, const T
   for (int l = 0; l < W; ++l) acc[l] = T(0);
   int base = 0;
   if (L == W) {  // power-of-two lane count: whole blocks without predicates
+    if constexpr (W <= 8)  // two blocks' gathers in flight together
+      for (; base + 2 * W <= len; base += 2 * W) {
+        T p[2 * W];
+#pragma unroll
+        for (int l = 0; l < 2 * W; ++l) p[l] = mul_rn(v[base + l], ldx(xb + c[base + l]));
+#pragma unroll
+        for (int l = 0; l < W; ++l) acc[l] = add_rn(acc[l], p[l]);
+#pragma unroll
+        for (int l = 0; l < W; ++l) acc[l] = add_rn(acc[l], p[W + l]);
+      }
     for (; base + W <= len; base += W) {
       T p[W];
 #pragma unroll
@@ -254,6 +264,16 @@ __device__ __forceinline__ T row_vla_coo(const uint32_t* __restrict__ c, const T
   T y = T(0);
   int base = 0;
   if (L == W) {  // power-of-two lane count: whole steps without predicates
+    if constexpr (W <= 8)  // two steps' gathers in flight together
+      for (; base + 2 * W <= len; base += 2 * W) {
+        T p[W], q[W];
+#pragma unroll
+        for (int l = 0; l < W; ++l) p[l] = mul_rn(v[base + l], ldx(xb + c[base + l]));
+#pragma unroll
+        for (int l = 0; l < W; ++l) q[l] = mul_rn(v[base + W + l], ldx(xb + c[base + W + l]));
+        y = add_rn(y, tree_regs<T, W>(p));
+        y = add_rn(y, tree_regs<T, W>(q));
+      }
     for (; base + W <= len; base += W) {
       T p[W];
 #pragma unroll
