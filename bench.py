@@ -68,6 +68,30 @@ def algo_bytes(fmt: str, nrows: int, ncols: int, nnz: int, sv: int, ndiags: int 
     return nrows * ndiags * sv + ndiags * 4 + ncols * sv + nrows * sv
 
 
+EXCHANGE = {"c5": "NCCL halo exchange of x planes", "c1": "NCCL halo exchange of x planes",
+            "c4": "NCCL halo exchange of 4096-entry x blocks", "c3": "NCCL all-gather of x"}
+
+
+def config_block(cfg_name: str, fmt: str, nrows: int, nnz: int, world: int) -> dict:
+    """The `config` object of a JSON line; both arms (ours, reference) emit
+    exactly this for the same run, so the driver sees the same config."""
+    cfg = CONFIGS[cfg_name]
+    return {"workload": cfg["workload"], "config": cfg_name, "format": fmt, "nrows": int(nrows), "nnz": int(nnz),
+            "l2": ("L2 flushed between steps (252 MB write, then read back so no dirty lines remain), outside the "
+                   "timed events") if cfg_name == "c1" else "inputs larger than L2 (126 MB), no flush",
+            "parallelism": "single GPU" if world == 1 else
+            f"row-partition: {world} contiguous row blocks, {EXCHANGE[cfg_name]}, interior rows overlapped with "
+            "the exchange"}
+
+
+def stencil_nnz(nx: int, ny: int, nz: int) -> int:
+    """prod(3 n_d - 2) (1 for n_d = 1), matrixio.py:170-210."""
+    out = 1
+    for d in (nx, ny, nz):
+        out *= 3 * d - 2 if d > 1 else 1
+    return out
+
+
 # ------------------------------------------------------------------ clocks --
 class ClockSampler:
     """NVML sampling of SM clock + clock-event reasons during a region."""
@@ -404,10 +428,7 @@ def run_ours(args, torch, dist, rank, world, local_rank):
         "metric": METRIC, "value": results[head]["gflops"], "unit": UNIT, "n_gpus": 1, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": results[head]["ms_per_spmv"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
-        "config": {"workload": cfg["workload"], "config": args.config, "format": head, "nrows": m.nrows,
-                   "nnz": m.nnz, "l2": "inputs larger than L2 (126 MB), no flush" if args.config != "c1"
-                   else "L2 flushed between steps (252 MB write, then read back so no dirty lines remain), outside the timed events",
-                   "parallelism": "row-partition" if world > 1 else "single GPU"},
+        "config": config_block(args.config, head, m.nrows, m.nnz, 1),
         "roofline": roofline(results[head]["bytes_per_spmv"], t, pk, traffic_for(f"{args.config}/{head}")),
         "gpu_launches": args.steps * results[head]["launches"],
         "clocks": clocks,
@@ -427,7 +448,83 @@ def run_ours(args, torch, dist, rank, world, local_rank):
             y_gpu = sp.spmv_csr_plain(csr, x).cpu().numpy()
             line["cpu_baseline"] = cpu_baseline_csr(h["row_pointers"], h["col_indices"], h["values"],
                                                     x.cpu().numpy(), args.cpu_budget, y_check=y_gpu)
+            del h, y_gpu
+    if not args.no_extras and args.config == "c5" and args.per_config:
+        # the other large configs under the same clock (BASELINE.json configs
+        # 3 and 4): device memory of the 256^3 containers is released first
+        del mats, m, x
+        import gc
+        gc.collect()
+        torch.cuda.empty_cache()
+        line["per_config"] = {c: per_config_measure(args, torch, sp, device, pk, c) for c in ("c3", "c4")}
     emit(line)
+
+
+def _oracle_check(y_gpu: np.ndarray, ref: np.ndarray, exact_rows=None) -> dict:
+    """GPU y against the C oracle's y: bit-exact row fraction, max rel_err
+    (tests/helpers.py:71-77 semantics), and whether every row that is
+    required to be bit-exact (exact_rows mask) is."""
+    ui = np.uint64 if y_gpu.dtype.itemsize == 8 else np.uint32
+    same = y_gpu.view(ui) == ref.astype(y_gpu.dtype).view(ui)
+    err = np.abs(y_gpu.astype(np.float64) - ref.astype(np.float64)) / np.maximum(np.abs(ref.astype(np.float64)), 1.0)
+    out = {"bit_exact_rows_frac": round(float(same.mean()), 6), "max_rel_err": float(err.max()) if err.size else 0.0}
+    if exact_rows is not None:
+        out["required_bit_exact_rows_ok"] = bool(same[exact_rows].all())
+    return out
+
+
+def per_config_measure(args, torch, sp, device, pk, name: str) -> dict:
+    """One config of BASELINE.json besides the headline: every format's
+    device-timed GFLOP/s and roofline fraction, plus its y against the C
+    oracle (oracle/spmv_oracle.c) on the same inputs."""
+    from oracle import c_oracle
+    mats, x = build_workload(torch, sp, name, device)
+    xh = x.cpu().numpy()
+    steps = max(10, args.steps)
+    out = {"workload": CONFIGS[name]["workload"]}
+    refs = {}
+    csr_h = mats["csr"].to_host()
+    irp = csr_h["row_pointers"]
+    short = np.diff(irp.astype(np.int64)) <= 32  # rows the kernels keep in the reference order
+    refs["csr"] = c_oracle.csr_plain(len(irp) - 1, irp, csr_h["col_indices"], csr_h["values"], xh)
+    if "dia" in mats:
+        hd = mats["dia"].to_host()
+        refs["dia"] = c_oracle.dia_plain(mats["dia"].nrows, mats["dia"].ncols, hd["offsets"], hd["values"], xh)
+        del hd
+    for fmt, m in mats.items():
+        y = torch.empty(m.nrows, dtype=m.values.dtype, device=device)
+        fn_ = spmv_fn(sp, fmt)
+        xx = x if m.values.dtype == torch.float64 else x.float()
+        fn = lambda: fn_(m, xx, out=y)  # noqa: E731
+        fn()
+        torch.cuda.synchronize()
+        t = time_steps(torch, fn, steps, args.warmup)
+        b = bytes_of(m, fmt)
+        r = {"gflops": round(2.0 * m.nnz / t / 1e9, 2), "ms_per_spmv": round(t * 1e3, 4),
+             "gbs": round(b / t / 1e9, 1), "bytes_per_spmv": b, "launches": launches_per_spmv(sp, m),
+             "plan": plan_of(sp, m), "roofline_frac": round(b / t / 1e9 / pk["hbm_gbs"], 4), "nnz": m.nnz,
+             "steps": steps}
+        if name == "c3":
+            r["gather_roofline"] = {
+                "achieved_ggathers_s": round(m.nnz / t / 1e9, 1), "ceiling_ggathers_s": GATHER_CEILING_GS,
+                "frac": round(m.nnz / t / 1e9 / GATHER_CEILING_GS, 3),
+                "source": "tools/gather_ceiling.cu, profiles/r1_gather_ceiling.txt"}
+        yg = y.cpu().numpy()
+        if fmt.startswith("dia"):
+            r["gpu_vs_oracle"] = _oracle_check(yg, refs["dia"], np.ones(m.nrows, dtype=bool))
+        elif fmt.endswith("f32"):
+            # fp32 bar: 1e-5 against the f64-evaluated product (SURVEY.md F6)
+            r["gpu_vs_oracle"] = _oracle_check(yg, refs["csr"])
+            r["gpu_vs_oracle"]["bar"] = "f32 within 1e-5 of the f64-evaluated oracle"
+        else:
+            r["gpu_vs_oracle"] = _oracle_check(yg, refs["csr"], short)
+        out[fmt] = r
+        del y
+    del mats, x
+    import gc
+    gc.collect()
+    torch.cuda.empty_cache()
+    return out
 
 
 def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
@@ -450,7 +547,6 @@ def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
         part = RowPartition.contiguous(n, world, unit=nx * ny)
         r0, r1 = part.rows(rank)
         rows = sp.gen_stencil27_rows(nx, ny, nz, r0, r1)
-        exchange = "NCCL halo exchange of x planes"
     elif args.config == "c4":
         # banded 2^23: row blocks (multiples of ROW_PAD), 4096-entry halos
         n = 1 << 23
@@ -458,10 +554,12 @@ def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
         nd = len(offs)
         part = RowPartition.contiguous(n, world, unit=8)
         r0, r1 = part.rows(rank)
-        full = sp.to_format(sp.DiaMatrix(sp.MatrixShape(n, n, nnz_total), offs, vals), "csr")
-        rows = _csr_rows(full, r0, r1)
-        del full
-        exchange = "NCCL halo exchange of 4096-entry x blocks"
+        # only this rank's rows go to the device: the slab's DIA rows with
+        # offsets shifted by r0 (column - local row) hold its global columns
+        slab = sp.DiaMatrix(sp.MatrixShape(r1 - r0, n, int(np.count_nonzero(vals[r0:r1]))),
+                            (offs.astype(np.int64) + r0).astype(np.int32), np.ascontiguousarray(vals[r0:r1]))
+        rows = sp.to_format(slab, "csr")
+        del slab
     else:
         # Zipf: every rank needs all of x (uniform columns): NCCL all-gather
         n = 2_000_000
@@ -472,7 +570,6 @@ def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
         e0, e1 = int(irp[r0]), int(irp[r1])
         rows = sp.CsrMatrix.from_arrays(r1 - r0, n, (irp[r0:r1 + 1].astype(np.int64) - e0).astype(np.uint32),
                                         cols[e0:e1], vals[e0:e1])
-        exchange = "NCCL all-gather of x"
     x_full = synthetic.probe_x(n, synthetic.X_SEED)
     x_local = torch.from_numpy(x_full[r0:r1]).to(device)
     head = args.format or cfg["formats"][0]
@@ -504,10 +601,7 @@ def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
         "metric": METRIC, "value": results[head]["gflops"], "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": results[head]["ms_per_spmv"], "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
-        "config": {"workload": cfg["workload"], "config": args.config, "format": head, "nrows": n, "nnz": nnz_total,
-                   "l2": "inputs larger than L2 (126 MB), no flush",
-                   "parallelism": f"row-partition: {world} contiguous row blocks, {exchange}, "
-                                  "interior rows overlapped with the exchange"},
+        "config": config_block(args.config, head, n, nnz_total, world),
         "roofline": roofline(results[head]["bytes_per_spmv"] // world, t, pk, traffic_for(f"{args.config}/{head}")),
         "gpu_launches": args.steps * results[head]["launches"],
         "clocks": clocks,
@@ -530,6 +624,33 @@ def run_ours_multi(args, torch, dist, rank, world, local_rank, pk):
         line["e2e"] = {"value": round(2.0 * nnz_total / te / 1e9, 2), "unit": UNIT,
                        "h2d_bytes_per_step": n * 8, "d2h_bytes_per_step": n * 8, "ms_per_step": round(te * 1e3, 3),
                        "path": "DistributedMatrix.spmv per rank, pinned host x slice in, pinned host y slice out"}
+        # parity of the row-partitioned product: every format's y gathered
+        # over the group (gather_global) against the C oracle of the whole
+        # matrix, on rank 0
+        from paper_2304_09511_b200.dist import gather_global
+        ref = None
+        if rank == 0:
+            from oracle import c_oracle
+            if args.config in ("c5", "c1"):
+                g_irp, g_cols, g_vals = c_oracle.stencil27_rows(*cfg["grid"], 0, n)
+                ref = c_oracle.csr_plain(n, g_irp, g_cols, g_vals, x_full)
+                lens = np.diff(g_irp.astype(np.int64))
+                del g_irp, g_cols, g_vals
+            elif args.config == "c4":
+                ref = c_oracle.dia_plain(n, n, offs, vals, x_full)
+                lens = np.zeros(n, dtype=np.int64)
+            else:
+                ref = c_oracle.csr_plain(n, irp, cols, vals, x_full)
+                lens = np.diff(irp.astype(np.int64))
+        parity = {}
+        for fmt, dm in dms.items():
+            yy = torch.empty(r1 - r0, dtype=torch.float64, device=device)
+            dm.spmv(out=yy)
+            g = gather_global(part, yy)
+            if rank == 0:
+                parity[fmt] = _oracle_check(g.cpu().numpy(), ref, lens <= 32)
+        if rank == 0:
+            line["gpu_vs_oracle"] = parity
     if rank == 0:
         emit(line)
 
@@ -620,7 +741,7 @@ def _reference_sample(args, c_oracle, synthetic):
             return (lambda: c_oracle.csr_plain(r1 - r0, irp, cols, vals, x)), vals.shape[0], desc
 
         fn, nnz, desc = calibrate(build, n, plane)
-        return fn, nnz, desc, "csr"
+        return fn, nnz, desc, "csr", (n, stencil_nnz(nx, ny, nz))
     if args.config == "c3":
         n = 2_000_000
         irp, cols, vals = synthetic.zipf_csr(n, n, synthetic.ZIPF_SEED)
@@ -634,10 +755,10 @@ def _reference_sample(args, c_oracle, synthetic):
             return (lambda: c_oracle.csr_plain(k, sirp, scols, svals, x)), e, desc
 
         fn, nnz, desc = calibrate(build, n, 1024)
-        return fn, nnz, desc, "csr"
+        return fn, nnz, desc, "csr", (n, int(irp[-1]))
     # c4: banded DIA, the config's headline format
     n = 1 << 23
-    offs, vals, _ = synthetic.banded_dia(n, synthetic.BANDED_OFFSETS, synthetic.BANDED_SEED)
+    offs, vals, nnz_total = synthetic.banded_dia(n, synthetic.BANDED_OFFSETS, synthetic.BANDED_SEED)
     x = synthetic.probe_x(n, synthetic.X_SEED)
     o64 = offs.astype(np.int64)
 
@@ -649,7 +770,7 @@ def _reference_sample(args, c_oracle, synthetic):
         return (lambda: c_oracle.dia_plain(k, n, offs, sv, x)), cells, desc
 
     fn, nnz, desc = calibrate(build, n, 8)
-    return fn, nnz, desc, "dia"
+    return fn, nnz, desc, "dia", (n, nnz_total)
 
 
 def run_reference(args, rank, world):
@@ -660,7 +781,7 @@ def run_reference(args, rank, world):
     from oracle import c_oracle
     from paper_2304_09511_b200 import synthetic
     cfg = CONFIGS[args.config]
-    fn, nnz, sample, fmt = _reference_sample(args, c_oracle, synthetic)
+    fn, nnz, sample, fmt, dims = _reference_sample(args, c_oracle, synthetic)
     for _ in range(args.warmup):
         fn()
     t0 = time.perf_counter()
@@ -671,7 +792,7 @@ def run_reference(args, rank, world):
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": round(t * 1e3, 3), "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded, BASELINE.json configs)",
-            "config": {"workload": cfg["workload"], "config": args.config, "format": fmt},
+            "config": config_block(args.config, fmt, dims[0], dims[1], world),
             "cpu_baseline": {"value": v, "unit": UNIT, "kind": "port", "cores": c_oracle.max_threads(),
                              "sample": sample},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -686,14 +807,46 @@ def emit(line: dict) -> None:
     os.write(_JSON_FD if _JSON_FD is not None else 1, (json.dumps(line) + "\n").encode())
 
 
+def launcher_cmd(argv: list, gpus: int, port: int) -> list:
+    """`bench.py --gpus N` outside torchrun (no WORLD_SIZE): the same command
+    under torch.distributed.run, one rank per GPU, rendezvous on 127.0.0.1."""
+    return [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={gpus}",
+            "--master-addr", "127.0.0.1", "--master-port", str(port), str(ROOT / "bench.py"), *argv]
+
+
+def _free_port() -> int:
+    import socket
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    return port
+
+
 def main():
     global _JSON_FD
+    pre = argparse.ArgumentParser(add_help=False)
+    pre.add_argument("--gpus", type=int, default=1)
+    pre.add_argument("--print-launcher", action="store_true")
+    known, _ = pre.parse_known_args()
+    if known.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # one process per GPU: re-launch this command under torchrun; rank 0
+        # prints the JSON line (n_gpus = N)
+        argv = [a for a in sys.argv[1:] if a != "--print-launcher"]
+        cmd = launcher_cmd(argv, known.gpus, _free_port())
+        if known.print_launcher:
+            print(json.dumps({"launcher": cmd}))
+            return
+        sys.stdout.flush()
+        os.execv(cmd[0], cmd)
     # Only the JSON line goes to stdout: everything else that writes to fd 1
     # (NCCL's version banner, library chatter) is sent to stderr.
     sys.stdout.flush()
     _JSON_FD = os.dup(1)
     os.dup2(2, 1)
     ap = argparse.ArgumentParser()
+    ap.add_argument("--print-launcher", action="store_true",
+                    help="with --gpus N > 1 outside torchrun: print the torchrun command instead of running it")
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=200)
     ap.add_argument("--warmup", type=int, default=5)
@@ -703,6 +856,8 @@ def main():
     ap.add_argument("--no-extras", action="store_true", help="headline format only (profiling runs)")
     ap.add_argument("--conversions", action="store_true", help="time the format conversions only")
     ap.add_argument("--cpu-budget", type=float, default=10.0)
+    ap.add_argument("--no-per-config", dest="per_config", action="store_false",
+                    help="c5 only: skip the c3 / c4 lines under per_config")
     ap.add_argument("--force-dist", action="store_true",
                     help="use the row-partitioned path even at world size 1 (exercises it on one GPU)")
     args = ap.parse_args()

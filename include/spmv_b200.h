@@ -216,10 +216,11 @@ int spmv_dia(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags,
 /* spmv_dia with a gap: launch rows v >= y_split are slab rows v + y_gap
  * (their values, x reach and y), so a rank's two boundary blocks run as one
  * launch after the halo exchange.  nrows and avail_rows count launch rows
- * (avail_rows = slab rows available from `values` minus y_gap).  y_split
- * must fall on the kernel's row-tile boundary (a multiple of 256 always
- * does) and y_gap rows must be a 16-byte multiple of the row bytes;
- * SPMV_UNSUPPORTED otherwise (run two spmv_dia launches then). */
+ * (avail_rows = slab rows available from `values` minus y_gap).  When
+ * y_split falls on the kernel's row-tile boundary R (R = 256 rows for up to
+ * 28 f64 / 56 f32 diagonals, fewer for wider rows) and y_gap rows are a
+ * 16-byte multiple of the row bytes, both blocks run in one launch;
+ * otherwise the call runs them as two spmv_dia launches (same result). */
 int spmv_dia_gapped(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags,
                     int64_t avail_rows, const int32_t* offsets, const void* values,
                     const void* x, int64_t row_base, int64_t col_base, int64_t x_len,

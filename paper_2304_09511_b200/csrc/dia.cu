@@ -202,9 +202,15 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) % 16 == 0) && ((R * row_bytes) % 16 == 0) &&
                        ((avail_rows * row_bytes) % 16 == 0);
   const bool use_bulk = nd > 0 && nd <= kMaxSmemOffsets && R >= 8 && aligned;
-  if (gapped && (!use_bulk || split % R != 0 || (gap * int64_t(row_bytes)) % 16 != 0))
-    return fail(SPMV_UNSUPPORTED, "gapped DIA launch needs the bulk kernel and a split on a %lld-row tile boundary",
-                (long long)R);
+  if (gapped && (!use_bulk || split % R != 0 || (gap * int64_t(row_bytes)) % 16 != 0)) {
+    // the split is not on this block's row-tile boundary (R depends on the
+    // diagonal count and dtype): the two blocks as two plain launches
+    int rc = dia_launch<T>(split, ncols, nd, avail_rows + gap, offsets, vals, x, row_base, col_base, y, st);
+    if (rc || nrows == split) return rc;
+    const int64_t s1 = split + gap;  // slab row of launch row `split`
+    return dia_launch<T>(nrows - split, ncols, nd, avail_rows - split, offsets, vals + s1 * nd, x, row_base + s1,
+                         col_base, y + s1, st);
+  }
   if (!use_bulk) {
     int64_t grid = (nrows + kDiaThreads - 1) / kDiaThreads;
     if (grid > int64_t(sms) * 32) grid = int64_t(sms) * 32;

@@ -11,14 +11,22 @@ Here each rank is one process on one GPU (torch.distributed, NCCL):
 * a rank holds its row slab with GLOBAL column indices and one contiguous
   x window [win_lo, win_hi) = its own rows plus the halo below and above;
   the kernels index x through `col_base = win_lo`, so there is no local /
-  remote split and every row keeps the single-GPU summation order — the
-  concatenated y is bit-identical to the single-GPU y (stronger than the
-  reference's split sum, which is only 1e-15-close, SURVEY.md A.7);
+  remote split.  Rows of at most exact_len (32) entries — every row of the
+  stencil and banded configs — keep the single-GPU summation order, so
+  their concatenated y is bit-identical to the single-GPU y (stronger than
+  the reference's split sum, which is only 1e-15-close).
+  Longer rows are reduced in per-tile / per-range partials whose cuts depend
+  on the slab, so they are within 1e-12 of the reference, not bit-identical;
 * the halo exchange is one batched NCCL send/recv group over NVLink (only
   neighbours for banded / stencil slabs; all_gather when every rank needs
   all of x);
 * rows that read no halo (the interior) run while the exchange is in
-  flight; the boundary rows run after it (`DistributedMatrix.spmv`).
+  flight; the boundary rows run after it (`DistributedMatrix.spmv`).  The
+  all_gather variant writes the whole window, the rank's own block
+  included, so it is not overlapped with any product;
+* over a gloo group (CPU collectives; the multi-process tests run several
+  ranks' kernels on one GPU that way) a device window is staged through
+  host memory for the exchange — the kernels never wait on each other.
 
 `build_halo_plan` and `halo_exchange` are pure host/torch.distributed logic
 (tested with gloo on CPU); everything that touches matrix data runs in the
@@ -128,6 +136,13 @@ def halo_exchange(plan: HaloPlan, window: torch.Tensor, group=None) -> list:
     needed."""
     import torch.distributed as dist
 
+    if window.is_cuda and dist.get_backend(group) == "gloo":
+        # gloo moves CPU tensors: exchange a host copy, then put it back
+        host = window.cpu()
+        for w in halo_exchange(plan, host, group):
+            w.wait()
+        window.copy_(host)
+        return []
     lo = plan.window[0]
     if plan.allgather:
         r0, r1 = plan.rows
@@ -363,7 +378,9 @@ class DistributedMatrix:
             s.x_local.copy_(x_local)
         y = out if out is not None else torch.empty(s.nloc, dtype=s.xw.dtype, device=s.xw.device)
         lower, interior, upper = s.parts
-        if self.overlap:
+        # all_gather rewrites the whole window (own block too): no product
+        # may read it meanwhile
+        if self.overlap and not self.plan.allgather:
             works = halo_exchange(self.plan, s.xw, self.group)
             s.run_part(interior if s.boundary is None else s.interior_g, y)
             for w in works:
@@ -381,7 +398,7 @@ class DistributedMatrix:
         return y
 
     def launches_per_spmv(self) -> int:
-        if self.overlap and self.slab.boundary is not None:
+        if self.overlap and not self.plan.allgather and self.slab.boundary is not None:
             return 2
         return sum(1 for p in self.slab.parts if p.matrix is not None and p.hi > p.lo)
 
@@ -391,9 +408,13 @@ def gather_global(part: RowPartition, y_local: torch.Tensor, group=None) -> torc
     import torch.distributed as dist
 
     sizes = [part.rows(r)[1] - part.rows(r)[0] for r in range(part.world)]
+    if y_local.shape[0] != sizes[dist.get_rank(group)]:
+        raise ValueError("y_local must hold exactly this rank's rows")
     m = max(sizes)
-    buf = torch.zeros(m, dtype=y_local.dtype, device=y_local.device)
+    # gloo moves CPU tensors (the multi-process tests); NCCL device ones
+    dev = torch.device("cpu") if dist.get_backend(group) == "gloo" else y_local.device
+    buf = torch.zeros(m, dtype=y_local.dtype, device=dev)
     buf[:y_local.shape[0]] = y_local
-    out = torch.empty(m * part.world, dtype=y_local.dtype, device=y_local.device)
+    out = torch.empty(m * part.world, dtype=y_local.dtype, device=dev)
     dist.all_gather_into_tensor(out, buf, group=group)
-    return torch.cat([out[r * m:r * m + sizes[r]] for r in range(part.world)])
+    return torch.cat([out[r * m:r * m + sizes[r]] for r in range(part.world)]).to(y_local.device)

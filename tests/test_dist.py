@@ -3,7 +3,7 @@
 CPU: partition / halo-plan logic, and the real halo exchange over gloo with
 world sizes 2 and 3 (multi-process).  GPU: P ranks emulated in one process
 on one device (no cross-waiting kernels): the concatenated slab products
-must be bit-identical to the single-GPU product for every format, mirroring
+must be bit-identical to the C oracle's product for every format, mirroring
 the reference's transparency tests (test_hpcg.py:97-107,
 test_acceptance.py:207-221) with a stricter bound.
 """
@@ -103,9 +103,19 @@ def test_emulated_ranks_bit_identical(lib_built, fmt, world):
     nx, ny, nz = 24, 20, 16
     n = nx * ny * nz
     glob = sp.gen_stencil27(nx, ny, nz)
-    x = torch.from_numpy(np.random.default_rng(5).uniform(-1, 1, n)).cuda()
-    ref_m = glob if fmt == "csr" else (sp.csr_to_coo(glob) if fmt == "coo" else sp.coo_to_dia(sp.csr_to_coo(glob)))
-    ref = sp.dispatch(ref_m, x).cpu().numpy()
+    from oracle import c_oracle
+    xh = np.random.default_rng(5).uniform(-1, 1, n)
+    x = torch.from_numpy(xh).cuda()
+    # checker: the C oracle of the whole matrix (the format's own reference
+    # kernel: csr_plain / np.add.at order / dia_plain over the stored block)
+    irp, cols, vals = c_oracle.stencil27_rows(nx, ny, nz, 0, n)
+    if fmt == "dia":
+        hd = sp.coo_to_dia(sp.csr_to_coo(glob)).to_host()
+        ref = c_oracle.dia_plain(n, n, hd["offsets"], hd["values"], xh)
+    elif fmt == "coo":
+        ref = c_oracle.coo_plain(n, np.repeat(np.arange(n), np.diff(irp.astype(np.int64))), cols, vals, xh)
+    else:
+        ref = c_oracle.csr_plain(n, irp, cols, vals, xh)
     part = RowPartition.contiguous(n, world, unit=nx * ny)
     slabs = []
     for r in range(world):
@@ -165,8 +175,10 @@ def test_emulated_ranks_random_matrix_allgather(lib_built):
     cols = np.concatenate([np.sort(rng.choice(n, size=int(k), replace=False)) for k in lens])
     vals = rng.standard_normal(cols.shape[0])
     glob = sp.CsrMatrix.from_arrays(n, n, irp, cols, vals)
-    x = torch.from_numpy(rng.uniform(-1, 1, n)).cuda()
-    ref = sp.spmv_csr_plain(glob, x).cpu().numpy()
+    from oracle import c_oracle
+    xh = rng.uniform(-1, 1, n)
+    x = torch.from_numpy(xh).cuda()
+    ref = c_oracle.csr_plain(n, irp.astype(np.uint32), cols, vals, xh)
     part = RowPartition.contiguous(n, world)
     slabs = [build_local_slab(_csr_rows(glob, *part.rows(r)), *part.rows(r), "csr") for r in range(world)]
     plans = [build_halo_plan(part, [s.window for s in slabs], r) for r in range(world)]
@@ -184,3 +196,43 @@ def test_emulated_ranks_random_matrix_allgather(lib_built):
     assert got[short].tobytes() == ref[short].tobytes()
     assert np.max(np.abs(got - ref) / np.maximum(np.abs(ref), 1.0)) <= 1e-12
     assert all(p.allgather or p.recv_entries == n - (p.rows[1] - p.rows[0]) for p in plans)
+
+
+@pytest.mark.gpu
+@pytest.mark.parametrize("world", [2, 3])
+def test_emulated_ranks_wide_dia(lib_built, world):
+    """33 diagonals: a 256-row f64 DIA tile no longer fits a stage, so the
+    boundary split is not on the kernel's row tile and spmv_dia_gapped runs
+    the two blocks as two launches (it used to return SPMV_UNSUPPORTED)."""
+    import torch
+
+    import paper_2304_09511_b200 as sp
+    from oracle import c_oracle
+    from paper_2304_09511_b200 import synthetic
+    from paper_2304_09511_b200.dist import _csr_rows, build_local_slab, exchange_in_process
+    n = 3 * 2048
+    o, v, nnz = synthetic.banded_dia(n, range(-16, 17), 3)
+    dia = sp.DiaMatrix(sp.MatrixShape(n, n, nnz), o, v)
+    full = sp.to_format(dia, "csr")
+    xh = np.random.default_rng(2).uniform(-1, 1, n)
+    ref = c_oracle.dia_plain(n, n, o, v, xh)
+    part = RowPartition.contiguous(n, world, unit=8)
+    slabs = [build_local_slab(_csr_rows(full, *part.rows(r)), *part.rows(r), "dia") for r in range(world)]
+    plans = [build_halo_plan(part, [s.window for s in slabs], r) for r in range(world)]
+    x = torch.from_numpy(xh).cuda()
+    for r, s in enumerate(slabs):
+        s.x_local.copy_(x[part.rows(r)[0]:part.rows(r)[1]])
+    exchange_in_process(plans, [s.xw for s in slabs])
+    ys = []
+    for s in slabs:
+        y = torch.full((s.nloc,), float("nan"), dtype=torch.float64, device="cuda")
+        if s.boundary is not None:
+            s.run_part(s.interior_g, y)
+            s.run_part(s.boundary, y)
+        else:
+            for p in s.parts:
+                s.run_part(p, y)
+        ys.append(y)
+    assert torch.cat(ys).cpu().numpy().tobytes() == ref.tobytes()
+    if world == 3:
+        assert slabs[1].boundary is not None
