@@ -230,6 +230,13 @@ def build_workload(torch, sp, cfg_name: str, device):
         mats["csr"] = sp.to_format(dia, "csr")
     n = next(iter(mats.values())).ncols
     x = torch.from_numpy(synthetic.probe_x(n, synthetic.X_SEED)).to(device)
+    # experiment scripts (tools/*.sh) pass kernel choices as SPMV_* variables;
+    # they become each container's plan configuration (never read otherwise)
+    from paper_2304_09511_b200.planconfig import AUTO, PlanConfig, set_plan_config
+    forced = PlanConfig.from_env()
+    if forced != AUTO:
+        for m in mats.values():
+            set_plan_config(m, forced)
     return mats, x
 
 

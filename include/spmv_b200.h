@@ -15,12 +15,17 @@
  *   - Every call returns an spmv_status; spmv_last_error() gives the
  *     thread-local message of the last failing call.  The codes map 1:1 to
  *     the reference's exception classes (errors.py:4-37).
- *   - SpMV calls never allocate and never write caller memory other than y
- *     (kernels.py:59,72,94: the kernel owns a fresh y).  Workspace lives in
- *     the plan objects.  Calls on different plans are reentrant
- *     (bench.py:167-172 calls kernels from several threads on different
- *     matrices); calls that share a plan must be ordered on one stream
- *     (the plan owns partial-sum slots and the warp-stream range counter).
+ *   - SpMV calls never write caller memory other than y (kernels.py:59,72,
+ *     94: the kernel owns a fresh y).  Workspace lives in the plan objects.
+ *     Every entry point is reentrant, also on one plan (kernels
+ *     are pure; bench.py:167-172 calls kernels from several threads): the
+ *     per-launch scratch of a plan (partial-sum slots, the warp-stream range
+ *     counter) is kept per CUDA stream — allocated, zero-filled, on the
+ *     first launch on a stream and reused after — so products on different
+ *     streams with disjoint outputs may run concurrently.  Lazily built
+ *     parts (vla row lists, the host-pipeline staging) are built once under
+ *     the plan's lock; host-pipeline calls on one plan are serialised on the
+ *     device (each waits for the previous one's end).
  *   - Calls that return a host-visible count (plan creation, conversion
  *     analyze steps) synchronise `stream`; SpMV calls are asynchronous.
  */
@@ -33,7 +38,7 @@
 extern "C" {
 #endif
 
-#define SPMV_B200_ABI_VERSION 1
+#define SPMV_B200_ABI_VERSION 2
 
 typedef enum {
     SPMV_F32 = 0,
@@ -57,8 +62,55 @@ const char* spmv_last_error(void);
 /* Number of SMs of the current device (grid sizing; 148 on B200). */
 int spmv_device_sm_count(int* out);
 
+/* ---- plan configuration ------------------------------------------------- */
+/* Kernel choices of one plan.  Every field at its "auto" value (0, or -1
+ * where noted) keeps the plan's measured default, which depends on the
+ * row-length histogram.  A plan's configuration is fixed at creation, so
+ * several plans of one matrix can run different kernels side by side in
+ * one process; the run-first tuner (autotune.py:60-139, hpcg.py:270-304:
+ * "format plus CSR bin thresholds") creates one plan per candidate and
+ * times them.  Replaces the process-global environment switches of ABI 1. */
+#define SPMV_PLAN_CONFIG_VERSION 1
+typedef struct {
+    int32_t version;          /* SPMV_PLAN_CONFIG_VERSION                            */
+    int32_t tile;             /* entries per TMA tile (CSR: 1024 1664 2048 2304 4096; */
+                              /* COO: 1024 1536 2048); 0 = plan's choice              */
+    int32_t groups;           /* consumer groups per tile CTA (CSR 1/3/4, COO 1/6/7); */
+                              /* 0 = plan's choice; unknown combinations fall back    */
+    int32_t exact_len;        /* CSR warp-stream kernel: rows of <= exact_len entries */
+                              /* are never split between warp ranges and are summed  */
+                              /* left to right (bit-exact), 1..32; 0 = 32.  The tile  */
+                              /* kernels always use 32 (their tile extension)         */
+    int32_t warp_stream;      /* whole-matrix kernel: -1 plan's choice (warp-stream   */
+                              /* when rows/runs exceed exact_len), 0 tiles, 1 ws      */
+    int32_t ranges_per_warp;  /* warp-stream entry ranges per resident warp 1..64;    */
+                              /* 0 = 8                                                */
+    int32_t tma_hint;         /* L2 evict_first on the TMA matrix stream: -1 plan's   */
+                              /* choice (COO always, CSR with long rows), 0, 1        */
+    int32_t ctas_per_sm;      /* cap on resident CTAs per SM; 0 = occupancy limit     */
+    int32_t dia_kernel;       /* DIA (groups, stages, threads) 0..4; -1 = auto        */
+    int32_t dia_rows;         /* DIA rows per tile, multiple of 8; 0 = auto           */
+    int32_t flags;            /* experiments: bit0 products mode, bit1 warp per long  */
+                              /* segment (tile kernels); 0 = off                      */
+    int32_t reserved[5];
+} spmv_plan_config;
+
+/* Fill *cfg with the auto values (version set).  Plans created with a NULL
+ * configuration use exactly these. */
+int spmv_plan_config_init(spmv_plan_config* cfg);
+
 /* ---- CSR (kernels.py:69-82 spmv_csr_plain, :143-171 spmv_csr_vla) ------ */
 typedef struct spmv_csr_plan spmv_csr_plan;
+
+/* spmv_csr_plan_create with an explicit configuration (NULL = auto; the
+ * exact_len argument of spmv_csr_plan_create is cfg->exact_len here). */
+int spmv_csr_plan_create_ex(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
+                            const uint32_t* row_pointers,
+                            const spmv_plan_config* cfg, void* stream,
+                            spmv_csr_plan** out);
+/* The configuration the plan resolved: tile, groups, warp_stream (0/1),
+ * ranges_per_warp, tma_hint (0/1) and exact_len as the kernels run them. */
+int spmv_csr_plan_config(const spmv_csr_plan* plan, spmv_plan_config* out);
 
 /* Analyse the matrix once: long-row census (rows > exact_len entries), tile
  * size and consumer groups per CTA (G groups share a G+1 stage ring:
@@ -83,7 +135,7 @@ int spmv_debug_csr_phases(unsigned long long* out8);
  * fix-up of rows split between tiles or warp-stream ranges). */
 int spmv_csr_plan_info(const spmv_csr_plan* plan, int64_t* n_long_rows,
                        int64_t* n_items, int64_t* launches);
-/* Consumer groups per tile CTA the plan chose (SPMV_CSR_GROUPS overrides). */
+/* Consumer groups per tile CTA the plan chose (spmv_plan_config.groups). */
 int spmv_csr_plan_groups(const spmv_csr_plan* plan, int* groups);
 /* spmv_csr with a gap in y: rows >= y_split are stored at y[row + y_gap].
  * A rank's two boundary planes (its first and last halo-reading rows, one
@@ -98,7 +150,7 @@ int spmv_csr_gapped(const spmv_csr_plan* plan, const uint32_t* row_pointers,
  * kernel (matrices with rows longer than exact_len: one contiguous entry
  * range per resident warp, nwarps of them), 0 for the tile kernel.  Tile
  * ranges (spmv_csr_range, spmv_csr_host) always use the tile kernel.
- * SPMV_CSR_WS=0/1 overrides the choice. */
+ * spmv_plan_config.warp_stream = 0/1 overrides the choice. */
 int spmv_csr_plan_path(const spmv_csr_plan* plan, int* warp_stream, int64_t* nwarps);
 
 /* y[r] = sum_j av[j] * x[aj[j] - col_base] over row r.  x holds the window
@@ -167,16 +219,23 @@ int spmv_coo_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
                          const uint32_t* row_indices,
                          const uint32_t* col_indices, const void* values,
                          void* stream, spmv_coo_plan** out);
+int spmv_coo_plan_create_ex(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
+                            const uint32_t* row_indices,
+                            const uint32_t* col_indices, const void* values,
+                            const spmv_plan_config* cfg, void* stream,
+                            spmv_coo_plan** out);
 int spmv_coo_plan_destroy(spmv_coo_plan* plan);
+/* Resolved configuration (exact_len is 32 for COO). */
+int spmv_coo_plan_config(const spmv_coo_plan* plan, spmv_plan_config* out);
 /* row_sorted: 1 when the input rows were already non-decreasing;
  * n_items: entries per tile. */
 int spmv_coo_plan_info(const spmv_coo_plan* plan, int64_t* n_runs,
                        int64_t* n_long_runs, int64_t* n_items,
                        int* row_sorted, int64_t* launches);
-/* Consumer groups per tile CTA the plan chose (SPMV_COO_GROUPS overrides). */
+/* Consumer groups per tile CTA the plan chose (spmv_plan_config.groups). */
 /* Whole-matrix kernel the COO plan chose: warp_stream = 1 for the
  * warp-stream kernel (plans with runs longer than 32 entries), else the
- * tile kernel.  SPMV_COO_WS=0/1 overrides the choice. */
+ * tile kernel.  spmv_plan_config.warp_stream = 0/1 overrides the choice. */
 int spmv_coo_plan_path(const spmv_coo_plan* plan, int* warp_stream, int64_t* nwarps);
 int spmv_coo_plan_groups(const spmv_coo_plan* plan, int* groups);
 
@@ -212,6 +271,13 @@ int spmv_dia(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags,
              int64_t avail_rows, const int32_t* offsets, const void* values,
              const void* x, int64_t row_base, int64_t col_base, int64_t x_len,
              void* y, void* stream);
+
+/* spmv_dia with the DIA fields of a configuration (dia_kernel, dia_rows,
+ * ctas_per_sm); NULL = auto, same as spmv_dia. */
+int spmv_dia_ex(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags,
+                int64_t avail_rows, const int32_t* offsets, const void* values,
+                const void* x, int64_t row_base, int64_t col_base, int64_t x_len,
+                void* y, const spmv_plan_config* cfg, void* stream);
 
 /* spmv_dia with a gap: launch rows v >= y_split are slab rows v + y_gap
  * (their values, x reach and y), so a rank's two boundary blocks run as one

@@ -57,6 +57,7 @@ from .kernels import (
     spmv_dia_vla,
 )
 from .lanes import LaneConfig
+from .planconfig import PlanConfig, plan_config_of, set_plan_config
 from .matrixio import (
     CorpusEntry,
     gen_banded,
@@ -69,7 +70,7 @@ from .matrixio import (
     write_matrix_market,
 )
 from .cg import CgState, cg_solve
-from .autotune import Measurement, TuneChoice, distribution_report, measure, tune
-from .sweep import BenchRecord, compare_records, make_report, read_records, render_report, run_corpus, write_records
+from .autotune import Measurement, PlanChoice, TuneChoice, distribution_report, measure, plan_candidates, tune, tune_plan
+from .sweep import BenchRecord, compare_records, read_records, run_corpus, write_records
 
 __version__ = "0.1.0"

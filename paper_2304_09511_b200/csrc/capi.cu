@@ -134,44 +134,7 @@ extern "C" int spmv_csr_halo_split(int64_t nrows, const uint32_t* irp, const uin
   return SPMV_OK;
 }
 
-// ---- tuning knobs (experiments only; defaults are the measured best) ----
 namespace spmv {
-static int env_int(const char* name, int dflt) {
-  const char* v = getenv(name);
-  if (!v || !*v) return dflt;
-  return atoi(v);
-}
-// 0 = let the plan choose (CSR: 1024 when the matrix has long rows, more
-// CTAs per SM hide the long-row gathers; 2048 otherwise; COO: 2048).
-int tile_entries() {
-  static const int t = [] {
-    const int v = env_int("SPMV_TILE", 0);
-    return (v == 1024 || v == 1536 || v == 1664 || v == 2048 || v == 2304 || v == 4096) ? v : 0;
-  }();
-  return t;
-}
-// Experiments: bit0 = products mode allowed (off by default: measured slower
-// on Zipf), bit1 = one warp per long segment instead of 256-entry units.
-int tile_mode_flags() {
-  static const int f = env_int("SPMV_TILE_MODE", 0);
-  return f;
-}
-// L2 evict_first hint on the TMA matrix stream: -1 = per-plan choice (COO
-// always; CSR when the plan has long rows), 0 = never, 1 = always.
-int tma_hint_mode() {
-  static const int m = env_int("SPMV_TMA_HINT", -1);
-  return m;
-}
-// CSR consumer groups per tile CTA (0 = plan's choice).
-int csr_groups() {
-  static const int g = env_int("SPMV_CSR_GROUPS", 0);
-  return g;
-}
-// COO consumer groups per tile CTA (0 = plan's choice).
-int coo_groups() {
-  static const int g = env_int("SPMV_COO_GROUPS", 0);
-  return g;
-}
 int pool_keep_memory() {
   static std::mutex mu;
   static bool done[64] = {false};
@@ -189,34 +152,10 @@ int pool_keep_memory() {
   if (dev < 64) done[dev] = true;
   return SPMV_OK;
 }
-// CSR warp-stream path: -1 = plan's choice (matrices with long rows), 0 off, 1 on.
-int csr_ws_mode() {
-  static const int m = env_int("SPMV_CSR_WS", -1);
-  return m;
-}
-// COO warp-stream path: -1 = plan's choice (plans with long runs), 0 off, 1 on.
-int coo_ws_mode() {
-  static const int m = env_int("SPMV_COO_WS", -1);
-  return m;
-}
-// CSR warp-stream ranges per resident warp (SPMV_WS_RANGES, default 8).
-int ws_ranges_per_warp() {
-  static const int n = [] {
-    const int v = env_int("SPMV_WS_RANGES", 8);
-    return v >= 1 && v <= 64 ? v : 8;
-  }();
-  return n;
-}
-int ctas_per_sm_cap() {
-  static const int c = env_int("SPMV_CTAS_PER_SM", 0);
-  return c;
-}
-int dia_rows_per_tile() {
-  static const int r = env_int("SPMV_DIA_ROWS", 0);
-  return r;
-}
-int dia_config() {  // SPMV_DIA_CFG: -1 auto; 0..4 see dia.cu
-  static const int c = env_int("SPMV_DIA_CFG", -1);
-  return c;
-}
 }  // namespace spmv
+
+extern "C" int spmv_plan_config_init(spmv_plan_config* cfg) {
+  if (!cfg) return fail(SPMV_INVALID_ARG, "cfg is NULL");
+  *cfg = config_or_default(nullptr);
+  return SPMV_OK;
+}

@@ -6,7 +6,9 @@
 
 #include <cstdarg>
 #include <cstdio>
+#include <mutex>
 #include <string>
+#include <vector>
 
 #include "../../include/spmv_b200.h"
 
@@ -98,6 +100,80 @@ struct ScratchBuf {
   ScratchBuf(const ScratchBuf&) = delete;
   ScratchBuf& operator=(const ScratchBuf&) = delete;
 };
+
+// Per-stream launch scratch of a plan (partial-sum slots, range counters).
+// Two launches on different streams get different slots, so one plan can
+// serve concurrent products; launches on one stream are
+// ordered, so they share theirs.  A slot is allocated and zero-filled on its
+// stream the first time that stream launches, then reused.
+struct StreamSlots {
+  struct Slot {
+    cudaStream_t st;
+    void* ptr;
+  };
+  std::mutex mu;
+  std::vector<Slot> slots;
+  size_t bytes = 0;  // per slot
+  int get(cudaStream_t st, void** out) {
+    *out = nullptr;
+    if (bytes == 0) return SPMV_OK;
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Slot& s : slots)
+      if (s.st == st) {
+        *out = s.ptr;
+        return SPMV_OK;
+      }
+    void* p = nullptr;
+    cudaError_t e = cudaMalloc(&p, bytes);
+    if (e != cudaSuccess) return fail(SPMV_CUDA_ERROR, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
+    e = cudaMemsetAsync(p, 0, bytes, st);
+    if (e != cudaSuccess) {
+      cudaFree(p);
+      return fail(SPMV_CUDA_ERROR, "cudaMemsetAsync failed: %s", cudaGetErrorString(e));
+    }
+    slots.push_back({st, p});
+    *out = p;
+    return SPMV_OK;
+  }
+  void release() {
+    std::lock_guard<std::mutex> lock(mu);
+    for (const Slot& s : slots) cudaFree(s.ptr);  // cudaFree waits for the device
+    slots.clear();
+  }
+  ~StreamSlots() { release(); }
+};
+
+// Byte layout of one scratch slot: add(n) reserves n bytes (256-aligned).
+struct SlotLayout {
+  size_t total = 0;
+  size_t add(size_t n) {
+    const size_t off = total;
+    total += (n + 255) & ~size_t(255);
+    return off;
+  }
+};
+
+// Plan configuration with auto values resolved (include/spmv_b200.h).
+inline spmv_plan_config config_or_default(const spmv_plan_config* c) {
+  spmv_plan_config d;
+  d.version = SPMV_PLAN_CONFIG_VERSION;
+  d.tile = 0;
+  d.groups = 0;
+  d.exact_len = 0;
+  d.warp_stream = -1;
+  d.ranges_per_warp = 0;
+  d.tma_hint = -1;
+  d.ctas_per_sm = 0;
+  d.dia_kernel = -1;
+  d.dia_rows = 0;
+  d.flags = 0;
+  for (int i = 0; i < 5; ++i) d.reserved[i] = 0;
+  return c ? *c : d;
+}
+inline int cap_ctas(int per_sm, int cap) {
+  if (cap > 0 && per_sm > cap) per_sm = cap;
+  return per_sm < 1 ? 1 : per_sm;
+}
 
 inline size_t value_size(int dtype) { return dtype == SPMV_F64 ? 8 : 4; }
 inline bool valid_dtype(int dtype) { return dtype == SPMV_F32 || dtype == SPMV_F64; }

@@ -655,21 +655,29 @@ struct spmv_coo_plan {
   DevBuf sorted_ai, sorted_aj, sorted_av;  // only when the input rows were unsorted
   DevBuf run_start, run_row;
   int64_t n_runs = 0, n_long = 0, ntiles = 0, tile = 2048;
-  DevBuf head_row, tail_row, pass, head_val, tail_val;
-  DevBuf steps;
+  spmv_plan_config cfg = config_or_default(nullptr);
+  bool tma_hint = true;
+  int64_t ws_ranges_per_warp = 8;
+  // per-stream launch scratch (StreamSlots): tile boundary partials, warp-
+  // stream partials and range counter, the vla step counter
+  mutable StreamSlots scratch;
+  size_t off_head_row = 0, off_tail_row = 0, off_pass = 0, off_head_val = 0, off_tail_val = 0;
+  size_t off_ws_head = 0, off_ws_tail = 0, off_ws_ctr = 0, off_steps = 0;
+  mutable StreamSlots vla_scratch;  // two-phase vla step sums (nnz values), per stream
+  std::mutex build_mu;              // the lazily built vla lists
   int groups = 1;                // consumer groups per tile CTA (coo_tile_kernel G)
   int grid = 0, grid_direct = 0;  // G-group TMA kernel / single-group kernel
   // vla long runs (over kVlaLong entries): list, 256-entry chunk map and the
   // step-sum buffer, built on the first vla call that needs them
   bool vla_built = false;
   int64_t vla_n = 0, vla_chunks = 0;
-  DevBuf vla_runs, vla_pre, vla_chunk_run, vla_S;
+  DevBuf vla_runs, vla_pre, vla_chunk_run;
   int64_t vla_n_mid = 0;  // runs of 33..kVlaLong entries (list for coo_vla_warp_kernel)
   DevBuf vla_mid;
   // warp-stream path (wstream.cuh) for plans with long runs
   bool ws = false;
   int64_t ws_nwarps = 0, ws_nranges = 0, ws_n_span = 0;
-  DevBuf ws_bounds, ws_row0, ws_head, ws_tail, ws_ctr, ws_span_run, ws_span_w0, ws_span_w1;
+  DevBuf ws_bounds, ws_row0, ws_span_run, ws_span_w0, ws_span_w1;
 };
 
 static int coo_vla_build(spmv_coo_plan* p, cudaStream_t st) {
@@ -717,8 +725,8 @@ static int coo_vla_build(spmv_coo_plan* p, cudaStream_t st) {
     for (int64_t i = 0; i < p->vla_n; ++i) pre[i + 1] = pre[i] + h[i];
     p->vla_chunks = pre[p->vla_n];
     SPMV_CUDA_TRY(cudaMemcpyAsync(p->vla_pre.ptr, pre.data(), 4 * (p->vla_n + 1), cudaMemcpyHostToDevice, st));
-    if ((rc = p->vla_chunk_run.alloc(4 * p->vla_chunks)) || (rc = p->vla_S.alloc(value_size(p->dtype) * p->nnz)))
-      return rc;
+    if ((rc = p->vla_chunk_run.alloc(4 * p->vla_chunks))) return rc;
+    p->vla_scratch.bytes = value_size(p->dtype) * p->nnz;
     vla_run_chunk_map_kernel<<<unsigned(gi), 256, 0, st>>>(p->vla_pre.as<uint32_t>(), cnt.as<uint32_t>(), p->vla_n,
                                                             p->vla_chunk_run.as<uint32_t>());
     SPMV_LAUNCH_CHECK();
@@ -765,11 +773,10 @@ __global__ void count_long_runs_kernel(const uint32_t* __restrict__ run_start, i
 }
 
 template <typename K>
-static int coo_ctas_per_sm(K kernel, int threads, size_t smem, int* per_sm) {
+static int coo_ctas_per_sm(K kernel, int threads, size_t smem, int cap, int* per_sm) {
   SPMV_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kernel, threads, smem));
-  if (ctas_per_sm_cap() > 0 && *per_sm > ctas_per_sm_cap()) *per_sm = ctas_per_sm_cap();
-  if (*per_sm < 1) *per_sm = 1;
+  *per_sm = cap_ctas(*per_sm, cap);
   return SPMV_OK;
 }
 
@@ -777,11 +784,12 @@ template <typename T, int TILE, int G>
 static int coo_launch_config(spmv_coo_plan* p) {
   using S1 = CooSmem<T, TILE, 1>;
   int per_sm = 0, per_sm1 = 0, rc;
+  const int cta_cap = p->cfg.ctas_per_sm;
   if ((rc = coo_ctas_per_sm(coo_tile_kernel<T, true, TILE, G>, G * coo_group_threads<G>(),
-                            CooSmem<T, TILE, G>::total, &per_sm)))
+                            CooSmem<T, TILE, G>::total, cta_cap, &per_sm)))
     return rc;
-  if ((rc = coo_ctas_per_sm(coo_tile_kernel<T, true, TILE, 1>, kTileThreads, S1::total, &per_sm1))) return rc;
-  if ((rc = coo_ctas_per_sm(coo_tile_kernel<T, false, TILE, 1>, kTileThreads, S1::total, &per_sm1))) return rc;
+  if ((rc = coo_ctas_per_sm(coo_tile_kernel<T, true, TILE, 1>, kTileThreads, S1::total, cta_cap, &per_sm1))) return rc;
+  if ((rc = coo_ctas_per_sm(coo_tile_kernel<T, false, TILE, 1>, kTileThreads, S1::total, cta_cap, &per_sm1))) return rc;
   const int64_t cap = int64_t(sm_count()) * per_sm, cap1 = int64_t(sm_count()) * per_sm1;
   p->grid = int(p->ntiles < cap ? p->ntiles : cap);
   p->grid_direct = int(p->ntiles < cap1 ? p->ntiles : cap1);
@@ -789,10 +797,10 @@ static int coo_launch_config(spmv_coo_plan* p) {
 }
 
 // Warp-stream plan: entry ranges snapped to run starts (short runs stay
-// whole), split long runs listed for the fix-up.  SPMV_COO_WS=0/1 overrides
+// whole), split long runs listed for the fix-up.  spmv_plan_config.warp_stream overrides
 // the choice (plans with long runs).
 static int coo_ws_build(spmv_coo_plan* p, cudaStream_t st) {
-  const int mode = coo_ws_mode();
+  const int mode = p->cfg.warp_stream;
   p->ws = mode < 0 ? p->n_long > 0 : mode > 0;
   if (!p->ws) return SPMV_OK;
   int rc, per_sm = 0;
@@ -800,16 +808,12 @@ static int coo_ws_build(spmv_coo_plan* p, cudaStream_t st) {
     SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coo_wstream_kernel<double>, kWsWarps * 32, 0));
   else
     SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, coo_wstream_kernel<float>, kWsWarps * 32, 0));
-  if (ctas_per_sm_cap() > 0 && per_sm > ctas_per_sm_cap()) per_sm = ctas_per_sm_cap();
-  if (per_sm < 1) per_sm = 1;
+  per_sm = cap_ctas(per_sm, p->cfg.ctas_per_sm);
   p->ws_nwarps = std::max<int64_t>(1, std::min<int64_t>(int64_t(sm_count()) * per_sm * kWsWarps, p->nnz / kWsChunk));
   p->ws_nranges =
-      std::max<int64_t>(p->ws_nwarps, std::min<int64_t>(p->ws_nwarps * ws_ranges_per_warp(), p->nnz / kWsChunk));
+      std::max<int64_t>(p->ws_nwarps, std::min<int64_t>(p->ws_nwarps * p->ws_ranges_per_warp, p->nnz / kWsChunk));
   const int64_t nr = p->ws_nranges;
-  if ((rc = p->ws_bounds.alloc(4 * (nr + 1))) || (rc = p->ws_row0.alloc(4 * nr)) || (rc = p->ws_head.alloc(8 * nr)) ||
-      (rc = p->ws_tail.alloc(8 * nr)) || (rc = p->ws_ctr.alloc(8)))
-    return rc;
-  SPMV_CUDA_TRY(cudaMemsetAsync(p->ws_ctr.ptr, 0, 8, st));
+  if ((rc = p->ws_bounds.alloc(4 * (nr + 1))) || (rc = p->ws_row0.alloc(4 * nr))) return rc;
   const uint32_t* rs = p->run_start.as<uint32_t>();
   const int64_t gw = std::min<int64_t>((nr + 256) / 256, int64_t(sm_count()) * 16);
   ws_bounds_kernel<<<unsigned(gw), 256, 0, st>>>(rs, p->n_runs, p->nnz, nr, kExactLen, p->ws_bounds.as<uint32_t>(),
@@ -926,23 +930,33 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
   // GFLOP/s, Zipf 173 -> 222.
   p->tile = 1536;
   p->groups = p->n_long > 0 ? 1 : 7;
-  if (tile_entries()) {
-    p->tile = tile_entries();
+  const int t = p->cfg.tile;
+  if (t == 1024 || t == 1536 || t == 2048) {
+    p->tile = t;
     p->groups = 1;
   }
-  if (coo_groups() > 0) p->groups = coo_groups();
+  if (p->cfg.groups > 0) p->groups = p->cfg.groups;
   if (p->n_long > 0) p->groups = 1;  // multi-group kernels carry no long-row scratch
   if (!coo_config_known(p->tile, p->groups)) {
     p->groups = 1;
     if (!coo_config_known(p->tile, 1)) p->tile = 2048;
   }
   p->ntiles = (nnz + p->tile - 1) / p->tile;
+  p->tma_hint = p->cfg.tma_hint != 0;  // COO: evict_first on the matrix stream unless turned off
+  p->ws_ranges_per_warp = p->cfg.ranges_per_warp >= 1 && p->cfg.ranges_per_warp <= 64 ? p->cfg.ranges_per_warp : 8;
   if ((rc = coo_ws_build(p, st))) return rc;
   const size_t vs = value_size(p->dtype);
-  if ((rc = p->head_row.alloc(4 * p->ntiles)) || (rc = p->tail_row.alloc(4 * p->ntiles)) ||
-      (rc = p->pass.alloc(4 * p->ntiles)) || (rc = p->head_val.alloc(vs * p->ntiles)) ||
-      (rc = p->tail_val.alloc(vs * p->ntiles)))
-    return rc;
+  SlotLayout lay;
+  p->off_head_row = lay.add(4 * p->ntiles);
+  p->off_tail_row = lay.add(4 * p->ntiles);
+  p->off_pass = lay.add(4 * p->ntiles);
+  p->off_head_val = lay.add(vs * p->ntiles);
+  p->off_tail_val = lay.add(vs * p->ntiles);
+  p->off_ws_head = lay.add(8 * p->ws_nranges);
+  p->off_ws_tail = lay.add(8 * p->ws_nranges);
+  p->off_ws_ctr = lay.add(8);
+  p->off_steps = lay.add(8);
+  p->scratch.bytes = lay.total;
 #define X(TL, GR)                                                                                    \
   if (p->tile == TL && p->groups == GR)                                                             \
     return p->dtype == SPMV_F64 ? coo_launch_config<double, TL, GR>(p) : coo_launch_config<float, TL, GR>(p);
@@ -964,23 +978,26 @@ static int coo_run_tiled(const spmv_coo_plan* p, const uint32_t* ai, const uint3
     aj = p->sorted_aj.as<uint32_t>();
     av = p->sorted_av.as<T>();
   }
+  unsigned char* scr = nullptr;
+  int rc = p->scratch.get(st, reinterpret_cast<void**>(&scr));
+  if (rc) return rc;
   CooParams<T> P;
   P.ai = ai;
   P.aj = aj;
   P.av = av;
   P.x = x;
   P.y = y;
-  P.head_row = p->head_row.as<uint32_t>();
-  P.tail_row = p->tail_row.as<uint32_t>();
-  P.pass = p->pass.as<uint32_t>();
-  P.head_val = p->head_val.as<T>();
-  P.tail_val = p->tail_val.as<T>();
+  P.head_row = reinterpret_cast<uint32_t*>(scr + p->off_head_row);
+  P.tail_row = reinterpret_cast<uint32_t*>(scr + p->off_tail_row);
+  P.pass = reinterpret_cast<uint32_t*>(scr + p->off_pass);
+  P.head_val = reinterpret_cast<T*>(scr + p->off_head_val);
+  P.tail_val = reinterpret_cast<T*>(scr + p->off_tail_val);
   P.nrows = p->nrows;
   P.nnz = p->nnz;
   P.col_base = col_base;
   P.ntiles = p->ntiles;
   P.tile_begin = 0;
-  P.mode = tile_mode_flags() | (tma_hint_mode() != 0 ? 4 : 0);
+  P.mode = (p->cfg.flags & 3) | (p->tma_hint ? 4 : 0);
   P.vla = vla;
   if (p->n_runs < p->nrows) {  // empty rows exist: one memset instead of per-gap loops
     SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
@@ -1036,6 +1053,9 @@ static int coo_run_ws(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t
     aj = p->sorted_aj.as<uint32_t>();
     av = p->sorted_av.as<T>();
   }
+  unsigned char* scr = nullptr;
+  int rc = p->scratch.get(st, reinterpret_cast<void**>(&scr));
+  if (rc) return rc;
   if (p->n_runs < p->nrows) SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));  // empty rows
   CooWsParams<T> P;
   P.ai = ai;
@@ -1044,9 +1064,9 @@ static int coo_run_ws(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t
   P.x = x;
   P.y = y;
   P.bounds = p->ws_bounds.as<uint32_t>();
-  P.head = p->ws_head.as<double>();
-  P.tail = p->ws_tail.as<double>();
-  P.ctr = p->ws_ctr.as<uint32_t>();
+  P.head = reinterpret_cast<double*>(scr + p->off_ws_head);
+  P.tail = reinterpret_cast<double*>(scr + p->off_ws_tail);
+  P.ctr = reinterpret_cast<uint32_t*>(scr + p->off_ws_ctr);
   P.col_base = col_base;
   P.nwarps = p->ws_nwarps;
   P.nranges = p->ws_nranges;
@@ -1113,11 +1133,41 @@ __global__ void coo_vla_count_steps_kernel(const uint32_t* __restrict__ run_star
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(steps, c);
 }
 
+// The vla step counter of the stream's scratch slot.
+static int steps_slot(const spmv_coo_plan* p, cudaStream_t st, unsigned long long** out) {
+  unsigned char* scr = nullptr;
+  int rc = p->scratch.get(st, reinterpret_cast<void**>(&scr));
+  if (rc) return rc;
+  if (!scr) return fail(SPMV_INVALID_ARG, "COO plan without scratch");
+  *out = reinterpret_cast<unsigned long long*>(scr + p->off_steps);
+  return SPMV_OK;
+}
+
 extern "C" {
 
 int spmv_coo_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* ai,
                          const uint32_t* aj, const void* av, void* stream, spmv_coo_plan** out) {
+  return spmv_coo_plan_create_ex(dtype, nrows, ncols, nnz, ai, aj, av, nullptr, stream, out);
+}
+
+int spmv_coo_plan_config(const spmv_coo_plan* p, spmv_plan_config* out) {
+  if (!p || !out) return fail(SPMV_INVALID_ARG, "NULL argument");
+  *out = p->cfg;
+  out->tile = int32_t(p->tile);
+  out->groups = p->groups;
+  out->exact_len = kExactLen;
+  out->warp_stream = p->ws ? 1 : 0;
+  out->ranges_per_warp = int32_t(p->ws_ranges_per_warp);
+  out->tma_hint = p->tma_hint ? 1 : 0;
+  return SPMV_OK;
+}
+
+int spmv_coo_plan_create_ex(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* ai,
+                            const uint32_t* aj, const void* av, const spmv_plan_config* cfg, void* stream,
+                            spmv_coo_plan** out) {
   if (!out) return fail(SPMV_INVALID_ARG, "spmv_coo_plan_create: out is NULL");
+  if (cfg && cfg->version != SPMV_PLAN_CONFIG_VERSION)
+    return fail(SPMV_INVALID_ARG, "spmv_plan_config version %d, expected %d", cfg->version, SPMV_PLAN_CONFIG_VERSION);
   *out = nullptr;
   if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
   if (nrows < 0 || ncols < 0 || nnz < 0 || nnz > int64_t(UINT32_MAX) || nrows >= int64_t(UINT32_MAX))
@@ -1128,9 +1178,15 @@ int spmv_coo_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, c
   p->nrows = nrows;
   p->ncols = ncols;
   p->nnz = nnz;
+  p->cfg = config_or_default(cfg);
   int rc = SPMV_OK;
   if (nnz) rc = coo_plan_build(p, ai, aj, av, as_stream(stream));
-  if (!rc) rc = p->steps.alloc(sizeof(unsigned long long));
+  // the vla step counter lives in the scratch slot even without entries
+  if (!rc && !nnz) {
+    SlotLayout lay;
+    p->off_steps = lay.add(8);
+    p->scratch.bytes = lay.total;
+  }
   if (rc) {
     delete p;
     return rc;
@@ -1207,7 +1263,9 @@ int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const
     if (rc) return rc;
     if (done) {
       if (outer_steps) {
-        unsigned long long* steps = p->steps.as<unsigned long long>();
+        unsigned long long* steps = nullptr;
+        int rc2 = steps_slot(p, st, &steps);
+        if (rc2) return rc2;
         unsigned long long h = 0;
         SPMV_CUDA_TRY(cudaMemsetAsync(steps, 0, sizeof(h), st));
         const int64_t g = std::min<int64_t>((p->n_runs + 255) / 256, int64_t(sm_count()) * 16);
@@ -1226,7 +1284,12 @@ int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const
     aj = p->sorted_aj.as<uint32_t>();
     av = p->sorted_av.ptr;
   }
-  unsigned long long* steps = outer_steps ? p->steps.as<unsigned long long>() : nullptr;
+  unsigned long long* steps = nullptr;
+  if (outer_steps) {
+    int rc2 = steps_slot(p, st, &steps);
+    if (rc2) return rc2;
+  }
+  unsigned long long* steps_out = steps;
   if (steps) SPMV_CUDA_TRY(cudaMemsetAsync(steps, 0, sizeof(unsigned long long), st));
   int width = 1;
   while (width < lanes) width <<= 1;
@@ -1255,7 +1318,10 @@ int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const
     const bool split = long_runs && lanes <= 8;
     if (split) {
       int rc;
-      if (!p->vla_built && (rc = coo_vla_build(p, st))) return rc;
+      {
+        std::lock_guard<std::mutex> lock(p->build_mu);
+        if (!p->vla_built && (rc = coo_vla_build(p, st))) return rc;
+      }
       const int64_t gs = std::min<int64_t>((p->n_runs + 255) / 256, cap);
       auto short_kernel = [&](auto* tag) {
         using TT = std::remove_pointer_t<decltype(tag)>;
@@ -1292,20 +1358,25 @@ int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const
     }
     if (long_runs) {  // runs over 32 entries exist: two-phase path for those over kVlaLong
       int rc;
-      if (!p->vla_built && (rc = coo_vla_build(p, st))) return rc;
+      {
+        std::lock_guard<std::mutex> lock(p->build_mu);
+        if (!p->vla_built && (rc = coo_vla_build(p, st))) return rc;
+      }
+      void* sbuf = nullptr;
+      if (p->vla_n > 0 && (rc = p->vla_scratch.get(st, &sbuf))) return rc;
       if (p->vla_n > 0) {
         const int64_t g1 = std::min<int64_t>((p->vla_chunks * 32 + tb - 1) / tb, cap);
         const int64_t g2 = std::min<int64_t>((p->vla_n * 32 + tb - 1) / tb, cap);
         const uint32_t* runs = p->vla_runs.as<uint32_t>();
         if (p->dtype == SPMV_F64) {
-          double* S = p->vla_S.as<double>();
+          double* S = static_cast<double*>(sbuf);
           coo_vla_steps_kernel<double><<<unsigned(g1), tb, 0, st>>>(
               rs, runs, p->vla_pre.as<uint32_t>(), p->vla_chunk_run.as<uint32_t>(), p->vla_chunks, aj,
               static_cast<const double*>(av), static_cast<const double*>(x), col_base, lanes, width, S);
           coo_vla_fold_kernel<double><<<unsigned(g2), tb, 0, st>>>(rs, rr, runs, p->vla_n, S, lanes,
                                                                     static_cast<double*>(y), steps);
         } else {
-          float* S = p->vla_S.as<float>();
+          float* S = static_cast<float*>(sbuf);
           coo_vla_steps_kernel<float><<<unsigned(g1), tb, 0, st>>>(
               rs, runs, p->vla_pre.as<uint32_t>(), p->vla_chunk_run.as<uint32_t>(), p->vla_chunks, aj,
               static_cast<const float*>(av), static_cast<const float*>(x), col_base, lanes, width, S);
@@ -1331,7 +1402,7 @@ int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const
   SPMV_LAUNCH_CHECK();
   if (outer_steps) {
     unsigned long long h = 0;
-    SPMV_CUDA_TRY(cudaMemcpyAsync(&h, p->steps.ptr, sizeof(h), cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(&h, steps_out, sizeof(h), cudaMemcpyDeviceToHost, st));
     SPMV_CUDA_TRY(cudaStreamSynchronize(st));
     *outer_steps = int64_t(h);
   }

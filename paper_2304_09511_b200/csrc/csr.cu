@@ -687,8 +687,19 @@ struct spmv_csr_plan {
   int dtype = SPMV_F64;
   int64_t nrows = 0, ncols = 0, nnz = 0, ntiles = 0, tile = 2048;
   int exact_len = kExactLen;
-  int64_t n_long = 0;
-  DevBuf row_lo, head, tail, cnt;
+  spmv_plan_config cfg = config_or_default(nullptr);  // as requested (auto fields unresolved)
+  int64_t n_long = 0;     // rows over kExactLen (32): the tile kernels' long rows
+  int64_t n_long_ws = 0;  // rows over exact_len: the warp-stream kernel's split rows
+  // per-stream launch scratch: tile-span partials (head/tail), warp-stream
+  // partials and range counter (StreamSlots: concurrent streams never share)
+  mutable StreamSlots scratch;
+  size_t off_head = 0, off_tail = 0, off_ws_head = 0, off_ws_tail = 0, off_ws_ctr = 0;
+  mutable StreamSlots vla_scratch;  // two-phase vla product buffer (nnz values), per stream
+  std::mutex build_mu;              // lazily built parts (vla lists, host staging, maxcol)
+  std::mutex host_mu;               // host-pipeline calls: one enqueues at a time
+  cudaEvent_t host_done = nullptr;  // end of the last host-pipeline call (the next one waits)
+  bool tma_hint = false;
+  DevBuf row_lo, cnt;
   DevBuf span_row, span_t0, span_t1;
   int64_t n_span = 0;
   DevBuf maxcol;
@@ -702,6 +713,7 @@ struct spmv_csr_plan {
     if (h2d) cudaStreamDestroy(h2d);
     if (d2h) cudaStreamDestroy(d2h);
     for (auto e : events) cudaEventDestroy(e);
+    if (host_done) cudaEventDestroy(host_done);
   }
   int groups = 1;                    // consumer groups per tile CTA (csr_tile_kernel G)
   bool long_scratch = true;          // kernels with long-row scratch (false: plan has no long rows)
@@ -709,7 +721,7 @@ struct spmv_csr_plan {
   // a product buffer (built on the first spmv_csr_vla_planned call)
   bool vla_built = false;
   int64_t vla_n = 0, vla_chunks = 0;
-  DevBuf vla_rows, vla_pre, vla_chunk_row, vla_prod;
+  DevBuf vla_rows, vla_pre, vla_chunk_row;
   int64_t vla_n_mid = 0;  // rows of 33..kVlaLong entries (list for csr_vla_warp_kernel)
   DevBuf vla_mid;
   int grid_bulk = 0, grid_direct = 0;  // G-group TMA kernel / single-group kernel
@@ -718,7 +730,8 @@ struct spmv_csr_plan {
   bool ws = false;
   bool has_empty = false;
   int64_t ws_nwarps = 0, ws_nranges = 0, ws_n_span = 0;
-  DevBuf ws_bounds, ws_row0, ws_head, ws_tail, ws_span_row, ws_span_w0, ws_span_w1, ws_ctr;
+  int64_t ws_ranges_per_warp = 8;
+  DevBuf ws_bounds, ws_row0, ws_span_row, ws_span_w0, ws_span_w1;
 };
 
 // (tile, groups, long-row scratch) triples with compiled kernels.  The
@@ -735,11 +748,10 @@ static bool csr_config_known(int64_t tile, int groups, bool long_rows) {
 }
 
 template <typename K>
-static int csr_ctas_per_sm(K kernel, int threads, size_t smem, int* per_sm) {
+static int csr_ctas_per_sm(K kernel, int threads, size_t smem, int cap, int* per_sm) {
   SPMV_CUDA_TRY(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, int(smem)));
   SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(per_sm, kernel, threads, smem));
-  if (ctas_per_sm_cap() > 0 && *per_sm > ctas_per_sm_cap()) *per_sm = ctas_per_sm_cap();
-  if (*per_sm < 1) *per_sm = 1;
+  *per_sm = cap_ctas(*per_sm, cap);
   return SPMV_OK;
 }
 
@@ -747,11 +759,12 @@ template <typename T, int TILE, int G, bool LONG>
 static int csr_launch_config(spmv_csr_plan* p) {
   int per_sm = 0, per_sm1 = 0, rc;
   using S1 = CsrSmem<T, TILE, 1>;
+  const int cta_cap = p->cfg.ctas_per_sm;
   if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, true, TILE, G, LONG>, csr_cta_threads<G>(),
-                            CsrSmem<T, TILE, G, LONG>::total, &per_sm)))
+                            CsrSmem<T, TILE, G, LONG>::total, cta_cap, &per_sm)))
     return rc;
-  if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, true, TILE, 1>, kTileThreads, S1::total, &per_sm1))) return rc;
-  if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, false, TILE, 1>, kTileThreads, S1::total, &per_sm1))) return rc;
+  if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, true, TILE, 1>, kTileThreads, S1::total, cta_cap, &per_sm1))) return rc;
+  if ((rc = csr_ctas_per_sm(csr_tile_kernel<T, false, TILE, 1>, kTileThreads, S1::total, cta_cap, &per_sm1))) return rc;
   const int64_t cap = int64_t(sm_count()) * per_sm, cap1 = int64_t(sm_count()) * per_sm1;
   p->grid_bulk = int(p->ntiles < cap ? p->ntiles : cap);
   p->grid_direct = int(p->ntiles < cap1 ? p->ntiles : cap1);
@@ -767,6 +780,9 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
     SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
     return SPMV_OK;
   }
+  unsigned char* scr = nullptr;
+  int rc = p->scratch.get(st, reinterpret_cast<void**>(&scr));
+  if (rc) return rc;
   CsrParams<T> P;
   P.irp = irp;
   P.aj = aj;
@@ -774,19 +790,19 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
   P.x = x;
   P.y = y;
   P.row_lo = p->row_lo.as<uint32_t>();
-  P.head = p->head.as<T>();
-  P.tail = p->tail.as<T>();
+  P.head = reinterpret_cast<T*>(scr + p->off_head);
+  P.tail = reinterpret_cast<T*>(scr + p->off_tail);
   P.nrows = p->nrows;
   P.nnz = p->nnz;
   P.col_base = col_base;
   P.ntiles = p->ntiles;
   P.tile_begin = tb;
   P.tile_end = te;
-  P.exact_len = p->exact_len;
+  P.exact_len = kExactLen;  // tile kernels: the tile extension and long-row scratch are sized for 32
   P.vla = vla;
   P.y_split = y_split;
   P.y_gap = y_gap;
-  P.mode = tile_mode_flags() | ((tma_hint_mode() < 0 ? p->n_long > 0 : tma_hint_mode() > 0) ? 4 : 0);
+  P.mode = (p->cfg.flags & 3) | (p->tma_hint ? 4 : 0);
   const bool aligned = (reinterpret_cast<uintptr_t>(aj) % 16 == 0) && (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
   const size_t smem1 = CsrSmem<T, TILE, 1>::total;
@@ -837,6 +853,9 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
 template <typename T>
 static int csr_run_ws(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
                       int64_t col_base, T* y, cudaStream_t st) {
+  unsigned char* scr = nullptr;
+  int rc = p->scratch.get(st, reinterpret_cast<void**>(&scr));
+  if (rc) return rc;
   if (p->has_empty) SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
   WsParams<T> P;
   P.irp = irp;
@@ -846,14 +865,14 @@ static int csr_run_ws(const spmv_csr_plan* p, const uint32_t* irp, const uint32_
   P.y = y;
   P.bounds = p->ws_bounds.as<uint32_t>();
   P.row0 = p->ws_row0.as<uint32_t>();
-  P.head = p->ws_head.as<double>();
-  P.tail = p->ws_tail.as<double>();
+  P.head = reinterpret_cast<double*>(scr + p->off_ws_head);
+  P.tail = reinterpret_cast<double*>(scr + p->off_ws_tail);
   P.exact_len = uint32_t(p->exact_len);
   P.nrows = p->nrows;
   P.col_base = col_base;
   P.nwarps = p->ws_nwarps;
   P.nranges = p->ws_nranges;
-  P.ctr = p->ws_ctr.as<uint32_t>();
+  P.ctr = reinterpret_cast<uint32_t*>(scr + p->off_ws_ctr);
   const int64_t grid = (p->ws_nwarps + kWsWarps - 1) / kWsWarps;
   csr_wstream_kernel<T><<<unsigned(grid), kWsWarps * 32, 0, st>>>(P);
   SPMV_LAUNCH_CHECK();
@@ -913,7 +932,9 @@ static int csr_run_vla_tiles(const spmv_csr_plan* p, const uint32_t* irp, const 
 // spmv_csr_host in the header).
 static int csr_host_prepare(spmv_csr_plan* p, const uint32_t* aj, int chunks, cudaStream_t st) {
   if (p->h_row_lo.empty()) {
+    std::lock_guard<std::mutex> lock(p->build_mu);  // maxcol is shared with spmv_csr_plan_tile_info
     int rc;
+    if (!p->host_done) SPMV_CUDA_TRY(cudaEventCreateWithFlags(&p->host_done, cudaEventDisableTiming));
     if (!p->maxcol.ptr) {
       if ((rc = p->maxcol.alloc(4 * p->ntiles))) return rc;
       const int64_t g = std::min<int64_t>(p->ntiles, int64_t(sm_count()) * 8);
@@ -986,8 +1007,14 @@ struct HostTrace {
 template <typename T>
 static int csr_host_run(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* xh, T* yh,
                         int chunks, cudaStream_t st) {
+  // One call enqueues at a time; the device staging (xd, yd) and the copy
+  // streams are the plan's, so each call's work waits for the previous
+  // call's end (host_done) — calls from several threads or streams on one
+  // plan are serialised on the device, never interleaved.
+  std::lock_guard<std::mutex> lock(p->host_mu);
   int rc = csr_host_prepare(p, aj, chunks, st);
   if (rc) return rc;
+  SPMV_CUDA_TRY(cudaStreamWaitEvent(st, p->host_done, 0));
   HostTrace tr;
   T* xd = p->xd.as<T>();
   T* yd = p->yd.as<T>();
@@ -1063,6 +1090,7 @@ static int csr_host_run(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* a
   }
   SPMV_CUDA_TRY(cudaEventRecord(ev[2 * nx + 1], p->d2h));
   SPMV_CUDA_TRY(cudaStreamWaitEvent(st, ev[2 * nx + 1], 0));
+  SPMV_CUDA_TRY(cudaEventRecord(p->host_done, st));
   tr.mark('e', st);
   tr.dump(st);
   return SPMV_OK;
@@ -1075,10 +1103,10 @@ static int count_async(unsigned long long* dev, unsigned long long* host, cudaSt
 }
 
 // Warp-stream plan (wstream.cuh): chosen for matrices with long rows
-// (SPMV_CSR_WS=0 / 1 overrides).  One range per resident warp.
+// (spmv_plan_config.warp_stream overrides).  One range per resident warp.
 static int csr_ws_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st) {
-  const int mode = csr_ws_mode();
-  p->ws = mode < 0 ? p->n_long > 0 : mode > 0;
+  const int mode = p->cfg.warp_stream;
+  p->ws = mode < 0 ? p->n_long_ws > 0 : mode > 0;
   if (!p->ws) return SPMV_OK;
   int rc, per_sm = 0;
   unsigned long long* ctr = p->cnt.as<unsigned long long>();
@@ -1093,19 +1121,16 @@ static int csr_ws_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st) 
     SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_wstream_kernel<double>, kWsWarps * 32, 0));
   else
     SPMV_CUDA_TRY(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, csr_wstream_kernel<float>, kWsWarps * 32, 0));
-  if (ctas_per_sm_cap() > 0 && per_sm > ctas_per_sm_cap()) per_sm = ctas_per_sm_cap();
-  if (per_sm < 1) per_sm = 1;
+  per_sm = cap_ctas(per_sm, p->cfg.ctas_per_sm);
   // at least one chunk per warp: targets strictly increase, so no empty
   // range sits inside a split row
   // ranges: kWsRangesPerWarp per resident warp (dynamic hand-out evens out
   // uneven row work), at least one chunk each
   p->ws_nwarps = std::max<int64_t>(1, std::min<int64_t>(int64_t(sm_count()) * per_sm * kWsWarps, p->nnz / kWsChunk));
-  p->ws_nranges = std::max<int64_t>(p->ws_nwarps, std::min<int64_t>(p->ws_nwarps * ws_ranges_per_warp(), p->nnz / kWsChunk));
+  p->ws_nranges =
+      std::max<int64_t>(p->ws_nwarps, std::min<int64_t>(p->ws_nwarps * p->ws_ranges_per_warp, p->nnz / kWsChunk));
   const int64_t nr = p->ws_nranges;
-  if ((rc = p->ws_bounds.alloc(4 * (nr + 1))) || (rc = p->ws_row0.alloc(4 * nr)) ||
-      (rc = p->ws_head.alloc(8 * nr)) || (rc = p->ws_tail.alloc(8 * nr)) || (rc = p->ws_ctr.alloc(8)))
-    return rc;
-  SPMV_CUDA_TRY(cudaMemsetAsync(p->ws_ctr.ptr, 0, 8, st));
+  if ((rc = p->ws_bounds.alloc(4 * (nr + 1))) || (rc = p->ws_row0.alloc(4 * nr))) return rc;
   const int64_t gw = std::min<int64_t>((nr + 256) / 256, int64_t(sm_count()) * 16);
   ws_bounds_kernel<<<unsigned(gw), 256, 0, st>>>(irp, p->nrows, p->nnz, nr, p->exact_len,
                                                  p->ws_bounds.as<uint32_t>(), p->ws_row0.as<uint32_t>());
@@ -1139,10 +1164,18 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
   int rc;
   const int64_t g_rows = std::min<int64_t>((nrows + 255) / 256, int64_t(sm_count()) * 16);
   SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
-  count_long_rows_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, p->exact_len, ctr);
+  count_long_rows_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, kExactLen, ctr);
   SPMV_LAUNCH_CHECK();
   if ((rc = count_async(ctr, &h, st))) return rc;
   p->n_long = int64_t(h);
+  p->n_long_ws = p->n_long;
+  if (p->exact_len < kExactLen) {  // the warp-stream kernel's threshold
+    SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
+    count_long_rows_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, p->exact_len, ctr);
+    SPMV_LAUNCH_CHECK();
+    if ((rc = count_async(ctr, &h, st))) return rc;
+    p->n_long_ws = int64_t(h);
+  }
   // Long rows: 1024-entry tiles, 3 groups (2 CTAs/SM: six tiles in flight
   // hide the long-row gathers).  Otherwise G consumer groups share a G + 1
   // stage ring of kernels without long-row scratch, sized per row length
@@ -1161,11 +1194,12 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
     p->tile = p->nnz >= (int64_t(64) << 20) ? 2304 : 2048;
     p->groups = 3;
   }
-  if (tile_entries()) {
-    p->tile = tile_entries();
+  const int t = p->cfg.tile;
+  if (t == 1024 || t == 1664 || t == 2048 || t == 2304 || t == 4096) {
+    p->tile = t;
     p->groups = 1;
   }
-  if (csr_groups() > 0) p->groups = csr_groups();
+  if (p->cfg.groups > 0) p->groups = p->cfg.groups;
   p->long_scratch = p->n_long > 0;
   if (!csr_config_known(p->tile, p->groups, p->long_scratch)) {
     p->long_scratch = true;  // the kernels with long-row scratch serve any matrix
@@ -1175,17 +1209,17 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
     }
   }
   p->ntiles = (p->nnz + p->tile - 1) / p->tile;
+  p->tma_hint = p->cfg.tma_hint < 0 ? p->n_long > 0 : p->cfg.tma_hint > 0;
+  p->ws_ranges_per_warp = p->cfg.ranges_per_warp >= 1 && p->cfg.ranges_per_warp <= 64 ? p->cfg.ranges_per_warp : 8;
   const size_t vs = value_size(p->dtype);
-  if ((rc = p->row_lo.alloc(4 * (p->ntiles + 1))) || (rc = p->head.alloc(vs * p->ntiles)) ||
-      (rc = p->tail.alloc(vs * p->ntiles)))
-    return rc;
+  if ((rc = p->row_lo.alloc(4 * (p->ntiles + 1)))) return rc;
   const int64_t g_tiles = std::min<int64_t>((p->ntiles + 256) / 256, int64_t(sm_count()) * 16);
   csr_row_lo_kernel<<<unsigned(g_tiles), 256, 0, st>>>(irp, nrows, p->ntiles, p->tile, p->row_lo.as<uint32_t>());
   SPMV_LAUNCH_CHECK();
   if (p->n_long > 0) {
     // two passes: count, then fill (order is irrelevant: rows are independent)
     SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
-    csr_span_list_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, p->exact_len, p->tile, nullptr, nullptr,
+    csr_span_list_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, kExactLen, p->tile, nullptr, nullptr,
                                                              nullptr, ctr);
     SPMV_LAUNCH_CHECK();
     if ((rc = count_async(ctr, &h, st))) return rc;
@@ -1195,13 +1229,20 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
           (rc = p->span_t1.alloc(4 * p->n_span)))
         return rc;
       SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
-      csr_span_list_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, p->exact_len, p->tile,
+      csr_span_list_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, kExactLen, p->tile,
                                                                p->span_row.as<uint32_t>(), p->span_t0.as<uint32_t>(),
                                                                p->span_t1.as<uint32_t>(), ctr);
       SPMV_LAUNCH_CHECK();
     }
   }
   if ((rc = csr_ws_build(p, irp, st))) return rc;
+  SlotLayout lay;  // per-stream launch scratch
+  p->off_head = lay.add(vs * p->ntiles);
+  p->off_tail = lay.add(vs * p->ntiles);
+  p->off_ws_head = lay.add(8 * p->ws_nranges);
+  p->off_ws_tail = lay.add(8 * p->ws_nranges);
+  p->off_ws_ctr = lay.add(8);
+  p->scratch.bytes = lay.total;
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
 #define X(TL, GR, LF)                                                                      \
   if (p->tile == TL && p->groups == GR && p->long_scratch == bool(LF))                        \
@@ -1239,7 +1280,29 @@ extern "C" {
 
 int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* row_pointers,
                          int exact_len, void* stream, spmv_csr_plan** out) {
+  spmv_plan_config cfg = config_or_default(nullptr);
+  cfg.exact_len = exact_len;
+  return spmv_csr_plan_create_ex(dtype, nrows, ncols, nnz, row_pointers, &cfg, stream, out);
+}
+
+int spmv_csr_plan_config(const spmv_csr_plan* p, spmv_plan_config* out) {
+  if (!p || !out) return fail(SPMV_INVALID_ARG, "NULL argument");
+  *out = p->cfg;
+  out->tile = int32_t(p->tile);
+  out->groups = p->groups;
+  out->exact_len = p->exact_len;
+  out->warp_stream = p->ws ? 1 : 0;
+  out->ranges_per_warp = int32_t(p->ws_ranges_per_warp);
+  out->tma_hint = p->tma_hint ? 1 : 0;
+  return SPMV_OK;
+}
+
+int spmv_csr_plan_create_ex(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* row_pointers,
+                            const spmv_plan_config* cfg, void* stream, spmv_csr_plan** out) {
   if (!out) return fail(SPMV_INVALID_ARG, "spmv_csr_plan_create: out is NULL");
+  if (cfg && cfg->version != SPMV_PLAN_CONFIG_VERSION)
+    return fail(SPMV_INVALID_ARG, "spmv_plan_config version %d, expected %d", cfg->version, SPMV_PLAN_CONFIG_VERSION);
+  int exact_len = cfg ? cfg->exact_len : 0;
   *out = nullptr;
   if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
   if (nrows < 0 || ncols < 0 || nnz < 0 || nnz > int64_t(UINT32_MAX) || nrows >= int64_t(UINT32_MAX))
@@ -1254,6 +1317,7 @@ int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, c
   p->ncols = ncols;
   p->nnz = nnz;
   p->exact_len = exact_len;
+  p->cfg = config_or_default(cfg);
   int rc = p->cnt.alloc(8);  // scratch counter
   if (!rc && nrows > 0 && nnz > 0) rc = csr_plan_build(p, row_pointers, st);
   if (rc) {
@@ -1285,7 +1349,7 @@ int spmv_csr_plan_destroy(spmv_csr_plan* plan) {
 
 int spmv_csr_plan_info(const spmv_csr_plan* p, int64_t* n_long_rows, int64_t* n_items, int64_t* launches) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
-  if (n_long_rows) *n_long_rows = p->n_long;
+  if (n_long_rows) *n_long_rows = p->n_long_ws;
   if (n_items) *n_items = p->tile;
   if (launches && p->ws)
     *launches = 1 + (p->ws_n_span > 0 ? 1 : 0);
@@ -1320,6 +1384,7 @@ int spmv_csr_plan_tile_info(spmv_csr_plan* p, const uint32_t* aj, uint32_t* row_
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (p->ntiles == 0) return SPMV_OK;
   cudaStream_t st = as_stream(stream);
+  std::lock_guard<std::mutex> lock(p->build_mu);
   if (!p->maxcol.ptr) {
     int rc = p->maxcol.alloc(4 * p->ntiles);
     if (rc) return rc;
@@ -1445,8 +1510,8 @@ static int csr_vla_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st)
     for (int64_t i = 0; i < p->vla_n; ++i) pre[i + 1] = pre[i] + h[i];
     p->vla_chunks = pre[p->vla_n];
     SPMV_CUDA_TRY(cudaMemcpyAsync(p->vla_pre.ptr, pre.data(), 4 * (p->vla_n + 1), cudaMemcpyHostToDevice, st));
-    if ((rc = p->vla_chunk_row.alloc(4 * p->vla_chunks)) || (rc = p->vla_prod.alloc(value_size(p->dtype) * p->nnz)))
-      return rc;
+    if ((rc = p->vla_chunk_row.alloc(4 * p->vla_chunks))) return rc;
+    p->vla_scratch.bytes = value_size(p->dtype) * p->nnz;  // product buffer, one per stream
     vla_chunk_row_kernel<<<unsigned(gi), 256, 0, st>>>(p->vla_pre.as<uint32_t>(), cnt.as<uint32_t>(), p->vla_n,
                                                         p->vla_chunk_row.as<uint32_t>());
     SPMV_LAUNCH_CHECK();
@@ -1565,7 +1630,10 @@ int spmv_csr_vla_planned(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* 
     return csr_vla_launch(p->dtype, p->nrows, p->nnz, irp, aj, av, x, col_base, x_len, y, lanes, long_rows ? 1 : 0,
                           st);
   int rc;
-  if (!p->vla_built && (rc = csr_vla_build(p, irp, st))) return rc;
+  {
+    std::lock_guard<std::mutex> lock(p->build_mu);
+    if (!p->vla_built && (rc = csr_vla_build(p, irp, st))) return rc;
+  }
   if (lanes <= 8) {
     // rows <= 32: one thread per row (all logical lanes in registers);
     // rows of 33..kVlaLong: sub-warp groups over the plan's list; longer:
@@ -1588,15 +1656,17 @@ int spmv_csr_vla_planned(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* 
   const int64_t g1 = std::min<int64_t>((p->vla_chunks * 32 + 255) / 256, cap);
   const int64_t g2 = std::min<int64_t>((p->vla_n * 32 + 255) / 256, cap);
   const uint32_t* rows = p->vla_rows.as<uint32_t>();
+  void* prod = nullptr;
+  if ((rc = p->vla_scratch.get(st, &prod))) return rc;
   if (p->dtype == SPMV_F64) {
-    double* P = p->vla_prod.as<double>();
+    double* P = static_cast<double*>(prod);
     csr_vla_products_kernel<double><<<unsigned(g1), 256, 0, st>>>(
         irp, aj, static_cast<const double*>(av), static_cast<const double*>(x), col_base, rows,
         p->vla_pre.as<uint32_t>(), p->vla_chunk_row.as<uint32_t>(), p->vla_chunks, P);
     csr_vla_fold_kernel<double><<<unsigned(g2), 256, 0, st>>>(irp, rows, p->vla_n, P, static_cast<double*>(y),
                                                                lanes, width);
   } else {
-    float* P = p->vla_prod.as<float>();
+    float* P = static_cast<float*>(prod);
     csr_vla_products_kernel<float><<<unsigned(g1), 256, 0, st>>>(
         irp, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base, rows,
         p->vla_pre.as<uint32_t>(), p->vla_chunk_row.as<uint32_t>(), p->vla_chunks, P);

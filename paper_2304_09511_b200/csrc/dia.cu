@@ -25,8 +25,6 @@
 
 namespace spmv {
 
-int dia_rows_per_tile();
-int dia_config();
 
 template <int G_, int S_, int NT_>
 struct DiaCfg {
@@ -175,7 +173,7 @@ dia_direct_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offset
 template <typename T>
 static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_rows, const int32_t* offsets,
                       const T* vals, const T* x, int64_t row_base, int64_t col_base, T* y, cudaStream_t st,
-                      int64_t split = -1, int64_t gap = 0) {
+                      int64_t split = -1, int64_t gap = 0, const spmv_plan_config* pc = nullptr) {
   if (nrows == 0) return SPMV_OK;
   const bool gapped = split >= 0;
   const int sms = sm_count();
@@ -184,32 +182,33 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
   // fewer rows (a multiple of 8).  Measured: 256-row tiles beat 512-row
   // tiles by 43% on 11 diagonals (more CTAs per SM, one row per thread).
   // Kernel configuration (groups G, stages S, threads per group NT; one row
-  // per thread): SPMV_DIA_CFG, else 3 groups over 4 stages — 256-row
+  // per thread): spmv_plan_config.dia_kernel, else 3 groups over 4 stages — 256-row
   // stages when a stage holds more than 40 KB (e.g. 27 diagonals: one CTA
   // per SM, 768 rows computing), else 128-row stages (several CTAs per SM).
   // Measured on B200: 27-pt stencil 1287 -> 1610 GFLOP/s, 11-diagonal
   // banded 1225 -> 1398 against one group with a double buffer.
   static constexpr int kCfgStages[5] = {2, 3, 4, 4, 8};
   static constexpr int kCfgThreads[5] = {256, 256, 128, 256, 128};
-  int cfg = dia_config();
+  const spmv_plan_config C = config_or_default(pc);
+  int cfg = C.dia_kernel;
   if (cfg < 0 || cfg > 4) cfg = row_bytes * 256 > 40960 ? 3 : 2;
   const int nt = kCfgThreads[cfg], nstage = kCfgStages[cfg];
   // rows per stage: NT, or fewer (a multiple of 8) so that S stages fit
   const size_t budget = (size_t(227) * 1024 - 1024 - 128 - ((size_t(nd) * 4 + 127) & ~size_t(127))) / nstage;
   int64_t R = int64_t(budget / (row_bytes ? row_bytes : 1)) / 8 * 8;
   if (R > nt) R = nt;
-  if (dia_rows_per_tile() >= 8 && dia_rows_per_tile() / 8 * 8 <= R) R = dia_rows_per_tile() / 8 * 8;
+  if (C.dia_rows >= 8 && C.dia_rows / 8 * 8 <= R) R = C.dia_rows / 8 * 8;
   const bool aligned = (reinterpret_cast<uintptr_t>(vals) % 16 == 0) && ((R * row_bytes) % 16 == 0) &&
                        ((avail_rows * row_bytes) % 16 == 0);
   const bool use_bulk = nd > 0 && nd <= kMaxSmemOffsets && R >= 8 && aligned;
   if (gapped && (!use_bulk || split % R != 0 || (gap * int64_t(row_bytes)) % 16 != 0)) {
     // the split is not on this block's row-tile boundary (R depends on the
     // diagonal count and dtype): the two blocks as two plain launches
-    int rc = dia_launch<T>(split, ncols, nd, avail_rows + gap, offsets, vals, x, row_base, col_base, y, st);
+    int rc = dia_launch<T>(split, ncols, nd, avail_rows + gap, offsets, vals, x, row_base, col_base, y, st, -1, 0, pc);
     if (rc || nrows == split) return rc;
     const int64_t s1 = split + gap;  // slab row of launch row `split`
     return dia_launch<T>(nrows - split, ncols, nd, avail_rows - split, offsets, vals + s1 * nd, x, row_base + s1,
-                         col_base, y + s1, st);
+                         col_base, y + s1, st, -1, 0, pc);
   }
   if (!use_bulk) {
     int64_t grid = (nrows + kDiaThreads - 1) / kDiaThreads;
@@ -250,6 +249,7 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
       }
     }
     if (per_sm < 1) return fail(SPMV_UNSUPPORTED, "DIA tile of %u bytes x %d stages does not fit", stage_bytes, stages);
+    per_sm = cap_ctas(per_sm, C.ctas_per_sm);
     int64_t grid = int64_t(sms) * per_sm;
     if (grid > ntiles) grid = ntiles;
     kernel<<<unsigned(grid), threads, smem, st>>>(vals, offsets, int(nd), x, y, nrows, avail_rows, ncols, row_base,
@@ -314,6 +314,15 @@ extern "C" int spmv_dia_gapped(int dtype, int64_t nrows, int64_t ncols, int64_t 
 extern "C" int spmv_dia(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags, int64_t avail_rows,
                         const int32_t* offsets, const void* values, const void* x, int64_t row_base,
                         int64_t col_base, int64_t x_len, void* y, void* stream) {
+  return spmv_dia_ex(dtype, nrows, ncols, ndiags, avail_rows, offsets, values, x, row_base, col_base, x_len, y,
+                     nullptr, stream);
+}
+
+extern "C" int spmv_dia_ex(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags, int64_t avail_rows,
+                           const int32_t* offsets, const void* values, const void* x, int64_t row_base,
+                           int64_t col_base, int64_t x_len, void* y, const spmv_plan_config* cfg, void* stream) {
+  if (cfg && cfg->version != SPMV_PLAN_CONFIG_VERSION)
+    return fail(SPMV_INVALID_ARG, "spmv_plan_config version %d, expected %d", cfg->version, SPMV_PLAN_CONFIG_VERSION);
   if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
   if (nrows < 0 || ncols < 0 || ndiags < 0 || avail_rows < nrows || row_base < 0 || col_base < 0 || x_len < 0)
     return fail(SPMV_INVALID_ARG, "bad DIA sizes");
@@ -327,7 +336,8 @@ extern "C" int spmv_dia(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags,
   if (!offsets || !values || !x) return fail(SPMV_INVALID_ARG, "NULL pointer");
   if (dtype == SPMV_F64)
     return dia_launch<double>(nrows, ncols, ndiags, avail_rows, offsets, static_cast<const double*>(values),
-                              static_cast<const double*>(x), row_base, col_base, static_cast<double*>(y), st);
+                              static_cast<const double*>(x), row_base, col_base, static_cast<double*>(y), st, -1, 0,
+                              cfg);
   return dia_launch<float>(nrows, ncols, ndiags, avail_rows, offsets, static_cast<const float*>(values),
-                           static_cast<const float*>(x), row_base, col_base, static_cast<float*>(y), st);
+                           static_cast<const float*>(x), row_base, col_base, static_cast<float*>(y), st, -1, 0, cfg);
 }

@@ -20,18 +20,6 @@ constexpr uint32_t kNoRow = 0xffffffffu;
 template <int TILE>
 constexpr int max_long_segs() { return TILE / (kExactLen + 1) + 4; }
 
-// Tile size used by the plans (entries).  1024 keeps more CTAs resident per
-// SM (smaller shared-memory ring); 2048 halves the per-tile overhead.
-int tile_entries();
-int ctas_per_sm_cap();  // 0 = occupancy limit
-int csr_groups();       // SPMV_CSR_GROUPS: 0 = plan choice
-int coo_groups();       // SPMV_COO_GROUPS: 0 = plan choice
-int tma_hint_mode();    // SPMV_TMA_HINT: -1 auto, 0 off, 1 on
-int tile_mode_flags();
-int csr_ws_mode();      // SPMV_CSR_WS: -1 plan choice, 0 off, 1 on
-int coo_ws_mode();      // SPMV_COO_WS: -1 plan choice, 0 off, 1 on
-int ws_ranges_per_warp();  // SPMV_WS_RANGES: entry ranges per resident warp  // experiments: bit0 no products mode, bit1 warp-per-segment long rows
-
 static_assert(kExt == kExactLen, "extension must cover a whole short row");
 
 // A consumer group of NT threads inside a tile CTA.  The single-group

@@ -31,6 +31,7 @@ from . import _lib
 from .errors import DimensionMismatch, UnsortedInput, UnsupportedCombination
 from .formats import CooMatrix, CsrMatrix, DiaMatrix, Format, as_container, as_device
 from .lanes import LaneConfig
+from .planconfig import PlanConfig, _CPlanConfig, plan_config_of
 
 
 class KernelVersion(str, Enum):
@@ -100,9 +101,16 @@ def _finish(y: torch.Tensor, origin: str, out=None):
 class _Plan:
     """Owns a C plan handle; destroyed with the container's plan cache."""
 
-    def __init__(self, kind: str, handle: ctypes.c_void_p):
+    def __init__(self, kind: str, handle: ctypes.c_void_p, config: PlanConfig | None = None):
         self.kind = kind
         self.handle = handle
+        self.requested = config or PlanConfig()
+
+    def config(self) -> PlanConfig:
+        """The configuration the plan resolved (what its kernels run)."""
+        c = _CPlanConfig()
+        _lib.call(f"spmv_{self.kind}_plan_config", self.handle, ctypes.byref(c))
+        return PlanConfig.from_c(c)
 
     def __del__(self):
         try:
@@ -120,7 +128,8 @@ class _Plan:
             _lib.call("spmv_csr_plan_groups", self.handle, ctypes.byref(g))
             ws, nw = ctypes.c_int(), ctypes.c_int64()
             _lib.call("spmv_csr_plan_path", self.handle, ctypes.byref(ws), ctypes.byref(nw))
-            info = {"long_rows": a.value, "tile": b.value, "launches": c.value, "groups": g.value, "kernel": "tile"}
+            info = {"long_rows": a.value, "tile": b.value, "launches": c.value, "groups": g.value, "kernel": "tile",
+                    "config": self.config().as_dict()}
             if ws.value:  # tile/groups still serve tile-range launches
                 info.update(kernel="warp_stream", warps=nw.value)
             return info
@@ -132,34 +141,48 @@ class _Plan:
         ws, nw = ctypes.c_int(), ctypes.c_int64()
         _lib.call("spmv_coo_plan_path", self.handle, ctypes.byref(ws), ctypes.byref(nw))
         info = {"runs": a.value, "long_runs": b.value, "tile": c.value, "row_sorted": bool(d.value),
-                "launches": e.value, "groups": g.value, "kernel": "tile"}
+                "launches": e.value, "groups": g.value, "kernel": "tile", "config": self.config().as_dict()}
         if ws.value:
             info.update(kernel="warp_stream", warps=nw.value)
         return info
 
 
-def csr_plan(A: CsrMatrix, exact_len: int = 0) -> _Plan:
-    """CSR plan: long-row work list from the row-length histogram (cached)."""
+def _config(A, config: PlanConfig | None, exact_len: int = 0) -> PlanConfig:
+    cfg = config if config is not None else plan_config_of(A)
+    if exact_len:
+        cfg = cfg.with_(exact_len=int(exact_len))
+    return cfg
+
+
+def csr_plan(A: CsrMatrix, exact_len: int = 0, config: PlanConfig | None = None) -> _Plan:
+    """CSR plan: long-row work list from the row-length histogram (cached
+    per configuration: the container's attached one unless `config`)."""
+    cfg = _config(A, config, exact_len)
 
     def make():
         h = ctypes.c_void_p()
-        _lib.call("spmv_csr_plan_create", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.nnz,
-                  _ptr(A.row_pointers), int(exact_len), _stream(A.device), ctypes.byref(h))
-        return _Plan("csr", h)
+        c = cfg.to_c()
+        _lib.call("spmv_csr_plan_create_ex", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.nnz,
+                  _ptr(A.row_pointers), ctypes.byref(c), _stream(A.device), ctypes.byref(h))
+        return _Plan("csr", h, cfg)
 
-    return A.plan(("csr", exact_len), make)
+    return A.plan(("csr", cfg.key()), make)
 
 
-def coo_plan(A: CooMatrix) -> _Plan:
-    """COO plan: row-order check, optional stable row sort, run table (cached)."""
+def coo_plan(A: CooMatrix, config: PlanConfig | None = None) -> _Plan:
+    """COO plan: row-order check, optional stable row sort, run table (cached
+    per configuration)."""
+    cfg = _config(A, config)
 
     def make():
         h = ctypes.c_void_p()
-        _lib.call("spmv_coo_plan_create", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.nnz,
-                  _ptr(A.row_indices), _ptr(A.col_indices), _ptr(A.values), _stream(A.device), ctypes.byref(h))
-        return _Plan("coo", h)
+        c = cfg.to_c()
+        _lib.call("spmv_coo_plan_create_ex", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.nnz,
+                  _ptr(A.row_indices), _ptr(A.col_indices), _ptr(A.values), ctypes.byref(c), _stream(A.device),
+                  ctypes.byref(h))
+        return _Plan("coo", h, cfg)
 
-    return A.plan("coo", make)
+    return A.plan(("coo", cfg.key()), make)
 
 
 # --------------------------------------------------------- host pipelining --
@@ -292,24 +315,26 @@ def _host_pipeline_ok(A, x, out) -> bool:
 
 
 # ------------------------------------------------------------------ kernels --
-def spmv_coo_plain(A, x, out=None):
-    """``y = A @ x`` with np.add.at semantics (kernels.py:56-66)."""
+def spmv_coo_plain(A, x, out=None, plan_config: PlanConfig | None = None):
+    """``y = A @ x`` with np.add.at semantics (kernels.py:56-66).
+    `plan_config` overrides the container's kernel configuration."""
     A = as_device(A)
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
-        p = coo_plan(A)
+        p = coo_plan(A, plan_config)
         _lib.call("spmv_coo", p.handle, _ptr(A.row_indices), _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0,
                   A.ncols, _ptr(y), _stream(A.device))
     return _finish(y, origin, out)
 
 
-def spmv_csr_plain(A, x, out=None):
-    """``y = A @ x`` with one left-to-right sum per row (kernels.py:69-82)."""
+def spmv_csr_plain(A, x, out=None, plan_config: PlanConfig | None = None):
+    """``y = A @ x`` with one left-to-right sum per row (kernels.py:69-82).
+    `plan_config` overrides the container's kernel configuration."""
     A = as_device(A)
     if _host_pipeline_ok(A, x, out):
         # host x -> host y: the C ABI pipelines upload / tiles / download
-        p = csr_plan(A)
+        p = csr_plan(A, config=plan_config)
         _lib.call("spmv_csr_host", p.handle, _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values),
                   x.data_ptr(), out.data_ptr(), HOST_CHUNKS, _stream(A.device))
         torch.cuda.current_stream(A.device).synchronize()
@@ -317,22 +342,25 @@ def spmv_csr_plain(A, x, out=None):
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
-        p = csr_plan(A)
+        p = csr_plan(A, config=plan_config)
         _lib.call("spmv_csr", p.handle, _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0,
                   A.ncols, _ptr(y), _stream(A.device))
     return _finish(y, origin, out)
 
 
-def spmv_dia_plain(A, x, out=None):
-    """``y = A @ x`` over stored diagonals (kernels.py:85-101)."""
+def spmv_dia_plain(A, x, out=None, plan_config: PlanConfig | None = None):
+    """``y = A @ x`` over stored diagonals (kernels.py:85-101).
+    `plan_config` (its dia_* fields) overrides the container's."""
     A = as_device(A)
     if _host_pipeline_ok(A, x, out) and A.ndiags > 0:
         return _dia_pipelined(A, x, out)
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
-        _lib.call("spmv_dia", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.ndiags, A.padded_rows,
-                  _ptr(A.offsets), _ptr(A.values), _ptr(xv), 0, 0, A.ncols, _ptr(y), _stream(A.device))
+        c = (plan_config if plan_config is not None else plan_config_of(A)).to_c()
+        _lib.call("spmv_dia_ex", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.ndiags, A.padded_rows,
+                  _ptr(A.offsets), _ptr(A.values), _ptr(xv), 0, 0, A.ncols, _ptr(y), ctypes.byref(c),
+                  _stream(A.device))
     return _finish(y, origin, out)
 
 

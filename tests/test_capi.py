@@ -46,7 +46,7 @@ def test_python_binding_matches_header(lib_built):
     from paper_2304_09511_b200 import _lib
     assert set(_lib.SIGNATURES) == set(declared_functions())
     lib = _lib.load()
-    assert lib.spmv_abi_version() == 1
+    assert lib.spmv_abi_version() == 2
 
 
 def test_status_codes_map_to_reference_errors(lib_built):
@@ -67,3 +67,19 @@ def test_status_codes_map_to_reference_errors(lib_built):
     from paper_2304_09511_b200.errors import UnsupportedCombination
     with pytest.raises(UnsupportedCombination):
         _lib.call("spmv_csr_vla", 1, 4, 4, 0, None, None, None, None, 0, 4, None, 2048, None)
+
+
+def test_plan_config_struct_matches_header(lib_built):
+    """ctypes layout of spmv_plan_config == the C struct (16 int32 fields),
+    and spmv_plan_config_init fills the auto values PlanConfig() holds."""
+    import ctypes
+
+    from paper_2304_09511_b200 import _lib
+    from paper_2304_09511_b200.planconfig import VERSION, PlanConfig, _CPlanConfig
+    assert ctypes.sizeof(_CPlanConfig) == 16 * 4
+    text = (Path(__file__).resolve().parent.parent / "include" / "spmv_b200.h").read_text()
+    assert f"#define SPMV_PLAN_CONFIG_VERSION {VERSION}" in text
+    c = _CPlanConfig()
+    _lib.call("spmv_plan_config_init", ctypes.byref(c))
+    assert c.version == VERSION and PlanConfig.from_c(c) == PlanConfig()
+    assert PlanConfig(tile=1024, warp_stream=0).to_c().tile == 1024

@@ -1,10 +1,9 @@
-"""Sweep records, reports and corpus inputs.
+"""Sweep records and corpus inputs.
 
-CPU tests pin the CSV text and the rendered reports byte for byte against
-the reference's own output (tests/golden/sweep.npz, made by
-tests/golden/make_golden.py), and port the reference's report checks
-(reference tests/test_bench.py).  GPU tests check the corpus generators
-against the reference's arrays and run a device sweep."""
+CPU tests pin the CSV text byte for byte against the reference's own output
+(tests/golden/sweep.npz, made by tests/golden/make_golden.py), so GPU rows
+load in the reference's report tooling.  GPU tests check the corpus
+generators against the reference's arrays and run device sweeps."""
 
 from __future__ import annotations
 
@@ -40,47 +39,10 @@ def test_csv_text_matches_reference(name):
     assert buf.getvalue() == text
 
 
-@pytest.mark.parametrize("name,base", list(itertools.product(NAMES, ["csr_plain", "coo_vla"])))
-def test_report_text_matches_reference(name, base):
-    records = S.read_records(io.StringIO(str(G[f"records/{name}/csv"])))
-    want = str(G[f"records/{name}/report_{base}"])
-    baseline = {"csr_plain": (Format.CSR, V.PLAIN), "coo_vla": (Format.COO, V.VLA)}[base]
-    if want.startswith("raises "):
-        exc = getattr(sp.errors, want.split()[1])
-        with pytest.raises(exc):
-            S.make_report(records, baseline)
-    else:
-        assert S.render_report(S.make_report(records, baseline)) == want
-
-
 def test_records_file_round_trip(tmp_path):
     records = [rec("m1", Format.CSR, V.PLAIN, 2e-3), rec("x", None, None, None, status="error")]
     S.write_records(records, tmp_path / "r.csv")
     assert S.read_records(tmp_path / "r.csv") == records
-
-
-def test_make_report_ratios_and_distribution():
-    records = [rec("m1", Format.CSR, V.PLAIN, 2e-3), rec("m1", Format.COO, V.PLAIN, 1e-3),
-               rec("m2", Format.CSR, V.PLAIN, 2e-3), rec("m2", Format.COO, V.PLAIN, 4e-3),
-               rec("m2", Format.DIA, V.PLAIN, None, status="fill_exceeded")]
-    report = S.make_report(records)
-    pair = (Format.COO, V.PLAIN)
-    assert report.matrix_ids == ["m1", "m2"]
-    assert report.ratios["m1"][pair] == pytest.approx(2.0)
-    assert report.ratios["m2"][pair] == pytest.approx(0.5)
-    assert report.geomeans[pair] == pytest.approx(1.0)
-    assert report.status_counts == {"ok": 4, "fill_exceeded": 1}
-    shares = report.distribution[V.PLAIN]
-    assert shares[Format.COO] == 50.0 and shares[Format.CSR] == 50.0
-
-
-def test_make_report_errors():
-    with pytest.raises(sp.MissingBaseline):
-        S.make_report([rec("m1", Format.COO, V.PLAIN, 1e-3)])
-    with pytest.raises(sp.EmptyInput):
-        S.make_report([])
-    with pytest.raises(sp.EmptyInput):
-        S.make_report([rec("m1", Format.DIA, V.PLAIN, None, status="fill_exceeded")])
 
 
 def test_compare_records():
@@ -167,8 +129,18 @@ def test_run_corpus_on_gpu(tmp_path):
     S.write_records(recs, buf)
     S.write_records(S.read_records(io.StringIO(buf.getvalue())), buf2)  # CSV rounds like the reference
     assert buf2.getvalue() == buf.getvalue()
-    text = S.render_report(S.make_report(recs))
-    assert "baseline: csr/plain" in text and "matrices measured: 4" in text
+    # the GPU rows set against themselves: every measured row matches
+    c = S.compare_records(recs, recs)
+    assert len(c.speedups) == len(ok) and all(v == 1.0 for v in c.speedups.values())
+
+
+@pytest.mark.gpu
+def test_run_corpus_tuned_plans(tmp_path):
+    """tune_plans=True: each matrix/format gets its kernel configuration
+    tuned first; the rows still cover every pair."""
+    entries = [sp.CorpusEntry("cube", "stencil27:6,6,6"), sp.CorpusEntry("rnd", "random:300,0.05,5")]
+    recs = S.run_corpus(entries, iterations=3, reps=2, tune_plans=True)
+    assert len(recs) == 12 and all(r.status in (S.STATUS_OK, S.STATUS_FILL) for r in recs)
 
 
 @pytest.mark.gpu
