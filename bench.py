@@ -258,13 +258,13 @@ def plan_of(sp, m) -> dict:
     from paper_2304_09511_b200 import kernels as K
     if m.format == sp.Format.CSR:
         i = K.csr_plan(m).info()
-        if i["kernel"] == "warp_stream":
-            return {"kernel": "warp_stream", "warps": i["warps"]}
+        if i["kernel"] in ("warp_stream", "panel"):
+            return {"kernel": i["kernel"], "warps": i["warps"]}
         return {"tile": i["tile"], "groups": i["groups"]}
     if m.format == sp.Format.COO:
         i = K.coo_plan(m).info()
-        if i["kernel"] == "warp_stream":
-            return {"kernel": "warp_stream", "warps": i["warps"]}
+        if i["kernel"] in ("warp_stream", "panel"):
+            return {"kernel": i["kernel"], "warps": i["warps"]}
         return {"tile": i["tile"], "groups": i["groups"]}
     return {}
 

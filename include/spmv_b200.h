@@ -92,7 +92,11 @@ typedef struct {
     int32_t dia_rows;         /* DIA rows per tile, multiple of 8; 0 = auto           */
     int32_t flags;            /* experiments: bit0 products mode, bit1 warp per long  */
                               /* segment (tile kernels); 0 = off                      */
-    int32_t reserved[5];
+    int32_t panels;           /* CSR column-panel path for long rows: -1 auto (rows   */
+                              /* over 32 entries hold >= half the entries, ncols >=   */
+                              /* 65536), 0 off, 1 on (needs col_indices and values at */
+                              /* plan creation)                                       */
+    int32_t reserved[4];
 } spmv_plan_config;
 
 /* Fill *cfg with the auto values (version set).  Plans created with a NULL
@@ -103,9 +107,17 @@ int spmv_plan_config_init(spmv_plan_config* cfg);
 typedef struct spmv_csr_plan spmv_csr_plan;
 
 /* spmv_csr_plan_create with an explicit configuration (NULL = auto; the
- * exact_len argument of spmv_csr_plan_create is cfg->exact_len here). */
+ * exact_len argument of spmv_csr_plan_create is cfg->exact_len here) and
+ * optionally the matrix's column indices and values (may be NULL).  With
+ * them, a matrix whose long rows (over 32 entries) hold most of the
+ * entries gets the column-panel path: the plan keeps a panel-major copy of
+ * the long rows (csrc/panel.cuh) and whole-matrix products called with the
+ * same two arrays read that copy; the arrays must not change afterwards
+ * (containers are immutable).  Products called with other
+ * arrays run the warp-stream kernel. */
 int spmv_csr_plan_create_ex(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
                             const uint32_t* row_pointers,
+                            const uint32_t* col_indices, const void* values,
                             const spmv_plan_config* cfg, void* stream,
                             spmv_csr_plan** out);
 /* The configuration the plan resolved: tile, groups, warp_stream (0/1),
@@ -148,7 +160,8 @@ int spmv_csr_gapped(const spmv_csr_plan* plan, const uint32_t* row_pointers,
                     int64_t y_split, int64_t y_gap, void* stream);
 /* Whole-matrix kernel the plan chose: warp_stream = 1 for the warp-stream
  * kernel (matrices with rows longer than exact_len: one contiguous entry
- * range per resident warp, nwarps of them), 0 for the tile kernel.  Tile
+ * range per resident warp, nwarps of them), 2 for the column-panel path
+ * (nwarps = panel CTAs x 32), 0 for the tile kernel.  Tile
  * ranges (spmv_csr_range, spmv_csr_host) always use the tile kernel.
  * spmv_plan_config.warp_stream = 0/1 overrides the choice. */
 int spmv_csr_plan_path(const spmv_csr_plan* plan, int* warp_stream, int64_t* nwarps);

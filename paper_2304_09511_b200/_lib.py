@@ -54,7 +54,7 @@ SIGNATURES = {
     "spmv_csr_plan_create": [_c_int, _c_i64, _c_i64, _c_i64, _vp, _c_int, _vp, _pvp],
     "spmv_csr_plan_destroy": [_vp],
     "spmv_plan_config_init": [_vp],
-    "spmv_csr_plan_create_ex": [_c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _pvp],
+    "spmv_csr_plan_create_ex": [_c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _pvp],
     "spmv_csr_plan_config": [_vp, _vp],
     "spmv_coo_plan_create_ex": [_c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _pvp],
     "spmv_coo_plan_config": [_vp, _vp],

@@ -167,7 +167,8 @@ inline spmv_plan_config config_or_default(const spmv_plan_config* c) {
   d.dia_kernel = -1;
   d.dia_rows = 0;
   d.flags = 0;
-  for (int i = 0; i < 5; ++i) d.reserved[i] = 0;
+  d.panels = -1;
+  for (int i = 0; i < 4; ++i) d.reserved[i] = 0;
   return c ? *c : d;
 }
 inline int cap_ctas(int per_sm, int cap) {

@@ -22,10 +22,13 @@
 // Every stored entry is read from HBM exactly once (+kExt/TILE = 1.6%
 // overlap that hits L2), the row pointers once, x through L2, y written
 // once: the minimum-byte model of SURVEY.md §8(d).
+#include <cub/cub.cuh>
+
 #include <algorithm>
 #include <cstdlib>
 #include <vector>
 
+#include "panel.cuh"
 #include "tile.cuh"
 #include "wstream.cuh"
 
@@ -67,10 +70,14 @@ struct CsrParams {
   // rows >= y_split are stored y_gap entries further on (spmv_csr_gapped:
   // a slab's two boundary planes in one launch); y_split = INT64_MAX else
   int64_t y_split, y_gap;
+  // row r of this matrix is y[ymap[r]] (the panel path's short-row CSR);
+  // nullptr else
+  const uint32_t* ymap;
 };
 
 template <typename T>
 __device__ __forceinline__ int64_t yrow(const CsrParams<T>& P, int64_t r) {
+  if (P.ymap) return int64_t(P.ymap[r]);
   return r >= P.y_split ? r + P.y_gap : r;
 }
 
@@ -714,6 +721,7 @@ struct spmv_csr_plan {
     if (d2h) cudaStreamDestroy(d2h);
     for (auto e : events) cudaEventDestroy(e);
     if (host_done) cudaEventDestroy(host_done);
+    delete pn_sub;
   }
   int groups = 1;                    // consumer groups per tile CTA (csr_tile_kernel G)
   bool long_scratch = true;          // kernels with long-row scratch (false: plan has no long rows)
@@ -729,6 +737,18 @@ struct spmv_csr_plan {
   // launches only; tile ranges (halo split, host pipeline) keep the tiles
   bool ws = false;
   bool has_empty = false;
+  // panel path (panel.cuh) for long rows with random columns: whole-matrix
+  // launches; the short rows run as their own CSR (sub plan, y via srow)
+  bool panel = false;
+  int64_t pn_long = 0, pn_entries = 0, pn_seg = 0, pn_ctas = 0, pn_items = 0, pn_short = 0, pn_short_nnz = 0;
+  DevBuf pn_lrow, pn_ptr, pn_col, pn_val, pn_flag, pn_rseg, pn_cta_item, pn_item_panel, pn_item_end, pn_task_begin,
+      pn_task_seg0;
+  DevBuf pn_srow, pn_sirp, pn_saj, pn_sav, pn_empty;
+  int64_t pn_n_empty = 0;
+  spmv_csr_plan* pn_sub = nullptr;
+  const void* pn_aj = nullptr;  // the arrays the panel copy was made from: other arrays take the ws path
+  const void* pn_av = nullptr;
+  size_t off_part = 0;
   int64_t ws_nwarps = 0, ws_nranges = 0, ws_n_span = 0;
   int64_t ws_ranges_per_warp = 8;
   DevBuf ws_bounds, ws_row0, ws_span_row, ws_span_w0, ws_span_w1;
@@ -774,9 +794,15 @@ static int csr_launch_config(spmv_csr_plan* p) {
 template <typename T, int TILE, int G, bool LONG, int VW = 0>
 static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st, int64_t tb, int64_t te, bool fixup, int vla = 0,
-                   int64_t y_split = INT64_MAX, int64_t y_gap = 0) {
+                   int64_t y_split = INT64_MAX, int64_t y_gap = 0, const uint32_t* ymap = nullptr) {
   if (p->nrows == 0) return SPMV_OK;
   if (p->nnz == 0) {
+    if (ymap) {
+      const int64_t g = std::min<int64_t>((p->nrows + 255) / 256, int64_t(sm_count()) * 8);
+      scatter_zero_kernel<T><<<unsigned(g), 256, 0, st>>>(ymap, p->nrows, y);
+      SPMV_LAUNCH_CHECK();
+      return SPMV_OK;
+    }
     SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
     return SPMV_OK;
   }
@@ -802,6 +828,7 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
   P.vla = vla;
   P.y_split = y_split;
   P.y_gap = y_gap;
+  P.ymap = ymap;
   P.mode = (p->cfg.flags & 3) | (p->tma_hint ? 4 : 0);
   const bool aligned = (reinterpret_cast<uintptr_t>(aj) % 16 == 0) && (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
@@ -852,11 +879,12 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
 
 template <typename T>
 static int csr_run_ws(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
-                      int64_t col_base, T* y, cudaStream_t st) {
+                      int64_t col_base, T* y, cudaStream_t st, const uint32_t* ymap = nullptr) {
   unsigned char* scr = nullptr;
   int rc = p->scratch.get(st, reinterpret_cast<void**>(&scr));
   if (rc) return rc;
-  if (p->has_empty) SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
+  // empty rows: a memset of y (with a row map the caller zeroes them)
+  if (p->has_empty && !ymap) SPMV_CUDA_TRY(cudaMemsetAsync(y, 0, sizeof(T) * p->nrows, st));
   WsParams<T> P;
   P.irp = irp;
   P.aj = aj;
@@ -873,6 +901,7 @@ static int csr_run_ws(const spmv_csr_plan* p, const uint32_t* irp, const uint32_
   P.nwarps = p->ws_nwarps;
   P.nranges = p->ws_nranges;
   P.ctr = reinterpret_cast<uint32_t*>(scr + p->off_ws_ctr);
+  P.ymap = ymap;
   const int64_t grid = (p->ws_nwarps + kWsWarps - 1) / kWsWarps;
   csr_wstream_kernel<T><<<unsigned(grid), kWsWarps * 32, 0, st>>>(P);
   SPMV_LAUNCH_CHECK();
@@ -886,18 +915,66 @@ static int csr_run_ws(const spmv_csr_plan* p, const uint32_t* irp, const uint32_
 }
 
 template <typename T>
+static int csr_run_panel(const spmv_csr_plan* p, const T* x, int64_t col_base, int64_t x_len, T* y, cudaStream_t st);
+
+template <typename T>
 static int csr_run(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* x,
                    int64_t col_base, T* y, cudaStream_t st, int64_t tb = 0, int64_t te = -1, bool fixup = true,
-                   int64_t y_split = INT64_MAX, int64_t y_gap = 0) {
+                   int64_t y_split = INT64_MAX, int64_t y_gap = 0, const uint32_t* ymap = nullptr,
+                   int64_t x_len = -1) {
   if (te < 0) te = p->ntiles;
-  if (p->ws && tb == 0 && te == p->ntiles && fixup && y_gap == 0)
-    return csr_run_ws<T>(p, irp, aj, av, x, col_base, y, st);
+  const bool whole = tb == 0 && te == p->ntiles && fixup && y_gap == 0;
+  if (p->panel && whole && !ymap && aj == p->pn_aj && av == p->pn_av)
+    return csr_run_panel<T>(p, x, col_base, x_len < 0 ? p->ncols - col_base : x_len, y, st);
+  if (p->ws && whole) return csr_run_ws<T>(p, irp, aj, av, x, col_base, y, st, ymap);
 #define X(TL, GR, LF)                                                          \
   if (p->tile == TL && p->groups == GR && p->long_scratch == bool(LF))          \
-    return csr_run_tiled<T, TL, GR, bool(LF)>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup, 0, y_split, y_gap);
+    return csr_run_tiled<T, TL, GR, bool(LF)>(p, irp, aj, av, x, col_base, y, st, tb, te, fixup, 0, y_split, y_gap, \
+                                              ymap);
   SPMV_CSR_CONFIGS(X)
 #undef X
   return fail(SPMV_INVALID_ARG, "no CSR kernel for tile %lld x %d groups", (long long)p->tile, p->groups);
+}
+
+// Panel path (panel.cuh): the short rows through the sub plan's tile kernel
+// (y via the short-row map), the long rows' panel kernel, their partial sums.
+template <typename T>
+static int csr_run_panel(const spmv_csr_plan* p, const T* x, int64_t col_base, int64_t x_len, T* y,
+                         cudaStream_t st) {
+  unsigned char* scr = nullptr;
+  int rc = p->scratch.get(st, reinterpret_cast<void**>(&scr));
+  if (rc) return rc;
+  if (p->pn_n_empty > 0) {
+    const int64_t g0 = std::min<int64_t>((p->pn_n_empty + 255) / 256, int64_t(sm_count()) * 8);
+    scatter_zero_kernel<T><<<unsigned(g0), 256, 0, st>>>(p->pn_empty.as<uint32_t>(), p->pn_n_empty, y);
+    SPMV_LAUNCH_CHECK();
+  }
+  if (p->pn_short > 0 &&
+      (rc = csr_run<T>(p->pn_sub, p->pn_sirp.as<uint32_t>(), p->pn_saj.as<uint32_t>(), p->pn_sav.as<T>(), x,
+                       col_base, y, st, 0, -1, true, INT64_MAX, 0, p->pn_srow.as<uint32_t>())))
+    return rc;
+  if (p->pn_long == 0) return SPMV_OK;
+  PanelParams<T> P;
+  P.pcol = p->pn_col.as<uint16_t>();
+  P.pval = p->pn_val.as<T>();
+  P.pflag = p->pn_flag.as<uint8_t>();
+  P.x = x;
+  P.col_base = col_base;
+  P.x_len = x_len;
+  P.ncols = p->ncols;
+  P.cta_item = p->pn_cta_item.as<uint32_t>();
+  P.item_panel = p->pn_item_panel.as<uint32_t>();
+  P.item_end = p->pn_item_end.as<uint32_t>();
+  P.task_begin = p->pn_task_begin.as<uint32_t>();
+  P.task_seg0 = p->pn_task_seg0.as<uint32_t>();
+  P.part = reinterpret_cast<double*>(scr + p->off_part);
+  csr_panel_kernel<T><<<unsigned(p->pn_ctas), kPanelWarps * 32, 128 + sizeof(T) * kPanelCols, st>>>(P);
+  SPMV_LAUNCH_CHECK();
+  const int64_t g = std::min<int64_t>((p->pn_long * 8 + 255) / 256, int64_t(sm_count()) * 16);
+  csr_panel_finish_kernel<T><<<unsigned(g), 256, 0, st>>>(p->pn_lrow.as<uint32_t>(), p->pn_ptr.as<uint32_t>(),
+                                                          p->pn_rseg.as<uint32_t>(), p->pn_long, P.part, y);
+  SPMV_LAUNCH_CHECK();
+  return SPMV_OK;
 }
 
 // vla through the tile kernels (row-per-lane vla, tile.cuh row_vla_csr):
@@ -1106,7 +1183,7 @@ static int count_async(unsigned long long* dev, unsigned long long* host, cudaSt
 // (spmv_plan_config.warp_stream overrides).  One range per resident warp.
 static int csr_ws_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st) {
   const int mode = p->cfg.warp_stream;
-  p->ws = mode < 0 ? p->n_long_ws > 0 : mode > 0;
+  p->ws = (mode < 0 ? p->n_long_ws > 0 : mode > 0) || p->panel;  // the panel path falls back to it
   if (!p->ws) return SPMV_OK;
   int rc, per_sm = 0;
   unsigned long long* ctr = p->cnt.as<unsigned long long>();
@@ -1155,9 +1232,287 @@ static int csr_ws_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st) 
   return SPMV_OK;
 }
 
+__global__ void long_entries_kernel(const uint32_t* __restrict__ irp, int64_t nrows, uint32_t thr,
+                                    unsigned long long* __restrict__ n) {
+  unsigned long long c = 0;
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r < nrows; r += int64_t(gridDim.x) * blockDim.x) {
+    const uint32_t l = irp[r + 1] - irp[r];
+    c += l > thr ? l : 0u;
+  }
+  for (int o = 16; o >= 1; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(n, c);
+}
+
+// panel_ptr[q] = first panel-major entry of panel q (skey sorted).
+__global__ void panel_bounds_kernel(const uint32_t* __restrict__ skey, int64_t nl, int64_t npanels,
+                                    uint32_t* __restrict__ pan_ptr) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= nl; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t q1 = i < nl ? int64_t(skey[i]) : npanels;
+    const int64_t q0 = i == 0 ? -1 : int64_t(skey[i - 1]);
+    for (int64_t q = q0 + 1; q <= q1; ++q) pan_ptr[q] = uint32_t(i);
+  }
+}
+
+__global__ void gather_u32_kernel(const uint32_t* __restrict__ src, const uint32_t* __restrict__ idx, int64_t n,
+                                  int64_t limit, uint32_t* __restrict__ dst) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    dst[i] = idx[i] < limit ? src[idx[i]] : 0u;
+}
+
+__global__ void iota_u32_kernel(uint32_t* __restrict__ a, int64_t n) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
+    a[i] = uint32_t(i);
+}
+
+template <typename Fn>
+static int cub_call(Fn fn, ScratchBuf& tmp, cudaStream_t st) {
+  size_t bytes = 0;
+  SPMV_CUDA_TRY(fn(static_cast<void*>(nullptr), bytes));
+  if (bytes > tmp.bytes) {
+    int rc = tmp.alloc(bytes, st);
+    if (rc) return rc;
+  }
+  SPMV_CUDA_TRY(fn(tmp.ptr, bytes));
+  return SPMV_OK;
+}
+
+// The panel path's structures (panel.cuh): long rows copied panel-major
+// with segment flags and slots, the CTA / warp work cuts, and the short
+// rows as their own CSR with a sub plan.  Device work with cub sorts and
+// scans; a few small host round trips for the cuts.
+template <typename T>
+static int csr_panel_build(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, cudaStream_t st) {
+  int rc;
+  const int64_t n = p->nrows;
+  const int sms = sm_count();
+  const int64_t g = std::min<int64_t>((n + 255) / 256, int64_t(sms) * 16);
+  ScratchBuf is_long, pos, tmp;
+  if ((rc = is_long.alloc(4 * n, st)) || (rc = pos.alloc(4 * (n + 1), st))) return rc;
+  split_rows_flags_kernel<<<unsigned(g), 256, 0, st>>>(irp, n, uint32_t(kExactLen), is_long.as<uint32_t>());
+  SPMV_LAUNCH_CHECK();
+  if ((rc = cub_call([&](void* t, size_t& b) {
+         return cub::DeviceScan::ExclusiveSum(t, b, is_long.as<uint32_t>(), pos.as<uint32_t>(), n, st);
+       }, tmp, st)))
+    return rc;
+  const int64_t nlong = p->n_long, ns = n - nlong;
+  p->pn_long = nlong;
+  p->pn_short = ns;
+  if ((rc = p->pn_lrow.alloc(4 * std::max<int64_t>(nlong, 1))) || (rc = p->pn_srow.alloc(4 * std::max<int64_t>(ns, 1))))
+    return rc;
+  split_rows_scatter_kernel<<<unsigned(g), 256, 0, st>>>(is_long.as<uint32_t>(), pos.as<uint32_t>(), n,
+                                                         p->pn_lrow.as<uint32_t>(), p->pn_srow.as<uint32_t>());
+  SPMV_LAUNCH_CHECK();
+  // row lengths -> lptr (long rows) and the short CSR's IRP
+  ScratchBuf len;
+  if ((rc = len.alloc(4 * (std::max(nlong, ns) + 1), st)) || (rc = p->pn_sirp.alloc(4 * (ns + 1)))) return rc;
+  ScratchBuf lptr;
+  if ((rc = lptr.alloc(4 * (nlong + 1), st))) return rc;
+  auto scan_lengths = [&](const uint32_t* rows, int64_t cnt, uint32_t* out) -> int {
+    SPMV_CUDA_TRY(cudaMemsetAsync(len.ptr, 0, 4 * (cnt + 1), st));
+    if (cnt > 0) {
+      const int64_t gg = std::min<int64_t>((cnt + 255) / 256, int64_t(sms) * 16);
+      listed_lengths_kernel<<<unsigned(gg), 256, 0, st>>>(irp, rows, cnt, len.as<uint32_t>());
+      SPMV_LAUNCH_CHECK();
+    }
+    return cub_call([&](void* t, size_t& b) {
+      return cub::DeviceScan::ExclusiveSum(t, b, len.as<uint32_t>(), out, cnt + 1, st);
+    }, tmp, st);
+  };
+  if ((rc = scan_lengths(p->pn_lrow.as<uint32_t>(), nlong, lptr.as<uint32_t>()))) return rc;
+  if ((rc = scan_lengths(p->pn_srow.as<uint32_t>(), ns, p->pn_sirp.as<uint32_t>()))) return rc;
+  uint32_t h2[2] = {0, 0};
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&h2[0], lptr.as<uint32_t>() + nlong, 4, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&h2[1], p->pn_sirp.as<uint32_t>() + ns, 4, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t nl = h2[0];
+  p->pn_entries = nl;
+  p->pn_short_nnz = h2[1];
+  // the short rows' CSR and its plan (tile kernels, no long rows)
+  if ((rc = p->pn_saj.alloc(4 * std::max<int64_t>(p->pn_short_nnz, 1))) ||
+      (rc = p->pn_sav.alloc(sizeof(T) * std::max<int64_t>(p->pn_short_nnz, 1))))
+    return rc;
+  if (ns > 0) {
+    const int64_t gs = std::min<int64_t>((ns + 255) / 256, int64_t(sms) * 16);
+    short_copy_kernel<T><<<unsigned(gs), 256, 0, st>>>(irp, aj, av, p->pn_srow.as<uint32_t>(),
+                                                        p->pn_sirp.as<uint32_t>(), ns, p->pn_saj.as<uint32_t>(),
+                                                        p->pn_sav.as<T>());
+    SPMV_LAUNCH_CHECK();
+    // short rows: the warp-stream kernel (entry-per-lane gathers; a Zipf
+    // matrix's short rows average a few entries, too few for row-per-lane
+    // tiles); every row <= 32 entries, so no row is split: bit-exact
+    spmv_plan_config sc = p->cfg;
+    sc.warp_stream = 1;
+    sc.panels = 0;
+    sc.exact_len = 0;
+    if ((rc = spmv_csr_plan_create_ex(p->dtype, ns, p->ncols, p->pn_short_nnz, p->pn_sirp.as<uint32_t>(),
+                                      p->pn_saj.as<uint32_t>(), p->pn_sav.ptr, &sc, st, &p->pn_sub)))
+      return rc;
+    // empty short rows, zeroed by a scatter before each product
+    ScratchBuf cnt;
+    if ((rc = cnt.alloc(8, st))) return rc;
+    SPMV_CUDA_TRY(cudaMemsetAsync(cnt.ptr, 0, 8, st));
+    empty_listed_kernel<<<unsigned(gs), 256, 0, st>>>(p->pn_sirp.as<uint32_t>(), p->pn_srow.as<uint32_t>(), ns,
+                                                      nullptr, cnt.as<unsigned long long>());
+    SPMV_LAUNCH_CHECK();
+    unsigned long long ne = 0;
+    SPMV_CUDA_TRY(cudaMemcpyAsync(&ne, cnt.ptr, 8, cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    p->pn_n_empty = int64_t(ne);
+    if (ne > 0) {
+      if ((rc = p->pn_empty.alloc(4 * ne))) return rc;
+      SPMV_CUDA_TRY(cudaMemsetAsync(cnt.ptr, 0, 8, st));
+      empty_listed_kernel<<<unsigned(gs), 256, 0, st>>>(p->pn_sirp.as<uint32_t>(), p->pn_srow.as<uint32_t>(), ns,
+                                                        p->pn_empty.as<uint32_t>(), cnt.as<unsigned long long>());
+      SPMV_LAUNCH_CHECK();
+    }
+  }
+  if (nlong == 0) return SPMV_OK;
+  // long entries: (panel, long-entry index), stable sort by panel
+  const int64_t npanels = (p->ncols + kPanelCols - 1) / kPanelCols;
+  int end_bit = 1;
+  while (end_bit < 32 && (int64_t(1) << end_bit) < npanels) ++end_bit;
+  ScratchBuf key, skey, val, perm, erow, eidx;
+  if ((rc = key.alloc(4 * nl, st)) || (rc = skey.alloc(4 * nl, st)) || (rc = val.alloc(4 * nl, st)) ||
+      (rc = perm.alloc(4 * nl, st)) || (rc = erow.alloc(4 * nl, st)) || (rc = eidx.alloc(4 * nl, st)))
+    return rc;
+  const int64_t gl = std::min<int64_t>((nlong * 32 + 255) / 256, int64_t(sms) * 16);
+  panel_expand_kernel<<<unsigned(gl), 256, 0, st>>>(irp, aj, p->pn_lrow.as<uint32_t>(), lptr.as<uint32_t>(), nlong,
+                                                    key.as<uint32_t>(), val.as<uint32_t>(), erow.as<uint32_t>(),
+                                                    eidx.as<uint32_t>());
+  SPMV_LAUNCH_CHECK();
+  if ((rc = cub_call([&](void* t, size_t& b) {
+         return cub::DeviceRadixSort::SortPairs(t, b, key.as<uint32_t>(), skey.as<uint32_t>(), val.as<uint32_t>(),
+                                                perm.as<uint32_t>(), nl, 0, end_bit, st);
+       }, tmp, st)))
+    return rc;
+  // panel-major copy (padded: the kernel loads whole 8-entry groups)
+  const int64_t pad = 32 * kPanelK + 8;
+  if ((rc = p->pn_col.alloc(2 * (nl + pad))) || (rc = p->pn_val.alloc(sizeof(T) * (nl + pad)))) return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(p->pn_col.ptr, 0, 2 * (nl + pad), st));
+  SPMV_CUDA_TRY(cudaMemsetAsync(p->pn_val.ptr, 0, sizeof(T) * (nl + pad), st));
+  ScratchBuf flag, seg_of;
+  if ((rc = flag.alloc(4 * nl, st)) || (rc = seg_of.alloc(4 * (nl + 1), st))) return rc;
+  const int64_t ge = std::min<int64_t>((nl + 255) / 256, int64_t(sms) * 32);
+  panel_gather_kernel<T><<<unsigned(ge), 256, 0, st>>>(skey.as<uint32_t>(), perm.as<uint32_t>(), erow.as<uint32_t>(),
+                                                       eidx.as<uint32_t>(), aj, av, nl, p->pn_col.as<uint16_t>(),
+                                                       p->pn_val.as<T>(), flag.as<uint32_t>());
+  SPMV_LAUNCH_CHECK();
+  if ((rc = cub_call([&](void* t, size_t& b) {
+         return cub::DeviceScan::ExclusiveSum(t, b, flag.as<uint32_t>(), seg_of.as<uint32_t>(), nl, st);
+       }, tmp, st)))
+    return rc;
+  if ((rc = p->pn_flag.alloc((nl + pad) / 8 + 8))) return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(p->pn_flag.ptr, 0, (nl + pad) / 8 + 8, st));
+  panel_flag_bytes_kernel<<<unsigned(std::min<int64_t>((nl / 8 + 256) / 256, int64_t(sms) * 16)), 256, 0, st>>>(
+      flag.as<uint32_t>(), nl, p->pn_flag.as<uint8_t>());
+  SPMV_LAUNCH_CHECK();
+  uint32_t hs[2];
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&hs[0], seg_of.as<uint32_t>() + nl - 1, 4, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&hs[1], flag.as<uint32_t>() + nl - 1, 4, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t nseg = int64_t(hs[0]) + hs[1];
+  p->pn_seg = nseg;
+  // per segment its long row; per long row its segment count -> partial ptr
+  ScratchBuf seg_row, row_cnt, order, iota;
+  if ((rc = seg_row.alloc(4 * nseg, st)) || (rc = row_cnt.alloc(4 * (nlong + 1), st)) ||
+      (rc = order.alloc(4 * nseg, st)) || (rc = iota.alloc(4 * nseg, st)) || (rc = p->pn_ptr.alloc(4 * (nlong + 1))) ||
+      (rc = p->pn_rseg.alloc(4 * nseg)))
+    return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(row_cnt.ptr, 0, 4 * (nlong + 1), st));
+  panel_segments_kernel<<<unsigned(ge), 256, 0, st>>>(flag.as<uint32_t>(), seg_of.as<uint32_t>(), perm.as<uint32_t>(),
+                                                      erow.as<uint32_t>(), nl, seg_row.as<uint32_t>(),
+                                                      row_cnt.as<uint32_t>());
+  SPMV_LAUNCH_CHECK();
+  if ((rc = cub_call([&](void* t, size_t& b) {
+         return cub::DeviceScan::ExclusiveSum(t, b, row_cnt.as<uint32_t>(), p->pn_ptr.as<uint32_t>(), nlong + 1, st);
+       }, tmp, st)))
+    return rc;
+  const int64_t gsg = std::min<int64_t>((nseg + 255) / 256, int64_t(sms) * 16);
+  iota_u32_kernel<<<unsigned(gsg), 256, 0, st>>>(iota.as<uint32_t>(), nseg);
+  SPMV_LAUNCH_CHECK();
+  int row_bits = 1;
+  while (row_bits < 32 && (int64_t(1) << row_bits) < nlong) ++row_bits;
+  ScratchBuf srow_key;
+  if ((rc = srow_key.alloc(4 * nseg, st))) return rc;
+  if ((rc = cub_call([&](void* t, size_t& b) {
+         return cub::DeviceRadixSort::SortPairs(t, b, seg_row.as<uint32_t>(), srow_key.as<uint32_t>(),
+                                                iota.as<uint32_t>(), order.as<uint32_t>(), nseg, 0, row_bits, st);
+       }, tmp, st)))
+    return rc;
+  // row-major segment list (rseg): the sorted order itself
+  SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_rseg.ptr, order.ptr, 4 * nseg, cudaMemcpyDeviceToDevice, st));
+  // CTA cuts: equal entry counts, moved to segment starts
+  std::vector<uint32_t> pan_ptr(npanels + 1);
+  {
+    ScratchBuf dp;
+    if ((rc = dp.alloc(4 * (npanels + 1), st))) return rc;
+    panel_bounds_kernel<<<unsigned(ge), 256, 0, st>>>(skey.as<uint32_t>(), nl, npanels, dp.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+    SPMV_CUDA_TRY(cudaMemcpyAsync(pan_ptr.data(), dp.ptr, 4 * (npanels + 1), cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  }
+  auto snap = [&](std::vector<uint32_t>& pos, const std::vector<uint32_t>& lim) -> int {
+    const int64_t m = int64_t(pos.size());
+    ScratchBuf dpos, dlim;
+    int r2;
+    if ((r2 = dpos.alloc(4 * m, st)) || (r2 = dlim.alloc(4 * m, st))) return r2;
+    SPMV_CUDA_TRY(cudaMemcpyAsync(dpos.ptr, pos.data(), 4 * m, cudaMemcpyHostToDevice, st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(dlim.ptr, lim.data(), 4 * m, cudaMemcpyHostToDevice, st));
+    panel_snap_kernel<<<unsigned(std::min<int64_t>((m + 255) / 256, 1024)), 256, 0, st>>>(
+        flag.as<uint32_t>(), dpos.as<uint32_t>(), m, dlim.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+    SPMV_CUDA_TRY(cudaMemcpyAsync(pos.data(), dpos.ptr, 4 * m, cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    return SPMV_OK;
+  };
+  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(sms, (nl + 4095) / 4096));
+  std::vector<uint32_t> cut(C + 1), cut_lim(C + 1, uint32_t(nl));
+  for (int64_t c = 0; c <= C; ++c) cut[c] = uint32_t(nl * c / C);
+  if ((rc = snap(cut, cut_lim))) return rc;
+  cut[0] = 0;
+  cut[C] = uint32_t(nl);
+  std::vector<uint32_t> cta_item(C + 1), item_panel, item_end, tb, tlim;
+  for (int64_t c = 0; c < C; ++c) {
+    cta_item[c] = uint32_t(item_panel.size());
+    for (int64_t q = 0; q < npanels; ++q) {
+      const uint32_t lo = std::max(cut[c], pan_ptr[q]), hi = std::min(cut[c + 1], pan_ptr[q + 1]);
+      if (lo >= hi) continue;
+      item_panel.push_back(uint32_t(q));
+      item_end.push_back(hi);
+      for (int w = 0; w < kPanelWarps; ++w) {
+        tb.push_back(uint32_t(lo + (uint64_t(hi - lo) * w) / kPanelWarps));
+        tlim.push_back(hi);
+      }
+    }
+  }
+  cta_item[C] = uint32_t(item_panel.size());
+  if ((rc = snap(tb, tlim))) return rc;
+  p->pn_ctas = C;
+  p->pn_items = int64_t(item_panel.size());
+  const int64_t nt = int64_t(tb.size());
+  if ((rc = p->pn_cta_item.alloc(4 * (C + 1))) || (rc = p->pn_item_panel.alloc(4 * std::max<int64_t>(1, p->pn_items))) ||
+      (rc = p->pn_item_end.alloc(4 * std::max<int64_t>(1, p->pn_items))) ||
+      (rc = p->pn_task_begin.alloc(4 * std::max<int64_t>(1, nt))) ||
+      (rc = p->pn_task_seg0.alloc(4 * std::max<int64_t>(1, nt))))
+    return rc;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_cta_item.ptr, cta_item.data(), 4 * (C + 1), cudaMemcpyHostToDevice, st));
+  if (p->pn_items) {
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_item_panel.ptr, item_panel.data(), 4 * p->pn_items, cudaMemcpyHostToDevice,
+                                  st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_item_end.ptr, item_end.data(), 4 * p->pn_items, cudaMemcpyHostToDevice, st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_task_begin.ptr, tb.data(), 4 * nt, cudaMemcpyHostToDevice, st));
+    gather_u32_kernel<<<unsigned(std::min<int64_t>((nt + 255) / 256, 1024)), 256, 0, st>>>(
+        seg_of.as<uint32_t>(), p->pn_task_begin.as<uint32_t>(), nt, nl, p->pn_task_seg0.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+  }
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));  // temporaries are released on return
+  return SPMV_OK;
+}
+
 // Plan analysis (once per matrix): long-row census, tile size, per-tile row
 // ranges and the list of long rows spanning tiles.
-static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st) {
+static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av,
+                          cudaStream_t st) {
   const int64_t nrows = p->nrows;
   unsigned long long* ctr = p->cnt.as<unsigned long long>();
   unsigned long long h = 0;
@@ -1235,13 +1590,37 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, cudaStream_t st
       SPMV_LAUNCH_CHECK();
     }
   }
+  // panel path: rows over 32 entries holding at least half the entries of
+  // a matrix whose x does not fit L1 (spmv_plan_config.panels overrides);
+  // needs the column indices and values (copied panel-major)
+  if (p->n_long > 0 && aj && av && p->cfg.panels != 0) {
+    SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
+    long_entries_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, uint32_t(kExactLen), ctr);
+    SPMV_LAUNCH_CHECK();
+    if ((rc = count_async(ctr, &h, st))) return rc;
+    p->panel = p->cfg.panels > 0 || (2 * int64_t(h) >= p->nnz && p->ncols >= 65536);
+  }
   if ((rc = csr_ws_build(p, irp, st))) return rc;
+  if (p->panel) {
+    rc = p->dtype == SPMV_F64 ? csr_panel_build<double>(p, irp, aj, static_cast<const double*>(av), st)
+                              : csr_panel_build<float>(p, irp, aj, static_cast<const float*>(av), st);
+    if (rc) return rc;
+    p->pn_aj = aj;
+    p->pn_av = av;
+    if (p->dtype == SPMV_F64)
+      SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_panel_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(128 + sizeof(double) * kPanelCols)));
+    else
+      SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_panel_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         int(128 + sizeof(float) * kPanelCols)));
+  }
   SlotLayout lay;  // per-stream launch scratch
   p->off_head = lay.add(vs * p->ntiles);
   p->off_tail = lay.add(vs * p->ntiles);
   p->off_ws_head = lay.add(8 * p->ws_nranges);
   p->off_ws_tail = lay.add(8 * p->ws_nranges);
   p->off_ws_ctr = lay.add(8);
+  p->off_part = lay.add(8 * p->pn_seg);
   p->scratch.bytes = lay.total;
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
 #define X(TL, GR, LF)                                                                      \
@@ -1282,7 +1661,7 @@ int spmv_csr_plan_create(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, c
                          int exact_len, void* stream, spmv_csr_plan** out) {
   spmv_plan_config cfg = config_or_default(nullptr);
   cfg.exact_len = exact_len;
-  return spmv_csr_plan_create_ex(dtype, nrows, ncols, nnz, row_pointers, &cfg, stream, out);
+  return spmv_csr_plan_create_ex(dtype, nrows, ncols, nnz, row_pointers, nullptr, nullptr, &cfg, stream, out);
 }
 
 int spmv_csr_plan_config(const spmv_csr_plan* p, spmv_plan_config* out) {
@@ -1294,11 +1673,13 @@ int spmv_csr_plan_config(const spmv_csr_plan* p, spmv_plan_config* out) {
   out->warp_stream = p->ws ? 1 : 0;
   out->ranges_per_warp = int32_t(p->ws_ranges_per_warp);
   out->tma_hint = p->tma_hint ? 1 : 0;
+  out->panels = p->panel ? 1 : 0;
   return SPMV_OK;
 }
 
 int spmv_csr_plan_create_ex(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* row_pointers,
-                            const spmv_plan_config* cfg, void* stream, spmv_csr_plan** out) {
+                            const uint32_t* col_indices, const void* values, const spmv_plan_config* cfg,
+                            void* stream, spmv_csr_plan** out) {
   if (!out) return fail(SPMV_INVALID_ARG, "spmv_csr_plan_create: out is NULL");
   if (cfg && cfg->version != SPMV_PLAN_CONFIG_VERSION)
     return fail(SPMV_INVALID_ARG, "spmv_plan_config version %d, expected %d", cfg->version, SPMV_PLAN_CONFIG_VERSION);
@@ -1319,7 +1700,7 @@ int spmv_csr_plan_create_ex(int dtype, int64_t nrows, int64_t ncols, int64_t nnz
   p->exact_len = exact_len;
   p->cfg = config_or_default(cfg);
   int rc = p->cnt.alloc(8);  // scratch counter
-  if (!rc && nrows > 0 && nnz > 0) rc = csr_plan_build(p, row_pointers, st);
+  if (!rc && nrows > 0 && nnz > 0) rc = csr_plan_build(p, row_pointers, col_indices, values, st);
   if (rc) {
     delete p;
     return rc;
@@ -1351,7 +1732,11 @@ int spmv_csr_plan_info(const spmv_csr_plan* p, int64_t* n_long_rows, int64_t* n_
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (n_long_rows) *n_long_rows = p->n_long_ws;
   if (n_items) *n_items = p->tile;
-  if (launches && p->ws)
+  if (launches && p->panel) {
+    int64_t sub = 0;
+    if (p->pn_sub) spmv_csr_plan_info(p->pn_sub, nullptr, nullptr, &sub);
+    *launches = sub + (p->pn_long > 0 ? 2 : 0);
+  } else if (launches && p->ws)
     *launches = 1 + (p->ws_n_span > 0 ? 1 : 0);
   else if (launches)
     *launches = (p->nrows > 0 ? 1 : 0) + (p->n_span > 0 ? 1 : 0) +
@@ -1367,8 +1752,8 @@ int spmv_csr_plan_groups(const spmv_csr_plan* p, int* groups) {
 
 int spmv_csr_plan_path(const spmv_csr_plan* p, int* warp_stream, int64_t* nwarps) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
-  if (warp_stream) *warp_stream = p->ws ? 1 : 0;
-  if (nwarps) *nwarps = p->ws_nwarps;
+  if (warp_stream) *warp_stream = p->panel ? 2 : p->ws ? 1 : 0;
+  if (nwarps) *nwarps = p->panel ? p->pn_ctas * kPanelWarps : p->ws_nwarps;
   return SPMV_OK;
 }
 
@@ -1458,9 +1843,9 @@ int spmv_csr(const spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, co
   cudaStream_t st = as_stream(stream);
   if (p->dtype == SPMV_F64)
     return csr_run<double>(p, irp, aj, static_cast<const double*>(av), static_cast<const double*>(x), col_base,
-                           static_cast<double*>(y), st);
+                           static_cast<double*>(y), st, 0, -1, true, INT64_MAX, 0, nullptr, x_len);
   return csr_run<float>(p, irp, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
-                        static_cast<float*>(y), st);
+                        static_cast<float*>(y), st, 0, -1, true, INT64_MAX, 0, nullptr, x_len);
 }
 
 // The planned vla path's row list: rows over kVlaLong entries, their chunk

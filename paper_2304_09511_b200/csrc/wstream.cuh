@@ -66,7 +66,13 @@ struct WsParams {
   uint32_t* ctr;           // [next range - nwarps, warps done]; zero between launches
   int64_t nrows, col_base, nwarps, nranges;
   uint32_t exact_len;
+  const uint32_t* ymap;    // row r is y[ymap[r]] (the panel path's short-row CSR); nullptr else
 };
+
+template <typename T>
+__device__ __forceinline__ int64_t ws_yrow(const WsParams<T>& P, int64_t r) {
+  return P.ymap ? int64_t(P.ymap[r]) : r;
+}
 
 // Row sums accumulate in double.  f64: the plain rounded sum.  f32: rows of
 // at most exact_len entries add in float (every partial is a float, so this
@@ -139,7 +145,7 @@ __device__ __forceinline__ void csr_ws_range(const WsParams<T>& P, const int64_t
           if (head)
             P.head[w] = carry;
           else
-            P.y[r] = T(carry);
+            P.y[ws_yrow(P, r)] = T(carry);
         }
         r += 1;
         rs = c1;
@@ -183,7 +189,7 @@ __device__ __forceinline__ void csr_ws_range(const WsParams<T>& P, const int64_t
         if (lane == 0 && head)
           P.head[w] = s;
         else
-          P.y[r + lane] = T(s);
+          P.y[ws_yrow(P, r + lane)] = T(s);
       }
       if (nfin < 32) {
         // lane nfin's row continues into the next chunk (or is past nrows)

@@ -131,7 +131,7 @@ class _Plan:
             info = {"long_rows": a.value, "tile": b.value, "launches": c.value, "groups": g.value, "kernel": "tile",
                     "config": self.config().as_dict()}
             if ws.value:  # tile/groups still serve tile-range launches
-                info.update(kernel="warp_stream", warps=nw.value)
+                info.update(kernel="panel" if ws.value == 2 else "warp_stream", warps=nw.value)
             return info
         a, b, c, d, e = ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int64(), ctypes.c_int(), ctypes.c_int64()
         g = ctypes.c_int()
@@ -163,7 +163,8 @@ def csr_plan(A: CsrMatrix, exact_len: int = 0, config: PlanConfig | None = None)
         h = ctypes.c_void_p()
         c = cfg.to_c()
         _lib.call("spmv_csr_plan_create_ex", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.nnz,
-                  _ptr(A.row_pointers), ctypes.byref(c), _stream(A.device), ctypes.byref(h))
+                  _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values), ctypes.byref(c), _stream(A.device),
+                  ctypes.byref(h))
         return _Plan("csr", h, cfg)
 
     return A.plan(("csr", cfg.key()), make)

@@ -32,7 +32,7 @@ class _CPlanConfig(ctypes.Structure):
                 ("exact_len", ctypes.c_int32), ("warp_stream", ctypes.c_int32),
                 ("ranges_per_warp", ctypes.c_int32), ("tma_hint", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
                 ("dia_kernel", ctypes.c_int32), ("dia_rows", ctypes.c_int32), ("flags", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 5)]
+                ("panels", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
 
 
 @dataclass(frozen=True)
@@ -52,6 +52,8 @@ class PlanConfig:
     dia_kernel      DIA (groups, stages, threads) preset 0..4, -1 auto
     dia_rows        DIA rows per tile (multiple of 8), 0 auto
     flags           experiments (bit0 products mode, bit1 warp per long segment)
+    panels          CSR column-panel path for long rows (csrc/panel.cuh): -1 auto,
+                    0 off, 1 on
     """
 
     tile: int = 0
@@ -64,6 +66,7 @@ class PlanConfig:
     dia_kernel: int = -1
     dia_rows: int = 0
     flags: int = 0
+    panels: int = -1
 
     def to_c(self) -> _CPlanConfig:
         c = _CPlanConfig()
@@ -91,7 +94,7 @@ class PlanConfig:
         configuration.  Never read implicitly by the library."""
         env = {"tile": "SPMV_TILE", "flags": "SPMV_TILE_MODE", "tma_hint": "SPMV_TMA_HINT",
                "ranges_per_warp": "SPMV_WS_RANGES", "ctas_per_sm": "SPMV_CTAS_PER_SM", "dia_rows": "SPMV_DIA_ROWS",
-               "dia_kernel": "SPMV_DIA_CFG"}
+               "dia_kernel": "SPMV_DIA_CFG", "panels": "SPMV_PANELS"}
         kw = {k: int(os.environ[v]) for k, v in env.items() if os.environ.get(v)}
         for k, v in (("groups", "SPMV_CSR_GROUPS"), ("groups", "SPMV_COO_GROUPS")):
             if os.environ.get(v):

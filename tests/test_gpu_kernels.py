@@ -52,12 +52,12 @@ def plan_tile(m) -> dict:
 def check_rowwise(y, y_plain, y_vla32, lens, tol, plan):
     """Apply the exactness contract row by row.  Tile kernels: rows <= 32
     bit-exact, rows of 33..256 inside one tile bit-exact with vla(32), the
-    rest within tol.  Warp-stream kernel (csrc/wstream.cuh): rows <= 32
-    bit-exact, the rest within tol."""
+    rest within tol.  Warp-stream and panel kernels (csrc/wstream.cuh,
+    csrc/panel.cuh): rows <= 32 bit-exact, the rest within tol."""
     y = np.asarray(y)
     short = lens <= 32
     assert bit_equal(y[short], y_plain[short]), first_diff(y[short], y_plain[short])
-    if plan.get("kernel") == "warp_stream":
+    if plan.get("kernel") in ("warp_stream", "panel"):
         if (~short).any():
             assert rel_err(y[~short], y_plain[~short]) <= tol
         return
