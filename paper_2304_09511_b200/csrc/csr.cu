@@ -721,7 +721,6 @@ struct spmv_csr_plan {
     if (d2h) cudaStreamDestroy(d2h);
     for (auto e : events) cudaEventDestroy(e);
     if (host_done) cudaEventDestroy(host_done);
-    delete pn_sub;
   }
   int groups = 1;                    // consumer groups per tile CTA (csr_tile_kernel G)
   bool long_scratch = true;          // kernels with long-row scratch (false: plan has no long rows)
@@ -743,9 +742,8 @@ struct spmv_csr_plan {
   int64_t pn_long = 0, pn_entries = 0, pn_seg = 0, pn_ctas = 0, pn_items = 0, pn_short = 0, pn_short_nnz = 0;
   DevBuf pn_lrow, pn_ptr, pn_col, pn_val, pn_flag, pn_rseg, pn_cta_item, pn_item_panel, pn_item_end, pn_task_begin,
       pn_task_seg0;
-  DevBuf pn_srow, pn_sirp, pn_saj, pn_sav, pn_empty;
-  int64_t pn_n_empty = 0;
-  spmv_csr_plan* pn_sub = nullptr;
+  DevBuf pn_srow, pn_scol, pn_sval;  // short rows by length class (ShortEll)
+  ShortEll pn_ell;
   const void* pn_aj = nullptr;  // the arrays the panel copy was made from: other arrays take the ws path
   const void* pn_av = nullptr;
   size_t off_part = 0;
@@ -944,15 +942,12 @@ static int csr_run_panel(const spmv_csr_plan* p, const T* x, int64_t col_base, i
   unsigned char* scr = nullptr;
   int rc = p->scratch.get(st, reinterpret_cast<void**>(&scr));
   if (rc) return rc;
-  if (p->pn_n_empty > 0) {
-    const int64_t g0 = std::min<int64_t>((p->pn_n_empty + 255) / 256, int64_t(sm_count()) * 8);
-    scatter_zero_kernel<T><<<unsigned(g0), 256, 0, st>>>(p->pn_empty.as<uint32_t>(), p->pn_n_empty, y);
+  if (p->pn_short > 0) {
+    const int64_t gs = std::min<int64_t>((p->pn_short + 255) / 256, int64_t(sm_count()) * 16);
+    short_ell_kernel<T><<<unsigned(gs), 256, 0, st>>>(p->pn_ell, p->pn_scol.as<uint32_t>(), p->pn_sval.as<T>(),
+                                                      p->pn_srow.as<uint32_t>(), p->pn_short, x, col_base, y);
     SPMV_LAUNCH_CHECK();
   }
-  if (p->pn_short > 0 &&
-      (rc = csr_run<T>(p->pn_sub, p->pn_sirp.as<uint32_t>(), p->pn_saj.as<uint32_t>(), p->pn_sav.as<T>(), x,
-                       col_base, y, st, 0, -1, true, INT64_MAX, 0, p->pn_srow.as<uint32_t>())))
-    return rc;
   if (p->pn_long == 0) return SPMV_OK;
   PanelParams<T> P;
   P.pcol = p->pn_col.as<uint16_t>();
@@ -968,7 +963,7 @@ static int csr_run_panel(const spmv_csr_plan* p, const T* x, int64_t col_base, i
   P.task_begin = p->pn_task_begin.as<uint32_t>();
   P.task_seg0 = p->pn_task_seg0.as<uint32_t>();
   P.part = reinterpret_cast<double*>(scr + p->off_part);
-  csr_panel_kernel<T><<<unsigned(p->pn_ctas), kPanelWarps * 32, 128 + sizeof(T) * kPanelCols, st>>>(P);
+  csr_panel_kernel<T><<<unsigned(p->pn_ctas), kPanelWarps * 32, panel_smem_bytes<T>(), st>>>(P);
   SPMV_LAUNCH_CHECK();
   const int64_t g = std::min<int64_t>((p->pn_long * 8 + 255) / 256, int64_t(sm_count()) * 16);
   csr_panel_finish_kernel<T><<<unsigned(g), 256, 0, st>>>(p->pn_lrow.as<uint32_t>(), p->pn_ptr.as<uint32_t>(),
@@ -1302,69 +1297,56 @@ static int csr_panel_build(spmv_csr_plan* p, const uint32_t* irp, const uint32_t
   split_rows_scatter_kernel<<<unsigned(g), 256, 0, st>>>(is_long.as<uint32_t>(), pos.as<uint32_t>(), n,
                                                          p->pn_lrow.as<uint32_t>(), p->pn_srow.as<uint32_t>());
   SPMV_LAUNCH_CHECK();
-  // row lengths -> lptr (long rows) and the short CSR's IRP
-  ScratchBuf len;
-  if ((rc = len.alloc(4 * (std::max(nlong, ns) + 1), st)) || (rc = p->pn_sirp.alloc(4 * (ns + 1)))) return rc;
-  ScratchBuf lptr;
-  if ((rc = lptr.alloc(4 * (nlong + 1), st))) return rc;
-  auto scan_lengths = [&](const uint32_t* rows, int64_t cnt, uint32_t* out) -> int {
-    SPMV_CUDA_TRY(cudaMemsetAsync(len.ptr, 0, 4 * (cnt + 1), st));
-    if (cnt > 0) {
-      const int64_t gg = std::min<int64_t>((cnt + 255) / 256, int64_t(sms) * 16);
-      listed_lengths_kernel<<<unsigned(gg), 256, 0, st>>>(irp, rows, cnt, len.as<uint32_t>());
-      SPMV_LAUNCH_CHECK();
-    }
-    return cub_call([&](void* t, size_t& b) {
-      return cub::DeviceScan::ExclusiveSum(t, b, len.as<uint32_t>(), out, cnt + 1, st);
-    }, tmp, st);
-  };
-  if ((rc = scan_lengths(p->pn_lrow.as<uint32_t>(), nlong, lptr.as<uint32_t>()))) return rc;
-  if ((rc = scan_lengths(p->pn_srow.as<uint32_t>(), ns, p->pn_sirp.as<uint32_t>()))) return rc;
-  uint32_t h2[2] = {0, 0};
-  SPMV_CUDA_TRY(cudaMemcpyAsync(&h2[0], lptr.as<uint32_t>() + nlong, 4, cudaMemcpyDeviceToHost, st));
-  SPMV_CUDA_TRY(cudaMemcpyAsync(&h2[1], p->pn_sirp.as<uint32_t>() + ns, 4, cudaMemcpyDeviceToHost, st));
-  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
-  const int64_t nl = h2[0];
-  p->pn_entries = nl;
-  p->pn_short_nnz = h2[1];
-  // the short rows' CSR and its plan (tile kernels, no long rows)
-  if ((rc = p->pn_saj.alloc(4 * std::max<int64_t>(p->pn_short_nnz, 1))) ||
-      (rc = p->pn_sav.alloc(sizeof(T) * std::max<int64_t>(p->pn_short_nnz, 1))))
+  // row lengths -> lptr (long rows)
+  ScratchBuf len, lptr;
+  if ((rc = len.alloc(4 * (std::max(nlong, ns) + 1), st)) || (rc = lptr.alloc(4 * (nlong + 1), st))) return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(len.ptr, 0, 4 * (nlong + 1), st));
+  if (nlong > 0) {
+    const int64_t gg = std::min<int64_t>((nlong + 255) / 256, int64_t(sms) * 16);
+    listed_lengths_kernel<<<unsigned(gg), 256, 0, st>>>(irp, p->pn_lrow.as<uint32_t>(), nlong, len.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+  }
+  if ((rc = cub_call([&](void* t, size_t& bb) {
+         return cub::DeviceScan::ExclusiveSum(t, bb, len.as<uint32_t>(), lptr.as<uint32_t>(), nlong + 1, st);
+       }, tmp, st)))
     return rc;
+  uint32_t hnl = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&hnl, lptr.as<uint32_t>() + nlong, 4, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  const int64_t nl = hnl;
+  p->pn_entries = nl;
+  p->pn_short_nnz = p->nnz - nl;
+  // the short rows (<= 32 entries) grouped by exact length, each class
+  // stored column-major (entry j of every row of the class contiguous):
+  // one thread per row, coalesced loads, the row summed left to right
   if (ns > 0) {
+    ScratchBuf skey2, srow2;
+    if ((rc = skey2.alloc(4 * ns, st)) || (rc = srow2.alloc(4 * ns, st))) return rc;
     const int64_t gs = std::min<int64_t>((ns + 255) / 256, int64_t(sms) * 16);
-    short_copy_kernel<T><<<unsigned(gs), 256, 0, st>>>(irp, aj, av, p->pn_srow.as<uint32_t>(),
-                                                        p->pn_sirp.as<uint32_t>(), ns, p->pn_saj.as<uint32_t>(),
-                                                        p->pn_sav.as<T>());
+    listed_lengths_kernel<<<unsigned(gs), 256, 0, st>>>(irp, p->pn_srow.as<uint32_t>(), ns, len.as<uint32_t>());
     SPMV_LAUNCH_CHECK();
-    // short rows: the warp-stream kernel (entry-per-lane gathers; a Zipf
-    // matrix's short rows average a few entries, too few for row-per-lane
-    // tiles); every row <= 32 entries, so no row is split: bit-exact
-    spmv_plan_config sc = p->cfg;
-    sc.warp_stream = 1;
-    sc.panels = 0;
-    sc.exact_len = 0;
-    if ((rc = spmv_csr_plan_create_ex(p->dtype, ns, p->ncols, p->pn_short_nnz, p->pn_sirp.as<uint32_t>(),
-                                      p->pn_saj.as<uint32_t>(), p->pn_sav.ptr, &sc, st, &p->pn_sub)))
+    if ((rc = cub_call([&](void* t, size_t& bb) {
+           return cub::DeviceRadixSort::SortPairs(t, bb, len.as<uint32_t>(), skey2.as<uint32_t>(),
+                                                  p->pn_srow.as<uint32_t>(), srow2.as<uint32_t>(), ns, 0, 6, st);
+         }, tmp, st)))
       return rc;
-    // empty short rows, zeroed by a scatter before each product
-    ScratchBuf cnt;
-    if ((rc = cnt.alloc(8, st))) return rc;
-    SPMV_CUDA_TRY(cudaMemsetAsync(cnt.ptr, 0, 8, st));
-    empty_listed_kernel<<<unsigned(gs), 256, 0, st>>>(p->pn_sirp.as<uint32_t>(), p->pn_srow.as<uint32_t>(), ns,
-                                                      nullptr, cnt.as<unsigned long long>());
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_srow.ptr, srow2.ptr, 4 * ns, cudaMemcpyDeviceToDevice, st));
+    ScratchBuf dcls;
+    if ((rc = dcls.alloc(4 * (kShortClasses + 1), st))) return rc;
+    panel_bounds_kernel<<<unsigned(gs), 256, 0, st>>>(skey2.as<uint32_t>(), ns, kShortClasses, dcls.as<uint32_t>());
     SPMV_LAUNCH_CHECK();
-    unsigned long long ne = 0;
-    SPMV_CUDA_TRY(cudaMemcpyAsync(&ne, cnt.ptr, 8, cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_ell.cls, dcls.ptr, 4 * (kShortClasses + 1), cudaMemcpyDeviceToHost, st));
     SPMV_CUDA_TRY(cudaStreamSynchronize(st));
-    p->pn_n_empty = int64_t(ne);
-    if (ne > 0) {
-      if ((rc = p->pn_empty.alloc(4 * ne))) return rc;
-      SPMV_CUDA_TRY(cudaMemsetAsync(cnt.ptr, 0, 8, st));
-      empty_listed_kernel<<<unsigned(gs), 256, 0, st>>>(p->pn_sirp.as<uint32_t>(), p->pn_srow.as<uint32_t>(), ns,
-                                                        p->pn_empty.as<uint32_t>(), cnt.as<unsigned long long>());
-      SPMV_LAUNCH_CHECK();
+    uint64_t acc = 0;
+    for (int L = 0; L < kShortClasses; ++L) {
+      p->pn_ell.ebase[L] = uint32_t(acc);
+      acc += uint64_t(L) * (p->pn_ell.cls[L + 1] - p->pn_ell.cls[L]);
     }
+    if ((rc = p->pn_scol.alloc(4 * std::max<uint64_t>(acc, 1))) || (rc = p->pn_sval.alloc(sizeof(T) * std::max<uint64_t>(acc, 1))))
+      return rc;
+    short_ell_fill_kernel<T><<<unsigned(gs), 256, 0, st>>>(p->pn_ell, irp, aj, av, p->pn_srow.as<uint32_t>(), ns,
+                                                            p->pn_scol.as<uint32_t>(), p->pn_sval.as<T>());
+    SPMV_LAUNCH_CHECK();
   }
   if (nlong == 0) return SPMV_OK;
   // long entries: (panel, long-entry index), stable sort by panel
@@ -1609,10 +1591,10 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, const uint32_t*
     p->pn_av = av;
     if (p->dtype == SPMV_F64)
       SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_panel_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(128 + sizeof(double) * kPanelCols)));
+                                         panel_smem_bytes<double>()));
     else
       SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_panel_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         int(128 + sizeof(float) * kPanelCols)));
+                                         panel_smem_bytes<float>()));
   }
   SlotLayout lay;  // per-stream launch scratch
   p->off_head = lay.add(vs * p->ntiles);
@@ -1733,9 +1715,7 @@ int spmv_csr_plan_info(const spmv_csr_plan* p, int64_t* n_long_rows, int64_t* n_
   if (n_long_rows) *n_long_rows = p->n_long_ws;
   if (n_items) *n_items = p->tile;
   if (launches && p->panel) {
-    int64_t sub = 0;
-    if (p->pn_sub) spmv_csr_plan_info(p->pn_sub, nullptr, nullptr, &sub);
-    *launches = sub + (p->pn_long > 0 ? 2 : 0);
+    *launches = (p->pn_short > 0 ? 1 : 0) + (p->pn_long > 0 ? 2 : 0);
   } else if (launches && p->ws)
     *launches = 1 + (p->ws_n_span > 0 ? 1 : 0);
   else if (launches)

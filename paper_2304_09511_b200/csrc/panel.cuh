@@ -42,9 +42,19 @@
 
 namespace spmv {
 
-constexpr int kPanelCols = 28672;     // x entries per panel: 224 KB of f64 (+ the flag bit fits 16 bits)
+constexpr int kPanelCols = 23552;     // x entries per panel: 184 KB of f64
 constexpr int kPanelWarps = 16;       // warps per CTA (one CTA per SM)
 constexpr int kPanelK = 8;            // consecutive entries per lane per step
+constexpr int kPanelStep = 32 * kPanelK;  // entries per warp step
+// per-warp staging of one step (TMA bulk copies): values, column pairs, start bits
+template <typename T> constexpr int panel_stage_bytes() {
+  return int(align_up(kPanelStep * sizeof(T) + kPanelStep * 2 + 32, 128));
+}
+constexpr int kPanelHeader = 256;  // mbarriers: [0] panel, [1 + w] warp w's stage
+template <typename T> constexpr int panel_smem_bytes() {
+  return kPanelHeader + kPanelWarps * panel_stage_bytes<T>() + kPanelCols * int(sizeof(T));
+}
+static_assert(panel_smem_bytes<double>() <= 232448, "panel kernel shared memory");
 static_assert(kPanelCols <= 0xffff, "panel column in 16 bits");
 
 template <typename T>
@@ -64,43 +74,20 @@ struct PanelParams {
 
 template <typename T> __device__ __forceinline__ double panel_prod(T v, T x) { return double(mul_rn(v, x)); }
 
-// Entries [j0, j0 + 8) of the panel stream, 16-byte vector loads (the
-// arrays are padded, csr_panel_build).
-__device__ __forceinline__ void panel_load(const uint16_t* __restrict__ pcol, const double* __restrict__ pval,
-                                           uint32_t j0, uint16_t (&c)[kPanelK], double (&v)[kPanelK]) {
-  const uint4 cw = __ldcs(reinterpret_cast<const uint4*>(pcol + j0));
-  const uint32_t w[4] = {cw.x, cw.y, cw.z, cw.w};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    c[2 * k] = uint16_t(w[k] & 0xffffu);
-    c[2 * k + 1] = uint16_t(w[k] >> 16);
-  }
-  const double2* vp = reinterpret_cast<const double2*>(pval + j0);
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const double2 d = __ldcs(vp + k);
-    v[2 * k] = d.x;
-    v[2 * k + 1] = d.y;
-  }
+// Stream layout: within each 256-entry step (absolute entry index
+// multiple of 256) the lane-contiguous order is transposed, so a lane's k-th
+// entry sits at k * 32 + lane: values at step * 256 + k * 32 + lane, column
+// pairs (entries 2m, 2m+1 of a lane in one 32-bit word) at word
+// step * 128 + m * 32 + lane, and the lane's 8 start bits at byte
+// step * 32 + lane.  Shared-memory reads of a staged step are then
+// conflict-free.
+__host__ __device__ __forceinline__ uint32_t panel_val_pos(uint32_t i) {
+  const uint32_t r = i & (kPanelStep - 1);
+  return (i - r) + (r & (kPanelK - 1)) * 32 + (r >> 3);
 }
-__device__ __forceinline__ void panel_load(const uint16_t* __restrict__ pcol, const float* __restrict__ pval,
-                                           uint32_t j0, uint16_t (&c)[kPanelK], float (&v)[kPanelK]) {
-  const uint4 cw = __ldcs(reinterpret_cast<const uint4*>(pcol + j0));
-  const uint32_t w[4] = {cw.x, cw.y, cw.z, cw.w};
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    c[2 * k] = uint16_t(w[k] & 0xffffu);
-    c[2 * k + 1] = uint16_t(w[k] >> 16);
-  }
-  const float4* vp = reinterpret_cast<const float4*>(pval + j0);
-#pragma unroll
-  for (int k = 0; k < 2; ++k) {
-    const float4 d = __ldcs(vp + k);
-    v[4 * k] = d.x;
-    v[4 * k + 1] = d.y;
-    v[4 * k + 2] = d.z;
-    v[4 * k + 3] = d.w;
-  }
+__host__ __device__ __forceinline__ uint32_t panel_col_pos(uint32_t i) {  // u16 index
+  const uint32_t r = i & (kPanelStep - 1), k = r & (kPanelK - 1);
+  return (i - r) + (k >> 1) * 64 + (r >> 3) * 2 + (k & 1);
 }
 
 __device__ __forceinline__ void st_if(double* p, double v, bool pred) {
@@ -109,8 +96,8 @@ __device__ __forceinline__ void st_if(double* p, double v, bool pred) {
                : "memory");
 }
 
-// Columns (8 x 16 bit) and values of one lane's 8 entries, and the step's
-// segment-start byte of this lane (bit k: entry k starts a segment).
+// A lane's 8 entries of one step: columns, values, start bits (bit k: its
+// entry k starts a segment).
 template <typename T>
 struct PanelRegs {
   uint16_t c[kPanelK];
@@ -118,11 +105,33 @@ struct PanelRegs {
   unsigned fl;
 };
 
+// Warp stage: [0, 256 sizeof(T)) values, then 128 column-pair words, then
+// 32 start-bit bytes.  Issued by lane 0 (three TMA bulk copies on the warp's
+// mbarrier); read back into registers by every lane.
 template <typename T>
-__device__ __forceinline__ void panel_fetch(const uint16_t* __restrict__ pcol, const T* __restrict__ pval,
-                                            const uint8_t* __restrict__ pflag, uint32_t j0, PanelRegs<T>& r) {
-  panel_load(pcol, pval, j0, r.c, r.v);
-  r.fl = __ldcs(pflag + (j0 >> 3));
+__device__ __forceinline__ void panel_issue(unsigned char* stage, uint64_t* bar, const uint16_t* __restrict__ pcol,
+                                            const T* __restrict__ pval, const uint8_t* __restrict__ pflag,
+                                            uint32_t base) {
+  constexpr uint32_t vb = kPanelStep * sizeof(T), cb = kPanelStep * 2;
+  mbar_arrive_expect_tx(bar, vb + cb + 32);
+  bulk_g2s(stage, pval + base, vb, bar, true);
+  bulk_g2s(stage + vb, pcol + base, cb, bar, true);
+  bulk_g2s(stage + vb + cb, pflag + base / 8, 32, bar, true);
+}
+
+template <typename T>
+__device__ __forceinline__ void panel_read(const unsigned char* stage, int lane, PanelRegs<T>& r) {
+  const T* vs = reinterpret_cast<const T*>(stage);
+  const uint32_t* cs = reinterpret_cast<const uint32_t*>(stage + kPanelStep * sizeof(T));
+#pragma unroll
+  for (int k = 0; k < kPanelK; ++k) r.v[k] = vs[k * 32 + lane];
+#pragma unroll
+  for (int m = 0; m < kPanelK / 2; ++m) {
+    const uint32_t w = cs[m * 32 + lane];
+    r.c[2 * m] = uint16_t(w & 0xffffu);
+    r.c[2 * m + 1] = uint16_t(w >> 16);
+  }
+  r.fl = stage[kPanelStep * sizeof(T) + kPanelStep * 2 + lane];
 }
 
 // One step of a warp slice: 32 lanes x kPanelK consecutive entries at
@@ -135,16 +144,18 @@ __device__ __forceinline__ void panel_step(const T* __restrict__ xs, const Panel
                                            int lo_ok, double* __restrict__ part_open, int& open_adv,
                                            double& carry) {
   const unsigned fl = FULL ? r.fl : (r.fl & ok);
-  // segments started before this lane in the step (exclusive scan)
+  // segments started before this lane in the step: the flag counts (<= 8)
+  // summed bit-plane by bit-plane with ballots (no shuffles)
   const int nf = __popc(fl);
-  int incl = nf;
+  const unsigned lt = (1u << lane) - 1u;
+  int before = 0, total = 0;
 #pragma unroll
-  for (int d = 1; d < 32; d <<= 1) {
-    const int t = __shfl_up_sync(0xffffffffu, incl, d);
-    if (lane >= d) incl += t;
+  for (int bit = 0; bit < 4; ++bit) {
+    const unsigned m = __ballot_sync(0xffffffffu, (nf >> bit) & 1);
+    before += __popc(m & lt) << bit;
+    total += __popc(m) << bit;
   }
-  const int before = incl - nf;
-  open_adv = __shfl_sync(0xffffffffu, incl, 31);
+  open_adv = total;
   double p[kPanelK];
 #pragma unroll
   for (int k = 0; k < kPanelK; ++k) {
@@ -167,7 +178,7 @@ __device__ __forceinline__ void panel_step(const T* __restrict__ xs, const Panel
   }
   // segmented inclusive scan over lanes of (started, run); lane 0 first
   // takes the carried segment.  A lane adds the value d lanes up only while
-  // no segment starts between (its last start at or before it: `ls`).
+  // no segment starts between (its last start at or before it: `reach`).
   if (lane == 0) {
     if (started)
       head = __dadd_rn(carry, head);
@@ -175,7 +186,7 @@ __device__ __forceinline__ void panel_step(const T* __restrict__ xs, const Panel
       run = __dadd_rn(carry, run);
   }
   const unsigned smask = __ballot_sync(0xffffffffu, started) & ((2u << lane) - 1u);
-  const int reach = smask ? lane - (31 - __clz(smask)) : lane + 1;  // lanes back to (not incl.) the last start
+  const int reach = smask ? lane - (31 - __clz(smask)) : lane + 1;
   double sc = run;
 #pragma unroll
   for (int d = 1; d < 32; d <<= 1) {
@@ -189,39 +200,41 @@ __device__ __forceinline__ void panel_step(const T* __restrict__ xs, const Panel
 
 // One warp's slice [b, e) of the panel stream (b is a segment start, seg0
 // its segment index; the slice ends at a segment start or the item end).
-// Software pipeline, one step ahead in two register sets: the next step's
-// columns, values and start bits load while this step is reduced.
+// The warp's stage is refilled by TMA with the next step as soon as this
+// step is in registers, so the copy runs while the step is reduced.
 template <typename T>
 __device__ __forceinline__ void panel_slice(const uint16_t* __restrict__ pcol, const T* __restrict__ pval,
                                             const uint8_t* __restrict__ pflag, double* __restrict__ part,
-                                            const T* __restrict__ xs, uint32_t b, uint32_t e, uint32_t seg0,
-                                            int lane) {
+                                            const T* __restrict__ xs, unsigned char* stage, uint64_t* bar,
+                                            uint32_t& phase, uint32_t b, uint32_t e, uint32_t seg0, int lane) {
   if (b >= e) return;
-  constexpr uint32_t STEP = 32 * kPanelK;
   double carry = 0.0;                // the open segment's sum over earlier steps
   int64_t open = int64_t(seg0) - 1;  // index of the segment open before this step (seg0 - 1: none)
-  uint32_t base = b & ~(STEP - 1);
-  PanelRegs<T> ra, rb;
-  panel_fetch(pcol, pval, pflag, base + uint32_t(lane) * kPanelK, ra);
-  auto run_step = [&](const PanelRegs<T>& cur, PanelRegs<T>& nxt) -> bool {
+  uint32_t base = b & ~uint32_t(kPanelStep - 1);
+  if (lane == 0) panel_issue(stage, bar, pcol, pval, pflag, base);
+  for (; base < e; base += kPanelStep) {
     const uint32_t j0 = base + uint32_t(lane) * kPanelK;
-    const bool more = base + STEP < e;
-    if (more) panel_fetch(pcol, pval, pflag, j0 + STEP, nxt);
+    const bool more = base + kPanelStep < e;
+    PanelRegs<T> r;
+    mbar_wait(bar, phase);
+    phase ^= 1u;
+    panel_read(stage, lane, r);
+    __syncwarp();
+    if (more && lane == 0) {
+      fence_proxy_async();
+      panel_issue(stage, bar, pcol, pval, pflag, base + kPanelStep);
+    }
     const int lo_ok = open < int64_t(seg0) ? 1 : 0;  // relative index 0 is seg0 - 1 (none) on the first step
     int adv = 0;
-    if (base >= b && base + STEP <= e) {
-      panel_step<T, true>(xs, cur, 0xffu, lane, lo_ok, part + open, adv, carry);
+    if (base >= b && base + kPanelStep <= e) {
+      panel_step<T, true>(xs, r, 0xffu, lane, lo_ok, part + open, adv, carry);
     } else {
       const int lo = min(max(int(int64_t(b) - int64_t(j0)), 0), kPanelK);
       const int hi = min(max(int(int64_t(e) - int64_t(j0)), 0), kPanelK);
       const unsigned ok = ((1u << hi) - 1u) & ~((1u << lo) - 1u);
-      panel_step<T, false>(xs, cur, ok, lane, lo_ok, part + open, adv, carry);
+      panel_step<T, false>(xs, r, ok, lane, lo_ok, part + open, adv, carry);
     }
     open += adv;
-    base += STEP;
-    return more;
-  };
-  while (run_step(ra, rb) && run_step(rb, ra)) {
   }
   if (lane == 0 && open >= int64_t(seg0)) part[open] = carry;  // the slice's last segment
 }
@@ -229,15 +242,14 @@ __device__ __forceinline__ void panel_slice(const uint16_t* __restrict__ pcol, c
 template <typename T>
 __global__ void __launch_bounds__(kPanelWarps * 32, 1) csr_panel_kernel(const __grid_constant__ PanelParams<T> P) {
   extern __shared__ __align__(128) unsigned char panel_smem[];
-  T* xs = reinterpret_cast<T*>(panel_smem + 128);
   uint64_t* bar = reinterpret_cast<uint64_t*>(panel_smem);
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  if (threadIdx.x == 0) {
-    mbar_init(bar, 1);
-    mbar_fence_init();
-  }
+  unsigned char* stage = panel_smem + kPanelHeader + warp * panel_stage_bytes<T>();
+  T* xs = reinterpret_cast<T*>(panel_smem + kPanelHeader + kPanelWarps * panel_stage_bytes<T>());
+  if (threadIdx.x < 1 + kPanelWarps) mbar_init(&bar[threadIdx.x], 1);
+  if (threadIdx.x == 0) mbar_fence_init();
   __syncthreads();
-  uint32_t phase = 0;
+  uint32_t phase = 0, wphase = 0;
   for (uint32_t it = P.cta_item[blockIdx.x]; it < P.cta_item[blockIdx.x + 1]; ++it) {
     const int64_t c0 = int64_t(P.item_panel[it]) * kPanelCols;  // global column of xs[0]
     const int64_t lo = max(c0, P.col_base), hi = min(min(c0 + kPanelCols, P.col_base + P.x_len), P.ncols);
@@ -265,7 +277,7 @@ __global__ void __launch_bounds__(kPanelWarps * 32, 1) csr_panel_kernel(const __
     const uint32_t t = it * kPanelWarps + uint32_t(warp);
     const uint32_t b = P.task_begin[t];
     const uint32_t e = warp + 1 < kPanelWarps ? P.task_begin[t + 1] : P.item_end[it];
-    panel_slice<T>(P.pcol, P.pval, P.pflag, P.part, xs, b, e, P.task_seg0[t], lane);
+    panel_slice<T>(P.pcol, P.pval, P.pflag, P.part, xs, stage, &bar[1 + warp], wphase, b, e, P.task_seg0[t], lane);
   }
 }
 
@@ -284,7 +296,19 @@ __global__ void csr_panel_finish_kernel(const uint32_t* __restrict__ lrow, const
     double s = -0.0;
     if (k < n_long) {
       const uint32_t p0 = __ldg(ptr + k), p1 = __ldg(ptr + k + 1);
-      for (uint32_t i = p0 + sub; i < p1; i += 8) s = __dadd_rn(s, __ldg(part + __ldg(rseg + i)));
+      // batches of 8 partials per lane: indices, then values, all in
+      // flight, then added in order
+      for (uint32_t i0 = p0 + sub; i0 < p1; i0 += 64) {
+        uint32_t idx[8];
+        double val[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) idx[u] = i0 + 8u * u < p1 ? __ldg(rseg + i0 + 8u * u) : 0u;
+#pragma unroll
+        for (int u = 0; u < 8; ++u) val[u] = i0 + 8u * u < p1 ? __ldg(part + idx[u]) : 0.0;
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (i0 + 8u * u < p1) s = __dadd_rn(s, val[u]);
+      }
     }
 #pragma unroll
     for (int o = 4; o >= 1; o >>= 1) s = __dadd_rn(s, __shfl_xor_sync(0xffffffffu, s, o));
@@ -322,8 +346,8 @@ __global__ void panel_gather_kernel(const uint32_t* __restrict__ skey, const uin
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < nl; i += int64_t(gridDim.x) * blockDim.x) {
     const uint32_t le = perm[i], e = eidx[le], q = skey[i];
     const bool start = i == 0 || skey[i - 1] != q || erow[perm[i - 1]] != erow[le];
-    pcol[i] = uint16_t(aj[e] - q * uint32_t(kPanelCols));
-    pval[i] = av[e];
+    pcol[panel_col_pos(uint32_t(i))] = uint16_t(aj[e] - q * uint32_t(kPanelCols));
+    pval[panel_val_pos(uint32_t(i))] = av[e];
     flag[i] = start ? 1u : 0u;
   }
 }
@@ -381,36 +405,79 @@ __global__ void split_rows_scatter_kernel(const uint32_t* __restrict__ is_long, 
   }
 }
 
-// Lengths of listed rows (for the scans of lptr / the short CSR's IRP).
+// Lengths of listed rows.
 __global__ void listed_lengths_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ rows, int64_t n,
                                       uint32_t* __restrict__ len) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < n; i += int64_t(gridDim.x) * blockDim.x)
     len[i] = irp[rows[i] + 1] - irp[rows[i]];
 }
 
-// The short rows as their own CSR (a warp per row copies its entries).
+// Short rows (<= 32 entries) grouped by exact length L: rows [cls[L],
+// cls[L+1]) of the sorted list have L entries, stored column-major from
+// ebase[L]: entry j of the class's r-th row at ebase[L] + j * n_L + r.
+constexpr int kShortClasses = 33;  // lengths 0..32
+struct ShortEll {
+  uint32_t cls[kShortClasses + 1];
+  uint32_t ebase[kShortClasses];
+};
+
+__device__ __forceinline__ int short_class(const ShortEll& P, uint32_t i) {
+  int L = 0;  // the last class whose first row is <= i
+#pragma unroll
+  for (int step = 32; step >= 1; step >>= 1)
+    if (L + step <= kShortClasses - 1 && P.cls[L + step] <= i) L += step;
+  return L;
+}
+
 template <typename T>
-__global__ void short_copy_kernel(const uint32_t* __restrict__ irp, const uint32_t* __restrict__ aj,
-                                  const T* __restrict__ av, const uint32_t* __restrict__ srow,
-                                  const uint32_t* __restrict__ sirp, int64_t ns, uint32_t* __restrict__ saj,
-                                  T* __restrict__ sav) {
+__global__ void short_ell_fill_kernel(const __grid_constant__ ShortEll P, const uint32_t* __restrict__ irp,
+                                      const uint32_t* __restrict__ aj, const T* __restrict__ av,
+                                      const uint32_t* __restrict__ srow, int64_t ns, uint32_t* __restrict__ scol,
+                                      T* __restrict__ sval) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < ns; i += int64_t(gridDim.x) * blockDim.x) {
-    const uint32_t s = irp[srow[i]], d = sirp[i], n = sirp[i + 1] - d;
-    for (uint32_t j = 0; j < n; ++j) {
-      saj[d + j] = aj[s + j];
-      sav[d + j] = av[s + j];
+    const int L = short_class(P, uint32_t(i));
+    const uint32_t r = uint32_t(i) - P.cls[L], n = P.cls[L + 1] - P.cls[L], s = irp[srow[i]];
+    for (int j = 0; j < L; ++j) {
+      scol[P.ebase[L] + uint32_t(j) * n + r] = aj[s + j];
+      sval[P.ebase[L] + uint32_t(j) * n + r] = av[s + j];
     }
   }
 }
 
-// Listed rows with no entries (the short CSR's empty rows), original ids.
-__global__ void empty_listed_kernel(const uint32_t* __restrict__ sirp, const uint32_t* __restrict__ srow, int64_t ns,
-                                    uint32_t* __restrict__ out, unsigned long long* __restrict__ n) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < ns; i += int64_t(gridDim.x) * blockDim.x)
-    if (sirp[i + 1] == sirp[i]) {
-      const unsigned long long k = atomicAdd(n, 1ull);
-      if (out) out[k] = srow[i];
+// y of the short rows: one thread per row, its entries left to right from
+// -0.0 (cumsum order, kernels.py:81: bit-exact), empty rows +0.0.  Rows of
+// a warp share their length class, so the loop is uniform; loads are
+// coalesced (column-major classes), gathers 4 in flight.
+template <typename T>
+__global__ void __launch_bounds__(256) short_ell_kernel(const __grid_constant__ ShortEll P,
+                                                        const uint32_t* __restrict__ scol, const T* __restrict__ sval,
+                                                        const uint32_t* __restrict__ srow, int64_t ns,
+                                                        const T* __restrict__ x, int64_t col_base, T* __restrict__ y) {
+  const T* xb = x - col_base;
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < ns; i += int64_t(gridDim.x) * blockDim.x) {
+    const int L = short_class(P, uint32_t(i));
+    const uint32_t n = P.cls[L + 1] - P.cls[L];
+    const uint32_t o = P.ebase[L] + (uint32_t(i) - P.cls[L]);
+    const uint32_t* cp = scol + o;
+    const T* vp = sval + o;
+    T acc = T(-0.0);
+    int j = 0;
+    for (; j + 4 <= L; j += 4) {
+      uint32_t c[4];
+      T v[4], xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        c[u] = __ldcs(cp + uint32_t(j + u) * n);
+        v[u] = __ldcs(vp + uint32_t(j + u) * n);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; ++u) xv[u] = ldx(xb + c[u]);
+#pragma unroll
+      for (int u = 0; u < 4; ++u) acc = add_rn(acc, mul_rn(v[u], xv[u]));
     }
+    for (; j < L; ++j) acc = add_rn(acc, mul_rn(__ldcs(vp + uint32_t(j) * n), ldx(xb + __ldcs(cp + uint32_t(j) * n))));
+    y[srow[i]] = L == 0 ? T(0) : acc;
+  }
 }
 
 template <typename T>

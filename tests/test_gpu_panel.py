@@ -18,7 +18,7 @@ import pytest
 
 pytestmark = pytest.mark.gpu
 
-PANEL = 28672  # csrc/panel.cuh kPanelCols
+PANEL = 23552  # csrc/panel.cuh kPanelCols
 
 
 @pytest.fixture(scope="module")
