@@ -91,7 +91,9 @@ typedef struct {
     int32_t dia_kernel;       /* DIA (groups, stages, threads) 0..4; -1 = auto        */
     int32_t dia_rows;         /* DIA rows per tile, multiple of 8; 0 = auto           */
     int32_t flags;            /* experiments: bit0 products mode, bit1 warp per long  */
-                              /* segment (tile kernels); 0 = off                      */
+                              /* segment (tile kernels); bit2: the panel path's short */
+                              /* rows start from +0.0 (np.add.at order; COO plans set */
+                              /* it for their CSR view); 0 = off                      */
     int32_t panels;           /* CSR column-panel path for long rows: -1 auto (rows   */
                               /* over 32 entries hold >= half the entries, ncols >=   */
                               /* 65536), 0 off, 1 on (needs col_indices and values at */

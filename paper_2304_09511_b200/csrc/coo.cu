@@ -664,6 +664,14 @@ struct spmv_coo_plan {
   size_t off_head_row = 0, off_tail_row = 0, off_pass = 0, off_head_val = 0, off_tail_val = 0;
   size_t off_ws_head = 0, off_ws_tail = 0, off_ws_ctr = 0, off_steps = 0;
   mutable StreamSlots vla_scratch;  // two-phase vla step sums (nnz values), per stream
+  // column-panel path (csr.cu / panel.cuh) through a CSR view of the
+  // row-sorted triples: whole-matrix products with the create-time arrays
+  spmv_csr_plan* csr_view = nullptr;
+  DevBuf view_irp;
+  const void* view_ai = nullptr;
+  const void* view_aj = nullptr;
+  const void* view_av = nullptr;
+  ~spmv_coo_plan() { spmv_csr_plan_destroy(csr_view); }
   std::mutex build_mu;              // the lazily built vla lists
   int groups = 1;                // consumer groups per tile CTA (coo_tile_kernel G)
   int grid = 0, grid_direct = 0;  // G-group TMA kernel / single-group kernel
@@ -761,6 +769,19 @@ static bool coo_config_known(int64_t tile, int groups) {
   SPMV_COO_CONFIGS(X)
 #undef X
   return false;
+}
+
+// irp[r] = first entry of row r in non-decreasing rows (binary search).
+__global__ void row_bounds_kernel(const uint32_t* __restrict__ rows, int64_t nnz, int64_t nrows,
+                                  uint32_t* __restrict__ irp) {
+  for (int64_t r = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; r <= nrows; r += int64_t(gridDim.x) * blockDim.x) {
+    int64_t lo = 0, hi = nnz;
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (int64_t(rows[mid]) < r) lo = mid + 1; else hi = mid;
+    }
+    irp[r] = uint32_t(lo);
+  }
 }
 
 __global__ void count_long_runs_kernel(const uint32_t* __restrict__ run_start, int64_t n_runs,
@@ -942,6 +963,34 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
     if (!coo_config_known(p->tile, 1)) p->tile = 2048;
   }
   p->ntiles = (nnz + p->tile - 1) / p->tile;
+  if (p->n_long > 0 && p->cfg.panels != 0) {
+    // a CSR view (row pointers over the sorted rows; same column and value
+    // arrays): if its plan takes the column-panel path, whole-matrix COO
+    // products run it (short rows from +0.0: np.add.at order)
+    const uint32_t* vaj = p->row_sorted ? aj : p->sorted_aj.as<uint32_t>();
+    const void* vav = p->row_sorted ? av : p->sorted_av.ptr;
+    if ((rc = p->view_irp.alloc(4 * (p->nrows + 1)))) return rc;
+    const int64_t gr = std::min<int64_t>((p->nrows + 256) / 256, int64_t(sm_count()) * 16);
+    row_bounds_kernel<<<unsigned(gr), 256, 0, st>>>(rows, nnz, p->nrows, p->view_irp.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+    spmv_plan_config vc = p->cfg;
+    vc.flags |= 4;
+    spmv_csr_plan* v = nullptr;
+    if ((rc = spmv_csr_plan_create_ex(p->dtype, p->nrows, p->ncols, nnz, p->view_irp.as<uint32_t>(), vaj, vav, &vc,
+                                      st, &v)))
+      return rc;
+    int path = 0;
+    spmv_csr_plan_path(v, &path, nullptr);
+    if (path == 2) {
+      p->csr_view = v;
+      p->view_ai = ai;
+      p->view_aj = aj;
+      p->view_av = av;
+    } else {
+      spmv_csr_plan_destroy(v);
+      p->view_irp.release();
+    }
+  }
   p->tma_hint = p->cfg.tma_hint != 0;  // COO: evict_first on the matrix stream unless turned off
   p->ws_ranges_per_warp = p->cfg.ranges_per_warp >= 1 && p->cfg.ranges_per_warp <= 64 ? p->cfg.ranges_per_warp : 8;
   if ((rc = coo_ws_build(p, st))) return rc;
@@ -1087,7 +1136,11 @@ static int coo_run_ws(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t
 
 template <typename T>
 static int coo_run(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const T* av, const T* x,
-                   int64_t col_base, T* y, cudaStream_t st) {
+                   int64_t col_base, T* y, cudaStream_t st, int64_t x_len = -1) {
+  if (p->csr_view && ai == p->view_ai && aj == p->view_aj && av == p->view_av)
+    return spmv_csr(p->csr_view, p->view_irp.as<uint32_t>(), p->row_sorted ? aj : p->sorted_aj.as<uint32_t>(),
+                    p->row_sorted ? static_cast<const void*>(av) : p->sorted_av.ptr, x, col_base,
+                    x_len < 0 ? p->ncols - col_base : x_len, y, st);
   if (p->ws && p->nrows > 0 && p->nnz > 0) return coo_run_ws<T>(p, ai, aj, av, x, col_base, y, st);
 #define X(TL, GR) \
   if (p->tile == TL && p->groups == GR) return coo_run_tiled<T, TL, GR>(p, ai, aj, av, x, col_base, y, st);
@@ -1159,6 +1212,7 @@ int spmv_coo_plan_config(const spmv_coo_plan* p, spmv_plan_config* out) {
   out->warp_stream = p->ws ? 1 : 0;
   out->ranges_per_warp = int32_t(p->ws_ranges_per_warp);
   out->tma_hint = p->tma_hint ? 1 : 0;
+  out->panels = p->csr_view ? 1 : 0;
   return SPMV_OK;
 }
 
@@ -1207,7 +1261,9 @@ int spmv_coo_plan_info(const spmv_coo_plan* p, int64_t* n_runs, int64_t* n_long_
   if (n_long_runs) *n_long_runs = p->n_long;
   if (n_items) *n_items = p->tile;
   if (row_sorted) *row_sorted = p->row_sorted ? 1 : 0;
-  if (launches && p->ws)
+  if (launches && p->csr_view)
+    spmv_csr_plan_info(p->csr_view, nullptr, nullptr, launches);
+  else if (launches && p->ws)
     *launches = 1 + (p->ws_n_span > 0 ? 1 : 0);
   else if (launches)
     *launches = (p->nrows > 0 ? 1 : 0) + (p->n_long > 0 ? 1 : 0) +
@@ -1217,8 +1273,11 @@ int spmv_coo_plan_info(const spmv_coo_plan* p, int64_t* n_runs, int64_t* n_long_
 
 int spmv_coo_plan_path(const spmv_coo_plan* p, int* warp_stream, int64_t* nwarps) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
-  if (warp_stream) *warp_stream = p->ws ? 1 : 0;
-  if (nwarps) *nwarps = p->ws_nwarps;
+  if (warp_stream) *warp_stream = p->csr_view ? 2 : p->ws ? 1 : 0;
+  if (nwarps) {
+    *nwarps = p->ws_nwarps;
+    if (p->csr_view) spmv_csr_plan_path(p->csr_view, nullptr, nwarps);
+  }
   return SPMV_OK;
 }
 
@@ -1237,9 +1296,9 @@ int spmv_coo(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, con
   cudaStream_t st = as_stream(stream);
   if (p->dtype == SPMV_F64)
     return coo_run<double>(p, ai, aj, static_cast<const double*>(av), static_cast<const double*>(x), col_base,
-                           static_cast<double*>(y), st);
+                           static_cast<double*>(y), st, x_len);
   return coo_run<float>(p, ai, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
-                        static_cast<float*>(y), st);
+                        static_cast<float*>(y), st, x_len);
 }
 
 int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const void* av, const void* x,

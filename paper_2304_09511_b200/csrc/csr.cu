@@ -945,7 +945,8 @@ static int csr_run_panel(const spmv_csr_plan* p, const T* x, int64_t col_base, i
   if (p->pn_short > 0) {
     const int64_t gs = std::min<int64_t>((p->pn_short + 255) / 256, int64_t(sm_count()) * 16);
     short_ell_kernel<T><<<unsigned(gs), 256, 0, st>>>(p->pn_ell, p->pn_scol.as<uint32_t>(), p->pn_sval.as<T>(),
-                                                      p->pn_srow.as<uint32_t>(), p->pn_short, x, col_base, y);
+                                                      p->pn_srow.as<uint32_t>(), p->pn_short, x, col_base, y,
+                                                      (p->cfg.flags & 4) != 0);
     SPMV_LAUNCH_CHECK();
   }
   if (p->pn_long == 0) return SPMV_OK;

@@ -445,14 +445,17 @@ __global__ void short_ell_fill_kernel(const __grid_constant__ ShortEll P, const 
 }
 
 // y of the short rows: one thread per row, its entries left to right from
-// -0.0 (cumsum order, kernels.py:81: bit-exact), empty rows +0.0.  Rows of
+// -0.0 (cumsum order, kernels.py:81: bit-exact) or, for COO plans
+// (pos_seed), from +0.0 (np.add.at on a zeroed y, kernels.py:65); empty
+// rows +0.0.  Rows of
 // a warp share their length class, so the loop is uniform; loads are
 // coalesced (column-major classes), gathers 4 in flight.
 template <typename T>
 __global__ void __launch_bounds__(256) short_ell_kernel(const __grid_constant__ ShortEll P,
                                                         const uint32_t* __restrict__ scol, const T* __restrict__ sval,
                                                         const uint32_t* __restrict__ srow, int64_t ns,
-                                                        const T* __restrict__ x, int64_t col_base, T* __restrict__ y) {
+                                                        const T* __restrict__ x, int64_t col_base, T* __restrict__ y,
+                                                        bool pos_seed) {
   const T* xb = x - col_base;
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i < ns; i += int64_t(gridDim.x) * blockDim.x) {
     const int L = short_class(P, uint32_t(i));
@@ -460,7 +463,7 @@ __global__ void __launch_bounds__(256) short_ell_kernel(const __grid_constant__ 
     const uint32_t o = P.ebase[L] + (uint32_t(i) - P.cls[L]);
     const uint32_t* cp = scol + o;
     const T* vp = sval + o;
-    T acc = T(-0.0);
+    T acc = pos_seed ? T(0) : T(-0.0);
     int j = 0;
     for (; j + 4 <= L; j += 4) {
       uint32_t c[4];

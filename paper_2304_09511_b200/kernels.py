@@ -143,7 +143,7 @@ class _Plan:
         info = {"runs": a.value, "long_runs": b.value, "tile": c.value, "row_sorted": bool(d.value),
                 "launches": e.value, "groups": g.value, "kernel": "tile", "config": self.config().as_dict()}
         if ws.value:
-            info.update(kernel="warp_stream", warps=nw.value)
+            info.update(kernel="panel" if ws.value == 2 else "warp_stream", warps=nw.value)
         return info
 
 

@@ -136,3 +136,33 @@ def test_panel_vla_and_host_paths_unaffected(sp):
     yh = torch.empty(n, dtype=torch.float64).pin_memory()
     sp.spmv_csr_plain(A, xh, out=yh)
     _check(yh.numpy(), c_oracle.csr_plain(n, irp, cols, vals, x), lens, 1e-12)
+
+
+@pytest.mark.parametrize("shuffle", [False, True])
+def test_coo_panel_view(sp, shuffle):
+    """COO plans with long runs take the panel path through a CSR view of
+    the row-sorted triples: short rows bit-exact with np.add.at order (from
+    +0.0, so a lone -0.0 product gives +0.0), long rows within 1e-12; an
+    unsorted input (stable row sort, storage order kept) too."""
+    from oracle import c_oracle
+    from paper_2304_09511_b200 import kernels as K
+    rng = np.random.default_rng(23)
+    n, ncols = 30_000, 300_000
+    lens = np.minimum(rng.zipf(1.7, n), 8000)
+    irp, cols, vals = _matrix(rng, n, ncols, lens)
+    vals[irp[5]] = -0.0  # row 5's first product is -0.0
+    x = rng.uniform(-1, 1, ncols)
+    rows = np.repeat(np.arange(n), lens).astype(np.uint32)
+    if shuffle:
+        order = rng.permutation(rows.shape[0])
+        rows, cols, vals = rows[order], cols[order], vals[order]
+    A = sp.CooMatrix.from_arrays(n, ncols, rows, cols, vals, sorted=not shuffle)
+    p = K.coo_plan(A)
+    assert p.info()["kernel"] == "panel" and p.config().panels == 1
+    y = sp.spmv_coo_plain(A, x)
+    ref = c_oracle.coo_plain(n, rows, cols, vals, x, row_sorted=not shuffle)
+    _check(y, ref, lens, 1e-12)
+    yw = sp.spmv_coo_plain(A, x, plan_config=sp.PlanConfig(panels=0))
+    assert K.coo_plan(A, config=sp.PlanConfig(panels=0)).info()["kernel"] == "warp_stream"
+    from _util import rel_err
+    assert rel_err(y, yw) <= 1e-12
