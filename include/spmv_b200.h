@@ -193,18 +193,40 @@ int spmv_csr_range(const spmv_csr_plan* plan, const uint32_t* row_pointers,
                    int64_t tile_begin, int64_t tile_end, int fixup,
                    void* stream);
 
-/* Host x -> host y (both pinned for overlap): x is uploaded in `chunks`
- * column pieces on a plan-owned copy stream, tile ranges run on `stream`
- * as soon as the x prefix they read has arrived, and finished rows of y are
- * downloaded on a second copy stream while later tiles run (PCIe is full
- * duplex).  Device staging lives in the plan (not reentrant per plan).
- * Asynchronous: y_host is valid once `stream` is synchronised.
- * x goes up in chunks that ramp up to ncols / chunks columns (at least 1M)
- * and down again at the end; each tile range runs once the x it reads has
- * arrived.  chunks <= 0 selects the default (16). */
+/* Host x -> host y (see "host-buffer products" below; the plan owns the
+ * pipe): x goes up in chunks that ramp up to ncols / chunks columns (at
+ * least 1M) and down again at the end; each tile range runs once the x it
+ * reads has arrived (plans whose whole-matrix kernel is the panel or
+ * warp-stream kernel run it once x is complete).  chunks <= 0 = 16. */
 int spmv_csr_host(spmv_csr_plan* plan, const uint32_t* row_pointers,
                   const uint32_t* col_indices, const void* values,
                   const void* x_host, void* y_host, int chunks, void* stream);
+
+/* ---- host-buffer products (hostpipe.cuh) ------------------------------- */
+/* The reference's calling convention: x in host memory, a fresh y in host
+ * memory (kernels.py:46-53, :59, :72, :94).  x goes up in column chunks on
+ * a copy stream, each part of the product runs as soon as the x prefix it
+ * reads has arrived, finished rows of y come down on a second copy stream.
+ * Pinned x is copied directly; pageable x is staged through a pinned ring
+ * by host threads.  Pinned y overlaps its copies (pageable y is correct but
+ * not overlapped).  Asynchronous: y_host is valid once `stream` is
+ * synchronised.  One pipe (the CSR / COO plan's own, or an spmv_host_pipe)
+ * runs one call at a time; calls on it are serialised.  chunks <= 0 = 16. */
+typedef struct spmv_host_pipe spmv_host_pipe;
+typedef struct spmv_coo_plan spmv_coo_plan;
+int spmv_host_pipe_create(spmv_host_pipe** out);
+int spmv_host_pipe_destroy(spmv_host_pipe* pipe);
+/* COO: x chunks up, the whole product, y down. */
+int spmv_coo_host(spmv_coo_plan* plan, const uint32_t* row_indices,
+                  const uint32_t* col_indices, const void* values,
+                  const void* x_host, void* y_host, int chunks, void* stream);
+/* DIA: row blocks as soon as x holds row + max_offset (the largest offset,
+ * >= 0 if any diagonal is above the main one). */
+int spmv_dia_host(spmv_host_pipe* pipe, int dtype, int64_t nrows, int64_t ncols,
+                  int64_t ndiags, int64_t padded_rows, const int32_t* offsets,
+                  int64_t max_offset, const void* values, const void* x_host,
+                  void* y_host, int chunks, const spmv_plan_config* cfg,
+                  void* stream);
 
 /* Sub-warp vector kernel, lane l accumulates entries s+l, s+l+L, ... then a
  * pairwise-halving tree over next_pow2(L) lanes: bit-exact with

@@ -69,6 +69,10 @@ SIGNATURES = {
     "spmv_coo_plan_groups": [_vp, _pint],
     "spmv_coo_plan_path": [_vp, _pint, _pi64],
     "spmv_csr_host": [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _vp],
+    "spmv_host_pipe_create": [_pvp],
+    "spmv_host_pipe_destroy": [_vp],
+    "spmv_coo_host": [_vp, _vp, _vp, _vp, _vp, _vp, _c_int, _vp],
+    "spmv_dia_host": [_vp, _c_int, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _c_i64, _vp, _vp, _vp, _c_int, _vp, _vp],
     "spmv_csr_plan_tile_info": [_vp, _vp, _vp, _vp, _vp],
     "spmv_csr_range": [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _c_i64, _c_i64, _c_int, _vp],
     "spmv_csr_vla": [_c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _c_int, _vp],

@@ -25,6 +25,8 @@
 // they are not (np.add.at order inside a row = storage order, kept).
 #include <cub/cub.cuh>
 
+#include "hostpipe.cuh"
+
 #include <algorithm>
 #include <type_traits>
 #include <vector>
@@ -671,6 +673,7 @@ struct spmv_coo_plan {
   const void* view_ai = nullptr;
   const void* view_aj = nullptr;
   const void* view_av = nullptr;
+  HostPipe host;  // host-buffer products (hostpipe.cuh)
   ~spmv_coo_plan() { spmv_csr_plan_destroy(csr_view); }
   std::mutex build_mu;              // the lazily built vla lists
   int groups = 1;                // consumer groups per tile CTA (coo_tile_kernel G)
@@ -1299,6 +1302,31 @@ int spmv_coo(const spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, con
                            static_cast<double*>(y), st, x_len);
   return coo_run<float>(p, ai, aj, static_cast<const float*>(av), static_cast<const float*>(x), col_base,
                         static_cast<float*>(y), st, x_len);
+}
+
+// Host x -> host y: x goes up in chunks, the product runs once all of x is
+// on the device (COO rows are not tied to column prefixes), y comes down.
+int spmv_coo_host(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const void* av, const void* x_host,
+                  void* y_host, int chunks, void* stream) {
+  if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
+  if (!x_host || !y_host) return fail(SPMV_INVALID_ARG, "NULL host buffer");
+  if (p->nrows == 0 || p->ncols == 0) return fail(SPMV_INVALID_ARG, "host pipeline needs a non-empty matrix");
+  if (chunks <= 0) chunks = 16;
+  if (chunks > 1024) chunks = 1024;
+  cudaStream_t st = as_stream(stream);
+  const std::vector<int64_t> xb = host_x_chunks(p->ncols, chunks);
+  const int nx = int(xb.size()) - 1;
+  const size_t esz = value_size(p->dtype);
+  auto compute = [&](int j, char* xd, char* yd, cudaStream_t s) -> int64_t {
+    if (j < nx - 1) return 0;
+    const int rc = p->dtype == SPMV_F64
+                       ? coo_run<double>(p, ai, aj, static_cast<const double*>(av), reinterpret_cast<const double*>(xd),
+                                         0, reinterpret_cast<double*>(yd), s, p->ncols)
+                       : coo_run<float>(p, ai, aj, static_cast<const float*>(av), reinterpret_cast<const float*>(xd), 0,
+                                        reinterpret_cast<float*>(yd), s, p->ncols);
+    return rc ? -rc : p->nrows;
+  };
+  return run_host_pipeline(p->host, x_host, y_host, esz, p->ncols, p->nrows, xb, compute, true, st);
 }
 
 int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const void* av, const void* x,

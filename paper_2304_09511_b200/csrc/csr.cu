@@ -28,6 +28,7 @@
 #include <cstdlib>
 #include <vector>
 
+#include "hostpipe.cuh"
 #include "panel.cuh"
 #include "tile.cuh"
 #include "wstream.cuh"
@@ -703,8 +704,7 @@ struct spmv_csr_plan {
   size_t off_head = 0, off_tail = 0, off_ws_head = 0, off_ws_tail = 0, off_ws_ctr = 0;
   mutable StreamSlots vla_scratch;  // two-phase vla product buffer (nnz values), per stream
   std::mutex build_mu;              // lazily built parts (vla lists, host staging, maxcol)
-  std::mutex host_mu;               // host-pipeline calls: one enqueues at a time
-  cudaEvent_t host_done = nullptr;  // end of the last host-pipeline call (the next one waits)
+  HostPipe host;                    // host-buffer products (hostpipe.cuh)
   bool tma_hint = false;
   DevBuf row_lo, cnt;
   DevBuf span_row, span_t0, span_t1;
@@ -713,15 +713,6 @@ struct spmv_csr_plan {
   // host-buffer pipeline (spmv_csr_host): created on first use
   std::vector<uint32_t> h_row_lo;
   std::vector<int64_t> h_maxcol_prefix;
-  DevBuf xd, yd;
-  cudaStream_t h2d = nullptr, d2h = nullptr;
-  std::vector<cudaEvent_t> events;
-  ~spmv_csr_plan() {
-    if (h2d) cudaStreamDestroy(h2d);
-    if (d2h) cudaStreamDestroy(d2h);
-    for (auto e : events) cudaEventDestroy(e);
-    if (host_done) cudaEventDestroy(host_done);
-  }
   int groups = 1;                    // consumer groups per tile CTA (csr_tile_kernel G)
   bool long_scratch = true;          // kernels with long-row scratch (false: plan has no long rows)
   // planned vla path: rows over kVlaLong entries, their 256-entry chunks and
@@ -1001,172 +992,65 @@ static int csr_run_vla_tiles(const spmv_csr_plan* p, const uint32_t* irp, const 
   return SPMV_OK;
 }
 
-// Host x -> host y product with H2D / compute / D2H overlap (see
-// spmv_csr_host in the header).
-static int csr_host_prepare(spmv_csr_plan* p, const uint32_t* aj, int chunks, cudaStream_t st) {
-  if (p->h_row_lo.empty()) {
-    std::lock_guard<std::mutex> lock(p->build_mu);  // maxcol is shared with spmv_csr_plan_tile_info
-    int rc;
-    if (!p->host_done) SPMV_CUDA_TRY(cudaEventCreateWithFlags(&p->host_done, cudaEventDisableTiming));
-    if (!p->maxcol.ptr) {
-      if ((rc = p->maxcol.alloc(4 * p->ntiles))) return rc;
-      const int64_t g = std::min<int64_t>(p->ntiles, int64_t(sm_count()) * 8);
-      tile_maxcol_kernel<<<unsigned(g), 256, 0, st>>>(aj, p->nnz, p->ntiles, p->tile, p->maxcol.as<uint32_t>());
-      SPMV_LAUNCH_CHECK();
-    }
-    p->h_row_lo.resize(p->ntiles + 1);
-    std::vector<uint32_t> mc(p->ntiles);
-    SPMV_CUDA_TRY(cudaMemcpyAsync(p->h_row_lo.data(), p->row_lo.ptr, 4 * (p->ntiles + 1), cudaMemcpyDeviceToHost, st));
-    SPMV_CUDA_TRY(cudaMemcpyAsync(mc.data(), p->maxcol.ptr, 4 * p->ntiles, cudaMemcpyDeviceToHost, st));
-    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
-    p->h_maxcol_prefix.resize(p->ntiles);
-    int64_t m = 0;
-    for (int64_t t = 0; t < p->ntiles; ++t) p->h_maxcol_prefix[t] = m = std::max<int64_t>(m, mc[t]);
-    const size_t vs = value_size(p->dtype);
-    if ((rc = p->xd.alloc(vs * std::max<int64_t>(p->ncols, 1))) || (rc = p->yd.alloc(vs * p->nrows))) return rc;
-    SPMV_CUDA_TRY(cudaStreamCreateWithFlags(&p->h2d, cudaStreamNonBlocking));
-    SPMV_CUDA_TRY(cudaStreamCreateWithFlags(&p->d2h, cudaStreamNonBlocking));
+// Host x -> host y product (spmv_csr_host): the generic pipeline of
+// hostpipe.cuh with tile ranges as the unit of work.  Per-tile row ranges
+// and largest columns come to the host once (under the build lock).
+static int csr_host_prepare(spmv_csr_plan* p, const uint32_t* aj, cudaStream_t st) {
+  std::lock_guard<std::mutex> lock(p->build_mu);  // maxcol is shared with spmv_csr_plan_tile_info
+  if (!p->h_row_lo.empty()) return SPMV_OK;
+  int rc;
+  if (!p->maxcol.ptr) {
+    if ((rc = p->maxcol.alloc(4 * p->ntiles))) return rc;
+    const int64_t g = std::min<int64_t>(p->ntiles, int64_t(sm_count()) * 8);
+    tile_maxcol_kernel<<<unsigned(g), 256, 0, st>>>(aj, p->nnz, p->ntiles, p->tile, p->maxcol.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
   }
-  while (int(p->events.size()) < 2 * chunks + 2) {
-    cudaEvent_t e;
-    SPMV_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    p->events.push_back(e);
-  }
+  std::vector<uint32_t> row_lo(p->ntiles + 1), mc(p->ntiles);
+  SPMV_CUDA_TRY(cudaMemcpyAsync(row_lo.data(), p->row_lo.ptr, 4 * (p->ntiles + 1), cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaMemcpyAsync(mc.data(), p->maxcol.ptr, 4 * p->ntiles, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  std::vector<int64_t> prefix(p->ntiles);
+  int64_t m = 0;
+  for (int64_t t = 0; t < p->ntiles; ++t) prefix[t] = m = std::max<int64_t>(m, mc[t]);
+  p->h_maxcol_prefix = std::move(prefix);
+  p->h_row_lo = std::move(row_lo);
   return SPMV_OK;
 }
-
-// SPMV_HOST_TRACE=1: timing events after every H2D chunk, tile range and
-// D2H copy of spmv_csr_host, printed to stderr (pipeline tuning only).
-struct HostTrace {
-  bool on = false;
-  int flags = 0;  // SPMV_HOST_TRACE value - 1: bit 0 skips compute, bit 1 skips D2H
-  cudaEvent_t t0 = nullptr;
-  std::vector<std::pair<char, cudaEvent_t>> marks;
-  void begin(cudaStream_t s) {
-    static const int level = [] {
-      const char* v = getenv("SPMV_HOST_TRACE");
-      return v && *v ? atoi(v) : 0;
-    }();
-    on = level > 0;
-    flags = level > 0 ? level - 1 : 0;
-    if (!on) return;
-    cudaEventCreate(&t0);
-    cudaEventRecord(t0, s);
-  }
-  void mark(char kind, cudaStream_t s) {
-    if (!on) return;
-    cudaEvent_t e;
-    cudaEventCreate(&e);
-    cudaEventRecord(e, s);
-    marks.emplace_back(kind, e);
-  }
-  void dump(cudaStream_t s) {
-    if (!on) return;
-    cudaStreamSynchronize(s);
-    cudaDeviceSynchronize();
-    fprintf(stderr, "host-trace");
-    for (auto& m : marks) {
-      float ms = 0;
-      cudaEventElapsedTime(&ms, t0, m.second);
-      fprintf(stderr, " %c%.3f", m.first, ms);
-      cudaEventDestroy(m.second);
-    }
-    fprintf(stderr, "\n");
-    cudaEventDestroy(t0);
-    marks.clear();
-  }
-};
 
 template <typename T>
 static int csr_host_run(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, const T* xh, T* yh,
                         int chunks, cudaStream_t st) {
-  // One call enqueues at a time; the device staging (xd, yd) and the copy
-  // streams are the plan's, so each call's work waits for the previous
-  // call's end (host_done) — calls from several threads or streams on one
-  // plan are serialised on the device, never interleaved.
-  std::lock_guard<std::mutex> lock(p->host_mu);
-  int rc = csr_host_prepare(p, aj, chunks, st);
+  int rc = csr_host_prepare(p, aj, st);
   if (rc) return rc;
-  SPMV_CUDA_TRY(cudaStreamWaitEvent(st, p->host_done, 0));
-  HostTrace tr;
-  T* xd = p->xd.as<T>();
-  T* yd = p->yd.as<T>();
-  // x schedule: copies below ~8 MB lose PCIe bandwidth when both directions
-  // run, but the first y rows can only leave once their x has arrived.  So
-  // the chunks ramp up (1/16 .. 1/2 of a full chunk) to start the D2H stream
-  // early, run at full size (ncols / chunks) in the middle, and ramp down at
-  // the end so that little y is left to copy after the last tile range.
-  std::vector<int64_t> xb{0};
-  {
-    const int64_t n = p->ncols;
-    const int64_t big = std::max<int64_t>(std::max<int64_t>(1, n / chunks), std::min<int64_t>(n, int64_t(1) << 20));
-    std::vector<int64_t> ramp;
-    for (int sh = 4; sh >= 1; --sh)
-      if ((big >> sh) >= 4096) ramp.push_back(big >> sh);
-    int64_t ramp_total = 0;
-    for (int64_t r : ramp) ramp_total += 2 * r;
-    if (2 * ramp_total > n) ramp.clear(), ramp_total = 0;
-    for (int64_t r : ramp) xb.push_back(xb.back() + r);
-    const int64_t mid = n - ramp_total, nmid = std::max<int64_t>(1, (mid + big / 2) / big);
-    const int64_t m0 = xb.back();
-    for (int64_t j = 1; j <= nmid; ++j) xb.push_back(m0 + mid * j / nmid);
-    for (auto it = ramp.rbegin(); it != ramp.rend(); ++it) xb.push_back(xb.back() + *it);
-    xb.back() = n;
-  }
+  const std::vector<int64_t> xb = host_x_chunks(p->ncols, chunks);
   const int nx = int(xb.size()) - 1;
-  while (int(p->events.size()) < 2 * nx + 2) {
-    cudaEvent_t e;
-    SPMV_CUDA_TRY(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
-    p->events.push_back(e);
-  }
-  cudaEvent_t* ev = p->events.data();  // [0, nx): x chunks, [nx, 2nx): tile ranges, 2nx: start, 2nx+1: end
-  SPMV_CUDA_TRY(cudaEventRecord(ev[2 * nx], st));
-  tr.begin(st);
-  SPMV_CUDA_TRY(cudaStreamWaitEvent(p->h2d, ev[2 * nx], 0));
-  SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[2 * nx], 0));
-  for (int j = 0; j < nx; ++j) {
-    if (xb[j + 1] > xb[j])
-      SPMV_CUDA_TRY(cudaMemcpyAsync(xd + xb[j], xh + xb[j], sizeof(T) * (xb[j + 1] - xb[j]), cudaMemcpyHostToDevice,
-                                    p->h2d));
-    SPMV_CUDA_TRY(cudaEventRecord(ev[j], p->h2d));
-    tr.mark('h', p->h2d);
-  }
-  // After x chunk j has landed, run every tile whose columns are all below
-  // xb[j + 1] (h_maxcol_prefix is non-decreasing), then copy its rows of y.
-  const bool spans = p->n_span > 0;  // y final only after the fix-up
-  int64_t done = 0, tb = 0;
-  for (int j = 0; j < nx && tb < p->ntiles; ++j) {
-    int64_t te = j == nx - 1 ? p->ntiles
-                             : int64_t(std::lower_bound(p->h_maxcol_prefix.begin(), p->h_maxcol_prefix.end(),
-                                                        xb[j + 1]) - p->h_maxcol_prefix.begin());
-    if (te <= tb) continue;
-    SPMV_CUDA_TRY(cudaStreamWaitEvent(st, ev[j], 0));
-    if (!(tr.on && tr.flags & 1))  // trace flag 1: skip the compute (pipeline analysis)
-      if ((rc = csr_run<T>(p, irp, aj, av, xd, 0, yd, st, tb, te, te == p->ntiles))) return rc;
-    tr.mark('k', st);
-    const int64_t rows_done = te < p->ntiles ? int64_t(p->h_row_lo[te]) : p->nrows;
-    if (!spans && rows_done > done && !(tr.on && tr.flags & 2)) {  // flag 2: no D2H
-      SPMV_CUDA_TRY(cudaEventRecord(ev[nx + j], st));
-      SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[nx + j], 0));
-      SPMV_CUDA_TRY(cudaMemcpyAsync(yh + done, yd + done, sizeof(T) * (rows_done - done), cudaMemcpyDeviceToHost,
-                                    p->d2h));
-      tr.mark('d', p->d2h);
-      done = rows_done;
+  int64_t tb = 0;
+  // after x chunk j has landed, run every tile whose columns are all below
+  // xb[j + 1] (h_maxcol_prefix is non-decreasing): rows before the next
+  // tile's first row are then final
+  // plans whose whole-matrix kernel is not the tile kernel (panel,
+  // warp-stream): the product runs once all of x is on the device
+  const bool whole = p->panel || p->ws;
+  auto compute = [&](int j, char* xd, char* yd, cudaStream_t s) -> int64_t {
+    if (whole) {
+      if (j < nx - 1) return 0;
+      const int r = csr_run<T>(p, irp, aj, av, reinterpret_cast<const T*>(xd), 0, reinterpret_cast<T*>(yd), s, 0,
+                               -1, true, INT64_MAX, 0, nullptr, p->ncols);
+      return r ? -r : p->nrows;
     }
-    tb = te;
-  }
-  if (done < p->nrows) {
-    SPMV_CUDA_TRY(cudaEventRecord(ev[2 * nx - 1], st));
-    SPMV_CUDA_TRY(cudaStreamWaitEvent(p->d2h, ev[2 * nx - 1], 0));
-    SPMV_CUDA_TRY(cudaMemcpyAsync(yh + done, yd + done, sizeof(T) * (p->nrows - done), cudaMemcpyDeviceToHost,
-                                  p->d2h));
-  }
-  SPMV_CUDA_TRY(cudaEventRecord(ev[2 * nx + 1], p->d2h));
-  SPMV_CUDA_TRY(cudaStreamWaitEvent(st, ev[2 * nx + 1], 0));
-  SPMV_CUDA_TRY(cudaEventRecord(p->host_done, st));
-  tr.mark('e', st);
-  tr.dump(st);
-  return SPMV_OK;
+    const int64_t te = j == nx - 1 ? p->ntiles
+                                   : int64_t(std::lower_bound(p->h_maxcol_prefix.begin(), p->h_maxcol_prefix.end(),
+                                                              xb[j + 1]) - p->h_maxcol_prefix.begin());
+    if (te > tb) {
+      const int r = csr_run<T>(p, irp, aj, av, reinterpret_cast<const T*>(xd), 0, reinterpret_cast<T*>(yd), s, tb, te,
+                               te == p->ntiles);
+      if (r) return -r;
+      tb = te;
+    }
+    return tb < p->ntiles ? int64_t(p->h_row_lo[tb]) : p->nrows;
+  };
+  return run_host_pipeline(p->host, xh, yh, sizeof(T), p->ncols, p->nrows, xb, compute, !whole && p->n_span > 0,
+                           st);
 }
 
 static int count_async(unsigned long long* dev, unsigned long long* host, cudaStream_t st) {

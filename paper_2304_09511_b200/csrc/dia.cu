@@ -21,6 +21,7 @@
 #include <tuple>
 #include <utility>
 
+#include "hostpipe.cuh"
 #include "tma.cuh"
 
 namespace spmv {
@@ -340,4 +341,66 @@ extern "C" int spmv_dia_ex(int dtype, int64_t nrows, int64_t ncols, int64_t ndia
                               cfg);
   return dia_launch<float>(nrows, ncols, ndiags, avail_rows, offsets, static_cast<const float*>(values),
                            static_cast<const float*>(x), row_base, col_base, static_cast<float*>(y), st, -1, 0, cfg);
+}
+
+// ---- host-buffer products (hostpipe.cuh) -----------------------------------
+struct spmv_host_pipe {
+  HostPipe hp;
+};
+
+extern "C" int spmv_host_pipe_create(spmv_host_pipe** out) {
+  if (!out) return fail(SPMV_INVALID_ARG, "out is NULL");
+  *out = new spmv_host_pipe();
+  return SPMV_OK;
+}
+
+extern "C" int spmv_host_pipe_destroy(spmv_host_pipe* p) {
+  delete p;
+  return SPMV_OK;
+}
+
+// Row blocks: block [done, r) runs once x holds every column its rows reach
+// (row + max_offset < the uploaded prefix); its rows of y then go down.
+template <typename T>
+static int dia_host_run(HostPipe& hp, int64_t nrows, int64_t ncols, int64_t nd, int64_t padded_rows,
+                        const int32_t* offsets, int64_t max_offset, const T* vals, const T* xh, T* yh, int chunks,
+                        const spmv_plan_config* cfg, cudaStream_t st) {
+  const std::vector<int64_t> xb = host_x_chunks(ncols, chunks);
+  const int nx = int(xb.size()) - 1;
+  int64_t done = 0;
+  auto compute = [&](int j, char* xd, char* yd, cudaStream_t s) -> int64_t {
+    int64_t r = j == nx - 1 ? nrows : std::min<int64_t>(nrows, xb[j + 1] - std::max<int64_t>(max_offset, 0));
+    if (r < nrows) r = r / 8 * 8;  // row blocks start on 8-row (TMA-aligned) boundaries
+    if (r > done) {
+      const int rc = dia_launch<T>(r - done, ncols, nd, padded_rows - done, offsets, vals + done * nd,
+                                   reinterpret_cast<const T*>(xd), done, 0, reinterpret_cast<T*>(yd) + done, s, -1, 0,
+                                   cfg);
+      if (rc) return -rc;
+      done = r;
+    }
+    return done;
+  };
+  return run_host_pipeline(hp, xh, yh, sizeof(T), ncols, nrows, xb, compute, false, st);
+}
+
+extern "C" int spmv_dia_host(spmv_host_pipe* pipe, int dtype, int64_t nrows, int64_t ncols, int64_t ndiags,
+                             int64_t padded_rows, const int32_t* offsets, int64_t max_offset, const void* values,
+                             const void* x_host, void* y_host, int chunks, const spmv_plan_config* cfg,
+                             void* stream) {
+  if (!pipe) return fail(SPMV_INVALID_ARG, "pipe is NULL");
+  if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
+  if (nrows <= 0 || ncols <= 0 || ndiags <= 0 || padded_rows < nrows || !offsets || !values || !x_host || !y_host)
+    return fail(SPMV_INVALID_ARG, "host pipeline needs a non-empty DIA block and host buffers");
+  if (cfg && cfg->version != SPMV_PLAN_CONFIG_VERSION)
+    return fail(SPMV_INVALID_ARG, "spmv_plan_config version %d, expected %d", cfg->version, SPMV_PLAN_CONFIG_VERSION);
+  if (chunks <= 0) chunks = 16;
+  if (chunks > 1024) chunks = 1024;
+  cudaStream_t st = as_stream(stream);
+  if (dtype == SPMV_F64)
+    return dia_host_run<double>(pipe->hp, nrows, ncols, ndiags, padded_rows, offsets, max_offset,
+                                static_cast<const double*>(values), static_cast<const double*>(x_host),
+                                static_cast<double*>(y_host), chunks, cfg, st);
+  return dia_host_run<float>(pipe->hp, nrows, ncols, ndiags, padded_rows, offsets, max_offset,
+                             static_cast<const float*>(values), static_cast<const float*>(x_host),
+                             static_cast<float*>(y_host), chunks, cfg, st);
 }

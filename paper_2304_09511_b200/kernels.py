@@ -10,11 +10,13 @@ kernels of libspmv_b200.so:
   spmv_*_vla      kernels.py:104-210  sub-warp / CTA lane kernels
 
 Host/device behaviour: a numpy (or list) `x` gets the reference contract —
-x is cast to the value dtype on the host (kernels.py:51-52), copied to the
-device, and a fresh numpy y is returned.  A CPU torch tensor (pinned for
-asynchronous copies) gives a CPU tensor back.  A CUDA tensor `x` stays on
-the device and a fresh CUDA tensor y is returned.  `out=` may be a CUDA
-tensor (reused, no allocation) or a (pinned) CPU tensor that receives y.
+x is cast to the value dtype on the host (kernels.py:51-52) and a fresh
+numpy y is returned; the upload, the product and the download are
+pipelined by the C ABI (spmv_*_host, csrc/hostpipe.cuh), y lives in pinned
+memory.  A CPU torch tensor x gives a (pinned) CPU tensor back.  A CUDA
+tensor `x` stays on the device and a fresh CUDA tensor y is returned.
+`out=` may be a CUDA tensor (reused, no allocation) or a CPU tensor that
+receives y (pinned for overlapped copies).
 Matrices may be our device containers or reference host containers (these
 are uploaded once and cached, formats.as_device).
 """
@@ -115,7 +117,8 @@ class _Plan:
     def __del__(self):
         try:
             if self.handle:
-                getattr(_lib.load(), f"spmv_{self.kind}_plan_destroy")(self.handle)
+                name = "spmv_host_pipe_destroy" if self.kind == "host_pipe" else f"spmv_{self.kind}_plan_destroy"
+                getattr(_lib.load(), name)(self.handle)
                 self.handle = None
         except Exception:
             pass
@@ -187,132 +190,62 @@ def coo_plan(A: CooMatrix, config: PlanConfig | None = None) -> _Plan:
 
 
 # --------------------------------------------------------- host pipelining --
-# A product whose x and y both live in host memory is PCIe-bound (x in, y
-# out).  CSR and DIA products are split into row ranges so the upload of x
-# (column chunks, copy stream 1), the kernels (compute stream) and the
-# download of finished rows of y (copy stream 2) overlap; PCIe is full
-# duplex, so the step approaches max(H2D, D2H) instead of H2D + compute + D2H.
-_SIDE_STREAMS: dict = {}
-PIPELINE_CHUNKS = int(__import__("os").environ.get("SPMV_PIPELINE_CHUNKS", "32"))
+# x and y in host memory (the reference's numpy contract): the C ABI
+# pipelines the x upload, the product and the y download (csrc/hostpipe.cuh).
+# y comes back as a fresh numpy array over pinned memory (torch's pinned
+# caching allocator), so its download overlaps; pageable numpy x is staged
+# by the library's pinned ring.
 HOST_CHUNKS = int(__import__("os").environ.get("SPMV_HOST_CHUNKS", "0"))  # 0: library default
 
 
-def _side_streams(dev):
-    key = str(dev)
-    if key not in _SIDE_STREAMS:
-        _SIDE_STREAMS[key] = (torch.cuda.Stream(dev), torch.cuda.Stream(dev))
-    return _SIDE_STREAMS[key]
+def _host_x(A, x):
+    """(host x array or tensor in the value dtype, origin) when x lives on
+    the host, else None (kernels.py:46-53 checks and cast)."""
+    if isinstance(x, torch.Tensor):
+        if x.is_cuda:
+            return None
+        if x.dim() != 1 or x.shape[0] != A.shape.ncols:
+            raise DimensionMismatch(f"x has shape {tuple(x.shape)}, expected ({A.shape.ncols},)")
+        return x.to(A.values.dtype).contiguous(), "torch_host"
+    xh = np.asarray(x)
+    if xh.ndim != 1 or xh.shape[0] != A.shape.ncols:
+        raise DimensionMismatch(f"x has shape {xh.shape}, expected ({A.shape.ncols},)")
+    return np.ascontiguousarray(xh, dtype=A.dtype), "numpy"
 
 
-def _csr_tile_info(A: CsrMatrix, p: "_Plan"):
+def _host_ptr(xh) -> int:
+    return xh.data_ptr() if isinstance(xh, torch.Tensor) else xh.ctypes.data
+
+
+def _host_product(A, x, out, call) -> object:
+    """Run `call(x_ptr, y_ptr, stream)` (an spmv_*_host entry point) with
+    host x and a pinned host y; None when x is on the device or the matrix
+    is empty (the plain path handles those)."""
+    hx = _host_x(A, x)
+    if hx is None or A.nrows == 0 or A.ncols == 0:
+        return None
+    xh, origin = hx
+    if out is not None:
+        if out.is_cuda or out.shape != (A.nrows,) or out.dtype != A.values.dtype or not out.is_contiguous():
+            return None
+        yh = out
+    else:
+        yh = torch.empty(A.nrows, dtype=A.values.dtype, pin_memory=True)
+    stream = torch.cuda.current_stream(A.device)
+    call(_host_ptr(xh), yh.data_ptr(), stream.cuda_stream)
+    stream.synchronize()
+    if out is not None:
+        return out
+    return yh.numpy() if origin == "numpy" else yh
+
+
+def _host_pipe(A) -> "_Plan":
+    """A DIA container's own host pipe (staging, copy streams)."""
     def make():
-        nt, tile = ctypes.c_int64(), ctypes.c_int64()
-        _lib.call("spmv_csr_plan_tiles", p.handle, ctypes.byref(nt), ctypes.byref(tile))
-        n = int(nt.value)
-        row_lo = np.empty(n + 1, dtype=np.uint32)
-        maxcol = np.empty(max(n, 1), dtype=np.uint32)
-        _lib.call("spmv_csr_plan_tile_info", p.handle, _ptr(A.col_indices), row_lo.ctypes.data, maxcol.ctypes.data,
-                  _stream(A.device))
-        return n, row_lo.astype(np.int64), np.maximum.accumulate(maxcol[:n].astype(np.int64))
-    return A.plan("csr_tiles", make)
-
-
-def _upload_x_chunks(xh: torch.Tensor, xd: torch.Tensor, h2d, chunks: int):
-    """Column chunks of x, in order on `h2d`; returns (bounds, events)."""
-    n = xh.shape[0]
-    bounds = [n * j // chunks for j in range(chunks + 1)]
-    events = []
-    with torch.cuda.stream(h2d):
-        for j in range(chunks):
-            a, b = bounds[j], bounds[j + 1]
-            if b > a:
-                xd[a:b].copy_(xh[a:b], non_blocking=True)
-            ev = torch.cuda.Event()
-            ev.record(h2d)
-            events.append(ev)
-    return bounds, events
-
-
-def _wait_x(cur, bounds, events, col_hi: int) -> None:
-    """Make `cur` wait until x[0 .. col_hi] is on the device."""
-    j = 0
-    while j + 1 < len(bounds) - 1 and bounds[j + 1] <= col_hi:
-        j += 1
-    cur.wait_event(events[j])
-
-
-def _pipelined(A, xh: torch.Tensor, yh: torch.Tensor, launch_range, ranges, chunks: int, y_final_at_end: bool):
-    """Generic H2D / compute / D2H overlap.  `ranges`: list of
-    (col_hi, rows_done) per compute step; `launch_range(k, xd, yd, stream)`."""
-    dev = A.values.device
-    cur = torch.cuda.current_stream(dev)
-    h2d, d2h = _side_streams(dev)
-    xd = torch.empty(A.ncols, dtype=A.values.dtype, device=dev)
-    yd = torch.empty(A.nrows, dtype=A.values.dtype, device=dev)
-    h2d.wait_stream(cur)
-    d2h.wait_stream(cur)
-    bounds, events = _upload_x_chunks(xh, xd, h2d, chunks)
-    done = 0
-    for k, (col_hi, rows_done) in enumerate(ranges):
-        _wait_x(cur, bounds, events, col_hi)
-        launch_range(k, xd, yd, cur)
-        if not y_final_at_end and rows_done > done:
-            ev = torch.cuda.Event()
-            ev.record(cur)
-            d2h.wait_event(ev)
-            with torch.cuda.stream(d2h):
-                yh[done:rows_done].copy_(yd[done:rows_done], non_blocking=True)
-            done = rows_done
-    if done < A.nrows:
-        ev = torch.cuda.Event()
-        ev.record(cur)
-        d2h.wait_event(ev)
-        with torch.cuda.stream(d2h):
-            yh[done:].copy_(yd[done:], non_blocking=True)
-    xd.record_stream(h2d)
-    yd.record_stream(d2h)
-    d2h.synchronize()
-    return yh
-
-
-def _csr_pipelined(A: CsrMatrix, xh, yh, chunks: int = PIPELINE_CHUNKS):
-    p = csr_plan(A)
-    nt, row_lo, maxcol_prefix = _csr_tile_info(A, p)
-    tb = [nt * k // chunks for k in range(chunks + 1)]
-    steps = [(k, tb[k], tb[k + 1]) for k in range(chunks) if tb[k + 1] > tb[k]]
-    ranges = [(int(maxcol_prefix[te - 1]), int(row_lo[te]) if te < nt else A.nrows) for _, _, te in steps]
-    spans = p.info()["launches"] > 1  # long rows spanning tiles: y final only after the fix-up
-
-    def launch(k, xd, yd, stream):
-        _, a, b = steps[k]
-        _lib.call("spmv_csr_range", p.handle, _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values), _ptr(xd), 0,
-                  A.ncols, _ptr(yd), a, b, 1 if k == len(steps) - 1 else 0, stream.cuda_stream)
-
-    return _pipelined(A, xh, yh, launch, ranges, chunks, spans)
-
-
-def _dia_pipelined(A: DiaMatrix, xh, yh, chunks: int = PIPELINE_CHUNKS):
-    offs = A.plan("dia_offsets", lambda: A.offsets.cpu().numpy().astype(np.int64))
-    max_off = int(offs.max()) if offs.size else 0
-    rb = [(A.nrows * k // chunks) // 8 * 8 for k in range(chunks)] + [A.nrows]
-    steps = [(rb[k], rb[k + 1]) for k in range(chunks) if rb[k + 1] > rb[k]]
-    ranges = [(min(A.ncols - 1, b - 1 + max_off), b) for a, b in steps]
-    esz = A.values.element_size()
-
-    def launch(k, xd, yd, stream):
-        a, b = steps[k]
-        _lib.call("spmv_dia", _lib.dtype_code(A.values.dtype), b - a, A.ncols, A.ndiags, A.padded_rows - a,
-                  _ptr(A.offsets), A.values.data_ptr() + a * A.ndiags * esz, _ptr(xd), a, 0, A.ncols,
-                  yd.data_ptr() + a * esz, stream.cuda_stream)
-
-    return _pipelined(A, xh, yh, launch, ranges, chunks, False)
-
-
-def _host_pipeline_ok(A, x, out) -> bool:
-    return (isinstance(x, torch.Tensor) and not x.is_cuda and out is not None and not out.is_cuda
-            and x.dtype == A.values.dtype and x.dim() == 1 and x.shape[0] == A.ncols
-            and out.shape == (A.nrows,) and out.dtype == A.values.dtype and A.nnz > 0 and A.nrows > 0
-            and x.is_contiguous() and out.is_contiguous())
+        h = ctypes.c_void_p()
+        _lib.call("spmv_host_pipe_create", ctypes.byref(h))
+        return _Plan("host_pipe", h)
+    return A.plan("host_pipe", make)
 
 
 # ------------------------------------------------------------------ kernels --
@@ -320,6 +253,12 @@ def spmv_coo_plain(A, x, out=None, plan_config: PlanConfig | None = None):
     """``y = A @ x`` with np.add.at semantics (kernels.py:56-66).
     `plan_config` overrides the container's kernel configuration."""
     A = as_device(A)
+    p = coo_plan(A, plan_config) if A.nrows else None
+    y = _host_product(A, x, out, lambda xp, yp, st: _lib.call(
+        "spmv_coo_host", p.handle, _ptr(A.row_indices), _ptr(A.col_indices), _ptr(A.values), xp, yp, HOST_CHUNKS,
+        st))
+    if y is not None:
+        return y
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
@@ -333,13 +272,14 @@ def spmv_csr_plain(A, x, out=None, plan_config: PlanConfig | None = None):
     """``y = A @ x`` with one left-to-right sum per row (kernels.py:69-82).
     `plan_config` overrides the container's kernel configuration."""
     A = as_device(A)
-    if _host_pipeline_ok(A, x, out):
+    if A.nnz:
         # host x -> host y: the C ABI pipelines upload / tiles / download
         p = csr_plan(A, config=plan_config)
-        _lib.call("spmv_csr_host", p.handle, _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values),
-                  x.data_ptr(), out.data_ptr(), HOST_CHUNKS, _stream(A.device))
-        torch.cuda.current_stream(A.device).synchronize()
-        return out
+        y = _host_product(A, x, out, lambda xp, yp, st: _lib.call(
+            "spmv_csr_host", p.handle, _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values), xp, yp,
+            HOST_CHUNKS, st))
+        if y is not None:
+            return y
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
@@ -353,12 +293,21 @@ def spmv_dia_plain(A, x, out=None, plan_config: PlanConfig | None = None):
     """``y = A @ x`` over stored diagonals (kernels.py:85-101).
     `plan_config` (its dia_* fields) overrides the container's."""
     A = as_device(A)
-    if _host_pipeline_ok(A, x, out) and A.ndiags > 0:
-        return _dia_pipelined(A, x, out)
+    cfg = plan_config if plan_config is not None else plan_config_of(A)
+    if A.ndiags > 0:
+        offs = A.plan("dia_offsets", lambda: A.offsets.cpu().numpy().astype(np.int64))
+        pipe = _host_pipe(A)
+        c = cfg.to_c()
+        y = _host_product(A, x, out, lambda xp, yp, st: _lib.call(
+            "spmv_dia_host", pipe.handle, _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.ndiags,
+            A.padded_rows, _ptr(A.offsets), int(offs.max()), _ptr(A.values), xp, yp, HOST_CHUNKS, ctypes.byref(c),
+            st))
+        if y is not None:
+            return y
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
     if A.nrows:
-        c = (plan_config if plan_config is not None else plan_config_of(A)).to_c()
+        c = cfg.to_c()
         _lib.call("spmv_dia_ex", _lib.dtype_code(A.values.dtype), A.nrows, A.ncols, A.ndiags, A.padded_rows,
                   _ptr(A.offsets), _ptr(A.values), _ptr(xv), 0, 0, A.ncols, _ptr(y), ctypes.byref(c),
                   _stream(A.device))

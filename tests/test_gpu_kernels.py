@@ -274,7 +274,6 @@ def test_host_pipelined_products_match(sp):
     xh = torch.rand(A.ncols, dtype=torch.float64).pin_memory()
     yh = torch.empty(A.nrows, dtype=torch.float64).pin_memory()
     ref = sp.spmv_csr_plain(A, xh.cuda()).cpu()
-    assert K._host_pipeline_ok(A, xh, yh)
     assert torch.equal(sp.spmv_csr_plain(A, xh, out=yh), ref)
     dia = sp.to_format(A, "dia")
     yh2 = torch.empty_like(yh)
@@ -285,3 +284,31 @@ def test_host_pipelined_products_match(sp):
     y_dev = sp.spmv_csr_plain(csr, x.cuda()).cpu()
     y3 = torch.empty(csr.nrows, dtype=torch.float64)
     assert torch.equal(sp.spmv_csr_plain(csr, x, out=y3), y_dev)
+
+
+@pytest.mark.parametrize("fmt", ["csr", "coo", "dia"])
+def test_numpy_host_products(sp, fmt):
+    """The reference contract through the host pipeline (csrc/hostpipe.cuh):
+    numpy x (pageable, and over pinned memory), list x, CPU tensor x, and a
+    wrong-length x; y is a fresh numpy array equal bit for bit to the device
+    product."""
+    from paper_2304_09511_b200.plugin import gpu_kernel
+    A = sp.gen_stencil27(40, 36, 30)
+    m = {"csr": A, "coo": sp.csr_to_coo(A), "dia": sp.coo_to_dia(sp.csr_to_coo(A))}[fmt]
+    x = np.random.default_rng(4).uniform(-1, 1, A.ncols)
+    ref = sp.dispatch(m, torch.from_numpy(x).cuda()).cpu().numpy()
+    fn = gpu_kernel(fmt, "plain")
+    pinned = torch.from_numpy(x).pin_memory()
+    for xh in (x, pinned.numpy(), x.tolist(), x.astype(np.float32)):
+        y = fn(m, xh, None)
+        assert isinstance(y, np.ndarray) and y.dtype == np.float64
+        want = ref if np.asarray(xh).dtype == np.float64 else \
+            sp.dispatch(m, torch.from_numpy(x.astype(np.float32).astype(np.float64)).cuda()).cpu().numpy()
+        assert y.tobytes() == want.tobytes()
+    yt = sp.dispatch(m, pinned)
+    assert isinstance(yt, torch.Tensor) and not yt.is_cuda and torch.equal(yt, torch.from_numpy(ref))
+    with pytest.raises(sp.DimensionMismatch):
+        fn(m, x[:-1], None)
+    # repeated calls reuse the pinned y blocks and the plan's pipe
+    for _ in range(3):
+        assert fn(m, x, None).tobytes() == ref.tobytes()
