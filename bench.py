@@ -322,6 +322,14 @@ def conversions_measure(torch, sp, mats, pk, reps: int = 3) -> dict:
     perm = torch.randperm(nnz, device=csr.values.device, generator=g)
     shuffled = sp.CooMatrix(coo.shape, coo.row_indices[perm], coo.col_indices[perm], coo.values[perm], sorted=False)
     del perm
+    # a row-stable shuffle: sort the random permutation by row (stable), so
+    # rows stay in order and each row's entries are permuted
+    key = coo.row_indices.to(torch.int64) * nnz + torch.randperm(nnz, device=csr.values.device, generator=g)
+    order = torch.argsort(key)
+    del key
+    rows_ordered = sp.CooMatrix(coo.shape, coo.row_indices[order], coo.col_indices[order], coo.values[order],
+                                sorted=False)
+    del order
     idx = 4 * nnz
     cases = {
         # name: (callable, algorithmic bytes)
@@ -330,6 +338,9 @@ def conversions_measure(torch, sp, mats, pk, reps: int = 3) -> dict:
         "coo_to_dia": (lambda: C.coo_to_dia(coo), 2 * idx + nnz * (8 + sv) + prow * nd * sv),
         "dia_to_coo": (lambda: C.dia_to_coo(dia), 2 * prow * nd * sv + nnz * (8 + sv)),
         "sort_coo": (lambda: C.sort_coo(shuffled), 2 * nnz * (8 + sv)),
+        # rows in order, columns shuffled inside each row, flag unset: the
+        # within-row sort only (no row sort, no random gathers)
+        "sort_coo_rows_ordered": (lambda: C.sort_coo(rows_ordered), 2 * nnz * (8 + sv)),
     }
     if gen_args is not None:
         cases["gen_stencil27"] = (lambda: M.gen_stencil27(*gen_args), 4 * (n + 1) + nnz * (4 + sv))

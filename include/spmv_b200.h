@@ -376,23 +376,16 @@ int spmv_dia_collect_destroy(spmv_dia_collect* c);
 
 /* convert.py:60-84: stable (row, col) sort; duplicate coordinates summed in
  * numpy's np.add.reduceat order (first element + pairwise sum of the rest,
- * numpy 2.3 pairwise_sum), zero sums kept.  Two phases: sort + count, then
- * emit. */
-typedef struct spmv_coo_sorter spmv_coo_sorter;
-int spmv_sort_coo_analyze(int dtype, int64_t nnz, const uint32_t* row_indices,
-                          const uint32_t* col_indices, void* stream,
-                          spmv_coo_sorter** out, int64_t* nnz_out);
-/* Same, with the shape: the sort key packs (row, col) into
- * bits(nrows) + bits(ncols) bits, so the radix sort runs fewer passes. */
-int spmv_sort_coo_analyze_shape(int dtype, int64_t nrows, int64_t ncols,
-                                int64_t nnz, const uint32_t* row_indices,
-                                const uint32_t* col_indices, void* stream,
-                                spmv_coo_sorter** out, int64_t* nnz_out);
-int spmv_sort_coo_emit(const spmv_coo_sorter* s, int dtype,
-                       const void* values, uint32_t* row_indices_out,
-                       uint32_t* col_indices_out, void* values_out,
-                       void* stream);
-int spmv_coo_sorter_destroy(spmv_coo_sorter* s);
+ * numpy 2.3 pairwise_sum), zero sums kept.  One call: a stable radix sort on
+ * the row with the storage index as payload, then each row's columns sorted
+ * (warp bitonic sort for rows of <= 32 entries, a segmented sort above),
+ * duplicates merged only when some (row, column) repeats.  The outputs have
+ * capacity nnz; *nnz_out receives the merged count.  Synchronises. */
+int spmv_sort_coo(int dtype, int64_t nrows, int64_t ncols, int64_t nnz,
+                  const uint32_t* row_indices, const uint32_t* col_indices,
+                  const void* values, uint32_t* row_indices_out,
+                  uint32_t* col_indices_out, void* values_out,
+                  int64_t* nnz_out, void* stream);
 
 /* ---- generators (matrixio.py:170-210 gen_stencil27) -------------------- */
 /* nnz = prod(3*n_d - 2) (1 for n_d = 1).  IndexOverflow when 27*n > 2^32-1

@@ -94,10 +94,7 @@ SIGNATURES = {
     "spmv_dia_to_coo_count": [_c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _pvp, _pi64],
     "spmv_dia_to_coo_fill": [_vp, _c_int, _vp, _vp, _vp, _vp, _vp, _vp],
     "spmv_dia_collect_destroy": [_vp],
-    "spmv_sort_coo_analyze": [_c_int, _c_i64, _vp, _vp, _vp, _pvp, _pi64],
-    "spmv_sort_coo_analyze_shape": [_c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _pvp, _pi64],
-    "spmv_sort_coo_emit": [_vp, _c_int, _vp, _vp, _vp, _vp, _vp],
-    "spmv_coo_sorter_destroy": [_vp],
+    "spmv_sort_coo": [_c_int, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp, _vp, _vp, _pi64, _vp],
     "spmv_stencil27_nnz": [_c_i64, _c_i64, _c_i64, _pi64],
     "spmv_stencil27_fill": [_c_int, _c_i64, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _vp],
     "spmv_csr_col_bounds": [_c_i64, _vp, _vp, _vp, _pu32, _pu32],

@@ -72,26 +72,25 @@ def dense_to_coo(dense, dtype=None, device=None) -> CooMatrix:
 def sort_coo(coo) -> CooMatrix:
     """(row, col)-sorted COO with duplicates summed (convert.py:60-84).
 
-    A flagged-sorted matrix is returned unchanged.  Otherwise a stable 64-bit
-    key radix sort on the device; duplicate runs are added in
+    A flagged-sorted matrix is returned unchanged.  Otherwise, on the device:
+    a stable radix sort on the row (storage index as payload), each row's
+    columns sorted by (column, storage index), duplicate runs added in
     np.add.reduceat order (first + numpy pairwise sum of the rest), zero sums
-    kept."""
+    kept (csrc/convert.cu spmv_sort_coo)."""
     coo = as_device(coo)
     if coo.sorted:
         return coo
     dev = coo.values.device
-    code = _lib.dtype_code(coo.values.dtype)
-    h = ctypes.c_void_p()
+    nnz = coo.nnz
+    ai, aj = _empty_idx(nnz, dev), _empty_idx(nnz, dev)
+    av = torch.empty(nnz, dtype=coo.values.dtype, device=dev)
     n_out = ctypes.c_int64()
-    _lib.call("spmv_sort_coo_analyze_shape", code, max(coo.nrows, 1), max(coo.ncols, 1), coo.nnz,
-              _ptr(coo.row_indices), _ptr(coo.col_indices), _stream(coo.values), ctypes.byref(h), ctypes.byref(n_out))
-    try:
-        n = int(n_out.value)
-        ai, aj = _empty_idx(n, dev), _empty_idx(n, dev)
-        av = torch.empty(n, dtype=coo.values.dtype, device=dev)
-        _lib.call("spmv_sort_coo_emit", h, code, _ptr(coo.values), _ptr(ai), _ptr(aj), _ptr(av), _stream(coo.values))
-    finally:
-        _lib.load().spmv_coo_sorter_destroy(h)
+    _lib.call("spmv_sort_coo", _lib.dtype_code(coo.values.dtype), max(coo.nrows, 1), max(coo.ncols, 1), nnz,
+              _ptr(coo.row_indices), _ptr(coo.col_indices), _ptr(coo.values), _ptr(ai), _ptr(aj), _ptr(av),
+              ctypes.byref(n_out), _stream(coo.values))
+    n = int(n_out.value)
+    if n < nnz:  # duplicates merged: shrink to the merged count
+        ai, aj, av = ai[:n].clone(), aj[:n].clone(), av[:n].clone()
     return CooMatrix(MatrixShape(coo.nrows, coo.ncols, n), ai, aj, av, sorted=True)
 
 

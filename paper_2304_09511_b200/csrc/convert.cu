@@ -4,8 +4,10 @@
 //   csr_to_coo  (convert.py:97-110)  row expansion + strictly-increasing check
 //   coo_to_dia  (convert.py:113-144) diagonal-id bitmap, scan, scatter
 //   dia_to_coo  (convert.py:147-177) per-row compaction of nonzero cells
-//   sort_coo    (convert.py:60-84)   stable 64-bit key radix sort, duplicate
-//                                    runs summed in np.add.reduceat order
+//   sort_coo    (convert.py:60-84)   stable row sort (radix on the row only,
+//                                    columns ride along), column sort inside
+//                                    each row, duplicate runs summed in
+//                                    np.add.reduceat order
 #include <cub/cub.cuh>
 
 #include <algorithm>
@@ -185,21 +187,114 @@ __global__ void __launch_bounds__(256) dia_rows_kernel(const int32_t* __restrict
 }
 
 // ---- sort_coo ------------------------------------------------------------------
-__global__ void make_keys_kernel(const uint32_t* __restrict__ ai, const uint32_t* __restrict__ aj, int64_t nnz,
-                                 int col_bits, unsigned long long* __restrict__ keys, uint32_t* __restrict__ idx) {
-  GRID_STRIDE(k, nnz) {
-    keys[k] = (static_cast<unsigned long long>(ai[k]) << col_bits) | aj[k];
-    idx[k] = uint32_t(k);
+// Stage 1: a stable LSD radix sort of the 32-bit row keys (bits(nrows)
+// bits) carrying each entry's storage index: each row's entries in storage
+// order.  Stage 2: per row, its columns and values gathered through those
+// indices and sorted by (column, storage index) — the reference's stable
+// lexsort((cols, rows)) (convert.py:70) — written straight to the output
+// positions (a warp per row of <= 32 entries: a bitonic sort in registers;
+// longer rows: a segmented sort).  Stage 3, only when some (row, column)
+// repeats: duplicate runs summed in np.add.reduceat order and compacted.
+
+// flag = 1 if some row index is smaller than the one before it
+__global__ void rows_descend_kernel(const uint32_t* __restrict__ ai, int64_t nnz, int* __restrict__ flag) {
+  GRID_STRIDE(k, nnz) if (k > 0 && ai[k] < ai[k - 1]) *flag = 1;
+}
+
+// Rows of <= 32 entries: lane k holds entry k of the row, its payload
+// (col << 32 | storage index); a bitonic sort of the payloads, then the
+// value gathered through the storage index.  `pay` null: the rows were
+// already in order, entry k's payload is built from aj[k] and k itself
+// (no gathers at all).  Duplicate columns counted.
+template <typename T>
+__global__ void sort_rows_kernel(const uint32_t* __restrict__ rows_s, const unsigned long long* __restrict__ pay,
+                                 const uint32_t* __restrict__ seg, int64_t nseg, const uint32_t* __restrict__ aj,
+                                 const T* __restrict__ av, uint32_t* __restrict__ ai_out,
+                                 uint32_t* __restrict__ aj_out, T* __restrict__ av_out, uint32_t* __restrict__ ucnt,
+                                 unsigned long long* __restrict__ ndup) {
+  const int lane = threadIdx.x & 31;
+  const int64_t nw = (int64_t(gridDim.x) * blockDim.x) >> 5;
+  unsigned long long dups = 0;
+  for (int64_t i = (int64_t(blockIdx.x) * blockDim.x + threadIdx.x) >> 5; i < nseg; i += nw) {
+    const uint32_t a = seg[i], n = seg[i + 1] - a;
+    if (n > 32) continue;  // warp-uniform
+    const bool in = uint32_t(lane) < n;
+    unsigned long long key = ~0ull;
+    if (in) key = pay ? pay[a + lane] : (static_cast<unsigned long long>(aj[a + lane]) << 32) | (a + lane);
+#pragma unroll
+    for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+      for (int j = k >> 1; j >= 1; j >>= 1) {
+        const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, j);
+        const bool take_min = ((lane & j) == 0) == ((lane & k) == 0);
+        key = (take_min ? ok < key : ok > key) ? ok : key;
+      }
+    const unsigned long long prev = __shfl_up_sync(0xffffffffu, key, 1);
+    const bool head = in && (lane == 0 || (prev >> 32) != (key >> 32));
+    const unsigned heads = __ballot_sync(0xffffffffu, head);
+    if (in) {
+      ai_out[a + lane] = rows_s[a];
+      aj_out[a + lane] = uint32_t(key >> 32);
+      av_out[a + lane] = av[uint32_t(key)];
+    }
+    if (lane == 0) {
+      ucnt[i] = __popc(heads);
+      dups += n - __popc(heads);
+    }
+  }
+  if (lane == 0 && dups) atomicAdd(ndup, dups);
+}
+
+// Stage-1 payload: (col << 32 | storage index).
+__global__ void sort_payload_kernel(const uint32_t* __restrict__ aj, int64_t nnz,
+                                    unsigned long long* __restrict__ pay) {
+  GRID_STRIDE(k, nnz) pay[k] = (static_cast<unsigned long long>(aj[k]) << 32) | static_cast<unsigned long long>(k);
+}
+
+// Rows over 32 entries: (begin, end) of each (count only when lb is null).
+__global__ void list_long_segments_kernel(const uint32_t* __restrict__ seg, int64_t nseg, uint32_t* __restrict__ lb,
+                                          uint32_t* __restrict__ le, unsigned long long* __restrict__ n) {
+  GRID_STRIDE(i, nseg) {
+    const uint32_t a = seg[i], b = seg[i + 1];
+    if (b - a <= 32) continue;
+    const unsigned long long k = atomicAdd(n, 1ull);
+    if (lb) {
+      lb[k] = a;
+      le[k] = b;
+    }
   }
 }
 
-__global__ void key_heads_kernel(const unsigned long long* __restrict__ keys, int64_t n, uint32_t* __restrict__ head) {
-  GRID_STRIDE(k, n) head[k] = (k == 0 || keys[k] != keys[k - 1]) ? 1u : 0u;
+// Long rows, before their segmented sort: key = (col << 32 | storage
+// index), from the stage-1 payloads or (rows already in order) built.
+__global__ void long_keys_kernel(const unsigned long long* __restrict__ pay, const uint32_t* __restrict__ aj,
+                                 const uint32_t* __restrict__ lb, const uint32_t* __restrict__ le, int64_t nl,
+                                 unsigned long long* __restrict__ key) {
+  for (int64_t i = blockIdx.x; i < nl; i += gridDim.x)
+    for (uint32_t k = lb[i] + threadIdx.x; k < le[i]; k += blockDim.x)
+      key[k] = pay ? pay[k] : (static_cast<unsigned long long>(aj[k]) << 32) | k;
 }
 
-__global__ void key_runs_kernel(const uint32_t* __restrict__ head, const uint32_t* __restrict__ pos, int64_t n,
-                                uint32_t* __restrict__ run_start) {
-  GRID_STRIDE(k, n) if (head[k]) run_start[pos[k]] = uint32_t(k);
+// Long rows after the segmented sort: outputs in place, duplicates counted.
+template <typename T>
+__global__ void long_emit_kernel(const uint32_t* __restrict__ rows_s, const unsigned long long* __restrict__ key,
+                                 const uint32_t* __restrict__ seg, int64_t nseg, const T* __restrict__ av,
+                                 uint32_t* __restrict__ ai_out, uint32_t* __restrict__ aj_out,
+                                 T* __restrict__ av_out, uint32_t* __restrict__ ucnt,
+                                 unsigned long long* __restrict__ ndup) {
+  GRID_STRIDE(i, nseg) {
+    const uint32_t a = seg[i], b = seg[i + 1];
+    if (b - a <= 32) continue;
+    uint32_t u = 0;
+    for (uint32_t k = a; k < b; ++k) {
+      ai_out[k] = rows_s[a];
+      aj_out[k] = uint32_t(key[k] >> 32);
+      av_out[k] = av[uint32_t(key[k])];
+      u += (k == a || (key[k] >> 32) != (key[k - 1] >> 32));
+    }
+    ucnt[i] = u;
+    if (b - a > u) atomicAdd(ndup, static_cast<unsigned long long>(b - a - u));
+  }
 }
 
 // numpy 2.3 pairwise_sum (loops_utils.h): < 8 terms sequential from -0.0,
@@ -207,43 +302,52 @@ __global__ void key_runs_kernel(const uint32_t* __restrict__ head, const uint32_
 // down to a multiple of 8.  Verified bit-for-bit against np.add.reduceat
 // (tests/golden/make_golden.py pins it).
 template <typename T>
-__device__ T np_pairwise(const T* __restrict__ av, const uint32_t* __restrict__ perm, uint32_t lo, uint32_t n) {
+__device__ T np_pairwise(const T* __restrict__ v, uint32_t n) {
   if (n < 8) {
     T res = T(-0.0);
-    for (uint32_t i = 0; i < n; ++i) res = add_rn(res, av[perm[lo + i]]);
+    for (uint32_t i = 0; i < n; ++i) res = add_rn(res, v[i]);
     return res;
   }
   if (n <= 128) {
     T r[8];
 #pragma unroll
-    for (int j = 0; j < 8; ++j) r[j] = av[perm[lo + j]];
+    for (int j = 0; j < 8; ++j) r[j] = v[j];
     uint32_t i = 8;
     for (; i < n - (n % 8); i += 8)
 #pragma unroll
-      for (int j = 0; j < 8; ++j) r[j] = add_rn(r[j], av[perm[lo + i + j]]);
+      for (int j = 0; j < 8; ++j) r[j] = add_rn(r[j], v[i + j]);
     T res = add_rn(add_rn(add_rn(r[0], r[1]), add_rn(r[2], r[3])), add_rn(add_rn(r[4], r[5]), add_rn(r[6], r[7])));
-    for (; i < n; ++i) res = add_rn(res, av[perm[lo + i]]);
+    for (; i < n; ++i) res = add_rn(res, v[i]);
     return res;
   }
   uint32_t n2 = n / 2;
   n2 -= n2 % 8;
-  return add_rn(np_pairwise(av, perm, lo, n2), np_pairwise(av, perm, lo + n2, n - n2));
+  return add_rn(np_pairwise(v, n2), np_pairwise(v + n2, n - n2));
 }
 
+// Duplicate runs (some (row, column) repeats): each run of equal columns in
+// a row, already in storage order, becomes first + pairwise sum of the rest
+// (np.add.reduceat, convert.py:80; zero sums kept), written compacted at
+// opos[i] into the second buffers.
 template <typename T>
-__global__ void sort_emit_kernel(const unsigned long long* __restrict__ keys, const uint32_t* __restrict__ perm,
-                                 const uint32_t* __restrict__ run_start, int64_t n_runs, int64_t nnz, int col_bits,
-                                 const T* __restrict__ av, uint32_t* __restrict__ ai, uint32_t* __restrict__ aj,
-                                 T* __restrict__ out) {
-  GRID_STRIDE(i, n_runs) {
-    const uint32_t a = run_start[i];
-    const uint32_t b = (i + 1 < n_runs) ? run_start[i + 1] : uint32_t(nnz);
-    const unsigned long long key = keys[a];
-    ai[i] = uint32_t(key >> col_bits);
-    aj[i] = uint32_t(key & ((1ull << col_bits) - 1ull));
-    T v = av[perm[a]];
-    if (b - a > 1) v = add_rn(v, np_pairwise(av, perm, a + 1, b - a - 1));
-    out[i] = v;
+__global__ void merge_runs_kernel(const uint32_t* __restrict__ seg, const uint32_t* __restrict__ opos, int64_t nseg,
+                                  const uint32_t* __restrict__ ai_s, const uint32_t* __restrict__ aj_s,
+                                  const T* __restrict__ av_s, uint32_t* __restrict__ ai_o, uint32_t* __restrict__ aj_o,
+                                  T* __restrict__ av_o) {
+  GRID_STRIDE(i, nseg) {
+    const uint32_t a = seg[i], b = seg[i + 1];
+    uint32_t o = opos[i];
+    for (uint32_t k = a; k < b;) {
+      uint32_t e = k + 1;
+      while (e < b && aj_s[e] == aj_s[k]) ++e;
+      T v = av_s[k];
+      if (e - k > 1) v = add_rn(v, np_pairwise(av_s + k + 1, e - k - 1));
+      ai_o[o] = ai_s[k];
+      aj_o[o] = aj_s[k];
+      av_o[o] = v;
+      ++o;
+      k = e;
+    }
   }
 }
 
@@ -259,12 +363,6 @@ struct spmv_dia_builder {
 struct spmv_dia_collect {
   int64_t nrows = 0, ncols = 0, ndiags = 0, nnz = 0;
   ScratchBuf counts, starts;
-};
-
-struct spmv_coo_sorter {
-  int64_t nnz = 0, n_runs = 0;
-  int col_bits = 32;  // key = row << col_bits | col
-  ScratchBuf keys, perm, run_start;
 };
 
 template <typename V>
@@ -505,95 +603,146 @@ static int bits_for(int64_t n) {  // bits holding 0 .. n-1 (at least 1)
   return b;
 }
 
-int spmv_sort_coo_analyze(int dtype, int64_t nnz, const uint32_t* ai, const uint32_t* aj, void* stream,
-                          spmv_coo_sorter** out, int64_t* nnz_out) {
-  return spmv_sort_coo_analyze_shape(dtype, int64_t(1) << 32, int64_t(1) << 32, nnz, ai, aj, stream, out, nnz_out);
+}  // extern "C"
+
+template <typename T>
+static int sort_coo_run(int64_t nrows, int64_t nnz, const uint32_t* ai, const uint32_t* aj, const T* av,
+                        uint32_t* ai_out, uint32_t* aj_out, T* av_out, int64_t* n_out, cudaStream_t st) {
+  *n_out = 0;
+  if (nnz == 0) return SPMV_OK;
+  int r;
+  ScratchBuf pay_in, rows_buf, pay_buf, tmp, flag;
+  auto tmp_for = [&](size_t bytes) -> int { return bytes > tmp.bytes ? tmp.alloc(bytes, st) : SPMV_OK; };
+  // rows already non-decreasing (a COO without its sorted flag): no stage 1
+  if ((r = flag.alloc(sizeof(int), st))) return r;
+  SPMV_CUDA_TRY(cudaMemsetAsync(flag.ptr, 0, sizeof(int), st));
+  rows_descend_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, nnz, flag.as<int>());
+  SPMV_LAUNCH_CHECK();
+  int hflag = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&hflag, flag.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  const bool rows_sorted = hflag == 0;
+  const uint32_t* rows_p = ai;
+  const unsigned long long* pay_p = nullptr;
+  if (!rows_sorted) {
+    // stage 1: stable sort on the row, (col, storage index) as the payload
+    if ((r = pay_in.alloc(8 * nnz, st)) || (r = pay_buf.alloc(8 * nnz, st)) || (r = rows_buf.alloc(4 * nnz, st)))
+      return r;
+    sort_payload_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(aj, nnz, pay_in.as<unsigned long long>());
+    SPMV_LAUNCH_CHECK();
+    size_t tb = 0;
+    SPMV_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, ai, rows_buf.as<uint32_t>(),
+                                                  pay_in.as<unsigned long long>(), pay_buf.as<unsigned long long>(),
+                                                  nnz, 0, bits_for(nrows), st));
+    if ((r = tmp_for(tb))) return r;
+    SPMV_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, ai, rows_buf.as<uint32_t>(),
+                                                  pay_in.as<unsigned long long>(), pay_buf.as<unsigned long long>(),
+                                                  nnz, 0, bits_for(nrows), st));
+    pay_in.release();
+    rows_p = rows_buf.as<uint32_t>();
+    pay_p = pay_buf.as<unsigned long long>();
+  }
+  size_t tb = 0;
+  // row segments: run lengths of the sorted rows, scanned
+  ScratchBuf uniq, counts, nseg_d, seg;
+  if ((r = uniq.alloc(4 * nnz, st)) || (r = counts.alloc(4 * (nnz + 1), st)) || (r = nseg_d.alloc(8, st))) return r;
+  SPMV_CUDA_TRY(cub::DeviceRunLengthEncode::Encode(nullptr, tb, rows_p, uniq.as<uint32_t>(),
+                                                   counts.as<uint32_t>(), nseg_d.as<int64_t>(), nnz, st));
+  if ((r = tmp_for(tb))) return r;
+  SPMV_CUDA_TRY(cub::DeviceRunLengthEncode::Encode(tmp.ptr, tb, rows_p, uniq.as<uint32_t>(),
+                                                   counts.as<uint32_t>(), nseg_d.as<int64_t>(), nnz, st));
+  int64_t nseg = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&nseg, nseg_d.ptr, 8, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  uniq.release();
+  if ((r = seg.alloc(4 * (nseg + 1), st))) return r;
+  SPMV_CUDA_TRY(cudaMemsetAsync(counts.as<uint32_t>() + nseg, 0, 4, st));
+  if ((r = excl_scan<uint32_t>(counts.as<uint32_t>(), seg.as<uint32_t>(), nseg + 1, st))) return r;
+  // stage 2: columns inside each row, straight to the output positions
+  ScratchBuf ucnt, ndup;
+  if ((r = ucnt.alloc(4 * (nseg + 1), st)) || (r = ndup.alloc(8, st))) return r;
+  SPMV_CUDA_TRY(cudaMemsetAsync(ucnt.ptr, 0, 4 * (nseg + 1), st));
+  SPMV_CUDA_TRY(cudaMemsetAsync(ndup.ptr, 0, 8, st));
+  const int64_t gw = std::min<int64_t>((nseg * 32 + 255) / 256, int64_t(sm_count()) * 64);
+  sort_rows_kernel<T><<<unsigned(gw), 256, 0, st>>>(rows_p, pay_p, seg.as<uint32_t>(), nseg, aj, av, ai_out, aj_out,
+                                                    av_out, ucnt.as<uint32_t>(), ndup.as<unsigned long long>());
+  SPMV_LAUNCH_CHECK();
+  ScratchBuf nlong;
+  if ((r = nlong.alloc(8, st))) return r;
+  SPMV_CUDA_TRY(cudaMemsetAsync(nlong.ptr, 0, 8, st));
+  list_long_segments_kernel<<<unsigned(grid_for(nseg)), 256, 0, st>>>(seg.as<uint32_t>(), nseg, nullptr, nullptr,
+                                                                      nlong.as<unsigned long long>());
+  SPMV_LAUNCH_CHECK();
+  unsigned long long hl = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&hl, nlong.ptr, 8, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  if (hl > 0) {  // rows over 32 entries: a segmented sort of their keys
+    const int64_t nl = int64_t(hl);
+    ScratchBuf lb, le, keys, sorted;
+    if ((r = lb.alloc(4 * nl, st)) || (r = le.alloc(4 * nl, st)) || (r = keys.alloc(8 * nnz, st)) ||
+        (r = sorted.alloc(8 * nnz, st)))
+      return r;
+    SPMV_CUDA_TRY(cudaMemsetAsync(nlong.ptr, 0, 8, st));
+    list_long_segments_kernel<<<unsigned(grid_for(nseg)), 256, 0, st>>>(seg.as<uint32_t>(), nseg, lb.as<uint32_t>(),
+                                                                        le.as<uint32_t>(),
+                                                                        nlong.as<unsigned long long>());
+    const unsigned gl = unsigned(std::min<int64_t>(nl, int64_t(sm_count()) * 16));
+    long_keys_kernel<<<gl, 256, 0, st>>>(pay_p, aj, lb.as<uint32_t>(), le.as<uint32_t>(), nl,
+                                         keys.as<unsigned long long>());
+    SPMV_LAUNCH_CHECK();
+    tb = 0;
+    SPMV_CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(nullptr, tb, keys.as<unsigned long long>(),
+                                                     sorted.as<unsigned long long>(), nnz, nl, lb.as<uint32_t>(),
+                                                     le.as<uint32_t>(), st));
+    if ((r = tmp_for(tb))) return r;
+    SPMV_CUDA_TRY(cub::DeviceSegmentedSort::SortKeys(tmp.ptr, tb, keys.as<unsigned long long>(),
+                                                     sorted.as<unsigned long long>(), nnz, nl, lb.as<uint32_t>(),
+                                                     le.as<uint32_t>(), st));
+    long_emit_kernel<T><<<unsigned(grid_for(nseg)), 256, 0, st>>>(rows_p, sorted.as<unsigned long long>(),
+                                                                  seg.as<uint32_t>(), nseg, av, ai_out, aj_out, av_out,
+                                                                  ucnt.as<uint32_t>(), ndup.as<unsigned long long>());
+    SPMV_LAUNCH_CHECK();
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));  // temporaries leave scope
+  }
+  unsigned long long hd = 0;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(&hd, ndup.ptr, 8, cudaMemcpyDeviceToHost, st));
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  *n_out = nnz - int64_t(hd);
+  if (hd == 0) return SPMV_OK;
+  // stage 3: duplicate runs merged and compacted (through a copy: rows move
+  // to lower positions)
+  ScratchBuf opos, ai_s, aj_s, av_s;
+  if ((r = opos.alloc(4 * (nseg + 1), st)) || (r = ai_s.alloc(4 * nnz, st)) || (r = aj_s.alloc(4 * nnz, st)) ||
+      (r = av_s.alloc(sizeof(T) * nnz, st)))
+    return r;
+  if ((r = excl_scan<uint32_t>(ucnt.as<uint32_t>(), opos.as<uint32_t>(), nseg + 1, st))) return r;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(ai_s.ptr, ai_out, 4 * nnz, cudaMemcpyDeviceToDevice, st));
+  SPMV_CUDA_TRY(cudaMemcpyAsync(aj_s.ptr, aj_out, 4 * nnz, cudaMemcpyDeviceToDevice, st));
+  SPMV_CUDA_TRY(cudaMemcpyAsync(av_s.ptr, av_out, sizeof(T) * nnz, cudaMemcpyDeviceToDevice, st));
+  merge_runs_kernel<T><<<unsigned(grid_for(nseg)), 256, 0, st>>>(seg.as<uint32_t>(), opos.as<uint32_t>(), nseg,
+                                                                 ai_s.as<uint32_t>(), aj_s.as<uint32_t>(), av_s.as<T>(),
+                                                                 ai_out, aj_out, av_out);
+  SPMV_LAUNCH_CHECK();
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  return SPMV_OK;
 }
 
-int spmv_sort_coo_analyze_shape(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* ai,
-                                const uint32_t* aj, void* stream, spmv_coo_sorter** out, int64_t* nnz_out) {
-  if (!out || !nnz_out) return fail(SPMV_INVALID_ARG, "NULL output");
-  *out = nullptr;
+extern "C" int spmv_sort_coo(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* ai, const uint32_t* aj,
+                  const void* av, uint32_t* ai_out, uint32_t* aj_out, void* av_out, int64_t* nnz_out, void* stream) {
+  if (!nnz_out) return fail(SPMV_INVALID_ARG, "NULL output");
   if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
-  if (nnz < 0 || nnz > int64_t(UINT32_MAX)) return fail(SPMV_INVALID_ARG, "bad nnz");
-  cudaStream_t st = as_stream(stream);
+  if (nnz < 0 || nnz > int64_t(UINT32_MAX) - 1) return fail(SPMV_INVALID_ARG, "bad nnz");
   if (nrows < 1 || ncols < 1 || nrows > (int64_t(1) << 32) || ncols > (int64_t(1) << 32))
     return fail(SPMV_INVALID_ARG, "bad COO shape");
-  auto* s = new spmv_coo_sorter();
-  s->nnz = nnz;
-  // Pack (row, col) into bits(nrows) + bits(ncols) bits so the radix sort
-  // runs only the passes it needs (48 bits = 6 passes at 256^3, not 8).
-  s->col_bits = bits_for(ncols);
-  const int key_bits = bits_for(nrows) + s->col_bits;
-  int rc = SPMV_OK;
-  if (nnz > 0) {
-    ScratchBuf keys_in, idx_in, head, pos, tmp;
-    rc = keys_in.alloc(8 * nnz, st);
-    if (!rc) rc = idx_in.alloc(4 * nnz, st);
-    if (!rc) rc = s->keys.alloc(8 * nnz, st);
-    if (!rc) rc = s->perm.alloc(4 * nnz, st);
-    if (!rc) rc = head.alloc(4 * nnz, st);
-    if (!rc) rc = pos.alloc(4 * nnz, st);
-    if (!rc) {
-      make_keys_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, aj, nnz, s->col_bits,
-                                                                keys_in.as<unsigned long long>(), idx_in.as<uint32_t>());
-      size_t tmp_bytes = 0;
-      cudaError_t e = cub::DeviceRadixSort::SortPairs(nullptr, tmp_bytes, keys_in.as<unsigned long long>(),
-                                                      s->keys.as<unsigned long long>(), idx_in.as<uint32_t>(),
-                                                      s->perm.as<uint32_t>(), nnz, 0, key_bits, st);
-      if (e == cudaSuccess) {
-        rc = tmp.alloc(tmp_bytes, st);
-        if (!rc)
-          e = cub::DeviceRadixSort::SortPairs(tmp.ptr, tmp_bytes, keys_in.as<unsigned long long>(),
-                                              s->keys.as<unsigned long long>(), idx_in.as<uint32_t>(),
-                                              s->perm.as<uint32_t>(), nnz, 0, key_bits, st);
-      }
-      if (!rc && e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "radix sort: %s", cudaGetErrorString(e));
-    }
-    if (!rc) {
-      key_heads_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(s->keys.as<unsigned long long>(), nnz,
-                                                                head.as<uint32_t>());
-      rc = excl_scan<uint32_t>(head.as<uint32_t>(), pos.as<uint32_t>(), nnz, st);
-    }
-    if (!rc) rc = scan_total<uint32_t>(head.as<uint32_t>(), pos.as<uint32_t>(), nnz, st, &s->n_runs);
-    if (!rc) rc = s->run_start.alloc(4 * s->n_runs, st);
-    if (!rc) {
-      key_runs_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(head.as<uint32_t>(), pos.as<uint32_t>(), nnz,
-                                                               s->run_start.as<uint32_t>());
-      cudaError_t e = cudaStreamSynchronize(st);
-      if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "sort_coo analyze: %s", cudaGetErrorString(e));
-    }
-  }
-  if (rc) {
-    delete s;
-    return rc;
-  }
-  *nnz_out = s->n_runs;
-  *out = s;
-  return SPMV_OK;
-}
-
-int spmv_sort_coo_emit(const spmv_coo_sorter* s, int dtype, const void* av, uint32_t* ai_out, uint32_t* aj_out,
-                       void* av_out, void* stream) {
-  if (!s) return fail(SPMV_INVALID_ARG, "sorter is NULL");
-  if (!valid_dtype(dtype)) return fail(SPMV_INVALID_ARG, "unsupported dtype %d", dtype);
-  if (s->n_runs == 0) return SPMV_OK;
+  if (nnz > 0 && (!ai || !aj || !av || !ai_out || !aj_out || !av_out)) return fail(SPMV_INVALID_ARG, "NULL pointer");
   cudaStream_t st = as_stream(stream);
   if (dtype == SPMV_F64)
-    sort_emit_kernel<double><<<unsigned(grid_for(s->n_runs)), 256, 0, st>>>(
-        s->keys.as<unsigned long long>(), s->perm.as<uint32_t>(), s->run_start.as<uint32_t>(), s->n_runs, s->nnz,
-        s->col_bits, static_cast<const double*>(av), ai_out, aj_out, static_cast<double*>(av_out));
-  else
-    sort_emit_kernel<float><<<unsigned(grid_for(s->n_runs)), 256, 0, st>>>(
-        s->keys.as<unsigned long long>(), s->perm.as<uint32_t>(), s->run_start.as<uint32_t>(), s->n_runs, s->nnz,
-        s->col_bits, static_cast<const float*>(av), ai_out, aj_out, static_cast<float*>(av_out));
-  SPMV_LAUNCH_CHECK();
-  return SPMV_OK;
+    return sort_coo_run<double>(nrows, nnz, ai, aj, static_cast<const double*>(av), ai_out, aj_out,
+                                static_cast<double*>(av_out), nnz_out, st);
+  return sort_coo_run<float>(nrows, nnz, ai, aj, static_cast<const float*>(av), ai_out, aj_out,
+                             static_cast<float*>(av_out), nnz_out, st);
 }
 
-int spmv_coo_sorter_destroy(spmv_coo_sorter* s) {
-  delete s;
-  return SPMV_OK;
-}
 
-}  // extern "C"
+
+
