@@ -144,6 +144,11 @@ int spmv_csr_plan_destroy(spmv_csr_plan* plan);
 /* Profiling builds only (-DSPMV_PHASE_TIMING): per-phase cycle counters of
  * the CSR tile kernel, read and reset (8 entries); else SPMV_UNSUPPORTED. */
 int spmv_debug_csr_phases(unsigned long long* out8);
+/* Debug builds only (-DSPMV_DEBUG_CHECKS): device-side check counters, read
+ * and reset — [0] TMA-staged tile/step differs from global memory (a ring
+ * race), [1] index out of range, [2] x panel differs from x, [3] other;
+ * else SPMV_UNSUPPORTED. */
+int spmv_debug_check_counts(unsigned long long* out4);
 /* n_long_rows: rows longer than exact_len; n_items: entries per tile;
  * launches: kernels one spmv_csr call launches (1; +1 for the span
  * fix-up of rows split between tiles or warp-stream ranges). */

@@ -45,11 +45,11 @@ def _stale(target: Path, deps) -> bool:
     return any(d.stat().st_mtime > t for d in deps)
 
 
-def _compile(src: Path, verbose: bool) -> Path:
-    obj = OBJ_DIR / (src.stem + ".o")
+def _compile(src: Path, verbose: bool, obj_dir: Path = OBJ_DIR, flags=None) -> Path:
+    obj = obj_dir / (src.stem + ".o")
     if not _stale(obj, [src, *_headers(), Path(__file__)]):
         return obj
-    cmd = [NVCC, *NVCC_FLAGS, "-c", str(src), "-o", str(obj)]
+    cmd = [NVCC, *(flags or NVCC_FLAGS), "-c", str(src), "-o", str(obj)]
     if verbose:
         print(" ".join(cmd), flush=True)
     res = subprocess.run(cmd, capture_output=True, text=True)
@@ -60,31 +60,43 @@ def _compile(src: Path, verbose: bool) -> Path:
     return obj
 
 
-def build(verbose: bool = False, force: bool = False) -> Path:
-    """Compile every csrc/*.cu for sm_100a and link libspmv_b200.so."""
-    OBJ_DIR.mkdir(exist_ok=True)
+DEBUG_LIB_PATH = PKG_DIR / "libspmv_b200_debug.so"
+
+
+def build(verbose: bool = False, force: bool = False, debug: bool = False) -> Path:
+    """Compile every csrc/*.cu for sm_100a and link libspmv_b200.so.
+
+    debug=True builds libspmv_b200_debug.so instead, with the device-side
+    consistency checks (-DSPMV_DEBUG_CHECKS: TMA stages compared with global
+    memory, panel indices bounds-checked; read with spmv_debug_check_counts)
+    — the substitute for compute-sanitizer, which is closed on this pool.
+    Select it at run time with SPMV_B200_LIB."""
+    obj_dir = PKG_DIR / "_objs_debug" if debug else OBJ_DIR
+    lib_path = DEBUG_LIB_PATH if debug else LIB_PATH
+    nvcc_flags = NVCC_FLAGS + (["-DSPMV_DEBUG_CHECKS"] if debug else [])
+    obj_dir.mkdir(exist_ok=True)
     srcs = _sources()
-    stamp = OBJ_DIR / "flags.txt"  # objects built with other flags are stale
-    flags = " ".join(NVCC_FLAGS)
+    stamp = obj_dir / "flags.txt"  # objects built with other flags are stale
+    flags = " ".join(nvcc_flags)
     if not stamp.exists() or stamp.read_text() != flags:
         force = True
     if force:
-        for o in OBJ_DIR.glob("*.o"):
+        for o in obj_dir.glob("*.o"):
             o.unlink()
     with ThreadPoolExecutor(max_workers=min(8, len(srcs))) as ex:
-        objs = list(ex.map(lambda s: _compile(s, verbose), srcs))
+        objs = list(ex.map(lambda s: _compile(s, verbose, obj_dir, nvcc_flags), srcs))
     stamp.write_text(flags)
-    if force or _stale(LIB_PATH, objs):
+    if force or _stale(lib_path, objs):
         # Export only the C ABI (spmv_*); static cudart and C++ internals stay local.
-        cmd = [NVCC, *ARCH, "-shared", "-o", str(LIB_PATH), *map(str, objs),
+        cmd = [NVCC, *ARCH, "-shared", "-o", str(lib_path), *map(str, objs),
                "-Xlinker", f"--version-script={PKG_DIR / 'csrc' / 'exports.map'}"]
         if verbose:
             print(" ".join(cmd), flush=True)
         res = subprocess.run(cmd, capture_output=True, text=True)
         if res.returncode != 0:
             raise RuntimeError(f"link failed:\n{res.stdout}\n{res.stderr}")
-    return LIB_PATH
+    return lib_path
 
 
 if __name__ == "__main__":
-    print(build(verbose=True, force="--force" in sys.argv))
+    print(build(verbose=True, force="--force" in sys.argv, debug="--debug" in sys.argv))

@@ -60,6 +60,7 @@ SIGNATURES = {
     "spmv_coo_plan_config": [_vp, _vp],
     "spmv_dia_ex": [_c_int, _c_i64, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp, _c_i64, _c_i64, _c_i64, _vp, _vp, _vp],
     "spmv_debug_csr_phases": [ctypes.POINTER(ctypes.c_ulonglong)],
+    "spmv_debug_check_counts": [ctypes.POINTER(ctypes.c_ulonglong)],
     "spmv_csr_plan_info": [_vp, _pi64, _pi64, _pi64],
     "spmv_csr": [_vp, _vp, _vp, _vp, _vp, _c_i64, _c_i64, _vp, _vp],
     "spmv_csr_plan_tiles": [_vp, _pi64, _pi64],

@@ -154,6 +154,25 @@ int pool_keep_memory() {
 }
 }  // namespace spmv
 
+namespace spmv {
+int debug_counts_csr(unsigned long long* out4);
+int debug_counts_coo(unsigned long long* out4);
+int debug_counts_dia(unsigned long long* out4);
+}  // namespace spmv
+
+// Debug builds: read and reset the device-side check counters of every
+// kernel translation unit (common.cuh SPMV_DCHECK).  SPMV_UNSUPPORTED in
+// normal builds.
+extern "C" int spmv_debug_check_counts(unsigned long long* out4) {
+  if (!out4) return fail(SPMV_INVALID_ARG, "out is NULL");
+  for (int i = 0; i < 4; ++i) out4[i] = 0;
+  int rc = debug_counts_csr(out4);
+  if (rc == SPMV_UNSUPPORTED) return fail(SPMV_UNSUPPORTED, "library built without SPMV_DEBUG_CHECKS");
+  if (rc || (rc = debug_counts_coo(out4)) || (rc = debug_counts_dia(out4)))
+    return fail(rc, "reading the debug counters failed");
+  return SPMV_OK;
+}
+
 extern "C" int spmv_plan_config_init(spmv_plan_config* cfg) {
   if (!cfg) return fail(SPMV_INVALID_ARG, "cfg is NULL");
   *cfg = config_or_default(nullptr);

@@ -177,6 +177,42 @@ inline int cap_ctas(int per_sm, int cap) {
 }
 
 inline size_t value_size(int dtype) { return dtype == SPMV_F64 ? 8 : 4; }
+
+// ---- debug builds (-DSPMV_DEBUG_CHECKS; _build.build(debug=True)) -----------
+// Device-side consistency checks in place of compute-sanitizer (closed on
+// this pool): every TMA-staged tile / step / x panel is compared with global
+// memory after its barrier completes (a stale or half-written stage, i.e. a
+// ring race, shows up as a mismatch), and the panel path's indices are
+// bounds-checked.  Counters per translation unit: [0] stage mismatch,
+// [1] index out of range, [2] x panel mismatch, [3] other.
+#ifdef SPMV_DEBUG_CHECKS
+static __device__ unsigned long long spmv_dbg_counts[4];
+#define SPMV_DCHECK(cond, k)                                      \
+  do {                                                            \
+    if (!(cond)) atomicAdd(&spmv_dbg_counts[k], 1ull);             \
+  } while (0)
+static inline int debug_read_tu(unsigned long long* out4) {
+  unsigned long long h[4] = {0, 0, 0, 0};
+  if (cudaDeviceSynchronize() != cudaSuccess) return SPMV_CUDA_ERROR;
+  if (cudaMemcpyFromSymbol(h, spmv_dbg_counts, sizeof(h)) != cudaSuccess) return SPMV_CUDA_ERROR;
+  const unsigned long long z[4] = {0, 0, 0, 0};
+  if (cudaMemcpyToSymbol(spmv_dbg_counts, z, sizeof(z)) != cudaSuccess) return SPMV_CUDA_ERROR;
+  for (int i = 0; i < 4; ++i) out4[i] += h[i];
+  return SPMV_OK;
+}
+#else
+#define SPMV_DCHECK(cond, k) \
+  do {                       \
+  } while (0)
+static inline int debug_read_tu(unsigned long long*) { return SPMV_UNSUPPORTED; }
+#endif
+template <typename T> __device__ __forceinline__ bool same_bits(T a, T b);
+template <> __device__ __forceinline__ bool same_bits<double>(double a, double b) {
+  return __double_as_longlong(a) == __double_as_longlong(b);
+}
+template <> __device__ __forceinline__ bool same_bits<float>(float a, float b) {
+  return __float_as_uint(a) == __float_as_uint(b);
+}
 inline bool valid_dtype(int dtype) { return dtype == SPMV_F32 || dtype == SPMV_F64; }
 
 // ------------------------------------------------------------ arithmetic --

@@ -317,6 +317,20 @@ coo_tile_kernel(const __grid_constant__ CooParams<T> P) {
       if (G > 1)
         while (tickets[s] != int(i)) __nanosleep(32);
       mbar_wait(&bars[s], uint32_t((i / STAGES) & 1));
+#ifdef SPMV_DEBUG_CHECKS
+      {  // the staged rows / columns / values are exactly the global ones
+        const int64_t E0 = t * TILE;
+        const int cnt = int(min(int64_t(TILE + kExt), P.nnz - E0));
+        const int pre = t > 0 ? kExt : 0;
+        for (int k = tid - pre; k < cnt; k += NT) {
+          SPMV_DCHECK(rows_of(s)[kExt + k] == P.ai[E0 + k], 0);
+          if (k >= 0) {
+            SPMV_DCHECK(cols_of(s)[k] == P.aj[E0 + k], 0);
+            SPMV_DCHECK(same_bits(vals_of(s)[k], P.av[E0 + k]), 0);
+          }
+        }
+      }
+#endif
     } else {
       t = tail0 + (i - mine_bulk) * stride;
       const int64_t E0 = t * TILE;
@@ -1188,6 +1202,10 @@ __global__ void coo_vla_count_steps_kernel(const uint32_t* __restrict__ run_star
   for (int o = 16; o >= 1; o >>= 1) c += __shfl_down_sync(0xffffffffu, c, o);
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(steps, c);
 }
+
+namespace spmv {
+int debug_counts_coo(unsigned long long* out4) { return debug_read_tu(out4); }
+}  // namespace spmv
 
 // The vla step counter of the stream's scratch slot.
 static int steps_slot(const spmv_coo_plan* p, cudaStream_t st, unsigned long long** out) {

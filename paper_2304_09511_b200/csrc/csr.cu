@@ -304,6 +304,16 @@ csr_tile_kernel(const __grid_constant__ CsrParams<T> P) {
       if (G > 1)
         while (tickets[s] != int(i)) __nanosleep(32);
       mbar_wait(&bars[s], uint32_t((i / STAGES) & 1));
+#ifdef SPMV_DEBUG_CHECKS
+      {  // the staged tile is exactly the global entries (no ring race)
+        const int64_t E0 = t * TILE;
+        const int cnt = int(min(int64_t(TILE + kExt), P.nnz - E0));
+        for (int k = grp.tid; k < cnt; k += NT) {
+          SPMV_DCHECK(cols_of(s)[k] == P.aj[E0 + k], 0);
+          SPMV_DCHECK(same_bits(vals_of(s)[k], P.av[E0 + k]), 0);
+        }
+      }
+#endif
     } else {
       t = tail0 + (i - mine_bulk) * stride;
       const int64_t E0 = t * TILE;
@@ -1521,6 +1531,10 @@ static int csr_vla_split_launch(const spmv_csr_plan* p, const uint32_t* irp, con
   }
   return SPMV_OK;
 }
+
+namespace spmv {
+int debug_counts_csr(unsigned long long* out4) { return debug_read_tu(out4); }
+}  // namespace spmv
 
 extern "C" {
 

@@ -140,6 +140,13 @@ dia_bulk_kernel(const T* __restrict__ vals, const int32_t* __restrict__ offsets,
     const int64_t lr0 = t * rows_per_tile;
     const int64_t sr0 = slab_row(lr0);
     const T* tile = reinterpret_cast<const T*>(bufs + size_t(s) * stage_bytes);
+#ifdef SPMV_DEBUG_CHECKS
+    {  // the staged rows are exactly the global block (no ring race)
+      int64_t rr = (GAPPED && lr0 < split ? split : avail_rows) - lr0;
+      if (rr > rows_per_tile) rr = rows_per_tile;
+      for (int64_t k = tid; k < rr * nd; k += NT) SPMV_DCHECK(same_bits(tile[k], vals[sr0 * nd + k]), 0);
+    }
+#endif
     int64_t rows = (GAPPED && lr0 < split ? split : nrows) - lr0;
     if (rows > rows_per_tile) rows = rows_per_tile;
     for (int lr = tid; lr < rows; lr += NT)
@@ -292,6 +299,10 @@ static int dia_launch(int64_t nrows, int64_t ncols, int64_t nd, int64_t avail_ro
 }  // namespace spmv
 
 using namespace spmv;
+
+namespace spmv {
+int debug_counts_dia(unsigned long long* out4) { return debug_read_tu(out4); }
+}  // namespace spmv
 
 extern "C" int spmv_dia_gapped(int dtype, int64_t nrows, int64_t ncols, int64_t ndiags, int64_t avail_rows,
                                const int32_t* offsets, const void* values, const void* x, int64_t row_base,

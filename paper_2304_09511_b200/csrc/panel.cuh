@@ -218,6 +218,18 @@ __device__ __forceinline__ void panel_slice(const uint16_t* __restrict__ pcol, c
     PanelRegs<T> r;
     mbar_wait(bar, phase);
     phase ^= 1u;
+#ifdef SPMV_DEBUG_CHECKS
+    {  // the warp's stage holds exactly this step (no stage race)
+      const T* vs = reinterpret_cast<const T*>(stage);
+      const uint16_t* cs = reinterpret_cast<const uint16_t*>(stage + kPanelStep * sizeof(T));
+      for (int k = lane; k < kPanelStep; k += 32) {
+        SPMV_DCHECK(same_bits(vs[k], pval[base + k]), 0);
+        SPMV_DCHECK(cs[k] == pcol[base + k], 0);
+        SPMV_DCHECK(cs[k] < kPanelCols, 1);
+      }
+      SPMV_DCHECK(stage[kPanelStep * sizeof(T) + kPanelStep * 2 + lane] == pflag[base / 8 + lane], 0);
+    }
+#endif
     panel_read(stage, lane, r);
     __syncwarp();
     if (more && lane == 0) {
@@ -274,6 +286,9 @@ __global__ void __launch_bounds__(kPanelWarps * 32, 1) csr_panel_kernel(const __
       phase ^= 1u;
     }
     __syncthreads();
+#ifdef SPMV_DEBUG_CHECKS
+    for (int64_t c = lo + threadIdx.x; c < hi; c += blockDim.x) SPMV_DCHECK(same_bits(xs[c - c0], src[c - lo]), 2);
+#endif
     const uint32_t t = it * kPanelWarps + uint32_t(warp);
     const uint32_t b = P.task_begin[t];
     const uint32_t e = warp + 1 < kPanelWarps ? P.task_begin[t + 1] : P.item_end[it];

@@ -43,3 +43,20 @@ def lib_built():
     """Build libspmv_b200.so in-tree (cheap when up to date)."""
     from paper_2304_09511_b200 import _build
     return _build.build()
+
+
+def pytest_sessionfinish(session, exitstatus):
+    """Debug-library runs (SPMV_DEBUG_CHECKS=1 with SPMV_B200_LIB pointing at
+    libspmv_b200_debug.so): the device-side check counters must be zero."""
+    import os
+    if os.environ.get("SPMV_DEBUG_CHECKS") != "1":
+        return
+    import ctypes
+
+    from paper_2304_09511_b200 import _lib
+    c = (ctypes.c_ulonglong * 4)()
+    _lib.call("spmv_debug_check_counts", c)
+    counts = list(c)
+    print(f"\ndebug check counters (stage mismatch, index range, x panel, other): {counts}")
+    if any(counts):
+        session.exitstatus = 1

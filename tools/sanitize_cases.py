@@ -87,4 +87,15 @@ for s in (s1, s2, s1, s2):
 torch.cuda.synchronize()
 for o in outs:
     check(o.cpu().numpy(), lref, short)
+import ctypes  # noqa: E402
+import os  # noqa: E402
+
+from paper_2304_09511_b200 import _lib  # noqa: E402
+
+if os.environ.get("SPMV_DEBUG_CHECKS") == "1":
+    c = (ctypes.c_ulonglong * 4)()
+    _lib.call("spmv_debug_check_counts", c)
+    counts = list(c)
+    print("debug check counters (stage mismatch, index range, x panel, other):", counts)
+    assert counts == [0, 0, 0, 0], counts
 print("sanitize cases ok")
