@@ -95,18 +95,10 @@ typedef struct {
                               /* rows start from +0.0 (np.add.at order; COO plans set */
                               /* it for their CSR view); 0 = off                      */
     int32_t panels;           /* CSR column-panel path for long rows: -1 auto (rows   */
-                              /* over panel_row_len entries hold >= half the entries, */
-                              /* ncols >= 65536), 0 off, 1 on (needs col_indices and  */
-                              /* values at plan creation)                             */
-    int32_t panel_cols;       /* columns per x panel of the column-panel path; 0 =    */
-                              /* plan's choice (panel count dividing the SM count,    */
-                              /* the panel and two stream stages per warp in shared   */
-                              /* memory); clamped to what fits                        */
-    int32_t panel_row_len;    /* column-panel path: rows of at most this many entries */
-                              /* are computed in row order by the kernel's gather     */
-                              /* warps (bit-exact), longer ones through the panels;   */
-                              /* 32..256, 0 = 128                                     */
-    int32_t reserved[2];
+                              /* over 32 entries hold >= half the entries, ncols >=   */
+                              /* 65536), 0 off, 1 on (needs col_indices and values at */
+                              /* plan creation)                                       */
+    int32_t reserved[4];
 } spmv_plan_config;
 
 /* Fill *cfg with the auto values (version set).  Plans created with a NULL

@@ -168,9 +168,7 @@ inline spmv_plan_config config_or_default(const spmv_plan_config* c) {
   d.dia_rows = 0;
   d.flags = 0;
   d.panels = -1;
-  d.panel_cols = 0;
-  d.panel_row_len = 0;
-  for (int i = 0; i < 2; ++i) d.reserved[i] = 0;
+  for (int i = 0; i < 4; ++i) d.reserved[i] = 0;
   return c ? *c : d;
 }
 inline int cap_ctas(int per_sm, int cap) {

@@ -741,13 +741,10 @@ struct spmv_csr_plan {
   // launches; the short rows run as their own CSR (sub plan, y via srow)
   bool panel = false;
   int64_t pn_long = 0, pn_entries = 0, pn_seg = 0, pn_ctas = 0, pn_items = 0, pn_short = 0, pn_short_nnz = 0;
-  int64_t pn_cols = 0, pn_slices = 0, pn_steps = 0, pn_parts = 0;  // panel width, slices, stream steps, partials listed
-  int pn_stages = 0;                                               // stream stages per warp
-  DevBuf pn_lrow, pn_ptr, pn_col, pn_val, pn_rseg, pn_cta_item, pn_item_panel, pn_task;
-  // gather side: rows of <= pn_row_len entries by length class (PanelParams)
-  int64_t pn_row_len = 0, pn_nblk = 0;
-  DevBuf pn_srow, pn_scol, pn_sval, pn_cls, pn_ebase, pn_blk;
-  size_t off_pn_ctr = 0;
+  DevBuf pn_lrow, pn_ptr, pn_col, pn_val, pn_flag, pn_rseg, pn_cta_item, pn_item_panel, pn_item_end, pn_task_begin,
+      pn_task_seg0;
+  DevBuf pn_srow, pn_scol, pn_sval;  // short rows by length class (ShortEll)
+  ShortEll pn_ell;
   const void* pn_aj = nullptr;  // the arrays the panel copy was made from: other arrays take the ws path
   const void* pn_av = nullptr;
   size_t off_part = 0;
@@ -946,37 +943,31 @@ static int csr_run_panel(const spmv_csr_plan* p, const T* x, int64_t col_base, i
   unsigned char* scr = nullptr;
   int rc = p->scratch.get(st, reinterpret_cast<void**>(&scr));
   if (rc) return rc;
-  const int sms = sm_count();
+  if (p->pn_short > 0) {
+    const int64_t gs = std::min<int64_t>((p->pn_short + 255) / 256, int64_t(sm_count()) * 16);
+    short_ell_kernel<T><<<unsigned(gs), 256, 0, st>>>(p->pn_ell, p->pn_scol.as<uint32_t>(), p->pn_sval.as<T>(),
+                                                      p->pn_srow.as<uint32_t>(), p->pn_short, x, col_base, y,
+                                                      (p->cfg.flags & 4) != 0);
+    SPMV_LAUNCH_CHECK();
+  }
+  if (p->pn_long == 0) return SPMV_OK;
   PanelParams<T> P;
-  P.pcol = p->pn_col.as<uint8_t>();
+  P.pcol = p->pn_col.as<uint16_t>();
   P.pval = p->pn_val.as<T>();
+  P.pflag = p->pn_flag.as<uint8_t>();
   P.x = x;
   P.col_base = col_base;
   P.x_len = x_len;
   P.ncols = p->ncols;
-  P.panel_cols = int32_t(p->pn_cols);
-  P.nstg = p->pn_stages;
   P.cta_item = p->pn_cta_item.as<uint32_t>();
   P.item_panel = p->pn_item_panel.as<uint32_t>();
-  P.task = p->pn_task.as<uint32_t>();
+  P.item_end = p->pn_item_end.as<uint32_t>();
+  P.task_begin = p->pn_task_begin.as<uint32_t>();
+  P.task_seg0 = p->pn_task_seg0.as<uint32_t>();
   P.part = reinterpret_cast<double*>(scr + p->off_part);
-  P.y = y;
-  P.blk = p->pn_blk.as<uint32_t>();
-  P.cls = p->pn_cls.as<uint32_t>();
-  P.ebase = p->pn_ebase.as<uint32_t>();
-  P.scol = p->pn_scol.as<uint32_t>();
-  P.sval = p->pn_sval.as<T>();
-  P.srow = p->pn_srow.as<uint32_t>();
-  P.nblk = uint32_t(p->pn_nblk);
-  P.gather_warps = uint32_t(sms) * kGatherWarps;
-  P.ctr = reinterpret_cast<uint32_t*>(scr + p->off_pn_ctr);
-  P.pos_seed = (p->cfg.flags & 4) != 0;
-  // one CTA per SM: panel warps stream the long rows, gather warps the short ones
-  const size_t smem = p->pn_long > 0 ? size_t(panel_smem_bytes<T>(p->pn_cols, p->pn_stages)) : 0;
-  csr_panel_kernel<T><<<unsigned(sms), kPanelThreads, smem, st>>>(P);
+  csr_panel_kernel<T><<<unsigned(p->pn_ctas), kPanelWarps * 32, panel_smem_bytes<T>(), st>>>(P);
   SPMV_LAUNCH_CHECK();
-  if (p->pn_long == 0) return SPMV_OK;
-  const int64_t g = std::min<int64_t>((p->pn_long + 7) / 8, int64_t(sms) * 8);
+  const int64_t g = std::min<int64_t>((p->pn_long * 8 + 255) / 256, int64_t(sm_count()) * 16);
   csr_panel_finish_kernel<T><<<unsigned(g), 256, 0, st>>>(p->pn_lrow.as<uint32_t>(), p->pn_ptr.as<uint32_t>(),
                                                           p->pn_rseg.as<uint32_t>(), p->pn_long, P.part, y);
   SPMV_LAUNCH_CHECK();
@@ -1142,13 +1133,13 @@ __global__ void long_entries_kernel(const uint32_t* __restrict__ irp, int64_t nr
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(n, c);
 }
 
-// ptr[q] = first index whose key >> shift is >= q (keys sorted by that field), q = 0..nkeys.
-__global__ void panel_bounds_kernel(const uint32_t* __restrict__ skey, int64_t nl, int64_t nkeys,
-                                    uint32_t* __restrict__ ptr, int shift = 0) {
+// panel_ptr[q] = first panel-major entry of panel q (skey sorted).
+__global__ void panel_bounds_kernel(const uint32_t* __restrict__ skey, int64_t nl, int64_t npanels,
+                                    uint32_t* __restrict__ pan_ptr) {
   for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= nl; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t q1 = i < nl ? int64_t(skey[i] >> shift) : nkeys;
-    const int64_t q0 = i == 0 ? -1 : int64_t(skey[i - 1] >> shift);
-    for (int64_t q = q0 + 1; q <= q1; ++q) ptr[q] = uint32_t(i);
+    const int64_t q1 = i < nl ? int64_t(skey[i]) : npanels;
+    const int64_t q0 = i == 0 ? -1 : int64_t(skey[i - 1]);
+    for (int64_t q = q0 + 1; q <= q1; ++q) pan_ptr[q] = uint32_t(i);
   }
 }
 
@@ -1179,52 +1170,21 @@ static int cub_call(Fn fn, ScratchBuf& tmp, cudaStream_t st) {
 // with segment flags and slots, the CTA / warp work cuts, and the short
 // rows as their own CSR with a sub plan.  Device work with cub sorts and
 // scans; a few small host round trips for the cuts.
-// Panel width and stream stages per warp: the fewest panels whose width
-// fits shared memory beside two stages per warp, with a panel count that
-// divides the SM count or is a multiple of it (every CTA's equal share of
-// the stream then lies inside one panel when the columns are spread
-// evenly).  `want` > 0 (spmv_plan_config.panel_cols) fixes the width.
-template <typename T>
-static void panel_shape(int64_t ncols, int sms, int64_t want, int64_t* W, int* nstg) {
-  const int64_t unit = 16 / int64_t(sizeof(T));
-  int64_t w;
-  if (want > 0) {
-    w = std::min<int64_t>(std::max<int64_t>(want, unit), panel_max_cols<T>(1));
-  } else {
-    const int64_t wmax = panel_max_cols<T>(2);
-    int64_t np = (std::max<int64_t>(ncols, 1) + wmax - 1) / wmax;
-    while (!(sms % np == 0 || np % sms == 0)) ++np;
-    w = (std::max<int64_t>(ncols, 1) + np - 1) / np;
-  }
-  w = std::min<int64_t>((w + unit - 1) / unit * unit, panel_max_cols<T>(1));
-  int s = kPanelMaxStages;
-  while (s > 1 && panel_smem_bytes<T>(w, s) > kPanelSmemMax) --s;
-  *W = w;
-  *nstg = s;
-}
-
 template <typename T>
 static int csr_panel_build(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const T* av, cudaStream_t st) {
   int rc;
   const int64_t n = p->nrows;
   const int sms = sm_count();
-  panel_shape<T>(p->ncols, sms, p->cfg.panel_cols, &p->pn_cols, &p->pn_stages);
-  // rows of at most T entries go to the gather side, longer ones to the panels
-  const int64_t T_len = p->pn_row_len;
   const int64_t g = std::min<int64_t>((n + 255) / 256, int64_t(sms) * 16);
   ScratchBuf is_long, pos, tmp;
-  if ((rc = is_long.alloc(4 * (n + 1), st)) || (rc = pos.alloc(4 * (n + 1), st))) return rc;
-  SPMV_CUDA_TRY(cudaMemsetAsync(is_long.as<uint32_t>() + n, 0, 4, st));
-  split_rows_flags_kernel<<<unsigned(g), 256, 0, st>>>(irp, n, uint32_t(T_len), is_long.as<uint32_t>());
+  if ((rc = is_long.alloc(4 * n, st)) || (rc = pos.alloc(4 * (n + 1), st))) return rc;
+  split_rows_flags_kernel<<<unsigned(g), 256, 0, st>>>(irp, n, uint32_t(kExactLen), is_long.as<uint32_t>());
   SPMV_LAUNCH_CHECK();
   if ((rc = cub_call([&](void* t, size_t& b) {
-         return cub::DeviceScan::ExclusiveSum(t, b, is_long.as<uint32_t>(), pos.as<uint32_t>(), n + 1, st);
+         return cub::DeviceScan::ExclusiveSum(t, b, is_long.as<uint32_t>(), pos.as<uint32_t>(), n, st);
        }, tmp, st)))
     return rc;
-  uint32_t hlong = 0;
-  SPMV_CUDA_TRY(cudaMemcpyAsync(&hlong, pos.as<uint32_t>() + n, 4, cudaMemcpyDeviceToHost, st));
-  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
-  const int64_t nlong = hlong, ns = n - nlong;
+  const int64_t nlong = p->n_long, ns = n - nlong;
   p->pn_long = nlong;
   p->pn_short = ns;
   if ((rc = p->pn_lrow.alloc(4 * std::max<int64_t>(nlong, 1))) || (rc = p->pn_srow.alloc(4 * std::max<int64_t>(ns, 1))))
@@ -1251,258 +1211,177 @@ static int csr_panel_build(spmv_csr_plan* p, const uint32_t* irp, const uint32_t
   const int64_t nl = hnl;
   p->pn_entries = nl;
   p->pn_short_nnz = p->nnz - nl;
-  // the gather side's rows grouped by exact length, each class stored
-  // column-major (entry j of every row of the class contiguous): one thread
-  // per row, coalesced loads, the row summed left to right
-  const int ncls = int(T_len) + 1;  // lengths 0..T
-  std::vector<uint32_t> cls(ncls + 1, 0), ebase(ncls + 1, 0), blk;
+  // the short rows (<= 32 entries) grouped by exact length, each class
+  // stored column-major (entry j of every row of the class contiguous):
+  // one thread per row, coalesced loads, the row summed left to right
   if (ns > 0) {
     ScratchBuf skey2, srow2;
     if ((rc = skey2.alloc(4 * ns, st)) || (rc = srow2.alloc(4 * ns, st))) return rc;
     const int64_t gs = std::min<int64_t>((ns + 255) / 256, int64_t(sms) * 16);
     listed_lengths_kernel<<<unsigned(gs), 256, 0, st>>>(irp, p->pn_srow.as<uint32_t>(), ns, len.as<uint32_t>());
     SPMV_LAUNCH_CHECK();
-    int len_bits = 1;
-    while ((int64_t(1) << len_bits) <= T_len) ++len_bits;
     if ((rc = cub_call([&](void* t, size_t& bb) {
            return cub::DeviceRadixSort::SortPairs(t, bb, len.as<uint32_t>(), skey2.as<uint32_t>(),
-                                                  p->pn_srow.as<uint32_t>(), srow2.as<uint32_t>(), ns, 0, len_bits, st);
+                                                  p->pn_srow.as<uint32_t>(), srow2.as<uint32_t>(), ns, 0, 6, st);
          }, tmp, st)))
       return rc;
     SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_srow.ptr, srow2.ptr, 4 * ns, cudaMemcpyDeviceToDevice, st));
     ScratchBuf dcls;
-    if ((rc = dcls.alloc(4 * (ncls + 1), st))) return rc;
-    panel_bounds_kernel<<<unsigned(gs), 256, 0, st>>>(skey2.as<uint32_t>(), ns, ncls, dcls.as<uint32_t>());
+    if ((rc = dcls.alloc(4 * (kShortClasses + 1), st))) return rc;
+    panel_bounds_kernel<<<unsigned(gs), 256, 0, st>>>(skey2.as<uint32_t>(), ns, kShortClasses, dcls.as<uint32_t>());
     SPMV_LAUNCH_CHECK();
-    SPMV_CUDA_TRY(cudaMemcpyAsync(cls.data(), dcls.ptr, 4 * (ncls + 1), cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_ell.cls, dcls.ptr, 4 * (kShortClasses + 1), cudaMemcpyDeviceToHost, st));
     SPMV_CUDA_TRY(cudaStreamSynchronize(st));
     uint64_t acc = 0;
-    for (int L = 0; L < ncls; ++L) {
-      ebase[L] = uint32_t(acc);
-      acc += uint64_t(L) * (cls[L + 1] - cls[L]);
+    for (int L = 0; L < kShortClasses; ++L) {
+      p->pn_ell.ebase[L] = uint32_t(acc);
+      acc += uint64_t(L) * (p->pn_ell.cls[L + 1] - p->pn_ell.cls[L]);
     }
-    ebase[ncls] = uint32_t(acc);
-    if (acc >= (uint64_t(1) << 32)) return fail(SPMV_UNSUPPORTED, "gather side too large");
-    for (int L = ncls - 1; L >= 0; --L) {  // blocks, longest class first
-      const uint32_t nL = cls[L + 1] - cls[L], per = uint32_t(short_rows_per_thread(L));
-      for (uint32_t b = 0; uint64_t(b) * 32 * per < nL; ++b) blk.push_back((uint32_t(L) << 23) | (b * per));
-      if (uint64_t(nL) >= (uint64_t(1) << 28)) return fail(SPMV_UNSUPPORTED, "gather class too large");
-    }
-    if ((rc = p->pn_scol.alloc(4 * std::max<uint64_t>(acc, 1))) || (rc = p->pn_sval.alloc(sizeof(T) * std::max<uint64_t>(acc, 1))) ||
-        (rc = p->pn_cls.alloc(4 * (ncls + 1))) || (rc = p->pn_ebase.alloc(4 * (ncls + 1))) ||
-        (rc = p->pn_blk.alloc(4 * std::max<size_t>(1, blk.size()))))
+    if ((rc = p->pn_scol.alloc(4 * std::max<uint64_t>(acc, 1))) || (rc = p->pn_sval.alloc(sizeof(T) * std::max<uint64_t>(acc, 1))))
       return rc;
-    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_cls.ptr, cls.data(), 4 * (ncls + 1), cudaMemcpyHostToDevice, st));
-    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_ebase.ptr, ebase.data(), 4 * (ncls + 1), cudaMemcpyHostToDevice, st));
-    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_blk.ptr, blk.data(), 4 * blk.size(), cudaMemcpyHostToDevice, st));
-    short_ell_fill_kernel<T><<<unsigned(gs), 256, 0, st>>>(p->pn_cls.as<uint32_t>(), p->pn_ebase.as<uint32_t>(), ncls,
-                                                            irp, aj, av, p->pn_srow.as<uint32_t>(), ns,
+    short_ell_fill_kernel<T><<<unsigned(gs), 256, 0, st>>>(p->pn_ell, irp, aj, av, p->pn_srow.as<uint32_t>(), ns,
                                                             p->pn_scol.as<uint32_t>(), p->pn_sval.as<T>());
     SPMV_LAUNCH_CHECK();
-    SPMV_CUDA_TRY(cudaStreamSynchronize(st));  // the host vectors are read by the copies above
   }
-  p->pn_nblk = int64_t(blk.size());
-  // CTAs without panel work still run their gather warps
-  if ((rc = p->pn_cta_item.alloc(4 * (sms + 1)))) return rc;
-  SPMV_CUDA_TRY(cudaMemsetAsync(p->pn_cta_item.ptr, 0, 4 * (sms + 1), st));
   if (nlong == 0) return SPMV_OK;
   // long entries: (panel, long-entry index), stable sort by panel
-  const int64_t W = p->pn_cols;
-  const int64_t npanels = (p->ncols + W - 1) / W;
-  int panel_bits = 1;
-  while (panel_bits < 26 && (int64_t(1) << panel_bits) < npanels) ++panel_bits;
+  const int64_t npanels = (p->ncols + kPanelCols - 1) / kPanelCols;
+  int end_bit = 1;
+  while (end_bit < 32 && (int64_t(1) << end_bit) < npanels) ++end_bit;
   ScratchBuf key, skey, val, perm, erow, eidx;
   if ((rc = key.alloc(4 * nl, st)) || (rc = skey.alloc(4 * nl, st)) || (rc = val.alloc(4 * nl, st)) ||
       (rc = perm.alloc(4 * nl, st)) || (rc = erow.alloc(4 * nl, st)) || (rc = eidx.alloc(4 * nl, st)))
     return rc;
   const int64_t gl = std::min<int64_t>((nlong * 32 + 255) / 256, int64_t(sms) * 16);
   panel_expand_kernel<<<unsigned(gl), 256, 0, st>>>(irp, aj, p->pn_lrow.as<uint32_t>(), lptr.as<uint32_t>(), nlong,
-                                                    uint32_t(W), key.as<uint32_t>(), val.as<uint32_t>(),
-                                                    erow.as<uint32_t>(), eidx.as<uint32_t>());
+                                                    key.as<uint32_t>(), val.as<uint32_t>(), erow.as<uint32_t>(),
+                                                    eidx.as<uint32_t>());
   SPMV_LAUNCH_CHECK();
   if ((rc = cub_call([&](void* t, size_t& b) {
          return cub::DeviceRadixSort::SortPairs(t, b, key.as<uint32_t>(), skey.as<uint32_t>(), val.as<uint32_t>(),
-                                                perm.as<uint32_t>(), nl, 0, panel_bits, st);
+                                                perm.as<uint32_t>(), nl, 0, end_bit, st);
        }, tmp, st)))
     return rc;
-  // (row, panel) segments of the panel-major order
+  // panel-major copy (padded: the kernel loads whole 8-entry groups)
+  const int64_t pad = 32 * kPanelK + 8;
+  if ((rc = p->pn_col.alloc(2 * (nl + pad))) || (rc = p->pn_val.alloc(sizeof(T) * (nl + pad)))) return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(p->pn_col.ptr, 0, 2 * (nl + pad), st));
+  SPMV_CUDA_TRY(cudaMemsetAsync(p->pn_val.ptr, 0, sizeof(T) * (nl + pad), st));
   ScratchBuf flag, seg_of;
   if ((rc = flag.alloc(4 * nl, st)) || (rc = seg_of.alloc(4 * (nl + 1), st))) return rc;
   const int64_t ge = std::min<int64_t>((nl + 255) / 256, int64_t(sms) * 32);
-  panel_flag_kernel<<<unsigned(ge), 256, 0, st>>>(skey.as<uint32_t>(), perm.as<uint32_t>(), erow.as<uint32_t>(), nl,
-                                                  flag.as<uint32_t>());
+  panel_gather_kernel<T><<<unsigned(ge), 256, 0, st>>>(skey.as<uint32_t>(), perm.as<uint32_t>(), erow.as<uint32_t>(),
+                                                       eidx.as<uint32_t>(), aj, av, nl, p->pn_col.as<uint16_t>(),
+                                                       p->pn_val.as<T>(), flag.as<uint32_t>());
   SPMV_LAUNCH_CHECK();
   if ((rc = cub_call([&](void* t, size_t& b) {
          return cub::DeviceScan::ExclusiveSum(t, b, flag.as<uint32_t>(), seg_of.as<uint32_t>(), nl, st);
        }, tmp, st)))
     return rc;
+  if ((rc = p->pn_flag.alloc((nl + pad) / 8 + 8))) return rc;
+  SPMV_CUDA_TRY(cudaMemsetAsync(p->pn_flag.ptr, 0, (nl + pad) / 8 + 8, st));
+  panel_flag_bytes_kernel<<<unsigned(std::min<int64_t>((nl / 8 + 256) / 256, int64_t(sms) * 16)), 256, 0, st>>>(
+      flag.as<uint32_t>(), nl, p->pn_flag.as<uint8_t>());
+  SPMV_LAUNCH_CHECK();
   uint32_t hs[2];
   SPMV_CUDA_TRY(cudaMemcpyAsync(&hs[0], seg_of.as<uint32_t>() + nl - 1, 4, cudaMemcpyDeviceToHost, st));
   SPMV_CUDA_TRY(cudaMemcpyAsync(&hs[1], flag.as<uint32_t>() + nl - 1, 4, cudaMemcpyDeviceToHost, st));
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
   const int64_t nseg = int64_t(hs[0]) + hs[1];
   p->pn_seg = nseg;
-  ScratchBuf seg_start, seg_row, seg_panel, nsub, sub_base;
-  if ((rc = seg_start.alloc(4 * (nseg + 1), st)) || (rc = seg_row.alloc(4 * nseg, st)) ||
-      (rc = seg_panel.alloc(4 * nseg, st)) || (rc = nsub.alloc(4 * (nseg + 1), st)) ||
-      (rc = sub_base.alloc(4 * (nseg + 1), st)))
+  // per segment its long row; per long row its segment count -> partial ptr
+  ScratchBuf seg_row, row_cnt, order, iota;
+  if ((rc = seg_row.alloc(4 * nseg, st)) || (rc = row_cnt.alloc(4 * (nlong + 1), st)) ||
+      (rc = order.alloc(4 * nseg, st)) || (rc = iota.alloc(4 * nseg, st)) || (rc = p->pn_ptr.alloc(4 * (nlong + 1))) ||
+      (rc = p->pn_rseg.alloc(4 * nseg)))
     return rc;
-  panel_segments_kernel<<<unsigned(ge), 256, 0, st>>>(flag.as<uint32_t>(), seg_of.as<uint32_t>(), skey.as<uint32_t>(),
-                                                      perm.as<uint32_t>(), erow.as<uint32_t>(), nl, nseg,
-                                                      seg_start.as<uint32_t>(), seg_row.as<uint32_t>(),
-                                                      seg_panel.as<uint32_t>());
-  SPMV_LAUNCH_CHECK();
-  // sub-segments of at most kPanelH entries, sorted by (panel, longest first)
-  const int64_t gsg = std::min<int64_t>((nseg + 256) / 256, int64_t(sms) * 16);
-  panel_nsub_kernel<<<unsigned(gsg), 256, 0, st>>>(seg_start.as<uint32_t>(), nseg, nsub.as<uint32_t>());
+  SPMV_CUDA_TRY(cudaMemsetAsync(row_cnt.ptr, 0, 4 * (nlong + 1), st));
+  panel_segments_kernel<<<unsigned(ge), 256, 0, st>>>(flag.as<uint32_t>(), seg_of.as<uint32_t>(), perm.as<uint32_t>(),
+                                                      erow.as<uint32_t>(), nl, seg_row.as<uint32_t>(),
+                                                      row_cnt.as<uint32_t>());
   SPMV_LAUNCH_CHECK();
   if ((rc = cub_call([&](void* t, size_t& b) {
-         return cub::DeviceScan::ExclusiveSum(t, b, nsub.as<uint32_t>(), sub_base.as<uint32_t>(), nseg + 1, st);
+         return cub::DeviceScan::ExclusiveSum(t, b, row_cnt.as<uint32_t>(), p->pn_ptr.as<uint32_t>(), nlong + 1, st);
        }, tmp, st)))
     return rc;
-  uint32_t hns = 0;
-  SPMV_CUDA_TRY(cudaMemcpyAsync(&hns, sub_base.as<uint32_t>() + nseg, 4, cudaMemcpyDeviceToHost, st));
-  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
-  const int64_t nsubs = hns;
-  p->pn_parts = nsubs;
-  ScratchBuf sub_key, sub_id, sub_seg, skey_s, sperm;
-  if ((rc = sub_key.alloc(4 * nsubs, st)) || (rc = sub_id.alloc(4 * nsubs, st)) || (rc = sub_seg.alloc(4 * nsubs, st)) ||
-      (rc = skey_s.alloc(4 * nsubs, st)) || (rc = sperm.alloc(4 * nsubs, st)))
-    return rc;
-  panel_subs_kernel<<<unsigned(gsg), 256, 0, st>>>(seg_start.as<uint32_t>(), seg_panel.as<uint32_t>(),
-                                                   sub_base.as<uint32_t>(), nseg, sub_key.as<uint32_t>(),
-                                                   sub_id.as<uint32_t>(), sub_seg.as<uint32_t>());
+  const int64_t gsg = std::min<int64_t>((nseg + 255) / 256, int64_t(sms) * 16);
+  iota_u32_kernel<<<unsigned(gsg), 256, 0, st>>>(iota.as<uint32_t>(), nseg);
   SPMV_LAUNCH_CHECK();
+  int row_bits = 1;
+  while (row_bits < 32 && (int64_t(1) << row_bits) < nlong) ++row_bits;
+  ScratchBuf srow_key;
+  if ((rc = srow_key.alloc(4 * nseg, st))) return rc;
   if ((rc = cub_call([&](void* t, size_t& b) {
-         return cub::DeviceRadixSort::SortPairs(t, b, sub_key.as<uint32_t>(), skey_s.as<uint32_t>(),
-                                                sub_id.as<uint32_t>(), sperm.as<uint32_t>(), nsubs, 0, 6 + panel_bits,
-                                                st);
+         return cub::DeviceRadixSort::SortPairs(t, b, seg_row.as<uint32_t>(), srow_key.as<uint32_t>(),
+                                                iota.as<uint32_t>(), order.as<uint32_t>(), nseg, 0, row_bits, st);
        }, tmp, st)))
     return rc;
-  // slices: 32 sub-segments of a panel side by side
-  const int64_t gsub = std::min<int64_t>((nsubs + 256) / 256, int64_t(sms) * 32);
-  std::vector<uint32_t> sub_ptr(npanels + 1), slice_base(npanels + 1);
-  ScratchBuf d_sub_ptr, d_slice_base;
-  if ((rc = d_sub_ptr.alloc(4 * (npanels + 1), st)) || (rc = d_slice_base.alloc(4 * (npanels + 1), st))) return rc;
-  panel_bounds_kernel<<<unsigned(gsub), 256, 0, st>>>(skey_s.as<uint32_t>(), nsubs, npanels, d_sub_ptr.as<uint32_t>(), 6);
-  SPMV_LAUNCH_CHECK();
-  SPMV_CUDA_TRY(cudaMemcpyAsync(sub_ptr.data(), d_sub_ptr.ptr, 4 * (npanels + 1), cudaMemcpyDeviceToHost, st));
-  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
-  slice_base[0] = 0;
-  for (int64_t q = 0; q < npanels; ++q) slice_base[q + 1] = slice_base[q] + (sub_ptr[q + 1] - sub_ptr[q] + 31) / 32;
-  const int64_t nslices = slice_base[npanels];
-  p->pn_slices = nslices;
-  SPMV_CUDA_TRY(cudaMemcpyAsync(d_slice_base.ptr, slice_base.data(), 4 * (npanels + 1), cudaMemcpyHostToDevice, st));
-  ScratchBuf width, d_row_ptr;
-  if ((rc = width.alloc(4 * (nslices + 1), st)) || (rc = d_row_ptr.alloc(4 * (nslices + 1), st))) return rc;
-  const int64_t gsl = std::min<int64_t>((nslices + 256) / 256, int64_t(sms) * 16);
-  panel_slice_width_kernel<<<unsigned(gsl), 256, 0, st>>>(skey_s.as<uint32_t>(), d_sub_ptr.as<uint32_t>(),
-                                                          d_slice_base.as<uint32_t>(), uint32_t(npanels), nslices,
-                                                          width.as<uint32_t>());
-  SPMV_LAUNCH_CHECK();
-  if ((rc = cub_call([&](void* t, size_t& b) {
-         return cub::DeviceScan::ExclusiveSum(t, b, width.as<uint32_t>(), d_row_ptr.as<uint32_t>(), nslices + 1, st);
-       }, tmp, st)))
-    return rc;
-  std::vector<uint32_t> row_ptr(nslices + 1);
-  SPMV_CUDA_TRY(cudaMemcpyAsync(row_ptr.data(), d_row_ptr.ptr, 4 * (nslices + 1), cudaMemcpyDeviceToHost, st));
-  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
-  // CTA cuts: equal entry-rows, at slice boundaries, moved to a panel
-  // boundary when one is close (a CTA then loads one x panel, not two);
-  // warp tasks inside each (CTA, panel) item the same way.  A task's slices
-  // are laid end to end in the stream and padded to whole steps.
-  const uint64_t R = row_ptr[nslices];
-  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(sms, int64_t((R + 127) / 128)));
-  auto slice_at = [&](uint64_t target, uint32_t lo, uint32_t hi) {  // first slice in [lo, hi] starting at or after target
-    return uint32_t(std::lower_bound(row_ptr.begin() + lo, row_ptr.begin() + hi, uint32_t(std::min<uint64_t>(target, R))) -
-                    row_ptr.begin());
-  };
-  std::vector<uint32_t> cut(C + 1);
-  for (int64_t c = 0; c <= C; ++c) {
-    const uint64_t target = R * uint64_t(c) / uint64_t(C);
-    uint32_t sl = slice_at(target, 0, uint32_t(nslices));
-    const auto it = std::lower_bound(slice_base.begin(), slice_base.end(), sl);
-    const uint64_t slack = R / uint64_t(C) / 16;
-    for (int d = 0; d < 2; ++d) {
-      if (d == 0 && it == slice_base.end()) continue;
-      if (d == 1 && it == slice_base.begin()) continue;
-      const uint32_t b = d == 0 ? *it : *(it - 1);
-      const uint64_t rb = row_ptr[b];
-      if ((rb > target ? rb - target : target - rb) <= slack) {
-        sl = b;
-        break;
-      }
-    }
-    cut[c] = c == 0 ? 0u : std::max(sl, cut[c - 1]);
+  // row-major segment list (rseg): the sorted order itself
+  SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_rseg.ptr, order.ptr, 4 * nseg, cudaMemcpyDeviceToDevice, st));
+  // CTA cuts: equal entry counts, moved to segment starts
+  std::vector<uint32_t> pan_ptr(npanels + 1);
+  {
+    ScratchBuf dp;
+    if ((rc = dp.alloc(4 * (npanels + 1), st))) return rc;
+    panel_bounds_kernel<<<unsigned(ge), 256, 0, st>>>(skey.as<uint32_t>(), nl, npanels, dp.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+    SPMV_CUDA_TRY(cudaMemcpyAsync(pan_ptr.data(), dp.ptr, 4 * (npanels + 1), cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
   }
-  cut[C] = uint32_t(nslices);
-  std::vector<uint32_t> cta_item(sms + 1), item_panel, task, slice_row(nslices);
-  uint64_t steps = 0;
+  auto snap = [&](std::vector<uint32_t>& pos, const std::vector<uint32_t>& lim) -> int {
+    const int64_t m = int64_t(pos.size());
+    ScratchBuf dpos, dlim;
+    int r2;
+    if ((r2 = dpos.alloc(4 * m, st)) || (r2 = dlim.alloc(4 * m, st))) return r2;
+    SPMV_CUDA_TRY(cudaMemcpyAsync(dpos.ptr, pos.data(), 4 * m, cudaMemcpyHostToDevice, st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(dlim.ptr, lim.data(), 4 * m, cudaMemcpyHostToDevice, st));
+    panel_snap_kernel<<<unsigned(std::min<int64_t>((m + 255) / 256, 1024)), 256, 0, st>>>(
+        flag.as<uint32_t>(), dpos.as<uint32_t>(), m, dlim.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+    SPMV_CUDA_TRY(cudaMemcpyAsync(pos.data(), dpos.ptr, 4 * m, cudaMemcpyDeviceToHost, st));
+    SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+    return SPMV_OK;
+  };
+  const int64_t C = std::max<int64_t>(1, std::min<int64_t>(sms, (nl + 4095) / 4096));
+  std::vector<uint32_t> cut(C + 1), cut_lim(C + 1, uint32_t(nl));
+  for (int64_t c = 0; c <= C; ++c) cut[c] = uint32_t(nl * c / C);
+  if ((rc = snap(cut, cut_lim))) return rc;
+  cut[0] = 0;
+  cut[C] = uint32_t(nl);
+  std::vector<uint32_t> cta_item(C + 1), item_panel, item_end, tb, tlim;
   for (int64_t c = 0; c < C; ++c) {
     cta_item[c] = uint32_t(item_panel.size());
     for (int64_t q = 0; q < npanels; ++q) {
-      const uint32_t lo = std::max(cut[c], slice_base[q]), hi = std::min(cut[c + 1], slice_base[q + 1]);
+      const uint32_t lo = std::max(cut[c], pan_ptr[q]), hi = std::min(cut[c + 1], pan_ptr[q + 1]);
       if (lo >= hi) continue;
       item_panel.push_back(uint32_t(q));
-      const uint64_t r0 = row_ptr[lo], rows = row_ptr[hi] - r0;
-      uint32_t prev = lo;
+      item_end.push_back(hi);
       for (int w = 0; w < kPanelWarps; ++w) {
-        const uint32_t next = w + 1 == kPanelWarps ? hi : std::max(prev, slice_at(r0 + rows * uint64_t(w + 1) / kPanelWarps, lo, hi));
-        const uint64_t trows = row_ptr[next] - row_ptr[prev], tsteps = (trows + kPanelK - 1) / kPanelK;
-        task.push_back(uint32_t(steps));
-        task.push_back(uint32_t(tsteps));
-        task.push_back(prev);
-        for (uint32_t sl = prev; sl < next; ++sl) slice_row[sl] = uint32_t(steps * kPanelK + (row_ptr[sl] - row_ptr[prev]));
-        steps += tsteps;
-        prev = next;
+        tb.push_back(uint32_t(lo + (uint64_t(hi - lo) * w) / kPanelWarps));
+        tlim.push_back(hi);
       }
     }
   }
-  for (int64_t c = C; c <= sms; ++c) cta_item[c] = uint32_t(item_panel.size());  // CTAs past C: gather warps only
-  if (steps * kPanelStep >= (uint64_t(1) << 32)) return fail(SPMV_UNSUPPORTED, "panel stream too long");
+  cta_item[C] = uint32_t(item_panel.size());
+  if ((rc = snap(tb, tlim))) return rc;
   p->pn_ctas = C;
   p->pn_items = int64_t(item_panel.size());
-  p->pn_steps = int64_t(steps);
-  ScratchBuf d_slice_row;
-  if ((rc = d_slice_row.alloc(4 * std::max<int64_t>(1, nslices), st)) ||
-      (rc = p->pn_item_panel.alloc(4 * std::max<int64_t>(1, p->pn_items))) ||
-      (rc = p->pn_task.alloc(4 * std::max<size_t>(1, task.size()))) ||
-      (rc = p->pn_col.alloc(size_t(steps) * kPanelColBytes)) || (rc = p->pn_val.alloc(size_t(steps) * kPanelStep * sizeof(T))))
+  const int64_t nt = int64_t(tb.size());
+  if ((rc = p->pn_cta_item.alloc(4 * (C + 1))) || (rc = p->pn_item_panel.alloc(4 * std::max<int64_t>(1, p->pn_items))) ||
+      (rc = p->pn_item_end.alloc(4 * std::max<int64_t>(1, p->pn_items))) ||
+      (rc = p->pn_task_begin.alloc(4 * std::max<int64_t>(1, nt))) ||
+      (rc = p->pn_task_seg0.alloc(4 * std::max<int64_t>(1, nt))))
     return rc;
-  SPMV_CUDA_TRY(cudaMemcpyAsync(d_slice_row.ptr, slice_row.data(), 4 * nslices, cudaMemcpyHostToDevice, st));
-  SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_cta_item.ptr, cta_item.data(), 4 * (sms + 1), cudaMemcpyHostToDevice, st));
-  SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_item_panel.ptr, item_panel.data(), 4 * p->pn_items, cudaMemcpyHostToDevice, st));
-  SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_task.ptr, task.data(), 4 * task.size(), cudaMemcpyHostToDevice, st));
-  // the stream: padding everywhere, then every sub-segment down its lane
-  SPMV_CUDA_TRY(cudaMemsetAsync(p->pn_val.ptr, 0, size_t(steps) * kPanelStep * sizeof(T), st));
-  const int64_t gst = std::min<int64_t>((int64_t(steps) * (kPanelColBytes / 2) + 255) / 256, int64_t(sms) * 32);
-  panel_init_cols_kernel<<<unsigned(gst), 256, 0, st>>>(p->pn_col.as<uint16_t>(), int64_t(steps), uint32_t(W));
-  SPMV_LAUNCH_CHECK();
-  ScratchBuf sub_part, sub_row, sub_row_s;
-  if ((rc = sub_part.alloc(4 * nsubs, st)) || (rc = sub_row.alloc(4 * nsubs, st)) || (rc = sub_row_s.alloc(4 * nsubs, st)) ||
-      (rc = p->pn_rseg.alloc(4 * nsubs)) || (rc = p->pn_ptr.alloc(4 * (nlong + 1))))
-    return rc;
-  panel_fill_kernel<T><<<unsigned(gsub), 256, 0, st>>>(
-      skey_s.as<uint32_t>(), sperm.as<uint32_t>(), d_sub_ptr.as<uint32_t>(), d_slice_base.as<uint32_t>(),
-      d_slice_row.as<uint32_t>(), sub_seg.as<uint32_t>(), sub_base.as<uint32_t>(), seg_start.as<uint32_t>(),
-      seg_row.as<uint32_t>(), perm.as<uint32_t>(), eidx.as<uint32_t>(), aj, av, nsubs, uint32_t(W),
-      p->pn_col.as<uint8_t>(), p->pn_val.as<T>(), sub_part.as<uint32_t>(), sub_row.as<uint32_t>());
-  SPMV_LAUNCH_CHECK();
-  panel_endbits_kernel<<<unsigned(gsl), 256, 0, st>>>(d_slice_row.as<uint32_t>(), width.as<uint32_t>(), nslices,
-                                                      p->pn_col.as<uint8_t>());
-  SPMV_LAUNCH_CHECK();
-  // row-major list of partials: stable sort of the sub-segments by long row
-  // (they are in panel order, a segment's pieces in order)
-  int row_bits = 1;
-  while (row_bits < 32 && (int64_t(1) << row_bits) < nlong) ++row_bits;
-  if ((rc = cub_call([&](void* t, size_t& b) {
-         return cub::DeviceRadixSort::SortPairs(t, b, sub_row.as<uint32_t>(), sub_row_s.as<uint32_t>(),
-                                                sub_part.as<uint32_t>(), p->pn_rseg.as<uint32_t>(), nsubs, 0, row_bits,
-                                                st);
-       }, tmp, st)))
-    return rc;
-  panel_bounds_kernel<<<unsigned(gsub), 256, 0, st>>>(sub_row_s.as<uint32_t>(), nsubs, nlong, p->pn_ptr.as<uint32_t>());
-  SPMV_LAUNCH_CHECK();
+  SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_cta_item.ptr, cta_item.data(), 4 * (C + 1), cudaMemcpyHostToDevice, st));
+  if (p->pn_items) {
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_item_panel.ptr, item_panel.data(), 4 * p->pn_items, cudaMemcpyHostToDevice,
+                                  st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_item_end.ptr, item_end.data(), 4 * p->pn_items, cudaMemcpyHostToDevice, st));
+    SPMV_CUDA_TRY(cudaMemcpyAsync(p->pn_task_begin.ptr, tb.data(), 4 * nt, cudaMemcpyHostToDevice, st));
+    gather_u32_kernel<<<unsigned(std::min<int64_t>((nt + 255) / 256, 1024)), 256, 0, st>>>(
+        seg_of.as<uint32_t>(), p->pn_task_begin.as<uint32_t>(), nt, nl, p->pn_task_seg0.as<uint32_t>());
+    SPMV_LAUNCH_CHECK();
+  }
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));  // temporaries are released on return
   return SPMV_OK;
 }
@@ -1588,15 +1467,12 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, const uint32_t*
       SPMV_LAUNCH_CHECK();
     }
   }
-  // panel path: rows over pn_row_len entries holding at least half the
-  // entries of a matrix whose x does not fit L1 (spmv_plan_config.panels
-  // overrides); needs the column indices and values (copied panel-major)
+  // panel path: rows over 32 entries holding at least half the entries of
+  // a matrix whose x does not fit L1 (spmv_plan_config.panels overrides);
+  // needs the column indices and values (copied panel-major)
   if (p->n_long > 0 && aj && av && p->cfg.panels != 0) {
-    p->pn_row_len = p->cfg.panel_row_len > 0
-                        ? std::min<int64_t>(std::max<int64_t>(p->cfg.panel_row_len, kExactLen), kRowLenMax)
-                        : kRowLenDefault;
     SPMV_CUDA_TRY(cudaMemsetAsync(ctr, 0, 8, st));
-    long_entries_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, uint32_t(p->pn_row_len), ctr);
+    long_entries_kernel<<<unsigned(g_rows), 256, 0, st>>>(irp, nrows, uint32_t(kExactLen), ctr);
     SPMV_LAUNCH_CHECK();
     if ((rc = count_async(ctr, &h, st))) return rc;
     p->panel = p->cfg.panels > 0 || (2 * int64_t(h) >= p->nnz && p->ncols >= 65536);
@@ -1610,10 +1486,10 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, const uint32_t*
     p->pn_av = av;
     if (p->dtype == SPMV_F64)
       SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_panel_kernel<double>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kPanelSmemMax));
+                                         panel_smem_bytes<double>()));
     else
       SPMV_CUDA_TRY(cudaFuncSetAttribute(csr_panel_kernel<float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         kPanelSmemMax));
+                                         panel_smem_bytes<float>()));
   }
   SlotLayout lay;  // per-stream launch scratch
   p->off_head = lay.add(vs * p->ntiles);
@@ -1621,8 +1497,7 @@ static int csr_plan_build(spmv_csr_plan* p, const uint32_t* irp, const uint32_t*
   p->off_ws_head = lay.add(8 * p->ws_nranges);
   p->off_ws_tail = lay.add(8 * p->ws_nranges);
   p->off_ws_ctr = lay.add(8);
-  p->off_part = lay.add(8 * 32 * p->pn_slices);
-  p->off_pn_ctr = lay.add(8);
+  p->off_part = lay.add(8 * p->pn_seg);
   p->scratch.bytes = lay.total;
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
 #define X(TL, GR, LF)                                                                      \
@@ -1680,8 +1555,6 @@ int spmv_csr_plan_config(const spmv_csr_plan* p, spmv_plan_config* out) {
   out->ranges_per_warp = int32_t(p->ws_ranges_per_warp);
   out->tma_hint = p->tma_hint ? 1 : 0;
   out->panels = p->panel ? 1 : 0;
-  out->panel_cols = p->panel ? int32_t(p->pn_cols) : 0;
-  out->panel_row_len = p->panel ? int32_t(p->pn_row_len) : 0;
   return SPMV_OK;
 }
 
@@ -1741,7 +1614,7 @@ int spmv_csr_plan_info(const spmv_csr_plan* p, int64_t* n_long_rows, int64_t* n_
   if (n_long_rows) *n_long_rows = p->n_long_ws;
   if (n_items) *n_items = p->tile;
   if (launches && p->panel) {
-    *launches = 1 + (p->pn_long > 0 ? 1 : 0);
+    *launches = (p->pn_short > 0 ? 1 : 0) + (p->pn_long > 0 ? 2 : 0);
   } else if (launches && p->ws)
     *launches = 1 + (p->ws_n_span > 0 ? 1 : 0);
   else if (launches)
@@ -1759,7 +1632,7 @@ int spmv_csr_plan_groups(const spmv_csr_plan* p, int* groups) {
 int spmv_csr_plan_path(const spmv_csr_plan* p, int* warp_stream, int64_t* nwarps) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
   if (warp_stream) *warp_stream = p->panel ? 2 : p->ws ? 1 : 0;
-  if (nwarps) *nwarps = p->panel ? int64_t(sm_count()) * (kPanelWarps + kGatherWarps) : p->ws_nwarps;
+  if (nwarps) *nwarps = p->panel ? p->pn_ctas * kPanelWarps : p->ws_nwarps;
   return SPMV_OK;
 }
 

@@ -32,8 +32,7 @@ class _CPlanConfig(ctypes.Structure):
                 ("exact_len", ctypes.c_int32), ("warp_stream", ctypes.c_int32),
                 ("ranges_per_warp", ctypes.c_int32), ("tma_hint", ctypes.c_int32), ("ctas_per_sm", ctypes.c_int32),
                 ("dia_kernel", ctypes.c_int32), ("dia_rows", ctypes.c_int32), ("flags", ctypes.c_int32),
-                ("panels", ctypes.c_int32), ("panel_cols", ctypes.c_int32), ("panel_row_len", ctypes.c_int32),
-                ("reserved", ctypes.c_int32 * 2)]
+                ("panels", ctypes.c_int32), ("reserved", ctypes.c_int32 * 4)]
 
 
 @dataclass(frozen=True)
@@ -55,9 +54,6 @@ class PlanConfig:
     flags           experiments (bit0 products mode, bit1 warp per long segment)
     panels          CSR column-panel path for long rows (csrc/panel.cuh): -1 auto,
                     0 off, 1 on
-    panel_cols      columns per x panel of that path (0 = the plan's choice)
-    panel_row_len   that path's rows of at most this many entries are computed
-                    in row order by the gather warps, bit-exact (32..256, 0 = 128)
     """
 
     tile: int = 0
@@ -71,8 +67,6 @@ class PlanConfig:
     dia_rows: int = 0
     flags: int = 0
     panels: int = -1
-    panel_cols: int = 0
-    panel_row_len: int = 0
 
     def to_c(self) -> _CPlanConfig:
         c = _CPlanConfig()
