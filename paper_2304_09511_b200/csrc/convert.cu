@@ -187,10 +187,12 @@ __global__ void __launch_bounds__(256) dia_rows_kernel(const int32_t* __restrict
 }
 
 // ---- sort_coo ------------------------------------------------------------------
-// Stage 1: a stable LSD radix sort of the 32-bit row keys (bits(nrows)
-// bits) carrying each entry's storage index: each row's entries in storage
-// order.  Stage 2: per row, its columns and values gathered through those
-// indices and sorted by (column, storage index) — the reference's stable
+// Unsorted rows take the group path further down (values ride along the
+// radix sort, 256-row groups sorted in shared memory); matrices with groups
+// too large for it, and inputs whose rows are already in order, take the
+// per-row stage: Stage 1: a stable LSD radix sort of the row keys: each row's
+// entries in storage order.  Stage 2: per row, its columns and values
+// sorted by (column, storage index) — the reference's stable
 // lexsort((cols, rows)) (convert.py:70) — written straight to the output
 // positions (a warp per row of <= 32 entries: a bitonic sort in registers;
 // longer rows: a segmented sort).  Stage 3, only when some (row, column)
@@ -199,6 +201,34 @@ __global__ void __launch_bounds__(256) dia_rows_kernel(const int32_t* __restrict
 // flag = 1 if some row index is smaller than the one before it
 __global__ void rows_descend_kernel(const uint32_t* __restrict__ ai, int64_t nnz, int* __restrict__ flag) {
   GRID_STRIDE(k, nnz) if (k > 0 && ai[k] < ai[k - 1]) *flag = 1;
+}
+
+// A row of m <= 32 entries, one column per lane (lanes >= m: `in` false):
+// each lane's rank in ascending column order, by a bitonic sort of the bare
+// 32-bit columns and a 5-step binary search of the lane's own column in the
+// sorted registers — a third of the instructions of sorting 64-bit (column,
+// index) keys, which bound these kernels (ncu: ALU pipe).  Equal columns
+// (duplicates, rare) are reported instead: the caller then sorts the full
+// keys, whose index part is the stable tie-break.
+__device__ __forceinline__ int warp_col_rank(uint32_t c, bool in, uint32_t m, int lane, bool& has_dup) {
+  uint32_t k = in ? c : 0xffffffffu;
+#pragma unroll
+  for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+    for (int j = kk >> 1; j >= 1; j >>= 1) {
+      const uint32_t o = __shfl_xor_sync(0xffffffffu, k, j);
+      const bool take_min = ((lane & j) == 0) == ((lane & kk) == 0);
+      k = take_min ? min(k, o) : max(k, o);
+    }
+  const uint32_t prev = __shfl_up_sync(0xffffffffu, k, 1);
+  has_dup = __any_sync(0xffffffffu, lane > 0 && uint32_t(lane) < m && prev == k);
+  int lo = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1) {
+    const uint32_t probe = __shfl_sync(0xffffffffu, k, lo + step - 1);
+    if (probe < c) lo += step;
+  }
+  return lo;  // sorted columns below c
 }
 
 // Rows of <= 32 entries: lane k holds entry k of the row, its payload
@@ -221,6 +251,17 @@ __global__ void sort_rows_kernel(const uint32_t* __restrict__ rows_s, const unsi
     const bool in = uint32_t(lane) < n;
     unsigned long long key = ~0ull;
     if (in) key = pay ? pay[a + lane] : (static_cast<unsigned long long>(aj[a + lane]) << 32) | (a + lane);
+    bool has_dup;
+    const int rank = warp_col_rank(uint32_t(key >> 32), in, n, lane, has_dup);
+    if (!has_dup) {  // distinct columns: every lane stores its own entry at its rank
+      if (in) {
+        ai_out[a + lane] = rows_s[a];
+        aj_out[a + rank] = uint32_t(key >> 32);
+        av_out[a + rank] = av[uint32_t(key)];
+      }
+      if (lane == 0) ucnt[i] = n;
+      continue;
+    }
 #pragma unroll
     for (int k = 2; k <= 32; k <<= 1)
 #pragma unroll
@@ -243,12 +284,6 @@ __global__ void sort_rows_kernel(const uint32_t* __restrict__ rows_s, const unsi
     }
   }
   if (lane == 0 && dups) atomicAdd(ndup, dups);
-}
-
-// Stage-1 payload: (col << 32 | storage index).
-__global__ void sort_payload_kernel(const uint32_t* __restrict__ aj, int64_t nnz,
-                                    unsigned long long* __restrict__ pay) {
-  GRID_STRIDE(k, nnz) pay[k] = (static_cast<unsigned long long>(aj[k]) << 32) | static_cast<unsigned long long>(k);
 }
 
 // Rows over 32 entries: (begin, end) of each (count only when lb is null).
@@ -294,6 +329,234 @@ __global__ void long_emit_kernel(const uint32_t* __restrict__ rows_s, const unsi
     }
     ucnt[i] = u;
     if (b - a > u) atomicAdd(ndup, static_cast<unsigned long long>(b - a - u));
+  }
+}
+
+// ---- sort_coo, unsorted rows: values ride along, 256-row groups ---------------
+// The stage-1 sort above fetched every value through a random storage
+// index afterwards (a 32-byte DRAM sector per 8-byte value: ~10 ms at
+// 256^3).  Here the (column, value) pair is the radix sort's payload and the
+// sort stops 8 bits short: a stable LSD sort on row bits [8, bits(nrows))
+// leaves every group of 256 consecutive rows contiguous, its entries in
+// storage order.  One CTA then sorts a group in shared memory: a counting
+// sort on the low 8 row bits, a warp bitonic sort of each row's (column,
+// local index) keys — the local index is the storage order, i.e. the
+// stable tie-break of lexsort((cols, rows)) (convert.py:70) — and coalesced
+// stores of the finished rows.  One radix pass fewer, no random fetch.
+// Sort key of the radix passes: row << 32 | column (only row bits are sorted on).
+__global__ void sort_pack_kernel(const uint32_t* __restrict__ ai, const uint32_t* __restrict__ aj, int64_t nnz,
+                                 unsigned long long* __restrict__ key) {
+  GRID_STRIDE(k, nnz) key[k] = (static_cast<unsigned long long>(ai[k]) << 32) | aj[k];
+}
+
+// start[q] = first sorted entry whose key >> shift is >= q, q = 0..ngroups.
+__global__ void group_bounds_kernel(const unsigned long long* __restrict__ key_s, int64_t nnz, int shift,
+                                    int64_t ngroups, uint32_t* __restrict__ start) {
+  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= nnz; i += int64_t(gridDim.x) * blockDim.x) {
+    const int64_t q1 = i < nnz ? int64_t(key_s[i] >> shift) : ngroups;
+    const int64_t q0 = i == 0 ? -1 : int64_t(key_s[i - 1] >> shift);
+    for (int64_t q = q0 + 1; q <= q1; ++q) start[q] = uint32_t(i);
+  }
+}
+
+__global__ void max_diff_kernel(const uint32_t* __restrict__ start, int64_t n, uint32_t* __restrict__ out) {
+  uint32_t m = 0;
+  GRID_STRIDE(i, n) m = max(m, start[i + 1] - start[i]);
+  for (int o = 16; o >= 1; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0 && m) atomicMax(out, m);
+}
+
+constexpr int kGroupBits = 8;       // low row bits sorted inside a group, at most
+constexpr int kGroupRows = 1 << kGroupBits;
+constexpr int kGroupMax = 7168;     // entries per group the shared-memory sort takes (two CTAs per SM for f64)
+constexpr int kGroupThreads = 512;
+static_assert(kGroupMax <= 8192, "local index in 13 bits");
+template <typename T> constexpr size_t group_smem_bytes() {
+  return size_t(kGroupMax) * (sizeof(T) + 4 + 2 + 1) + (kGroupRows + 4) * 4 * 2;
+}
+
+// (column, local index) order of two entries of a group.
+__device__ __forceinline__ bool group_less(const uint32_t* scol, uint32_t i, uint32_t l) {
+  const uint32_t ci = scol[i], cl = scol[l];
+  return ci < cl || (ci == cl && i < l);
+}
+
+template <typename T>
+__global__ void __launch_bounds__(kGroupThreads, 2)
+    group_sort_kernel(const unsigned long long* __restrict__ key_s, const T* __restrict__ val_s,
+                      const uint32_t* __restrict__ gstart, int64_t ngroups, int lo, uint32_t* __restrict__ ai_out,
+                      uint32_t* __restrict__ aj_out, T* __restrict__ av_out, uint32_t* __restrict__ seg,
+                      uint32_t* __restrict__ ucnt, unsigned long long* __restrict__ ndup) {
+  extern __shared__ __align__(16) unsigned char group_smem[];
+  T* sval = reinterpret_cast<T*>(group_smem);
+  uint32_t* scol = reinterpret_cast<uint32_t*>(sval + kGroupMax);
+  uint32_t* cnt = scol + kGroupMax;            // kGroupRows + 1 (+ pad): counts, then row starts
+  uint32_t* cur = cnt + kGroupRows + 4;        // scatter cursors
+  uint16_t* sord = reinterpret_cast<uint16_t*>(cur + kGroupRows + 4);  // local indices grouped by row
+  uint8_t* srow = reinterpret_cast<uint8_t*>(sord + kGroupMax);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int grows = 1 << lo;  // rows per group
+  const uint32_t rmask = uint32_t(grows - 1);
+  unsigned long long dups = 0;
+  for (int64_t g = blockIdx.x; g < ngroups; g += gridDim.x) {
+    const uint32_t a = gstart[g], n = gstart[g + 1] - a;
+    if (tid < kGroupRows) cnt[tid] = 0;
+    __syncthreads();
+    // the group's entries into shared memory, 7 loads in flight per thread
+    for (uint32_t i0 = 0; i0 < n; i0 += 7 * kGroupThreads) {
+      unsigned long long k[7];
+      T v[7];
+#pragma unroll
+      for (int u = 0; u < 7; ++u) {
+        const uint32_t i = i0 + u * kGroupThreads + tid;
+        if (i < n) {
+          k[u] = __ldcs(key_s + a + i);
+          v[u] = __ldcs(val_s + a + i);
+        }
+      }
+#pragma unroll
+      for (int u = 0; u < 7; ++u) {
+        const uint32_t i = i0 + u * kGroupThreads + tid;
+        if (i < n) {
+          const uint32_t r = uint32_t(k[u] >> 32) & rmask;
+          srow[i] = uint8_t(r);
+          scol[i] = uint32_t(k[u]);
+          sval[i] = v[u];
+          atomicAdd(&cnt[r], 1u);
+        }
+      }
+    }
+    __syncthreads();
+    if (warp == 0) {  // exclusive scan of the 256 row counts: 8 per lane
+      uint32_t c[8], sum = 0;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        c[k] = cnt[lane * 8 + k];
+        sum += c[k];
+      }
+      uint32_t inc = sum;
+#pragma unroll
+      for (int o = 1; o < 32; o <<= 1) {
+        const uint32_t up = __shfl_up_sync(0xffffffffu, inc, o);
+        if (lane >= o) inc += up;
+      }
+      uint32_t run = inc - sum;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        cnt[lane * 8 + k] = run;
+        cur[lane * 8 + k] = run;
+        run += c[k];
+      }
+      if (lane == 31) cnt[kGroupRows] = run;
+    }
+    __syncthreads();
+    for (uint32_t i = tid; i < n; i += kGroupThreads) sord[atomicAdd(&cur[srow[i]], 1u)] = uint16_t(i);
+    __syncthreads();
+    for (int r = warp; r < grows; r += kGroupThreads / 32) {
+      const uint32_t s0 = cnt[r], m = cnt[r + 1] - s0;
+      const int64_t sidx = g * grows + r;
+      const uint32_t row = uint32_t(sidx);
+      if (lane == 0) seg[sidx] = a + s0;
+      if (m == 0) continue;
+      uint32_t heads_n = 0;
+      if (m <= 32) {
+        const bool in = uint32_t(lane) < m;
+        unsigned long long key = ~0ull;
+        uint32_t i = 0, c = 0;
+        if (in) {
+          i = sord[s0 + lane];
+          c = scol[i];
+          key = (static_cast<unsigned long long>(c) << 13) | i;
+        }
+        bool has_dup;
+        const int rank = warp_col_rank(c, in, m, lane, has_dup);
+        if (!has_dup) {  // distinct columns: every lane stores its own entry at its rank
+          if (in) {
+            ai_out[a + s0 + lane] = row;
+            aj_out[a + s0 + rank] = c;
+            av_out[a + s0 + rank] = sval[i];
+          }
+          if (lane == 0) ucnt[sidx] = m;
+          continue;
+        }
+#pragma unroll
+        for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+          for (int j = k >> 1; j >= 1; j >>= 1) {
+            const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, j);
+            const bool take_min = ((lane & j) == 0) == ((lane & k) == 0);
+            key = (take_min ? ok < key : ok > key) ? ok : key;
+          }
+        const unsigned long long prev = __shfl_up_sync(0xffffffffu, key, 1);
+        const bool head = in && (lane == 0 || (prev >> 13) != (key >> 13));
+        heads_n = __popc(__ballot_sync(0xffffffffu, head));
+        if (in) {
+          ai_out[a + s0 + lane] = row;
+          aj_out[a + s0 + lane] = uint32_t(key >> 13);
+          av_out[a + s0 + lane] = sval[uint32_t(key) & 8191u];
+        }
+      } else {
+        // a longer row: its local indices sorted in place by (column, index),
+        // a bitonic network with every merge ascending (entries past m act as
+        // +infinity and never move)
+        uint32_t N = 64;
+        while (N < m) N <<= 1;
+        for (uint32_t k = 2; k <= N; k <<= 1) {
+          for (uint32_t j = k >> 1; j >= 1; j >>= 1) {
+            for (uint32_t t = lane; t < N / 2; t += 32) {
+              uint32_t i, l;
+              if (j == (k >> 1)) {  // mirror step
+                const uint32_t blk = t / j, off = t % j;
+                i = blk * k + off;
+                l = blk * k + k - 1 - off;
+              } else {
+                const uint32_t blk = t / j, off = t % j;
+                i = blk * 2 * j + off;
+                l = i + j;
+              }
+              if (l < m) {
+                const uint32_t x = sord[s0 + i], y = sord[s0 + l];
+                if (group_less(scol, y, x)) {
+                  sord[s0 + i] = uint16_t(y);
+                  sord[s0 + l] = uint16_t(x);
+                }
+              }
+            }
+            __syncwarp();
+          }
+        }
+        for (uint32_t t0 = 0; t0 < m; t0 += 32) {
+          const uint32_t t = t0 + lane;
+          const bool in = t < m;
+          uint32_t i = 0;
+          bool head = false;
+          if (in) {
+            i = sord[s0 + t];
+            head = t == 0 || scol[sord[s0 + t - 1]] != scol[i];
+            ai_out[a + s0 + t] = row;
+            aj_out[a + s0 + t] = scol[i];
+            av_out[a + s0 + t] = sval[i];
+          }
+          heads_n += __popc(__ballot_sync(0xffffffffu, head));
+        }
+      }
+      if (lane == 0) {
+        ucnt[sidx] = heads_n;
+        dups += m - heads_n;
+      }
+    }
+    __syncthreads();
+  }
+  if (lane == 0 && dups) atomicAdd(ndup, dups);
+}
+
+// Fallback after a full row sort: stage-2 inputs from the sorted keys.
+__global__ void sort_unpack_kernel(const unsigned long long* __restrict__ key_s, int64_t nnz,
+                                   uint32_t* __restrict__ rows, unsigned long long* __restrict__ pay) {
+  GRID_STRIDE(k, nnz) {
+    const unsigned long long key = key_s[k];
+    rows[k] = uint32_t(key >> 32);
+    pay[k] = (key << 32) | static_cast<unsigned long long>(k);
   }
 }
 
@@ -605,13 +868,35 @@ static int bits_for(int64_t n) {  // bits holding 0 .. n-1 (at least 1)
 
 }  // extern "C"
 
+// Stage 3: duplicate runs merged and compacted (through a copy: rows move to
+// lower positions).  seg: nseg + 1 row starts; ucnt: unique columns per row.
+template <typename T>
+static int merge_duplicates(const uint32_t* seg, const uint32_t* ucnt, int64_t nseg, int64_t nnz, uint32_t* ai_out,
+                            uint32_t* aj_out, T* av_out, cudaStream_t st) {
+  int r;
+  ScratchBuf opos, ai_s, aj_s, av_s;
+  if ((r = opos.alloc(4 * (nseg + 1), st)) || (r = ai_s.alloc(4 * nnz, st)) || (r = aj_s.alloc(4 * nnz, st)) ||
+      (r = av_s.alloc(sizeof(T) * nnz, st)))
+    return r;
+  if ((r = excl_scan<uint32_t>(ucnt, opos.as<uint32_t>(), nseg + 1, st))) return r;
+  SPMV_CUDA_TRY(cudaMemcpyAsync(ai_s.ptr, ai_out, 4 * nnz, cudaMemcpyDeviceToDevice, st));
+  SPMV_CUDA_TRY(cudaMemcpyAsync(aj_s.ptr, aj_out, 4 * nnz, cudaMemcpyDeviceToDevice, st));
+  SPMV_CUDA_TRY(cudaMemcpyAsync(av_s.ptr, av_out, sizeof(T) * nnz, cudaMemcpyDeviceToDevice, st));
+  merge_runs_kernel<T><<<unsigned(grid_for(nseg)), 256, 0, st>>>(seg, opos.as<uint32_t>(), nseg, ai_s.as<uint32_t>(),
+                                                                 aj_s.as<uint32_t>(), av_s.as<T>(), ai_out, aj_out,
+                                                                 av_out);
+  SPMV_LAUNCH_CHECK();
+  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+  return SPMV_OK;
+}
+
 template <typename T>
 static int sort_coo_run(int64_t nrows, int64_t nnz, const uint32_t* ai, const uint32_t* aj, const T* av,
                         uint32_t* ai_out, uint32_t* aj_out, T* av_out, int64_t* n_out, cudaStream_t st) {
   *n_out = 0;
   if (nnz == 0) return SPMV_OK;
   int r;
-  ScratchBuf pay_in, rows_buf, pay_buf, tmp, flag;
+  ScratchBuf rows_buf, pay_buf, tmp, flag;
   auto tmp_for = [&](size_t bytes) -> int { return bytes > tmp.bytes ? tmp.alloc(bytes, st) : SPMV_OK; };
   // rows already non-decreasing (a COO without its sorted flag): no stage 1
   if ((r = flag.alloc(sizeof(int), st))) return r;
@@ -624,23 +909,99 @@ static int sort_coo_run(int64_t nrows, int64_t nnz, const uint32_t* ai, const ui
   const bool rows_sorted = hflag == 0;
   const uint32_t* rows_p = ai;
   const unsigned long long* pay_p = nullptr;
+  const T* av_p = av;
+  ScratchBuf av_buf;
   if (!rows_sorted) {
-    // stage 1: stable sort on the row, (col, storage index) as the payload
-    if ((r = pay_in.alloc(8 * nnz, st)) || (r = pay_buf.alloc(8 * nnz, st)) || (r = rows_buf.alloc(4 * nnz, st)))
+    // stage 1: stable radix sort on the row bits above the low `lo`, the
+    // column (in the key's low half) and the value riding along; then groups
+    // of 2^lo rows in shared memory.  lo: the most bits (<= 8) whose groups
+    // should fit going by the mean row length (checked exactly after the sort).
+    const int bits = bits_for(nrows);
+    int lo = std::min(bits, kGroupBits);
+    while (lo > 0 && double(nnz) / double(nrows) * double(1 << lo) * 1.03 > double(kGroupMax)) --lo;
+    ScratchBuf key_in, key_s, val_s;
+    if ((r = key_in.alloc(8 * nnz, st)) || (r = key_s.alloc(8 * nnz, st)) || (r = val_s.alloc(sizeof(T) * nnz, st)))
       return r;
-    sort_payload_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(aj, nnz, pay_in.as<unsigned long long>());
+    sort_pack_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, aj, nnz, key_in.as<unsigned long long>());
     SPMV_LAUNCH_CHECK();
-    size_t tb = 0;
-    SPMV_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, ai, rows_buf.as<uint32_t>(),
-                                                  pay_in.as<unsigned long long>(), pay_buf.as<unsigned long long>(),
-                                                  nnz, 0, bits_for(nrows), st));
-    if ((r = tmp_for(tb))) return r;
-    SPMV_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, ai, rows_buf.as<uint32_t>(),
-                                                  pay_in.as<unsigned long long>(), pay_buf.as<unsigned long long>(),
-                                                  nnz, 0, bits_for(nrows), st));
-    pay_in.release();
+    auto radix = [&](int b0, int b1) -> int {  // (key_in, av) -> (key_s, val_s), stable, on key bits [b0, b1)
+      size_t tb = 0;
+      SPMV_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, key_in.as<unsigned long long>(),
+                                                    key_s.as<unsigned long long>(), av, val_s.as<T>(), nnz, b0, b1, st));
+      int rr = tmp_for(tb);
+      if (rr) return rr;
+      SPMV_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, key_in.as<unsigned long long>(),
+                                                    key_s.as<unsigned long long>(), av, val_s.as<T>(), nnz, b0, b1, st));
+      return SPMV_OK;
+    };
+    bool grouped = false;
+    if (lo > 0) {
+      const unsigned long long* ks = key_in.as<unsigned long long>();
+      const T* vs = av;
+      if (bits > lo) {
+        if ((r = radix(32 + lo, 32 + bits))) return r;
+        ks = key_s.as<unsigned long long>();
+        vs = val_s.as<T>();
+      }
+      const int64_t ngroups = ((nrows - 1) >> lo) + 1;
+      ScratchBuf gstart, gmax;
+      if ((r = gstart.alloc(4 * (ngroups + 1), st)) || (r = gmax.alloc(4, st))) return r;
+      SPMV_CUDA_TRY(cudaMemsetAsync(gmax.ptr, 0, 4, st));
+      group_bounds_kernel<<<unsigned(grid_for(nnz + 1)), 256, 0, st>>>(ks, nnz, 32 + lo, ngroups, gstart.as<uint32_t>());
+      SPMV_LAUNCH_CHECK();
+      max_diff_kernel<<<unsigned(grid_for(ngroups)), 256, 0, st>>>(gstart.as<uint32_t>(), ngroups, gmax.as<uint32_t>());
+      SPMV_LAUNCH_CHECK();
+      uint32_t hmax = 0;
+      SPMV_CUDA_TRY(cudaMemcpyAsync(&hmax, gmax.ptr, 4, cudaMemcpyDeviceToHost, st));
+      SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+      if (hmax <= uint32_t(kGroupMax)) {
+        grouped = true;
+        const int64_t nseg = ngroups << lo;
+        ScratchBuf seg, ucnt, ndup;
+        if ((r = seg.alloc(4 * (nseg + 1), st)) || (r = ucnt.alloc(4 * (nseg + 1), st)) || (r = ndup.alloc(8, st)))
+          return r;
+        SPMV_CUDA_TRY(cudaMemsetAsync(ucnt.ptr, 0, 4 * (nseg + 1), st));
+        SPMV_CUDA_TRY(cudaMemsetAsync(ndup.ptr, 0, 8, st));
+        const uint32_t nnz32 = uint32_t(nnz);
+        SPMV_CUDA_TRY(cudaMemcpyAsync(seg.as<uint32_t>() + nseg, &nnz32, 4, cudaMemcpyHostToDevice, st));
+        static bool attr = [] {
+          cudaFuncSetAttribute(group_sort_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                               int(group_smem_bytes<T>()));
+          return true;
+        }();
+        (void)attr;
+        const unsigned gg = unsigned(std::min<int64_t>(ngroups, int64_t(sm_count()) * 2));
+        group_sort_kernel<T><<<gg, kGroupThreads, group_smem_bytes<T>(), st>>>(
+            ks, vs, gstart.as<uint32_t>(), ngroups, lo, ai_out, aj_out, av_out, seg.as<uint32_t>(),
+            ucnt.as<uint32_t>(), ndup.as<unsigned long long>());
+        SPMV_LAUNCH_CHECK();
+        unsigned long long hd = 0;
+        SPMV_CUDA_TRY(cudaMemcpyAsync(&hd, ndup.ptr, 8, cudaMemcpyDeviceToHost, st));
+        SPMV_CUDA_TRY(cudaStreamSynchronize(st));
+        *n_out = nnz - int64_t(hd);
+        if (hd == 0) return SPMV_OK;
+        return merge_duplicates<T>(seg.as<uint32_t>(), ucnt.as<uint32_t>(), nseg, nnz, ai_out, aj_out, av_out, st);
+      }
+    }
+    // groups too large for shared memory (long rows): the full stable row
+    // sort, then the per-row stage below on the sorted (column, value) pairs
+    (void)grouped;
+    if ((r = radix(32, 32 + bits))) return r;
+    if ((r = rows_buf.alloc(4 * nnz, st)) || (r = pay_buf.alloc(8 * nnz, st))) return r;
+    sort_unpack_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(key_s.as<unsigned long long>(), nnz,
+                                                                rows_buf.as<uint32_t>(),
+                                                                pay_buf.as<unsigned long long>());
+    SPMV_LAUNCH_CHECK();
+    key_in.release();
+    key_s.release();
+    av_buf.ptr = val_s.ptr;  // keeps the sorted values alive past this block
+    av_buf.bytes = val_s.bytes;
+    av_buf.st = st;
+    val_s.ptr = nullptr;
+    val_s.bytes = 0;
     rows_p = rows_buf.as<uint32_t>();
     pay_p = pay_buf.as<unsigned long long>();
+    av_p = av_buf.as<T>();
   }
   size_t tb = 0;
   // row segments: run lengths of the sorted rows, scanned
@@ -664,7 +1025,7 @@ static int sort_coo_run(int64_t nrows, int64_t nnz, const uint32_t* ai, const ui
   SPMV_CUDA_TRY(cudaMemsetAsync(ucnt.ptr, 0, 4 * (nseg + 1), st));
   SPMV_CUDA_TRY(cudaMemsetAsync(ndup.ptr, 0, 8, st));
   const int64_t gw = std::min<int64_t>((nseg * 32 + 255) / 256, int64_t(sm_count()) * 64);
-  sort_rows_kernel<T><<<unsigned(gw), 256, 0, st>>>(rows_p, pay_p, seg.as<uint32_t>(), nseg, aj, av, ai_out, aj_out,
+  sort_rows_kernel<T><<<unsigned(gw), 256, 0, st>>>(rows_p, pay_p, seg.as<uint32_t>(), nseg, aj, av_p, ai_out, aj_out,
                                                     av_out, ucnt.as<uint32_t>(), ndup.as<unsigned long long>());
   SPMV_LAUNCH_CHECK();
   ScratchBuf nlong;
@@ -699,7 +1060,7 @@ static int sort_coo_run(int64_t nrows, int64_t nnz, const uint32_t* ai, const ui
                                                      sorted.as<unsigned long long>(), nnz, nl, lb.as<uint32_t>(),
                                                      le.as<uint32_t>(), st));
     long_emit_kernel<T><<<unsigned(grid_for(nseg)), 256, 0, st>>>(rows_p, sorted.as<unsigned long long>(),
-                                                                  seg.as<uint32_t>(), nseg, av, ai_out, aj_out, av_out,
+                                                                  seg.as<uint32_t>(), nseg, av_p, ai_out, aj_out, av_out,
                                                                   ucnt.as<uint32_t>(), ndup.as<unsigned long long>());
     SPMV_LAUNCH_CHECK();
     SPMV_CUDA_TRY(cudaStreamSynchronize(st));  // temporaries leave scope
@@ -709,22 +1070,7 @@ static int sort_coo_run(int64_t nrows, int64_t nnz, const uint32_t* ai, const ui
   SPMV_CUDA_TRY(cudaStreamSynchronize(st));
   *n_out = nnz - int64_t(hd);
   if (hd == 0) return SPMV_OK;
-  // stage 3: duplicate runs merged and compacted (through a copy: rows move
-  // to lower positions)
-  ScratchBuf opos, ai_s, aj_s, av_s;
-  if ((r = opos.alloc(4 * (nseg + 1), st)) || (r = ai_s.alloc(4 * nnz, st)) || (r = aj_s.alloc(4 * nnz, st)) ||
-      (r = av_s.alloc(sizeof(T) * nnz, st)))
-    return r;
-  if ((r = excl_scan<uint32_t>(ucnt.as<uint32_t>(), opos.as<uint32_t>(), nseg + 1, st))) return r;
-  SPMV_CUDA_TRY(cudaMemcpyAsync(ai_s.ptr, ai_out, 4 * nnz, cudaMemcpyDeviceToDevice, st));
-  SPMV_CUDA_TRY(cudaMemcpyAsync(aj_s.ptr, aj_out, 4 * nnz, cudaMemcpyDeviceToDevice, st));
-  SPMV_CUDA_TRY(cudaMemcpyAsync(av_s.ptr, av_out, sizeof(T) * nnz, cudaMemcpyDeviceToDevice, st));
-  merge_runs_kernel<T><<<unsigned(grid_for(nseg)), 256, 0, st>>>(seg.as<uint32_t>(), opos.as<uint32_t>(), nseg,
-                                                                 ai_s.as<uint32_t>(), aj_s.as<uint32_t>(), av_s.as<T>(),
-                                                                 ai_out, aj_out, av_out);
-  SPMV_LAUNCH_CHECK();
-  SPMV_CUDA_TRY(cudaStreamSynchronize(st));
-  return SPMV_OK;
+  return merge_duplicates<T>(seg.as<uint32_t>(), ucnt.as<uint32_t>(), nseg, nnz, ai_out, aj_out, av_out, st);
 }
 
 extern "C" int spmv_sort_coo(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uint32_t* ai, const uint32_t* aj,
