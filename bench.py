@@ -265,6 +265,8 @@ def plan_of(sp, m) -> dict:
         i = K.coo_plan(m).info()
         if i["kernel"] in ("warp_stream", "panel"):
             return {"kernel": i["kernel"], "warps": i["warps"]}
+        if i["kernel"] == "csr_view":  # row pointers over the sorted rows: the CSR tile kernel, +0.0 seed
+            return {"kernel": "csr_view"}
         return {"tile": i["tile"], "groups": i["groups"]}
     return {}
 
@@ -415,6 +417,29 @@ def run_ours(args, torch, dist, rank, world, local_rank):
         results[fmt] = {"gflops": round(2.0 * m.nnz / t / 1e9, 2), "ms_per_spmv": round(t * 1e3, 4),
                         "gbs": round(b / t / 1e9, 1), "bytes_per_spmv": b, "launches": launches_per_spmv(sp, m),
                         "plan": plan_of(sp, m), "roofline_frac": round(b / t / 1e9 / pk["hbm_gbs"], 4), "nnz": m.nnz}
+        if results[fmt]["plan"].get("kernel") == "csr_view":
+            # COO plan without long runs: products run the CSR tile kernel on
+            # the plan's row-pointer view and never read the row indices, so
+            # the bytes moved are CSR's; roofline_frac above is against the COO
+            # minimum-byte model of SURVEY.md 8(d) and can exceed 1
+            bs = algo_bytes("csr", m.nrows, m.ncols, m.nnz, m.values.element_size(), 0)
+            results[fmt].update(bytes_streamed=bs, streamed_gbs=round(bs / t / 1e9, 1),
+                                streamed_frac=round(bs / t / 1e9 / pk["hbm_gbs"], 4))
+            if not args.no_extras:
+                # the COO tile kernel itself (segmented scan over the (row, col, value) stream)
+                from paper_2304_09511_b200.planconfig import PlanConfig
+                tile_cfg = PlanConfig(panels=0)
+                fn_t = lambda: fn_(m, xx, out=y, plan_config=tile_cfg)  # noqa: E731
+                fn_t()
+                torch.cuda.synchronize()
+                tt = time_steps(torch, fn_t, max(10, args.steps // 4), args.warmup, flush)
+                from paper_2304_09511_b200 import kernels as K
+                ti = K.coo_plan(m, config=tile_cfg).info()
+                results[fmt + "_tile_kernel"] = {
+                    "gflops": round(2.0 * m.nnz / tt / 1e9, 2), "ms_per_spmv": round(tt * 1e3, 4),
+                    "gbs": round(b / tt / 1e9, 1), "bytes_per_spmv": b, "launches": ti["launches"],
+                    "plan": {"tile": ti["tile"], "groups": ti["groups"], "config": "PlanConfig(panels=0)"},
+                    "roofline_frac": round(b / tt / 1e9 / pk["hbm_gbs"], 4), "nnz": m.nnz}
         if args.config == "c3":
             # uniform random columns: every entry is one random 32-byte x
             # sector; the bound is the measured random-gather rate, not HBM

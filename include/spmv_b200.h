@@ -275,9 +275,15 @@ int spmv_coo_plan_info(const spmv_coo_plan* plan, int64_t* n_runs,
                        int64_t* n_long_runs, int64_t* n_items,
                        int* row_sorted, int64_t* launches);
 /* Consumer groups per tile CTA the plan chose (spmv_plan_config.groups). */
-/* Whole-matrix kernel the COO plan chose: warp_stream = 1 for the
- * warp-stream kernel (plans with runs longer than 32 entries), else the
- * tile kernel.  spmv_plan_config.warp_stream = 0/1 overrides the choice. */
+/* Whole-matrix kernel the COO plan chose: warp_stream = 0 the COO tile
+ * kernel, 1 the warp-stream kernel (runs longer than 32 entries), 2 / 3 a
+ * CSR view of the plan's row-sorted triples (row pointers built at plan
+ * creation; products read 4 bytes per row instead of 4 bytes per entry of
+ * row indices and sum every row from +0.0 in storage order, np.add.at
+ * order): 2 on the column-panel path, 3 on the CSR tile kernel (plans
+ * without long runs, unless tile / groups / warp_stream are configured or
+ * spmv_plan_config.panels is 0).  The view serves products called with the
+ * arrays the plan was created from. */
 int spmv_coo_plan_path(const spmv_coo_plan* plan, int* warp_stream, int64_t* nwarps);
 int spmv_coo_plan_groups(const spmv_coo_plan* plan, int* groups);
 

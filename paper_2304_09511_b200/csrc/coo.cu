@@ -683,6 +683,7 @@ struct spmv_coo_plan {
   // column-panel path (csr.cu / panel.cuh) through a CSR view of the
   // row-sorted triples: whole-matrix products with the create-time arrays
   spmv_csr_plan* csr_view = nullptr;
+  bool view_panel = false;  // the view runs the column-panel path (else the CSR tile kernel)
   DevBuf view_irp;
   const void* view_ai = nullptr;
   const void* view_aj = nullptr;
@@ -980,10 +981,18 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
     if (!coo_config_known(p->tile, 1)) p->tile = 2048;
   }
   p->ntiles = (nnz + p->tile - 1) / p->tile;
-  if (p->n_long > 0 && p->cfg.panels != 0) {
-    // a CSR view (row pointers over the sorted rows; same column and value
-    // arrays): if its plan takes the column-panel path, whole-matrix COO
-    // products run it (short rows from +0.0: np.add.at order)
+  // A CSR view of the plan's row-sorted triples (row pointers over the
+  // sorted rows; the same column and value arrays): whole-matrix products
+  // then stream 4 bytes per row instead of 4 bytes per entry of row indices
+  // (16 -> 12 bytes per f64 entry: 256^3 COO 735 -> the CSR kernel's rate),
+  // rows summed from +0.0 in storage order: np.add.at order (kernels.py:65),
+  // bit-exact.  With long runs the view is kept if its plan takes the
+  // column-panel path; without, unless the caller configured the COO tile
+  // kernels (tile / groups / warp_stream) or turned views off (panels = 0).
+  const bool view_long = p->n_long > 0 && p->cfg.panels != 0;
+  const bool view_short = p->n_long == 0 && p->cfg.panels != 0 && p->cfg.tile == 0 && p->cfg.groups == 0 &&
+                          p->cfg.warp_stream < 0 && p->nrows > 0 && nnz > 0 && p->nrows < int64_t(UINT32_MAX) - 1;
+  if (view_long || view_short) {
     const uint32_t* vaj = p->row_sorted ? aj : p->sorted_aj.as<uint32_t>();
     const void* vav = p->row_sorted ? av : p->sorted_av.ptr;
     if ((rc = p->view_irp.alloc(4 * (p->nrows + 1)))) return rc;
@@ -998,8 +1007,9 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
       return rc;
     int path = 0;
     spmv_csr_plan_path(v, &path, nullptr);
-    if (path == 2) {
+    if (path == 2 || view_short) {
       p->csr_view = v;
+      p->view_panel = path == 2;
       p->view_ai = ai;
       p->view_aj = aj;
       p->view_av = av;
@@ -1233,7 +1243,7 @@ int spmv_coo_plan_config(const spmv_coo_plan* p, spmv_plan_config* out) {
   out->warp_stream = p->ws ? 1 : 0;
   out->ranges_per_warp = int32_t(p->ws_ranges_per_warp);
   out->tma_hint = p->tma_hint ? 1 : 0;
-  out->panels = p->csr_view ? 1 : 0;
+  out->panels = p->csr_view && p->view_panel ? 1 : 0;
   return SPMV_OK;
 }
 
@@ -1294,7 +1304,7 @@ int spmv_coo_plan_info(const spmv_coo_plan* p, int64_t* n_runs, int64_t* n_long_
 
 int spmv_coo_plan_path(const spmv_coo_plan* p, int* warp_stream, int64_t* nwarps) {
   if (!p) return fail(SPMV_INVALID_ARG, "plan is NULL");
-  if (warp_stream) *warp_stream = p->csr_view ? 2 : p->ws ? 1 : 0;
+  if (warp_stream) *warp_stream = p->csr_view ? (p->view_panel ? 2 : 3) : p->ws ? 1 : 0;
   if (nwarps) {
     *nwarps = p->ws_nwarps;
     if (p->csr_view) spmv_csr_plan_path(p->csr_view, nullptr, nwarps);

@@ -156,9 +156,12 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
         else if constexpr (VW > 0)
           P.y[yrow(P, r)] = row_vla_csr<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla);
         else
-          // -0.0 seed: the sum starts from the first product, like cumsum
-          P.y[yrow(P, r)] = products ? row_sum(vals + (s - E0), int(len), T(-0.0))
-                            : row_dot<T, true>(cols + (s - E0), vals + (s - E0), int(len), xb, T(-0.0));
+          // -0.0 seed: the sum starts from the first product, like cumsum;
+          // +0.0 (mode bit 3) for a COO plan's row-pointer view: np.add.at
+          // on a zeroed y (kernels.py:65)
+          P.y[yrow(P, r)] = products ? row_sum(vals + (s - E0), int(len), (P.mode & 8) ? T(0) : T(-0.0))
+                            : row_dot<T, true>(cols + (s - E0), vals + (s - E0), int(len), xb,
+                                               (P.mode & 8) ? T(0) : T(-0.0));
       }
     } else {
       const int64_t lo = max(int64_t(s), E0), hi = min(int64_t(e), E1);
@@ -828,7 +831,7 @@ static int csr_run_tiled(const spmv_csr_plan* p, const uint32_t* irp, const uint
   P.y_split = y_split;
   P.y_gap = y_gap;
   P.ymap = ymap;
-  P.mode = (p->cfg.flags & 3) | (p->tma_hint ? 4 : 0);
+  P.mode = (p->cfg.flags & 3) | (p->tma_hint ? 4 : 0) | ((p->cfg.flags & 4) ? 8 : 0);
   const bool aligned = (reinterpret_cast<uintptr_t>(aj) % 16 == 0) && (reinterpret_cast<uintptr_t>(av) % 16 == 0);
   P.n_bulk = aligned ? bulk_tiles(p->nnz, p->ntiles, TILE) : 0;
   const size_t smem1 = CsrSmem<T, TILE, 1>::total;

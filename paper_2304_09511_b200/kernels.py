@@ -145,8 +145,8 @@ class _Plan:
         _lib.call("spmv_coo_plan_path", self.handle, ctypes.byref(ws), ctypes.byref(nw))
         info = {"runs": a.value, "long_runs": b.value, "tile": c.value, "row_sorted": bool(d.value),
                 "launches": e.value, "groups": g.value, "kernel": "tile", "config": self.config().as_dict()}
-        if ws.value:
-            info.update(kernel="panel" if ws.value == 2 else "warp_stream", warps=nw.value)
+        if ws.value:  # 3: whole-matrix products run the CSR tile kernel on the plan's row-pointer view
+            info.update(kernel={1: "warp_stream", 2: "panel", 3: "csr_view"}[ws.value], warps=nw.value)
         return info
 
 

@@ -223,3 +223,41 @@ def test_vla_two_streams(sp):
     torch.cuda.synchronize()
     for y in ys:
         assert y.cpu().numpy().tobytes() == want.tobytes()
+
+
+@pytest.mark.parametrize("shuffle", [False, True])
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+def test_coo_row_pointer_view(sp, shuffle, dtype):
+    """COO plans without long runs run whole-matrix products on a CSR view of
+    their row-sorted triples (row pointers built by the plan; the CSR tile
+    kernel with a +0.0 seed): np.add.at order, bit for bit, also for an
+    unsorted input (stable row sort: storage order kept) and a lone -0.0
+    product (+0.0, not cumsum's -0.0).  panels=0 or a configured COO tile
+    keeps the COO tile kernel; both give the same bits."""
+    from _util import bit_equal, first_diff
+    from oracle import c_oracle
+    from paper_2304_09511_b200 import kernels as K
+    rng = np.random.default_rng(31)
+    n, ncols = 50_000, 70_000
+    lens = rng.integers(0, 33, n)
+    rows = np.repeat(np.arange(n), lens).astype(np.uint32)
+    cols = np.concatenate([np.sort(rng.choice(ncols, size=int(k), replace=False)) for k in lens]).astype(np.uint32)
+    vals = rng.uniform(-1, 1, rows.shape[0]).astype(dtype)
+    one = np.flatnonzero(lens == 1)[0]
+    vals[np.flatnonzero(rows == one)[0]] = -0.0
+    x = np.abs(rng.uniform(0.1, 1, ncols)).astype(dtype)
+    if shuffle:
+        order = rng.permutation(rows.shape[0])
+        rows, cols, vals = rows[order], cols[order], vals[order]
+    A = sp.CooMatrix.from_arrays(n, ncols, rows, cols, vals, sorted=not shuffle)
+    ref = c_oracle.coo_plain(n, rows, cols, vals, x, row_sorted=not shuffle)
+    assert K.coo_plan(A).info()["kernel"] == "csr_view"
+    y = sp.spmv_coo_plain(A, x)
+    assert bit_equal(y, ref), first_diff(y, ref)
+    assert y[one] == 0 and not np.signbit(y[one])
+    for cfg in (sp.PlanConfig(panels=0), sp.PlanConfig(tile=1536, groups=7)):
+        assert K.coo_plan(A, config=cfg).info()["kernel"] == "tile"
+        assert sp.spmv_coo_plain(A, x, plan_config=cfg).tobytes() == y.tobytes()
+    if not shuffle:  # vla keeps its own kernels (and refuses unsorted input like the reference)
+        from oracle import spmv_oracle as O
+        assert sp.spmv_coo_vla(A, x, sp.LaneConfig(8)).tobytes() == O.coo_vla(n, rows, cols, vals, x, 8).tobytes()
