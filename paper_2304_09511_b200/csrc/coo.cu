@@ -1368,7 +1368,16 @@ int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const
   if (p->nrows == 0) return SPMV_OK;
   if (p->nnz > 0) {
     bool done = false;
-    const int rc = p->dtype == SPMV_F64
+    if (p->csr_view && !p->view_panel && ai == p->view_ai && aj == p->view_aj && av == p->view_av) {
+      // the row-pointer view: the CSR tile kernel with the COO step order
+      int d = 0;
+      const int rcv = spmv_csr_vla_tiles(p->csr_view, p->view_irp.as<uint32_t>(),
+                                         p->row_sorted ? aj : p->sorted_aj.as<uint32_t>(),
+                                         p->row_sorted ? av : p->sorted_av.ptr, x, col_base, y, lanes, stream, &d);
+      if (rcv) return rcv;
+      done = d != 0;
+    }
+    const int rc = done ? SPMV_OK : p->dtype == SPMV_F64
                        ? coo_run_vla_tiles<double>(p, ai, aj, static_cast<const double*>(av),
                                                    static_cast<const double*>(x), col_base, static_cast<double*>(y),
                                                    lanes, st, &done)

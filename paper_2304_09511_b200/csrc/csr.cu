@@ -151,10 +151,16 @@ __device__ __forceinline__ void csr_tile_rows(const CsrParams<T>& P, int64_t t, 
       if (r < R1) P.y[yrow(P, r)] = T(0);
     } else if (len <= uint32_t(P.exact_len)) {
       if (int64_t(s) >= E0 && int64_t(s) < E1) {
+        // vla: the CSR lane order, or (mode bit 3: a COO plan's row-pointer
+        // view) the COO step order of kernels.py:174-210
         if constexpr (VW >= 16)
-          P.y[yrow(P, r)] = row_vla_csr_wide<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla);
+          P.y[yrow(P, r)] = (P.mode & 8) ? row_vla_coo_wide<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb,
+                                                                   P.vla, P.vla > 32)
+                                         : row_vla_csr_wide<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb,
+                                                                   P.vla);
         else if constexpr (VW > 0)
-          P.y[yrow(P, r)] = row_vla_csr<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla);
+          P.y[yrow(P, r)] = (P.mode & 8) ? row_vla_coo<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla)
+                                         : row_vla_csr<T, VW>(cols + (s - E0), vals + (s - E0), int(len), xb, P.vla);
         else
           // -0.0 seed: the sum starts from the first product, like cumsum;
           // +0.0 (mode bit 3) for a COO plan's row-pointer view: np.add.at
@@ -1874,6 +1880,26 @@ int spmv_csr_vla(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uin
                  void* stream) {
   (void)ncols;
   return csr_vla_launch(dtype, nrows, nnz, irp, aj, av, x, col_base, x_len, y, lanes, 1, as_stream(stream));
+}
+
+// vla through the tile kernels only (plans without long rows); *done = 0
+// when the plan has no such kernel.  COO plans call it for their
+// row-pointer view (the view's plan carries the COO-order flag).
+int spmv_csr_vla_tiles(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av, const void* x,
+                       int64_t col_base, void* y, int lanes, void* stream, int* done) {
+  if (!p || !done) return fail(SPMV_INVALID_ARG, "NULL argument");
+  *done = 0;
+  if (p->nrows == 0 || p->nnz == 0) return SPMV_OK;
+  bool d = false;
+  cudaStream_t st = as_stream(stream);
+  const int rc = p->dtype == SPMV_F64
+                     ? csr_run_vla_tiles<double>(p, irp, aj, static_cast<const double*>(av),
+                                                 static_cast<const double*>(x), col_base, static_cast<double*>(y), lanes,
+                                                 st, &d)
+                     : csr_run_vla_tiles<float>(p, irp, aj, static_cast<const float*>(av), static_cast<const float*>(x),
+                                                col_base, static_cast<float*>(y), lanes, st, &d);
+  *done = d ? 1 : 0;
+  return rc;
 }
 
 int spmv_csr_vla_planned(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av,
