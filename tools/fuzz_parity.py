@@ -2,7 +2,8 @@
 
 Random shapes and row-length mixes (empty rows, short rows, rows on the
 32 / 64 / 256 thresholds, long rows), f64 and f32, CSR / COO plain and vla
-at random lane counts, on whichever kernel each plan picks.  Contract as in
+at random lane counts, on whichever kernel each plan picks, plus sort_coo of
+the shuffled triples (with repeated coordinates) and the unsorted COO product.  Contract as in
 tests/test_gpu_kernels.py: rows <= 32 bit-exact, everything within 1e-12
 (f64) / 1e-5 of the f64-evaluated product (f32); vla bit-exact.  Prints
 one line per failure and a summary; exit code 1 on any failure.
@@ -92,14 +93,34 @@ def main():
                 yv = sp.spmv_coo_vla(C, x, sp.LaneConfig(lanes), st)
                 ok_cv = bit_equal(yv, O.coo_vla(nrows, rows, cols, vals, x, lanes, rst)) and \
                     st["outer_steps"] == rst["outer_steps"]
+            # sort_coo of the shuffled triples, some coordinates repeated
+            # (stable lexsort + reduceat-order duplicate sums, bit-exact) and
+            # the product of the unsorted COO (stable row sort in the plan)
+            ok_s = ok_u = True
+            if cols.shape[0] and cols.shape[0] <= 400000:
+                perm = rng.permutation(cols.shape[0])
+                sr, sc, sv = rows[perm].copy(), cols[perm].copy(), vals[perm].copy()
+                U = sp.CooMatrix.from_arrays(nrows, ncols, sr, sc, sv, False)
+                yu = sp.spmv_coo_plain(U, x)
+                ref_u = c_oracle.coo_plain(nrows, sr, sc, sv, x, row_sorted=False)
+                ok_u = bit_equal(yu[short], ref_u[short]) and rel_err(yu, ref64) <= tol
+                if rng.random() < 0.5:
+                    k = max(1, cols.shape[0] // 5)
+                    src, dst = rng.integers(0, cols.shape[0], k), rng.integers(0, cols.shape[0], k)
+                    sr[dst], sc[dst] = sr[src], sc[src]
+                got = sp.sort_coo(sp.CooMatrix.from_arrays(nrows, ncols, sr, sc, sv, False)).to_host()
+                r_ref, c_ref, v_ref = O.sort_coo(sr, sc, sv)
+                ok_s = np.array_equal(got["row_indices"], r_ref) and np.array_equal(got["col_indices"], c_ref) and \
+                    bit_equal(got["values"], v_ref)
         except Exception as e:  # noqa: BLE001
             print(f"case {case}: exception {type(e).__name__}: {e}")
             fails += 1
             continue
-        if not (ok and ok_c and ok_v and ok_cv):
+        if not (ok and ok_c and ok_v and ok_cv and ok_s and ok_u):
             fails += 1
             print(f"case {case}: nrows={nrows} ncols={ncols} nnz={cols.shape[0]} {np.dtype(dtype).name} "
-                  f"lanes={lanes} csr={ok} coo={ok_c} csr_vla={ok_v} coo_vla={ok_cv} max_len={lens.max()}")
+                  f"lanes={lanes} csr={ok} coo={ok_c} csr_vla={ok_v} coo_vla={ok_cv} sort_coo={ok_s} "
+                  f"coo_unsorted={ok_u} max_len={lens.max()}")
     # DIA: random diagonal sets (conversions on the device, product and
     # round trip bit-exact against the oracle)
     for case in range(cases // 2):
