@@ -935,7 +935,9 @@ static int sort_coo_run(int64_t nrows, int64_t nnz, const uint32_t* ai, const ui
       return SPMV_OK;
     };
     bool grouped = false;
-    if (lo > 0) {
+    // (hypersparse matrices, far more rows than entries, skip the group path:
+    // its per-row segment arrays would dwarf the entries)
+    if (lo > 0 && nrows <= 4 * nnz + 65536) {
       const unsigned long long* ks = key_in.as<unsigned long long>();
       const T* vs = av;
       if (bits > lo) {

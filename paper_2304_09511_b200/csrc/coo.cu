@@ -991,7 +991,8 @@ static int coo_plan_build(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* 
   // kernels (tile / groups / warp_stream) or turned views off (panels = 0).
   const bool view_long = p->n_long > 0 && p->cfg.panels != 0;
   const bool view_short = p->n_long == 0 && p->cfg.panels != 0 && p->cfg.tile == 0 && p->cfg.groups == 0 &&
-                          p->cfg.warp_stream < 0 && p->nrows > 0 && nnz > 0 && p->nrows < int64_t(UINT32_MAX) - 1;
+                          p->cfg.warp_stream < 0 && p->nrows > 0 && nnz > 0 && p->nrows < int64_t(UINT32_MAX) - 1 &&
+                          p->nrows <= 4 * nnz;  // hypersparse: the COO kernels' work follows the entries, not the rows
   if (view_long || view_short) {
     const uint32_t* vaj = p->row_sorted ? aj : p->sorted_aj.as<uint32_t>();
     const void* vav = p->row_sorted ? av : p->sorted_av.ptr;

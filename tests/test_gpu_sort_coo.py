@@ -62,6 +62,7 @@ CASES = {
     "huge_row": (50_000, 60_000, lambda r, n: np.where(np.arange(n) == 1234, 30_000, r.integers(0, 12, n)), 0.0),
     "gaps": (300_000, 1000, lambda r, n: np.where(np.arange(n) % 997 == 0, 25, 0), 0.1),  # mostly empty groups
     "one_entry": (5, 5, lambda r, n: np.array([0, 0, 1, 0, 0]), 0.0),
+    "hypersparse": (3_000_000, 50, lambda r, n: (r.random(n) < 0.001).astype(np.int64) * 3, 0.2),  # rows >> entries
 }
 
 
