@@ -14,7 +14,7 @@
 
 // Internal entry points shared between translation units (not part of
 // include/spmv_b200.h).
-extern "C" int spmv_csr_vla_tiles(spmv_csr_plan* plan, const uint32_t* irp, const uint32_t* aj, const void* av,
+extern "C" int spmvi_csr_vla_tiles(spmv_csr_plan* plan, const uint32_t* irp, const uint32_t* aj, const void* av,
                                   const void* x, int64_t col_base, void* y, int lanes, void* stream, int* done);
 
 namespace spmv {

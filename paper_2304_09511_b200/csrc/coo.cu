@@ -1372,7 +1372,7 @@ int spmv_coo_vla(spmv_coo_plan* p, const uint32_t* ai, const uint32_t* aj, const
     if (p->csr_view && !p->view_panel && ai == p->view_ai && aj == p->view_aj && av == p->view_av) {
       // the row-pointer view: the CSR tile kernel with the COO step order
       int d = 0;
-      const int rcv = spmv_csr_vla_tiles(p->csr_view, p->view_irp.as<uint32_t>(),
+      const int rcv = spmvi_csr_vla_tiles(p->csr_view, p->view_irp.as<uint32_t>(),
                                          p->row_sorted ? aj : p->sorted_aj.as<uint32_t>(),
                                          p->row_sorted ? av : p->sorted_av.ptr, x, col_base, y, lanes, stream, &d);
       if (rcv) return rcv;

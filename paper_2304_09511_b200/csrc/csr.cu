@@ -1885,7 +1885,7 @@ int spmv_csr_vla(int dtype, int64_t nrows, int64_t ncols, int64_t nnz, const uin
 // vla through the tile kernels only (plans without long rows); *done = 0
 // when the plan has no such kernel.  COO plans call it for their
 // row-pointer view (the view's plan carries the COO-order flag).
-int spmv_csr_vla_tiles(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av, const void* x,
+int spmvi_csr_vla_tiles(spmv_csr_plan* p, const uint32_t* irp, const uint32_t* aj, const void* av, const void* x,
                        int64_t col_base, void* y, int lanes, void* stream, int* done) {
   if (!p || !done) return fail(SPMV_INVALID_ARG, "NULL argument");
   *done = 0;
