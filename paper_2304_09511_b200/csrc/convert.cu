@@ -330,8 +330,19 @@ __global__ void __launch_bounds__(256) dia_rows_kernel(const int32_t* __restrict
 // repeats: duplicate runs summed in np.add.reduceat order and compacted.
 
 // flag = 1 if some row index is smaller than the one before it
+// (a thread stops at its first descent and stores once: on shuffled rows every
+// thread used to store on every step, 1.5 ms of same-address traffic at 256^3)
 __global__ void rows_descend_kernel(const uint32_t* __restrict__ ai, int64_t nnz, int* __restrict__ flag) {
-  GRID_STRIDE(k, nnz) if (k > 0 && ai[k] < ai[k - 1]) *flag = 1;
+  bool bad = false;
+  int it = 0;
+  GRID_STRIDE(k, nnz) {
+    if (k > 0 && ai[k] < ai[k - 1]) {
+      bad = true;
+      break;
+    }
+    if ((++it & 15) == 0 && *reinterpret_cast<volatile int*>(flag)) break;  // another thread found one
+  }
+  if (bad) *flag = 1;
 }
 
 // A row of m <= 32 entries, one column per lane (lanes >= m: `in` false):
@@ -481,12 +492,17 @@ __global__ void sort_pack_kernel(const uint32_t* __restrict__ ai, const uint32_t
 }
 
 // start[q] = first sorted entry whose key >> shift is >= q, q = 0..ngroups.
+// One binary search per group over the sorted keys (a few thousand random
+// reads) instead of a pass over all of them.
 __global__ void group_bounds_kernel(const unsigned long long* __restrict__ key_s, int64_t nnz, int shift,
                                     int64_t ngroups, uint32_t* __restrict__ start) {
-  for (int64_t i = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; i <= nnz; i += int64_t(gridDim.x) * blockDim.x) {
-    const int64_t q1 = i < nnz ? int64_t(key_s[i] >> shift) : ngroups;
-    const int64_t q0 = i == 0 ? -1 : int64_t(key_s[i - 1] >> shift);
-    for (int64_t q = q0 + 1; q <= q1; ++q) start[q] = uint32_t(i);
+  GRID_STRIDE(q, ngroups + 1) {
+    int64_t lo = 0, hi = nnz;  // first i in [0, nnz] with key_s[i] >> shift >= q
+    while (lo < hi) {
+      const int64_t mid = (lo + hi) >> 1;
+      if (int64_t(__ldg(key_s + mid) >> shift) < q) lo = mid + 1; else hi = mid;
+    }
+    start[q] = uint32_t(lo);
   }
 }
 
@@ -1101,7 +1117,7 @@ static int sort_coo_run(int64_t nrows, int64_t nnz, const uint32_t* ai, const ui
       ScratchBuf gstart, gmax;
       if ((r = gstart.alloc(4 * (ngroups + 1), st)) || (r = gmax.alloc(4, st))) return r;
       SPMV_CUDA_TRY(cudaMemsetAsync(gmax.ptr, 0, 4, st));
-      group_bounds_kernel<<<unsigned(grid_for(nnz + 1)), 256, 0, st>>>(ks, nnz, 32 + lo, ngroups, gstart.as<uint32_t>());
+      group_bounds_kernel<<<unsigned(grid_for(ngroups + 1)), 256, 0, st>>>(ks, nnz, 32 + lo, ngroups, gstart.as<uint32_t>());
       SPMV_LAUNCH_CHECK();
       max_diff_kernel<<<unsigned(grid_for(ngroups)), 256, 0, st>>>(gstart.as<uint32_t>(), ngroups, gmax.as<uint32_t>());
       SPMV_LAUNCH_CHECK();
