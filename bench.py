@@ -556,6 +556,14 @@ def per_config_measure(args, torch, sp, device, pk, name: str) -> dict:
              "gbs": round(b / t / 1e9, 1), "bytes_per_spmv": b, "launches": launches_per_spmv(sp, m),
              "plan": plan_of(sp, m), "roofline_frac": round(b / t / 1e9 / pk["hbm_gbs"], 4), "nnz": m.nnz,
              "steps": steps}
+        if flush is not None:
+            # back-to-back products: the 64^3 operator (87 MB CSR) stays in the
+            # 126 MB L2, which is how a solver iteration sees it; reported
+            # beside the flushed number, never as the roofline figure
+            tw = time_steps(torch, fn, steps * 4, args.warmup)
+            r["l2_resident"] = {"gflops": round(2.0 * m.nnz / tw / 1e9, 2), "ms_per_spmv": round(tw * 1e3, 4),
+                                "gbs": round(b / tw / 1e9, 1),
+                                "note": "back-to-back, no flush: matrix and x served from L2; not an HBM roofline number"}
         if name == "c3":
             r["gather_roofline"] = {
                 "achieved_ggathers_s": round(m.nnz / t / 1e9, 1), "ceiling_ggathers_s": GATHER_CEILING_GS,
@@ -842,6 +850,47 @@ def _reference_sample(args, c_oracle, synthetic):
     return fn, nnz, desc, "dia", (n, nnz_total)
 
 
+def _reference_numpy(args, c_oracle, synthetic):
+    """The unmodified reference's own numpy CSR kernel (spmvkit.kernels.
+    spmv_csr_plain from baseline/_ref, the installed reference package) on a
+    small sample of the stencil configs: the number the C port stands in for.
+    Reported beside the port, never used as `value`."""
+    ref_dir = ROOT / "baseline" / "_ref"
+    if args.config not in ("c5", "c1"):
+        return {"unavailable": "stencil configs only"}
+    if not (ref_dir / "spmvkit" / "__init__.py").exists():
+        return {"unavailable": "reference package not installed in baseline/_ref"}
+    try:
+        sys.path.insert(0, str(ref_dir))
+        from spmvkit.formats import CsrMatrix
+        from spmvkit.kernels import spmv_csr_plain
+        nx, ny, nz = CONFIGS[args.config]["grid"]
+        plane, planes = nx * ny, max(1, min(nz, 262144 // (nx * ny)))
+        r0 = (nz // 2 - planes // 2) * plane
+        r1 = r0 + planes * plane
+        irp, cols, vals = c_oracle.stencil27_rows(nx, ny, nz, r0, r1)
+        x = synthetic.probe_x(nx * ny * nz, synthetic.X_SEED)
+        A = CsrMatrix.from_arrays(r1 - r0, nx * ny * nz, irp, cols, vals)
+        y = spmv_csr_plain(A, x)  # warm-up, and the port's parity on the sample
+        same = y.tobytes() == c_oracle.csr_plain(r1 - r0, irp, cols, vals, x).tobytes()
+        ts = []
+        for _ in range(3):
+            t0 = time.perf_counter()
+            spmv_csr_plain(A, x)
+            ts.append(time.perf_counter() - t0)
+        t = sorted(ts)[1]
+        return {"value": round(2.0 * vals.shape[0] / t / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "reference",
+                "s_per_step": round(t, 4), "port_bit_identical_on_sample": bool(same),
+                "sample": (f"z-planes {r0 // plane}..{r1 // plane - 1} of the {nx}x{ny}x{nz} stencil "
+                           f"({r1 - r0} rows, {vals.shape[0]} entries); spmvkit.kernels.spmv_csr_plain "
+                           "(kernels.py:69-82) from baseline/_ref, median of 3")}
+    except Exception as exc:  # a report field only: never fails the arm
+        return {"unavailable": f"{type(exc).__name__}: {exc}"}
+    finally:
+        if sys.path and sys.path[0] == str(ref_dir):
+            sys.path.pop(0)
+
+
 def run_reference(args, rank, world):
     """The reference's CPU SpMV (C restatement of kernels.py, all host
     threads) on a bounded sample of the same workload; no GPU touched."""
@@ -864,7 +913,8 @@ def run_reference(args, rank, world):
             "config": config_block(args.config, fmt, dims[0], dims[1], world),
             "cpu_baseline": {"value": v, "unit": UNIT, "kind": "port", "cores": c_oracle.max_threads(),
                              "sample": sample},
-            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+            "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+            "reference_numpy": _reference_numpy(args, c_oracle, synthetic)}
     emit(line)
 
 
