@@ -158,3 +158,38 @@ def test_validate_device(sp):
         assert sp.validate(dev_matrix(sp, matrix_arrays(d, fmt), fmt)) == []
     bad = sp.CooMatrix.from_arrays(2, 2, [1, 0], [0, 1], [1.0, 2.0], sorted=True)
     assert any("sorted flag" in v for v in sp.validate(bad))
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("nrows,ncols,offsets", [
+    (1000, 1000, [-65, -1, 0, 1, 65]),                       # 8 lanes per row, 4 rows per warp step
+    (5000, 5000, [-4096, -1024, -512, -2, -1, 0, 1, 2, 512, 1024, 4096]),  # 16 lanes per row
+    (4097, 4097, list(range(-13, 14))),                        # 27 diagonals, a partial last tile
+    (3000, 3000, list(range(-16, 16))),                        # 32 diagonals: the tile kernels' limit
+    (3000, 3000, list(range(-20, 20))),                        # 40 diagonals: the per-row kernels
+    (700, 2500, [-900, -3, 0, 5, 1800, 2600]),                 # wide: a diagonal with no in-bounds cell
+    (2500, 300, [-2600, -2400, -7, 0, 3, 299]),                # tall
+    (129, 129, [0]),                                           # one lane per row, 32 rows per warp step
+])
+def test_dia_to_coo_tile_kernels_match_oracle(sp, dtype, nrows, ncols, offsets):
+    """dia_to_coo (per-tile count + emit kernels up to 32 diagonals, per-row
+    kernels above) against the oracle's convert.py:147-177 restatement: dense
+    diagonals with zeros, -0.0 (dropped) and NaN (kept) sprinkled in, several
+    row tiles, every lane-group width."""
+    from oracle import spmv_oracle as O
+    rng = np.random.default_rng(nrows * 31 + len(offsets))
+    offs = np.array(offsets, dtype=np.int32)
+    padded = O.round_up(nrows, 8)
+    vals = rng.uniform(-1.0, 1.0, (padded, len(offs))).astype(dtype)
+    vals[rng.random(vals.shape) < 0.05] = 0.0
+    vals[rng.random(vals.shape) < 0.02] = -0.0
+    vals[rng.random(vals.shape) < 0.01] = np.nan
+    vals[nrows:] = 0.0
+    r = np.arange(padded, dtype=np.int64)[:, None] + offs[None, :].astype(np.int64)
+    vals[(r < 0) | (r >= ncols)] = 0.0  # out-of-matrix cells are stored as zero (formats.py:166-207)
+    wr, wc, wv = O.dia_to_coo(nrows, ncols, offs, vals)
+    dia = sp.DiaMatrix(sp.MatrixShape(nrows, ncols, wr.shape[0]), offs, vals)
+    got = sp.dia_to_coo(dia).to_host()
+    assert got["shape"].nnz == wr.shape[0]
+    assert np.array_equal(got["row_indices"], wr) and np.array_equal(got["col_indices"], wc)
+    assert bit_equal(got["values"], wv)
