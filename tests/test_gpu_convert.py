@@ -193,3 +193,40 @@ def test_dia_to_coo_tile_kernels_match_oracle(sp, dtype, nrows, ncols, offsets):
     assert got["shape"].nnz == wr.shape[0]
     assert np.array_equal(got["row_indices"], wr) and np.array_equal(got["col_indices"], wc)
     assert bit_equal(got["values"], wv)
+
+
+@pytest.mark.parametrize("dtype", [np.float64, np.float32])
+@pytest.mark.parametrize("nrows,ncols,offsets,pad_to,misflag", [
+    (1000, 1000, [-65, -1, 0, 1, 65], 8, False),
+    (4099, 4099, list(range(-13, 14)), 8, False),        # 27 diagonals: 128-row tiles (f64), a partial last tile
+    (4099, 4099, list(range(-13, 14)), 64, False),       # padding rows past nrows in the last tile
+    (3000, 3500, [-2999, -40, 0, 7, 3499], 8, False),    # corner diagonals with one cell each
+    (2000, 2000, list(range(-300, 300, 3)), 8, False),   # 200 diagonals: 16-row tiles (f64)
+    (600, 600, list(range(-599, 600)), 8, False),        # 1199 diagonals: rows over 4 KB, the scatter path for f64
+    (1500, 1500, [-3, 0, 4], 8, True),                    # flagged sorted, rows out of order: the scatter path
+])
+def test_coo_to_dia_row_tiles_match_oracle(sp, dtype, nrows, ncols, offsets, pad_to, misflag):
+    """coo_to_dia's row-tile fill (shared-memory tiles of row-ordered triples,
+    one coalesced store of every tile) and its entry-by-entry fallback against
+    the oracle's convert.py:113-144 restatement: empty rows, tile-straddling
+    structure, padding rows, wide blocks, mis-flagged row order."""
+    from oracle import spmv_oracle as O
+    rng = np.random.default_rng(nrows + 7 * len(offsets) + pad_to)
+    offs = np.array(offsets, dtype=np.int64)
+    rows = np.repeat(np.arange(nrows, dtype=np.int64), len(offs))
+    cols = rows + np.tile(offs, nrows)
+    keep = (cols >= 0) & (cols < ncols) & (rng.random(rows.shape[0]) < 0.8)
+    keep &= ~np.isin(rows, rng.choice(nrows, nrows // 20, replace=False))  # some empty rows
+    for o in offs:  # every diagonal keeps at least one cell
+        i = int(np.flatnonzero((cols - rows == o) & (cols >= 0) & (cols < ncols))[0])
+        keep[i] = True
+    rows, cols = rows[keep], cols[keep]
+    vals = rng.uniform(-1.0, 1.0, rows.shape[0]).astype(dtype)
+    if misflag:
+        perm = rng.permutation(rows.shape[0])
+        rows, cols, vals = rows[perm], cols[perm], vals[perm]
+    want_off, want_vals = O.coo_to_dia(nrows, ncols, rows, cols, vals, pad_to)
+    coo = sp.CooMatrix.from_arrays(nrows, ncols, rows.astype(np.uint32), cols.astype(np.uint32), vals, sorted=True)
+    got = sp.coo_to_dia(coo, sp.DiaFillPolicy(float("inf")), pad_to).to_host()
+    assert np.array_equal(got["offsets"], want_off)
+    assert got["values"].shape == want_vals.shape and bit_equal(got["values"], want_vals)
