@@ -198,18 +198,17 @@ def test_dia_to_coo_tile_kernels_match_oracle(sp, dtype, nrows, ncols, offsets):
 @pytest.mark.parametrize("dtype", [np.float64, np.float32])
 @pytest.mark.parametrize("nrows,ncols,offsets,pad_to,misflag", [
     (1000, 1000, [-65, -1, 0, 1, 65], 8, False),
-    (4099, 4099, list(range(-13, 14)), 8, False),        # 27 diagonals: 128-row tiles (f64), a partial last tile
-    (4099, 4099, list(range(-13, 14)), 64, False),       # padding rows past nrows in the last tile
+    (4099, 4099, list(range(-13, 14)), 8, False),        # 27 diagonals
+    (4099, 4099, list(range(-13, 14)), 64, False),       # padding rows past nrows
     (3000, 3500, [-2999, -40, 0, 7, 3499], 8, False),    # corner diagonals with one cell each
-    (2000, 2000, list(range(-300, 300, 3)), 8, False),   # 200 diagonals: 16-row tiles (f64)
-    (600, 600, list(range(-599, 600)), 8, False),        # 1199 diagonals: rows over 4 KB, the scatter path for f64
-    (1500, 1500, [-3, 0, 4], 8, True),                    # flagged sorted, rows out of order: the scatter path
+    (2000, 2000, list(range(-300, 300, 3)), 8, False),   # 200 diagonals
+    (600, 600, list(range(-599, 600)), 8, False),        # 1199 diagonals
+    (1500, 1500, [-3, 0, 4], 8, True),                    # flagged sorted, rows out of order
 ])
-def test_coo_to_dia_row_tiles_match_oracle(sp, dtype, nrows, ncols, offsets, pad_to, misflag):
-    """coo_to_dia's row-tile fill (shared-memory tiles of row-ordered triples,
-    one coalesced store of every tile) and its entry-by-entry fallback against
-    the oracle's convert.py:113-144 restatement: empty rows, tile-straddling
-    structure, padding rows, wide blocks, mis-flagged row order."""
+def test_coo_to_dia_structures_match_oracle(sp, dtype, nrows, ncols, offsets, pad_to, misflag):
+    """coo_to_dia (diagonal census, zero fill, scatter) against the oracle's
+    convert.py:113-144 restatement: empty rows, padding rows past nrows, corner
+    diagonals, wide blocks, and triples flagged sorted whose rows are not."""
     from oracle import spmv_oracle as O
     rng = np.random.default_rng(nrows + 7 * len(offsets) + pad_to)
     offs = np.array(offsets, dtype=np.int64)
