@@ -223,87 +223,12 @@ __global__ void __launch_bounds__(256) csr_expand_vec_kernel(const uint32_t* __r
 
 // ---- coo -> dia --------------------------------------------------------------
 __global__ void diag_mark_kernel(const uint32_t* __restrict__ ai, const uint32_t* __restrict__ aj, int64_t nnz,
-                                 int64_t nrows, uint32_t* __restrict__ flags, int* __restrict__ descending) {
+                                 int64_t nrows, uint32_t* __restrict__ flags) {
   // A matrix has few distinct diagonals: reading first (through L1) keeps
   // the flag lines shared instead of storing to the same words nnz times.
-  // descending: some row index is smaller than the one before it (the fill
-  // then scatters entry by entry instead of building row tiles).
-  bool bad = false;
   GRID_STRIDE(k, nnz) {
-    const uint32_t r = ai[k];
-    uint32_t* f = flags + (int64_t(aj[k]) - int64_t(r) + nrows - 1);
+    uint32_t* f = flags + (int64_t(aj[k]) - int64_t(ai[k]) + nrows - 1);
     if (__ldg(f) == 0u) *f = 1u;  // a stale 0 only repeats an idempotent store
-    bad |= k > 0 && r < __ldg(ai + k - 1);
-  }
-  if (bad) *descending = 1;
-}
-
-// Row-tile fill for row-ordered triples: a CTA builds R rows of the block in
-// shared memory (zeros, then its entries scattered by diagonal) and writes
-// them out as one contiguous run of 16-byte stores — every cell of the block
-// written exactly once (no zero-fill pass over the block, no scattered 8-byte
-// stores to HBM).  first[t] = first entry of row tile t (binary search).
-__global__ void dia_tile_bounds_kernel(const uint32_t* __restrict__ ai, int64_t nnz, int64_t R, int64_t ntiles,
-                                       uint32_t* __restrict__ first) {
-  GRID_STRIDE(t, ntiles + 1) {
-    const int64_t want = t * R;
-    int64_t lo = 0, hi = nnz;  // first k with ai[k] >= want
-    while (lo < hi) {
-      const int64_t mid = (lo + hi) >> 1;
-      if (int64_t(__ldg(ai + mid)) < want) lo = mid + 1; else hi = mid;
-    }
-    first[t] = uint32_t(lo);
-  }
-}
-
-template <typename T>
-__global__ void __launch_bounds__(256) dia_tile_fill_kernel(const uint32_t* __restrict__ ai,
-                                                            const uint32_t* __restrict__ aj,
-                                                            const T* __restrict__ av,
-                                                            const uint32_t* __restrict__ first, int64_t nrows,
-                                                            int64_t padded_rows, int64_t nd, int R, int64_t ntiles,
-                                                            const uint32_t* __restrict__ pos, T* __restrict__ out,
-                                                            bool vec_ok) {
-  extern __shared__ __align__(16) unsigned char dia_tile_smem[];
-  T* tile = reinterpret_cast<T*>(dia_tile_smem);
-  constexpr int V = 16 / int(sizeof(T));
-  for (int64_t t = blockIdx.x; t < ntiles; t += gridDim.x) {
-    const int64_t r0 = t * R;
-    const int n = int(min(int64_t(R), padded_rows - r0) * nd);
-    for (int i = threadIdx.x; i < n; i += blockDim.x) tile[i] = T(0);
-    __syncthreads();
-    const uint32_t e0 = first[t], e1 = first[t + 1];
-    for (uint32_t e = e0 + threadIdx.x; e < e1; e += 4 * blockDim.x) {
-      uint32_t r[4], c[4];
-      T v[4];
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t k = e + u * blockDim.x;
-        if (k < e1) {
-          r[u] = __ldcs(ai + k);
-          c[u] = __ldcs(aj + k);
-          v[u] = __ldcs(av + k);
-        }
-      }
-#pragma unroll
-      for (int u = 0; u < 4; ++u) {
-        const uint32_t k = e + u * blockDim.x;
-        if (k < e1) {
-          const uint32_t d = __ldg(pos + (int64_t(c[u]) - int64_t(r[u]) + nrows - 1));
-          tile[(int64_t(r[u]) - r0) * nd + d] = v[u];
-        }
-      }
-    }
-    __syncthreads();
-    T* dst = out + r0 * nd;
-    if (vec_ok && n % V == 0) {
-      const uint4* s4 = reinterpret_cast<const uint4*>(tile);
-      uint4* d4 = reinterpret_cast<uint4*>(dst);
-      for (int i = threadIdx.x; i < n / V; i += blockDim.x) __stcs(d4 + i, s4[i]);
-    } else {
-      for (int i = threadIdx.x; i < n; i += blockDim.x) dst[i] = tile[i];
-    }
-    __syncthreads();
   }
 }
 
@@ -916,7 +841,6 @@ using namespace spmv;
 
 struct spmv_dia_builder {
   int64_t nrows = 0, ncols = 0, nnz = 0, nd_all = 0, ndiags = 0;
-  bool rows_ordered = false;  // the triples' rows never descend: the fill builds row tiles
   ScratchBuf flags, pos;
 };
 
@@ -1052,26 +976,16 @@ int spmv_coo_to_dia_analyze(int64_t nrows, int64_t ncols, int64_t nnz, const uin
   int rc = SPMV_OK;
   if (nnz > 0) {
     b->nd_all = nrows + ncols - 1;
-    ScratchBuf desc;
-    if (!(rc = b->flags.alloc(4 * b->nd_all, st)) && !(rc = b->pos.alloc(4 * b->nd_all, st)) &&
-        !(rc = desc.alloc(sizeof(int), st))) {
+    if (!(rc = b->flags.alloc(4 * b->nd_all, st)) && !(rc = b->pos.alloc(4 * b->nd_all, st))) {
       cudaError_t e = cudaMemsetAsync(b->flags.ptr, 0, 4 * b->nd_all, st);
-      if (e == cudaSuccess) e = cudaMemsetAsync(desc.ptr, 0, sizeof(int), st);
       if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "memset: %s", cudaGetErrorString(e));
       if (!rc) {
-        diag_mark_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, aj, nnz, nrows, b->flags.as<uint32_t>(),
-                                                                 desc.as<int>());
+        diag_mark_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, aj, nnz, nrows, b->flags.as<uint32_t>());
         e = cudaGetLastError();
         if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "diag_mark: %s", cudaGetErrorString(e));
       }
-      int hdesc = 1;
-      if (!rc) {
-        e = cudaMemcpyAsync(&hdesc, desc.ptr, sizeof(int), cudaMemcpyDeviceToHost, st);  // read by scan_total's sync
-        if (e != cudaSuccess) rc = fail(SPMV_CUDA_ERROR, "memcpy: %s", cudaGetErrorString(e));
-      }
       if (!rc) rc = excl_scan<uint32_t>(b->flags.as<uint32_t>(), b->pos.as<uint32_t>(), b->nd_all, st);
       if (!rc) rc = scan_total<uint32_t>(b->flags.as<uint32_t>(), b->pos.as<uint32_t>(), b->nd_all, st, &b->ndiags);
-      if (!rc) b->rows_ordered = hdesc == 0;
     }
   }
   if (rc) {
@@ -1100,32 +1014,6 @@ int spmv_coo_to_dia_fill(const spmv_dia_builder* b, int dtype, int64_t padded_ro
   if (padded_rows < b->nrows) return fail(SPMV_INVALID_ARG, "padded_rows < nrows");
   cudaStream_t st = as_stream(stream);
   const size_t bytes = value_size(dtype) * size_t(padded_rows) * size_t(b->ndiags);
-  // row-ordered triples: row tiles of up to 32 KB built in shared memory
-  const int64_t row_bytes = int64_t(value_size(dtype)) * b->ndiags;
-  const int64_t R = row_bytes > 0 ? std::min<int64_t>(256, 32768 / row_bytes) / 8 * 8 : 0;
-  if (b->rows_ordered && b->nnz > 0 && R >= 8) {
-    const int64_t ntiles = (padded_rows + R - 1) / R;
-    ScratchBuf first;
-    int rc = first.alloc(4 * (ntiles + 1), st);
-    if (rc) return rc;
-    dia_tile_bounds_kernel<<<unsigned(grid_for(ntiles + 1)), 256, 0, st>>>(ai, b->nnz, R, ntiles, first.as<uint32_t>());
-    SPMV_LAUNCH_CHECK();
-    const unsigned grid = unsigned(std::min<int64_t>(ntiles, int64_t(sm_count()) * 8));
-    const size_t smem = size_t(R * row_bytes);
-    const bool vec_ok = reinterpret_cast<uintptr_t>(values_out) % 16 == 0 && (R * row_bytes) % 16 == 0;
-    if (dtype == SPMV_F64)
-      dia_tile_fill_kernel<double><<<grid, 256, smem, st>>>(ai, aj, static_cast<const double*>(av),
-                                                            first.as<uint32_t>(), b->nrows, padded_rows, b->ndiags,
-                                                            int(R), ntiles, b->pos.as<uint32_t>(),
-                                                            static_cast<double*>(values_out), vec_ok);
-    else
-      dia_tile_fill_kernel<float><<<grid, 256, smem, st>>>(ai, aj, static_cast<const float*>(av),
-                                                           first.as<uint32_t>(), b->nrows, padded_rows, b->ndiags,
-                                                           int(R), ntiles, b->pos.as<uint32_t>(),
-                                                           static_cast<float*>(values_out), vec_ok);
-    SPMV_LAUNCH_CHECK();
-    return SPMV_OK;
-  }
   if (bytes) SPMV_CUDA_TRY(cudaMemsetAsync(values_out, 0, bytes, st));
   if (b->nnz == 0 || b->ndiags == 0) return SPMV_OK;
   if (dtype == SPMV_F64)
