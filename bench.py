@@ -873,17 +873,31 @@ def _reference_numpy(args, c_oracle, synthetic):
         A = CsrMatrix.from_arrays(r1 - r0, nx * ny * nz, irp, cols, vals)
         y = spmv_csr_plain(A, x)  # warm-up, and the port's parity on the sample
         same = y.tobytes() == c_oracle.csr_plain(r1 - r0, irp, cols, vals, x).tobytes()
-        ts = []
-        for _ in range(3):
-            t0 = time.perf_counter()
-            spmv_csr_plain(A, x)
-            ts.append(time.perf_counter() - t0)
-        t = sorted(ts)[1]
-        return {"value": round(2.0 * vals.shape[0] / t / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "reference",
-                "s_per_step": round(t, 4), "port_bit_identical_on_sample": bool(same),
-                "sample": (f"z-planes {r0 // plane}..{r1 // plane - 1} of the {nx}x{ny}x{nz} stencil "
-                           f"({r1 - r0} rows, {vals.shape[0]} entries); spmvkit.kernels.spmv_csr_plain "
-                           "(kernels.py:69-82) from baseline/_ref, median of 3")}
+
+        def med3(fn):
+            ts = []
+            for _ in range(3):
+                t0 = time.perf_counter()
+                fn()
+                ts.append(time.perf_counter() - t0)
+            return sorted(ts)[1]
+
+        t = med3(lambda: spmv_csr_plain(A, x))
+        out = {"value": round(2.0 * vals.shape[0] / t / 1e9, 4), "unit": UNIT, "cores": 1, "kind": "reference",
+               "s_per_step": round(t, 4), "port_bit_identical_on_sample": bool(same),
+               "sample": (f"z-planes {r0 // plane}..{r1 // plane - 1} of the {nx}x{ny}x{nz} stencil "
+                          f"({r1 - r0} rows, {vals.shape[0]} entries); spmvkit.kernels.spmv_csr_plain "
+                          "(kernels.py:69-82) from baseline/_ref, median of 3")}
+        # the other two formats of the same sample (kernels.py:56-66, :85-101), the reference's own conversions
+        from spmvkit.convert import DiaFillPolicy, to_format
+        from spmvkit.kernels import spmv_coo_plain, spmv_dia_plain
+        coo = to_format(A, "coo")
+        dia = to_format(coo, "dia", DiaFillPolicy(float("inf")))
+        for name, fn in (("coo", lambda: spmv_coo_plain(coo, x)), ("dia", lambda: spmv_dia_plain(dia, x))):
+            fn()
+            tf = med3(fn)
+            out[name] = {"value": round(2.0 * vals.shape[0] / tf / 1e9, 4), "s_per_step": round(tf, 4)}
+        return out
     except Exception as exc:  # a report field only: never fails the arm
         return {"unavailable": f"{type(exc).__name__}: {exc}"}
     finally:
