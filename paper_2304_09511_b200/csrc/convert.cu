@@ -404,17 +404,20 @@ __global__ void __launch_bounds__(kDiaTileThreads, 3)
 // repeats: duplicate runs summed in np.add.reduceat order and compacted.
 
 // flag = 1 if some row index is smaller than the one before it
-// (a thread stops at its first descent and stores once: on shuffled rows every
-// thread used to store on every step, 1.5 ms of same-address traffic at 256^3)
+// (a thread stops after the batch holding its first descent and stores once:
+// on shuffled rows every thread used to store on every step, 1.5 ms of
+// same-address traffic at 256^3; batches of 8 independent loads keep the
+// ordered case a plain stream)
 __global__ void rows_descend_kernel(const uint32_t* __restrict__ ai, int64_t nnz, int* __restrict__ flag) {
+  const int64_t stride = int64_t(gridDim.x) * blockDim.x;
   bool bad = false;
-  int it = 0;
-  GRID_STRIDE(k, nnz) {
-    if (k > 0 && ai[k] < ai[k - 1]) {
-      bad = true;
-      break;
+  for (int64_t k0 = int64_t(blockIdx.x) * blockDim.x + threadIdx.x; k0 < nnz && !bad; k0 += 8 * stride) {
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int64_t k = k0 + u * stride;
+      if (k > 0 && k < nnz) bad |= __ldg(ai + k) < __ldg(ai + k - 1);
     }
-    if ((++it & 15) == 0 && *reinterpret_cast<volatile int*>(flag)) break;  // another thread found one
+    if (!bad && *reinterpret_cast<volatile int*>(flag)) break;  // another thread found one
   }
   if (bad) *flag = 1;
 }
@@ -1159,6 +1162,38 @@ static int merge_duplicates(const uint32_t* seg, const uint32_t* ucnt, int64_t n
   return SPMV_OK;
 }
 
+// Onesweep tile shape of sort_coo's radix passes.  CUB's sm_100 policy for
+// 8-byte keys is 384 threads x 24 items; tools/radix_tune.cu (B200, two
+// passes + histogram over 449M (key, value) records, input kept) measures
+// 9.06 ms for it with 64-bit offsets, 13.14 ms with 32-bit offsets (an
+// occupancy cliff), and 8.36 ms for 256 threads x 30 items with either offset
+// width (f32 values: 7.57 default, 7.55 at 256 x 32): profiles/r2d_radix_tune.txt.
+// Everything else is CUB's own policy.
+template <typename T>
+struct SortHub {
+  using Base = cub::detail::radix::policy_hub<unsigned long long, T, unsigned int>;
+  using B = typename Base::Policy1000;
+  struct Policy : cub::ChainedPolicy<500, Policy, Policy> {
+    static constexpr bool ONESWEEP = true;
+    static constexpr int ONESWEEP_RADIX_BITS = 8;
+    using HistogramPolicy = typename B::HistogramPolicy;
+    using ExclusiveSumPolicy = typename B::ExclusiveSumPolicy;
+    using OnesweepPolicy =
+        cub::AgentRadixSortOnesweepPolicy<256, sizeof(T) == 8 ? 30 : 32, unsigned long long, 1,
+                                          cub::RADIX_RANK_MATCH_EARLY_COUNTS_ANY, cub::BLOCK_SCAN_RAKING_MEMOIZE,
+                                          cub::RADIX_SORT_STORE_DIRECT, 8>;
+    using ScanPolicy = typename B::ScanPolicy;
+    using DownsweepPolicy = typename B::DownsweepPolicy;
+    using AltDownsweepPolicy = typename B::AltDownsweepPolicy;
+    using UpsweepPolicy = typename B::UpsweepPolicy;
+    using AltUpsweepPolicy = typename B::AltUpsweepPolicy;
+    using SingleTilePolicy = typename B::SingleTilePolicy;
+    using SegmentedPolicy = typename B::SegmentedPolicy;
+    using AltSegmentedPolicy = typename B::AltSegmentedPolicy;
+  };
+  using MaxPolicy = Policy;
+};
+
 template <typename T>
 static int sort_coo_run(int64_t nrows, int64_t nnz, const uint32_t* ai, const uint32_t* aj, const T* av,
                         uint32_t* ai_out, uint32_t* aj_out, T* av_out, int64_t* n_out, cudaStream_t st) {
@@ -1194,13 +1229,15 @@ static int sort_coo_run(int64_t nrows, int64_t nnz, const uint32_t* ai, const ui
     sort_pack_kernel<<<unsigned(grid_for(nnz)), 256, 0, st>>>(ai, aj, nnz, key_in.as<unsigned long long>());
     SPMV_LAUNCH_CHECK();
     auto radix = [&](int b0, int b1) -> int {  // (key_in, av) -> (key_s, val_s), stable, on key bits [b0, b1)
+      // DeviceRadixSort::SortPairs with the onesweep tile shape of SortHub (32-bit offsets: nnz < 2^32)
+      using Dispatch = cub::DispatchRadixSort<false, unsigned long long, T, unsigned int, SortHub<T>>;
+      cub::DoubleBuffer<unsigned long long> dk(key_in.as<unsigned long long>(), key_s.as<unsigned long long>());
+      cub::DoubleBuffer<T> dv(const_cast<T*>(av), val_s.as<T>());  // not overwritten: is_overwrite_okay = false
       size_t tb = 0;
-      SPMV_CUDA_TRY(cub::DeviceRadixSort::SortPairs(nullptr, tb, key_in.as<unsigned long long>(),
-                                                    key_s.as<unsigned long long>(), av, val_s.as<T>(), nnz, b0, b1, st));
+      SPMV_CUDA_TRY(Dispatch::Dispatch(nullptr, tb, dk, dv, static_cast<unsigned int>(nnz), b0, b1, false, st));
       int rr = tmp_for(tb);
       if (rr) return rr;
-      SPMV_CUDA_TRY(cub::DeviceRadixSort::SortPairs(tmp.ptr, tb, key_in.as<unsigned long long>(),
-                                                    key_s.as<unsigned long long>(), av, val_s.as<T>(), nnz, b0, b1, st));
+      SPMV_CUDA_TRY(Dispatch::Dispatch(tmp.ptr, tb, dk, dv, static_cast<unsigned int>(nnz), b0, b1, false, st));
       return SPMV_OK;
     };
     bool grouped = false;
