@@ -450,6 +450,42 @@ __device__ __forceinline__ int warp_col_rank(uint32_t c, bool in, uint32_t m, in
   return lo;  // sorted columns below c
 }
 
+// Two rows at once (two independent shuffle / compare chains in flight per
+// warp: the kernels using this are bound by shuffle and load latency, not by
+// issue slots).  dup: one of the two rows repeats a column.
+__device__ __forceinline__ void warp_col_rank2(const uint32_t (&c)[2], const bool (&in)[2], const uint32_t (&m)[2],
+                                               int lane, int (&rank)[2], bool& dup) {
+  uint32_t k[2];
+#pragma unroll
+  for (int u = 0; u < 2; ++u) k[u] = in[u] ? c[u] : 0xffffffffu;
+#pragma unroll
+  for (int kk = 2; kk <= 32; kk <<= 1)
+#pragma unroll
+    for (int j = kk >> 1; j >= 1; j >>= 1) {
+      const bool take_min = ((lane & j) == 0) == ((lane & kk) == 0);
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const uint32_t o = __shfl_xor_sync(0xffffffffu, k[u], j);
+        k[u] = take_min ? min(k[u], o) : max(k[u], o);
+      }
+    }
+  bool d = false;
+#pragma unroll
+  for (int u = 0; u < 2; ++u) {
+    const uint32_t prev = __shfl_up_sync(0xffffffffu, k[u], 1);
+    d |= lane > 0 && uint32_t(lane) < m[u] && prev == k[u];
+  }
+  dup = __any_sync(0xffffffffu, d);
+  rank[0] = rank[1] = 0;
+#pragma unroll
+  for (int step = 16; step >= 1; step >>= 1)
+#pragma unroll
+    for (int u = 0; u < 2; ++u) {
+      const uint32_t probe = __shfl_sync(0xffffffffu, k[u], rank[u] + step - 1);
+      if (probe < c[u]) rank[u] += step;
+    }
+}
+
 // Rows of <= 32 entries: lane k holds entry k of the row, its payload
 // (col << 32 | storage index); a bitonic sort of the payloads, then the
 // value gathered through the storage index.  `pay` null: the rows were
@@ -676,97 +712,141 @@ __global__ void __launch_bounds__(kGroupThreads, 2)
     __syncthreads();
     for (uint32_t i = tid; i < n; i += kGroupThreads) sord[atomicAdd(&cur[srow[i]], 1u)] = uint16_t(i);
     __syncthreads();
-    for (int r = warp; r < grows; r += kGroupThreads / 32) {
-      const uint32_t s0 = cnt[r], m = cnt[r + 1] - s0;
-      const int64_t sidx = g * grows + r;
-      const uint32_t row = uint32_t(sidx);
-      if (lane == 0) seg[sidx] = a + s0;
-      if (m == 0) continue;
-      uint32_t heads_n = 0;
-      if (m <= 32) {
-        const bool in = uint32_t(lane) < m;
-        unsigned long long key = ~0ull;
-        uint32_t i = 0, c = 0;
-        if (in) {
-          i = sord[s0 + lane];
-          c = scol[i];
-          key = (static_cast<unsigned long long>(c) << 13) | i;
-        }
-        bool has_dup;
-        const int rank = warp_col_rank(c, in, m, lane, has_dup);
-        if (!has_dup) {  // distinct columns: every lane stores its own entry at its rank
-          if (in) {
-            ai_out[a + s0 + lane] = row;
-            aj_out[a + s0 + rank] = c;
-            av_out[a + s0 + rank] = sval[i];
-          }
-          if (lane == 0) ucnt[sidx] = m;
-          continue;
-        }
+    constexpr int NWG = kGroupThreads / 32;
+    for (int rp = warp; rp < grows; rp += 2 * NWG) {
+      // two rows per step (rp and rp + NWG) when both hold 1..32 entries with
+      // distinct columns: two rank networks in flight per warp
+      if (rp + NWG < grows) {
+        uint32_t s2[2], m2[2], i2[2] = {0u, 0u}, c2[2] = {0u, 0u};
+        bool in2[2];
 #pragma unroll
-        for (int k = 2; k <= 32; k <<= 1)
-#pragma unroll
-          for (int j = k >> 1; j >= 1; j >>= 1) {
-            const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, j);
-            const bool take_min = ((lane & j) == 0) == ((lane & k) == 0);
-            key = (take_min ? ok < key : ok > key) ? ok : key;
-          }
-        const unsigned long long prev = __shfl_up_sync(0xffffffffu, key, 1);
-        const bool head = in && (lane == 0 || (prev >> 13) != (key >> 13));
-        heads_n = __popc(__ballot_sync(0xffffffffu, head));
-        if (in) {
-          ai_out[a + s0 + lane] = row;
-          aj_out[a + s0 + lane] = uint32_t(key >> 13);
-          av_out[a + s0 + lane] = sval[uint32_t(key) & 8191u];
+        for (int u = 0; u < 2; ++u) {
+          s2[u] = cnt[rp + u * NWG];
+          m2[u] = cnt[rp + u * NWG + 1] - s2[u];
         }
-      } else {
-        // a longer row: its local indices sorted in place by (column, index),
-        // a bitonic network with every merge ascending (entries past m act as
-        // +infinity and never move)
-        uint32_t N = 64;
-        while (N < m) N <<= 1;
-        for (uint32_t k = 2; k <= N; k <<= 1) {
-          for (uint32_t j = k >> 1; j >= 1; j >>= 1) {
-            for (uint32_t t = lane; t < N / 2; t += 32) {
-              uint32_t i, l;
-              if (j == (k >> 1)) {  // mirror step
-                const uint32_t blk = t / j, off = t % j;
-                i = blk * k + off;
-                l = blk * k + k - 1 - off;
-              } else {
-                const uint32_t blk = t / j, off = t % j;
-                i = blk * 2 * j + off;
-                l = i + j;
+        if (m2[0] - 1u < 32u && m2[1] - 1u < 32u) {
+#pragma unroll
+          for (int u = 0; u < 2; ++u) {
+            in2[u] = uint32_t(lane) < m2[u];
+            if (in2[u]) {
+              i2[u] = sord[s2[u] + lane];
+              c2[u] = scol[i2[u]];
+            }
+          }
+          int rank2[2];
+          bool dup2;
+          warp_col_rank2(c2, in2, m2, lane, rank2, dup2);
+          if (!dup2) {
+#pragma unroll
+            for (int u = 0; u < 2; ++u) {
+              const int64_t sidx = g * grows + rp + u * NWG;
+              if (in2[u]) {
+                ai_out[a + s2[u] + lane] = uint32_t(sidx);
+                aj_out[a + s2[u] + rank2[u]] = c2[u];
+                av_out[a + s2[u] + rank2[u]] = sval[i2[u]];
               }
-              if (l < m) {
-                const uint32_t x = sord[s0 + i], y = sord[s0 + l];
-                if (group_less(scol, y, x)) {
-                  sord[s0 + i] = uint16_t(y);
-                  sord[s0 + l] = uint16_t(x);
-                }
+              if (lane == 0) {
+                seg[sidx] = a + s2[u];
+                ucnt[sidx] = m2[u];
               }
             }
-            __syncwarp();
+            continue;
           }
-        }
-        for (uint32_t t0 = 0; t0 < m; t0 += 32) {
-          const uint32_t t = t0 + lane;
-          const bool in = t < m;
-          uint32_t i = 0;
-          bool head = false;
-          if (in) {
-            i = sord[s0 + t];
-            head = t == 0 || scol[sord[s0 + t - 1]] != scol[i];
-            ai_out[a + s0 + t] = row;
-            aj_out[a + s0 + t] = scol[i];
-            av_out[a + s0 + t] = sval[i];
-          }
-          heads_n += __popc(__ballot_sync(0xffffffffu, head));
         }
       }
-      if (lane == 0) {
-        ucnt[sidx] = heads_n;
-        dups += m - heads_n;
+      // one row at a time: a pair with an empty, long or repeated-column row, and the last odd row
+      for (int r = rp; r < grows && r <= rp + NWG; r += NWG) {
+        const uint32_t s0 = cnt[r], m = cnt[r + 1] - s0;
+        const int64_t sidx = g * grows + r;
+        const uint32_t row = uint32_t(sidx);
+        if (lane == 0) seg[sidx] = a + s0;
+        if (m == 0) continue;
+        uint32_t heads_n = 0;
+        if (m <= 32) {
+          const bool in = uint32_t(lane) < m;
+          unsigned long long key = ~0ull;
+          uint32_t i = 0, c = 0;
+          if (in) {
+            i = sord[s0 + lane];
+            c = scol[i];
+            key = (static_cast<unsigned long long>(c) << 13) | i;
+          }
+          bool has_dup;
+          const int rank = warp_col_rank(c, in, m, lane, has_dup);
+          if (!has_dup) {  // distinct columns: every lane stores its own entry at its rank
+            if (in) {
+              ai_out[a + s0 + lane] = row;
+              aj_out[a + s0 + rank] = c;
+              av_out[a + s0 + rank] = sval[i];
+            }
+            if (lane == 0) ucnt[sidx] = m;
+            continue;
+          }
+#pragma unroll
+          for (int k = 2; k <= 32; k <<= 1)
+#pragma unroll
+            for (int j = k >> 1; j >= 1; j >>= 1) {
+              const unsigned long long ok = __shfl_xor_sync(0xffffffffu, key, j);
+              const bool take_min = ((lane & j) == 0) == ((lane & k) == 0);
+              key = (take_min ? ok < key : ok > key) ? ok : key;
+            }
+          const unsigned long long prev = __shfl_up_sync(0xffffffffu, key, 1);
+          const bool head = in && (lane == 0 || (prev >> 13) != (key >> 13));
+          heads_n = __popc(__ballot_sync(0xffffffffu, head));
+          if (in) {
+            ai_out[a + s0 + lane] = row;
+            aj_out[a + s0 + lane] = uint32_t(key >> 13);
+            av_out[a + s0 + lane] = sval[uint32_t(key) & 8191u];
+          }
+        } else {
+          // a longer row: its local indices sorted in place by (column, index),
+          // a bitonic network with every merge ascending (entries past m act as
+          // +infinity and never move)
+          uint32_t N = 64;
+          while (N < m) N <<= 1;
+          for (uint32_t k = 2; k <= N; k <<= 1) {
+            for (uint32_t j = k >> 1; j >= 1; j >>= 1) {
+              for (uint32_t t = lane; t < N / 2; t += 32) {
+                uint32_t i, l;
+                if (j == (k >> 1)) {  // mirror step
+                  const uint32_t blk = t / j, off = t % j;
+                  i = blk * k + off;
+                  l = blk * k + k - 1 - off;
+                } else {
+                  const uint32_t blk = t / j, off = t % j;
+                  i = blk * 2 * j + off;
+                  l = i + j;
+                }
+                if (l < m) {
+                  const uint32_t x = sord[s0 + i], y = sord[s0 + l];
+                  if (group_less(scol, y, x)) {
+                    sord[s0 + i] = uint16_t(y);
+                    sord[s0 + l] = uint16_t(x);
+                  }
+                }
+              }
+              __syncwarp();
+            }
+          }
+          for (uint32_t t0 = 0; t0 < m; t0 += 32) {
+            const uint32_t t = t0 + lane;
+            const bool in = t < m;
+            uint32_t i = 0;
+            bool head = false;
+            if (in) {
+              i = sord[s0 + t];
+              head = t == 0 || scol[sord[s0 + t - 1]] != scol[i];
+              ai_out[a + s0 + t] = row;
+              aj_out[a + s0 + t] = scol[i];
+              av_out[a + s0 + t] = sval[i];
+            }
+            heads_n += __popc(__ballot_sync(0xffffffffu, head));
+          }
+        }
+        if (lane == 0) {
+          ucnt[sidx] = heads_n;
+          dups += m - heads_n;
+        }
       }
     }
     __syncthreads();
