@@ -491,8 +491,11 @@ __device__ __forceinline__ void warp_col_rank2(const uint32_t (&c)[2], const boo
 // value gathered through the storage index.  `pay` null: the rows were
 // already in order, entry k's payload is built from aj[k] and k itself
 // (no gathers at all).  Duplicate columns counted.
+// (32 registers, 8 CTAs of 256 threads per SM: the kernel waits on its row's
+// dependent loads, so rows in flight decide its speed: 256^3 rows-ordered
+// sort 7.1 -> 6.3 ms against 6 CTAs per SM)
 template <typename T>
-__global__ void sort_rows_kernel(const uint32_t* __restrict__ rows_s, const unsigned long long* __restrict__ pay,
+__global__ void __launch_bounds__(256, 8) sort_rows_kernel(const uint32_t* __restrict__ rows_s, const unsigned long long* __restrict__ pay,
                                  const uint32_t* __restrict__ seg, int64_t nseg, const uint32_t* __restrict__ aj,
                                  const T* __restrict__ av, uint32_t* __restrict__ ai_out,
                                  uint32_t* __restrict__ aj_out, T* __restrict__ av_out, uint32_t* __restrict__ ucnt,
