@@ -60,3 +60,24 @@ def test_parse_errors():
     for text, exc in bad.items():
         with pytest.raises(exc):
             read_matrix_market(text)
+
+
+def test_bulk_parse_equals_line_walk():
+    """The numpy text-reader pass and the reference-style line walk give the
+    same (row, column, value) arrays, bit for bit, on well-formed entry lines
+    (tabs, exponents, signed zeros, subnormals, inf / nan), and the bulk pass
+    declines (None) what only the line walk may judge."""
+    from paper_2304_09511_b200 import matrixio as M
+    rng = np.random.default_rng(5)
+    n = 20000
+    i, j = rng.integers(1, 5001, n), rng.integers(1, 5001, n)
+    v = rng.standard_normal(n) * 10.0 ** rng.integers(-300, 300, n)
+    data = ["%d %d %.17g" % t for t in zip(i.tolist(), j.tolist(), v.tolist())]
+    data += ["1\t2   3e-2", "3 4 -1E5", "5 6 nan", "7 8 -inf", "9 10 +.5", "11 12 1e-320", "13 14 -0.0", "+15 16 1."]
+    bulk, walk = M._mm_entries_bulk(data, 3), M._mm_entries_by_line(data, 3, 5000, 5000)
+    assert bulk is not None and all(a.tobytes() == b.tobytes() for a, b in zip(bulk, walk))
+    pat = ["%d %d" % t for t in zip(i.tolist(), j.tolist())]
+    bulk, walk = M._mm_entries_bulk(pat, 2), M._mm_entries_by_line(pat, 2, 5000, 5000)
+    assert all(a.tobytes() == b.tobytes() for a, b in zip(bulk, walk))
+    for odd in (["1 2 3", "1.0 2 3"], ["1 2 3 4", "1 2"], ["1 2 x"], ["1_0 2 3"], ["99999999999999999999 1 3"]):
+        assert M._mm_entries_bulk(odd, 3) is None
