@@ -347,19 +347,23 @@ __global__ void __launch_bounds__(kDiaTileThreads, 3)
   const int64_t tile = blockIdx.x;
   const int64_t row0 = tile * (int64_t(NW) * U * gpw) + int64_t(warp) * U * gpw;
   const int64_t off = gl < nd ? int64_t(__ldg(offs + gl)) : 0;
+  // this lane's rows are i_u = i0 + u * gpw; the first nu of them exist; the
+  // rows whose cell on the lane's diagonal lies inside the matrix are
+  // [lo_i, lo_i + span) (one unsigned compare per cell; lanes past ndiags: none)
+  const int64_t i0 = row0 + sub;
+  const int nu = gl < nd ? int(min(int64_t(U), max(int64_t(0), (nrows - i0 + gpw - 1) / gpw))) : 0;
+  const int64_t lo_i = max(int64_t(0), -off), hi_i = min(nrows, ncols - off);
+  const uint64_t span = gl < nd && hi_i > lo_i ? uint64_t(hi_i - lo_i) : 0;
+  const T* __restrict__ p = vals + i0 * nd + gl;
+  const int64_t pstride = int64_t(gpw) * nd;
   T v[U];
 #pragma unroll
-  for (int u = 0; u < U; ++u) {
-    const int64_t i = row0 + int64_t(u) * gpw + sub;
-    v[u] = (i < nrows && gl < nd) ? (EMIT ? __ldcs(vals + i * nd + gl) : __ldg(vals + i * nd + gl)) : T(0);
-  }
+  for (int u = 0; u < U; ++u) v[u] = u < nu ? (EMIT ? __ldcs(p + u * pstride) : __ldg(p + u * pstride)) : T(0);
   unsigned keepbits = 0;  // bit u: this lane's cell of row u is kept
   unsigned cnt = 0;       // the warp's kept cells
 #pragma unroll
   for (int u = 0; u < U; ++u) {
-    const int64_t i = row0 + int64_t(u) * gpw + sub;
-    const int64_t col = i + off;
-    const bool keep = i < nrows && gl < nd && col >= 0 && col < ncols && v[u] != T(0);
+    const bool keep = uint64_t(i0 + u * gpw - lo_i) < span && v[u] != T(0);
     keepbits |= keep ? 1u << u : 0u;
     cnt += __popc(__ballot_sync(0xffffffffu, keep));
   }
