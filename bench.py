@@ -564,6 +564,19 @@ def per_config_measure(args, torch, sp, device, pk, name: str) -> dict:
             r["l2_resident"] = {"gflops": round(2.0 * m.nnz / tw / 1e9, 2), "ms_per_spmv": round(tw * 1e3, 4),
                                 "gbs": round(b / tw / 1e9, 1),
                                 "note": "back-to-back, no flush: matrix and x served from L2; not an HBM roofline number"}
+            # the same 100 products as one CUDA graph: eager launches of a ~13 us
+            # product are bound by the host's launch rate, a graph replay is not
+            graph = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(graph):
+                for _ in range(100):
+                    fn()
+            graph.replay()
+            torch.cuda.synchronize()
+            tg = time_steps(torch, graph.replay, 10, 3) / 100
+            r["l2_resident"].update({"graph_gflops": round(2.0 * m.nnz / tg / 1e9, 2),
+                                     "graph_ms_per_spmv": round(tg * 1e3, 4),
+                                     "graph_note": "100 products captured in one CUDA graph, replayed 10 times"})
+            del graph
         if name == "c3":
             r["gather_roofline"] = {
                 "achieved_ggathers_s": round(m.nnz / t / 1e9, 1), "ceiling_ggathers_s": GATHER_CEILING_GS,

@@ -128,8 +128,20 @@ struct StreamSlots {
         *out = s.ptr;
         return SPMV_OK;
       }
+    // A stream's first product may be inside a CUDA graph capture (global
+    // capture mode forbids cudaMalloc): allocate under relaxed mode; the
+    // zero fill below is then captured as the graph's first node on this
+    // stream and re-zeroes the slot at every replay.
+    cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cap) != cudaSuccess) {
+      cudaGetLastError();
+      cap = cudaStreamCaptureStatusNone;
+    }
+    cudaStreamCaptureMode mode = cudaStreamCaptureModeRelaxed;
+    if (cap == cudaStreamCaptureStatusActive) cudaThreadExchangeStreamCaptureMode(&mode);
     void* p = nullptr;
     cudaError_t e = cudaMalloc(&p, bytes);
+    if (cap == cudaStreamCaptureStatusActive) cudaThreadExchangeStreamCaptureMode(&mode);
     if (e != cudaSuccess) return fail(SPMV_CUDA_ERROR, "cudaMalloc(%zu) failed: %s", bytes, cudaGetErrorString(e));
     e = cudaMemsetAsync(p, 0, bytes, st);
     if (e != cudaSuccess) {

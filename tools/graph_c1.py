@@ -34,7 +34,7 @@ for fmt, m in mats.items():
             fn()
     torch.cuda.current_stream().wait_stream(s)
     g = torch.cuda.CUDAGraph()
-    with torch.cuda.graph(g):
+    with torch.cuda.graph(g):  # (torch's own capture stream: the plan's first product on it)
         for _ in range(100):
             fn()
     g.replay()
