@@ -43,7 +43,14 @@ class KernelVersion(str, Enum):
     VLA = "vla"
 
 
+_raw_stream = getattr(torch._C, "_cuda_getCurrentRawStream", None)
+
+
 def _stream(device: torch.device) -> int:
+    """The device's current stream handle (torch's raw query: every product
+    call needs it, and torch.cuda.current_stream builds a Stream object)."""
+    if _raw_stream is not None and device.index is not None:
+        return _raw_stream(device.index)
     return torch.cuda.current_stream(device).cuda_stream
 
 
@@ -254,15 +261,15 @@ def spmv_coo_plain(A, x, out=None, plan_config: PlanConfig | None = None):
     `plan_config` overrides the container's kernel configuration."""
     A = as_device(A)
     p = coo_plan(A, plan_config) if A.nrows else None
-    y = _host_product(A, x, out, lambda xp, yp, st: _lib.call(
-        "spmv_coo_host", p.handle, _ptr(A.row_indices), _ptr(A.col_indices), _ptr(A.values), xp, yp, HOST_CHUNKS,
-        st))
-    if y is not None:
-        return y
+    if not (isinstance(x, torch.Tensor) and x.is_cuda):
+        y = _host_product(A, x, out, lambda xp, yp, st: _lib.call(
+            "spmv_coo_host", p.handle, _ptr(A.row_indices), _ptr(A.col_indices), _ptr(A.values), xp, yp,
+            HOST_CHUNKS, st))
+        if y is not None:
+            return y
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
-    if A.nrows:
-        p = coo_plan(A, plan_config)
+    if p is not None:
         _lib.call("spmv_coo", p.handle, _ptr(A.row_indices), _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0,
                   A.ncols, _ptr(y), _stream(A.device))
     return _finish(y, origin, out)
@@ -272,9 +279,9 @@ def spmv_csr_plain(A, x, out=None, plan_config: PlanConfig | None = None):
     """``y = A @ x`` with one left-to-right sum per row (kernels.py:69-82).
     `plan_config` overrides the container's kernel configuration."""
     A = as_device(A)
-    if A.nnz:
+    p = csr_plan(A, config=plan_config) if A.nrows else None
+    if A.nnz and not (isinstance(x, torch.Tensor) and x.is_cuda):
         # host x -> host y: the C ABI pipelines upload / tiles / download
-        p = csr_plan(A, config=plan_config)
         y = _host_product(A, x, out, lambda xp, yp, st: _lib.call(
             "spmv_csr_host", p.handle, _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values), xp, yp,
             HOST_CHUNKS, st))
@@ -282,8 +289,7 @@ def spmv_csr_plain(A, x, out=None, plan_config: PlanConfig | None = None):
             return y
     xv, origin = _checked_x(A, x)
     y = _new_y(A, out)
-    if A.nrows:
-        p = csr_plan(A, config=plan_config)
+    if p is not None:
         _lib.call("spmv_csr", p.handle, _ptr(A.row_pointers), _ptr(A.col_indices), _ptr(A.values), _ptr(xv), 0,
                   A.ncols, _ptr(y), _stream(A.device))
     return _finish(y, origin, out)
@@ -294,7 +300,7 @@ def spmv_dia_plain(A, x, out=None, plan_config: PlanConfig | None = None):
     `plan_config` (its dia_* fields) overrides the container's."""
     A = as_device(A)
     cfg = plan_config if plan_config is not None else plan_config_of(A)
-    if A.ndiags > 0:
+    if A.ndiags > 0 and not (isinstance(x, torch.Tensor) and x.is_cuda):
         offs = A.plan("dia_offsets", lambda: A.offsets.cpu().numpy().astype(np.int64))
         pipe = _host_pipe(A)
         c = cfg.to_c()

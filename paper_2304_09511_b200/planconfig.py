@@ -69,10 +69,14 @@ class PlanConfig:
     panels: int = -1
 
     def to_c(self) -> _CPlanConfig:
-        c = _CPlanConfig()
-        c.version = VERSION
-        for f in fields(self):
-            setattr(c, f.name, int(getattr(self, f.name)))
+        """The C struct (built once per instance; the callee only reads it)."""
+        c = self.__dict__.get("_c")
+        if c is None:
+            c = _CPlanConfig()
+            c.version = VERSION
+            for f in fields(self):
+                setattr(c, f.name, int(getattr(self, f.name)))
+            object.__setattr__(self, "_c", c)
         return c
 
     @classmethod
@@ -80,7 +84,13 @@ class PlanConfig:
         return cls(**{f.name: int(getattr(c, f.name)) for f in fields(cls)})
 
     def key(self) -> tuple:
-        return tuple(getattr(self, f.name) for f in fields(self))
+        """Plan-cache key (every product looks its plan up by it: computed
+        once per instance, the dataclass is frozen)."""
+        k = self.__dict__.get("_key")
+        if k is None:
+            k = tuple(getattr(self, f.name) for f in fields(self))
+            object.__setattr__(self, "_key", k)
+        return k
 
     def with_(self, **kw) -> "PlanConfig":
         return replace(self, **kw)
